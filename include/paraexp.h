@@ -1,0 +1,192 @@
+/*
+ * paraexp.h — C ABI of the B200 Paraexp direct-adjoint gradient path.
+ *
+ * The reference (pkg/src/paradjoint, pure Python) has no native boundary: its
+ * hot path is called as Python functions taking CSR operators and callables.
+ * This ABI is what a ctypes binding of the reference would call when its
+ * existing backend selector (`backend=`, config.py:44,154-156 -> workers.py:335-340)
+ * is given "cuda". Each entry point below names the reference interface it
+ * replaces. Plain pointers and sizes only; no torch types.
+ *
+ * Conventions
+ *  - One handle per GPU process, bound to the device current at px_create.
+ *    Not thread-safe: one host thread drives a handle.
+ *  - All work is enqueued on the caller's stream (`stream` is a cudaStream_t;
+ *    NULL = legacy default stream). Functions that return host scalars
+ *    synchronise that stream.
+ *  - Fields are fp64, x fastest (flat index i + nx*j), batch-major: a (B, n)
+ *    array holds batch member b at offset b*n (problems.py:48-56).
+ *  - Return value 0 = success; otherwise a PX_ERR_* code, with a message from
+ *    px_last_error(). The Python layer maps codes onto the reference's
+ *    exceptions (errors.py:4-57): PX_ERR_NONFINITE -> IntegrationFailure,
+ *    PX_ERR_PLAN -> PropagationFailure, PX_ERR_ARG -> ValueError.
+ */
+#ifndef PARAEXP_H_
+#define PARAEXP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PX_ABI_VERSION 1
+
+enum {
+  PX_OK = 0,
+  PX_ERR_ARG = 1,
+  PX_ERR_CUDA = 2,
+  PX_ERR_NONFINITE = 3,
+  PX_ERR_PLAN = 4,
+  PX_ERR_STATE = 5,
+  PX_ERR_NOMEM = 6
+};
+
+enum { PX_KIND_ADVDIFF = 0, PX_KIND_BURGERS = 1 };
+enum { PX_EXP_CHEBYSHEV = 0, PX_EXP_KRYLOV = 1 };
+enum { PX_MEM_HOST = 0, PX_MEM_DEVICE = 1 };
+
+/* plan slots */
+enum {
+  PX_PLAN_SLICE = 0,        /* slice width Δ, operator A and Aᵀ (same spectrum) */
+  PX_PLAN_LONG_DIRECT = 1,  /* span (P - p_end)·Δ, block carry -> T (blockscan) */
+  PX_PLAN_LONG_ADJOINT = 2, /* span p_begin·Δ, block carry -> 0 (blockscan) */
+  PX_PLAN_FROZEN = 3,       /* Burgers: slice width, frozen J(ū_p)ᵀ */
+  PX_PLAN_COUNT = 4
+};
+
+/* fields for px_get / px_buffer */
+enum {
+  PX_FIELD_J = 0,           /* (B)            objective ½‖u(T) − u_target‖² */
+  PX_FIELD_GRAD = 1,        /* (B, K)         ∂J/∂c_k (rank-partial before px_finish_adjoint) */
+  PX_FIELD_UT = 2,          /* (B, n)         u(T) (rank-partial carry before px_finish_direct) */
+  PX_FIELD_QDAG0 = 3,       /* (B, n)         q†(0) (rank-partial before px_finish_adjoint) */
+  PX_FIELD_G = 4,           /* (B, n)         ∫ q† dt (rank-partial before px_finish_adjoint) */
+  PX_FIELD_UBND = 5,        /* (B, P+1, n)    direct boundary states u(T_p) (flag, world = 1) */
+  PX_FIELD_FROZEN_BOUNDS = 6, /* (3)          Burgers: re_lo, re_hi, im of the frozen-operator FOV union */
+  PX_FIELD_VEND = 7,        /* (B, P_local, n) per-slice inhomogeneous end states v_p(T_{p+1}) */
+  PX_FIELD_WEND = 8,        /* (B, P_local, n) per-slice adjoint inhomogeneous end states */
+  PX_FIELD_TRAJ = 9,        /* (S+1, B, n)    Burgers direct trajectory (S = P·nsteps) */
+  PX_FIELD_COUNT = 10
+};
+
+enum { PX_FLAG_BOUNDARY_STATES = 1 };
+
+typedef struct px_problem_desc {
+  int kind;             /* PX_KIND_* */
+  int nx, ny;           /* ny == 1: 1D */
+  double stencil[5];    /* direct operator (cc, ce, cw, cn, cs); Burgers: D∇² part */
+  double D;             /* diffusion (Burgers nonlinear terms use hx and D) */
+  double hx;            /* grid spacing in x */
+  double T;             /* horizon */
+  int P;                /* global slice count (TimePartition.N) */
+  int nsteps;           /* RK4 steps per slice, slice rule ⌈Δ/dt⌉ */
+  int p_begin, p_end;   /* this rank's contiguous slice block */
+  int batch;            /* B independent controls */
+  int K;                /* control modes */
+  int basis_rows_x;     /* rows of the x factor table */
+  int basis_rows_y;     /* rows of the y factor table (1 in 1D) */
+  int expaction;        /* PX_EXP_* */
+  int krylov_m;         /* Arnoldi vectors (PX_EXP_KRYLOV) */
+  int flags;            /* PX_FLAG_* */
+} px_problem_desc;
+
+typedef struct px_cheb_plan {
+  double span;          /* total span τ = substeps·τ_s */
+  int substeps;
+  int degree;           /* K: coefficients 0..K */
+  double center;        /* c0 */
+  double scale;         /* d: X = (M − c0)/d */
+  int sigma;            /* +1 imaginary foci, −1 real foci: U_{k+1} = 2X·U_k + σ·U_{k−1} */
+  const double* coef_exp;  /* degree+1 host values: e^{τ_s z} */
+  const double* coef_phi;  /* degree+1 host values: τ_s·φ₁(τ_s z) (may be NULL) */
+} px_cheb_plan;
+
+typedef struct px_stats {
+  uint64_t rk4_lane_steps;   /* RK4 steps × lanes executed (one lane = one n-field) */
+  uint64_t exp_terms;        /* operator applications inside exp-actions × vectors */
+  uint64_t arnoldi_steps;    /* Arnoldi steps × vectors */
+  uint64_t kernel_launches;  /* launches of this library's kernels */
+  double algorithmic_bytes;  /* Σ units × bytes/unit */
+  double rk4_bytes;          /* part of the above in RK4 sweeps */
+  double exp_bytes;          /* part of the above in exp-actions */
+} px_stats;
+
+/* Library identity (C-ABI version; compiled sm arch string). */
+int px_abi_version(void);
+const char* px_build_info(void);
+
+/* Problem setup: replaces build_system/System (systems.py:27-117) and the
+ * partition (paraexp.py:72-78); allocates device scratch on the current device. */
+int px_create(const px_problem_desc* desc, void** out_handle);
+void px_destroy(void* handle);
+const char* px_last_error(const void* handle);
+
+/* Control basis factor tables (host): tx[rows_x][nx], ty[rows_y][ny], ix[K], iy[K]. */
+int px_set_basis(void* handle, const double* tx, const double* ty, const int* ix, const int* iy);
+
+/* Exp-action plans: replace relpm_propagate's adaptive Leja setup
+ * (timestepping.py:360-423) by the host planner's a-priori plan. */
+int px_set_cheb_plan(void* handle, int slot, const px_cheb_plan* plan);
+int px_set_krylov_plan(void* handle, int slot, double span, int substeps);
+
+/* Inputs: u0 (n), u_target (n), ctrl (B×K); host or device memory. Replaces the
+ * q0 / q_true / f arguments of direct_adjoint_loop (optimization.py:154-169). */
+int px_set_inputs(void* handle, const double* u0, const double* u_target, const double* ctrl,
+                  int mem, void* stream);
+
+/* Direct sweep (solve_direct_linear, paraexp.py:221-248; Burgers: the hybrid's
+ * serial sweep, hybrid.py:185-191): rank-partial u(T) carry in PX_FIELD_UT. */
+int px_direct(void* handle, void* stream);
+/* After the caller's allreduce of PX_FIELD_UT (world > 1): u(T) = u0 + Σ partials,
+ * q†_T = u(T) − u_target, J (cost, optimization.py:84-93 with the terminal objective). */
+int px_finish_direct(void* handle, void* stream);
+/* Standalone adjoint terminal data q†_T (B×n): replaces the qdag_T argument of
+ * solve_adjoint_linear / solve_adjoint_varying (paraexp.py:298-353) when the
+ * adjoint is run without px_finish_direct. Burgers needs px_direct first. */
+int px_set_adjoint_terminal(void* handle, const double* qdag_T, int mem, void* stream);
+/* Adjoint sweep (solve_adjoint_linear / solve_adjoint_varying, paraexp.py:298-353):
+ * rank-partials of q†(0), ∫q† dt and the projected gradient. */
+int px_adjoint(void* handle, void* stream);
+/* After the caller's allreduce of QDAG0/G/GRAD partials: adds the q†_T terms
+ * (gradient_wrt_forcing / initial_condition_gradient, optimization.py:103-117). */
+int px_finish_adjoint(void* handle, void* stream);
+/* world = 1 convenience: direct + finish + adjoint + finish (one gradient evaluation,
+ * direct_adjoint_loop, optimization.py:154-231). Linear testbed only (Burgers needs the
+ * host planner between the sweeps). */
+int px_gradient(void* handle, void* stream);
+
+/* Device pointer and element count of a field (for NCCL allreduce by the caller). */
+int px_buffer(void* handle, int field, double** dev_ptr, size_t* count);
+/* Copy a field out (host or device destination). */
+int px_get(void* handle, int field, double* dst, size_t count, int mem, void* stream);
+
+/* Phase timing with CUDA events recorded on the work stream around each sweep
+ * phase (enable before the timed region; px_get_timing synchronises the events).
+ * Phases: PX_PHASE_*; ms[i] = summed device time, launches[i] = kernel launches
+ * inside those phase windows. */
+enum {
+  PX_PHASE_RK4_DIRECT = 0,
+  PX_PHASE_RK4_ADJOINT = 1,
+  PX_PHASE_EXP_DIRECT = 2,
+  PX_PHASE_EXP_ADJOINT = 3,
+  PX_PHASE_OTHER = 4,
+  PX_PHASE_COUNT = 5
+};
+typedef struct px_timing {
+  double ms[PX_PHASE_COUNT];
+  uint64_t launches[PX_PHASE_COUNT];
+  double bytes[PX_PHASE_COUNT];   /* algorithmic bytes executed inside each phase */
+} px_timing;
+int px_set_timing(void* handle, int enable);
+int px_get_timing(void* handle, px_timing* out);
+
+int px_get_stats(void* handle, px_stats* out);
+int px_reset_stats(void* handle);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PARAEXP_H_ */

@@ -1,0 +1,412 @@
+"""CPU oracle, config mode — TEST INFRASTRUCTURE ONLY.
+
+This module is the checker for the CUDA path. Only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline / ``--impl reference``
+legs may import it; the product package never does (and has no CPU fallback).
+
+It is a plain numpy restatement of the reference's Paraexp structure with the
+BASELINE configs' numerics (fixed-step classical RK4, Chebyshev/Krylov exponential
+actions, terminal objective, time-constant Fourier control). Structure followed:
+
+* absorbed initial condition, per-slice zero-data inhomogeneous solves, homogeneous
+  propagation, superposition — `pkg/src/paradjoint/paraexp.py:187-248`;
+* absorbed final condition, reflected time σ = T_p + T_{p+1} − t, chains P → 0 —
+  `paraexp.py:256-326`; time-varying operator + per-slice frozen operator —
+  `paraexp.py:329-353`, `systems.py:64-97`;
+* Burgers: serial direct sweep keeping the trajectory (`hybrid.py:185-191`),
+  matrix-free Jᵀ(u)y (`problems.py:316-343`, V ≡ 0), linear interpolation of the
+  stored trajectory (`timestepping.py:64-75`), trapezoid-averaged frozen
+  linearisation (`problems.py:346-366`);
+* objective/gradient conventions: unweighted inner products (`PAPER.md:149-155`),
+  ∂J/∂c_k = ⟨φ_k, ∫q† dt⟩ (control-to-state map ∂N/∂c_k = φ_k).
+
+Homogeneous formulations: ``chains`` is the reference's
+neighbour form (each slice end propagated separately, `paraexp.py:207-217`);
+``scan`` is the summed-chain carry D_{p+1} = exp(ΔA)·D_p + v_p (equal by
+linearity, P−1 actions); ``blockscan`` with G ranks is scan per contiguous block
+plus one long action per block (the multi-GPU form). The GPU executes the same
+operation sequence as ``scan``/``blockscan`` so parity is at rounding level.
+
+The exponential-action plans (degree, substeps, coefficients) are inputs — built
+by the product's host planner, validated independently here against FFT-exact
+circulant propagators (tests/test_oracle.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from paper_2004_00546_b200.expaction import ChebPlan, KrylovPlan
+from paper_2004_00546_b200.partition import rank_block
+
+# ---------------------------------------------------------------------------
+# Operators
+# ---------------------------------------------------------------------------
+
+
+def stencil_apply(st, u: np.ndarray, nx: int, ny: int) -> np.ndarray:
+    """(M u) with coefficients (cc, ce, cw, cn, cs) on a periodic grid, x fastest.
+
+    Same operator as `problems.py:149-152` (central differences, periodic wrap).
+    """
+    cc, ce, cw, cn, cs = st
+    shp = u.shape
+    U = u.reshape(shp[:-1] + (ny, nx))
+    out = cc * U + ce * np.roll(U, -1, axis=-1) + cw * np.roll(U, 1, axis=-1)
+    if ny > 1:
+        out = out + cn * np.roll(U, -1, axis=-2) + cs * np.roll(U, 1, axis=-2)
+    return out.reshape(shp)
+
+
+def dx_central(u: np.ndarray, h: float) -> np.ndarray:
+    return (np.roll(u, -1, axis=-1) - np.roll(u, 1, axis=-1)) / (2.0 * h)
+
+
+def burgers_rhs(u, f, D, h):
+    """−u∘Dx u + D·L u + f (`problems.py:177-185` with V ≡ 0, time-constant f)."""
+    lap = (np.roll(u, -1, axis=-1) - 2.0 * u + np.roll(u, 1, axis=-1)) / (h * h)
+    return -u * dx_central(u, h) + D * lap + f
+
+
+def burgers_adjoint_apply(u, y, D, h):
+    """J(u)ᵀy = Dx(u∘y) − (Dx u)∘y + D·L y (`problems.py:316-343`, V ≡ 0)."""
+    lap = (np.roll(y, -1, axis=-1) - 2.0 * y + np.roll(y, 1, axis=-1)) / (h * h)
+    return dx_central(u * y, h) - dx_central(u, h) * y + D * lap
+
+
+# ---------------------------------------------------------------------------
+# Steppers and exponential actions
+# ---------------------------------------------------------------------------
+
+
+def rk4_linear(apply, g, h: float, nsteps: int, want_z: bool = False):
+    """Zero-data classical RK4 for y' = M y + g; optionally z = ∫y (RK4-consistent).
+
+    z is RK4 applied to the augmented system (y, z)' = (M y + g, y).
+    """
+    y = np.zeros_like(g)
+    z = np.zeros_like(g) if want_z else None
+    for _ in range(nsteps):
+        k1 = apply(y) + g
+        Y2 = y + (0.5 * h) * k1
+        k2 = apply(Y2) + g
+        Y3 = y + (0.5 * h) * k2
+        k3 = apply(Y3) + g
+        Y4 = y + h * k3
+        k4 = apply(Y4) + g
+        if want_z:
+            z = z + (h / 6.0) * (y + 2.0 * Y2 + 2.0 * Y3 + Y4)
+        y = y + (h / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+    return y, z
+
+
+def cheb_action(apply, plan: ChebPlan, v: np.ndarray, phi: np.ndarray | None = None):
+    """exp(span·M)v by substeps of the planned Chebyshev series; when ``phi`` is
+    given, adds span·φ₁(span·M)v = Σ_j exp(jτ_s M)(τ_s φ₁(τ_s M) y_j) into it."""
+    c0, d, sigma = plan.center, plan.scale, float(plan.sigma)
+    be, bp = plan.coef_exp, plan.coef_phi
+    two_over = 2.0 / d
+    y = v
+    for _ in range(plan.substeps):
+        u_prev = y
+        acc = be[0] * u_prev
+        pacc = bp[0] * u_prev if phi is not None else None
+        u_cur = (apply(u_prev) - c0 * u_prev) / d
+        acc = acc + be[1] * u_cur
+        if phi is not None:
+            pacc = pacc + bp[1] * u_cur
+        for k in range(2, plan.degree + 1):
+            u_next = two_over * (apply(u_cur) - c0 * u_cur) + sigma * u_prev
+            u_prev, u_cur = u_cur, u_next
+            acc = acc + be[k] * u_cur
+            if phi is not None:
+                pacc = pacc + bp[k] * u_cur
+        if phi is not None:
+            phi += pacc
+        y = acc
+    return y
+
+
+def expm_taylor(A: np.ndarray) -> np.ndarray:
+    """exp(A) by scaling and squaring with a degree-18 Taylor polynomial."""
+    nrm = float(np.max(np.sum(np.abs(A), axis=0))) if A.size else 0.0
+    sq = 0 if nrm <= 0.5 else int(np.ceil(np.log2(nrm / 0.5)))
+    B = A / (2.0 ** sq)
+    n = A.shape[0]
+    E = np.eye(n)
+    for k in range(18, 0, -1):
+        E = np.eye(n) + (B @ E) / k
+    for _ in range(sq):
+        E = E @ E
+    return E
+
+
+KRYLOV_BREAKDOWN = 1e-13
+
+
+def krylov_action(apply, plan: KrylovPlan, v: np.ndarray, phi: np.ndarray | None = None):
+    """exp(span·M)v by substeps of m-step Arnoldi (CGS2) + small augmented expm.
+
+    Per substep: y_{j+1} = β V_m e^{τH_m} e_1 and φ += β V_m τφ₁(τH_m) e_1, both
+    read off exp([[τH_m, τe_1], [0, 0]]). Happy breakdown (h_{j+1,j} ≤
+    1e-13·β_0-scaled) truncates the basis.
+    """
+    m = plan.m
+    tau = plan.span / plan.substeps
+    y = v
+    for _ in range(plan.substeps):
+        beta = float(np.sqrt(np.dot(y, y)))
+        if beta == 0.0:
+            continue
+        V = np.zeros((m + 1, y.size))
+        H = np.zeros((m + 1, m))
+        V[0] = y / beta
+        meff = m
+        for j in range(m):
+            w = apply(V[j])
+            h1 = V[: j + 1] @ w
+            w = w - V[: j + 1].T @ h1
+            h2 = V[: j + 1] @ w
+            w = w - V[: j + 1].T @ h2
+            H[: j + 1, j] = h1 + h2
+            nrm = float(np.sqrt(np.dot(w, w)))
+            H[j + 1, j] = nrm
+            if nrm <= KRYLOV_BREAKDOWN * max(1.0, float(np.max(np.abs(H[: j + 2, j])))):
+                meff = j + 1
+                break
+            V[j + 1] = w / nrm
+        Ha = np.zeros((meff + 1, meff + 1))
+        Ha[:meff, :meff] = tau * H[:meff, :meff]
+        Ha[0, meff] = tau
+        E = expm_taylor(Ha)
+        ce = beta * E[:meff, 0]
+        cp = beta * E[:meff, meff]
+        if phi is not None:
+            phi += cp @ V[:meff]
+        y = ce @ V[:meff]
+    return y
+
+
+def exp_action(apply, plan, v, phi=None):
+    if isinstance(plan, KrylovPlan):
+        return krylov_action(apply, plan, v, phi)
+    return cheb_action(apply, plan, v, phi)
+
+
+# ---------------------------------------------------------------------------
+# Linear advection–diffusion gradient (configs 1, 2, 4, 5)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class OracleResult:
+    J: np.ndarray                 # (B,)
+    grad: np.ndarray              # (B, K)
+    uT: np.ndarray                # (B, n)
+    qdag0: np.ndarray             # (B, n)
+    G: np.ndarray                 # (B, n)  ∫ q† dt
+    u_bnd: np.ndarray | None = None   # (B, P+1, n) direct boundary states (scan only)
+    extras: dict = field(default_factory=dict)
+
+
+def _as_batch(a, n):
+    a = np.asarray(a, dtype=np.float64)
+    return a.reshape(-1, n) if a.ndim > 1 else a[None, :]
+
+
+def linear_gradient(grid_nx, grid_ny, A, basis, T, P, nsteps, u0, u_target, ctrl,
+                    plan_slice, plan_long_direct=None, plan_long_adjoint=None,
+                    formulation: str = "scan", world: int = 1, want_boundary=False):
+    """One Paraexp direct-adjoint gradient for the linear testbed (App. B of SURVEY).
+
+    ``A`` stencil tuple; ``basis`` ModeBasis; ``ctrl`` (B, K). ``plan_long_*``:
+    callables span → plan for the blockscan long spans (world > 1).
+    """
+    nx, ny = grid_nx, grid_ny
+    n = nx * ny
+    ctrl = np.atleast_2d(np.asarray(ctrl, dtype=np.float64))
+    B = ctrl.shape[0]
+    u0 = _as_batch(u0, n)
+    u0 = np.broadcast_to(u0, (B, n))
+    ut = np.broadcast_to(_as_batch(u_target, n), (B, n))
+    AT = tuple(np.asarray(A)[[0, 2, 1, 4, 3]])
+    applyA = lambda u: stencil_apply(A, u, nx, ny)
+    applyAT = lambda u: stencil_apply(AT, u, nx, ny)
+    delta = T / P
+    h = delta / nsteps
+
+    f = basis.field(ctrl)                        # (B, n)
+    g = applyA(u0) + f                           # absorbed IC source (`paraexp.py:239-242`)
+    # every slice solves the same zero-data problem (time-constant source);
+    # the checker computes it once, the GPU computes all P of them.
+    v_end, _ = rk4_linear(applyA, g, h, nsteps)
+
+    u_bnd = None
+    if formulation == "chains":
+        # reference neighbour form: slice p's end state is carried by its own chain
+        total = np.zeros_like(v_end)
+        for p in range(P):
+            c = v_end
+            for _ in range(P - 1 - p):
+                c = exp_action(applyA, plan_slice, c)
+            total = total + c
+        uT = u0 + total
+    elif formulation == "scan" and world == 1:
+        D = np.zeros_like(v_end)
+        if want_boundary:
+            u_bnd = np.empty((B, P + 1, n))
+            u_bnd[:, 0] = u0
+        for p in range(P):
+            D = v_end.copy() if p == 0 else exp_action(applyA, plan_slice, D) + v_end
+            if want_boundary:
+                u_bnd[:, p + 1] = u0 + D
+        uT = u0 + D
+    else:  # blockscan over `world` contiguous blocks, summed as an allreduce would
+        partial = np.zeros_like(v_end)
+        for r in range(world):
+            p0, p1 = rank_block(P, r, world)
+            D = np.zeros_like(v_end)
+            for p in range(p0, p1):
+                D = v_end.copy() if p == p0 else exp_action(applyA, plan_slice, D) + v_end
+            if p1 < P:
+                D = exp_action(applyA, plan_long_direct((P - p1) * delta), D)
+            partial = partial + D
+        uT = u0 + partial
+
+    qT = uT - ut
+    J = 0.5 * np.sum(qT * qT, axis=1)
+
+    # adjoint: w' = Aᵀ(w + q†_T), zero data, per slice; z = ∫w
+    gadj = applyAT(qT)
+    w_end, z = rk4_linear(applyAT, gadj, h, nsteps, want_z=True)
+    if formulation == "chains":
+        qd = np.zeros_like(w_end)
+        Gh = np.zeros_like(w_end)
+        for p in range(P):   # chain of slice p's end, run down to t = 0
+            c = w_end
+            for _ in range(p):
+                c = exp_action(applyAT, plan_slice, c, Gh)
+            qd = qd + c
+        qdag0 = qT + qd
+        G = T * qT + P * z + Gh
+    elif formulation == "scan" and world == 1:
+        C = np.zeros_like(w_end)
+        Gh = np.zeros_like(w_end)
+        for p in range(P - 1, -1, -1):
+            C = w_end.copy() if p == P - 1 else exp_action(applyAT, plan_slice, C, Gh) + w_end
+        qdag0 = qT + C
+        G = T * qT + P * z + Gh
+    else:
+        qd = np.zeros_like(w_end)
+        Gh = np.zeros_like(w_end)
+        for r in range(world):
+            p0, p1 = rank_block(P, r, world)
+            C = np.zeros_like(w_end)
+            Gr = np.zeros_like(w_end)
+            for p in range(p1 - 1, p0 - 1, -1):
+                C = w_end.copy() if p == p1 - 1 else exp_action(applyAT, plan_slice, C, Gr) + w_end
+            if p0 > 0:
+                C = exp_action(applyAT, plan_long_adjoint(p0 * delta), C, Gr)
+            qd = qd + C
+            Gh = Gh + (p1 - p0) * z + Gr
+        qdag0 = qT + qd
+        G = T * qT + Gh
+    grad = basis.project(G)
+    return OracleResult(J=J, grad=grad, uT=uT, qdag0=qdag0, G=G, u_bnd=u_bnd,
+                        extras={"v_end": v_end, "w_end": w_end, "z": z})
+
+
+# ---------------------------------------------------------------------------
+# Burgers (config 3): serial direct + Paraexp adjoint with frozen slices
+# ---------------------------------------------------------------------------
+
+
+def burgers_direct(u0, f, D, h_grid, h, nsteps_total):
+    """Serial classical RK4 keeping every node (the HBM trajectory)."""
+    traj = np.empty((nsteps_total + 1,) + u0.shape)
+    u = u0.copy()
+    traj[0] = u
+    for i in range(nsteps_total):
+        k1 = burgers_rhs(u, f, D, h_grid)
+        k2 = burgers_rhs(u + (0.5 * h) * k1, f, D, h_grid)
+        k3 = burgers_rhs(u + (0.5 * h) * k2, f, D, h_grid)
+        k4 = burgers_rhs(u + h * k3, f, D, h_grid)
+        u = u + (h / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+        traj[i + 1] = u
+    return traj
+
+
+def slice_means(traj, P, nsteps):
+    """Trapezoid-weighted mean of each slice's nodes (`problems.py:346-366`)."""
+    w = np.ones(nsteps + 1)
+    w[0] = w[-1] = 0.5
+    w /= nsteps
+    return np.stack([np.tensordot(w, traj[p * nsteps: (p + 1) * nsteps + 1], axes=(0, 0))
+                     for p in range(P)])
+
+
+def burgers_gradient(nx, D, basis, T, P, nsteps, u0, u_target, ctrl, plan_for_region,
+                     region_fn, world: int = 1):
+    """Config 3 (Option A of SURVEY §8(c)): absorbed final condition, exact Jᵀ(u(t))
+    in the inhomogeneous solves, frozen J(ū_p)ᵀ in the homogeneous ones."""
+    n = nx
+    hg = 2.0 * np.pi / nx
+    ctrl = np.atleast_2d(np.asarray(ctrl, dtype=np.float64))
+    B = ctrl.shape[0]
+    u0 = np.broadcast_to(_as_batch(u0, n), (B, n)).copy()
+    ut = np.broadcast_to(_as_batch(u_target, n), (B, n))
+    delta = T / P
+    h = delta / nsteps
+    f = basis.field(ctrl)
+    traj = burgers_direct(u0, f, D, hg, h, P * nsteps)          # (S+1, B, n)
+    uT = traj[-1]
+    qT = uT - ut
+    J = 0.5 * np.sum(qT * qT, axis=1)
+
+    ubar = slice_means(traj, P, nsteps)                          # (P, B, n)
+    region = region_fn(ubar)
+    plan = plan_for_region(region, delta)
+
+    w_end = np.empty((P, B, n))
+    zsum = np.zeros((B, n))
+    for p in range(P):
+        w = np.zeros((B, n))
+        z = np.zeros((B, n))
+        top = (p + 1) * nsteps
+        for i in range(nsteps):
+            ua = traj[top - i]
+            ub = traj[top - i - 1]
+            um = 0.5 * ua + 0.5 * ub
+            k1 = burgers_adjoint_apply(ua, w + qT, D, hg)
+            Y2 = w + (0.5 * h) * k1
+            k2 = burgers_adjoint_apply(um, Y2 + qT, D, hg)
+            Y3 = w + (0.5 * h) * k2
+            k3 = burgers_adjoint_apply(um, Y3 + qT, D, hg)
+            Y4 = w + h * k3
+            k4 = burgers_adjoint_apply(ub, Y4 + qT, D, hg)
+            z = z + (h / 6.0) * (w + 2.0 * Y2 + 2.0 * Y3 + Y4)
+            w = w + (h / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+        w_end[p] = w
+        zsum += z
+
+    def frozen(p):
+        ub = ubar[p]
+        return lambda y: burgers_adjoint_apply(ub, y, D, hg)
+
+    qd = np.zeros((B, n))
+    Gh = np.zeros((B, n))
+    for r in range(world):
+        p0, p1 = rank_block(P, r, world)
+        C = np.zeros((B, n))
+        for p in range(p1 - 1, p0 - 1, -1):
+            C = w_end[p].copy() if p == p1 - 1 else exp_action(frozen(p), plan, C, Gh) + w_end[p]
+        for p in range(p0 - 1, -1, -1):       # carry through earlier ranks' frozen slices
+            C = exp_action(frozen(p), plan, C, Gh)
+        qd = qd + C
+    qdag0 = qT + qd
+    G = T * qT + zsum + Gh
+    grad = basis.project(G)
+    return OracleResult(J=J, grad=grad, uT=uT, qdag0=qdag0, G=G,
+                        extras={"traj": traj, "ubar": ubar, "plan": plan, "w_end": w_end})

@@ -1,0 +1,58 @@
+"""B200-native Paraexp direct-adjoint gradient path (arXiv 2004.00546).
+
+Drop-in for the reference's hot path (`pkg/src/paradjoint`): the
+host API keeps the reference's names — problem setup, time partition, the
+direct-adjoint loop and the descent driver — and ``backend="cuda"`` runs the
+sweeps as hand-written sm_100a fp64 kernels behind the C ABI in
+``include/paraexp.h`` (``libparaexp.so``). There is no CPU fallback.
+"""
+
+from .configs import BaselineCase, baseline, scaled
+from .engine import EngineSpec, ParaexpEngine
+from .errors import (
+    CollectiveFailure,
+    ConfigError,
+    IntegrationFailure,
+    NativeUnavailable,
+    PropagationFailure,
+)
+from .expaction import ChebPlan, ChebyshevConfig, KrylovConfig, KrylovPlan, plan_chebyshev, plan_krylov
+from .optimization import (
+    ALGORITHMS,
+    HYBRID,
+    LINEAR,
+    AdjointSolution,
+    DescentResult,
+    DirectSolution,
+    LoopResult,
+    cost,
+    descend,
+    direct_adjoint_loop,
+    initial_condition_gradient,
+    release_engines,
+)
+from .partition import (
+    RK4Config,
+    TimePartition,
+    WorkerPlan,
+    partition_equidistant,
+    rank_block,
+    slice_steps,
+    worker_plans,
+)
+from .problems import (
+    ADVECTION_DIFFUSION,
+    BURGERS,
+    Grid,
+    ModeBasis,
+    ProblemSpec,
+    SpectralRegion,
+    Stencil,
+    advdiff_region,
+    advdiff_stencil,
+    burgers_frozen_region,
+    mode_basis,
+)
+from .systems import System, build_system
+
+__all__ = [name for name in dir() if not name.startswith("_")]

@@ -1,0 +1,156 @@
+"""ctypes binding of ``libparaexp.so`` (the C ABI in ``include/paraexp.h``).
+
+This is the binding a maintainer of the (pure-Python) reference would add for
+``backend="cuda"``; see INTEGRATION.md. The library is built in-tree by
+``__graft_entry__.build()`` (nvcc, sm_100a). There is no CPU fallback: if the
+library or a CUDA device is missing, :class:`NativeUnavailable` is raised.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_double, c_int, c_size_t, c_uint64, c_void_p
+
+from .errors import NativeUnavailable, raise_for_status
+
+LIB_NAME = "libparaexp.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+PX_KIND_ADVDIFF, PX_KIND_BURGERS = 0, 1
+PX_EXP_CHEBYSHEV, PX_EXP_KRYLOV = 0, 1
+PX_MEM_HOST, PX_MEM_DEVICE = 0, 1
+PX_PLAN_SLICE, PX_PLAN_LONG_DIRECT, PX_PLAN_LONG_ADJOINT, PX_PLAN_FROZEN = 0, 1, 2, 3
+(PX_FIELD_J, PX_FIELD_GRAD, PX_FIELD_UT, PX_FIELD_QDAG0, PX_FIELD_G, PX_FIELD_UBND,
+ PX_FIELD_FROZEN_BOUNDS, PX_FIELD_VEND, PX_FIELD_WEND, PX_FIELD_TRAJ) = range(10)
+PX_FLAG_BOUNDARY_STATES = 1
+
+
+class ProblemDesc(ctypes.Structure):
+    _fields_ = [
+        ("kind", c_int),
+        ("nx", c_int),
+        ("ny", c_int),
+        ("stencil", c_double * 5),
+        ("D", c_double),
+        ("hx", c_double),
+        ("T", c_double),
+        ("P", c_int),
+        ("nsteps", c_int),
+        ("p_begin", c_int),
+        ("p_end", c_int),
+        ("batch", c_int),
+        ("K", c_int),
+        ("basis_rows_x", c_int),
+        ("basis_rows_y", c_int),
+        ("expaction", c_int),
+        ("krylov_m", c_int),
+        ("flags", c_int),
+    ]
+
+
+class ChebPlanC(ctypes.Structure):
+    _fields_ = [
+        ("span", c_double),
+        ("substeps", c_int),
+        ("degree", c_int),
+        ("center", c_double),
+        ("scale", c_double),
+        ("sigma", c_int),
+        ("coef_exp", POINTER(c_double)),
+        ("coef_phi", POINTER(c_double)),
+    ]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("rk4_lane_steps", c_uint64),
+        ("exp_terms", c_uint64),
+        ("arnoldi_steps", c_uint64),
+        ("kernel_launches", c_uint64),
+        ("algorithmic_bytes", c_double),
+        ("rk4_bytes", c_double),
+        ("exp_bytes", c_double),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+PX_PHASES = ("rk4_direct", "rk4_adjoint", "exp_direct", "exp_adjoint", "other")
+
+
+class Timing(ctypes.Structure):
+    _fields_ = [("ms", c_double * 5), ("launches", c_uint64 * 5), ("bytes", c_double * 5)]
+
+    def as_dict(self) -> dict:
+        return {ph: {"ms": self.ms[i], "launches": int(self.launches[i]), "bytes": self.bytes[i]}
+                for i, ph in enumerate(PX_PHASES)}
+
+
+# exported symbols and their prototypes: (restype, argtypes)
+SIGNATURES = {
+    "px_abi_version": (c_int, []),
+    "px_build_info": (ctypes.c_char_p, []),
+    "px_create": (c_int, [POINTER(ProblemDesc), POINTER(c_void_p)]),
+    "px_destroy": (None, [c_void_p]),
+    "px_last_error": (ctypes.c_char_p, [c_void_p]),
+    "px_set_basis": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double), POINTER(c_int), POINTER(c_int)]),
+    "px_set_cheb_plan": (c_int, [c_void_p, c_int, POINTER(ChebPlanC)]),
+    "px_set_krylov_plan": (c_int, [c_void_p, c_int, c_double, c_int]),
+    "px_set_inputs": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
+    "px_direct": (c_int, [c_void_p, c_void_p]),
+    "px_finish_direct": (c_int, [c_void_p, c_void_p]),
+    "px_set_adjoint_terminal": (c_int, [c_void_p, c_void_p, c_int, c_void_p]),
+    "px_adjoint": (c_int, [c_void_p, c_void_p]),
+    "px_finish_adjoint": (c_int, [c_void_p, c_void_p]),
+    "px_gradient": (c_int, [c_void_p, c_void_p]),
+    "px_buffer": (c_int, [c_void_p, c_int, POINTER(c_void_p), POINTER(c_size_t)]),
+    "px_get": (c_int, [c_void_p, c_int, c_void_p, c_size_t, c_int, c_void_p]),
+    "px_set_timing": (c_int, [c_void_p, c_int]),
+    "px_get_timing": (c_int, [c_void_p, POINTER(Timing)]),
+    "px_get_stats": (c_int, [c_void_p, POINTER(Stats)]),
+    "px_reset_stats": (c_int, [c_void_p]),
+}
+
+_lib = None
+
+
+def load(path: str | None = None):
+    """Load the library (idempotent). Raises NativeUnavailable if absent."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise NativeUnavailable(
+            f"{p} not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the Paraexp path has no CPU fallback)")
+    lib = ctypes.CDLL(p)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.px_abi_version() != 1:
+        raise NativeUnavailable("libparaexp.so ABI version mismatch")
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def check(lib, rc: int, handle=None, t: float = float("nan")) -> None:
+    if rc != 0:
+        msg = lib.px_last_error(handle)
+        raise_for_status(rc, msg.decode() if msg else "", t)
+
+
+def dptr(a) -> ctypes.POINTER(c_double):
+    import numpy as np
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a.ctypes.data_as(POINTER(c_double)), a
+
+
+def iptr(a):
+    import numpy as np
+    a = np.ascontiguousarray(a, dtype=np.int32)
+    return a.ctypes.data_as(POINTER(c_int)), a

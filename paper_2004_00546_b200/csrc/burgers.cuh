@@ -1,0 +1,532 @@
+// burgers.cuh — BASELINE config 3: 1D viscous Burgers, serial direct sweep with
+// the trajectory kept in HBM, Paraexp adjoint with piecewise-frozen linearisation.
+//
+// Reference pieces restated here (Option A of SURVEY.md §8(c)):
+//   serial direct sweep        hybrid.py:185-191, serial.py:17-25 (rk45 -> fixed RK4)
+//   Burgers rhs (V ≡ 0)        problems.py:177-185
+//   Jᵀ(u)·y matrix-free        problems.py:316-343
+//   linear interpolation of the stored trajectory at RK stages   timestepping.py:64-75
+//   trapezoid-averaged frozen operator J(ū_p)ᵀ                   problems.py:346-366,
+//                                                                systems.py:76-97
+//   absorbed final condition, reflected time                    paraexp.py:256-295,329-353
+// The states are small (n ≤ 8192): every sweep runs with the state in shared
+// memory — the direct sweep is ONE persistent CTA per batch member stepping
+// P·nsteps times, the adjoint slice solves are one CTA per (member, slice), and
+// the homogeneous carry over all slices is one persistent CTA per member.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "../../include/paraexp.h"
+#include "kernels.cuh"
+
+namespace px {
+
+constexpr int BURGERS_MAX_N = 8192;
+constexpr int BURGERS_NT = 1024;
+
+struct BurgersDirectArgs {
+  const double *u0, *ctrl, *tx;
+  const int* ix;
+  int K;
+  double *traj, *ubar, *UT, *bpart, *bounds;
+  int bounds_blocks;
+  double D, hx, h;
+  int nx, B, P, nsteps;
+};
+
+struct BurgersAdjointArgs {
+  const double *traj, *ubar, *QT;
+  double *W0, *W1, *Z, *G, *QDAG0;
+  double* Wk[3];
+  double* ACC[2];
+  double D, hx, h;
+  int nx, B, P, nsteps, p_begin, p_end;
+  int substeps, degree, sigma;
+  double center, scale;
+  const double *be, *bp;
+};
+
+// rhs(u)_i = −u_i·(u_{i+1} − u_{i−1})/(2h) + D·(u_{i+1} − 2u_i + u_{i−1})/h² + f_i
+__device__ __forceinline__ double burgers_rhs_at(const double* s, int i, int n, double inv2h, double Dih2,
+                                                 double f) {
+  const int ip = (i + 1 == n) ? 0 : i + 1, im = (i == 0) ? n - 1 : i - 1;
+  const double u = s[i], up = s[ip], um = s[im];
+  const double dx = (up - um) * inv2h;
+  const double lap = (up - 2.0 * u + um) * Dih2;
+  return -u * dx + lap + f;
+}
+
+// One CTA per member; whole serial sweep (S = P·nsteps steps) with u in smem.
+// Every node is written to traj[s][b][:] (the HBM-resident direct trajectory).
+template <int PPT>
+__global__ void __launch_bounds__(BURGERS_NT) k_burgers_direct(BurgersDirectArgs a) {
+  extern __shared__ double sm[];
+  const int n = a.nx;
+  double* s_u = sm;
+  double* s_a = sm + n;
+  double* s_b = sm + 2 * n;
+  const int b = blockIdx.x;
+  const double inv2h = 1.0 / (2.0 * a.hx);
+  const double Dih2 = a.D / (a.hx * a.hx);
+  const double h = a.h, hh = 0.5 * a.h, h6 = a.h / 6.0;
+  double f[PPT], u[PPT], acc[PPT];
+  const double* c = a.ctrl + (size_t)b * a.K;
+#pragma unroll
+  for (int t = 0; t < PPT; ++t) {
+    const int i = threadIdx.x + t * BURGERS_NT;
+    f[t] = 0.0;
+    u[t] = 0.0;
+    if (i < n) {
+      double fv = 0.0;
+      for (int k = 0; k < a.K; ++k) fv += c[k] * a.tx[(size_t)a.ix[k] * n + i];
+      f[t] = fv;
+      u[t] = a.u0[i];
+      s_u[i] = u[t];
+      a.traj[(size_t)b * n + i] = u[t];
+    }
+  }
+  __syncthreads();
+  const size_t S = (size_t)a.P * a.nsteps;
+  const size_t node_stride = (size_t)a.B * n;
+  for (size_t st = 0; st < S; ++st) {
+#pragma unroll
+    for (int t = 0; t < PPT; ++t) {
+      const int i = threadIdx.x + t * BURGERS_NT;
+      if (i < n) {
+        const double k = burgers_rhs_at(s_u, i, n, inv2h, Dih2, f[t]);
+        acc[t] = k;
+        s_a[i] = u[t] + hh * k;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < PPT; ++t) {
+      const int i = threadIdx.x + t * BURGERS_NT;
+      if (i < n) {
+        const double k = burgers_rhs_at(s_a, i, n, inv2h, Dih2, f[t]);
+        acc[t] += 2.0 * k;
+        s_b[i] = u[t] + hh * k;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < PPT; ++t) {
+      const int i = threadIdx.x + t * BURGERS_NT;
+      if (i < n) {
+        const double k = burgers_rhs_at(s_b, i, n, inv2h, Dih2, f[t]);
+        acc[t] += 2.0 * k;
+        s_a[i] = u[t] + h * k;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < PPT; ++t) {
+      const int i = threadIdx.x + t * BURGERS_NT;
+      if (i < n) {
+        const double k = burgers_rhs_at(s_a, i, n, inv2h, Dih2, f[t]);
+        u[t] = u[t] + h6 * (acc[t] + k);
+        a.traj[(st + 1) * node_stride + (size_t)b * n + i] = u[t];
+      }
+    }
+    __syncthreads();  // all reads of s_a done before s_u is overwritten
+#pragma unroll
+    for (int t = 0; t < PPT; ++t) {
+      const int i = threadIdx.x + t * BURGERS_NT;
+      if (i < n) s_u[i] = u[t];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int t = 0; t < PPT; ++t) {
+    const int i = threadIdx.x + t * BURGERS_NT;
+    if (i < n) a.UT[(size_t)b * n + i] = u[t];
+  }
+}
+
+// ū_p[b][i] = Σ_j w_j traj[p·ns + j][b][i], trapezoid weights (½,1,…,1,½)/ns
+__global__ void k_slice_means(double* ubar, const double* traj, int P, int nsteps, int B, int n) {
+  const size_t total = (size_t)P * B * n;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const int p = (int)(idx / ((size_t)B * n));
+    const size_t rem = idx - (size_t)p * B * n;  // b*n + i
+    const double* src = traj + (size_t)p * nsteps * B * n + rem;
+    const double w = 1.0 / nsteps;
+    double s = (0.5 * w) * src[0];
+    for (int j = 1; j < nsteps; ++j) s += w * src[(size_t)j * B * n];
+    s += (0.5 * w) * src[(size_t)nsteps * B * n];
+    ubar[idx] = s;
+  }
+}
+
+// Field-of-values box of B̄ = J(ū)ᵀ, union over slices and members (see
+// problems.burgers_frozen_region): (min re_lo, max re_hi, max im) partials.
+__global__ void __launch_bounds__(256) k_frozen_bounds(double* bpart, const double* ubar, size_t total, int n,
+                                                       double hx, double D) {
+  __shared__ double r0[8], r1[8], r2[8];
+  double lo = 1e300, hi = -1e300, im = 0.0;
+  const double inv2h = 1.0 / (2.0 * hx), inv4h = 1.0 / (4.0 * hx), dh2 = 2.0 * D / (hx * hx);
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = idx / n;
+    const int i = (int)(idx - row * n);
+    const double* u = ubar + row * n;
+    const double uc = u[i], up = u[i + 1 == n ? 0 : i + 1], um = u[i == 0 ? n - 1 : i - 1];
+    const double dxu = (up - um) * inv2h;
+    const double diag = -dxu - dh2;
+    const double rad = (fabs(up - uc) + fabs(uc - um)) * inv4h + dh2;
+    lo = fmin(lo, diag - rad);
+    hi = fmax(hi, diag + rad);
+    im = fmax(im, (fabs(up + uc) + fabs(uc + um)) * inv4h);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_down_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_down_sync(0xffffffffu, hi, o));
+    im = fmax(im, __shfl_down_sync(0xffffffffu, im, o));
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { r0[w] = lo; r1[w] = hi; r2[w] = im; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < 8; ++k) { lo = fmin(lo, r0[k]); hi = fmax(hi, r1[k]); im = fmax(im, r2[k]); }
+    bpart[3 * blockIdx.x + 0] = lo;
+    bpart[3 * blockIdx.x + 1] = hi;
+    bpart[3 * blockIdx.x + 2] = im;
+  }
+}
+
+__global__ void k_frozen_bounds_final(double* bounds, const double* bpart, int m) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double lo = 1e300, hi = -1e300, im = 0.0;
+  for (int k = 0; k < m; ++k) {
+    lo = fmin(lo, bpart[3 * k]);
+    hi = fmax(hi, bpart[3 * k + 1]);
+    im = fmax(im, bpart[3 * k + 2]);
+  }
+  bounds[0] = lo;
+  bounds[1] = hi;
+  bounds[2] = im;
+}
+
+// (Jᵀ(u) y)_i = (u_{i+1}y_{i+1} − u_{i−1}y_{i−1})/(2h) − (u_{i+1} − u_{i−1})/(2h)·y_i
+//              + D(y_{i+1} − 2y_i + y_{i−1})/h²
+__device__ __forceinline__ double jt_at(const double* su, const double* sy, int i, int n, double inv2h,
+                                        double Dih2) {
+  const int ip = (i + 1 == n) ? 0 : i + 1, im = (i == 0) ? n - 1 : i - 1;
+  const double up = su[ip], um = su[im];
+  const double yp = sy[ip], ym = sy[im], yc = sy[i];
+  const double dxuy = (up * yp - um * ym) * inv2h;
+  const double dxu = (up - um) * inv2h;
+  const double lap = (yp - 2.0 * yc + ym) * Dih2;
+  return dxuy - dxu * yc + lap;
+}
+
+// One CTA per lane (member b, slice p): reflected-time RK4 of
+// w' = Jᵀ(u(t))(w + q†_T), w(0) = 0, z = ∫w; u at stage times by linear
+// interpolation of the stored nodes (half steps: 0.5·u_j + 0.5·u_{j−1}).
+template <int PPT>
+__global__ void __launch_bounds__(BURGERS_NT) k_burgers_adjoint_rk4(BurgersAdjointArgs a) {
+  extern __shared__ double sm[];
+  const int n = a.nx;
+  double* s_ua = sm;
+  double* s_ub = sm + n;
+  double* s_um = sm + 2 * n;
+  double* s_y = sm + 3 * n;
+  const int Pl = a.p_end - a.p_begin;
+  const int lane = blockIdx.x;
+  const int b = lane / Pl;
+  const int p = a.p_begin + (lane - b * Pl);
+  const double inv2h = 1.0 / (2.0 * a.hx);
+  const double Dih2 = a.D / (a.hx * a.hx);
+  const double h = a.h, hh = 0.5 * a.h, h6 = a.h / 6.0;
+  const size_t node_stride = (size_t)a.B * n;
+  const double* qT = a.QT + (size_t)b * n;
+  double q[PPT], w[PPT], z[PPT], acc[PPT], zacc[PPT];
+  const int top = (p + 1) * a.nsteps;
+#pragma unroll
+  for (int t = 0; t < PPT; ++t) {
+    const int i = threadIdx.x + t * BURGERS_NT;
+    w[t] = 0.0;
+    z[t] = 0.0;
+    q[t] = 0.0;
+    if (i < n) {
+      q[t] = qT[i];
+      s_ua[i] = a.traj[(size_t)top * node_stride + (size_t)b * n + i];
+    }
+  }
+  double* ua = s_ua;
+  double* ub = s_ub;
+  for (int st = 0; st < a.nsteps; ++st) {
+    const double* nodeb = a.traj + (size_t)(top - st - 1) * node_stride + (size_t)b * n;
+#pragma unroll
+    for (int t = 0; t < PPT; ++t) {
+      const int i = threadIdx.x + t * BURGERS_NT;
+      if (i < n) {
+        const double vb = nodeb[i];
+        ub[i] = vb;
+        s_um[i] = 0.5 * ua[i] + 0.5 * vb;
+        s_y[i] = w[t] + q[t];
+      }
+    }
+    __syncthreads();
+    double Y[PPT];
+#pragma unroll
+    for (int t = 0; t < PPT; ++t) {
+      const int i = threadIdx.x + t * BURGERS_NT;
+      if (i < n) {
+        const double k = jt_at(ua, s_y, i, n, inv2h, Dih2);
+        acc[t] = k;
+        Y[t] = w[t] + hh * k;
+        zacc[t] = w[t] + 2.0 * Y[t];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < PPT; ++t) {
+      const int i = threadIdx.x + t * BURGERS_NT;
+      if (i < n) s_y[i] = Y[t] + q[t];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < PPT; ++t) {
+      const int i = threadIdx.x + t * BURGERS_NT;
+      if (i < n) {
+        const double k = jt_at(s_um, s_y, i, n, inv2h, Dih2);
+        acc[t] += 2.0 * k;
+        Y[t] = w[t] + hh * k;
+        zacc[t] += 2.0 * Y[t];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < PPT; ++t) {
+      const int i = threadIdx.x + t * BURGERS_NT;
+      if (i < n) s_y[i] = Y[t] + q[t];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < PPT; ++t) {
+      const int i = threadIdx.x + t * BURGERS_NT;
+      if (i < n) {
+        const double k = jt_at(s_um, s_y, i, n, inv2h, Dih2);
+        acc[t] += 2.0 * k;
+        Y[t] = w[t] + h * k;
+        zacc[t] += Y[t];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < PPT; ++t) {
+      const int i = threadIdx.x + t * BURGERS_NT;
+      if (i < n) s_y[i] = Y[t] + q[t];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < PPT; ++t) {
+      const int i = threadIdx.x + t * BURGERS_NT;
+      if (i < n) {
+        const double k = jt_at(ub, s_y, i, n, inv2h, Dih2);
+        z[t] = z[t] + h6 * zacc[t];
+        w[t] = w[t] + h6 * (acc[t] + k);
+      }
+    }
+    __syncthreads();
+    double* tmp = ua;
+    ua = ub;
+    ub = tmp;
+  }
+#pragma unroll
+  for (int t = 0; t < PPT; ++t) {
+    const int i = threadIdx.x + t * BURGERS_NT;
+    if (i < n) {
+      a.W0[(size_t)lane * n + i] = w[t];
+      a.Z[(size_t)lane * n + i] = z[t];
+    }
+  }
+}
+
+// One CTA per member: the homogeneous carry over all slices, frozen operators
+// J(ū_p)ᵀ, Chebyshev substeps with exp and φ₁ accumulators, state in smem.
+//   C <- w_{p1−1};  for p = p1−2 … p0: C <- exp(ΔB̄_p)C + w_p,  G += Δφ₁(ΔB̄_p)C
+//   for p = p0−1 … 0: C <- exp(ΔB̄_p)C (carry through earlier ranks' slices)
+template <int PPT>
+__global__ void __launch_bounds__(BURGERS_NT) k_burgers_scan(BurgersAdjointArgs a, const double* coef) {
+  extern __shared__ double sm[];
+  const int n = a.nx;
+  double* s_u = sm;          // ū_p
+  double* s_cur = sm + n;    // U_k
+  const int b = blockIdx.x;
+  const int Pl = a.p_end - a.p_begin;
+  const double inv2h = 1.0 / (2.0 * a.hx);
+  const double Dih2 = a.D / (a.hx * a.hx);
+  const double c0 = a.center, d = a.scale, two_over = 2.0 / a.scale, sigma = (double)a.sigma;
+  const double* be = coef;
+  const double* bp = coef + a.degree + 1;
+  double C[PPT], Gp[PPT], prev[PPT], cur[PPT], acc[PPT], pac[PPT];
+#pragma unroll
+  for (int t = 0; t < PPT; ++t) {
+    const int i = threadIdx.x + t * BURGERS_NT;
+    C[t] = Gp[t] = 0.0;
+    if (i < n) {
+      C[t] = a.W0[((size_t)b * Pl + (Pl - 1)) * n + i];
+      Gp[t] = a.G[(size_t)b * n + i];
+    }
+  }
+  for (int p = a.p_end - 2; p >= 0; --p) {
+    const bool own = p >= a.p_begin;
+    const double* ub = a.ubar + ((size_t)p * a.B + b) * n;
+#pragma unroll
+    for (int t = 0; t < PPT; ++t) {
+      const int i = threadIdx.x + t * BURGERS_NT;
+      if (i < n) s_u[i] = ub[i];
+    }
+    for (int sub = 0; sub < a.substeps; ++sub) {
+      // k = 0, 1
+#pragma unroll
+      for (int t = 0; t < PPT; ++t) {
+        const int i = threadIdx.x + t * BURGERS_NT;
+        if (i < n) s_cur[i] = C[t];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int t = 0; t < PPT; ++t) {
+        const int i = threadIdx.x + t * BURGERS_NT;
+        if (i < n) {
+          const double u0 = C[t];
+          const double u1 = (jt_at(s_u, s_cur, i, n, inv2h, Dih2) - c0 * u0) / d;
+          prev[t] = u0;
+          cur[t] = u1;
+          acc[t] = be[0] * u0 + be[1] * u1;
+          pac[t] = bp[0] * u0 + bp[1] * u1;
+        }
+      }
+      for (int k = 2; k <= a.degree; ++k) {
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < PPT; ++t) {
+          const int i = threadIdx.x + t * BURGERS_NT;
+          if (i < n) s_cur[i] = cur[t];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < PPT; ++t) {
+          const int i = threadIdx.x + t * BURGERS_NT;
+          if (i < n) {
+            const double un = two_over * (jt_at(s_u, s_cur, i, n, inv2h, Dih2) - c0 * cur[t]) + sigma * prev[t];
+            prev[t] = cur[t];
+            cur[t] = un;
+            acc[t] += be[k] * un;
+            pac[t] += bp[k] * un;
+          }
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int t = 0; t < PPT; ++t) {
+        C[t] = acc[t];
+        Gp[t] += pac[t];
+      }
+    }
+    if (own) {
+#pragma unroll
+      for (int t = 0; t < PPT; ++t) {
+        const int i = threadIdx.x + t * BURGERS_NT;
+        if (i < n) C[t] += a.W0[((size_t)b * Pl + (p - a.p_begin)) * n + i];
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < PPT; ++t) {
+    const int i = threadIdx.x + t * BURGERS_NT;
+    if (i < n) {
+      a.QDAG0[(size_t)b * n + i] = C[t];
+      a.G[(size_t)b * n + i] = Gp[t];
+    }
+  }
+}
+
+inline int burgers_direct(const BurgersDirectArgs& a, cudaStream_t s, px_stats* stats) {
+  if (a.nx > BURGERS_MAX_N) return PX_ERR_ARG;
+  const size_t smem = 3 * (size_t)a.nx * sizeof(double);
+  const int ppt = (a.nx + BURGERS_NT - 1) / BURGERS_NT;
+#define PX_BD(PP)                                                                              \
+  do {                                                                                         \
+    cudaFuncSetAttribute(k_burgers_direct<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    k_burgers_direct<PP><<<a.B, BURGERS_NT, smem, s>>>(a);                                     \
+  } while (0)
+  if (ppt <= 1) PX_BD(1);
+  else if (ppt <= 2) PX_BD(2);
+  else if (ppt <= 4) PX_BD(4);
+  else PX_BD(8);
+#undef PX_BD
+  const size_t total = (size_t)a.P * a.B * a.nx;
+  k_slice_means<<<(unsigned)std::min<size_t>((total + 255) / 256, 4096), 256, 0, s>>>(a.ubar, a.traj, a.P,
+                                                                                       a.nsteps, a.B, a.nx);
+  k_frozen_bounds<<<a.bounds_blocks, 256, 0, s>>>(a.bpart, a.ubar, total, a.nx, a.hx, a.D);
+  k_frozen_bounds_final<<<1, 32, 0, s>>>(a.bounds, a.bpart, a.bounds_blocks);
+  if (cudaGetLastError() != cudaSuccess) return PX_ERR_CUDA;
+  if (stats) {
+    stats->kernel_launches += 4;
+    const double S = (double)a.P * a.nsteps;
+    stats->rk4_lane_steps += (uint64_t)(S * a.B);
+    const double bytes = 24.0 * a.nx * S * a.B;  // read u_n, (f), write node u_{n+1}
+    stats->rk4_bytes += bytes;
+    stats->algorithmic_bytes += bytes;
+  }
+  return PX_OK;
+}
+
+inline int burgers_adjoint(const BurgersAdjointArgs& a, cudaStream_t s, px_stats* stats, const double** wend) {
+  if (a.nx > BURGERS_MAX_N) return PX_ERR_ARG;
+  const int Pl = a.p_end - a.p_begin;
+  const int ppt = (a.nx + BURGERS_NT - 1) / BURGERS_NT;
+  const size_t smem_rk = 4 * (size_t)a.nx * sizeof(double);
+#define PX_BA(PP)                                                                                  \
+  do {                                                                                             \
+    cudaFuncSetAttribute(k_burgers_adjoint_rk4<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rk); \
+    k_burgers_adjoint_rk4<PP><<<a.B * Pl, BURGERS_NT, smem_rk, s>>>(a);                            \
+  } while (0)
+  if (ppt <= 1) PX_BA(1);
+  else if (ppt <= 2) PX_BA(2);
+  else if (ppt <= 4) PX_BA(4);
+  else PX_BA(8);
+#undef PX_BA
+  k_lane_sum<<<dim3((unsigned)std::min<size_t>(((size_t)a.nx + 255) / 256, 64), a.B), 256, 0, s>>>(
+      a.G, a.Z, Pl, (size_t)a.nx);
+  // coefficients to device (scratch ACC[0] is free here: n ≥ 2·(degree+1) not guaranteed, use Wk[2])
+  double* coef = a.Wk[2];
+  const size_t ncoef = 2 * (size_t)(a.degree + 1);
+  if ((size_t)a.B * a.nx < ncoef) return PX_ERR_ARG;
+  cudaMemcpyAsync(coef, a.be, sizeof(double) * (a.degree + 1), cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(coef + a.degree + 1, a.bp, sizeof(double) * (a.degree + 1), cudaMemcpyHostToDevice, s);
+  const size_t smem_sc = 2 * (size_t)a.nx * sizeof(double);
+#define PX_BS(PP)                                                                               \
+  do {                                                                                          \
+    cudaFuncSetAttribute(k_burgers_scan<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sc); \
+    k_burgers_scan<PP><<<a.B, BURGERS_NT, smem_sc, s>>>(a, coef);                               \
+  } while (0)
+  if (ppt <= 1) PX_BS(1);
+  else if (ppt <= 2) PX_BS(2);
+  else if (ppt <= 4) PX_BS(4);
+  else PX_BS(8);
+#undef PX_BS
+  if (cudaGetLastError() != cudaSuccess) return PX_ERR_CUDA;
+  *wend = a.W0;
+  if (stats) {
+    stats->kernel_launches += 3;
+    stats->rk4_lane_steps += (uint64_t)a.B * Pl * a.nsteps;
+    const double rb = 40.0 * a.nx * (double)a.B * Pl * a.nsteps;  // y, q†_T, node, y', z
+    stats->rk4_bytes += rb;
+    const uint64_t acts = (uint64_t)(a.p_end - 1);
+    const uint64_t terms = acts * a.substeps * a.degree * a.B;
+    stats->exp_terms += terms;
+    const double eb = 56.0 * a.nx * (double)terms;
+    stats->exp_bytes += eb;
+    stats->algorithmic_bytes += rb + eb;
+  }
+  return PX_OK;
+}
+
+}  // namespace px

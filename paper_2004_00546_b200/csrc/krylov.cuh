@@ -1,0 +1,353 @@
+// krylov.cuh — batched Arnoldi exponential action (BASELINE config 4: m = 30).
+//
+// No reference equivalent (Krylov is out of the reference's scope, SPEC.md:13,204;
+// the paper describes it). Per substep of width τ:
+//   β = ‖y‖, V_0 = y/β; for j < m: w = M V_j, CGS2 against V_0..V_j (the
+//   stencil application is fused with the first pass's dot products),
+//   h_{j+1,j} = ‖w‖, V_{j+1} = w/h_{j+1,j};
+//   E = exp([[τH_m, τe_1], [0, 0]]) (one CTA, Taylor-18 scaling and squaring);
+//   y <- β·V_m·E[:m, 0],  φ-accumulator += β·V_m·E[:m, m]  (= τφ₁(τM)y).
+// Reductions are two-level and fixed-order (deterministic). The basis for
+// config 4 (31 × 2 MB) stays resident in the 126 MB L2.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "../../include/paraexp.h"
+#include "kernels.cuh"
+
+namespace px {
+
+constexpr int KRYLOV_MAX_M = 40;
+constexpr double KRYLOV_BREAKDOWN = 1e-13;
+
+struct KrylovWork {
+  int m = 0, B = 0, nblk = 0;
+  size_t n = 0;
+  double* V = nullptr;        // (m+1) × B × n
+  double* w = nullptr;        // B × n
+  double* H = nullptr;        // B × (m+1) × m   (row i, col j at i*m + j)
+  double* hcol = nullptr;     // B × (MAX_M+1)  current column pass values
+  double* part = nullptr;     // B × (MAX_M+1) × nblk partial dots
+  double* beta = nullptr;     // B
+  double* coef = nullptr;     // B × 2 × m  (exp column, φ column), β-scaled
+};
+
+inline int krylov_alloc(KrylovWork& kw, int m, size_t n, int B, std::string* err) {
+  kw.m = m;
+  kw.n = n;
+  kw.B = B;
+  kw.nblk = (int)((n + 255) / 256);
+  auto al = [&](double** p, size_t cnt) -> bool {
+    cudaError_t e = cudaMalloc(p, cnt * sizeof(double));
+    if (e != cudaSuccess) {
+      if (err) *err = std::string("krylov cudaMalloc: ") + cudaGetErrorString(e);
+      return false;
+    }
+    return true;
+  };
+  if (!al(&kw.V, (size_t)(m + 1) * B * n) || !al(&kw.w, (size_t)B * n) ||
+      !al(&kw.H, (size_t)B * (m + 1) * m) || !al(&kw.hcol, (size_t)B * (KRYLOV_MAX_M + 1)) ||
+      !al(&kw.part, (size_t)B * (KRYLOV_MAX_M + 1) * kw.nblk) || !al(&kw.beta, B) ||
+      !al(&kw.coef, (size_t)B * 2 * m))
+    return PX_ERR_NOMEM;
+  return PX_OK;
+}
+
+inline void krylov_free(KrylovWork& kw) {
+  cudaFree(kw.V); cudaFree(kw.w); cudaFree(kw.H); cudaFree(kw.hcol);
+  cudaFree(kw.part); cudaFree(kw.beta); cudaFree(kw.coef);
+  kw = KrylovWork{};
+}
+
+// partial[b][0][blk] = Σ y², one point per thread
+__global__ void __launch_bounds__(256) k_kr_sumsq(double* part, int nblk, const double* y, long long ybs,
+                                                  size_t n) {
+  __shared__ double red[8];
+  const int b = blockIdx.y;
+  const size_t i = (size_t)blockIdx.x * 256 + threadIdx.x;
+  double v = 0.0;
+  if (i < n) {
+    const double t = y[b * ybs + i];
+    v = t * t;
+  }
+  v = block_sum<256>(v, red);
+  if (threadIdx.x == 0) part[(size_t)b * nblk + blockIdx.x] = v;
+}
+
+// out[b] = sqrt(Σ part[b][:])
+__global__ void __launch_bounds__(256) k_kr_beta(double* beta, const double* part, int nblk) {
+  __shared__ double red[8];
+  const int b = blockIdx.x;
+  double v = 0.0;
+  for (int j = threadIdx.x; j < nblk; j += 256) v += part[(size_t)b * nblk + j];
+  v = block_sum<256>(v, red);
+  if (threadIdx.x == 0) beta[b] = sqrt(v);
+}
+
+// V0[b] = y[b] / beta[b] (0 if beta == 0)
+__global__ void k_kr_v0(double* V0, const double* y, long long ybs, const double* beta, size_t n) {
+  const int b = blockIdx.y;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double bt = beta[b];
+  V0[(size_t)b * n + i] = bt > 0.0 ? y[b * ybs + i] / bt : 0.0;
+}
+
+// w = M V_j; part[b][i][blk] = Σ V_i·w for i ≤ j
+template <int DIM>
+__global__ void __launch_bounds__(256) k_kr_spmv_dots(double* w, const double* V, int j, Stencil5 st,
+                                                      double* part, int nblk, int B, int nx, int ny) {
+  __shared__ double red[8];
+  const size_t n = (size_t)nx * ny;
+  const int b = blockIdx.y;
+  const size_t i = (size_t)blockIdx.x * 256 + threadIdx.x;
+  double wv = 0.0;
+  if (i < n) {
+    const int y = (int)(i / nx), x = (int)(i - (size_t)y * nx);
+    wv = stencil_at<DIM>(V + ((size_t)j * B + b) * n, st, x, y, nx, ny);
+    w[(size_t)b * n + i] = wv;
+  }
+  for (int q = 0; q <= j; ++q) {
+    const double v = (i < n) ? V[((size_t)q * B + b) * n + i] * wv : 0.0;
+    const double s = block_sum<256>(v, red);
+    if (threadIdx.x == 0) part[((size_t)b * (KRYLOV_MAX_M + 1) + q) * nblk + blockIdx.x] = s;
+  }
+}
+
+// w -= Σ_{q≤j} hcol[b][q] V_q; then part = dots (mode 0) or ‖w‖² (mode 1)
+__global__ void __launch_bounds__(256) k_kr_update(double* w, const double* V, int j, const double* hcol,
+                                                   double* part, int nblk, int B, size_t n, int mode) {
+  __shared__ double red[8];
+  const int b = blockIdx.y;
+  const size_t i = (size_t)blockIdx.x * 256 + threadIdx.x;
+  double wv = 0.0;
+  if (i < n) {
+    wv = w[(size_t)b * n + i];
+    for (int q = 0; q <= j; ++q) wv -= hcol[(size_t)b * (KRYLOV_MAX_M + 1) + q] * V[((size_t)q * B + b) * n + i];
+    w[(size_t)b * n + i] = wv;
+  }
+  if (mode == 0) {
+    for (int q = 0; q <= j; ++q) {
+      const double v = (i < n) ? V[((size_t)q * B + b) * n + i] * wv : 0.0;
+      const double s = block_sum<256>(v, red);
+      if (threadIdx.x == 0) part[((size_t)b * (KRYLOV_MAX_M + 1) + q) * nblk + blockIdx.x] = s;
+    }
+  } else {
+    const double s = block_sum<256>(wv * wv, red);
+    if (threadIdx.x == 0) part[((size_t)b * (KRYLOV_MAX_M + 1)) * nblk + blockIdx.x] = s;
+  }
+}
+
+// hcol[b][q] = Σ_blk part[b][q][blk]; H[b][q][j] (+)= hcol  (grid: (j+1, B))
+__global__ void __launch_bounds__(256) k_kr_finalize_dots(double* hcol, double* H, const double* part, int nblk,
+                                                          int m, int j, int accumulate) {
+  __shared__ double red[8];
+  const int q = blockIdx.x, b = blockIdx.y;
+  double v = 0.0;
+  const double* p = part + ((size_t)b * (KRYLOV_MAX_M + 1) + q) * nblk;
+  for (int t = threadIdx.x; t < nblk; t += 256) v += p[t];
+  v = block_sum<256>(v, red);
+  if (threadIdx.x == 0) {
+    hcol[(size_t)b * (KRYLOV_MAX_M + 1) + q] = v;
+    double* hq = H + ((size_t)b * (m + 1) + q) * m + j;
+    *hq = accumulate ? *hq + v : v;
+  }
+}
+
+// H[b][j+1][j] = ‖w‖ (0 on breakdown); hcol[b][0] = 1/‖w‖ (0 on breakdown)
+__global__ void __launch_bounds__(256) k_kr_finalize_norm(double* hcol, double* H, const double* part, int nblk,
+                                                          int m, int j) {
+  __shared__ double red[8];
+  const int b = blockIdx.x;
+  double v = 0.0;
+  const double* p = part + ((size_t)b * (KRYLOV_MAX_M + 1)) * nblk;
+  for (int t = threadIdx.x; t < nblk; t += 256) v += p[t];
+  v = block_sum<256>(v, red);
+  if (threadIdx.x == 0) {
+    const double nrm = sqrt(v);
+    double mx = 1.0;
+    for (int q = 0; q <= j; ++q) mx = fmax(mx, fabs(H[((size_t)b * (m + 1) + q) * m + j]));
+    mx = fmax(mx, nrm);
+    const bool brk = nrm <= KRYLOV_BREAKDOWN * mx;
+    H[((size_t)b * (m + 1) + j + 1) * m + j] = brk ? 0.0 : nrm;
+    hcol[(size_t)b * (KRYLOV_MAX_M + 1)] = brk ? 0.0 : 1.0 / nrm;
+  }
+}
+
+// V_{j+1}[b] = w[b] · hcol[b][0]
+__global__ void k_kr_scale(double* Vn, const double* w, const double* hcol, int B, size_t n) {
+  const int b = blockIdx.y;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Vn[(size_t)b * n + i] = w[(size_t)b * n + i] * hcol[(size_t)b * (KRYLOV_MAX_M + 1)];
+}
+
+// One CTA per member: E = exp([[τH_m, τe_1],[0,0]]) by scaling and squaring + Taylor-18;
+// coef[b] = (β·E[:m,0], β·E[:m,m]).  Truncation at the first zero subdiagonal is implicit:
+// columns beyond a breakdown are zero and do not reach the first column.
+__global__ void __launch_bounds__(256) k_kr_expm(double* coef, const double* H, const double* beta, int m,
+                                                 double tau) {
+  extern __shared__ double sm[];
+  const int N = m + 1;
+  double* Aa = sm;            // N×N scaled matrix
+  double* E = Aa + N * N;     // accumulator
+  double* T = E + N * N;      // scratch
+  __shared__ double s_norm;
+  __shared__ int s_sq;
+  const int b = blockIdx.x;
+  const double* Hb = H + (size_t)b * (m + 1) * m;
+  // meff: first zero subdiagonal
+  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+    const int r = idx / N, c = idx - r * N;
+    double v = 0.0;
+    if (c < m && r < m) v = tau * Hb[r * m + c];
+    if (c == m && r == 0) v = tau;
+    Aa[idx] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // truncate at breakdown: zero rows/cols beyond meff
+    int meff = m;
+    for (int j = 0; j < m - 1; ++j)
+      if (Hb[(j + 1) * m + j] == 0.0) { meff = j + 1; break; }
+    if (meff < m) {
+      // move the τe_1 column to position meff and clear the rest
+      for (int r = 0; r < N; ++r)
+        for (int c = 0; c < N; ++c)
+          if (r >= meff || c >= meff) Aa[r * N + c] = 0.0;
+      Aa[0 * N + meff] = tau;
+    }
+    s_sq = meff;  // stash meff temporarily
+  }
+  __syncthreads();
+  const int meff = s_sq;
+  const int Ne = meff + 1;
+  // compact to Ne×Ne in T then back to Aa
+  for (int idx = threadIdx.x; idx < Ne * Ne; idx += blockDim.x) {
+    const int r = idx / Ne, c = idx - r * Ne;
+    T[idx] = Aa[r * N + c];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < Ne * Ne; idx += blockDim.x) Aa[idx] = T[idx];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double nrm = 0.0;
+    for (int c = 0; c < Ne; ++c) {
+      double s = 0.0;
+      for (int r = 0; r < Ne; ++r) s += fabs(Aa[r * Ne + c]);
+      nrm = fmax(nrm, s);
+    }
+    s_norm = nrm;
+    s_sq = nrm <= 0.5 ? 0 : (int)ceil(log2(nrm / 0.5));
+  }
+  __syncthreads();
+  const int sq = s_sq;
+  const double scale = ldexp(1.0, -sq);
+  for (int idx = threadIdx.x; idx < Ne * Ne; idx += blockDim.x) {
+    Aa[idx] *= scale;
+    E[idx] = (idx / Ne == idx % Ne) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int k = 18; k >= 1; --k) {
+    for (int idx = threadIdx.x; idx < Ne * Ne; idx += blockDim.x) {
+      const int r = idx / Ne, c = idx - r * Ne;
+      double s = 0.0;
+      for (int q = 0; q < Ne; ++q) s += Aa[r * Ne + q] * E[q * Ne + c];
+      T[idx] = ((r == c) ? 1.0 : 0.0) + s / k;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < Ne * Ne; idx += blockDim.x) E[idx] = T[idx];
+    __syncthreads();
+  }
+  for (int it = 0; it < sq; ++it) {
+    for (int idx = threadIdx.x; idx < Ne * Ne; idx += blockDim.x) {
+      const int r = idx / Ne, c = idx - r * Ne;
+      double s = 0.0;
+      for (int q = 0; q < Ne; ++q) s += E[r * Ne + q] * E[q * Ne + c];
+      T[idx] = s;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < Ne * Ne; idx += blockDim.x) E[idx] = T[idx];
+    __syncthreads();
+  }
+  const double bt = beta[b];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    coef[(size_t)b * 2 * m + i] = i < meff ? bt * E[i * Ne + 0] : 0.0;
+    coef[(size_t)b * 2 * m + m + i] = i < meff ? bt * E[i * Ne + meff] : 0.0;
+  }
+}
+
+// out[b] = Σ_i coef_e[b][i] V_i (+ addend);  pacc[b] += Σ_i coef_p[b][i] V_i
+__global__ void k_kr_combine(double* out, const double* V, const double* coef, int m, int B, size_t n,
+                             const double* addend, long long add_bs, double* pacc) {
+  const int b = blockIdx.y;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* ce = coef + (size_t)b * 2 * m;
+  const double* cp = ce + m;
+  double e = 0.0, p = 0.0;
+  for (int q = 0; q < m; ++q) {
+    const double v = V[((size_t)q * B + b) * n + i];
+    e += ce[q] * v;
+    p += cp[q] * v;
+  }
+  if (addend) e += addend[b * add_bs + i];
+  out[(size_t)b * n + i] = e;
+  if (pacc) pacc[(size_t)b * n + i] += p;
+}
+
+inline int krylov_action(KrylovWork& kw, double tau, int substeps, int m, const Stencil5& st,
+                         const double* src, long long src_bs, const double* addend, long long add_bs,
+                         double* pacc, double* const* ACC, int B, int nx, int ny, int dim,
+                         double** result, cudaStream_t s, px_stats* stats) {
+  const size_t n = kw.n;
+  const dim3 g(kw.nblk, B);
+  const long long nb = (long long)n;
+  uint64_t launches = 0;
+  for (int sub = 0; sub < substeps; ++sub) {
+    double* out = (src == ACC[0]) ? ACC[1] : ACC[0];
+    k_kr_sumsq<<<g, 256, 0, s>>>(kw.part, kw.nblk, src, src_bs, n);
+    k_kr_beta<<<B, 256, 0, s>>>(kw.beta, kw.part, kw.nblk);
+    k_kr_v0<<<g, 256, 0, s>>>(kw.V, src, src_bs, kw.beta, n);
+    launches += 3;
+    cudaMemsetAsync(kw.H, 0, sizeof(double) * B * (m + 1) * m, s);
+    for (int j = 0; j < m; ++j) {
+      if (dim == 2) k_kr_spmv_dots<2><<<g, 256, 0, s>>>(kw.w, kw.V, j, st, kw.part, kw.nblk, B, nx, ny);
+      else k_kr_spmv_dots<1><<<g, 256, 0, s>>>(kw.w, kw.V, j, st, kw.part, kw.nblk, B, nx, ny);
+      k_kr_finalize_dots<<<dim3(j + 1, B), 256, 0, s>>>(kw.hcol, kw.H, kw.part, kw.nblk, m, j, 0);
+      k_kr_update<<<g, 256, 0, s>>>(kw.w, kw.V, j, kw.hcol, kw.part, kw.nblk, B, n, 0);
+      k_kr_finalize_dots<<<dim3(j + 1, B), 256, 0, s>>>(kw.hcol, kw.H, kw.part, kw.nblk, m, j, 1);
+      k_kr_update<<<g, 256, 0, s>>>(kw.w, kw.V, j, kw.hcol, kw.part, kw.nblk, B, n, 1);
+      k_kr_finalize_norm<<<B, 256, 0, s>>>(kw.hcol, kw.H, kw.part, kw.nblk, m, j);
+      k_kr_scale<<<dim3((unsigned)((n + 255) / 256), B), 256, 0, s>>>(kw.V + (size_t)(j + 1) * B * n, kw.w,
+                                                                     kw.hcol, B, n);
+      launches += 7;
+    }
+    const int N = m + 1;
+    const size_t smem = 3 * (size_t)N * N * sizeof(double);
+    k_kr_expm<<<B, 256, smem, s>>>(kw.coef, kw.H, kw.beta, m, tau);
+    k_kr_combine<<<dim3((unsigned)((n + 255) / 256), B), 256, 0, s>>>(
+        out, kw.V, kw.coef, m, B, n, sub == substeps - 1 ? addend : nullptr, add_bs, pacc);
+    launches += 2;
+    src = out;
+    src_bs = nb;
+  }
+  if (stats) {
+    stats->kernel_launches += launches;
+    stats->arnoldi_steps += (uint64_t)substeps * m * B;
+    stats->exp_terms += (uint64_t)substeps * m * B;
+    // Arnoldi step j (CGS2): SpMV in/out 16n + 2 passes × (read V_0..V_j twice) ≈ 16n + 32n(j+1)
+    double bytes = 0.0;
+    for (int j = 0; j < m; ++j) bytes += 16.0 * n + 32.0 * n * (j + 1);
+    bytes += 8.0 * n * (m + 2);  // combine (+ pacc)
+    bytes *= (double)substeps * B;
+    stats->exp_bytes += bytes;
+    stats->algorithmic_bytes += bytes;
+  }
+  *result = const_cast<double*>(src);
+  return PX_OK;
+}
+
+}  // namespace px

@@ -1,0 +1,836 @@
+// paraexp_capi.cu — C ABI (include/paraexp.h) and native orchestration of one
+// Paraexp direct-adjoint gradient on one GPU (one rank's slice block).
+//
+// Sweep structure (reference structure paraexp.py:187-353):
+//   direct : g = A·u0 + f                       (absorbed IC, paraexp.py:239-242)
+//            v_p = RK4 zero-data solve per slice (all local slices × batch as lanes)
+//            D <- v_{p0};  D <- exp(ΔA)·D + v_p  (summed-chain carry; equals the
+//                                                 reference's neighbour chains by linearity)
+//            D <- exp((P − p1)Δ·A)·D             (blockscan long span, world > 1)
+//   adjoint: w' = Aᵀ(w + q†_T), z = ∫w           (absorbed FC, reflected time,
+//                                                 paraexp.py:256-295)
+//            C <- w_{p1−1};  C <- exp(ΔAᵀ)·C + w_p,  G += Δ·φ₁(ΔAᵀ)·C
+//            C <- exp(p0Δ·Aᵀ)·C (+φ₁)            (blockscan long span)
+//   outputs: u(T), J, q†(0), G = ∫q†dt, grad_k = ⟨φ_k, G⟩.
+// Everything is enqueued on the caller's stream; no host synchronisation.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/paraexp.h"
+#include "kernels.cuh"
+#include "burgers.cuh"
+#include "krylov.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Plan {
+  bool set = false;
+  bool krylov = false;
+  double span = 0.0;
+  int substeps = 0, degree = 0, sigma = -1;
+  double center = 0.0, scale = 1.0;
+  std::vector<double> be, bp;
+};
+
+struct Handle {
+  px_problem_desc d{};
+  int device = 0;
+  int dim = 1;
+  size_t n = 0;
+  int B = 1, K = 1, Pl = 1, L = 1;
+  int rows_x = 1, rows_y = 1;
+  px::Stencil5 A{}, AT{};
+
+  // inputs
+  double *u0 = nullptr, *ut = nullptr, *ctrl = nullptr;
+  double *tx = nullptr, *ty = nullptr;
+  int *ix = nullptr, *iy = nullptr;
+  bool basis_set = false, inputs_set = false;
+  // sources and lanes
+  double *g = nullptr, *gadj = nullptr;
+  double *Y0 = nullptr, *Y1 = nullptr, *Z = nullptr;
+  const double *vend = nullptr, *wend = nullptr;
+  // exp-action work
+  double* Wk[3] = {nullptr, nullptr, nullptr};
+  double* ACC[2] = {nullptr, nullptr};
+  // outputs
+  double *UT = nullptr, *QT = nullptr, *QDAG0 = nullptr, *G = nullptr;
+  double *J = nullptr, *GRAD = nullptr, *R = nullptr, *partial = nullptr;
+  int* nonfinite = nullptr;
+  double* UBND = nullptr;
+  int red_blocks = 0;
+  // Burgers
+  double *traj = nullptr, *ubar = nullptr, *bounds = nullptr, *bpart = nullptr;
+  int bounds_blocks = 0;
+  // Krylov
+  px::KrylovWork kw{};
+
+  Plan plans[PX_PLAN_COUNT];
+  px_stats stats{};
+  // phase timing (CUDA events on the work stream)
+  struct TMark { int phase; cudaEvent_t a, b; uint64_t launches; double bytes; };
+  bool timing = false;
+  std::vector<TMark> marks;
+  std::vector<cudaEvent_t> event_pool;
+  px_timing tacc{};
+  std::string err;
+  int stage = 0;  // 0 none, 1 direct, 2 finished direct, 3 adjoint, 4 finished
+  std::vector<void*> allocs;
+};
+
+int fail(Handle* h, int code, const std::string& msg) {
+  if (h) h->err = msg;
+  g_last_error = msg;
+  return code;
+}
+
+cudaEvent_t take_event(Handle* h) {
+  if (!h->event_pool.empty()) {
+    cudaEvent_t e = h->event_pool.back();
+    h->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Open a timing window for `phase` (returns -1 when timing is off).
+int tbegin(Handle* h, int phase, cudaStream_t s) {
+  if (!h->timing) return -1;
+  Handle::TMark m{phase, take_event(h), take_event(h), h->stats.kernel_launches, h->stats.algorithmic_bytes};
+  cudaEventRecord(m.a, s);
+  h->marks.push_back(m);
+  return (int)h->marks.size() - 1;
+}
+
+void tend(Handle* h, int idx, cudaStream_t s) {
+  if (idx < 0) return;
+  Handle::TMark& m = h->marks[idx];
+  cudaEventRecord(m.b, s);
+  m.launches = h->stats.kernel_launches - m.launches;
+  m.bytes = h->stats.algorithmic_bytes - m.bytes;
+}
+
+#define PX_CUDA(h, call)                                                          \
+  do {                                                                            \
+    cudaError_t _e = (call);                                                      \
+    if (_e != cudaSuccess)                                                        \
+      return fail((h), _e == cudaErrorMemoryAllocation ? PX_ERR_NOMEM : PX_ERR_CUDA, \
+                  std::string(#call) + ": " + cudaGetErrorString(_e));            \
+  } while (0)
+
+#define PX_CHECK_LAUNCH(h)                                                        \
+  do {                                                                            \
+    cudaError_t _e = cudaGetLastError();                                          \
+    if (_e != cudaSuccess)                                                        \
+      return fail((h), PX_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+    (h)->stats.kernel_launches++;                                                 \
+  } while (0)
+
+#define PX_TRY(expr)            \
+  do {                          \
+    int _rc = (expr);           \
+    if (_rc != PX_OK) return _rc; \
+  } while (0)
+
+int dalloc(Handle* h, void** p, size_t bytes) {
+  if (bytes == 0) bytes = 8;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess)
+    return fail(h, e == cudaErrorMemoryAllocation ? PX_ERR_NOMEM : PX_ERR_CUDA,
+                "cudaMalloc(" + std::to_string(bytes) + " B): " + cudaGetErrorString(e));
+  h->allocs.push_back(*p);
+  return PX_OK;
+}
+
+template <typename T>
+int dalloc_t(Handle* h, T** p, size_t count) {
+  return dalloc(h, reinterpret_cast<void**>(p), count * sizeof(T));
+}
+
+inline dim3 grid1(size_t n, int B, int nt = 256) {
+  size_t blocks = (n + nt - 1) / nt;
+  return dim3((unsigned)blocks, (unsigned)B);
+}
+
+inline dim3 grid_stride(size_t n, int B) {
+  size_t blocks = std::min<size_t>((n + 255) / 256, 148 * 16);
+  return dim3((unsigned)std::max<size_t>(blocks, 1), (unsigned)B);
+}
+
+// ---------------------------------------------------------------------------
+// RK4 lanes sweep
+// ---------------------------------------------------------------------------
+
+constexpr int TX2 = 64, TY2 = 16, NT2 = 256;
+constexpr int TX1 = 1024, TY1 = 1, NT1 = 256;
+
+template <int DIM>
+constexpr size_t rk4_smem() {
+  return DIM == 2 ? 4 * (TX2 + 8) * (TY2 + 8) * sizeof(double)
+                  : 4 * (TX1 + 8) * (TY1) * sizeof(double);
+}
+
+template <int DIM, bool ADJ>
+int launch_rk4(Handle* h, const px::RK4Args& a, cudaStream_t s) {
+  constexpr int TX = DIM == 2 ? TX2 : TX1;
+  constexpr int TY = DIM == 2 ? TY2 : TY1;
+  constexpr int NT = DIM == 2 ? NT2 : NT1;
+  constexpr size_t smem = rk4_smem<DIM>();
+  static bool attr_set = false;
+  auto kfn = px::k_rk4_tile<DIM, TX, TY, NT, ADJ>;
+  if (!attr_set) {
+    PX_CUDA(h, cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  const unsigned blocks = (unsigned)(a.tiles_x * a.tiles_y) * (unsigned)a.lanes;
+  kfn<<<blocks, NT, smem, s>>>(a);
+  PX_CHECK_LAUNCH(h);
+  return PX_OK;
+}
+
+// Zero-data RK4 sweep of all local lanes: nsteps fused steps; returns final buffer.
+int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s) {
+  px::RK4Args a{};
+  a.g = adjoint ? h->gadj : h->g;
+  a.z = adjoint ? h->Z : nullptr;
+  a.st = adjoint ? h->AT : h->A;
+  a.h = (h->d.T / h->d.P) / h->d.nsteps;
+  a.nx = h->d.nx;
+  a.ny = h->d.ny;
+  a.lanes = h->L;
+  a.lanes_per_b = h->Pl;
+  const int TX = h->dim == 2 ? TX2 : TX1, TY = h->dim == 2 ? TY2 : TY1;
+  a.tiles_x = (h->d.nx + TX - 1) / TX;
+  a.tiles_y = h->dim == 2 ? (h->d.ny + TY - 1) / TY : 1;
+  double* cur = nullptr;
+  for (int st = 0; st < h->d.nsteps; ++st) {
+    double* out = (cur == h->Y0) ? h->Y1 : h->Y0;
+    a.y_in = cur;
+    a.y_out = out;
+    int rc;
+    if (h->dim == 2)
+      rc = adjoint ? launch_rk4<2, true>(h, a, s) : launch_rk4<2, false>(h, a, s);
+    else
+      rc = adjoint ? launch_rk4<1, true>(h, a, s) : launch_rk4<1, false>(h, a, s);
+    if (rc != PX_OK) return rc;
+    cur = out;
+  }
+  const double bytes_per_point = adjoint ? 40.0 : 24.0;  // y,g,y' (+ z in/out)
+  h->stats.rk4_lane_steps += (uint64_t)h->L * h->d.nsteps;
+  const double bytes = bytes_per_point * (double)h->n * h->L * h->d.nsteps;
+  h->stats.rk4_bytes += bytes;
+  h->stats.algorithmic_bytes += bytes;
+  *final_out = cur;
+  return PX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Chebyshev action over B vectors (batch-strided input)
+// ---------------------------------------------------------------------------
+
+// result <- exp(span·M)·src (+ addend);  pacc += span·φ₁(span·M)·src  (if pacc)
+int cheb_action(Handle* h, const Plan& pl, const px::Stencil5& st, const double* src, long long src_bs,
+                const double* addend, long long add_bs, double* pacc, double** result, cudaStream_t s) {
+  if (!pl.set || pl.krylov) return fail(h, PX_ERR_STATE, "Chebyshev plan not set");
+  const size_t n = h->n;
+  const int B = h->B;
+  const dim3 grid = grid1(n, B);
+  const long long nb = (long long)n;
+  for (int sub = 0; sub < pl.substeps; ++sub) {
+    double* acc = (src == h->ACC[0]) ? h->ACC[1] : h->ACC[0];
+    px::ChebFirstArgs fa{};
+    fa.u0 = src; fa.u0_bstride = src_bs;
+    fa.u1 = h->Wk[0];
+    fa.acc = acc;
+    fa.addend = (sub == pl.substeps - 1) ? addend : nullptr;
+    fa.add_bstride = add_bs;
+    fa.pacc = pacc;
+    fa.st = st;
+    fa.c0 = pl.center; fa.d = pl.scale;
+    fa.b0 = pl.be[0]; fa.b1 = pl.be[1];
+    fa.p0 = pacc ? pl.bp[0] : 0.0; fa.p1 = pacc ? pl.bp[1] : 0.0;
+    fa.nx = h->d.nx; fa.ny = h->d.ny;
+    if (h->dim == 2) px::k_cheb_first<2><<<grid, 256, 0, s>>>(fa);
+    else px::k_cheb_first<1><<<grid, 256, 0, s>>>(fa);
+    PX_CHECK_LAUNCH(h);
+    const double* uprev = src;
+    long long uprev_bs = src_bs;
+    int cur = 0;
+    for (int k = 2; k <= pl.degree; ++k) {
+      int nxt = (cur + 1) % 3;
+      if (h->Wk[nxt] == uprev) nxt = (nxt + 1) % 3;
+      px::ChebTermArgs ta{};
+      ta.ucur = h->Wk[cur]; ta.ucur_bstride = nb;
+      ta.uprev = uprev; ta.uprev_bstride = uprev_bs;
+      ta.unext = h->Wk[nxt];
+      ta.acc = acc;
+      ta.pacc = pacc;
+      ta.st = st;
+      ta.c0 = pl.center; ta.two_over_d = 2.0 / pl.scale; ta.sigma = (double)pl.sigma;
+      ta.bk = pl.be[k]; ta.pk = pacc ? pl.bp[k] : 0.0;
+      ta.nx = h->d.nx; ta.ny = h->d.ny;
+      if (h->dim == 2) px::k_cheb_term<2><<<grid, 256, 0, s>>>(ta);
+      else px::k_cheb_term<1><<<grid, 256, 0, s>>>(ta);
+      PX_CHECK_LAUNCH(h);
+      uprev = h->Wk[cur]; uprev_bs = nb;
+      cur = nxt;
+    }
+    src = acc;
+    src_bs = nb;
+  }
+  const uint64_t terms = (uint64_t)pl.substeps * pl.degree * B;
+  h->stats.exp_terms += terms;
+  const double bpp = pacc ? 56.0 : 40.0;
+  const double bytes = bpp * (double)n * terms;
+  h->stats.exp_bytes += bytes;
+  h->stats.algorithmic_bytes += bytes;
+  *result = const_cast<double*>(src);
+  return PX_OK;
+}
+
+int exp_action(Handle* h, int slot, const px::Stencil5& st, const double* src, long long src_bs,
+               const double* addend, long long add_bs, double* pacc, double** result, cudaStream_t s) {
+  const Plan& pl = h->plans[slot];
+  if (!pl.set) return fail(h, PX_ERR_STATE, "exp-action plan slot " + std::to_string(slot) + " not set");
+  if (pl.krylov) {
+    PX_TRY(px::krylov_action(h->kw, pl.span / pl.substeps, pl.substeps, h->d.krylov_m, st, src, src_bs,
+                             addend, add_bs, pacc, h->ACC, h->B, h->d.nx, h->d.ny, h->dim, result, s,
+                             &h->stats));
+    if (cudaGetLastError() != cudaSuccess) return fail(h, PX_ERR_CUDA, "krylov launch failed");
+    return PX_OK;
+  }
+  return cheb_action(h, pl, st, src, src_bs, addend, add_bs, pacc, result, s);
+}
+
+int axpby(Handle* h, double* out, long long obs, const double* x, long long xbs, double alpha,
+          const double* y, long long ybs, double beta, cudaStream_t s) {
+  px::k_axpby<<<grid_stride(h->n, h->B), 256, 0, s>>>(out, obs, x, xbs, alpha, y, ybs, beta, h->n);
+  PX_CHECK_LAUNCH(h);
+  return PX_OK;
+}
+
+int project(Handle* h, double* grad, const double* F, long long Fbs, double alpha, double beta,
+            cudaStream_t s) {
+  const int rx = h->rows_x;
+  if (rx <= 8)
+    px::k_project_rows<8><<<dim3(h->d.ny, h->B), 256, 0, s>>>(h->R, F, Fbs, h->tx, rx, h->d.nx, h->d.ny);
+  else if (rx <= 16)
+    px::k_project_rows<16><<<dim3(h->d.ny, h->B), 256, 0, s>>>(h->R, F, Fbs, h->tx, rx, h->d.nx, h->d.ny);
+  else if (rx <= 32)
+    px::k_project_rows<32><<<dim3(h->d.ny, h->B), 256, 0, s>>>(h->R, F, Fbs, h->tx, rx, h->d.nx, h->d.ny);
+  else
+    px::k_project_rows<64><<<dim3(h->d.ny, h->B), 256, 0, s>>>(h->R, F, Fbs, h->tx, rx, h->d.nx, h->d.ny);
+  PX_CHECK_LAUNCH(h);
+  px::k_project_cols<<<dim3(h->K, h->B), 256, 0, s>>>(grad, h->R, h->ty, h->ix, h->iy, rx, h->K,
+                                                      h->d.ny, alpha, beta);
+  PX_CHECK_LAUNCH(h);
+  return PX_OK;
+}
+
+int apply_plus_control(Handle* h, double* out, const double* x, long long xbs, const px::Stencil5& st,
+                       bool with_control, cudaStream_t s) {
+  const dim3 grid = grid1(h->n, h->B);
+  if (h->dim == 2)
+    px::k_apply_plus_control<2><<<grid, 256, 0, s>>>(out, x, xbs, st, with_control ? h->ctrl : nullptr,
+                                                     h->tx, h->ty, h->ix, h->iy, h->K, h->d.nx, h->d.ny);
+  else
+    px::k_apply_plus_control<1><<<grid, 256, 0, s>>>(out, x, xbs, st, with_control ? h->ctrl : nullptr,
+                                                     h->tx, h->ty, h->ix, h->iy, h->K, h->d.nx, h->d.ny);
+  PX_CHECK_LAUNCH(h);
+  return PX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Linear sweeps
+// ---------------------------------------------------------------------------
+
+int direct_linear(Handle* h, cudaStream_t s) {
+  const long long nb = (long long)h->n;
+  const long long lane_bs = (long long)h->Pl * nb;  // stride between batch members in lanes
+  // g = A·u0 + f  (u0 shared by all members)
+  PX_TRY(apply_plus_control(h, h->g, h->u0, 0, h->A, true, s));
+  const double* vend = nullptr;
+  int tm = tbegin(h, PX_PHASE_RK4_DIRECT, s);
+  PX_TRY(rk4_sweep(h, false, &vend, s));
+  tend(h, tm, s);
+  h->vend = vend;
+  tm = tbegin(h, PX_PHASE_EXP_DIRECT, s);
+  const bool bnd = (h->d.flags & PX_FLAG_BOUNDARY_STATES) && h->UBND;
+  const long long ubs = (long long)(h->d.P + 1) * nb;
+  if (bnd) {
+    PX_TRY(axpby(h, h->UBND, ubs, h->u0, 0, 1.0, nullptr, 0, 0.0, s));
+  }
+  // summed-chain carry over the local block
+  const double* D = vend;  // lane p0 of each member
+  long long D_bs = lane_bs;
+  if (bnd) PX_TRY(axpby(h, h->UBND + nb, ubs, D, D_bs, 1.0, h->u0, 0, 1.0, s));
+  for (int q = 1; q < h->Pl; ++q) {
+    double* res = nullptr;
+    PX_TRY(exp_action(h, PX_PLAN_SLICE, h->A, D, D_bs, vend + (size_t)q * h->n, lane_bs, nullptr, &res, s));
+    D = res;
+    D_bs = nb;
+    if (bnd) PX_TRY(axpby(h, h->UBND + (size_t)(q + 1) * h->n, ubs, D, D_bs, 1.0, h->u0, 0, 1.0, s));
+  }
+  if (h->d.p_end < h->d.P) {
+    double* res = nullptr;
+    PX_TRY(exp_action(h, PX_PLAN_LONG_DIRECT, h->A, D, D_bs, nullptr, 0, nullptr, &res, s));
+    D = res;
+    D_bs = nb;
+  }
+  PX_TRY(axpby(h, h->UT, nb, D, D_bs, 1.0, nullptr, 0, 0.0, s));
+  tend(h, tm, s);
+  return PX_OK;
+}
+
+int adjoint_linear(Handle* h, cudaStream_t s) {
+  const long long nb = (long long)h->n;
+  const long long lane_bs = (long long)h->Pl * nb;
+  const double* wend = nullptr;
+  int tm = tbegin(h, PX_PHASE_RK4_ADJOINT, s);
+  PX_TRY(rk4_sweep(h, true, &wend, s));
+  tend(h, tm, s);
+  h->wend = wend;
+  tm = tbegin(h, PX_PHASE_EXP_ADJOINT, s);
+  // G partial <- Σ_p z_p
+  px::k_lane_sum<<<grid_stride(h->n, h->B), 256, 0, s>>>(h->G, h->Z, h->Pl, h->n);
+  PX_CHECK_LAUNCH(h);
+  const double* C = wend + (size_t)(h->Pl - 1) * h->n;
+  long long C_bs = lane_bs;
+  for (int q = h->Pl - 2; q >= 0; --q) {
+    double* res = nullptr;
+    PX_TRY(exp_action(h, PX_PLAN_SLICE, h->AT, C, C_bs, wend + (size_t)q * h->n, lane_bs, h->G, &res, s));
+    C = res;
+    C_bs = nb;
+  }
+  if (h->d.p_begin > 0) {
+    double* res = nullptr;
+    PX_TRY(exp_action(h, PX_PLAN_LONG_ADJOINT, h->AT, C, C_bs, nullptr, 0, h->G, &res, s));
+    C = res;
+    C_bs = nb;
+  }
+  PX_TRY(axpby(h, h->QDAG0, nb, C, C_bs, 1.0, nullptr, 0, 0.0, s));
+  tend(h, tm, s);
+  tm = tbegin(h, PX_PHASE_OTHER, s);
+  PX_TRY(project(h, h->GRAD, h->G, nb, 1.0, 0.0, s));
+  tend(h, tm, s);
+  return PX_OK;
+}
+
+int finish_direct_impl(Handle* h, cudaStream_t s) {
+  const long long nb = (long long)h->n;
+  const int tm = tbegin(h, PX_PHASE_OTHER, s);
+  if (h->d.kind == PX_KIND_ADVDIFF) {
+    // u(T) = u0 + Σ carries
+    PX_TRY(axpby(h, h->UT, nb, h->UT, nb, 1.0, h->u0, 0, 1.0, s));
+  }
+  PX_TRY(axpby(h, h->QT, nb, h->UT, nb, 1.0, h->ut, 0, -1.0, s));
+  px::k_sumsq_partial<<<dim3(h->red_blocks, h->B), 256, 0, s>>>(h->partial, h->QT, h->n);
+  PX_CHECK_LAUNCH(h);
+  px::k_finalize_sum<<<h->B, 256, 0, s>>>(h->J, h->partial, h->red_blocks, 0.5, h->nonfinite);
+  PX_CHECK_LAUNCH(h);
+  if (h->d.kind == PX_KIND_ADVDIFF) PX_TRY(apply_plus_control(h, h->gadj, h->QT, nb, h->AT, false, s));
+  tend(h, tm, s);
+  return PX_OK;
+}
+
+int finish_adjoint_impl(Handle* h, cudaStream_t s) {
+  const long long nb = (long long)h->n;
+  const int tm = tbegin(h, PX_PHASE_OTHER, s);
+  PX_TRY(axpby(h, h->QDAG0, nb, h->QDAG0, nb, 1.0, h->QT, nb, 1.0, s));
+  PX_TRY(axpby(h, h->G, nb, h->G, nb, 1.0, h->QT, nb, h->d.T, s));
+  PX_TRY(project(h, h->GRAD, h->QT, nb, h->d.T, 1.0, s));
+  tend(h, tm, s);
+  return PX_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+
+extern "C" {
+
+int px_abi_version(void) { return PX_ABI_VERSION; }
+
+const char* px_build_info(void) {
+  return "paraexp sm_100a fp64 (RK4 tile/halo-4 fused stages, Chebyshev fused recurrence, "
+         "Arnoldi CGS2, Burgers serial sweep)";
+}
+
+const char* px_last_error(const void* handle) {
+  const Handle* h = static_cast<const Handle*>(handle);
+  if (h && !h->err.empty()) return h->err.c_str();
+  return g_last_error.c_str();
+}
+
+int px_create(const px_problem_desc* desc, void** out_handle) {
+  if (!desc || !out_handle) return fail(nullptr, PX_ERR_ARG, "null argument");
+  const px_problem_desc& d = *desc;
+  if (d.nx < 3 || d.ny < 1 || (d.ny > 1 && d.ny < 3)) return fail(nullptr, PX_ERR_ARG, "bad grid");
+  if (d.P < 1 || d.nsteps < 1 || d.batch < 1 || d.K < 1) return fail(nullptr, PX_ERR_ARG, "bad sizes");
+  if (d.p_begin < 0 || d.p_end > d.P || d.p_begin >= d.p_end)
+    return fail(nullptr, PX_ERR_ARG, "bad slice block");
+  if (!(d.T > 0)) return fail(nullptr, PX_ERR_ARG, "T must be positive");
+  if (d.kind != PX_KIND_ADVDIFF && d.kind != PX_KIND_BURGERS) return fail(nullptr, PX_ERR_ARG, "bad kind");
+  if (d.kind == PX_KIND_BURGERS && d.ny != 1) return fail(nullptr, PX_ERR_ARG, "Burgers path is 1D");
+  if (d.expaction == PX_EXP_KRYLOV && (d.krylov_m < 2 || d.krylov_m > px::KRYLOV_MAX_M))
+    return fail(nullptr, PX_ERR_ARG, "krylov_m out of range");
+  if (d.basis_rows_x < 1 || d.basis_rows_x > 64 || d.basis_rows_y < 1)
+    return fail(nullptr, PX_ERR_ARG, "bad basis table sizes");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(nullptr, PX_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+
+  Handle* h = new Handle();
+  h->d = d;
+  cudaGetDevice(&h->device);
+  h->dim = d.ny == 1 ? 1 : 2;
+  h->n = (size_t)d.nx * d.ny;
+  h->B = d.batch;
+  h->K = d.K;
+  h->Pl = d.p_end - d.p_begin;
+  h->L = h->B * h->Pl;
+  h->rows_x = d.basis_rows_x;
+  h->rows_y = d.basis_rows_y;
+  h->A = {d.stencil[0], d.stencil[1], d.stencil[2], d.stencil[3], d.stencil[4]};
+  h->AT = {d.stencil[0], d.stencil[2], d.stencil[1], d.stencil[4], d.stencil[3]};
+  const size_t n = h->n, B = h->B;
+  int rc = PX_OK;
+  auto A = [&](double** p, size_t cnt) { if (rc == PX_OK) rc = dalloc_t(h, p, cnt); };
+  A(&h->u0, n);
+  A(&h->ut, n);
+  A(&h->ctrl, B * h->K);
+  A(&h->tx, (size_t)h->rows_x * d.nx);
+  A(&h->ty, (size_t)h->rows_y * d.ny);
+  if (rc == PX_OK) rc = dalloc_t(h, &h->ix, h->K);
+  if (rc == PX_OK) rc = dalloc_t(h, &h->iy, h->K);
+  A(&h->UT, B * n);
+  A(&h->QT, B * n);
+  A(&h->QDAG0, B * n);
+  A(&h->G, B * n);
+  A(&h->J, B);
+  A(&h->GRAD, B * h->K);
+  A(&h->R, B * h->rows_x * d.ny);
+  h->red_blocks = (int)std::min<size_t>((n + 255) / 256, 1024);
+  A(&h->partial, B * h->red_blocks);
+  if (rc == PX_OK) rc = dalloc_t(h, &h->nonfinite, 1);
+  for (int i = 0; i < 3; ++i) A(&h->Wk[i], B * n);
+  for (int i = 0; i < 2; ++i) A(&h->ACC[i], B * n);
+  if (d.kind == PX_KIND_ADVDIFF) {
+    A(&h->g, B * n);
+    A(&h->gadj, B * n);
+    A(&h->Y0, (size_t)h->L * n);
+    A(&h->Y1, (size_t)h->L * n);
+    A(&h->Z, (size_t)h->L * n);
+    if ((d.flags & PX_FLAG_BOUNDARY_STATES) && d.p_begin == 0 && d.p_end == d.P)
+      A(&h->UBND, B * (size_t)(d.P + 1) * n);
+  } else {
+    const size_t S = (size_t)d.P * d.nsteps;
+    A(&h->traj, (S + 1) * B * n);
+    A(&h->ubar, (size_t)d.P * B * n);
+    h->bounds_blocks = (int)std::min<size_t>(((size_t)d.P * B * n + 255) / 256, 1024);
+    A(&h->bpart, 3 * (size_t)h->bounds_blocks);
+    A(&h->bounds, 3);
+    A(&h->Y0, (size_t)h->L * n);
+    A(&h->Y1, (size_t)h->L * n);
+    A(&h->Z, (size_t)h->L * n);
+  }
+  if (rc == PX_OK && d.expaction == PX_EXP_KRYLOV) rc = px::krylov_alloc(h->kw, d.krylov_m, n, B, &g_last_error);
+  if (rc != PX_OK) {
+    std::string msg = g_last_error;
+    px_destroy(h);
+    g_last_error = msg;
+    return rc;
+  }
+  if (cudaMemset(h->nonfinite, 0, sizeof(int)) != cudaSuccess) {
+    px_destroy(h);
+    return fail(nullptr, PX_ERR_CUDA, "memset failed");
+  }
+  *out_handle = h;
+  return PX_OK;
+}
+
+void px_destroy(void* handle) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return;
+  for (void* p : h->allocs) cudaFree(p);
+  for (auto& m : h->marks) { cudaEventDestroy(m.a); cudaEventDestroy(m.b); }
+  for (auto e : h->event_pool) cudaEventDestroy(e);
+  px::krylov_free(h->kw);
+  delete h;
+}
+
+int px_set_basis(void* handle, const double* tx, const double* ty, const int* ix, const int* iy) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !tx || !ty || !ix || !iy) return fail(h, PX_ERR_ARG, "null argument");
+  for (int k = 0; k < h->K; ++k)
+    if (ix[k] < 0 || ix[k] >= h->rows_x || iy[k] < 0 || iy[k] >= h->rows_y)
+      return fail(h, PX_ERR_ARG, "basis index out of range");
+  PX_CUDA(h, cudaMemcpy(h->tx, tx, sizeof(double) * h->rows_x * h->d.nx, cudaMemcpyHostToDevice));
+  PX_CUDA(h, cudaMemcpy(h->ty, ty, sizeof(double) * h->rows_y * h->d.ny, cudaMemcpyHostToDevice));
+  PX_CUDA(h, cudaMemcpy(h->ix, ix, sizeof(int) * h->K, cudaMemcpyHostToDevice));
+  PX_CUDA(h, cudaMemcpy(h->iy, iy, sizeof(int) * h->K, cudaMemcpyHostToDevice));
+  h->basis_set = true;
+  return PX_OK;
+}
+
+int px_set_cheb_plan(void* handle, int slot, const px_cheb_plan* p) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !p) return fail(h, PX_ERR_ARG, "null argument");
+  if (slot < 0 || slot >= PX_PLAN_COUNT) return fail(h, PX_ERR_ARG, "bad plan slot");
+  if (p->substeps < 1 || p->degree < 1 || !(p->scale > 0) || (p->sigma != 1 && p->sigma != -1) ||
+      !p->coef_exp)
+    return fail(h, PX_ERR_ARG, "bad Chebyshev plan");
+  Plan& pl = h->plans[slot];
+  pl.set = true;
+  pl.krylov = false;
+  pl.span = p->span;
+  pl.substeps = p->substeps;
+  pl.degree = p->degree;
+  pl.center = p->center;
+  pl.scale = p->scale;
+  pl.sigma = p->sigma;
+  pl.be.assign(p->coef_exp, p->coef_exp + p->degree + 1);
+  if (p->coef_phi) pl.bp.assign(p->coef_phi, p->coef_phi + p->degree + 1);
+  else pl.bp.assign(p->degree + 1, 0.0);
+  return PX_OK;
+}
+
+int px_set_krylov_plan(void* handle, int slot, double span, int substeps) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return fail(h, PX_ERR_ARG, "null handle");
+  if (slot < 0 || slot >= PX_PLAN_COUNT) return fail(h, PX_ERR_ARG, "bad plan slot");
+  if (h->d.expaction != PX_EXP_KRYLOV) return fail(h, PX_ERR_ARG, "handle not created for Krylov");
+  if (substeps < 1 || !(span > 0)) return fail(h, PX_ERR_ARG, "bad Krylov plan");
+  Plan& pl = h->plans[slot];
+  pl.set = true;
+  pl.krylov = true;
+  pl.span = span;
+  pl.substeps = substeps;
+  pl.degree = h->d.krylov_m;
+  return PX_OK;
+}
+
+int px_set_inputs(void* handle, const double* u0, const double* u_target, const double* ctrl, int mem,
+                  void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !u0 || !u_target || !ctrl) return fail(h, PX_ERR_ARG, "null argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const cudaMemcpyKind kind = mem == PX_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  PX_CUDA(h, cudaMemcpyAsync(h->u0, u0, sizeof(double) * h->n, kind, s));
+  PX_CUDA(h, cudaMemcpyAsync(h->ut, u_target, sizeof(double) * h->n, kind, s));
+  PX_CUDA(h, cudaMemcpyAsync(h->ctrl, ctrl, sizeof(double) * h->B * h->K, kind, s));
+  h->inputs_set = true;
+  h->stage = 0;
+  return PX_OK;
+}
+
+int px_direct(void* handle, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return fail(h, PX_ERR_ARG, "null handle");
+  if (!h->basis_set || !h->inputs_set) return fail(h, PX_ERR_STATE, "basis/inputs not set");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int rc;
+  if (h->d.kind == PX_KIND_ADVDIFF) {
+    if (h->Pl > 1 && !h->plans[PX_PLAN_SLICE].set) return fail(h, PX_ERR_STATE, "slice plan not set");
+    if (h->d.p_end < h->d.P && !h->plans[PX_PLAN_LONG_DIRECT].set)
+      return fail(h, PX_ERR_STATE, "long-span direct plan not set");
+    rc = direct_linear(h, s);
+  } else {
+    px::BurgersDirectArgs a{};
+    a.u0 = h->u0; a.ctrl = h->ctrl; a.tx = h->tx; a.ix = h->ix; a.K = h->K;
+    a.traj = h->traj; a.ubar = h->ubar; a.UT = h->UT;
+    a.bpart = h->bpart; a.bounds = h->bounds; a.bounds_blocks = h->bounds_blocks;
+    a.D = h->d.D; a.hx = h->d.hx; a.h = (h->d.T / h->d.P) / h->d.nsteps;
+    a.nx = h->d.nx; a.B = h->B; a.P = h->d.P; a.nsteps = h->d.nsteps;
+    const int tm = tbegin(h, PX_PHASE_RK4_DIRECT, s);
+    rc = px::burgers_direct(a, s, &h->stats);
+    tend(h, tm, s);
+    if (rc != PX_OK) return fail(h, rc, "Burgers direct sweep failed: " + std::string(cudaGetErrorString(cudaGetLastError())));
+  }
+  if (rc == PX_OK) h->stage = 1;
+  return rc;
+}
+
+int px_finish_direct(void* handle, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return fail(h, PX_ERR_ARG, "null handle");
+  if (h->stage != 1) return fail(h, PX_ERR_STATE, "px_finish_direct before px_direct");
+  int rc = finish_direct_impl(h, static_cast<cudaStream_t>(stream));
+  if (rc == PX_OK) h->stage = 2;
+  return rc;
+}
+
+int px_set_adjoint_terminal(void* handle, const double* qdag_T, int mem, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !qdag_T) return fail(h, PX_ERR_ARG, "null argument");
+  if (!h->basis_set) return fail(h, PX_ERR_STATE, "basis not set");
+  if (h->d.kind == PX_KIND_BURGERS && h->stage < 1)
+    return fail(h, PX_ERR_STATE, "Burgers adjoint needs the direct trajectory (px_direct)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const cudaMemcpyKind kind = mem == PX_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  PX_CUDA(h, cudaMemcpyAsync(h->QT, qdag_T, sizeof(double) * h->B * h->n, kind, s));
+  if (h->d.kind == PX_KIND_ADVDIFF)
+    PX_TRY(apply_plus_control(h, h->gadj, h->QT, (long long)h->n, h->AT, false, s));
+  h->stage = 2;
+  return PX_OK;
+}
+
+int px_adjoint(void* handle, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return fail(h, PX_ERR_ARG, "null handle");
+  if (h->stage != 2) return fail(h, PX_ERR_STATE, "px_adjoint before px_finish_direct");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int rc;
+  if (h->d.kind == PX_KIND_ADVDIFF) {
+    if (h->d.p_begin > 0 && !h->plans[PX_PLAN_LONG_ADJOINT].set)
+      return fail(h, PX_ERR_STATE, "long-span adjoint plan not set");
+    rc = adjoint_linear(h, s);
+  } else {
+    const Plan& pl = h->plans[PX_PLAN_FROZEN];
+    if (!pl.set || pl.krylov) return fail(h, PX_ERR_STATE, "frozen-operator plan not set");
+    px::BurgersAdjointArgs a{};
+    a.traj = h->traj; a.ubar = h->ubar; a.QT = h->QT;
+    a.W0 = h->Y0; a.W1 = h->Y1; a.Z = h->Z;
+    a.G = h->G; a.QDAG0 = h->QDAG0;
+    a.Wk[0] = h->Wk[0]; a.Wk[1] = h->Wk[1]; a.Wk[2] = h->Wk[2];
+    a.ACC[0] = h->ACC[0]; a.ACC[1] = h->ACC[1];
+    a.D = h->d.D; a.hx = h->d.hx; a.h = (h->d.T / h->d.P) / h->d.nsteps;
+    a.nx = h->d.nx; a.B = h->B; a.P = h->d.P; a.nsteps = h->d.nsteps;
+    a.p_begin = h->d.p_begin; a.p_end = h->d.p_end;
+    a.substeps = pl.substeps; a.degree = pl.degree; a.center = pl.center; a.scale = pl.scale;
+    a.sigma = pl.sigma; a.be = pl.be.data(); a.bp = pl.bp.data();
+    const int tm = tbegin(h, PX_PHASE_RK4_ADJOINT, s);
+    rc = px::burgers_adjoint(a, s, &h->stats, &h->wend);
+    tend(h, tm, s);
+    if (rc != PX_OK) return fail(h, rc, "Burgers adjoint sweep failed");
+    rc = project(h, h->GRAD, h->G, (long long)h->n, 1.0, 0.0, s);
+  }
+  if (rc == PX_OK) h->stage = 3;
+  return rc;
+}
+
+int px_finish_adjoint(void* handle, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return fail(h, PX_ERR_ARG, "null handle");
+  if (h->stage != 3) return fail(h, PX_ERR_STATE, "px_finish_adjoint before px_adjoint");
+  int rc = finish_adjoint_impl(h, static_cast<cudaStream_t>(stream));
+  if (rc == PX_OK) h->stage = 4;
+  return rc;
+}
+
+int px_gradient(void* handle, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return fail(h, PX_ERR_ARG, "null handle");
+  if (h->d.kind != PX_KIND_ADVDIFF) return fail(h, PX_ERR_ARG, "px_gradient: linear testbed only");
+  PX_TRY(px_direct(handle, stream));
+  PX_TRY(px_finish_direct(handle, stream));
+  PX_TRY(px_adjoint(handle, stream));
+  PX_TRY(px_finish_adjoint(handle, stream));
+  return PX_OK;
+}
+
+int px_buffer(void* handle, int field, double** dev_ptr, size_t* count) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !dev_ptr || !count) return fail(h, PX_ERR_ARG, "null argument");
+  const size_t Bn = (size_t)h->B * h->n;
+  switch (field) {
+    case PX_FIELD_J: *dev_ptr = h->J; *count = h->B; break;
+    case PX_FIELD_GRAD: *dev_ptr = h->GRAD; *count = (size_t)h->B * h->K; break;
+    case PX_FIELD_UT: *dev_ptr = h->UT; *count = Bn; break;
+    case PX_FIELD_QDAG0: *dev_ptr = h->QDAG0; *count = Bn; break;
+    case PX_FIELD_G: *dev_ptr = h->G; *count = Bn; break;
+    case PX_FIELD_UBND:
+      if (!h->UBND) return fail(h, PX_ERR_STATE, "boundary states not enabled");
+      *dev_ptr = h->UBND; *count = Bn * (h->d.P + 1); break;
+    case PX_FIELD_FROZEN_BOUNDS:
+      if (!h->bounds) return fail(h, PX_ERR_STATE, "no frozen bounds (linear testbed)");
+      *dev_ptr = h->bounds; *count = 3; break;
+    case PX_FIELD_VEND:
+      if (!h->vend) return fail(h, PX_ERR_STATE, "direct lanes not computed");
+      *dev_ptr = const_cast<double*>(h->vend); *count = (size_t)h->L * h->n; break;
+    case PX_FIELD_WEND:
+      if (!h->wend) return fail(h, PX_ERR_STATE, "adjoint lanes not computed");
+      *dev_ptr = const_cast<double*>(h->wend); *count = (size_t)h->L * h->n; break;
+    case PX_FIELD_TRAJ:
+      if (!h->traj) return fail(h, PX_ERR_STATE, "no trajectory (linear testbed)");
+      *dev_ptr = h->traj; *count = ((size_t)h->d.P * h->d.nsteps + 1) * Bn; break;
+    default: return fail(h, PX_ERR_ARG, "bad field");
+  }
+  return PX_OK;
+}
+
+int px_get(void* handle, int field, double* dst, size_t count, int mem, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  double* src = nullptr;
+  size_t have = 0;
+  PX_TRY(px_buffer(handle, field, &src, &have));
+  if (count > have) return fail(h, PX_ERR_ARG, "count exceeds field size");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const cudaMemcpyKind kind = mem == PX_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  PX_CUDA(h, cudaMemcpyAsync(dst, src, sizeof(double) * count, kind, s));
+  if (mem == PX_MEM_HOST) PX_CUDA(h, cudaStreamSynchronize(s));
+  if (field == PX_FIELD_J && mem == PX_MEM_HOST) {
+    int flag = 0;
+    PX_CUDA(h, cudaMemcpy(&flag, h->nonfinite, sizeof(int), cudaMemcpyDeviceToHost));
+    if (flag) {
+      cudaMemset(h->nonfinite, 0, sizeof(int));
+      return fail(h, PX_ERR_NONFINITE, "non-finite objective (state blew up)");
+    }
+  }
+  return PX_OK;
+}
+
+int px_set_timing(void* handle, int enable) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return fail(h, PX_ERR_ARG, "null handle");
+  h->timing = enable != 0;
+  return PX_OK;
+}
+
+int px_get_timing(void* handle, px_timing* out) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !out) return fail(h, PX_ERR_ARG, "null argument");
+  for (auto& m : h->marks) {
+    PX_CUDA(h, cudaEventSynchronize(m.b));
+    float ms = 0.f;
+    PX_CUDA(h, cudaEventElapsedTime(&ms, m.a, m.b));
+    h->tacc.ms[m.phase] += ms;
+    h->tacc.launches[m.phase] += m.launches;
+    h->tacc.bytes[m.phase] += m.bytes;
+    h->event_pool.push_back(m.a);
+    h->event_pool.push_back(m.b);
+  }
+  h->marks.clear();
+  *out = h->tacc;
+  h->tacc = px_timing{};
+  return PX_OK;
+}
+
+int px_get_stats(void* handle, px_stats* out) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !out) return fail(h, PX_ERR_ARG, "null argument");
+  *out = h->stats;
+  return PX_OK;
+}
+
+int px_reset_stats(void* handle) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return fail(h, PX_ERR_ARG, "null handle");
+  h->stats = px_stats{};
+  return PX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,304 @@
+"""GPU engine: one native handle per (problem, rank), driven phase by phase.
+
+Replaces the reference's worker transport for this path (`workers.py:298-346`,
+Python threads or forked processes exchanging n-vectors): the P time slices of a
+rank run as one batched kernel grid on its GPU, the neighbour chains become one
+summed-chain carry per sweep, and the only inter-rank exchange is an allreduce
+of the u(T) partials (direct) and of the q†(0)/∫q†/gradient partials (adjoint),
+done here with ``torch.distributed`` (NCCL over NVLink) on the handle's device
+buffers when ``world > 1``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import ConfigError, IntegrationFailure, NativeUnavailable
+from .expaction import ChebPlan, ChebyshevConfig, KrylovConfig, KrylovPlan, plan_chebyshev, plan_krylov
+from .partition import partition_equidistant, rank_block, slice_steps
+from .problems import ADVECTION_DIFFUSION, frozen_region_from_bounds
+from .systems import System
+
+
+def _torch():
+    try:
+        import torch
+        return torch
+    except Exception:  # pragma: no cover - torch is in the image
+        return None
+
+
+def current_stream_handle() -> int:
+    """The caller's current CUDA stream (torch's), or 0 (legacy default stream)."""
+    torch = _torch()
+    if torch is not None and torch.cuda.is_available():
+        return int(torch.cuda.current_stream().cuda_stream)
+    return 0
+
+
+class _DeviceView:
+    """__cuda_array_interface__ over a native device buffer (for torch/NCCL)."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {
+            "shape": (count,), "typestr": "<f8", "data": (ptr, False), "version": 3, "strides": None,
+        }
+
+
+@dataclass(frozen=True)
+class EngineSpec:
+    system: System
+    P: int
+    dt: float
+    expaction: ChebyshevConfig | KrylovConfig
+    batch: int = 1
+    rank: int = 0
+    world: int = 1
+    boundary_states: bool = False
+
+    @property
+    def nsteps(self) -> int:
+        return slice_steps(self.system.spec.T / self.P, self.dt)
+
+
+class ParaexpEngine:
+    """Owns one ``px_handle``; computes gradients of J = ½‖u(T) − u_target‖²."""
+
+    def __init__(self, spec: EngineSpec):
+        self.spec = spec
+        self.lib = N.load()
+        sysm = spec.system
+        grid = sysm.grid
+        if spec.world > 1 and spec.world > spec.P:
+            raise ConfigError(f"world={spec.world} exceeds P={spec.P} slices")
+        p0, p1 = rank_block(spec.P, spec.rank, spec.world)
+        self.p0, self.p1 = p0, p1
+        self.n = grid.npoints
+        self.B = spec.batch
+        self.K = sysm.basis.K
+        d = N.ProblemDesc()
+        d.kind = N.PX_KIND_ADVDIFF if sysm.spec.kind == ADVECTION_DIFFUSION else N.PX_KIND_BURGERS
+        d.nx, d.ny = grid.nx, grid.ny
+        for i, v in enumerate(sysm.A.as_tuple()):
+            d.stencil[i] = v
+        d.D = sysm.spec.D
+        d.hx = grid.hx
+        d.T = sysm.spec.T
+        d.P = spec.P
+        d.nsteps = spec.nsteps
+        d.p_begin, d.p_end = p0, p1
+        d.batch = spec.batch
+        d.K = self.K
+        d.basis_rows_x = sysm.basis.tx.shape[0]
+        d.basis_rows_y = sysm.basis.ty.shape[0]
+        krylov = isinstance(spec.expaction, KrylovConfig)
+        d.expaction = N.PX_EXP_KRYLOV if krylov else N.PX_EXP_CHEBYSHEV
+        d.krylov_m = spec.expaction.m if krylov else 0
+        d.flags = N.PX_FLAG_BOUNDARY_STATES if spec.boundary_states else 0
+        self._desc = d
+        h = ctypes.c_void_p()
+        N.check(self.lib, self.lib.px_create(ctypes.byref(d), ctypes.byref(h)))
+        self.h = h
+        tx, _a = N.dptr(sysm.basis.tx)
+        ty, _b = N.dptr(sysm.basis.ty)
+        ix, _c = N.iptr(sysm.basis.ix)
+        iy, _d = N.iptr(sysm.basis.iy)
+        N.check(self.lib, self.lib.px_set_basis(h, tx, ty, ix, iy), h)
+        self.plans: dict[int, ChebPlan | KrylovPlan] = {}
+        self._keep = []
+        if sysm.is_linear:
+            region = sysm.region()
+            delta = sysm.spec.T / spec.P
+            if p1 - p0 > 1 or spec.world == 1:
+                self._set_plan(N.PX_PLAN_SLICE, self._plan(region, delta))
+            if p1 < spec.P:
+                self._set_plan(N.PX_PLAN_LONG_DIRECT, self._plan(region, (spec.P - p1) * delta))
+            if p0 > 0:
+                self._set_plan(N.PX_PLAN_LONG_ADJOINT, self._plan(region, p0 * delta))
+
+    # -- plans ---------------------------------------------------------------
+
+    def _plan(self, region, span):
+        cfg = self.spec.expaction
+        if isinstance(cfg, KrylovConfig):
+            return plan_krylov(region, span, cfg)
+        return plan_chebyshev(region, span, cfg)
+
+    def _set_plan(self, slot: int, plan) -> None:
+        self.plans[slot] = plan
+        if isinstance(plan, KrylovPlan):
+            N.check(self.lib, self.lib.px_set_krylov_plan(self.h, slot, plan.span, plan.substeps), self.h)
+            return
+        be, ka = N.dptr(plan.coef_exp)
+        bp, kb = N.dptr(plan.coef_phi)
+        c = N.ChebPlanC(plan.span, plan.substeps, plan.degree, plan.center, plan.scale, plan.sigma, be, bp)
+        N.check(self.lib, self.lib.px_set_cheb_plan(self.h, slot, ctypes.byref(c)), self.h)
+
+    # -- inputs / outputs ----------------------------------------------------
+
+    def set_inputs(self, u0, u_target, ctrl, stream: int | None = None) -> None:
+        """numpy arrays (host) or CUDA torch tensors (device)."""
+        s = current_stream_handle() if stream is None else stream
+        torch = _torch()
+        if torch is not None and isinstance(u0, torch.Tensor) and u0.is_cuda:
+            for t in (u0, u_target, ctrl):
+                if t.dtype != torch.float64 or not t.is_contiguous():
+                    raise ValueError("device inputs must be contiguous float64 tensors")
+            if ctrl.numel() != self.B * self.K or u0.numel() != self.n or u_target.numel() != self.n:
+                raise ValueError("input sizes do not match the problem")
+            rc = self.lib.px_set_inputs(self.h, u0.data_ptr(), u_target.data_ptr(), ctrl.data_ptr(),
+                                        N.PX_MEM_DEVICE, s)
+            self._keep = [u0, u_target, ctrl]
+        else:
+            a = np.ascontiguousarray(u0, dtype=np.float64).ravel()
+            b = np.ascontiguousarray(u_target, dtype=np.float64).ravel()
+            c = np.ascontiguousarray(ctrl, dtype=np.float64).reshape(-1)
+            if a.size != self.n or b.size != self.n or c.size != self.B * self.K:
+                raise ValueError("input sizes do not match the problem")
+            rc = self.lib.px_set_inputs(self.h, a.ctypes.data, b.ctypes.data, c.ctypes.data,
+                                        N.PX_MEM_HOST, s)
+            self._keep = [a, b, c]
+        N.check(self.lib, rc, self.h)
+
+    def field_count(self, field: int) -> int:
+        p = ctypes.c_void_p()
+        cnt = ctypes.c_size_t()
+        N.check(self.lib, self.lib.px_buffer(self.h, field, ctypes.byref(p), ctypes.byref(cnt)), self.h)
+        return int(cnt.value)
+
+    def device_view(self, field: int):
+        """Torch CUDA tensor aliasing a native device buffer (no copy)."""
+        torch = _torch()
+        p = ctypes.c_void_p()
+        cnt = ctypes.c_size_t()
+        N.check(self.lib, self.lib.px_buffer(self.h, field, ctypes.byref(p), ctypes.byref(cnt)), self.h)
+        return torch.as_tensor(_DeviceView(int(p.value), int(cnt.value)), device="cuda")
+
+    def get(self, field: int, stream: int | None = None) -> np.ndarray:
+        s = current_stream_handle() if stream is None else stream
+        cnt = self.field_count(field)
+        out = np.empty(cnt, dtype=np.float64)
+        N.check(self.lib, self.lib.px_get(self.h, field, out.ctypes.data, cnt, N.PX_MEM_HOST, s), self.h,
+                t=self.spec.system.spec.T)
+        return out
+
+    def stats(self) -> dict:
+        st = N.Stats()
+        N.check(self.lib, self.lib.px_get_stats(self.h, ctypes.byref(st)), self.h)
+        return st.as_dict()
+
+    def set_timing(self, enable: bool) -> None:
+        N.check(self.lib, self.lib.px_set_timing(self.h, 1 if enable else 0), self.h)
+
+    def timing(self) -> dict:
+        """Per-phase device time (CUDA events around each sweep phase) since the last call."""
+        t = N.Timing()
+        N.check(self.lib, self.lib.px_get_timing(self.h, ctypes.byref(t)), self.h)
+        return t.as_dict()
+
+    def reset_stats(self) -> None:
+        N.check(self.lib, self.lib.px_reset_stats(self.h), self.h)
+
+    # -- phases --------------------------------------------------------------
+
+    def _allreduce(self, fields, group=None):
+        if self.spec.world == 1:
+            return
+        import torch.distributed as dist
+        for f in fields:
+            dist.all_reduce(self.device_view(f), op=dist.ReduceOp.SUM, group=group)
+
+    # Phase-level entry points (a rank's partial, then the finish after the caller's
+    # reduction). ``run_direct``/``run_adjoint`` chain them with an NCCL allreduce.
+
+    def direct_partial(self, stream: int | None = None) -> None:
+        s = current_stream_handle() if stream is None else stream
+        N.check(self.lib, self.lib.px_direct(self.h, s), self.h)
+
+    def finish_direct(self, stream: int | None = None) -> None:
+        s = current_stream_handle() if stream is None else stream
+        N.check(self.lib, self.lib.px_finish_direct(self.h, s), self.h)
+
+    def adjoint_partial(self, stream: int | None = None) -> None:
+        s = current_stream_handle() if stream is None else stream
+        if not self.spec.system.is_linear:
+            self.plan_frozen(s)
+        N.check(self.lib, self.lib.px_adjoint(self.h, s), self.h)
+
+    def finish_adjoint(self, stream: int | None = None) -> None:
+        s = current_stream_handle() if stream is None else stream
+        N.check(self.lib, self.lib.px_finish_adjoint(self.h, s), self.h)
+
+    def direct_reduce_fields(self) -> list[int]:
+        return [N.PX_FIELD_UT] if self.spec.system.is_linear else []
+
+    @staticmethod
+    def adjoint_reduce_fields(want_fields: bool = True) -> list[int]:
+        return [N.PX_FIELD_GRAD] + ([N.PX_FIELD_QDAG0, N.PX_FIELD_G] if want_fields else [])
+
+    def run_direct(self, stream: int | None = None, group=None) -> None:
+        s = current_stream_handle() if stream is None else stream
+        self.direct_partial(s)
+        self._allreduce(self.direct_reduce_fields(), group)
+        self.finish_direct(s)
+
+    def plan_frozen(self, stream: int | None = None) -> ChebPlan:
+        """Burgers: read the frozen-operator FOV union, plan on the host (cached)."""
+        lo, hi, im = self.get(N.PX_FIELD_FROZEN_BOUNDS, stream)
+        region = frozen_region_from_bounds(float(lo), float(hi), float(im))
+        cfg = self.spec.expaction
+        if not isinstance(cfg, ChebyshevConfig):
+            raise ConfigError("the Burgers frozen adjoint uses the Chebyshev action")
+        plan = plan_chebyshev(region, self.spec.system.spec.T / self.spec.P, cfg)
+        self._set_plan(N.PX_PLAN_FROZEN, plan)
+        return plan
+
+    def run_adjoint(self, stream: int | None = None, group=None, want_fields: bool = True) -> None:
+        s = current_stream_handle() if stream is None else stream
+        self.adjoint_partial(s)
+        self._allreduce(self.adjoint_reduce_fields(want_fields), group)
+        self.finish_adjoint(s)
+
+    def set_adjoint_terminal(self, qdag_T, stream: int | None = None) -> None:
+        s = current_stream_handle() if stream is None else stream
+        a = np.ascontiguousarray(qdag_T, dtype=np.float64).reshape(-1)
+        if a.size != self.B * self.n:
+            raise ValueError("qdag_T must have B·n values")
+        N.check(self.lib, self.lib.px_set_adjoint_terminal(self.h, a.ctypes.data, N.PX_MEM_HOST, s), self.h)
+        self._keep.append(a)
+
+    def gradient(self, stream: int | None = None, group=None, want_fields: bool = True) -> None:
+        """One full direct-adjoint gradient evaluation, enqueued on ``stream``."""
+        s = current_stream_handle() if stream is None else stream
+        if self.spec.world == 1 and self.spec.system.is_linear:
+            N.check(self.lib, self.lib.px_gradient(self.h, s), self.h)
+            return
+        self.run_direct(s, group)
+        self.run_adjoint(s, group, want_fields)
+
+    def results(self, stream: int | None = None) -> dict:
+        J = self.get(N.PX_FIELD_J, stream)
+        if not np.all(np.isfinite(J)):
+            raise IntegrationFailure(self.spec.system.spec.T, "non-finite objective")
+        return {
+            "J": J,
+            "grad": self.get(N.PX_FIELD_GRAD, stream).reshape(self.B, self.K),
+            "uT": self.get(N.PX_FIELD_UT, stream).reshape(self.B, self.n),
+            "qdag0": self.get(N.PX_FIELD_QDAG0, stream).reshape(self.B, self.n),
+            "G": self.get(N.PX_FIELD_G, stream).reshape(self.B, self.n),
+        }
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.px_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

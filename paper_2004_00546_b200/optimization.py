@@ -1,0 +1,206 @@
+"""Reference-facing optimisation API with ``backend="cuda"``.
+
+Mirrors `pkg/src/paradjoint/optimization.py`: ``direct_adjoint_loop``
+(`:154-231`) runs one direct solve plus one adjoint solve and returns
+``LoopResult(J, grad, direct, adjoint, …)``; ``descend`` (`:242-281`) is the
+fixed-step steepest-descent driver with the same non-finite check.
+
+Differences forced by the BASELINE configs: the
+control is a time-constant Fourier-mode field f = Σ c_k φ_k (``f`` holds the
+coefficients, batched as (B, K)); the objective is terminal,
+J = ½‖u(T) − u_target‖² (``q_true`` is u_target); ∂J/∂c_k = ⟨φ_k, ∫q† dt⟩; the
+initial state ``u0`` is passed through (the reference hard-wires q0 = 0,
+`optimization.py:179`). ``algorithm`` is "linear" (Paraexp direct + adjoint,
+advection–diffusion) or "hybrid" (serial direct sweep + Paraexp adjoint with
+frozen linearisation, Burgers). The only backend is "cuda": there is no CPU
+fallback.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .engine import EngineSpec, ParaexpEngine
+from .errors import ConfigError
+from .expaction import ChebyshevConfig, KrylovConfig
+from .partition import RK4Config, TimePartition, partition_equidistant
+from .systems import System
+
+LINEAR = "linear"
+HYBRID = "hybrid"
+ALGORITHMS = (LINEAR, HYBRID)
+BACKENDS = ("cuda",)
+
+
+@dataclass
+class DirectSolution:
+    """u(T) (and, when requested, the boundary states u(T_p))."""
+
+    partition: TimePartition
+    final_state: np.ndarray
+    boundary_states: np.ndarray | None = None
+
+
+@dataclass
+class AdjointSolution:
+    """q†(0) and G = ∫₀ᵀ q† dt (the gradient with respect to a full control field)."""
+
+    partition: TimePartition
+    initial_state: np.ndarray
+    integral: np.ndarray
+
+
+@dataclass
+class LoopResult:
+    J: np.ndarray | float
+    grad: np.ndarray
+    direct: DirectSolution
+    adjoint: AdjointSolution
+    iterations: int = 1
+    seconds: float = 0.0
+    error_history: list[float] = field(default_factory=list)
+    stats: dict = field(default_factory=dict)
+
+
+@dataclass
+class DescentResult:
+    f_final: np.ndarray
+    J_history: list
+    grad_norms: list
+    step_seconds: list[float]
+
+
+def cost(u_T: np.ndarray, u_target: np.ndarray) -> np.ndarray:
+    """J = ½‖u(T) − u_target‖² (unweighted discrete norm, `PAPER.md:149-155`)."""
+    d = np.atleast_2d(u_T) - np.asarray(u_target)
+    return 0.5 * np.sum(d * d, axis=-1)
+
+
+def initial_condition_gradient(adjoint: AdjointSolution) -> np.ndarray:
+    """∂J/∂u0 = q†(0) (`optimization.py:115-117`)."""
+    return adjoint.initial_state
+
+
+_ENGINES: dict = {}
+
+
+def _default_expaction(system: System):
+    return ChebyshevConfig(tol=1e-12)
+
+
+def get_engine(system: System, N: int, rk: RK4Config, expaction, batch: int, rank: int = 0, world: int = 1,
+               boundary_states: bool = False) -> ParaexpEngine:
+    """Cached engine per (problem, partition, numerics, rank): handles own HBM scratch."""
+    key = (system.grid, system.spec, system.basis.K, N, rk.dt, expaction, batch, rank, world, boundary_states)
+    eng = _ENGINES.get(key)
+    if eng is None:
+        eng = ParaexpEngine(EngineSpec(system, N, rk.dt, expaction, batch, rank, world, boundary_states))
+        _ENGINES[key] = eng
+    return eng
+
+
+def release_engines() -> None:
+    for e in _ENGINES.values():
+        e.close()
+    _ENGINES.clear()
+
+
+def _dist_rank_world():
+    try:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            return dist.get_rank(), dist.get_world_size()
+    except Exception:
+        pass
+    return 0, 1
+
+
+def direct_adjoint_loop(
+    system: System,
+    f: np.ndarray,
+    q_true: np.ndarray,
+    algorithm: str = LINEAR,
+    N: int = 1,
+    rk: RK4Config | None = None,
+    expaction: ChebyshevConfig | KrylovConfig | None = None,
+    u0: np.ndarray | None = None,
+    backend: str = "cuda",
+    boundary_states: bool = False,
+    distributed: bool = True,
+) -> LoopResult:
+    """One direct solve plus one adjoint solve, yielding J and ∂J/∂c (`optimization.py:154-231`).
+
+    ``f``: control coefficients (K,) or (B, K); ``q_true``: u_target (n,);
+    ``N``: number of time slices; with ``torch.distributed`` initialised the
+    slices are sharded over the ranks (contiguous blocks) unless
+    ``distributed=False``.
+    """
+    if backend not in BACKENDS:
+        raise ValueError(f"unknown backend {backend!r}; the B200 path provides {BACKENDS}")
+    if algorithm not in ALGORITHMS:
+        raise ValueError(f"unknown algorithm {algorithm!r}")
+    if algorithm == LINEAR and not system.is_linear:
+        raise ValueError("linear algorithm requires a linear testbed")
+    if algorithm == HYBRID and system.is_linear:
+        raise ValueError("the hybrid (serial direct) path is the Burgers testbed's")
+    if rk is None:
+        raise ConfigError("rk: an RK4Config(dt) is required (fixed-step RK4)")
+    expaction = expaction or _default_expaction(system)
+    ctrl = np.atleast_2d(np.asarray(f, dtype=np.float64))
+    B = ctrl.shape[0]
+    if ctrl.shape[1] != system.basis.K:
+        raise ValueError("control coefficient count does not match the basis")
+    u0 = np.zeros(system.n) if u0 is None else np.asarray(u0, dtype=np.float64)
+    rank, world = _dist_rank_world() if distributed else (0, 1)
+    eng = get_engine(system, N, rk, expaction, B, rank, world, boundary_states and world == 1)
+    tick = time.perf_counter()
+    eng.set_inputs(u0, np.asarray(q_true, dtype=np.float64), ctrl)
+    eng.gradient()
+    res = eng.results()
+    part = partition_equidistant(system.spec.T, N)
+    bnd = None
+    if boundary_states and world == 1:
+        from . import _native as NN
+        bnd = eng.get(NN.PX_FIELD_UBND).reshape(B, N + 1, system.n)
+    J = res["J"] if B > 1 or np.ndim(f) > 1 else float(res["J"][0])
+    grad = res["grad"] if B > 1 or np.ndim(f) > 1 else res["grad"][0]
+    return LoopResult(
+        J, grad,
+        DirectSolution(part, res["uT"], bnd),
+        AdjointSolution(part, res["qdag0"], res["G"]),
+        seconds=time.perf_counter() - tick,
+        stats=eng.stats(),
+    )
+
+
+def descend(
+    system: System,
+    f_init: np.ndarray,
+    q_true: np.ndarray,
+    steps: int,
+    lr: float,
+    algorithm: str = LINEAR,
+    N: int = 1,
+    rk: RK4Config | None = None,
+    expaction=None,
+    u0: np.ndarray | None = None,
+    backend: str = "cuda",
+) -> DescentResult:
+    """Fixed-step gradient descent on the control coefficients (`optimization.py:242-281`)."""
+    if lr <= 0:
+        raise ValueError("learning rate must be positive")
+    f = np.array(f_init, dtype=np.float64)
+    J_history, grad_norms, step_seconds = [], [], []
+    for _ in range(steps):
+        loop = direct_adjoint_loop(system, f, q_true, algorithm, N=N, rk=rk, expaction=expaction, u0=u0,
+                                   backend=backend)
+        if not np.all(np.isfinite(loop.J)):
+            raise FloatingPointError("cost became non-finite during descent")
+        J_history.append(loop.J)
+        grad_norms.append(np.linalg.norm(np.atleast_2d(loop.grad), axis=-1))
+        step_seconds.append(loop.seconds)
+        f = f - lr * loop.grad
+    return DescentResult(f, J_history, grad_norms, step_seconds)

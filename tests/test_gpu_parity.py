@@ -1,0 +1,278 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle (same seeded inputs).
+
+Tolerances (BASELINE north_star): final-time and adjoint states ≤ 1e-10 relative L2,
+gradients ≤ 1e-8 relative L2, objectives ≤ 1e-10 relative. Both sides execute the
+same operation sequence (fixed-step RK4, planned Chebyshev/Krylov actions, summed-
+chain scan / blockscan), so differences are rounding-level.
+"""
+
+import numpy as np
+import pytest
+
+from tests.conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    import torch
+    assert torch.cuda.is_available(), "the -m gpu suite must run on a CUDA device"
+    from paper_2004_00546_b200 import _native
+    _native.load()  # fails loudly if the extension is missing
+    yield
+    from paper_2004_00546_b200 import release_engines
+    release_engines()
+
+
+def _plans(c):
+    from paper_2004_00546_b200.expaction import plan_for
+    region = c.system.region()
+    slice_plan = plan_for(region, c.spec.T / c.P, c.expaction)
+    long_plan = lambda span: plan_for(region, span, c.expaction)
+    return slice_plan, long_plan
+
+
+def _oracle_linear(c, world=1, want_boundary=False):
+    from oracle.config_mode import linear_gradient
+    sysm = c.system
+    u0, ut, ctrl = c.inputs()
+    sp, lp = _plans(c)
+    return linear_gradient(c.grid.nx, c.grid.ny, sysm.A.as_tuple(), sysm.basis, c.spec.T, c.P, c.nsteps,
+                           u0, ut, ctrl, sp, lp, lp, formulation="scan" if world == 1 else "blockscan",
+                           world=world, want_boundary=want_boundary)
+
+
+def _gpu_linear(c, boundary=False):
+    from paper_2004_00546_b200 import RK4Config, direct_adjoint_loop
+    u0, ut, ctrl = c.inputs()
+    return direct_adjoint_loop(c.system, ctrl, ut, "linear", N=c.P, rk=RK4Config(c.dt), expaction=c.expaction,
+                               u0=u0, boundary_states=boundary)
+
+
+def _check(loop, ref):
+    B = np.atleast_2d(loop.grad).shape[0]
+    assert rel_l2(loop.direct.final_state, ref.uT) <= 1e-10
+    assert rel_l2(loop.adjoint.initial_state, ref.qdag0) <= 1e-10
+    assert rel_l2(loop.adjoint.integral, ref.G) <= 1e-10
+    assert rel_l2(np.reshape(loop.grad, (B, -1)), ref.grad) <= 1e-8
+    J = np.ravel(loop.J)
+    assert np.max(np.abs(J - ref.J) / np.abs(ref.J)) <= 1e-10
+
+
+def test_config1_full():
+    from paper_2004_00546_b200 import baseline
+    c = baseline(1)
+    _check(_gpu_linear(c), _oracle_linear(c))
+
+
+def test_config1_boundary_states_and_slices():
+    from paper_2004_00546_b200 import baseline
+    c = baseline(1)
+    loop = _gpu_linear(c, boundary=True)
+    ref = _oracle_linear(c, want_boundary=True)
+    assert rel_l2(loop.direct.boundary_states, ref.u_bnd) <= 1e-10
+    for p in range(c.P + 1):
+        assert rel_l2(loop.direct.boundary_states[:, p], ref.u_bnd[:, p]) <= 1e-10
+
+
+def test_every_slice_lane_matches():
+    """Each of the P batched slice solves (lanes) equals the oracle's slice solve."""
+    from paper_2004_00546_b200 import baseline, scaled, _native as N
+    from paper_2004_00546_b200.optimization import get_engine
+    from paper_2004_00546_b200 import RK4Config
+    c = scaled(baseline(5), nx=64, P=8, steps_per_slice=6, K=16)
+    loop = _gpu_linear(c)
+    ref = _oracle_linear(c)
+    eng = get_engine(c.system, c.P, RK4Config(c.dt), c.expaction, c.batch)
+    wend = eng.get(N.PX_FIELD_WEND).reshape(c.batch, c.P, c.n)
+    for p in range(c.P):
+        assert rel_l2(wend[:, p], ref.extras["w_end"]) <= 1e-12
+    _check(loop, ref)
+
+
+def test_config2_full_batch16():
+    from paper_2004_00546_b200 import baseline
+    c = baseline(2)
+    _check(_gpu_linear(c), _oracle_linear(c))
+
+
+def test_config2_descent_two_steps():
+    from oracle.config_mode import linear_gradient
+    from paper_2004_00546_b200 import RK4Config, baseline, descend
+    c = baseline(2)
+    u0, ut, ctrl = c.inputs()
+    res = descend(c.system, ctrl, ut, steps=2, lr=c.lr, N=c.P, rk=RK4Config(c.dt), expaction=c.expaction, u0=u0)
+    sp, _ = _plans(c)
+    f = ctrl.copy()
+    for it in range(2):
+        r = linear_gradient(c.grid.nx, 1, c.system.A.as_tuple(), c.system.basis, c.spec.T, c.P, c.nsteps,
+                            u0, ut, f, sp)
+        assert np.max(np.abs(np.ravel(res.J_history[it]) - r.J) / r.J) <= 1e-10
+        f = f - c.lr * r.grad
+    assert rel_l2(res.f_final, f) <= 1e-8
+    assert np.all(np.ravel(res.J_history[1]) < np.ravel(res.J_history[0]))
+
+
+def test_config3_burgers_full():
+    from oracle.config_mode import burgers_gradient
+    from paper_2004_00546_b200 import RK4Config, baseline, direct_adjoint_loop
+    from paper_2004_00546_b200.expaction import plan_chebyshev
+    from paper_2004_00546_b200.problems import burgers_frozen_region
+    c = baseline(3)
+    u0, ut, ctrl = c.inputs()
+    loop = direct_adjoint_loop(c.system, ctrl, ut, "hybrid", N=c.P, rk=RK4Config(c.dt), expaction=c.expaction,
+                               u0=u0)
+    ref = burgers_gradient(c.grid.nx, c.spec.D, c.system.basis, c.spec.T, c.P, c.nsteps, u0, ut, ctrl,
+                           lambda region, span: plan_chebyshev(region, span, c.expaction),
+                           lambda ub: burgers_frozen_region(ub, c.grid, c.spec.D))
+    _check(loop, ref)
+
+
+def test_config4_krylov_scaled():
+    from paper_2004_00546_b200 import baseline, scaled
+    c = scaled(baseline(4), nx=96, P=12, steps_per_slice=5, K=16)
+    _check(_gpu_linear(c), _oracle_linear(c))
+
+
+def test_config5_scaled():
+    from paper_2004_00546_b200 import baseline, scaled
+    c = scaled(baseline(5), nx=128, P=16, steps_per_slice=8, K=64)
+    _check(_gpu_linear(c), _oracle_linear(c))
+
+
+def test_non_multiple_tile_grid():
+    """Grid sizes that do not divide the 64×16 tile nor the 1024-point 1D tile."""
+    from paper_2004_00546_b200 import baseline, scaled
+    c = scaled(baseline(5), nx=40, P=5, steps_per_slice=3, K=4)
+    _check(_gpu_linear(c), _oracle_linear(c))
+    c1 = scaled(baseline(1), nx=1500, P=3, steps_per_slice=20)
+    _check(_gpu_linear(c1), _oracle_linear(c1))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_blockscan_ranks_emulated(world):
+    """World-`world` sharding on one GPU: ranks run one after another (no rank waits on
+    another), partials are summed as NCCL's allreduce would; equals the oracle blockscan."""
+    import torch
+    from paper_2004_00546_b200 import baseline, scaled, _native as N
+    from paper_2004_00546_b200.engine import EngineSpec, ParaexpEngine
+    c = scaled(baseline(5), nx=64, P=9, steps_per_slice=5, K=16)
+    u0, ut, ctrl = c.inputs()
+    engs = [ParaexpEngine(EngineSpec(c.system, c.P, c.dt, c.expaction, c.batch, r, world)) for r in range(world)]
+    for e in engs:
+        e.set_inputs(u0, ut, ctrl)
+        e.direct_partial()
+
+    def allreduce(fields):
+        for f in fields:
+            views = [e.device_view(f) for e in engs]
+            total = torch.stack(views).sum(0)
+            for v in views:
+                v.copy_(total)
+
+    allreduce(engs[0].direct_reduce_fields())
+    for e in engs:
+        e.finish_direct()
+        e.adjoint_partial()
+    allreduce(engs[0].adjoint_reduce_fields(True))
+    for e in engs:
+        e.finish_adjoint()
+    ref = _oracle_linear(c, world=world)
+    for e in engs:
+        r = e.results()
+        assert rel_l2(r["uT"], ref.uT) <= 1e-10
+        assert rel_l2(r["qdag0"], ref.qdag0) <= 1e-10
+        assert rel_l2(r["grad"], ref.grad) <= 1e-8
+        assert np.max(np.abs(r["J"] - ref.J) / ref.J) <= 1e-10
+    # G-invariance: blockscan agrees with the single-rank scan to far below the parity bar
+    ref1 = _oracle_linear(c, world=1)
+    assert rel_l2(ref.uT, ref1.uT) <= 1e-9
+    for e in engs:
+        e.close()
+
+
+def test_burgers_blockscan_emulated():
+    import torch
+    from oracle.config_mode import burgers_gradient
+    from paper_2004_00546_b200 import baseline, scaled
+    from paper_2004_00546_b200.engine import EngineSpec, ParaexpEngine
+    from paper_2004_00546_b200.expaction import plan_chebyshev
+    from paper_2004_00546_b200.problems import burgers_frozen_region
+    c = scaled(baseline(3), nx=256, P=8, steps_per_slice=16)
+    u0, ut, ctrl = c.inputs()
+    world = 3
+    engs = [ParaexpEngine(EngineSpec(c.system, c.P, c.dt, c.expaction, c.batch, r, world)) for r in range(world)]
+    for e in engs:
+        e.set_inputs(u0, ut, ctrl)
+        e.direct_partial()
+        e.finish_direct()
+        e.adjoint_partial()
+    for f in engs[0].adjoint_reduce_fields(True):
+        views = [e.device_view(f) for e in engs]
+        total = torch.stack(views).sum(0)
+        for v in views:
+            v.copy_(total)
+    for e in engs:
+        e.finish_adjoint()
+    ref = burgers_gradient(c.grid.nx, c.spec.D, c.system.basis, c.spec.T, c.P, c.nsteps, u0, ut, ctrl,
+                           lambda region, span: plan_chebyshev(region, span, c.expaction),
+                           lambda ub: burgers_frozen_region(ub, c.grid, c.spec.D), world=world)
+    for e in engs:
+        r = e.results()
+        assert rel_l2(r["uT"], ref.uT) <= 1e-10
+        assert rel_l2(r["qdag0"], ref.qdag0) <= 1e-10
+        assert rel_l2(r["grad"], ref.grad) <= 1e-8
+        e.close()
+
+
+def test_deterministic_bitwise():
+    from paper_2004_00546_b200 import baseline, scaled
+    c = scaled(baseline(5), nx=64, P=8, steps_per_slice=4, K=16)
+    a = _gpu_linear(c)
+    b = _gpu_linear(c)
+    assert np.array_equal(a.grad, b.grad)
+    assert np.array_equal(a.direct.final_state, b.direct.final_state)
+
+
+def test_device_inputs_match_host_inputs():
+    import torch
+    from paper_2004_00546_b200 import RK4Config, baseline, scaled
+    from paper_2004_00546_b200.optimization import get_engine
+    c = scaled(baseline(5), nx=64, P=8, steps_per_slice=4, K=16)
+    u0, ut, ctrl = c.inputs()
+    eng = get_engine(c.system, c.P, RK4Config(c.dt), c.expaction, c.batch)
+    eng.set_inputs(u0, ut, ctrl)
+    eng.gradient()
+    host = eng.results()
+    eng.set_inputs(*(torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (u0, ut, ctrl)))
+    eng.gradient()
+    dev = eng.results()
+    assert np.array_equal(host["grad"], dev["grad"])
+
+
+def test_full_config5_gradient_vs_directional_fd():
+    """Full BASELINE size (2048², P = 512): J is quadratic in c, so the central
+    difference along a random direction is exact up to rounding; the adjoint
+    gradient must agree (size-independent property, oracle too slow at full size)."""
+    from paper_2004_00546_b200 import RK4Config, baseline
+    from paper_2004_00546_b200.optimization import get_engine
+    c = baseline(5)
+    u0, ut, ctrl = c.inputs()
+    eng = get_engine(c.system, c.P, RK4Config(c.dt), c.expaction, c.batch)
+    eng.set_inputs(u0, ut, ctrl)
+    eng.gradient()
+    r = eng.results()
+    rng = np.random.default_rng(7)
+    dirn = rng.normal(0.0, 1.0, ctrl.shape)
+    dirn /= np.linalg.norm(dirn)
+    eps = 1e-2
+    Js = []
+    for s in (1.0, -1.0):
+        eng.set_inputs(u0, ut, ctrl + s * eps * dirn)
+        eng.gradient()
+        Js.append(eng.results()["J"][0])
+    fd = (Js[0] - Js[1]) / (2 * eps)
+    ad = float(np.sum(r["grad"] * dirn))
+    assert abs(fd - ad) <= 1e-6 * abs(ad)
+    assert np.all(np.isfinite(r["grad"])) and r["J"][0] > 0
