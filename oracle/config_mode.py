@@ -191,7 +191,13 @@ def krylov_action(apply, plan: KrylovPlan, v: np.ndarray, phi: np.ndarray | None
 
 def exp_action(apply, plan, v, phi=None):
     if isinstance(plan, KrylovPlan):
-        return krylov_action(apply, plan, v, phi)
+        if v.ndim == 1:
+            return krylov_action(apply, plan, v, phi)
+        # one Arnoldi process per batch member (the GPU batches them in one grid)
+        out = np.empty_like(v)
+        for b in range(v.shape[0]):
+            out[b] = krylov_action(apply, plan, v[b], None if phi is None else phi[b])
+        return out
     return cheb_action(apply, plan, v, phi)
 
 

@@ -2,10 +2,7 @@
 //
 // Replaces the reference's per-stage Python/scipy arithmetic:
 //   rk45_integrate stage loop (timestepping.py:162-201) + csr_matvec (linalg.py:70-74)
-//     -> k_rk4_tile: one fused classical-RK4 step per launch over all (batch × slice)
-//        lanes, the four stages computed from one shared-memory tile with a
-//        4-point halo (temporal fusion of the stages: 24n algorithmic bytes per
-//        step instead of ~160n for stage-by-stage kernels);
+//     -> rk4.cuh (row-marching fused RK4 steps over all batch × slice lanes);
 //   _LejaInterpolant.step Newton loop (timestepping.py:343-356)
 //     -> k_cheb_first / k_cheb_term: stencil fused with the Chebyshev three-term
 //        recurrence and the exp and φ₁ accumulators;
@@ -46,168 +43,6 @@ __device__ __forceinline__ double stencil_at(const double* __restrict__ u, const
     r += s.cs * __ldg(u + (size_t)ys * nx + x);
   }
   return r;
-}
-
-// ---------------------------------------------------------------------------
-// Fused RK4 step over lanes (zero-data inhomogeneous slice solves)
-// ---------------------------------------------------------------------------
-
-struct RK4Args {
-  const double* y_in;  // lanes × n; nullptr = zero state (first step of a sweep)
-  double* y_out;       // lanes × n
-  const double* g;     // B × n constant source; lane l uses member l / lanes_per_b
-  double* z;           // ADJ: lanes × n running ∫y (in place)
-  Stencil5 st;
-  double h;
-  int nx, ny;
-  int lanes, lanes_per_b;
-  int tiles_x, tiles_y;
-};
-
-// Stage regions: stage s (1..4) computes on the tile grown by (4 - s) points.
-// Tile-interior points are owned by fixed threads (accumulators in registers);
-// ring points are distributed round-robin.
-template <int DIM, int TX, int TY, int NT, bool ADJ>
-__global__ void __launch_bounds__(NT) k_rk4_tile(RK4Args a) {
-  constexpr int HX = 4;
-  constexpr int HY = (DIM == 2) ? 4 : 0;
-  constexpr int W = TX + 2 * HX;
-  constexpr int H = TY + 2 * HY;
-  constexpr int NPT = (TX * TY) / NT;
-  static_assert((TX * TY) % NT == 0, "tile must split evenly over threads");
-  extern __shared__ double smem[];
-  double* s_y = smem;
-  double* s_g = s_y + W * H;
-  double* s_a = s_g + W * H;
-  double* s_b = s_a + W * H;
-
-  const int lane = blockIdx.x % a.lanes;
-  const int tile = blockIdx.x / a.lanes;
-  const int tx0 = (tile % a.tiles_x) * TX;
-  const int ty0 = (tile / a.tiles_x) * TY;
-  const int nx = a.nx, ny = a.ny;
-  const size_t n = (size_t)nx * ny;
-  const double* __restrict__ yin = a.y_in ? a.y_in + (size_t)lane * n : nullptr;
-  const double* __restrict__ g = a.g + (size_t)(lane / a.lanes_per_b) * n;
-  const Stencil5 st = a.st;
-  const double h = a.h, hh = 0.5 * a.h, h6 = a.h / 6.0;
-
-  for (int idx = threadIdx.x; idx < W * H; idx += NT) {
-    const int ly = idx / W, lx = idx - ly * W;
-    const int gx = wrapi(tx0 + lx - HX, nx);
-    const int gy = (DIM == 2) ? wrapi(ty0 + ly - HY, ny) : 0;
-    const size_t off = (size_t)gy * nx + gx;
-    s_y[idx] = yin ? __ldg(yin + off) : 0.0;
-    s_g[idx] = __ldg(g + off);
-  }
-  __syncthreads();
-
-  auto A = [&](const double* s, int i) -> double {
-    double r = st.cc * s[i];
-    r += st.ce * s[i + 1];
-    r += st.cw * s[i - 1];
-    if (DIM == 2) {
-      r += st.cn * s[i + W];
-      r += st.cs * s[i - W];
-    }
-    return r;
-  };
-  auto interior_index = [&](int t) -> int {
-    const int q = threadIdx.x + t * NT;
-    const int qy = q / TX, qx = q - qy * TX;
-    return (qy + HY) * W + (qx + HX);
-  };
-  // ring of the tile grown by `s`: local index of the idx-th ring point
-  auto ring_count = [&](int s) -> int {
-    const int sy = (DIM == 2) ? s : 0;
-    return (TX + 2 * s) * (TY + 2 * sy) - TX * TY;
-  };
-  auto ring_index = [&](int s, int idx) -> int {
-    const int sy = (DIM == 2) ? s : 0;
-    const int rw = TX + 2 * s;
-    int r, c;
-    if (idx < sy * rw) {
-      r = idx / rw; c = idx - r * rw;
-    } else if (idx < 2 * sy * rw) {
-      idx -= sy * rw;
-      r = sy + TY + idx / rw; c = idx % rw;
-    } else {
-      idx -= 2 * sy * rw;
-      r = sy + idx / (2 * s);
-      c = idx % (2 * s);
-      if (c >= s) c += TX;
-    }
-    // rectangle origin is (HX - s, HY - sy)
-    return (r + HY - sy) * W + (c + HX - s);
-  };
-
-  double acc[NPT];
-  double zacc[ADJ ? NPT : 1];
-
-  // stage 1: k1 = A y + g, Y2 = y + h/2 k1 (on tile+3)
-#pragma unroll
-  for (int t = 0; t < NPT; ++t) {
-    const int i = interior_index(t);
-    const double k = A(s_y, i) + s_g[i];
-    const double Y = s_y[i] + hh * k;
-    acc[t] = k;
-    if (ADJ) zacc[t] = s_y[i] + 2.0 * Y;
-    s_a[i] = Y;
-  }
-  for (int idx = threadIdx.x, m = ring_count(3); idx < m; idx += NT) {
-    const int i = ring_index(3, idx);
-    s_a[i] = s_y[i] + hh * (A(s_y, i) + s_g[i]);
-  }
-  __syncthreads();
-  // stage 2: k2 = A Y2 + g, Y3 = y + h/2 k2 (on tile+2)
-#pragma unroll
-  for (int t = 0; t < NPT; ++t) {
-    const int i = interior_index(t);
-    const double k = A(s_a, i) + s_g[i];
-    const double Y = s_y[i] + hh * k;
-    acc[t] += 2.0 * k;
-    if (ADJ) zacc[t] += 2.0 * Y;
-    s_b[i] = Y;
-  }
-  for (int idx = threadIdx.x, m = ring_count(2); idx < m; idx += NT) {
-    const int i = ring_index(2, idx);
-    s_b[i] = s_y[i] + hh * (A(s_a, i) + s_g[i]);
-  }
-  __syncthreads();
-  // stage 3: k3 = A Y3 + g, Y4 = y + h k3 (on tile+1), into s_a
-#pragma unroll
-  for (int t = 0; t < NPT; ++t) {
-    const int i = interior_index(t);
-    const double k = A(s_b, i) + s_g[i];
-    const double Y = s_y[i] + h * k;
-    acc[t] += 2.0 * k;
-    if (ADJ) zacc[t] += Y;
-    s_a[i] = Y;
-  }
-  for (int idx = threadIdx.x, m = ring_count(1); idx < m; idx += NT) {
-    const int i = ring_index(1, idx);
-    s_a[i] = s_y[i] + h * (A(s_b, i) + s_g[i]);
-  }
-  __syncthreads();
-  // stage 4: k4 = A Y4 + g; y += h/6 (k1 + 2k2 + 2k3 + k4)
-  double* __restrict__ yout = a.y_out + (size_t)lane * n;
-  double* __restrict__ z = ADJ ? a.z + (size_t)lane * n : nullptr;
-#pragma unroll
-  for (int t = 0; t < NPT; ++t) {
-    const int q = threadIdx.x + t * NT;
-    const int qy = q / TX, qx = q - qy * TX;
-    const int gx = tx0 + qx, gy = ty0 + qy;
-    const int i = (qy + HY) * W + (qx + HX);
-    const double k = A(s_a, i) + s_g[i];
-    if (gx < nx && (DIM == 1 || gy < ny)) {
-      const size_t off = (size_t)gy * nx + gx;
-      yout[off] = s_y[i] + h6 * (acc[t] + k);
-      if (ADJ) {
-        const double zin = yin ? z[off] : 0.0;
-        z[off] = zin + h6 * zacc[t];
-      }
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------

@@ -26,6 +26,7 @@
 #include "kernels.cuh"
 #include "burgers.cuh"
 #include "krylov.cuh"
+#include "rk4.cuh"
 
 namespace {
 
@@ -56,6 +57,8 @@ struct Handle {
   bool basis_set = false, inputs_set = false;
   // sources and lanes
   double *g = nullptr, *gadj = nullptr;
+  double *bsrc = nullptr, *cz = nullptr;  // h·S(hM)·g and h²·U(hM)·g (RK4 Horner constants)
+  bool z_valid = false;
   double *Y0 = nullptr, *Y1 = nullptr, *Z = nullptr;
   const double *vend = nullptr, *wend = nullptr;
   // exp-action work
@@ -171,63 +174,102 @@ inline dim3 grid_stride(size_t n, int B) {
 // RK4 lanes sweep
 // ---------------------------------------------------------------------------
 
-constexpr int TX2 = 64, TY2 = 16, NT2 = 256;
-constexpr int TX1 = 1024, TY1 = 1, NT1 = 256;
-
-template <int DIM>
-constexpr size_t rk4_smem() {
-  return DIM == 2 ? 4 * (TX2 + 8) * (TY2 + 8) * sizeof(double)
-                  : 4 * (TX1 + 8) * (TY1) * sizeof(double);
-}
-
-template <int DIM, bool ADJ>
-int launch_rk4(Handle* h, const px::RK4Args& a, cudaStream_t s) {
-  constexpr int TX = DIM == 2 ? TX2 : TX1;
-  constexpr int TY = DIM == 2 ? TY2 : TY1;
-  constexpr int NT = DIM == 2 ? NT2 : NT1;
-  constexpr size_t smem = rk4_smem<DIM>();
-  static bool attr_set = false;
-  auto kfn = px::k_rk4_tile<DIM, TX, TY, NT, ADJ>;
-  if (!attr_set) {
-    PX_CUDA(h, cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = true;
-  }
-  const unsigned blocks = (unsigned)(a.tiles_x * a.tiles_y) * (unsigned)a.lanes;
-  kfn<<<blocks, NT, smem, s>>>(a);
+int axpby(Handle* h, double* out, long long obs, const double* x, long long xbs, double alpha,
+          const double* y, long long ybs, double beta, cudaStream_t s) {
+  px::k_axpby<<<grid_stride(h->n, h->B), 256, 0, s>>>(out, obs, x, xbs, alpha, y, ybs, beta, h->n);
   PX_CHECK_LAUNCH(h);
   return PX_OK;
 }
 
-// Zero-data RK4 sweep of all local lanes: nsteps fused steps; returns final buffer.
+// Zero-data RK4 sweep of all local lanes (rk4.cuh); returns the final lane buffer.
 int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s) {
-  px::RK4Args a{};
-  a.g = adjoint ? h->gadj : h->g;
-  a.z = adjoint ? h->Z : nullptr;
-  a.st = adjoint ? h->AT : h->A;
-  a.h = (h->d.T / h->d.P) / h->d.nsteps;
-  a.nx = h->d.nx;
-  a.ny = h->d.ny;
-  a.lanes = h->L;
-  a.lanes_per_b = h->Pl;
-  const int TX = h->dim == 2 ? TX2 : TX1, TY = h->dim == 2 ? TY2 : TY1;
-  a.tiles_x = (h->d.nx + TX - 1) / TX;
-  a.tiles_y = h->dim == 2 ? (h->d.ny + TY - 1) / TY : 1;
+  const px::Stencil5 st = adjoint ? h->AT : h->A;
+  const double hs = (h->d.T / h->d.P) / h->d.nsteps;
+  const double* g = adjoint ? h->gadj : h->g;
+  const dim3 grid = grid1(h->n, h->B);
+  const int nx = h->d.nx, ny = h->d.ny;
+  // Horner constants: t1 = g + (h/4)Mg, t2 = g + (h/3)M t1, b = h(g + (h/2)M t2), c = (h²/2) t2
+  auto sax = [&](double* out, const double* x, const double* y, double al, double sc) -> int {
+    if (h->dim == 2) px::k_stencil_axpy<2><<<grid, 256, 0, s>>>(out, x, y, st, al, sc, nx, ny);
+    else px::k_stencil_axpy<1><<<grid, 256, 0, s>>>(out, x, y, st, al, sc, nx, ny);
+    PX_CHECK_LAUNCH(h);
+    return PX_OK;
+  };
+  PX_TRY(sax(h->Wk[0], g, g, 0.25 * hs, 1.0));
+  PX_TRY(sax(h->Wk[1], g, h->Wk[0], hs / 3.0, 1.0));
+  PX_TRY(sax(h->bsrc, g, h->Wk[1], 0.5 * hs, hs));
+  if (adjoint)
+    PX_TRY(axpby(h, h->cz, (long long)h->n, h->Wk[1], (long long)h->n, 0.5 * hs * hs, nullptr, 0, 0.0, s));
+
+  const int nsteps = h->d.nsteps;
   double* cur = nullptr;
-  for (int st = 0; st < h->d.nsteps; ++st) {
-    double* out = (cur == h->Y0) ? h->Y1 : h->Y0;
-    a.y_in = cur;
-    a.y_out = out;
-    int rc;
-    if (h->dim == 2)
-      rc = adjoint ? launch_rk4<2, true>(h, a, s) : launch_rk4<2, false>(h, a, s);
-    else
-      rc = adjoint ? launch_rk4<1, true>(h, a, s) : launch_rk4<1, false>(h, a, s);
-    if (rc != PX_OK) return rc;
-    cur = out;
+  uint64_t launched_steps = 0;
+  h->z_valid = false;
+  if (h->dim == 1 && h->n <= 4096) {
+    px::Lane1DArgs a{};
+    a.y_out = h->Y0; a.b = h->bsrc; a.z = h->Z; a.st = st; a.h = hs;
+    a.n = (int)h->n; a.lanes_per_b = h->Pl; a.nsteps = nsteps;
+    const int ppt = h->n <= 1024 ? 1 : (h->n <= 2048 ? 2 : 4);
+    const int nt = (int)((h->n + ppt - 1) / ppt);
+#define PX_L1(PP)                                                   \
+  do {                                                              \
+    if (adjoint) px::k_rk4_lane1d<PP, true><<<h->L, nt, 0, s>>>(a); \
+    else px::k_rk4_lane1d<PP, false><<<h->L, nt, 0, s>>>(a);        \
+  } while (0)
+    if (ppt == 1) PX_L1(1);
+    else if (ppt == 2) PX_L1(2);
+    else PX_L1(4);
+#undef PX_L1
+    PX_CHECK_LAUNCH(h);
+    cur = h->Y0;
+    launched_steps = nsteps;
+    h->z_valid = adjoint;
+  } else if (nsteps == 1) {
+    px::k_broadcast_lanes<<<dim3((unsigned)std::min<size_t>((h->n + 255) / 256, 1024), h->L), 256, 0, s>>>(
+        h->Y0, h->bsrc, h->Pl, h->n);
+    PX_CHECK_LAUNCH(h);
+    cur = h->Y0;
+  } else {
+    if (h->dim == 2 && (nx & 1)) return fail(h, PX_ERR_ARG, "2D grids need an even nx");
+    px::MarchArgs a{};
+    a.b = h->bsrc; a.z = h->Z; a.st = st; a.h = hs;
+    a.nx = nx; a.ny = ny; a.lanes = h->L; a.lanes_per_b = h->Pl;
+    if (nx <= px::MARCH_MAX_CW) {
+      a.strip_w = nx; a.halo = 0; a.nstrips = 1;
+    } else {
+      a.strip_w = px::MARCH_STRIP; a.halo = px::MARCH_HALO;
+      a.nstrips = (nx + px::MARCH_STRIP - 1) / px::MARCH_STRIP;
+    }
+    // bands of rows: enough CTAs for ≥ 4 waves at 2 CTAs/SM, ≥ 32 rows per band
+    int br = ny;
+    while (br > 32 && (size_t)h->L * a.nstrips * ((ny + br - 1) / br) < 4 * 2 * 148) br = (br + 1) / 2;
+    if (ny >= 1024 && br > 256) br = 256;
+    a.band_rows = br;
+    a.nbands = (ny + br - 1) / br;
+    const unsigned blocks = (unsigned)((size_t)h->L * a.nstrips * a.nbands);
+    const size_t smem = px::march_smem(adjoint);
+    static bool attr_done[2] = {false, false};
+    if (!attr_done[adjoint]) {
+      if (adjoint) PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      else PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_done[adjoint] = true;
+    }
+    for (int st_i = 1; st_i < nsteps; ++st_i) {
+      double* out = (cur == h->Y0) ? h->Y1 : h->Y0;
+      a.y_in = cur;
+      a.y_out = out;
+      a.z_zero = (st_i == 1);
+      if (adjoint) px::k_rk4_march<true><<<blocks, px::MARCH_NT, smem, s>>>(a);
+      else px::k_rk4_march<false><<<blocks, px::MARCH_NT, smem, s>>>(a);
+      PX_CHECK_LAUNCH(h);
+      cur = out;
+    }
+    launched_steps = nsteps - 1;
+    h->z_valid = adjoint;
   }
-  const double bytes_per_point = adjoint ? 40.0 : 24.0;  // y,g,y' (+ z in/out)
-  h->stats.rk4_lane_steps += (uint64_t)h->L * h->d.nsteps;
-  const double bytes = bytes_per_point * (double)h->n * h->L * h->d.nsteps;
+  const double bytes_per_point = adjoint ? 40.0 : 24.0;  // y, b, y' (+ z in/out)
+  h->stats.rk4_lane_steps += (uint64_t)h->L * launched_steps;
+  const double bytes = bytes_per_point * (double)h->n * h->L * launched_steps;
   h->stats.rk4_bytes += bytes;
   h->stats.algorithmic_bytes += bytes;
   *final_out = cur;
@@ -312,13 +354,6 @@ int exp_action(Handle* h, int slot, const px::Stencil5& st, const double* src, l
   return cheb_action(h, pl, st, src, src_bs, addend, add_bs, pacc, result, s);
 }
 
-int axpby(Handle* h, double* out, long long obs, const double* x, long long xbs, double alpha,
-          const double* y, long long ybs, double beta, cudaStream_t s) {
-  px::k_axpby<<<grid_stride(h->n, h->B), 256, 0, s>>>(out, obs, x, xbs, alpha, y, ybs, beta, h->n);
-  PX_CHECK_LAUNCH(h);
-  return PX_OK;
-}
-
 int project(Handle* h, double* grad, const double* F, long long Fbs, double alpha, double beta,
             cudaStream_t s) {
   const int rx = h->rows_x;
@@ -401,8 +436,10 @@ int adjoint_linear(Handle* h, cudaStream_t s) {
   tend(h, tm, s);
   h->wend = wend;
   tm = tbegin(h, PX_PHASE_EXP_ADJOINT, s);
-  // G partial <- Σ_p z_p
-  px::k_lane_sum<<<grid_stride(h->n, h->B), 256, 0, s>>>(h->G, h->Z, h->Pl, h->n);
+  // G partial <- Σ_p z_p  (z_p = Σ_steps h·w3 + nsteps·c)
+  px::k_lane_sum_plus<<<grid_stride(h->n, h->B), 256, 0, s>>>(h->G, h->Z, h->Pl, h->cz,
+                                                              (double)h->Pl * h->d.nsteps, h->n,
+                                                              h->z_valid ? 1 : 0);
   PX_CHECK_LAUNCH(h);
   const double* C = wend + (size_t)(h->Pl - 1) * h->n;
   long long C_bs = lane_bs;
@@ -464,7 +501,7 @@ extern "C" {
 int px_abi_version(void) { return PX_ABI_VERSION; }
 
 const char* px_build_info(void) {
-  return "paraexp sm_100a fp64 (RK4 tile/halo-4 fused stages, Chebyshev fused recurrence, "
+  return "paraexp sm_100a fp64 (row-marching Horner RK4, on-chip 1D lanes, Chebyshev fused recurrence, "
          "Arnoldi CGS2, Burgers serial sweep)";
 }
 
@@ -531,6 +568,8 @@ int px_create(const px_problem_desc* desc, void** out_handle) {
   if (d.kind == PX_KIND_ADVDIFF) {
     A(&h->g, B * n);
     A(&h->gadj, B * n);
+    A(&h->bsrc, B * n);
+    A(&h->cz, B * n);
     A(&h->Y0, (size_t)h->L * n);
     A(&h->Y1, (size_t)h->L * n);
     A(&h->Z, (size_t)h->L * n);

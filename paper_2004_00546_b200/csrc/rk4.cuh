@@ -1,0 +1,363 @@
+// rk4.cuh — zero-data RK4 slice solves for the linear testbed, all lanes batched.
+//
+// For y' = M·y + g with constant g (absorbed initial / final condition,
+// paraexp.py:239-242, :268-270) one classical RK4 step is exactly
+//     y⁺ = R(hM)·y + b,   R(x) = 1 + x·S(x),   S(x) = 1 + x/2 + x²/6 + x³/24,
+//     b  = h·S(hM)·g,
+// and the RK4-consistent running integral z = ∫y (RK4 on the augmented system
+// (y, z)' = (M y + g, y)) advances by  h·S(hM)·y + c,  c = h²·U(hM)·g,
+// U(x) = 1/2 + x/6 + x²/24. The Horner evaluation of R,
+//     w1 = y + (h/4)·M·y,  w2 = y + (h/3)·M·w1,  w3 = y + (h/2)·M·w2 (= S(hM)y),
+//     y⁺ = y + h·M·w3 + b,
+// needs four stencil applications per step like the stage form, but no source
+// reads and no stage accumulators, and it yields S(hM)y (= w3) for the integral.
+// b and c are formed once per sweep and member (3 stencil passes).
+//
+// 2D kernel (k_rk4_march): each CTA owns a strip of columns of one lane and
+// MARCHES along y; the four Horner stages are pipelined one row apart
+// (stage s of iteration i works on row r−s), so the vertical neighbours come
+// from per-thread register row queues and only the x neighbours are exchanged
+// through shared memory (even/odd split arrays, double buffered: one barrier
+// per row). Strips are 512 columns wide with a 4-column recomputed halo (or the
+// whole periodic row when nx ≤ 576); bands of rows add 8 pipeline-fill rows.
+// HBM traffic ≈ 24n per step (y, b in; y⁺ out) + 16n with z.
+//
+// 1D kernel (k_rk4_lane1d): a lane (≤ 8192 points) lives on chip; one CTA runs
+// all nsteps of its lane, exchanging only the edge values of each thread's run.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace px {
+
+constexpr int MARCH_NT = 288;          // 9 warps: pairs of columns per thread
+constexpr int MARCH_MAX_CW = 2 * MARCH_NT;
+constexpr int MARCH_STRIP = 512;       // useful strip width in strip mode
+constexpr int MARCH_HALO = 4;
+
+struct MarchArgs {
+  const double* y_in;  // lanes × n; nullptr → y = b (state after the first step from zero)
+  double* y_out;       // lanes × n
+  const double* b;     // B × n   h·S(hM)·g
+  double* z;           // ADJ: lanes × n, z += h·w3
+  int z_zero;          // ADJ: treat z_in as 0
+  Stencil5 st;
+  double h;
+  int nx, ny, lanes, lanes_per_b;
+  int strip_w;   // useful width per strip (even)
+  int halo;      // MARCH_HALO (strips) or 0 (whole periodic row in one CTA)
+  int nstrips, band_rows, nbands;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Row ring: each thread streams its own column pair of the y, b (and z) rows
+// MARCH_DEPTH rows ahead with cp.async (LDGSTS) into shared memory, so ~6 rows
+// per CTA are in flight without holding registers; a thread only reads back
+// the bytes it copied, so the ring needs no barrier.
+// ring depth: 6 rows (direct: y, b) / 4 rows (adjoint: y, b, z) keeps two CTAs per SM
+template <bool ADJ>
+struct MarchDepth {
+  static constexpr int value = ADJ ? 4 : 6;
+};
+
+template <bool ADJ>
+__global__ void __launch_bounds__(MARCH_NT, 2) k_rk4_march(MarchArgs a) {
+  constexpr int NQ = ADJ ? 3 : 2;  // streamed arrays: y, b (, z)
+  constexpr int MARCH_DEPTH = MarchDepth<ADJ>::value;
+  // publish area: [parity][quantity: y, w1, w2, w3][pair] split in even / odd columns
+  __shared__ double pubE[2][4][MARCH_NT];
+  __shared__ double pubO[2][4][MARCH_NT];
+  extern __shared__ double2 ring[];  // [MARCH_DEPTH][NQ][MARCH_NT]
+
+  const int lane = blockIdx.x % a.lanes;
+  const int rest = blockIdx.x / a.lanes;
+  const int strip = rest % a.nstrips;
+  const int band = rest / a.nstrips;
+  const int nx = a.nx, ny = a.ny;
+  const size_t n = (size_t)nx * ny;
+  const int x0 = strip * a.strip_w;
+  const int U = min(a.strip_w, nx - x0);
+  const int CW = U + 2 * a.halo;
+  const int T = CW >> 1;  // active pairs
+  const int t = threadIdx.x;
+  const bool active = t < T;
+  const int tc = active ? t : 0;
+  const int gx = (((x0 - a.halo + 2 * tc) % nx) + nx) % nx;  // even
+  const int j0 = band * a.band_rows;
+  const int rows_out = min(a.band_rows, ny - j0);
+  const int iters = rows_out + 8;
+  const bool full_row = a.halo == 0;
+  const int tl = (t == 0) ? (full_row ? T - 1 : 0) : t - 1;
+  const int tr = (t + 1 >= T) ? (full_row ? 0 : T - 1) : t + 1;
+  const bool store_ok = active && (2 * t >= a.halo) && (2 * t + 1 < CW - a.halo);
+
+  const Stencil5 st = a.st;
+  const double h = a.h, c1 = a.h * 0.25, c2 = a.h / 3.0, c3 = a.h * 0.5;
+  const size_t member = (size_t)(lane / a.lanes_per_b);
+  const double* __restrict__ bsrc = a.b + member * n;
+  const double* __restrict__ ysrc = a.y_in ? a.y_in + (size_t)lane * n : bsrc;
+  double* __restrict__ yout = a.y_out + (size_t)lane * n;
+  double* __restrict__ zl = ADJ ? a.z + (size_t)lane * n : nullptr;
+  const bool zread = ADJ && !a.z_zero;
+
+  // incremental periodic row counters (no per-row integer division)
+  auto wrapr = [&](int row) -> int {
+    row %= ny;
+    return row < 0 ? row + ny : row;
+  };
+  const int r0 = j0 - 4;
+  // issue stream: y row r0+k and b/z rows r0+k-4 for the k-th issued iteration
+  int iss_k = 0, iss_slot = 0;
+  int ry = wrapr(r0), rb = wrapr(r0 - 4);
+  const size_t coloff = (size_t)gx;
+  auto issue = [&]() {
+    if (iss_k < iters) {
+      double2* slot = ring + (size_t)iss_slot * NQ * MARCH_NT;
+      cp_async16(slot + t, ysrc + (size_t)ry * nx + coloff);
+      cp_async16(slot + MARCH_NT + t, bsrc + (size_t)rb * nx + coloff);
+      if (zread) cp_async16(slot + 2 * MARCH_NT + t, zl + (size_t)rb * nx + coloff);
+    }
+    cp_async_commit();
+    ++iss_k;
+    iss_slot = (iss_slot + 1 == MARCH_DEPTH) ? 0 : iss_slot + 1;
+    ry = (ry + 1 == ny) ? 0 : ry + 1;
+    rb = (rb + 1 == ny) ? 0 : rb + 1;
+  };
+#pragma unroll
+  for (int k = 0; k < MARCH_DEPTH; ++k) issue();
+  int rslot = 0;              // ring slot consumed this iteration
+  int rs = wrapr(r0 - 4);     // output row (r − 4) of this iteration
+
+  // register row queues as rings indexed by the (unrolled, compile-time) iteration
+  // phase k = i mod 6: y rows r-4..r in yq[(k-4..k) mod 6]; w1/w2/w3 keep the last
+  // two rows in wq[(k-2) mod 2], wq[(k-1) mod 2]. Unrolling by 6 turns the queue
+  // rotation into register renaming (no moves).
+  double2 yq[6], w1q[2], w2q[2], w3q[2];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) yq[k] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) w1q[k] = w2q[k] = w3q[k] = make_double2(0.0, 0.0);
+
+  auto apply = [&](double2 c, double2 s, double2 nn, double l, double r) -> double2 {
+    double2 o;
+    o.x = st.cc * c.x;
+    o.x += st.ce * c.y;
+    o.x += st.cw * l;
+    o.x += st.cn * nn.x;
+    o.x += st.cs * s.x;
+    o.y = st.cc * c.y;
+    o.y += st.ce * r;
+    o.y += st.cw * c.x;
+    o.y += st.cn * nn.y;
+    o.y += st.cs * s.y;
+    return o;
+  };
+
+  for (int i0 = 0; i0 < iters; i0 += 6) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const int i = i0 + k;
+      if (i >= iters) break;
+      const int pin = (k + 1) & 1;  // parity published in the previous iteration (i0 even)
+      const int pout = k & 1;
+      cp_async_wait<MARCH_DEPTH - 1>();
+      const double2* slot = ring + (size_t)rslot * NQ * MARCH_NT;
+      rslot = (rslot + 1 == MARCH_DEPTH) ? 0 : rslot + 1;
+      const double2 yr = slot[t];
+      const double2 brow = slot[MARCH_NT + t];  // row r-4
+      const double2 zrow = zread ? slot[2 * MARCH_NT + t] : make_double2(0.0, 0.0);
+      issue();  // refills the slot just consumed (its values are in registers)
+      yq[k] = yr;
+      // rows r-4 .. r-1 (yr = row r)
+      const double2 y0 = yq[(k + 2) % 6], y1 = yq[(k + 3) % 6], y2 = yq[(k + 4) % 6], y3 = yq[(k + 5) % 6];
+      const int po = k & 1, pp = (k + 1) & 1;  // w?q[po]: row of iteration i-2, [pp]: i-1
+
+      double2 nw1 = make_double2(0.0, 0.0), nw2 = nw1, nw3 = nw1;
+      if (i >= 2) {  // stage 1 at row r-1: w1 = y + (h/4)·M·y
+        const double l = pubO[pin][0][tl], rr = pubE[pin][0][tr];
+        const double2 m = apply(y3, y2, yr, l, rr);
+        nw1 = make_double2(y3.x + c1 * m.x, y3.y + c1 * m.y);
+      }
+      if (i >= 4) {  // stage 2 at row r-2: w2 = y + (h/3)·M·w1  (w1 rows r-3, r-2, r-1)
+        const double l = pubO[pin][1][tl], rr = pubE[pin][1][tr];
+        const double2 m = apply(w1q[pp], w1q[po], nw1, l, rr);
+        nw2 = make_double2(y2.x + c2 * m.x, y2.y + c2 * m.y);
+      }
+      if (i >= 6) {  // stage 3 at row r-3: w3 = y + (h/2)·M·w2  (w2 rows r-4, r-3, r-2)
+        const double l = pubO[pin][2][tl], rr = pubE[pin][2][tr];
+        const double2 m = apply(w2q[pp], w2q[po], nw2, l, rr);
+        nw3 = make_double2(y1.x + c3 * m.x, y1.y + c3 * m.y);
+      }
+      if (i >= 8) {  // stage 4 at row r-4: y⁺ = y + h·M·w3 + b  (w3 rows r-5, r-4, r-3)
+        const double l = pubO[pin][3][tl], rr = pubE[pin][3][tr];
+        const double2 w3c = w3q[pp];
+        const double2 m = apply(w3c, w3q[po], nw3, l, rr);
+        if (store_ok) {
+          const size_t off = (size_t)rs * nx + coloff;
+          double2 yn;
+          yn.x = y0.x + h * m.x + brow.x;
+          yn.y = y0.y + h * m.y + brow.y;
+          __stcs(reinterpret_cast<double2*>(yout + off), yn);
+          if (ADJ) {
+            double2 zn;
+            zn.x = zrow.x + h * w3c.x;
+            zn.y = zrow.y + h * w3c.y;
+            __stcs(reinterpret_cast<double2*>(zl + off), zn);
+          }
+        }
+      }
+      rs = (rs + 1 == ny) ? 0 : rs + 1;
+      w1q[po] = nw1;
+      w2q[po] = nw2;
+      w3q[po] = nw3;
+      if (active) {
+        pubE[pout][0][t] = yr.x;  pubO[pout][0][t] = yr.y;
+        pubE[pout][1][t] = nw1.x; pubO[pout][1][t] = nw1.y;
+        pubE[pout][2][t] = nw2.x; pubO[pout][2][t] = nw2.y;
+        pubE[pout][3][t] = nw3.x; pubO[pout][3][t] = nw3.y;
+      }
+      __syncthreads();
+    }
+  }
+  cp_async_wait<0>();
+}
+
+inline size_t march_smem(bool adj) {
+  return (size_t)(adj ? MarchDepth<true>::value * 3 : MarchDepth<false>::value * 2) * MARCH_NT * sizeof(double2);
+}
+
+// ---------------------------------------------------------------------------
+// 1D: one CTA per lane, all nsteps on chip
+// ---------------------------------------------------------------------------
+
+constexpr int LANE1D_MAX_N = 8192;
+
+struct Lane1DArgs {
+  double* y_out;      // lanes × n (lane end states)
+  const double* b;    // B × n
+  double* z;          // ADJ: lanes × n (written, Σ h·w3 over the steps)
+  Stencil5 st;
+  double h;
+  int n, lanes_per_b, nsteps;
+};
+
+template <int PPT, bool ADJ>
+__global__ void __launch_bounds__(1024) k_rk4_lane1d(Lane1DArgs a) {
+  __shared__ double eL[2][1024];
+  __shared__ double eR[2][1024];
+  const int n = a.n;
+  const int lane = blockIdx.x;
+  const int t = threadIdx.x;
+  const int NT = blockDim.x;
+  const int start = t * PPT;
+  const int cnt = max(0, min(PPT, n - start));
+  const int last = (n + PPT - 1) / PPT - 1;  // last thread with points
+  const int tl = (t == 0) ? last : t - 1;
+  const int tr = (t >= last) ? 0 : t + 1;
+  const Stencil5 st = a.st;
+  const double h = a.h;
+  const double cs[4] = {a.h * 0.25, a.h / 3.0, a.h * 0.5, a.h};
+  const double* bm = a.b + (size_t)(lane / a.lanes_per_b) * n;
+  double y[PPT], b[PPT], w[PPT], z[PPT];
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    y[k] = 0.0;
+    z[k] = 0.0;
+    b[k] = (k < cnt) ? bm[start + k] : 0.0;
+  }
+  int par = 0;
+  for (int s = 0; s < a.nsteps; ++s) {
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) w[k] = y[k];
+#pragma unroll
+    for (int stage = 0; stage < 4; ++stage) {
+      if (t <= last) {
+        eL[par][t] = w[0];
+        eR[par][t] = w[cnt > 0 ? cnt - 1 : 0];
+      }
+      __syncthreads();
+      const double left = eR[par][tl], right = eL[par][tr];
+      par ^= 1;
+      double m[PPT];
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        const double wl = (k == 0) ? left : w[k - 1];
+        const double wr = (k + 1 == PPT || k + 1 >= cnt) ? right : w[k + 1];
+        double v = st.cc * w[k];
+        v += st.ce * wr;
+        v += st.cw * wl;
+        m[k] = v;
+      }
+      const double c = cs[stage];
+      if (stage < 3) {
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) w[k] = y[k] + c * m[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          if (ADJ) z[k] += h * w[k];
+          y[k] = y[k] + h * m[k] + b[k];
+        }
+      }
+    }
+  }
+  double* yo = a.y_out + (size_t)lane * n;
+  double* zo = ADJ ? a.z + (size_t)lane * n : nullptr;
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    if (k < cnt) {
+      yo[start + k] = y[k];
+      if (ADJ) zo[start + k] = z[k];
+    }
+  }
+  (void)NT;
+}
+
+// out = s·(x + α·M·y)  (batch in blockIdx.y)
+template <int DIM>
+__global__ void k_stencil_axpy(double* out, const double* x, const double* y, Stencil5 st, double alpha,
+                               double s, int nx, int ny) {
+  const size_t n = (size_t)nx * ny;
+  const int b = blockIdx.y;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int yy = (int)(i / nx), xx = (int)(i - (size_t)yy * nx);
+  const size_t o = (size_t)b * n;
+  out[o + i] = s * (x[o + i] + alpha * stencil_at<DIM>(y + o, st, xx, yy, nx, ny));
+}
+
+// out[b*lanes_per_b + p] = src[b] for every lane (nsteps == 1 corner case)
+__global__ void k_broadcast_lanes(double* out, const double* src, int lanes_per_b, size_t n) {
+  const int l = blockIdx.y;
+  const double* s = src + (size_t)(l / lanes_per_b) * n;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    out[(size_t)l * n + i] = s[i];
+}
+
+// out[b][i] = Σ_p lanes[b*Pl + p][i] + scale·c[b][i]  (fixed order)
+__global__ void k_lane_sum_plus(double* out, const double* lanes, int lanes_per_b, const double* c, double scale,
+                                size_t n, int with_lanes) {
+  const int b = blockIdx.y;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    double r = 0.0;
+    if (with_lanes) {
+      const double* src = lanes + (size_t)b * lanes_per_b * n + i;
+      for (int p = 0; p < lanes_per_b; ++p) r += src[(size_t)p * n];
+    }
+    if (c) r += scale * c[(size_t)b * n + i];
+    out[(size_t)b * n + i] = r;
+  }
+}
+
+}  // namespace px

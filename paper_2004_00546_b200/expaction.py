@@ -142,7 +142,16 @@ def chebyshev_coefficients(f, center: float, d: float, imag: bool, n: int) -> np
 
 def _evaluate(region_pts: np.ndarray, crouzeix: float, center: float, d: float,
               imag: bool, tau: float, kmax: int):
-    """Truncation errors (exp, φ₁) and rounding estimates for degrees 0..kmax."""
+    """Truncation errors (exp, φ₁) and rounding estimates for degrees 0..kmax.
+
+    Candidates whose coefficients overflow yield non-finite errors and are
+    rejected by the caller's comparisons.
+    """
+    with np.errstate(all="ignore"):
+        return _evaluate_impl(region_pts, crouzeix, center, d, imag, tau, kmax)
+
+
+def _evaluate_impl(region_pts, crouzeix, center, d, imag, tau, kmax):
     nq = max(64, 2 * kmax + 32)
     be = chebyshev_coefficients(lambda z: np.exp(tau * z), center, d, imag, nq)[: kmax + 1]
     bp = chebyshev_coefficients(lambda z: tau * phi1(tau * z), center, d, imag, nq)[: kmax + 1]
