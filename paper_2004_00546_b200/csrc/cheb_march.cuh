@@ -1,0 +1,242 @@
+// cheb_march.cuh — M Chebyshev terms per pass, row-marching (2D).
+//
+// Replaces the reference's Newton–Leja loop (timestepping.py:343-356: one CSR
+// matvec + two norms per term) by the planned Chebyshev series of
+// exp(τM)·v (and τφ₁(τM)·v) with the stencil fused into the three-term
+// recurrence
+//     U_1 = (M − c0)U_0 / d,   U_{j+1} = (2/d)(M − c0)U_j + σ·U_{j−1},
+//     acc += b_j U_j,  pacc += p_j U_j.
+// A pass computes terms k+1 … k+M for one strip/band of a field: term s of the
+// pass works on row r−s while row r of U_k streams in, so only U_{k−1}, U_k,
+// acc, pacc are read and U_{k+M−1}, U_{k+M}, acc, pacc written once per pass —
+// ≈ (4+4)·8n bytes per M terms instead of 56n per term. The x neighbours of each
+// term's input row are exchanged through shared memory (even/odd split arrays,
+// double buffered, one barrier per row); vertical neighbours and the per-row
+// acc/pacc values live in register queues (the loop is unrolled so the queues
+// rotate by renaming).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+#include "rk4.cuh"
+
+namespace px {
+
+constexpr int CM_NT = 160;  // 5 warps, pairs of columns: computed width ≤ 320
+constexpr int CM_MAXT = 4;  // terms per pass (template M ≤ CM_MAXT)
+constexpr int CM_DEPTH = 5; // cp.async ring depth (rows)
+
+struct ChebMarchArgs {
+  const double* u_prev; long long prev_bs;  // U_{k−1} (unused on the first pass)
+  const double* u_cur; long long cur_bs;    // U_k (first pass: U_0)
+  const double* addend; long long add_bs;   // first pass only, may be null
+  double* acc;                              // B × n (in/out; first pass: out)
+  double* pacc;                             // B × n in/out, may be null
+  double* out_prev;                         // U_{k+M−1} (null on the last pass)
+  double* out_cur;                          // U_{k+M}
+  Stencil5 st;
+  double c0, d, two_over_d, sigma;
+  double be[CM_MAXT + 1], bp[CM_MAXT + 1];  // coefficients of terms k … k+M
+  int first;
+  int nx, ny, B;
+  int strip_w, halo, nstrips, band_rows, nbands;
+};
+
+template <int M>
+struct CmUnroll {
+  static constexpr int value = (M == 4) ? 12 : 6;  // lcm(3, 2, M)
+};
+
+template <int M>
+__global__ void __launch_bounds__(CM_NT, 2) k_cheb_march(ChebMarchArgs a) {
+  __shared__ double pubE[2][M][CM_NT];
+  __shared__ double pubO[2][M][CM_NT];
+  // ring slots (dynamic smem): [depth][4 arrays: cur(r), prev(r−1), acc(r−1), pacc(r−1)][pairs]
+  extern __shared__ double2 cm_ring[];
+  constexpr int UN = CmUnroll<M>::value;
+
+  const int b = blockIdx.x % a.B;
+  const int rest = blockIdx.x / a.B;
+  const int strip = rest % a.nstrips;
+  const int band = rest / a.nstrips;
+  const int nx = a.nx, ny = a.ny;
+  const size_t n = (size_t)nx * ny;
+  const int x0 = strip * a.strip_w;
+  const int U = min(a.strip_w, nx - x0);
+  const int CW = U + 2 * a.halo;
+  const int T = CW >> 1;
+  const int t = threadIdx.x;
+  const bool active = t < T;
+  const int tc = active ? t : 0;
+  const int gx = (((x0 - a.halo + 2 * tc) % nx) + nx) % nx;
+  const int j0 = band * a.band_rows;
+  const int rows_out = min(a.band_rows, ny - j0);
+  const int iters = rows_out + 2 * M;
+  const bool full_row = a.halo == 0;
+  const int tl = (t == 0) ? (full_row ? T - 1 : 0) : t - 1;
+  const int tr = (t + 1 >= T) ? (full_row ? 0 : T - 1) : t + 1;
+  const bool store_ok = active && (2 * t >= a.halo) && (2 * t + 1 < CW - a.halo);
+  const bool first = a.first != 0;
+  const bool has_add = first && a.addend != nullptr;
+  const bool has_p = a.pacc != nullptr;
+  const bool write_u = a.out_cur != nullptr;
+
+  const Stencil5 st = a.st;
+  const double c0 = a.c0, d = a.d, tod = a.two_over_d, sig = a.sigma;
+  const double* __restrict__ cur = a.u_cur + b * a.cur_bs;
+  const double* __restrict__ prv = first ? cur : a.u_prev + b * a.prev_bs;
+  const double* __restrict__ accin = has_add ? a.addend + b * a.add_bs : a.acc + (size_t)b * n;
+  double* __restrict__ accout = a.acc + (size_t)b * n;
+  double* __restrict__ pac = has_p ? a.pacc + (size_t)b * n : nullptr;
+  double* __restrict__ oprev = write_u ? a.out_prev + (size_t)b * n : nullptr;
+  double* __restrict__ ocur = write_u ? a.out_cur + (size_t)b * n : nullptr;
+  const bool read_acc = !first || has_add;
+
+  auto wrapr = [&](int row) -> int {
+    row %= ny;
+    return row < 0 ? row + ny : row;
+  };
+  const int r0 = j0 - M;
+  const size_t coloff = (size_t)gx;
+  int iss_k = 0, iss_slot = 0;
+  int rc = wrapr(r0), rl = wrapr(r0 - 1);  // streams: cur row r, lagged rows r−1
+  auto issue = [&]() {
+    if (iss_k < iters) {
+      double2* sl = cm_ring + (size_t)iss_slot * 4 * CM_NT;
+      cp_async16(sl + t, cur + (size_t)rc * nx + coloff);
+      if (!first) cp_async16(sl + CM_NT + t, prv + (size_t)rl * nx + coloff);
+      if (read_acc) cp_async16(sl + 2 * CM_NT + t, accin + (size_t)rl * nx + coloff);
+      if (has_p) cp_async16(sl + 3 * CM_NT + t, pac + (size_t)rl * nx + coloff);
+    }
+    cp_async_commit();
+    ++iss_k;
+    iss_slot = (iss_slot + 1 == CM_DEPTH) ? 0 : iss_slot + 1;
+    rc = (rc + 1 == ny) ? 0 : rc + 1;
+    rl = (rl + 1 == ny) ? 0 : rl + 1;
+  };
+#pragma unroll
+  for (int k = 0; k < CM_DEPTH; ++k) issue();
+  int rslot = 0;
+  int rs = wrapr(r0 - M);  // output row r − M
+
+  double2 q0[3];               // U_k rows (ring by phase mod 3)
+  double2 qs[M + 1][2];        // stage-s outputs, last two rows (index 1..M)
+  double2 qa[M], qp[M];        // acc / pacc of rows r−1 … r−M (ring by phase mod M)
+#pragma unroll
+  for (int k = 0; k < 3; ++k) q0[k] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int s = 0; s <= M; ++s) qs[s][0] = qs[s][1] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int s = 0; s < M; ++s) qa[s] = qp[s] = make_double2(0.0, 0.0);
+
+  // (M − c0)·u for the pair (c centre, s south, nn north, l/r x-neighbours)
+  auto shifted = [&](double2 c, double2 s, double2 nn, double l, double r) -> double2 {
+    double2 o;
+    o.x = st.cc * c.x;
+    o.x += st.ce * c.y;
+    o.x += st.cw * l;
+    o.x += st.cn * nn.x;
+    o.x += st.cs * s.x;
+    o.x -= c0 * c.x;
+    o.y = st.cc * c.y;
+    o.y += st.ce * r;
+    o.y += st.cw * c.x;
+    o.y += st.cn * nn.y;
+    o.y += st.cs * s.y;
+    o.y -= c0 * c.y;
+    return o;
+  };
+
+  for (int i0 = 0; i0 < iters; i0 += UN) {
+#pragma unroll
+    for (int k = 0; k < UN; ++k) {
+      const int i = i0 + k;
+      if (i >= iters) break;
+      const int pin = (k + 1) & 1;
+      const int pout = k & 1;
+      cp_async_wait<CM_DEPTH - 1>();
+      const double2* sl = cm_ring + (size_t)rslot * 4 * CM_NT;
+      rslot = (rslot + 1 == CM_DEPTH) ? 0 : rslot + 1;
+      const double2 ur = sl[t];
+      const double2 upv = first ? make_double2(0.0, 0.0) : sl[CM_NT + t];
+      const double2 ain = read_acc ? sl[2 * CM_NT + t] : make_double2(0.0, 0.0);
+      const double2 pin_v = has_p ? sl[3 * CM_NT + t] : make_double2(0.0, 0.0);
+      issue();
+      q0[k % 3] = ur;
+      const double2 u0m2 = q0[(k + 1) % 3], u0m1 = q0[(k + 2) % 3];  // rows r−2, r−1
+      const int po = k & 1, pp = (k + 1) & 1;  // qs[s][po]: row of iteration i−2, [pp]: i−1
+      double2 nq[M + 1];
+      nq[0] = ur;
+      // term 1 of the pass at row r−1 (creates the acc/pacc entry of that row)
+      if (i >= 2) {
+        const double l = pubO[pin][0][tl], r = pubE[pin][0][tr];
+        const double2 sh = shifted(u0m1, u0m2, ur, l, r);
+        double2 u1, acc, pc;
+        if (first) {
+          u1 = make_double2(sh.x / d, sh.y / d);
+          acc.x = a.be[0] * u0m1.x + a.be[1] * u1.x + ain.x;
+          acc.y = a.be[0] * u0m1.y + a.be[1] * u1.y + ain.y;
+          pc.x = pin_v.x + (a.bp[0] * u0m1.x + a.bp[1] * u1.x);
+          pc.y = pin_v.y + (a.bp[0] * u0m1.y + a.bp[1] * u1.y);
+        } else {
+          u1 = make_double2(tod * sh.x + sig * upv.x, tod * sh.y + sig * upv.y);
+          acc = make_double2(ain.x + a.be[1] * u1.x, ain.y + a.be[1] * u1.y);
+          pc = make_double2(pin_v.x + a.bp[1] * u1.x, pin_v.y + a.bp[1] * u1.y);
+        }
+        nq[1] = u1;
+        qa[k % M] = acc;
+        qp[k % M] = pc;
+      } else {
+        nq[1] = make_double2(0.0, 0.0);
+      }
+      // terms 2 … M of the pass at rows r−s
+#pragma unroll
+      for (int s = 2; s <= M; ++s) {
+        if (i >= 2 * s) {
+          const double l = pubO[pin][s - 1][tl], r = pubE[pin][s - 1][tr];
+          const double2 c = qs[s - 1][pp];        // row r−s
+          const double2 so = qs[s - 1][po];       // row r−s−1
+          const double2 sh = shifted(c, so, nq[s - 1], l, r);
+          const double2 pv = (s == 2) ? u0m2 : qs[s - 2][po];  // U_{k+s−2} at row r−s
+          const double2 u = make_double2(tod * sh.x + sig * pv.x, tod * sh.y + sig * pv.y);
+          nq[s] = u;
+          const int ai = (k - s + 1 + 2 * M) % M;  // acc slot of row r−s
+          qa[ai].x += a.be[s] * u.x;
+          qa[ai].y += a.be[s] * u.y;
+          qp[ai].x += a.bp[s] * u.x;
+          qp[ai].y += a.bp[s] * u.y;
+        } else {
+          nq[s] = make_double2(0.0, 0.0);
+        }
+      }
+      // row r−M is complete: acc, pacc, and the pass's last two terms
+      if (i >= 2 * M && store_ok) {
+        const size_t off = (size_t)rs * nx + coloff;
+        const int ai = (k - M + 1 + 2 * M) % M;
+        __stcs(reinterpret_cast<double2*>(accout + off), qa[ai]);
+        if (has_p) __stcs(reinterpret_cast<double2*>(pac + off), qp[ai]);
+        if (write_u) {
+          const double2 up = (M == 1) ? u0m1 : qs[M - 1][pp];
+          __stcs(reinterpret_cast<double2*>(oprev + off), up);
+          __stcs(reinterpret_cast<double2*>(ocur + off), nq[M]);
+        }
+      }
+      rs = (rs + 1 == ny) ? 0 : rs + 1;
+#pragma unroll
+      for (int s = 1; s <= M; ++s) qs[s][po] = nq[s];
+      if (active) {
+#pragma unroll
+        for (int s = 0; s < M; ++s) {
+          pubE[pout][s][t] = nq[s].x;
+          pubO[pout][s][t] = nq[s].y;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  cp_async_wait<0>();
+}
+
+constexpr size_t CM_SMEM = (size_t)CM_DEPTH * 4 * CM_NT * sizeof(double2);
+
+}  // namespace px

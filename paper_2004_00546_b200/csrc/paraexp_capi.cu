@@ -27,6 +27,9 @@
 #include "burgers.cuh"
 #include "krylov.cuh"
 #include "rk4.cuh"
+#include "cheb_march.cuh"
+
+#include <cstdlib>
 
 namespace {
 
@@ -62,7 +65,7 @@ struct Handle {
   double *Y0 = nullptr, *Y1 = nullptr, *Z = nullptr;
   const double *vend = nullptr, *wend = nullptr;
   // exp-action work
-  double* Wk[3] = {nullptr, nullptr, nullptr};
+  double* Wk[4] = {nullptr, nullptr, nullptr, nullptr};
   double* ACC[2] = {nullptr, nullptr};
   // outputs
   double *UT = nullptr, *QT = nullptr, *QDAG0 = nullptr, *G = nullptr;
@@ -280,6 +283,116 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
 // Chebyshev action over B vectors (batch-strided input)
 // ---------------------------------------------------------------------------
 
+
+// 2D: Chebyshev action by row-marching passes of up to CM_MAXT fused terms (cheb_march.cuh)
+template <int M>
+int launch_cm(Handle* h, const px::ChebMarchArgs& a, unsigned blocks, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    PX_CUDA(h, cudaFuncSetAttribute(px::k_cheb_march<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)px::CM_SMEM));
+    attr = true;
+  }
+  px::k_cheb_march<M><<<blocks, px::CM_NT, px::CM_SMEM, s>>>(a);
+  PX_CHECK_LAUNCH(h);
+  return PX_OK;
+}
+
+int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const double* src, long long src_bs,
+                      const double* addend, long long add_bs, double* pacc, double** result, cudaStream_t s) {
+  const size_t n = h->n;
+  const int B = h->B;
+  const long long nb = (long long)n;
+  const int nx = h->d.nx, ny = h->d.ny;
+  px::ChebMarchArgs a{};
+  a.st = st;
+  a.c0 = pl.center; a.d = pl.scale; a.two_over_d = 2.0 / pl.scale; a.sigma = (double)pl.sigma;
+  a.nx = nx; a.ny = ny; a.B = B;
+  static int env_strip = -1, env_band = -1;
+  if (env_strip < 0) {
+    const char* e1 = getenv("PX_CM_STRIP");
+    const char* e2 = getenv("PX_CM_BAND");
+    env_strip = e1 ? atoi(e1) : 0;
+    env_band = e2 ? atoi(e2) : 0;
+  }
+  if (nx <= 2 * px::CM_NT && env_strip == 0) {
+    a.strip_w = nx; a.halo = 0; a.nstrips = 1;
+  } else {
+    a.strip_w = env_strip > 0 ? env_strip : 256;
+    a.halo = px::CM_MAXT;
+    a.nstrips = (nx + a.strip_w - 1) / a.strip_w;
+  }
+  int br;
+  if (env_band > 0) {
+    br = env_band;
+  } else {
+    // about one full wave of 2 CTAs per SM, bands of ≥ 32 rows
+    const size_t per_band_ctas = (size_t)a.nstrips * B;
+    const size_t target = 2 * 148;
+    size_t nb_bands = std::max<size_t>(1, target / per_band_ctas);
+    br = (int)((ny + nb_bands - 1) / nb_bands);
+    if (br < 32) br = std::min(32, ny);
+  }
+  a.band_rows = br;
+  a.nbands = (ny + br - 1) / br;
+  const unsigned blocks = (unsigned)((size_t)B * a.nstrips * a.nbands);
+  const int K = pl.degree;
+  int wsel = 0;  // rotating pair of U output buffers
+  for (int sub = 0; sub < pl.substeps; ++sub) {
+    double* acc = (src == h->ACC[0]) ? h->ACC[1] : h->ACC[0];
+    const double* uprev = nullptr;
+    long long uprev_bs = 0;
+    const double* ucur = src;
+    long long ucur_bs = src_bs;
+    int k = 0;  // terms done
+    bool first = true;
+    while (k < K || first) {
+      const int M = std::min(px::CM_MAXT, K - k);
+      a.first = first ? 1 : 0;
+      a.u_prev = uprev; a.prev_bs = uprev_bs;
+      a.u_cur = ucur; a.cur_bs = ucur_bs;
+      a.addend = (first && sub == pl.substeps - 1) ? addend : nullptr;
+      a.add_bs = add_bs;
+      a.acc = acc;
+      a.pacc = pacc;
+      const bool last = (k + M >= K);
+      double* o0 = h->Wk[2 * wsel];
+      double* o1 = h->Wk[2 * wsel + 1];
+      a.out_prev = last ? nullptr : o0;
+      a.out_cur = last ? nullptr : o1;
+      for (int j = 0; j <= px::CM_MAXT; ++j) {
+        const int term = k + j;
+        a.be[j] = (j <= M && term <= K && (j > 0 || first)) ? pl.be[term] : 0.0;
+        a.bp[j] = (pacc && j <= M && term <= K && (j > 0 || first)) ? pl.bp[term] : 0.0;
+      }
+      int rc;
+      switch (M) {
+        case 1: rc = launch_cm<1>(h, a, blocks, s); break;
+        case 2: rc = launch_cm<2>(h, a, blocks, s); break;
+        case 3: rc = launch_cm<3>(h, a, blocks, s); break;
+        default: rc = launch_cm<4>(h, a, blocks, s); break;
+      }
+      if (rc != PX_OK) return rc;
+      // algorithmic bytes of the pass (streams read + written once)
+      const int nrd = 1 + (first ? 0 : 1) + ((!first || a.addend) ? 1 : 0) + (pacc ? 1 : 0);
+      const int nwr = 1 + (pacc ? 1 : 0) + (last ? 0 : 2);
+      const double bytes = 8.0 * (nrd + nwr) * (double)n * B;
+      h->stats.exp_bytes += bytes;
+      h->stats.algorithmic_bytes += bytes;
+      uprev = o0; uprev_bs = nb;
+      ucur = o1; ucur_bs = nb;
+      wsel ^= 1;
+      k += M;
+      first = false;
+    }
+    src = acc;
+    src_bs = nb;
+  }
+  h->stats.exp_terms += (uint64_t)pl.substeps * pl.degree * B;
+  *result = const_cast<double*>(src);
+  return PX_OK;
+}
+
 // result <- exp(span·M)·src (+ addend);  pacc += span·φ₁(span·M)·src  (if pacc)
 int cheb_action(Handle* h, const Plan& pl, const px::Stencil5& st, const double* src, long long src_bs,
                 const double* addend, long long add_bs, double* pacc, double** result, cudaStream_t s) {
@@ -288,6 +401,7 @@ int cheb_action(Handle* h, const Plan& pl, const px::Stencil5& st, const double*
   const int B = h->B;
   const dim3 grid = grid1(n, B);
   const long long nb = (long long)n;
+  if (h->dim == 2 && (h->d.nx % 2) == 0) return cheb_action_march(h, pl, st, src, src_bs, addend, add_bs, pacc, result, s);
   for (int sub = 0; sub < pl.substeps; ++sub) {
     double* acc = (src == h->ACC[0]) ? h->ACC[1] : h->ACC[0];
     px::ChebFirstArgs fa{};
@@ -563,7 +677,7 @@ int px_create(const px_problem_desc* desc, void** out_handle) {
   h->red_blocks = (int)std::min<size_t>((n + 255) / 256, 1024);
   A(&h->partial, B * h->red_blocks);
   if (rc == PX_OK) rc = dalloc_t(h, &h->nonfinite, 1);
-  for (int i = 0; i < 3; ++i) A(&h->Wk[i], B * n);
+  for (int i = 0; i < 4; ++i) A(&h->Wk[i], B * n);
   for (int i = 0; i < 2; ++i) A(&h->ACC[i], B * n);
   if (d.kind == PX_KIND_ADVDIFF) {
     A(&h->g, B * n);

@@ -40,6 +40,17 @@ def current_stream_handle() -> int:
     return 0
 
 
+def check_rk4_stability(region, h: float) -> None:
+    """Raise ConfigError if the classical RK4 step h is unstable on the spectral
+    enclosure: max |R(hλ)| over its boundary > 1 (R(z) = 1 + z + z²/2 + z³/6 + z⁴/24)."""
+    z = h * region.boundary(2048)
+    R = 1 + z * (1 + z * (0.5 + z * (1.0 / 6.0 + z / 24.0)))
+    amp = float(np.max(np.abs(R)))
+    if amp > 1.0 + 1e-9:
+        raise ConfigError(f"RK4 step h={h:.3g} is unstable on this operator (max |R(hλ)| = {amp:.4g}); "
+                          "decrease dt")
+
+
 class _DeviceView:
     """__cuda_array_interface__ over a native device buffer (for torch/NCCL)."""
 
@@ -77,6 +88,8 @@ class ParaexpEngine:
             raise ConfigError(f"world={spec.world} exceeds P={spec.P} slices")
         p0, p1 = rank_block(spec.P, spec.rank, spec.world)
         self.p0, self.p1 = p0, p1
+        if sysm.is_linear:
+            check_rk4_stability(sysm.region(), sysm.spec.T / spec.P / spec.nsteps)
         self.n = grid.npoints
         self.B = spec.batch
         self.K = sysm.basis.K

@@ -150,6 +150,14 @@ def test_non_multiple_tile_grid():
     _check(_gpu_linear(c1), _oracle_linear(c1))
 
 
+def test_strip_mode_2d():
+    """nx > 576: the RK4 march runs in 512-column strips with a 4-column halo and the
+    Chebyshev march in 256-column strips (last strips partial); nx·ny beyond one CTA row."""
+    from paper_2004_00546_b200 import baseline, scaled
+    c = scaled(baseline(5), nx=640, P=8, steps_per_slice=10, K=16)  # h·ρ ≈ 1.9 (RK4-stable)
+    _check(_gpu_linear(c), _oracle_linear(c))
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_blockscan_ranks_emulated(world):
     """World-`world` sharding on one GPU: ranks run one after another (no rank waits on

@@ -242,3 +242,11 @@ def test_burgers_gradient_vs_fd_within_frozen_model_error():
     assert rel_l2(res.grad[0], fd) < 2e-3
     rb = burgers_gradient(g.nx, spec.D, sysm.basis, 1.0, P, ns, u0, ut, ctrl, planf, regf, world=2)
     assert rel_l2(rb.grad, res.grad) < 1e-13
+
+
+def test_unstable_rk4_step_is_rejected_before_any_gpu_work():
+    from paper_2004_00546_b200 import ConfigError, baseline, scaled
+    from paper_2004_00546_b200.engine import EngineSpec, ParaexpEngine
+    c = scaled(baseline(5), nx=640, P=4, steps_per_slice=3, K=16)  # h·ρ ≈ 13
+    with pytest.raises(ConfigError):
+        ParaexpEngine(EngineSpec(c.system, c.P, c.dt, c.expaction))
