@@ -41,6 +41,8 @@ import numpy as np
 from paper_2004_00546_b200.expaction import ChebPlan, KrylovPlan
 from paper_2004_00546_b200.partition import rank_block
 
+from .reference_mode import chains_adjoint, chains_direct
+
 # ---------------------------------------------------------------------------
 # Operators
 # ---------------------------------------------------------------------------
@@ -250,15 +252,16 @@ def linear_gradient(grid_nx, grid_ny, A, basis, T, P, nsteps, u0, u_target, ctrl
     v_end, _ = rk4_linear(applyA, g, h, nsteps)
 
     u_bnd = None
+    bounds = T * np.arange(P + 1) / P
     if formulation == "chains":
-        # reference neighbour form: slice p's end state is carried by its own chain
-        total = np.zeros_like(v_end)
-        for p in range(P):
-            c = v_end
-            for _ in range(P - 1 - p):
-                c = exp_action(applyA, plan_slice, c)
-            total = total + c
-        uT = u0 + total
+        # the reference's neighbour-chain structure (reference_mode.chains_direct,
+        # pinned to `solve_direct_linear`) with RK4 slices and Chebyshev chains
+        zero_end = np.stack([np.zeros_like(v_end), v_end])
+        pieces = chains_direct(
+            bounds, u0, lambda p: (bounds[p:p + 2], zero_end),
+            lambda p, start, m: (lambda e: (e, e[None]))(exp_action(applyA, plan_slice, start)),
+            lambda p: bounds[p:p + 2])
+        uT = pieces[-1][1][-1]
     elif formulation == "scan" and world == 1:
         D = np.zeros_like(v_end)
         if want_boundary:
@@ -288,14 +291,15 @@ def linear_gradient(grid_nx, grid_ny, A, basis, T, P, nsteps, u0, u_target, ctrl
     gadj = applyAT(qT)
     w_end, z = rk4_linear(applyAT, gadj, h, nsteps, want_z=True)
     if formulation == "chains":
-        qd = np.zeros_like(w_end)
+        # reference_mode.chains_adjoint (pinned to `solve_adjoint_linear`); the φ₁
+        # accumulator collects ∫ of every homogeneous chain piece
         Gh = np.zeros_like(w_end)
-        for p in range(P):   # chain of slice p's end, run down to t = 0
-            c = w_end
-            for _ in range(p):
-                c = exp_action(applyAT, plan_slice, c, Gh)
-            qd = qd + c
-        qdag0 = qT + qd
+        zero_end = np.stack([np.zeros_like(w_end), w_end])
+        pieces = chains_adjoint(
+            bounds, qT, lambda p: (bounds[p:p + 2], zero_end),
+            lambda p, start, m: (lambda e: (e, e[None]))(exp_action(applyAT, plan_slice, start, Gh)),
+            lambda p: bounds[p:p + 2])
+        qdag0 = pieces[0][1][0]
         G = T * qT + P * z + Gh
     elif formulation == "scan" and world == 1:
         C = np.zeros_like(w_end)
