@@ -420,3 +420,84 @@ def burgers_gradient(nx, D, basis, T, P, nsteps, u0, u_target, ctrl, plan_for_re
     grad = basis.project(G)
     return OracleResult(J=J, grad=grad, uT=uT, qdag0=qdag0, G=G,
                         extras={"traj": traj, "ubar": ubar, "plan": plan, "w_end": w_end})
+
+
+# ---------------------------------------------------------------------------
+# Per-rank partials with the C ABI's conventions (for the gloo tests of the
+# product's multi-rank orchestration, engine.distributed_gradient)
+# ---------------------------------------------------------------------------
+
+
+class OracleRank:
+    """A CPU stand-in for one rank's ParaexpEngine: same phase methods and field
+    buffers (torch CPU tensors), computed with the oracle's block-scan pieces."""
+
+    FIELDS = ("J", "GRAD", "UT", "QDAG0", "G")
+
+    def __init__(self, nx, ny, A, basis, T, P, nsteps, u0, u_target, ctrl, plan_slice, plan_long, rank, world):
+        import torch
+        self.nx, self.ny, self.T, self.P, self.nsteps = nx, ny, T, P, nsteps
+        self.A = tuple(A)
+        self.AT = tuple(np.asarray(A)[[0, 2, 1, 4, 3]])
+        self.basis = basis
+        n = nx * ny
+        self.ctrl = np.atleast_2d(np.asarray(ctrl, dtype=np.float64))
+        B = self.ctrl.shape[0]
+        self.u0 = np.broadcast_to(_as_batch(u0, n), (B, n))
+        self.ut = np.broadcast_to(_as_batch(u_target, n), (B, n))
+        self.plan_slice, self.plan_long = plan_slice, plan_long
+        self.p0, self.p1 = rank_block(P, rank, world)
+        self.buf = {k: torch.zeros(B * (basis.K if k == "GRAD" else (1 if k == "J" else n)), dtype=torch.float64)
+                    for k in self.FIELDS}
+        self.B, self.n = B, n
+
+    def _np(self, k):
+        return self.buf[k].numpy().reshape(self.B, -1)
+
+    def view(self, k):
+        return self.buf[k]
+
+    @staticmethod
+    def direct_reduce_fields():
+        return ["UT"]
+
+    @staticmethod
+    def adjoint_reduce_fields(want_fields=True):
+        return ["GRAD"] + (["QDAG0", "G"] if want_fields else [])
+
+    def direct_partial(self, stream=None):
+        applyA = lambda u: stencil_apply(self.A, u, self.nx, self.ny)
+        h = self.T / self.P / self.nsteps
+        g = applyA(self.u0) + self.basis.field(self.ctrl)
+        v_end, _ = rk4_linear(applyA, g, h, self.nsteps)
+        D = np.zeros_like(v_end)
+        for p in range(self.p0, self.p1):
+            D = v_end.copy() if p == self.p0 else exp_action(applyA, self.plan_slice, D) + v_end
+        if self.p1 < self.P:
+            D = exp_action(applyA, self.plan_long((self.P - self.p1) * self.T / self.P), D)
+        self._np("UT")[:] = D
+
+    def finish_direct(self, stream=None):
+        uT = self._np("UT")
+        uT += self.u0
+        self.qT = uT - self.ut
+        self._np("J")[:, 0] = 0.5 * np.sum(self.qT * self.qT, axis=1)
+
+    def adjoint_partial(self, stream=None):
+        applyAT = lambda u: stencil_apply(self.AT, u, self.nx, self.ny)
+        h = self.T / self.P / self.nsteps
+        w_end, z = rk4_linear(applyAT, applyAT(self.qT), h, self.nsteps, want_z=True)
+        C = np.zeros_like(w_end)
+        Gr = (self.p1 - self.p0) * z
+        for p in range(self.p1 - 1, self.p0 - 1, -1):
+            C = w_end.copy() if p == self.p1 - 1 else exp_action(applyAT, self.plan_slice, C, Gr) + w_end
+        if self.p0 > 0:
+            C = exp_action(applyAT, self.plan_long(self.p0 * self.T / self.P), C, Gr)
+        self._np("QDAG0")[:] = C
+        self._np("G")[:] = Gr
+        self._np("GRAD")[:] = self.basis.project(Gr)
+
+    def finish_adjoint(self, stream=None):
+        self._np("QDAG0")[:] += self.qT
+        self._np("G")[:] += self.T * self.qT
+        self._np("GRAD")[:] += self.T * self.basis.project(self.qT)

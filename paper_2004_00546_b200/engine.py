@@ -76,6 +76,31 @@ class EngineSpec:
         return slice_steps(self.system.spec.T / self.P, self.dt)
 
 
+def allreduce_sum(tensors, group=None) -> None:
+    """In-place SUM allreduce of each tensor over the process group (NCCL on GPU)."""
+    import torch.distributed as dist
+    for t in tensors:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+
+def distributed_gradient(eng, stream=None, group=None, want_fields: bool = True, reduce=allreduce_sum) -> None:
+    """One sharded gradient evaluation: each rank runs its slice
+    block, the u(T) partials are summed, every rank finishes the direct sweep
+    identically, runs its adjoint block and the adjoint partials are summed.
+
+    ``eng`` provides ``direct_partial / finish_direct / adjoint_partial /
+    finish_adjoint`` and ``view(field)`` (a tensor aliasing the field's buffer);
+    the partial conventions are the C ABI's (`px_finish_*` add the q0 / q†_T terms
+    once, after the reduction).
+    """
+    eng.direct_partial(stream)
+    reduce([eng.view(f) for f in eng.direct_reduce_fields()], group)
+    eng.finish_direct(stream)
+    eng.adjoint_partial(stream)
+    reduce([eng.view(f) for f in eng.adjoint_reduce_fields(want_fields)], group)
+    eng.finish_adjoint(stream)
+
+
 class ParaexpEngine:
     """Owns one ``px_handle``; computes gradients of J = ½‖u(T) − u_target‖²."""
 
@@ -183,6 +208,9 @@ class ParaexpEngine:
         N.check(self.lib, self.lib.px_buffer(self.h, field, ctypes.byref(p), ctypes.byref(cnt)), self.h)
         return int(cnt.value)
 
+    def view(self, field: int):
+        return self.device_view(field)
+
     def device_view(self, field: int):
         """Torch CUDA tensor aliasing a native device buffer (no copy)."""
         torch = _torch()
@@ -218,15 +246,8 @@ class ParaexpEngine:
 
     # -- phases --------------------------------------------------------------
 
-    def _allreduce(self, fields, group=None):
-        if self.spec.world == 1:
-            return
-        import torch.distributed as dist
-        for f in fields:
-            dist.all_reduce(self.device_view(f), op=dist.ReduceOp.SUM, group=group)
-
     # Phase-level entry points (a rank's partial, then the finish after the caller's
-    # reduction). ``run_direct``/``run_adjoint`` chain them with an NCCL allreduce.
+    # reduction). ``distributed_gradient`` chains them with an NCCL allreduce.
 
     def direct_partial(self, stream: int | None = None) -> None:
         s = current_stream_handle() if stream is None else stream
@@ -253,11 +274,6 @@ class ParaexpEngine:
     def adjoint_reduce_fields(want_fields: bool = True) -> list[int]:
         return [N.PX_FIELD_GRAD] + ([N.PX_FIELD_QDAG0, N.PX_FIELD_G] if want_fields else [])
 
-    def run_direct(self, stream: int | None = None, group=None) -> None:
-        s = current_stream_handle() if stream is None else stream
-        self.direct_partial(s)
-        self._allreduce(self.direct_reduce_fields(), group)
-        self.finish_direct(s)
 
     def plan_frozen(self, stream: int | None = None) -> ChebPlan:
         """Burgers: read the frozen-operator FOV union, plan on the host (cached)."""
@@ -270,11 +286,6 @@ class ParaexpEngine:
         self._set_plan(N.PX_PLAN_FROZEN, plan)
         return plan
 
-    def run_adjoint(self, stream: int | None = None, group=None, want_fields: bool = True) -> None:
-        s = current_stream_handle() if stream is None else stream
-        self.adjoint_partial(s)
-        self._allreduce(self.adjoint_reduce_fields(want_fields), group)
-        self.finish_adjoint(s)
 
     def set_adjoint_terminal(self, qdag_T, stream: int | None = None) -> None:
         s = current_stream_handle() if stream is None else stream
@@ -290,8 +301,13 @@ class ParaexpEngine:
         if self.spec.world == 1 and self.spec.system.is_linear:
             N.check(self.lib, self.lib.px_gradient(self.h, s), self.h)
             return
-        self.run_direct(s, group)
-        self.run_adjoint(s, group, want_fields)
+        if self.spec.world == 1:
+            self.direct_partial(s)
+            self.finish_direct(s)
+            self.adjoint_partial(s)
+            self.finish_adjoint(s)
+            return
+        distributed_gradient(self, s, group, want_fields)
 
     def results(self, stream: int | None = None) -> dict:
         J = self.get(N.PX_FIELD_J, stream)
