@@ -205,9 +205,9 @@ def cpu_reference_rate(cfg_index: int, reps: int = 1, workers: int | None = None
             per = sp.terms if not isinstance(sp, KrylovPlan) else sp.terms * 4  # Arnoldi ≈ 4 vector passes/step
             t += (Pl - 1) * per * (u["term"] + u["term_phi"])
             if p1 < c.P:
-                t += plan_for(region, (c.P - p1) * delta, c.expaction).terms * u["term"]
+                t += plan_for(region, (c.P - p1) * delta, c.expaction, base_span=delta).terms * u["term"]
             if p0 > 0:
-                t += plan_for(region, p0 * delta, c.expaction).terms * u["term_phi"]
+                t += plan_for(region, p0 * delta, c.expaction, base_span=delta).terms * u["term_phi"]
         worst = max(worst, t)
     rate = c.batch / worst
     sample = (f"per-unit oracle costs timed on the full {c.grid.nx}x{c.grid.ny} field by {W} concurrent "
@@ -235,7 +235,7 @@ def run_reference(args):
         return 0
     rates = []
     for i in range(args.warmup + args.steps):
-        rate, W, sample, _ = cpu_reference_rate(args.config, reps=1)
+        rate, W, sample, _ = cpu_reference_rate(args.config, reps=args.cpu_reps)
         if i >= args.warmup:
             rates.append(rate)
     v = statistics.median(rates)
@@ -270,10 +270,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-reps", type=int, default=3, help="oracle unit repetitions per CPU worker (~3 s each)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="warmup+steps only (for ncu); no extras")
     args = ap.parse_args()
-    if args.warmup < 3 and not args.profile_only:
+    if args.warmup < 3 and not args.profile_only and args.impl != "reference":
         args.warmup = 3
 
     if args.impl == "reference":
@@ -343,9 +344,15 @@ def main():
     avg_launch_s = (ph["ms"] / 1e3) / max(ph["launches"], 1)
     bytes_per_launch = ph["bytes"] / max(ph["launches"], 1)
     achieved = bytes_per_launch / avg_launch_s / 1e9 if avg_launch_s > 0 else 0.0
-    kernel_name = {"rk4_direct": "k_rk4_tile<2,...,false>", "rk4_adjoint": "k_rk4_tile<2,...,true>",
-                   "exp_direct": "k_cheb_term<2>", "exp_adjoint": "k_cheb_term<2>+phi",
-                   "other": "reductions"}[dom]
+    two_d = c.grid.dim == 2
+    kernel_name = {"rk4_direct": "k_rk4_march<false>" if two_d else "k_rk4_lane1d<false>",
+                   "rk4_adjoint": "k_rk4_march<true>" if two_d else "k_rk4_lane1d<true>",
+                   "exp_direct": "k_cheb_march<M>" if two_d else "k_scan1d",
+                   "exp_adjoint": "k_cheb_march<M>+phi" if two_d else "k_scan1d+phi",
+                   "other": "reductions/projection"}[dom]
+    if not c.system.is_linear:
+        kernel_name = {"rk4_direct": "k_burgers_direct", "rk4_adjoint": "k_burgers_adjoint_rk4+k_burgers_scan"}.get(
+            dom, kernel_name)
     roofline = {"bound": "hbm", "kernel": kernel_name, "phase": dom, "achieved": achieved, "peak": peak,
                 "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                 "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_s * 1e3,
@@ -384,7 +391,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, W, sample, units = cpu_reference_rate(args.config, reps=1)
+        rate, W, sample, units = cpu_reference_rate(args.config, reps=args.cpu_reps)
         cpu = {"value": rate, "unit": UNIT, "cores": W, "kind": "port", "sample": sample,
                "unit_seconds": units}
 

@@ -28,6 +28,7 @@
 #include "krylov.cuh"
 #include "rk4.cuh"
 #include "cheb_march.cuh"
+#include "scan1d.cuh"
 
 #include <cstdlib>
 
@@ -42,6 +43,7 @@ struct Plan {
   int substeps = 0, degree = 0, sigma = -1;
   double center = 0.0, scale = 1.0;
   std::vector<double> be, bp;
+  double* dcoef = nullptr;  // device copy: be[0..K], bp[0..K]
 };
 
 struct Handle {
@@ -503,6 +505,63 @@ int apply_plus_control(Handle* h, double* out, const double* x, long long xbs, c
 // Linear sweeps
 // ---------------------------------------------------------------------------
 
+// 1D linear sweeps: the whole carry recursion in one CTA per member (scan1d.cuh)
+bool use_scan1d(const Handle* h) {
+  const Plan& sl = h->plans[PX_PLAN_SLICE];
+  return h->dim == 1 && h->n <= 4096 && (!sl.set || !sl.krylov) &&
+         !(h->d.flags & PX_FLAG_BOUNDARY_STATES);
+}
+
+px::Scan1DPlan scan_plan(const Plan& pl) {
+  px::Scan1DPlan sp{};
+  if (!pl.set) return sp;
+  sp.be = pl.dcoef;
+  sp.bp = pl.dcoef + pl.degree + 1;
+  sp.degree = pl.degree;
+  sp.substeps = pl.substeps;
+  sp.sigma = pl.sigma;
+  sp.c0 = pl.center;
+  sp.d = pl.scale;
+  return sp;
+}
+
+int scan1d(Handle* h, bool adjoint, const double* lanes, double* out, double* pacc, int long_slot,
+           cudaStream_t s) {
+  px::Scan1DArgs a{};
+  a.lanes = lanes;
+  a.out = out;
+  a.pacc = pacc;
+  a.st = adjoint ? h->AT : h->A;
+  a.slice = scan_plan(h->plans[PX_PLAN_SLICE]);
+  a.use_long = long_slot >= 0 ? 1 : 0;
+  if (long_slot >= 0) {
+    if (!h->plans[long_slot].set || h->plans[long_slot].krylov)
+      return fail(h, PX_ERR_STATE, "long-span Chebyshev plan not set");
+    a.lng = scan_plan(h->plans[long_slot]);
+  }
+  a.adjoint = adjoint ? 1 : 0;
+  a.n = (int)h->n;
+  a.Pl = h->Pl;
+  if (h->Pl > 1 && !h->plans[PX_PLAN_SLICE].set) return fail(h, PX_ERR_STATE, "slice plan not set");
+  const int ppt = h->n <= 512 ? 1 : (h->n <= 1024 ? 2 : (h->n <= 2048 ? 4 : 8));
+  const int nt = (int)((h->n + ppt - 1) / ppt);
+  switch (ppt) {
+    case 1: px::k_scan1d<1><<<h->B, nt, 0, s>>>(a); break;
+    case 2: px::k_scan1d<2><<<h->B, nt, 0, s>>>(a); break;
+    case 4: px::k_scan1d<4><<<h->B, nt, 0, s>>>(a); break;
+    default: px::k_scan1d<8><<<h->B, nt, 0, s>>>(a); break;
+  }
+  PX_CHECK_LAUNCH(h);
+  uint64_t terms = (uint64_t)(h->Pl - 1) * h->plans[PX_PLAN_SLICE].substeps * h->plans[PX_PLAN_SLICE].degree;
+  if (long_slot >= 0) terms += (uint64_t)h->plans[long_slot].substeps * h->plans[long_slot].degree;
+  terms *= h->B;
+  h->stats.exp_terms += terms;
+  const double bytes = (adjoint ? 56.0 : 40.0) * (double)h->n * terms;
+  h->stats.exp_bytes += bytes;
+  h->stats.algorithmic_bytes += bytes;
+  return PX_OK;
+}
+
 int direct_linear(Handle* h, cudaStream_t s) {
   const long long nb = (long long)h->n;
   const long long lane_bs = (long long)h->Pl * nb;  // stride between batch members in lanes
@@ -514,6 +573,11 @@ int direct_linear(Handle* h, cudaStream_t s) {
   tend(h, tm, s);
   h->vend = vend;
   tm = tbegin(h, PX_PHASE_EXP_DIRECT, s);
+  if (use_scan1d(h)) {
+    PX_TRY(scan1d(h, false, vend, h->UT, nullptr, h->d.p_end < h->d.P ? PX_PLAN_LONG_DIRECT : -1, s));
+    tend(h, tm, s);
+    return PX_OK;
+  }
   const bool bnd = (h->d.flags & PX_FLAG_BOUNDARY_STATES) && h->UBND;
   const long long ubs = (long long)(h->d.P + 1) * nb;
   if (bnd) {
@@ -555,6 +619,14 @@ int adjoint_linear(Handle* h, cudaStream_t s) {
                                                               (double)h->Pl * h->d.nsteps, h->n,
                                                               h->z_valid ? 1 : 0);
   PX_CHECK_LAUNCH(h);
+  if (use_scan1d(h)) {
+    PX_TRY(scan1d(h, true, wend, h->QDAG0, h->G, h->d.p_begin > 0 ? PX_PLAN_LONG_ADJOINT : -1, s));
+    tend(h, tm, s);
+    tm = tbegin(h, PX_PHASE_OTHER, s);
+    PX_TRY(project(h, h->GRAD, h->G, nb, 1.0, 0.0, s));
+    tend(h, tm, s);
+    return PX_OK;
+  }
   const double* C = wend + (size_t)(h->Pl - 1) * h->n;
   long long C_bs = lane_bs;
   for (int q = h->Pl - 2; q >= 0; --q) {
@@ -719,6 +791,8 @@ void px_destroy(void* handle) {
   Handle* h = static_cast<Handle*>(handle);
   if (!h) return;
   for (void* p : h->allocs) cudaFree(p);
+  for (auto& pl : h->plans)
+    if (pl.dcoef) cudaFree(pl.dcoef);
   for (auto& m : h->marks) { cudaEventDestroy(m.a); cudaEventDestroy(m.b); }
   for (auto e : h->event_pool) cudaEventDestroy(e);
   px::krylov_free(h->kw);
@@ -758,6 +832,12 @@ int px_set_cheb_plan(void* handle, int slot, const px_cheb_plan* p) {
   pl.be.assign(p->coef_exp, p->coef_exp + p->degree + 1);
   if (p->coef_phi) pl.bp.assign(p->coef_phi, p->coef_phi + p->degree + 1);
   else pl.bp.assign(p->degree + 1, 0.0);
+  if (pl.dcoef) cudaFree(pl.dcoef);
+  pl.dcoef = nullptr;
+  PX_CUDA(h, cudaMalloc(&pl.dcoef, sizeof(double) * 2 * (p->degree + 1)));
+  PX_CUDA(h, cudaMemcpy(pl.dcoef, pl.be.data(), sizeof(double) * (p->degree + 1), cudaMemcpyHostToDevice));
+  PX_CUDA(h, cudaMemcpy(pl.dcoef + p->degree + 1, pl.bp.data(), sizeof(double) * (p->degree + 1),
+                        cudaMemcpyHostToDevice));
   return PX_OK;
 }
 

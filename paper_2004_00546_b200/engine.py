@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _native as N
 from .errors import ConfigError, IntegrationFailure, NativeUnavailable
-from .expaction import ChebPlan, ChebyshevConfig, KrylovConfig, KrylovPlan, plan_chebyshev, plan_krylov
+from .expaction import ChebPlan, ChebyshevConfig, KrylovConfig, KrylovPlan, plan_chebyshev, plan_for
 from .partition import partition_equidistant, rank_block, slice_steps
 from .problems import ADVECTION_DIFFUSION, frozen_region_from_bounds
 from .systems import System
@@ -161,10 +161,7 @@ class ParaexpEngine:
     # -- plans ---------------------------------------------------------------
 
     def _plan(self, region, span):
-        cfg = self.spec.expaction
-        if isinstance(cfg, KrylovConfig):
-            return plan_krylov(region, span, cfg)
-        return plan_chebyshev(region, span, cfg)
+        return plan_for(region, span, self.spec.expaction, base_span=self.spec.system.spec.T / self.spec.P)
 
     def _set_plan(self, slot: int, plan) -> None:
         self.plans[slot] = plan

@@ -287,7 +287,31 @@ def plan_krylov(region: SpectralRegion, span: float, cfg: KrylovConfig) -> Krylo
                           int(cfg.substep_limit))
 
 
-def plan_for(region: SpectralRegion, span: float, cfg):
-    if isinstance(cfg, KrylovConfig):
-        return plan_krylov(region, span, cfg)
-    return plan_chebyshev(region, span, cfg)
+def chained(plan, k: int):
+    """The same per-substep series applied k times in a row: span k·τ (always
+    feasible; accuracy that of k consecutive base actions, i.e. of the scan)."""
+    if isinstance(plan, KrylovPlan):
+        return KrylovPlan(span=plan.span * k, substeps=plan.substeps * k, m=plan.m)
+    return ChebPlan(span=plan.span * k, substeps=plan.substeps * k, degree=plan.degree, center=plan.center,
+                    scale=plan.scale, sigma=plan.sigma, coef_exp=plan.coef_exp, coef_phi=plan.coef_phi,
+                    err_bound=plan.err_bound * k)
+
+
+def plan_for(region: SpectralRegion, span: float, cfg, base_span: float | None = None):
+    """Plan for ``span``; when ``span`` is an integer multiple k of ``base_span``
+    (block-scan long spans are multiples of the slice width), the k-fold chained
+    base plan is also considered and the cheaper feasible plan is returned."""
+    one = plan_krylov if isinstance(cfg, KrylovConfig) else plan_chebyshev
+    k = None
+    if base_span is not None and span > base_span:
+        q = span / base_span
+        if abs(q - round(q)) <= 1e-9 * q:
+            k = int(round(q))
+    if k is None:
+        return one(region, span, cfg)
+    base = chained(one(region, base_span, cfg), k)
+    try:
+        direct = one(region, span, cfg)
+    except PropagationFailure:
+        return base
+    return direct if direct.terms <= base.terms else base

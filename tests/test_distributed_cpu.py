@@ -29,7 +29,7 @@ def _case():
     c = scaled(baseline(5), nx=24, P=6, steps_per_slice=4, K=4)
     region = c.system.region()
     ps = plan_for(region, c.spec.T / c.P, c.expaction)
-    pl = lambda span: plan_for(region, span, c.expaction)
+    pl = lambda span: plan_for(region, span, c.expaction, base_span=c.spec.T / c.P)
     return c, ps, pl
 
 

@@ -29,7 +29,7 @@ def _plans(c):
     from paper_2004_00546_b200.expaction import plan_for
     region = c.system.region()
     slice_plan = plan_for(region, c.spec.T / c.P, c.expaction)
-    long_plan = lambda span: plan_for(region, span, c.expaction)
+    long_plan = lambda span: plan_for(region, span, c.expaction, base_span=c.spec.T / c.P)
     return slice_plan, long_plan
 
 
