@@ -157,6 +157,11 @@ int px_finish_adjoint(void* handle, void* stream);
  * host planner between the sweeps). */
 int px_gradient(void* handle, void* stream);
 
+/* CUDA-graph replay of px_gradient (default on): the whole gradient is captured
+ * once per plan set / timing mode and replayed on an internal stream ordered
+ * after the caller's stream. */
+int px_set_graphs(void* handle, int enable);
+
 /* Device pointer and element count of a field (for NCCL allreduce by the caller). */
 int px_buffer(void* handle, int field, double** dev_ptr, size_t* count);
 /* Copy a field out (host or device destination). */

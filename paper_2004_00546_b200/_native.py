@@ -105,6 +105,7 @@ SIGNATURES = {
     "px_adjoint": (c_int, [c_void_p, c_void_p]),
     "px_finish_adjoint": (c_int, [c_void_p, c_void_p]),
     "px_gradient": (c_int, [c_void_p, c_void_p]),
+    "px_set_graphs": (c_int, [c_void_p, c_int]),
     "px_buffer": (c_int, [c_void_p, c_int, POINTER(c_void_p), POINTER(c_size_t)]),
     "px_get": (c_int, [c_void_p, c_int, c_void_p, c_size_t, c_int, c_void_p]),
     "px_set_timing": (c_int, [c_void_p, c_int]),

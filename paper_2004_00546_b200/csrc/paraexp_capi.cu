@@ -89,6 +89,21 @@ struct Handle {
   std::vector<TMark> marks;
   std::vector<cudaEvent_t> event_pool;
   px_timing tacc{};
+  // CUDA-graph replay of px_gradient (linear testbed): captured once per
+  // (plans, timing mode), replayed on an internal stream ordered after the caller's
+  bool graphs = true;
+  bool graph_valid = false;
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  px_stats graph_delta{};
+  // the captured gradient is a list of segments, one per timing phase (−1: untimed)
+  struct Seg { int phase; cudaGraphExec_t exec; uint64_t launches; double bytes; };
+  std::vector<Seg> segs;
+  bool capturing = false;
+  int cap_phase = -1;
+  uint64_t cap_launches0 = 0;
+  double cap_bytes0 = 0.0;
+  int cap_error = 0;
   std::string err;
   int stage = 0;  // 0 none, 1 direct, 2 finished direct, 3 adjoint, 4 finished
   std::vector<void*> allocs;
@@ -111,8 +126,44 @@ cudaEvent_t take_event(Handle* h) {
   return e;
 }
 
-// Open a timing window for `phase` (returns -1 when timing is off).
+void seg_open(Handle* h, int phase) {
+  h->cap_phase = phase;
+  h->cap_launches0 = h->stats.kernel_launches;
+  h->cap_bytes0 = h->stats.algorithmic_bytes;
+  if (cudaStreamBeginCapture(h->gstream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) h->cap_error = 1;
+}
+
+void seg_close(Handle* h) {
+  cudaGraph_t g = nullptr;
+  if (cudaStreamEndCapture(h->gstream, &g) != cudaSuccess || !g) {
+    h->cap_error = 1;
+    return;
+  }
+  size_t nn = 0;
+  cudaGraphGetNodes(g, nullptr, &nn);
+  if (nn > 0) {
+    cudaGraphExec_t ex = nullptr;
+    if (cudaGraphInstantiate(&ex, g, 0) != cudaSuccess) h->cap_error = 1;
+    else
+      h->segs.push_back({h->cap_phase, ex, h->stats.kernel_launches - h->cap_launches0,
+                         h->stats.algorithmic_bytes - h->cap_bytes0});
+  }
+  cudaGraphDestroy(g);
+}
+
+void drop_segments(Handle* h) {
+  for (auto& sg : h->segs) cudaGraphExecDestroy(sg.exec);
+  h->segs.clear();
+}
+
+// Open a timing window for `phase` (returns -1 when timing is off; while capturing a
+// graph the window becomes its own graph segment, timed at replay).
 int tbegin(Handle* h, int phase, cudaStream_t s) {
+  if (h->capturing) {
+    seg_close(h);
+    seg_open(h, phase);
+    return -2;
+  }
   if (!h->timing) return -1;
   Handle::TMark m{phase, take_event(h), take_event(h), h->stats.kernel_launches, h->stats.algorithmic_bytes};
   cudaEventRecord(m.a, s);
@@ -121,6 +172,11 @@ int tbegin(Handle* h, int phase, cudaStream_t s) {
 }
 
 void tend(Handle* h, int idx, cudaStream_t s) {
+  if (idx == -2 && h->capturing) {
+    seg_close(h);
+    seg_open(h, -1);
+    return;
+  }
   if (idx < 0) return;
   Handle::TMark& m = h->marks[idx];
   cudaEventRecord(m.b, s);
@@ -794,6 +850,10 @@ void px_destroy(void* handle) {
   for (auto& pl : h->plans)
     if (pl.dcoef) cudaFree(pl.dcoef);
   for (auto& m : h->marks) { cudaEventDestroy(m.a); cudaEventDestroy(m.b); }
+  drop_segments(h);
+  if (h->gstream) cudaStreamDestroy(h->gstream);
+  if (h->ev_in) cudaEventDestroy(h->ev_in);
+  if (h->ev_out) cudaEventDestroy(h->ev_out);
   for (auto e : h->event_pool) cudaEventDestroy(e);
   px::krylov_free(h->kw);
   delete h;
@@ -821,6 +881,7 @@ int px_set_cheb_plan(void* handle, int slot, const px_cheb_plan* p) {
       !p->coef_exp)
     return fail(h, PX_ERR_ARG, "bad Chebyshev plan");
   Plan& pl = h->plans[slot];
+  h->graph_valid = false;
   pl.set = true;
   pl.krylov = false;
   pl.span = p->span;
@@ -848,6 +909,7 @@ int px_set_krylov_plan(void* handle, int slot, double span, int substeps) {
   if (h->d.expaction != PX_EXP_KRYLOV) return fail(h, PX_ERR_ARG, "handle not created for Krylov");
   if (substeps < 1 || !(span > 0)) return fail(h, PX_ERR_ARG, "bad Krylov plan");
   Plan& pl = h->plans[slot];
+  h->graph_valid = false;
   pl.set = true;
   pl.krylov = true;
   pl.span = span;
@@ -964,14 +1026,89 @@ int px_finish_adjoint(void* handle, void* stream) {
   return rc;
 }
 
+int gradient_phases(Handle* h, void* stream) {
+  PX_TRY(px_direct(h, stream));
+  PX_TRY(px_finish_direct(h, stream));
+  PX_TRY(px_adjoint(h, stream));
+  PX_TRY(px_finish_adjoint(h, stream));
+  return PX_OK;
+}
+
+int capture_gradient(Handle* h) {
+  drop_segments(h);
+  const px_stats before = h->stats;
+  h->capturing = true;
+  h->cap_error = 0;
+  seg_open(h, -1);
+  const int rc = gradient_phases(h, h->gstream);
+  seg_close(h);
+  h->capturing = false;
+  if (rc != PX_OK || h->cap_error) {
+    drop_segments(h);
+    h->stats = before;
+    if (rc != PX_OK) return rc;
+    return fail(h, PX_ERR_CUDA, "graph capture failed");
+  }
+  px_stats d{};
+  d.rk4_lane_steps = h->stats.rk4_lane_steps - before.rk4_lane_steps;
+  d.exp_terms = h->stats.exp_terms - before.exp_terms;
+  d.arnoldi_steps = h->stats.arnoldi_steps - before.arnoldi_steps;
+  d.kernel_launches = h->stats.kernel_launches - before.kernel_launches;
+  d.algorithmic_bytes = h->stats.algorithmic_bytes - before.algorithmic_bytes;
+  d.rk4_bytes = h->stats.rk4_bytes - before.rk4_bytes;
+  d.exp_bytes = h->stats.exp_bytes - before.exp_bytes;
+  h->graph_delta = d;
+  h->stats = before;
+  h->graph_valid = true;
+  return PX_OK;
+}
+
 int px_gradient(void* handle, void* stream) {
   Handle* h = static_cast<Handle*>(handle);
   if (!h) return fail(h, PX_ERR_ARG, "null handle");
   if (h->d.kind != PX_KIND_ADVDIFF) return fail(h, PX_ERR_ARG, "px_gradient: linear testbed only");
-  PX_TRY(px_direct(handle, stream));
-  PX_TRY(px_finish_direct(handle, stream));
-  PX_TRY(px_adjoint(handle, stream));
-  PX_TRY(px_finish_adjoint(handle, stream));
+  if (!h->graphs) return gradient_phases(h, stream);
+  if (!h->basis_set || !h->inputs_set) return fail(h, PX_ERR_STATE, "basis/inputs not set");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!h->gstream) {
+    PX_CUDA(h, cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking));
+    PX_CUDA(h, cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
+    PX_CUDA(h, cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
+  }
+  if (!h->graph_valid) PX_TRY(capture_gradient(h));
+  // order: caller's stream -> graph stream -> caller's stream
+  PX_CUDA(h, cudaEventRecord(h->ev_in, s));
+  PX_CUDA(h, cudaStreamWaitEvent(h->gstream, h->ev_in, 0));
+  for (auto& sg : h->segs) {
+    if (h->timing && sg.phase >= 0) {
+      Handle::TMark m{sg.phase, take_event(h), take_event(h), sg.launches, sg.bytes};
+      PX_CUDA(h, cudaEventRecord(m.a, h->gstream));
+      PX_CUDA(h, cudaGraphLaunch(sg.exec, h->gstream));
+      PX_CUDA(h, cudaEventRecord(m.b, h->gstream));
+      h->marks.push_back(m);
+    } else {
+      PX_CUDA(h, cudaGraphLaunch(sg.exec, h->gstream));
+    }
+  }
+  PX_CUDA(h, cudaEventRecord(h->ev_out, h->gstream));
+  PX_CUDA(h, cudaStreamWaitEvent(s, h->ev_out, 0));
+  const px_stats& d = h->graph_delta;
+  h->stats.rk4_lane_steps += d.rk4_lane_steps;
+  h->stats.exp_terms += d.exp_terms;
+  h->stats.arnoldi_steps += d.arnoldi_steps;
+  h->stats.kernel_launches += d.kernel_launches;
+  h->stats.algorithmic_bytes += d.algorithmic_bytes;
+  h->stats.rk4_bytes += d.rk4_bytes;
+  h->stats.exp_bytes += d.exp_bytes;
+  h->stage = 4;
+  return PX_OK;
+}
+
+int px_set_graphs(void* handle, int enable) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return fail(h, PX_ERR_ARG, "null handle");
+  h->graphs = enable != 0;
+  h->graph_valid = false;
   return PX_OK;
 }
 

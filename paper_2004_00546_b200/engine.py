@@ -229,6 +229,10 @@ class ParaexpEngine:
         N.check(self.lib, self.lib.px_get_stats(self.h, ctypes.byref(st)), self.h)
         return st.as_dict()
 
+    def set_graphs(self, enable: bool) -> None:
+        """CUDA-graph replay of the single-rank gradient (default on)."""
+        N.check(self.lib, self.lib.px_set_graphs(self.h, 1 if enable else 0), self.h)
+
     def set_timing(self, enable: bool) -> None:
         N.check(self.lib, self.lib.px_set_timing(self.h, 1 if enable else 0), self.h)
 
