@@ -21,12 +21,14 @@ namespace px {
 
 constexpr int KRYLOV_MAX_M = 40;
 constexpr double KRYLOV_BREAKDOWN = 1e-13;
+constexpr int KR_PPT = 4;             // points per thread in the Arnoldi passes
+constexpr int KR_BLK = 256 * KR_PPT;  // points per block
 
 struct KrylovWork {
   int m = 0, B = 0, nblk = 0;
   size_t n = 0;
   double* V = nullptr;        // (m+1) × B × n
-  double* w = nullptr;        // B × n
+  double* w = nullptr;        // 2 × B × n (ping-pong: step j's w feeds V_{j+1} at step j+1)
   double* H = nullptr;        // B × (m+1) × m   (row i, col j at i*m + j)
   double* hcol = nullptr;     // B × (MAX_M+1)  current column pass values
   double* part = nullptr;     // B × (MAX_M+1) × nblk partial dots
@@ -38,7 +40,7 @@ inline int krylov_alloc(KrylovWork& kw, int m, size_t n, int B, std::string* err
   kw.m = m;
   kw.n = n;
   kw.B = B;
-  kw.nblk = (int)((n + 255) / 256);
+  kw.nblk = (int)((n + KR_BLK - 1) / KR_BLK);
   auto al = [&](double** p, size_t cnt) -> bool {
     cudaError_t e = cudaMalloc(p, cnt * sizeof(double));
     if (e != cudaSuccess) {
@@ -47,7 +49,7 @@ inline int krylov_alloc(KrylovWork& kw, int m, size_t n, int B, std::string* err
     }
     return true;
   };
-  if (!al(&kw.V, (size_t)(m + 1) * B * n) || !al(&kw.w, (size_t)B * n) ||
+  if (!al(&kw.V, (size_t)(m + 1) * B * n) || !al(&kw.w, 2 * (size_t)B * n) ||
       !al(&kw.H, (size_t)B * (m + 1) * m) || !al(&kw.hcol, (size_t)B * (KRYLOV_MAX_M + 1)) ||
       !al(&kw.part, (size_t)B * (KRYLOV_MAX_M + 1) * kw.nblk) || !al(&kw.beta, B) ||
       !al(&kw.coef, (size_t)B * 2 * m))
@@ -66,11 +68,14 @@ __global__ void __launch_bounds__(256) k_kr_sumsq(double* part, int nblk, const 
                                                   size_t n) {
   __shared__ double red[8];
   const int b = blockIdx.y;
-  const size_t i = (size_t)blockIdx.x * 256 + threadIdx.x;
   double v = 0.0;
-  if (i < n) {
-    const double t = y[b * ybs + i];
-    v = t * t;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const size_t i = (size_t)blockIdx.x * 1024 + threadIdx.x + 256 * k;
+    if (i < n) {
+      const double t = y[b * ybs + i];
+      v += t * t;
+    }
   }
   v = block_sum<256>(v, red);
   if (threadIdx.x == 0) part[(size_t)b * nblk + blockIdx.x] = v;
@@ -95,48 +100,104 @@ __global__ void k_kr_v0(double* V0, const double* y, long long ybs, const double
   V0[(size_t)b * n + i] = bt > 0.0 ? y[b * ybs + i] / bt : 0.0;
 }
 
-// w = M V_j; part[b][i][blk] = Σ V_i·w for i ≤ j
+
+// Block-reduce the per-thread values v[q], q ≤ j, with one barrier; thread q
+// writes the block sum of column q to out[q * stride] (fixed order).
+__device__ __forceinline__ void block_multi_sum(double (*red)[KRYLOV_MAX_M + 1], int nq,
+                                                const double* v, double* out, size_t stride) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int q = 0; q < nq; ++q) {
+    double x = v[q];
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (l == 0) red[w][q] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < nq) {
+    double s = 0.0;
+    for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x];
+    out[(size_t)threadIdx.x * stride] = s;
+  }
+}
+
+// Arnoldi step j, first pass: V_j = w_prev·inv (materialised, fused scale of the
+// previous step; j = 0 reads V_0 directly), w = M V_j, part[b][q][blk] = Σ V_q·w.
 template <int DIM>
-__global__ void __launch_bounds__(256) k_kr_spmv_dots(double* w, const double* V, int j, Stencil5 st,
-                                                      double* part, int nblk, int B, int nx, int ny) {
-  __shared__ double red[8];
+__global__ void __launch_bounds__(256) k_kr_spmv_dots(double* w, double* V, const double* w_prev,
+                                                      const double* hcol, int j, Stencil5 st, double* part,
+                                                      int nblk, int B, int nx, int ny) {
+  __shared__ double red[8][KRYLOV_MAX_M + 1];
   const size_t n = (size_t)nx * ny;
   const int b = blockIdx.y;
-  const size_t i = (size_t)blockIdx.x * 256 + threadIdx.x;
-  double wv = 0.0;
-  if (i < n) {
-    const int y = (int)(i / nx), x = (int)(i - (size_t)y * nx);
-    wv = stencil_at<DIM>(V + ((size_t)j * B + b) * n, st, x, y, nx, ny);
-    w[(size_t)b * n + i] = wv;
+  double* Vj = V + ((size_t)j * B + b) * n;
+  const double* src = Vj;
+  double inv = 1.0;
+  if (j > 0) {
+    src = w_prev + (size_t)b * n;
+    inv = hcol[(size_t)b * (KRYLOV_MAX_M + 1)];
+  }
+  double wv[KR_PPT], vq[KRYLOV_MAX_M + 1];
+#pragma unroll
+  for (int k = 0; k < KR_PPT; ++k) {
+    const size_t i = (size_t)blockIdx.x * KR_BLK + threadIdx.x + 256 * k;
+    wv[k] = 0.0;
+    if (i < n) {
+      const int y = (int)(i / nx), x = (int)(i - (size_t)y * nx);
+      wv[k] = inv * stencil_at<DIM>(src, st, x, y, nx, ny);
+      w[(size_t)b * n + i] = wv[k];
+      if (j > 0) Vj[i] = src[i] * inv;
+    }
   }
   for (int q = 0; q <= j; ++q) {
-    const double v = (i < n) ? V[((size_t)q * B + b) * n + i] * wv : 0.0;
-    const double s = block_sum<256>(v, red);
-    if (threadIdx.x == 0) part[((size_t)b * (KRYLOV_MAX_M + 1) + q) * nblk + blockIdx.x] = s;
+    double acc = 0.0;
+    const double* Vq = V + ((size_t)q * B + b) * n;
+#pragma unroll
+    for (int k = 0; k < KR_PPT; ++k) {
+      const size_t i = (size_t)blockIdx.x * KR_BLK + threadIdx.x + 256 * k;
+      if (i < n) acc += (q == j ? src[i] * inv : Vq[i]) * wv[k];
+    }
+    vq[q] = acc;
   }
+  block_multi_sum(red, j + 1, vq, part + ((size_t)b * (KRYLOV_MAX_M + 1)) * nblk + blockIdx.x, nblk);
 }
 
 // w -= Σ_{q≤j} hcol[b][q] V_q; then part = dots (mode 0) or ‖w‖² (mode 1)
 __global__ void __launch_bounds__(256) k_kr_update(double* w, const double* V, int j, const double* hcol,
                                                    double* part, int nblk, int B, size_t n, int mode) {
-  __shared__ double red[8];
+  __shared__ double red[8][KRYLOV_MAX_M + 1];
+  __shared__ double hs[KRYLOV_MAX_M + 1];
   const int b = blockIdx.y;
-  const size_t i = (size_t)blockIdx.x * 256 + threadIdx.x;
-  double wv = 0.0;
-  if (i < n) {
-    wv = w[(size_t)b * n + i];
-    for (int q = 0; q <= j; ++q) wv -= hcol[(size_t)b * (KRYLOV_MAX_M + 1) + q] * V[((size_t)q * B + b) * n + i];
-    w[(size_t)b * n + i] = wv;
+  if (threadIdx.x <= j) hs[threadIdx.x] = hcol[(size_t)b * (KRYLOV_MAX_M + 1) + threadIdx.x];
+  __syncthreads();
+  double wv[KR_PPT];
+#pragma unroll
+  for (int k = 0; k < KR_PPT; ++k) {
+    const size_t i = (size_t)blockIdx.x * KR_BLK + threadIdx.x + 256 * k;
+    wv[k] = 0.0;
+    if (i < n) {
+      double x = w[(size_t)b * n + i];
+      for (int q = 0; q <= j; ++q) x -= hs[q] * V[((size_t)q * B + b) * n + i];
+      wv[k] = x;
+      w[(size_t)b * n + i] = x;
+    }
   }
+  double vq[KRYLOV_MAX_M + 1];
   if (mode == 0) {
     for (int q = 0; q <= j; ++q) {
-      const double v = (i < n) ? V[((size_t)q * B + b) * n + i] * wv : 0.0;
-      const double s = block_sum<256>(v, red);
-      if (threadIdx.x == 0) part[((size_t)b * (KRYLOV_MAX_M + 1) + q) * nblk + blockIdx.x] = s;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < KR_PPT; ++k) {
+        const size_t i = (size_t)blockIdx.x * KR_BLK + threadIdx.x + 256 * k;
+        if (i < n) acc += V[((size_t)q * B + b) * n + i] * wv[k];
+      }
+      vq[q] = acc;
     }
+    block_multi_sum(red, j + 1, vq, part + ((size_t)b * (KRYLOV_MAX_M + 1)) * nblk + blockIdx.x, nblk);
   } else {
-    const double s = block_sum<256>(wv * wv, red);
-    if (threadIdx.x == 0) part[((size_t)b * (KRYLOV_MAX_M + 1)) * nblk + blockIdx.x] = s;
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < KR_PPT; ++k) acc += wv[k] * wv[k];
+    vq[0] = acc;
+    block_multi_sum(red, 1, vq, part + ((size_t)b * (KRYLOV_MAX_M + 1)) * nblk + blockIdx.x, nblk);
   }
 }
 
@@ -310,20 +371,22 @@ inline int krylov_action(KrylovWork& kw, double tau, int substeps, int m, const 
     double* out = (src == ACC[0]) ? ACC[1] : ACC[0];
     k_kr_sumsq<<<g, 256, 0, s>>>(kw.part, kw.nblk, src, src_bs, n);
     k_kr_beta<<<B, 256, 0, s>>>(kw.beta, kw.part, kw.nblk);
-    k_kr_v0<<<g, 256, 0, s>>>(kw.V, src, src_bs, kw.beta, n);
+    k_kr_v0<<<dim3((unsigned)((n + 255) / 256), B), 256, 0, s>>>(kw.V, src, src_bs, kw.beta, n);
     launches += 3;
     cudaMemsetAsync(kw.H, 0, sizeof(double) * B * (m + 1) * m, s);
     for (int j = 0; j < m; ++j) {
-      if (dim == 2) k_kr_spmv_dots<2><<<g, 256, 0, s>>>(kw.w, kw.V, j, st, kw.part, kw.nblk, B, nx, ny);
-      else k_kr_spmv_dots<1><<<g, 256, 0, s>>>(kw.w, kw.V, j, st, kw.part, kw.nblk, B, nx, ny);
+      double* wj = kw.w + (size_t)(j & 1) * B * n;
+      const double* wprev = kw.w + (size_t)((j + 1) & 1) * B * n;
+      if (dim == 2)
+        k_kr_spmv_dots<2><<<g, 256, 0, s>>>(wj, kw.V, wprev, kw.hcol, j, st, kw.part, kw.nblk, B, nx, ny);
+      else
+        k_kr_spmv_dots<1><<<g, 256, 0, s>>>(wj, kw.V, wprev, kw.hcol, j, st, kw.part, kw.nblk, B, nx, ny);
       k_kr_finalize_dots<<<dim3(j + 1, B), 256, 0, s>>>(kw.hcol, kw.H, kw.part, kw.nblk, m, j, 0);
-      k_kr_update<<<g, 256, 0, s>>>(kw.w, kw.V, j, kw.hcol, kw.part, kw.nblk, B, n, 0);
+      k_kr_update<<<g, 256, 0, s>>>(wj, kw.V, j, kw.hcol, kw.part, kw.nblk, B, n, 0);
       k_kr_finalize_dots<<<dim3(j + 1, B), 256, 0, s>>>(kw.hcol, kw.H, kw.part, kw.nblk, m, j, 1);
-      k_kr_update<<<g, 256, 0, s>>>(kw.w, kw.V, j, kw.hcol, kw.part, kw.nblk, B, n, 1);
+      k_kr_update<<<g, 256, 0, s>>>(wj, kw.V, j, kw.hcol, kw.part, kw.nblk, B, n, 1);
       k_kr_finalize_norm<<<B, 256, 0, s>>>(kw.hcol, kw.H, kw.part, kw.nblk, m, j);
-      k_kr_scale<<<dim3((unsigned)((n + 255) / 256), B), 256, 0, s>>>(kw.V + (size_t)(j + 1) * B * n, kw.w,
-                                                                     kw.hcol, B, n);
-      launches += 7;
+      launches += 6;
     }
     const int N = m + 1;
     const size_t smem = 3 * (size_t)N * N * sizeof(double);
