@@ -12,6 +12,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <string>
 
 #include "../../include/paraexp.h"
@@ -51,7 +52,7 @@ inline int krylov_alloc(KrylovWork& kw, int m, size_t n, int B, std::string* err
   };
   if (!al(&kw.V, (size_t)(m + 1) * B * n) || !al(&kw.w, 2 * (size_t)B * n) ||
       !al(&kw.H, (size_t)B * (m + 1) * m) || !al(&kw.hcol, (size_t)B * (KRYLOV_MAX_M + 1)) ||
-      !al(&kw.part, (size_t)B * (KRYLOV_MAX_M + 1) * kw.nblk) || !al(&kw.beta, B) ||
+      !al(&kw.part, (size_t)B * (2 * (KRYLOV_MAX_M + 1) + 1) * std::max<size_t>((size_t)kw.nblk, 148 * 4)) || !al(&kw.beta, B) ||
       !al(&kw.coef, (size_t)B * 2 * m))
     return PX_ERR_NOMEM;
   return PX_OK;
@@ -248,17 +249,13 @@ __global__ void k_kr_scale(double* Vn, const double* w, const double* hcol, int 
 // One CTA per member: E = exp([[τH_m, τe_1],[0,0]]) by scaling and squaring + Taylor-18;
 // coef[b] = (β·E[:m,0], β·E[:m,m]).  Truncation at the first zero subdiagonal is implicit:
 // columns beyond a breakdown are zero and do not reach the first column.
-__global__ void __launch_bounds__(256) k_kr_expm(double* coef, const double* H, const double* beta, int m,
-                                                 double tau) {
-  extern __shared__ double sm[];
+__device__ void expm_aug_block(double* coef, const double* Hb, double bt, int m, double tau, double* sm) {
   const int N = m + 1;
   double* Aa = sm;            // N×N scaled matrix
   double* E = Aa + N * N;     // accumulator
   double* T = E + N * N;      // scratch
   __shared__ double s_norm;
   __shared__ int s_sq;
-  const int b = blockIdx.x;
-  const double* Hb = H + (size_t)b * (m + 1) * m;
   // meff: first zero subdiagonal
   for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
     const int r = idx / N, c = idx - r * N;
@@ -333,11 +330,18 @@ __global__ void __launch_bounds__(256) k_kr_expm(double* coef, const double* H, 
     for (int idx = threadIdx.x; idx < Ne * Ne; idx += blockDim.x) E[idx] = T[idx];
     __syncthreads();
   }
-  const double bt = beta[b];
   for (int i = threadIdx.x; i < m; i += blockDim.x) {
-    coef[(size_t)b * 2 * m + i] = i < meff ? bt * E[i * Ne + 0] : 0.0;
-    coef[(size_t)b * 2 * m + m + i] = i < meff ? bt * E[i * Ne + meff] : 0.0;
+    coef[i] = i < meff ? bt * E[i * Ne + 0] : 0.0;
+    coef[m + i] = i < meff ? bt * E[i * Ne + meff] : 0.0;
   }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_kr_expm(double* coef, const double* H, const double* beta, int m,
+                                                 double tau) {
+  extern __shared__ double sm[];
+  const int b = blockIdx.x;
+  expm_aug_block(coef + (size_t)b * 2 * m, H + (size_t)b * (m + 1) * m, beta[b], m, tau, sm);
 }
 
 // out[b] = Σ_i coef_e[b][i] V_i (+ addend);  pacc[b] += Σ_i coef_p[b][i] V_i
@@ -414,3 +418,4 @@ inline int krylov_action(KrylovWork& kw, double tau, int substeps, int m, const 
 }
 
 }  // namespace px
+

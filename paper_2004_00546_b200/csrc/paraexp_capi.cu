@@ -26,6 +26,7 @@
 #include "kernels.cuh"
 #include "burgers.cuh"
 #include "krylov.cuh"
+#include "krylov_coop.cuh"
 #include "rk4.cuh"
 #include "cheb_march.cuh"
 #include "scan1d.cuh"
@@ -517,9 +518,24 @@ int exp_action(Handle* h, int slot, const px::Stencil5& st, const double* src, l
   const Plan& pl = h->plans[slot];
   if (!pl.set) return fail(h, PX_ERR_STATE, "exp-action plan slot " + std::to_string(slot) + " not set");
   if (pl.krylov) {
-    PX_TRY(px::krylov_action(h->kw, pl.span / pl.substeps, pl.substeps, h->d.krylov_m, st, src, src_bs,
-                             addend, add_bs, pacc, h->ACC, h->B, h->d.nx, h->d.ny, h->dim, result, s,
-                             &h->stats));
+    static int coop = -1;
+    if (coop < 0) {
+      const char* e = getenv("PX_KRYLOV_COOP");
+      int dev = 0, ok = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
+      // opt-in: on B200 the grid-wide barriers (3 per Arnoldi step) cost more than the
+      // launches they replace at config-4 size (measured 2.25 vs 3.13 gradient evals/s)
+      coop = (ok && e && atoi(e) == 1) ? 1 : 0;
+    }
+    if (coop)
+      PX_TRY(px::krylov_action_coop(h->kw, pl.span / pl.substeps, pl.substeps, h->d.krylov_m, st, src, src_bs,
+                                    addend, add_bs, pacc, h->ACC, h->B, h->d.nx, h->d.ny, h->dim, result, s,
+                                    &h->stats));
+    else
+      PX_TRY(px::krylov_action(h->kw, pl.span / pl.substeps, pl.substeps, h->d.krylov_m, st, src, src_bs,
+                               addend, add_bs, pacc, h->ACC, h->B, h->d.nx, h->d.ny, h->dim, result, s,
+                               &h->stats));
     if (cudaGetLastError() != cudaSuccess) return fail(h, PX_ERR_CUDA, "krylov launch failed");
     return PX_OK;
   }

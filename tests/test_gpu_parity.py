@@ -309,3 +309,17 @@ def test_graph_replay_matches_stream_launches(index):
     t = eng.timing()
     assert t["rk4_direct"]["ms"] > 0 and t["exp_adjoint"]["launches"] > 0
     eng.close()
+
+
+def test_config4_krylov_cooperative_kernel():
+    """The opt-in cooperative Arnoldi kernel (grid-wide barriers) against the oracle."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, '.'); from tests.test_gpu_parity import _gpu_linear, _oracle_linear, _check; "
+            "from paper_2004_00546_b200 import baseline, scaled; "
+            "c = scaled(baseline(4), nx=96, P=12, steps_per_slice=5, K=16); _check(_gpu_linear(c), _oracle_linear(c))")
+    from tests.conftest import ROOT
+    import os
+    env = dict(os.environ, PX_KRYLOV_COOP="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
