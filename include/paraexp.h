@@ -53,7 +53,9 @@ enum {
   PX_PLAN_LONG_DIRECT = 1,  /* span (P - p_end)·Δ, block carry -> T (blockscan) */
   PX_PLAN_LONG_ADJOINT = 2, /* span p_begin·Δ, block carry -> 0 (blockscan) */
   PX_PLAN_FROZEN = 3,       /* Burgers: slice width, frozen J(ū_p)ᵀ */
-  PX_PLAN_COUNT = 4
+  PX_PLAN_NL_SLICE = 4,     /* Burgers iterative direct: slice width, J(ū_p) */
+  PX_PLAN_NL_STEP = 5,      /* Burgers iterative direct: one RK4 step h, J(ū_p) (node recording) */
+  PX_PLAN_COUNT = 6
 };
 
 /* fields for px_get / px_buffer */
@@ -142,6 +144,19 @@ int px_direct(void* handle, void* stream);
 /* After the caller's allreduce of PX_FIELD_UT (world > 1): u(T) = u0 + Σ partials,
  * q†_T = u(T) − u_target, J (cost, optimization.py:84-93 with the terminal objective). */
 int px_finish_direct(void* handle, void* stream);
+/* Iterative nonlinear direct solve (Algorithm 2, nonlinear.py:69-194), Burgers only,
+ * one rank. The host drives the sweeps (it plans the J(ū_p) actions in between):
+ *   px_nl_init            iterate ← u0 at every node
+ *   loop: px_nl_prepare   slice means ū_p of the iterate + FOV bounds (PX_FIELD_FROZEN_BOUNDS)
+ *         [set PX_PLAN_NL_SLICE / PX_PLAN_NL_STEP for that region]
+ *         px_nl_sweep     one Jacobian-augmented sweep; *err_max = max_p relative L2 change
+ *   px_nl_finish          the converged iterate becomes the direct trajectory (then
+ *                         px_finish_direct / the adjoint proceed as after px_direct). */
+int px_nl_init(void* handle, void* stream);
+int px_nl_prepare(void* handle, void* stream);
+int px_nl_sweep(void* handle, double* err_max, void* stream);
+int px_nl_finish(void* handle, void* stream);
+
 /* Standalone adjoint terminal data q†_T (B×n): replaces the qdag_T argument of
  * solve_adjoint_linear / solve_adjoint_varying (paraexp.py:298-353) when the
  * adjoint is run without px_finish_direct. Burgers needs px_direct first. */

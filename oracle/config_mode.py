@@ -358,7 +358,7 @@ def slice_means(traj, P, nsteps):
 
 
 def burgers_gradient(nx, D, basis, T, P, nsteps, u0, u_target, ctrl, plan_for_region,
-                     region_fn, world: int = 1):
+                     region_fn, world: int = 1, traj=None):
     """Config 3 (Option A of SURVEY §8(c)): absorbed final condition, exact Jᵀ(u(t))
     in the inhomogeneous solves, frozen J(ū_p)ᵀ in the homogeneous ones."""
     n = nx
@@ -370,7 +370,8 @@ def burgers_gradient(nx, D, basis, T, P, nsteps, u0, u_target, ctrl, plan_for_re
     delta = T / P
     h = delta / nsteps
     f = basis.field(ctrl)
-    traj = burgers_direct(u0, f, D, hg, h, P * nsteps)          # (S+1, B, n)
+    if traj is None:   # serial direct sweep; Algorithm 2 passes its converged iterate
+        traj = burgers_direct(u0, f, D, hg, h, P * nsteps)      # (S+1, B, n)
     uT = traj[-1]
     qT = uT - ut
     J = 0.5 * np.sum(qT * qT, axis=1)
@@ -501,3 +502,95 @@ class OracleRank:
         self._np("QDAG0")[:] += self.qT
         self._np("G")[:] += self.T * self.qT
         self._np("GRAD")[:] += self.T * self.basis.project(self.qT)
+
+
+# ---------------------------------------------------------------------------
+# Algorithm 2: iterative Jacobian-augmented Paraexp direct solve (Burgers)
+# ---------------------------------------------------------------------------
+
+
+def jac_apply(ubar, y, D, h):
+    """J(ū)·y = D·L y − ū∘Dx y − (Dx ū)∘y (full Burgers linearisation, V ≡ 0)."""
+    lap = (np.roll(y, -1, axis=-1) - 2.0 * y + np.roll(y, 1, axis=-1)) / (h * h)
+    return D * lap - ubar * dx_central(y, h) - dx_central(ubar, h) * y
+
+
+def burgers_iterative_direct(nx, D, basis, T, P, nsteps, u0, ctrl, plan_for_region, region_fn, eps,
+                             max_iter=25, min_iter=2):
+    """`solve_direct_nonlinear` (`nonlinear.py:69-194`) with the configs' numerics.
+
+    Iterate Q (all RK4 nodes, constant u0 initially). Each sweep: ū_p = trapezoid
+    slice means of Q; per slice the linear problem y' = J(ū_p)y + s(t),
+    s = D·L u0 + f − Q∘Dx Q + ū_p∘Dx(Q − u0) + (Dx ū_p)(Q − u0) (i.e.
+    A·q0 + f + N(Q) − J̄_p(Q − q0), `nonlinear.py:113-116`), y(T_p) = 0, RK4 with Q
+    linearly interpolated at the stages; summed-chain carry D_{p+1} =
+    exp(Δ J(ū_p))D_p + y_p(end); new iterate q0 + y_p(kh) + exp(kh J(ū_p))D_p at
+    every node (h-width actions); stop when max_p relative L2 change < eps and at
+    least min_iter sweeps ran (`nonlinear.py:137-146`).
+    """
+    n = nx
+    hg = 2.0 * np.pi / nx
+    ctrl = np.atleast_2d(np.asarray(ctrl, dtype=np.float64))
+    B = ctrl.shape[0]
+    u0 = np.broadcast_to(_as_batch(u0, n), (B, n)).copy()
+    delta = T / P
+    h = delta / nsteps
+    f = basis.field(ctrl)
+    S = P * nsteps
+    Q = np.broadcast_to(u0, (S + 1, B, n)).copy()
+    lapu0 = D * (np.roll(u0, -1, axis=-1) - 2.0 * u0 + np.roll(u0, 1, axis=-1)) / (hg * hg)
+    history = []
+    for it in range(1, max_iter + 1):
+        ubar = slice_means(Q, P, nsteps)
+        region = region_fn(ubar)
+        plan_s = plan_for_region(region, delta)
+        plan_h = plan_for_region(region, h)
+        Qn = np.empty_like(Q)
+        y_end = np.empty((P, B, n))
+        for p in range(P):
+            ub = ubar[p]
+
+            def src(qt):
+                dq = qt - u0
+                return lapu0 + f - qt * dx_central(qt, hg) + ub * dx_central(dq, hg) + dx_central(ub, hg) * dq
+
+            y = np.zeros((B, n))
+            for k in range(nsteps):
+                qa = Q[p * nsteps + k]
+                qb = Q[p * nsteps + k + 1]
+                qm = 0.5 * qa + 0.5 * qb
+                k1 = jac_apply(ub, y, D, hg) + src(qa)
+                k2 = jac_apply(ub, y + (0.5 * h) * k1, D, hg) + src(qm)
+                k3 = jac_apply(ub, y + (0.5 * h) * k2, D, hg) + src(qm)
+                k4 = jac_apply(ub, y + h * k3, D, hg) + src(qb)
+                y = y + (h / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+                if k + 1 < nsteps:
+                    Qn[p * nsteps + k + 1] = u0 + y
+            y_end[p] = y
+        # summed-chain carry through the per-slice operators
+        Dc = np.zeros((P + 1, B, n))
+        for p in range(P):
+            op = lambda v, ub=ubar[p]: jac_apply(ub, v, D, hg)
+            Dc[p + 1] = (y_end[p].copy() if p == 0 else exp_action(op, plan_s, Dc[p]) + y_end[p])
+        for p in range(P):
+            op = lambda v, ub=ubar[p]: jac_apply(ub, v, D, hg)
+            Qn[p * nsteps] = u0 + Dc[p]
+            H = Dc[p]
+            for k in range(1, nsteps):
+                H = exp_action(op, plan_h, H)
+                Qn[p * nsteps + k] += H
+        Qn[S] = u0 + Dc[P]
+        # max over slices (and members) of the relative L2 change on the slice nodes
+        err = 0.0
+        for p in range(P):
+            a = Qn[p * nsteps:(p + 1) * nsteps + 1]
+            b = Q[p * nsteps:(p + 1) * nsteps + 1]
+            for m in range(B):
+                num = float(np.sqrt(np.sum((a[:, m] - b[:, m]) ** 2)))
+                den = float(np.sqrt(np.sum(b[:, m] ** 2)))
+                err = max(err, num / den if den > 0 else num)
+        history.append(err)
+        Q = Qn
+        if err < eps and it >= min_iter:
+            return Q, it, history
+    raise RuntimeError(f"no convergence after {max_iter} sweeps: {history}")

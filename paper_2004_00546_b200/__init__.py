@@ -13,14 +13,17 @@ from .errors import (
     CollectiveFailure,
     ConfigError,
     IntegrationFailure,
+    IterationDivergence,
     NativeUnavailable,
     PropagationFailure,
 )
 from .expaction import ChebPlan, ChebyshevConfig, KrylovConfig, KrylovPlan, plan_chebyshev, plan_krylov
+from .nonlinear import NonlinearResult, solve_direct_nonlinear
 from .optimization import (
     ALGORITHMS,
     HYBRID,
     LINEAR,
+    NONLINEAR,
     AdjointSolution,
     DescentResult,
     DirectSolution,

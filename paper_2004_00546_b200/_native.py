@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 PX_KIND_ADVDIFF, PX_KIND_BURGERS = 0, 1
 PX_EXP_CHEBYSHEV, PX_EXP_KRYLOV = 0, 1
 PX_MEM_HOST, PX_MEM_DEVICE = 0, 1
-PX_PLAN_SLICE, PX_PLAN_LONG_DIRECT, PX_PLAN_LONG_ADJOINT, PX_PLAN_FROZEN = 0, 1, 2, 3
+PX_PLAN_SLICE, PX_PLAN_LONG_DIRECT, PX_PLAN_LONG_ADJOINT, PX_PLAN_FROZEN, PX_PLAN_NL_SLICE, PX_PLAN_NL_STEP = range(6)
 (PX_FIELD_J, PX_FIELD_GRAD, PX_FIELD_UT, PX_FIELD_QDAG0, PX_FIELD_G, PX_FIELD_UBND,
  PX_FIELD_FROZEN_BOUNDS, PX_FIELD_VEND, PX_FIELD_WEND, PX_FIELD_TRAJ) = range(10)
 PX_FLAG_BOUNDARY_STATES = 1
@@ -102,6 +102,10 @@ SIGNATURES = {
     "px_direct": (c_int, [c_void_p, c_void_p]),
     "px_finish_direct": (c_int, [c_void_p, c_void_p]),
     "px_set_adjoint_terminal": (c_int, [c_void_p, c_void_p, c_int, c_void_p]),
+    "px_nl_init": (c_int, [c_void_p, c_void_p]),
+    "px_nl_prepare": (c_int, [c_void_p, c_void_p]),
+    "px_nl_sweep": (c_int, [c_void_p, POINTER(c_double), c_void_p]),
+    "px_nl_finish": (c_int, [c_void_p, c_void_p]),
     "px_adjoint": (c_int, [c_void_p, c_void_p]),
     "px_finish_adjoint": (c_int, [c_void_p, c_void_p]),
     "px_gradient": (c_int, [c_void_p, c_void_p]),

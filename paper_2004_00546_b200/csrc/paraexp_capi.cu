@@ -25,6 +25,7 @@
 #include "../../include/paraexp.h"
 #include "kernels.cuh"
 #include "burgers.cuh"
+#include "burgers_iter.cuh"
 #include "krylov.cuh"
 #include "krylov_coop.cuh"
 #include "rk4.cuh"
@@ -79,6 +80,9 @@ struct Handle {
   // Burgers
   double *traj = nullptr, *ubar = nullptr, *bounds = nullptr, *bpart = nullptr;
   int bounds_blocks = 0;
+  // Burgers iterative direct (Algorithm 2)
+  double *traj_b = nullptr, *Dc = nullptr, *nl_err = nullptr;
+  std::vector<double> nl_err_host;
   // Krylov
   px::KrylovWork kw{};
 
@@ -836,6 +840,11 @@ int px_create(const px_problem_desc* desc, void** out_handle) {
   } else {
     const size_t S = (size_t)d.P * d.nsteps;
     A(&h->traj, (S + 1) * B * n);
+    if (d.p_begin == 0 && d.p_end == d.P) {
+      A(&h->traj_b, (S + 1) * B * n);
+      A(&h->Dc, (size_t)(d.P + 1) * B * n);
+      A(&h->nl_err, B * (size_t)d.P);
+    }
     A(&h->ubar, (size_t)d.P * B * n);
     h->bounds_blocks = (int)std::min<size_t>(((size_t)d.P * B * n + 255) / 256, 1024);
     A(&h->bpart, 3 * (size_t)h->bounds_blocks);
@@ -982,6 +991,117 @@ int px_finish_direct(void* handle, void* stream) {
   int rc = finish_direct_impl(h, static_cast<cudaStream_t>(stream));
   if (rc == PX_OK) h->stage = 2;
   return rc;
+}
+
+
+px::NlPlan nl_plan(const Plan& pl) {
+  px::NlPlan p{};
+  p.be = pl.dcoef;
+  p.degree = pl.degree;
+  p.substeps = pl.substeps;
+  p.sigma = pl.sigma;
+  p.c0 = pl.center;
+  p.d = pl.scale;
+  return p;
+}
+
+int px_nl_init(void* handle, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return fail(h, PX_ERR_ARG, "null handle");
+  if (h->d.kind != PX_KIND_BURGERS || !h->traj_b) return fail(h, PX_ERR_ARG, "iterative direct: Burgers, one rank");
+  if (!h->inputs_set || !h->basis_set) return fail(h, PX_ERR_STATE, "basis/inputs not set");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t nodes = (size_t)h->d.P * h->d.nsteps + 1;
+  px::k_nl_init<<<1024, 256, 0, s>>>(h->traj, h->u0, nodes, h->B, (int)h->n);
+  PX_CHECK_LAUNCH(h);
+  h->stage = 0;
+  return PX_OK;
+}
+
+int nl_means_bounds(Handle* h, cudaStream_t s) {
+  const size_t total = (size_t)h->d.P * h->B * h->n;
+  px::k_slice_means<<<(unsigned)std::min<size_t>((total + 255) / 256, 4096), 256, 0, s>>>(
+      h->ubar, h->traj, h->d.P, h->d.nsteps, h->B, (int)h->n);
+  PX_CHECK_LAUNCH(h);
+  px::k_frozen_bounds<<<h->bounds_blocks, 256, 0, s>>>(h->bpart, h->ubar, total, (int)h->n, h->d.hx, h->d.D);
+  PX_CHECK_LAUNCH(h);
+  px::k_frozen_bounds_final<<<1, 32, 0, s>>>(h->bounds, h->bpart, h->bounds_blocks);
+  PX_CHECK_LAUNCH(h);
+  return PX_OK;
+}
+
+int px_nl_prepare(void* handle, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !h->traj_b) return fail(h, PX_ERR_ARG, "iterative direct not available");
+  return nl_means_bounds(h, static_cast<cudaStream_t>(stream));
+}
+
+int px_nl_sweep(void* handle, double* err_max, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !h->traj_b || !err_max) return fail(h, PX_ERR_ARG, "iterative direct not available");
+  const Plan& ps = h->plans[PX_PLAN_NL_SLICE];
+  const Plan& pt = h->plans[PX_PLAN_NL_STEP];
+  if (!ps.set || !pt.set || ps.krylov || pt.krylov) return fail(h, PX_ERR_STATE, "iterative-direct plans not set");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  px::NlArgs a{};
+  a.Q = h->traj; a.Qn = h->traj_b; a.ubar = h->ubar; a.u0 = h->u0; a.ctrl = h->ctrl;
+  a.tx = h->tx; a.ix = h->ix; a.K = h->K;
+  a.yend = h->Y0; a.Dc = h->Dc; a.err = h->nl_err;
+  a.slice = nl_plan(ps); a.step = nl_plan(pt);
+  a.D = h->d.D; a.hx = h->d.hx; a.h = (h->d.T / h->d.P) / h->d.nsteps;
+  a.nx = h->d.nx; a.B = h->B; a.P = h->d.P; a.nsteps = h->d.nsteps;
+  const int ppt = (a.nx + px::BURGERS_NT - 1) / px::BURGERS_NT;
+  const unsigned lanes = (unsigned)(h->B * h->d.P);
+  const size_t sm3 = 3 * (size_t)a.nx * sizeof(double), sm2 = 2 * (size_t)a.nx * sizeof(double);
+#define PX_NL(PP)                                                                                          \
+  do {                                                                                                     \
+    cudaFuncSetAttribute(px::k_nl_inhom<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);       \
+    px::k_nl_inhom<PP><<<lanes, px::BURGERS_NT, sm3, s>>>(a);                                             \
+    PX_CHECK_LAUNCH(h);                                                                                    \
+    cudaFuncSetAttribute(px::k_nl_scan<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);        \
+    px::k_nl_scan<PP><<<h->B, px::BURGERS_NT, sm2, s>>>(a);                                               \
+    PX_CHECK_LAUNCH(h);                                                                                    \
+    cudaFuncSetAttribute(px::k_nl_record<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);      \
+    px::k_nl_record<PP><<<lanes, px::BURGERS_NT, sm2, s>>>(a);                                            \
+    PX_CHECK_LAUNCH(h);                                                                                    \
+  } while (0)
+  if (ppt <= 1) PX_NL(1);
+  else if (ppt <= 2) PX_NL(2);
+  else if (ppt <= 4) PX_NL(4);
+  else PX_NL(8);
+#undef PX_NL
+  px::k_nl_error<<<lanes, 256, 0, s>>>(a);
+  PX_CHECK_LAUNCH(h);
+  h->nl_err_host.resize(lanes);
+  PX_CUDA(h, cudaMemcpyAsync(h->nl_err_host.data(), h->nl_err, sizeof(double) * lanes, cudaMemcpyDeviceToHost, s));
+  PX_CUDA(h, cudaStreamSynchronize(s));
+  double mx = 0.0;
+  for (double e : h->nl_err_host) mx = std::max(mx, e);
+  *err_max = mx;
+  std::swap(h->traj, h->traj_b);
+  // stats: one inhomogeneous RK4 sweep + the carry and the node recordings
+  const double n = (double)h->n;
+  h->stats.rk4_lane_steps += (uint64_t)lanes * h->d.nsteps;
+  h->stats.rk4_bytes += 32.0 * n * lanes * h->d.nsteps;
+  const uint64_t terms = (uint64_t)h->B * ((h->d.P - 1) * ps.substeps * ps.degree +
+                                            (uint64_t)(h->d.P - 1) * (h->d.nsteps - 1) * pt.substeps * pt.degree);
+  h->stats.exp_terms += terms;
+  h->stats.exp_bytes += 40.0 * n * terms;
+  h->stats.algorithmic_bytes += 32.0 * n * lanes * h->d.nsteps + 40.0 * n * terms;
+  if (!std::isfinite(mx)) return fail(h, PX_ERR_NONFINITE, "non-finite iterate in the nonlinear sweep");
+  return PX_OK;
+}
+
+int px_nl_finish(void* handle, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !h->traj_b) return fail(h, PX_ERR_ARG, "iterative direct not available");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t S = (size_t)h->d.P * h->d.nsteps;
+  PX_CUDA(h, cudaMemcpyAsync(h->UT, h->traj + S * h->B * h->n, sizeof(double) * h->B * h->n,
+                             cudaMemcpyDeviceToDevice, s));
+  PX_TRY(nl_means_bounds(h, s));
+  h->stage = 1;
+  return PX_OK;
 }
 
 int px_set_adjoint_terminal(void* handle, const double* qdag_T, int mem, void* stream) {

@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from .errors import ConfigError, IntegrationFailure, NativeUnavailable
+from .errors import ConfigError, IntegrationFailure, IterationDivergence, NativeUnavailable
 from .expaction import ChebPlan, ChebyshevConfig, KrylovConfig, KrylovPlan, plan_chebyshev, plan_for
 from .partition import partition_equidistant, rank_block, slice_steps
 from .problems import ADVECTION_DIFFUSION, frozen_region_from_bounds
@@ -70,6 +70,10 @@ class EngineSpec:
     rank: int = 0
     world: int = 1
     boundary_states: bool = False
+    direct: str = "serial"      # Burgers: "serial" sweep or "iterative" (Algorithm 2)
+    nl_eps: float = 1e-3
+    nl_max_iter: int = 25
+    nl_min_iter: int = 2
 
     @property
     def nsteps(self) -> int:
@@ -148,6 +152,11 @@ class ParaexpEngine:
         N.check(self.lib, self.lib.px_set_basis(h, tx, ty, ix, iy), h)
         self.plans: dict[int, ChebPlan | KrylovPlan] = {}
         self._keep = []
+        self.nl_history: list[float] = []
+        if spec.direct not in ("serial", "iterative"):
+            raise ConfigError(f"unknown direct solver {spec.direct!r}")
+        if spec.direct == "iterative" and (sysm.is_linear or spec.world != 1):
+            raise ConfigError("the iterative direct (Algorithm 2) is the one-rank Burgers path")
         if sysm.is_linear:
             region = sysm.region()
             delta = sysm.spec.T / spec.P
@@ -252,7 +261,41 @@ class ParaexpEngine:
 
     def direct_partial(self, stream: int | None = None) -> None:
         s = current_stream_handle() if stream is None else stream
+        if self.spec.direct == "iterative":
+            self.direct_iterative(s)
+            return
         N.check(self.lib, self.lib.px_direct(self.h, s), self.h)
+
+    def direct_iterative(self, stream: int | None = None) -> list[float]:
+        """Algorithm 2 (`nonlinear.py:149-194`): Jacobian-augmented sweeps until the
+        max-over-slices relative change < eps (and ≥ min_iter sweeps); the J(ū_p)
+        actions are planned on the host from each iterate's slice means."""
+        s = current_stream_handle() if stream is None else stream
+        spec = self.spec
+        cfg = spec.expaction
+        if not isinstance(cfg, ChebyshevConfig):
+            raise ConfigError("the iterative direct uses the Chebyshev action")
+        delta = spec.system.spec.T / spec.P
+        hstep = delta / spec.nsteps
+        N.check(self.lib, self.lib.px_nl_init(self.h, s), self.h)
+        history: list[float] = []
+        err = ctypes.c_double()
+        for it in range(1, spec.nl_max_iter + 1):
+            N.check(self.lib, self.lib.px_nl_prepare(self.h, s), self.h)
+            lo, hi, im = self.get(N.PX_FIELD_FROZEN_BOUNDS, s)
+            region = frozen_region_from_bounds(float(lo), float(hi), float(im))
+            self._set_plan(N.PX_PLAN_NL_SLICE, plan_chebyshev(region, delta, cfg))
+            self._set_plan(N.PX_PLAN_NL_STEP, plan_chebyshev(region, hstep, cfg))
+            N.check(self.lib, self.lib.px_nl_sweep(self.h, ctypes.byref(err), s), self.h, t=spec.system.spec.T)
+            history.append(float(err.value))
+            if err.value < spec.nl_eps and it >= spec.nl_min_iter:
+                break
+        else:
+            self.nl_history = history
+            raise IterationDivergence(history)
+        self.nl_history = history
+        N.check(self.lib, self.lib.px_nl_finish(self.h, s), self.h)
+        return history
 
     def finish_direct(self, stream: int | None = None) -> None:
         s = current_stream_handle() if stream is None else stream

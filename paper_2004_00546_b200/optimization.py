@@ -11,9 +11,11 @@ coefficients, batched as (B, K)); the objective is terminal,
 J = ½‖u(T) − u_target‖² (``q_true`` is u_target); ∂J/∂c_k = ⟨φ_k, ∫q† dt⟩; the
 initial state ``u0`` is passed through (the reference hard-wires q0 = 0,
 `optimization.py:179`). ``algorithm`` is "linear" (Paraexp direct + adjoint,
-advection–diffusion) or "hybrid" (serial direct sweep + Paraexp adjoint with
-frozen linearisation, Burgers). The only backend is "cuda": there is no CPU
-fallback.
+advection–diffusion), "hybrid" (serial direct sweep + Paraexp adjoint with
+frozen linearisation, Burgers) or "nonlinear" (Algorithm 2: iterative
+Jacobian-augmented Paraexp direct, then the same frozen-linearisation adjoint,
+Burgers; ``eps``/``min_iter``/``max_iter`` as `optimization.py:162-164`). The only
+backend is "cuda": there is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -30,8 +32,9 @@ from .partition import RK4Config, TimePartition, partition_equidistant
 from .systems import System
 
 LINEAR = "linear"
+NONLINEAR = "nonlinear"
 HYBRID = "hybrid"
-ALGORITHMS = (LINEAR, HYBRID)
+ALGORITHMS = (LINEAR, NONLINEAR, HYBRID)
 BACKENDS = ("cuda",)
 
 
@@ -92,12 +95,15 @@ def _default_expaction(system: System):
 
 
 def get_engine(system: System, N: int, rk: RK4Config, expaction, batch: int, rank: int = 0, world: int = 1,
-               boundary_states: bool = False) -> ParaexpEngine:
+               boundary_states: bool = False, direct: str = "serial", eps: float = 1e-3, max_iter: int = 25,
+               min_iter: int = 2) -> ParaexpEngine:
     """Cached engine per (problem, partition, numerics, rank): handles own HBM scratch."""
-    key = (system.grid, system.spec, system.basis.K, N, rk.dt, expaction, batch, rank, world, boundary_states)
+    key = (system.grid, system.spec, system.basis.K, N, rk.dt, expaction, batch, rank, world, boundary_states,
+           direct, eps, max_iter, min_iter)
     eng = _ENGINES.get(key)
     if eng is None:
-        eng = ParaexpEngine(EngineSpec(system, N, rk.dt, expaction, batch, rank, world, boundary_states))
+        eng = ParaexpEngine(EngineSpec(system, N, rk.dt, expaction, batch, rank, world, boundary_states,
+                                       direct, eps, max_iter, min_iter))
         _ENGINES[key] = eng
     return eng
 
@@ -130,6 +136,9 @@ def direct_adjoint_loop(
     backend: str = "cuda",
     boundary_states: bool = False,
     distributed: bool = True,
+    eps: float = 1e-3,
+    min_iter: int = 2,
+    max_iter: int = 25,
 ) -> LoopResult:
     """One direct solve plus one adjoint solve, yielding J and ∂J/∂c (`optimization.py:154-231`).
 
@@ -144,8 +153,8 @@ def direct_adjoint_loop(
         raise ValueError(f"unknown algorithm {algorithm!r}")
     if algorithm == LINEAR and not system.is_linear:
         raise ValueError("linear algorithm requires a linear testbed")
-    if algorithm == HYBRID and system.is_linear:
-        raise ValueError("the hybrid (serial direct) path is the Burgers testbed's")
+    if algorithm in (HYBRID, NONLINEAR) and system.is_linear:
+        raise ValueError(f"the {algorithm} path is the Burgers testbed's")
     if rk is None:
         raise ConfigError("rk: an RK4Config(dt) is required (fixed-step RK4)")
     expaction = expaction or _default_expaction(system)
@@ -155,7 +164,10 @@ def direct_adjoint_loop(
         raise ValueError("control coefficient count does not match the basis")
     u0 = np.zeros(system.n) if u0 is None else np.asarray(u0, dtype=np.float64)
     rank, world = _dist_rank_world() if distributed else (0, 1)
-    eng = get_engine(system, N, rk, expaction, B, rank, world, boundary_states and world == 1)
+    if algorithm == NONLINEAR:
+        rank, world = 0, 1  # Algorithm 2 runs on one rank (every rank computes it identically)
+    eng = get_engine(system, N, rk, expaction, B, rank, world, boundary_states and world == 1,
+                     "iterative" if algorithm == NONLINEAR else "serial", eps, max_iter, min_iter)
     tick = time.perf_counter()
     eng.set_inputs(u0, np.asarray(q_true, dtype=np.float64), ctrl)
     eng.gradient()
@@ -171,7 +183,9 @@ def direct_adjoint_loop(
         J, grad,
         DirectSolution(part, res["uT"], bnd),
         AdjointSolution(part, res["qdag0"], res["G"]),
+        iterations=len(eng.nl_history) if algorithm == NONLINEAR else 1,
         seconds=time.perf_counter() - tick,
+        error_history=list(eng.nl_history) if algorithm == NONLINEAR else [],
         stats=eng.stats(),
     )
 

@@ -323,3 +323,65 @@ def test_config4_krylov_cooperative_kernel():
     env = dict(os.environ, PX_KRYLOV_COOP="1")
     r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
+
+
+def _burgers_oracle_iter(c, eps, max_iter=30):
+    from oracle.config_mode import burgers_iterative_direct
+    from paper_2004_00546_b200.expaction import plan_chebyshev
+    from paper_2004_00546_b200.problems import burgers_frozen_region
+    u0, ut, ctrl = c.inputs()
+    return burgers_iterative_direct(c.grid.nx, c.spec.D, c.system.basis, c.spec.T, c.P, c.nsteps, u0, ctrl,
+                                    lambda region, span: plan_chebyshev(region, span, c.expaction),
+                                    lambda ub: burgers_frozen_region(ub, c.grid, c.spec.D), eps=eps,
+                                    max_iter=max_iter)
+
+
+def test_nonlinear_iterative_direct_matches_oracle():
+    """Algorithm 2 (`nonlinear.py:69-194`) on the GPU: every node of the converged
+    iterate, the sweep count and the error history against the numpy restatement."""
+    from paper_2004_00546_b200 import RK4Config, baseline, scaled, solve_direct_nonlinear
+    c = scaled(baseline(3), nx=256, P=8, steps_per_slice=16)
+    u0, ut, ctrl = c.inputs()
+    Q, it, hist = _burgers_oracle_iter(c, eps=1e-9)
+    res = solve_direct_nonlinear(c.system, u0, ctrl, c.P, RK4Config(c.dt), c.expaction, eps=1e-9, max_iter=30)
+    assert res.iterations == it
+    for a, b in zip(res.error_history, hist):
+        if b > 1e-6:
+            assert abs(a - b) <= 1e-8 * b
+    assert rel_l2(res.trajectory, Q) <= 1e-10
+    assert rel_l2(res.final_state, Q[-1]) <= 1e-10
+
+
+def test_nonlinear_loop_gradient_matches_oracle():
+    from oracle.config_mode import burgers_gradient
+    from paper_2004_00546_b200 import RK4Config, baseline, direct_adjoint_loop, scaled
+    from paper_2004_00546_b200.expaction import plan_chebyshev
+    from paper_2004_00546_b200.problems import burgers_frozen_region
+    c = scaled(baseline(3), nx=256, P=8, steps_per_slice=16)
+    u0, ut, ctrl = c.inputs()
+    Q, it, hist = _burgers_oracle_iter(c, eps=1e-9)
+    loop = direct_adjoint_loop(c.system, ctrl, ut, "nonlinear", N=c.P, rk=RK4Config(c.dt), expaction=c.expaction,
+                               u0=u0, eps=1e-9, max_iter=30)
+    ref = burgers_gradient(c.grid.nx, c.spec.D, c.system.basis, c.spec.T, c.P, c.nsteps, u0, ut, ctrl,
+                           lambda region, span: plan_chebyshev(region, span, c.expaction),
+                           lambda ub: burgers_frozen_region(ub, c.grid, c.spec.D), traj=Q)
+    _check(loop, ref)
+    assert loop.iterations == it and len(loop.error_history) == it
+
+
+def test_nonlinear_full_config3_converges_to_serial():
+    """Full config 3 size: Algorithm 2's fixed point agrees with the serial RK4 sweep
+    to the linear-interpolation (O(h²)) level of the frozen iterate."""
+    from paper_2004_00546_b200 import IterationDivergence, RK4Config, baseline, direct_adjoint_loop
+    c = baseline(3)
+    u0, ut, ctrl = c.inputs()
+    ser = direct_adjoint_loop(c.system, ctrl, ut, "hybrid", N=c.P, rk=RK4Config(c.dt), expaction=c.expaction,
+                              u0=u0)
+    it = direct_adjoint_loop(c.system, ctrl, ut, "nonlinear", N=c.P, rk=RK4Config(c.dt), expaction=c.expaction,
+                             u0=u0, eps=1e-8, max_iter=30)
+    assert it.iterations >= 2 and it.error_history[-1] < 1e-8
+    assert rel_l2(it.direct.final_state, ser.direct.final_state) <= 1e-4
+    assert rel_l2(it.grad, ser.grad) <= 1e-3
+    with pytest.raises(IterationDivergence):
+        direct_adjoint_loop(c.system, ctrl, ut, "nonlinear", N=c.P, rk=RK4Config(c.dt), expaction=c.expaction,
+                            u0=u0, eps=1e-14, max_iter=2)
