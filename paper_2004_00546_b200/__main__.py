@@ -1,0 +1,121 @@
+"""Command line (mirror of the reference's `paradjoint run|predict`, `cli.py:352-403`,
+for the BASELINE configs with ``backend="cuda"``).
+
+    python -m paper_2004_00546_b200 run --config 5 --repeats 3 --output results/c5
+    python -m paper_2004_00546_b200 predict --config 5 --gpus 1 2 4 8
+
+``run`` times `direct_adjoint_loop` (or config 2's 20-step `descend`) on this
+GPU and writes ``results.csv`` and ``summary.json`` (timing columns separate,
+as `reporting.py:22-55`); ``predict`` measures the per-unit kernel times with one
+gradient and prints the block-scan strong-scaling model (`scaling.py` here).
+Exit codes as the reference: 0 ok, 1 usage/config error, 2 solver failure.
+"""
+
+from __future__ import annotations
+
+import argparse
+import csv
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+
+def _case(index: int):
+    from .configs import baseline
+    return baseline(index)
+
+
+def cmd_run(args) -> int:
+    from .optimization import descend, direct_adjoint_loop
+    from .partition import RK4Config
+    c = _case(args.config)
+    u0, ut, ctrl = c.inputs()
+    algo = "linear" if c.system.is_linear else ("nonlinear" if args.nonlinear else "hybrid")
+    rk = RK4Config(c.dt)
+    rows, t = [], []
+    if c.descent_steps and not args.single:
+        tick = time.perf_counter()
+        res = descend(c.system, ctrl, ut, steps=c.descent_steps, lr=c.lr, algorithm=algo, N=c.P, rk=rk,
+                      expaction=c.expaction, u0=u0)
+        t.append(time.perf_counter() - tick)
+        for i, (J, g) in enumerate(zip(res.J_history, res.grad_norms)):
+            for b, (Jb, gb) in enumerate(zip(np.ravel(J), np.ravel(g))):
+                rows.append([i, b, f"{Jb:.17g}", f"{gb:.17g}"])
+        evals = c.descent_steps * c.batch
+    else:
+        for rep in range(args.repeats + 1):
+            tick = time.perf_counter()
+            loop = direct_adjoint_loop(c.system, ctrl, ut, algo, N=c.P, rk=rk, expaction=c.expaction, u0=u0)
+            if rep > 0:  # first run is the warm-up (plans, allocation)
+                t.append(time.perf_counter() - tick)
+        for b, (Jb, gb) in enumerate(zip(np.ravel(loop.J), np.atleast_2d(loop.grad))):
+            rows.append([0, b, f"{Jb:.17g}", f"{np.linalg.norm(gb):.17g}"])
+        evals = c.batch
+    os.makedirs(args.output, exist_ok=True)
+    with open(os.path.join(args.output, "results.csv"), "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(["iteration", "member", "J", "grad_norm"])
+        w.writerows(rows)
+    summary = {"config": c.name, "algorithm": algo, "backend": "cuda", "grid": [c.grid.nx, c.grid.ny],
+               "P": c.P, "steps_per_slice": c.nsteps, "batch": c.batch,
+               "timing": {"seconds_median": float(np.median(t)), "repeats": len(t),
+                          "gradient_evals_per_s": evals / float(np.median(t))}}
+    with open(os.path.join(args.output, "summary.json"), "w") as f:
+        json.dump(summary, f, indent=1)
+    print(json.dumps(summary))
+    return 0
+
+
+def cmd_predict(args) -> int:
+    from .engine import EngineSpec, ParaexpEngine
+    from .scaling import profile_from_timing, scaling_table
+    c = _case(args.config)
+    u0, ut, ctrl = c.inputs()
+    eng = ParaexpEngine(EngineSpec(c.system, c.P, c.dt, c.expaction, c.batch))
+    eng.set_inputs(u0, ut, ctrl)
+    eng.gradient()
+    eng.get(0)
+    eng.set_timing(True)
+    eng.timing()
+    for _ in range(args.repeats):
+        eng.gradient()
+    eng.get(0)
+    prof = profile_from_timing(c, eng.timing(), {}, args.repeats)
+    out = {"config": c.name, "profile": json.loads(prof.to_json()),
+           "prediction": [{"gpus": p.G, "seconds": p.seconds, "speedup": p.speedup, "efficiency": p.efficiency,
+                           "critical_rank": p.critical_rank, "breakdown": p.breakdown}
+                          for p in scaling_table(c, prof, tuple(args.gpus))]}
+    print(json.dumps(out, indent=1))
+    eng.close()
+    return 0
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(prog="python -m paper_2004_00546_b200")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    r = sub.add_parser("run", help="time the direct-adjoint loop of a BASELINE config on this GPU")
+    r.add_argument("--config", type=int, default=5)
+    r.add_argument("--repeats", type=int, default=3)
+    r.add_argument("--output", default="results")
+    r.add_argument("--single", action="store_true", help="one gradient even for descent configs")
+    r.add_argument("--nonlinear", action="store_true", help="Burgers: Algorithm 2 direct instead of serial")
+    p = sub.add_parser("predict", help="measure per-unit kernel times, print the multi-GPU scaling model")
+    p.add_argument("--config", type=int, default=5)
+    p.add_argument("--repeats", type=int, default=2)
+    p.add_argument("--gpus", type=int, nargs="+", default=[1, 2, 4, 8])
+    args = ap.parse_args(argv)
+    try:
+        return cmd_run(args) if args.cmd == "run" else cmd_predict(args)
+    except (ValueError, KeyError) as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 1
+    except RuntimeError as e:
+        print(f"solver failure: {e}", file=sys.stderr)
+        return 2
+
+
+if __name__ == "__main__":
+    sys.exit(main())
