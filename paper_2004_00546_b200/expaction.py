@@ -186,6 +186,53 @@ def _evaluate_impl(region_pts, crouzeix, center, d, imag, tau, kmax):
             2.0 * EPS * crouzeix * rnd, be, bp)
 
 
+def _first_feasible(pts, crouzeix, center, d, imag, tau, kmax, tol_s, with_rounding, kcap):
+    """Smallest degree K (≥ 1) whose exp and φ₁ truncation errors (and rounding
+    estimate) meet tol_s at K and K+1 — the same arithmetic as `_evaluate`, but
+    stopping as soon as K is found, the monotone rounding estimate exceeds its
+    budget, or K could no longer beat the best plan so far (``kcap``)."""
+    with np.errstate(all="ignore"):
+        nq = max(64, 2 * kmax + 32)
+        be = chebyshev_coefficients(lambda z: np.exp(tau * z), center, d, imag, nq)[: kmax + 1]
+        bp = chebyshev_coefficients(lambda z: tau * phi1(tau * z), center, d, imag, nq)[: kmax + 1]
+        if not (np.all(np.isfinite(be)) and np.all(np.isfinite(bp))):
+            return None
+        sigma = 1.0 if imag else -1.0
+        X = (pts - center) / d
+        fe = np.exp(tau * pts)
+        fp = tau * phi1(tau * pts)
+        ptau = max(tau, 1e-300)
+        Uprev, Ucur = np.ones_like(X), X.copy()
+        Se = be[0] * Uprev
+        Sp = bp[0] * Uprev
+        acc_r = abs(be[0]) + abs(bp[0]) / ptau
+        prev_ok = False
+        errs = []
+        for k in range(0, kmax + 1):
+            if k >= 1:
+                if k > 1:
+                    Unext = 2.0 * X * Ucur + sigma * Uprev
+                    Uprev, Ucur = Ucur, Unext
+                g = np.max(np.abs(Ucur))
+                Se = Se + be[k] * Ucur
+                Sp = Sp + bp[k] * Ucur
+                acc_r += (abs(be[k]) + abs(bp[k]) / ptau) * g
+            ee = crouzeix * np.max(np.abs(Se - fe))
+            ep = crouzeix * np.max(np.abs(Sp - fp)) / ptau
+            rr = 2.0 * EPS * crouzeix * acc_r
+            errs.append(max(ee, ep))
+            if with_rounding and not rr <= 0.5 * tol_s:
+                return None
+            ok = ee <= tol_s and ep <= tol_s
+            if ok and prev_ok:
+                K = max(k - 1, 1)
+                return K, be[: K + 1].copy(), bp[: K + 1].copy(), float(errs[K])
+            prev_ok = ok
+            if kcap is not None and k - 1 > kcap:
+                return None
+    return None
+
+
 def _foci_candidates(region: SpectralRegion):
     lo, hi, im = region.box()
     c0 = 0.5 * (lo + hi)
@@ -219,20 +266,17 @@ def _plan_cheb(region: SpectralRegion, span: float, tol: float, max_degree: int,
                 break
             tau = span / s
             tol_s = tol / s
-            ee, ep, rr, be, bp = _evaluate(pts, region.crouzeix, c0, d, imag, tau, max_degree)
-            ok = (ee <= tol_s) & (ep <= tol_s)
-            if with_rounding:
-                ok &= rr <= 0.5 * tol_s
-            # require the next degree to satisfy the bound too (no lucky dip)
-            ok2 = ok[:-1] & ok[1:]
-            idx = np.nonzero(ok2)[0]
-            if len(idx) == 0:
+            # degree bound beyond which this (foci, s) cannot beat the best plan so far
+            kcap = None if best is None else best[0] // s
+            # the next degree must satisfy the bound too (no lucky dip)
+            found = _first_feasible(pts, region.crouzeix, c0, d, imag, tau, max_degree, tol_s,
+                                    with_rounding, kcap)
+            if found is None:
                 continue
-            K = max(int(idx[0]), 1)
+            K, be, bp, err = found
             cost = s * K
             if best is None or cost < best[0]:
-                best = (cost, c0, d, imag, s, K, be[: K + 1].copy(), bp[: K + 1].copy(),
-                        float(max(ee[K], ep[K])))
+                best = (cost, c0, d, imag, s, K, be, bp, err)
     if best is None:
         raise PropagationFailure(
             f"no Chebyshev plan within {substep_limit} substeps of degree <= {max_degree} "
