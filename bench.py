@@ -345,8 +345,13 @@ def main():
     bytes_per_launch = ph["bytes"] / max(ph["launches"], 1)
     achieved = bytes_per_launch / avg_launch_s / 1e9 if avg_launch_s > 0 else 0.0
     two_d = c.grid.dim == 2
-    kernel_name = {"rk4_direct": "k_rk4_march<false>" if two_d else "k_rk4_lane1d<false>",
-                   "rk4_adjoint": "k_rk4_march<true>" if two_d else "k_rk4_lane1d<true>",
+    # two RK4 steps per launch (k_rk4_march2) when the phase launched fewer kernels than steps
+    fused = two_d and ph["launches"] / args.steps < (c.nsteps - 1) * 0.75
+    m2 = "k_rk4_march2<{},128,3,3>"
+    kernel_name = {"rk4_direct": (m2.format("false") if fused else "k_rk4_march<false>") if two_d
+                   else "k_rk4_lane1d<false>",
+                   "rk4_adjoint": (m2.format("true") if fused else "k_rk4_march<true>") if two_d
+                   else "k_rk4_lane1d<true>",
                    "exp_direct": "k_cheb_march<M>" if two_d else "k_scan1d",
                    "exp_adjoint": "k_cheb_march<M>+phi" if two_d else "k_scan1d+phi",
                    "other": "reductions/projection"}[dom]

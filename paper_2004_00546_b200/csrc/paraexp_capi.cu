@@ -270,6 +270,7 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
   const int nsteps = h->d.nsteps;
   double* cur = nullptr;
   uint64_t launched_steps = 0;
+  int64_t fused_launches = -1;  // march launches when some cover two steps (bytes are per launch)
   h->z_valid = false;
   if (h->dim == 1 && h->n <= 4096) {
     px::Lane1DArgs a{};
@@ -300,6 +301,87 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
     px::MarchArgs a{};
     a.b = h->bsrc; a.z = h->Z; a.st = st; a.h = hs;
     a.nx = nx; a.ny = ny; a.lanes = h->L; a.lanes_per_b = h->Pl;
+    // two RK4 steps per launch for large sweeps (PX_MARCH2=0 forces the one-step kernel); small
+    // sweeps keep one step per launch: the 8-stage pipeline fill (16 rows per band) and the
+    // 1-CTA-per-3-warps occupancy only pay off when each launch covers ≥ 2^28 lane-points
+    static const int m2_mode = [] { const char* e = getenv("PX_MARCH2"); return e ? atoi(e) : 1; }();
+    if (m2_mode && nsteps >= 3 && (m2_mode == 2 || (double)h->L * (double)h->n >= 268435456.0)) {
+      // two steps per launch: halo 8 (one column per stage and side)
+      static const int m2_var = [] { const char* e = getenv("PX_M2_VAR"); return e ? atoi(e) : 3; }();
+      const int m2_nt = m2_var == 2 ? 192 : 128;
+      const int cw_max = 2 * m2_nt;
+      if (nx <= cw_max) {
+        a.strip_w = nx; a.halo = 0; a.nstrips = 1;
+      } else {
+        a.halo = 8; a.strip_w = cw_max - 16;
+        a.nstrips = (nx + a.strip_w - 1) / a.strip_w;
+      }
+      static const int m2_band = [] { const char* e = getenv("PX_M2_BAND"); return e ? atoi(e) : 512; }();
+      // bands of rows (16 rows of pipeline fill each): ≥ 4 waves at 2 CTAs/SM, ≥ 128 rows per band
+      int br = std::min(ny, m2_band);
+      while (br > 128 && (size_t)h->L * a.nstrips * ((ny + br - 1) / br) < 4 * 3 * 148) br = (br + 1) / 2;
+      a.band_rows = br;
+      a.nbands = (ny + a.band_rows - 1) / a.band_rows;
+      const unsigned blocks = (unsigned)((size_t)h->L * a.nstrips * a.nbands);
+      auto launch2 = [&]() -> int {
+#define PX_M2(NT, DEP, MB)                                                                                 \
+  do {                                                                                                     \
+    const size_t sm = px::march2_smem<NT, DEP>(adjoint);                                                   \
+    static bool attr[2] = {false, false};                                                                  \
+    if (!attr[adjoint]) {                                                                                  \
+      if (adjoint) PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march2<true, NT, DEP, MB>,                    \
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+      else PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march2<false, NT, DEP, MB>,                           \
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));         \
+      attr[adjoint] = true;                                                                                \
+    }                                                                                                      \
+    if (adjoint) px::k_rk4_march2<true, NT, DEP, MB><<<blocks, NT, sm, s>>>(a);                            \
+    else px::k_rk4_march2<false, NT, DEP, MB><<<blocks, NT, sm, s>>>(a);                                   \
+  } while (0)
+        if (m2_var == 2) PX_M2(192, 3, 2);  // 2 CTAs/SM
+        else PX_M2(128, 3, 3);               // 3 CTAs/SM (default)
+#undef PX_M2
+        return PX_OK;
+      };
+      int st_i = 1;
+      fused_launches = 0;
+      while (st_i < nsteps) {
+        ++fused_launches;
+        double* out = (cur == h->Y0) ? h->Y1 : h->Y0;
+        a.y_in = cur;
+        a.y_out = out;
+        a.z_zero = (st_i == 1);
+        if (nsteps - st_i >= 2) {
+          PX_TRY(launch2());
+          st_i += 2;
+        } else {
+          px::MarchArgs b1 = a;  // odd remainder: one single-step launch
+          if (nx <= px::MARCH_MAX_CW) {
+            b1.strip_w = nx; b1.halo = 0; b1.nstrips = 1;
+          } else {
+            b1.strip_w = px::MARCH_STRIP; b1.halo = px::MARCH_HALO;
+            b1.nstrips = (nx + px::MARCH_STRIP - 1) / px::MARCH_STRIP;
+          }
+          b1.band_rows = std::min(ny, 256);
+          b1.nbands = (ny + b1.band_rows - 1) / b1.band_rows;
+          const unsigned blk1 = (unsigned)((size_t)h->L * b1.nstrips * b1.nbands);
+          const size_t sm1 = px::march_smem(adjoint);
+          static bool attr1 = false;
+          if (!attr1) {
+            PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)px::march_smem(true)));
+            PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)px::march_smem(false)));
+            attr1 = true;
+          }
+          if (adjoint) px::k_rk4_march<true><<<blk1, px::MARCH_NT, sm1, s>>>(b1);
+          else px::k_rk4_march<false><<<blk1, px::MARCH_NT, sm1, s>>>(b1);
+          st_i += 1;
+        }
+        PX_CHECK_LAUNCH(h);
+        cur = out;
+      }
+      launched_steps = nsteps - 1;
+      h->z_valid = adjoint;
+    } else {
     if (nx <= px::MARCH_MAX_CW) {
       a.strip_w = nx; a.halo = 0; a.nstrips = 1;
     } else {
@@ -332,10 +414,14 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
     }
     launched_steps = nsteps - 1;
     h->z_valid = adjoint;
+    }
   }
   const double bytes_per_point = adjoint ? 40.0 : 24.0;  // y, b, y' (+ z in/out)
   h->stats.rk4_lane_steps += (uint64_t)h->L * launched_steps;
-  const double bytes = bytes_per_point * (double)h->n * h->L * launched_steps;
+  // algorithmic bytes per launch: y, b, y_out (+ z in/out) once per point, whether the
+  // launch advances one step or two
+  const double bytes = bytes_per_point * (double)h->n * h->L *
+                       (double)(fused_launches >= 0 ? (uint64_t)fused_launches : launched_steps);
   h->stats.rk4_bytes += bytes;
   h->stats.algorithmic_bytes += bytes;
   *final_out = cur;

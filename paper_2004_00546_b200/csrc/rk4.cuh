@@ -31,6 +31,23 @@
 
 namespace px {
 
+// One RK4 stage on a column pair: base + k·(M·w), with M·w split so that the
+// north neighbour (produced by the previous stage in the SAME iteration) enters
+// last through one FMA: base + k·P + (k·cn)·n, P = cc·c + ce·e + cw·w + cs·s.
+// The dependent chain through a march iteration is then one DFMA per stage.
+__device__ __forceinline__ double2 rk_stage(const Stencil5& st, double2 base, double k, double kcn, double2 c,
+                                            double2 s, double2 nn, double l, double r) {
+  double px = st.cc * c.x;
+  px += st.ce * c.y;
+  px += st.cw * l;
+  px += st.cs * s.x;
+  double py = st.cc * c.y;
+  py += st.ce * r;
+  py += st.cw * c.x;
+  py += st.cs * s.y;
+  return make_double2(fma(kcn, nn.x, fma(k, px, base.x)), fma(kcn, nn.y, fma(k, py, base.y)));
+}
+
 constexpr int MARCH_NT = 288;          // 9 warps: pairs of columns per thread
 constexpr int MARCH_MAX_CW = 2 * MARCH_NT;
 constexpr int MARCH_STRIP = 512;       // useful strip width in strip mode
@@ -358,6 +375,205 @@ __global__ void k_lane_sum_plus(double* out, const double* lanes, int lanes_per_
     if (c) r += scale * c[(size_t)b * n + i];
     out[(size_t)b * n + i] = r;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Two RK4 steps per launch (temporal blocking of the march): stages 1–4 advance
+// y by one step (y⁺ at row r−4), stages 5–8 advance y⁺ by the next (y⁺⁺ at row
+// r−8). Halves the per-step DRAM traffic (y, z, y⁺ once per two steps) at the
+// cost of 8 pipelined stages of register queues (one CTA per SM). Same
+// arithmetic per step as k_rk4_march.
+// ---------------------------------------------------------------------------
+template <int V> struct IC { static constexpr int value = V; };
+template <bool V> struct BC { static constexpr bool value = V; };
+
+// NT threads (2 columns each), DEPTH ring rows of y(r), b(r−4), b(r−8), z(r−8)
+template <bool ADJ, int M2_NT, int M2_DEPTH, int MINB>
+__global__ void __launch_bounds__(M2_NT, MINB) k_rk4_march2(MarchArgs a) {
+  constexpr int NQ = ADJ ? 4 : 3;
+  extern __shared__ double2 dyn2[];
+  double2* ring2 = dyn2;                                                        // [M2_DEPTH][NQ][M2_NT]
+  double (*pubE)[8][M2_NT] = reinterpret_cast<double (*)[8][M2_NT]>(dyn2 + M2_DEPTH * NQ * M2_NT);
+  double (*pubO)[8][M2_NT] = pubE + 2;
+  double2* zs = reinterpret_cast<double2*>(pubE + 4);                           // [6][M2_NT]: h·w3 rows
+
+  const int lane = blockIdx.x % a.lanes;
+  const int rest = blockIdx.x / a.lanes;
+  const int strip = rest % a.nstrips;
+  const int band = rest / a.nstrips;
+  const int nx = a.nx, ny = a.ny;
+  const size_t n = (size_t)nx * ny;
+  const int x0 = strip * a.strip_w;
+  const int U = min(a.strip_w, nx - x0);
+  const int CW = U + 2 * a.halo;
+  const int T = CW >> 1;
+  const int t = threadIdx.x;
+  const bool active = t < T;
+  const int tc = active ? t : 0;
+  const int gx = (((x0 - a.halo + 2 * tc) % nx) + nx) % nx;
+  const int j0 = band * a.band_rows;
+  const int rows_out = min(a.band_rows, ny - j0);
+  const int iters = rows_out + 16;
+  const bool full_row = a.halo == 0;
+  const int tl = (t == 0) ? (full_row ? T - 1 : 0) : t - 1;
+  const int tr = (t + 1 >= T) ? (full_row ? 0 : T - 1) : t + 1;
+  const bool store_ok = active && (2 * t >= a.halo) && (2 * t + 1 < CW - a.halo);
+
+  const Stencil5 st = a.st;
+  const double h = a.h, c1 = a.h * 0.25, c2 = a.h / 3.0, c3 = a.h * 0.5;
+  const double c1n = c1 * a.st.cn, c2n = c2 * a.st.cn, c3n = c3 * a.st.cn, hn = h * a.st.cn;
+  const size_t member = (size_t)(lane / a.lanes_per_b);
+  const double* __restrict__ bsrc = a.b + member * n;
+  const double* __restrict__ ysrc = a.y_in ? a.y_in + (size_t)lane * n : bsrc;
+  double* __restrict__ yout = a.y_out + (size_t)lane * n;
+  double* __restrict__ zl = ADJ ? a.z + (size_t)lane * n : nullptr;
+  const bool zread = ADJ && !a.z_zero;
+
+  auto wrapr = [&](int row) -> int {
+    row %= ny;
+    return row < 0 ? row + ny : row;
+  };
+  const int r0 = j0 - 8;
+  const size_t coloff = (size_t)gx;
+  int iss_k = 0, iss_slot = 0;
+  int ry = wrapr(r0), rb4 = wrapr(r0 - 4), rb8 = wrapr(r0 - 8);
+  auto issue = [&]() {
+    if (iss_k < iters) {
+      double2* slot = ring2 + (size_t)iss_slot * NQ * M2_NT;
+      cp_async16(slot + t, ysrc + (size_t)ry * nx + coloff);
+      cp_async16(slot + M2_NT + t, bsrc + (size_t)rb4 * nx + coloff);
+      cp_async16(slot + 2 * M2_NT + t, bsrc + (size_t)rb8 * nx + coloff);
+      if (zread) cp_async16(slot + 3 * M2_NT + t, zl + (size_t)rb8 * nx + coloff);
+    }
+    cp_async_commit();
+    ++iss_k;
+    iss_slot = (iss_slot + 1 == M2_DEPTH) ? 0 : iss_slot + 1;
+    ry = (ry + 1 == ny) ? 0 : ry + 1;
+    rb4 = (rb4 + 1 == ny) ? 0 : rb4 + 1;
+    rb8 = (rb8 + 1 == ny) ? 0 : rb8 + 1;
+  };
+#pragma unroll
+  for (int k = 0; k < M2_DEPTH; ++k) issue();
+  int rslot = 0;
+  int rs = wrapr(r0 - 8);  // output row r − 8
+
+  // rings (phase k = i mod 6): y rows r-4..r, y⁺ rows r-8..r-4, h·w3 rows r-8..r-3
+  double2 yq[6], pq[6];
+  double2 wq[8][2];  // stage outputs w1,w2,w3 (1..3) and w5,w6,w7 (5..7): last two rows
+#pragma unroll
+  for (int k = 0; k < 6; ++k) yq[k] = pq[k] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) wq[s][0] = wq[s][1] = make_double2(0.0, 0.0);
+
+
+  // One march iteration at ring phase k (compile time); G = guarded (pipeline fill/drain).
+  auto iter = [&](auto kc, auto gc, const int i) {
+    constexpr int k = decltype(kc)::value;
+    constexpr bool G = decltype(gc)::value;
+      const int pin = (k + 1) & 1, pout = k & 1;
+      const int po = k & 1, pp = (k + 1) & 1;
+      cp_async_wait<M2_DEPTH - 1>();
+      const double2* slot = ring2 + (size_t)rslot * NQ * M2_NT;
+      rslot = (rslot + 1 == M2_DEPTH) ? 0 : rslot + 1;
+      const double2 yr = slot[t];
+      const double2 b4 = slot[M2_NT + t];
+      const double2 b8 = slot[2 * M2_NT + t];
+      const double2 zrow = zread ? slot[3 * M2_NT + t] : make_double2(0.0, 0.0);
+      issue();
+      yq[k] = yr;
+      const double2 y0 = yq[(k + 2) % 6], y1 = yq[(k + 3) % 6], y2 = yq[(k + 4) % 6], y3 = yq[(k + 5) % 6];
+      double2 nw[9];
+      if (G) {
+#pragma unroll
+        for (int s = 0; s < 9; ++s) nw[s] = make_double2(0.0, 0.0);
+      }
+      // ---- step A (rows r-1 .. r-4) ----
+      if (!G || i >= 2) {
+        nw[1] = rk_stage(st, y3, c1, c1n, y3, y2, yr, pubO[pin][0][tl], pubE[pin][0][tr]);
+      }
+      if (!G || i >= 4) {
+        nw[2] = rk_stage(st, y2, c2, c2n, wq[1][pp], wq[1][po], nw[1], pubO[pin][1][tl], pubE[pin][1][tr]);
+      }
+      if (!G || i >= 6) {
+        nw[3] = rk_stage(st, y1, c3, c3n, wq[2][pp], wq[2][po], nw[2], pubO[pin][2][tl], pubE[pin][2][tr]);
+        if (ADJ) zs[((k + 3) % 6) * M2_NT + t] = make_double2(h * nw[3].x, h * nw[3].y);  // row r-3
+      }
+      if (!G || i >= 8) {  // y⁺ at row r-4
+        nw[4] = rk_stage(st, make_double2(y0.x + b4.x, y0.y + b4.y), h, hn, wq[3][pp], wq[3][po], nw[3],
+                         pubO[pin][3][tl], pubE[pin][3][tr]);
+      }
+      pq[(k + 2) % 6] = nw[4];  // y⁺ row r-4
+      const double2 p4 = nw[4], p5 = pq[(k + 1) % 6], p6 = pq[k % 6], p7 = pq[(k + 5) % 6], p8 = pq[(k + 4) % 6];
+      // ---- step B (rows r-5 .. r-8) on y⁺ ----
+      if (!G || i >= 10) {
+        nw[5] = rk_stage(st, p5, c1, c1n, p5, p6, p4, pubO[pin][4][tl], pubE[pin][4][tr]);
+      }
+      if (!G || i >= 12) {
+        nw[6] = rk_stage(st, p6, c2, c2n, wq[5][pp], wq[5][po], nw[5], pubO[pin][5][tl], pubE[pin][5][tr]);
+      }
+      if (!G || i >= 14) {
+        nw[7] = rk_stage(st, p7, c3, c3n, wq[6][pp], wq[6][po], nw[6], pubO[pin][6][tl], pubE[pin][6][tr]);
+      }
+      if (!G || i >= 16) {  // y⁺⁺ at row r-8
+        const double2 w7c = wq[7][pp];
+        const double2 yn = rk_stage(st, make_double2(p8.x + b8.x, p8.y + b8.y), h, hn, w7c, wq[7][po], nw[7],
+                                    pubO[pin][7][tl], pubE[pin][7][tr]);
+        if (store_ok) {
+          const size_t off = (size_t)rs * nx + coloff;
+          __stcs(reinterpret_cast<double2*>(yout + off), yn);
+          if (ADJ) {
+            const double2 za = zs[((k + 4) % 6) * M2_NT + t];  // h·w3 at row r-8
+            double2 zn;
+            zn.x = zrow.x + za.x + h * w7c.x;
+            zn.y = zrow.y + za.y + h * w7c.y;
+            __stcs(reinterpret_cast<double2*>(zl + off), zn);
+          }
+        }
+      }
+      rs = (rs + 1 == ny) ? 0 : rs + 1;
+#pragma unroll
+      for (int s = 1; s <= 7; ++s)
+        if (s != 4) wq[s][po] = nw[s];
+      if (active) {
+        pubE[pout][0][t] = yr.x;     pubO[pout][0][t] = yr.y;
+        pubE[pout][1][t] = nw[1].x;  pubO[pout][1][t] = nw[1].y;
+        pubE[pout][2][t] = nw[2].x;  pubO[pout][2][t] = nw[2].y;
+        pubE[pout][3][t] = nw[3].x;  pubO[pout][3][t] = nw[3].y;
+        pubE[pout][4][t] = nw[4].x;  pubO[pout][4][t] = nw[4].y;
+        pubE[pout][5][t] = nw[5].x;  pubO[pout][5][t] = nw[5].y;
+        pubE[pout][6][t] = nw[6].x;  pubO[pout][6][t] = nw[6].y;
+        pubE[pout][7][t] = nw[7].x;  pubO[pout][7][t] = nw[7].y;
+      }
+      __syncthreads();
+  };
+  int i0 = 0;
+  // fill: the first 18 iterations (stages switch on at i = 2, 4, …, 16)
+  for (; i0 < 18; i0 += 6) {
+    if (i0 + 6 > iters) break;
+    iter(IC<0>{}, BC<true>{}, i0); iter(IC<1>{}, BC<true>{}, i0 + 1); iter(IC<2>{}, BC<true>{}, i0 + 2);
+    iter(IC<3>{}, BC<true>{}, i0 + 3); iter(IC<4>{}, BC<true>{}, i0 + 4); iter(IC<5>{}, BC<true>{}, i0 + 5);
+  }
+  if (i0 >= 18) {
+    // steady state: every stage live, no guards
+    for (; i0 + 6 <= iters; i0 += 6) {
+      iter(IC<0>{}, BC<false>{}, i0); iter(IC<1>{}, BC<false>{}, i0 + 1); iter(IC<2>{}, BC<false>{}, i0 + 2);
+      iter(IC<3>{}, BC<false>{}, i0 + 3); iter(IC<4>{}, BC<false>{}, i0 + 4); iter(IC<5>{}, BC<false>{}, i0 + 5);
+    }
+  }
+  // drain / short bands: guarded remainder
+  if (i0 + 0 < iters) iter(IC<0>{}, BC<true>{}, i0);
+  if (i0 + 1 < iters) iter(IC<1>{}, BC<true>{}, i0 + 1);
+  if (i0 + 2 < iters) iter(IC<2>{}, BC<true>{}, i0 + 2);
+  if (i0 + 3 < iters) iter(IC<3>{}, BC<true>{}, i0 + 3);
+  if (i0 + 4 < iters) iter(IC<4>{}, BC<true>{}, i0 + 4);
+  if (i0 + 5 < iters) iter(IC<5>{}, BC<true>{}, i0 + 5);
+  cp_async_wait<0>();
+}
+
+template <int M2_NT, int M2_DEPTH>
+inline size_t march2_smem(bool adj) {
+  return (size_t)M2_DEPTH * (adj ? 4 : 3) * M2_NT * sizeof(double2) + 4 * 8 * M2_NT * sizeof(double) +
+         (adj ? 6 * M2_NT * sizeof(double2) : 0);
 }
 
 }  // namespace px
