@@ -301,6 +301,12 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
     px::MarchArgs a{};
     a.b = h->bsrc; a.z = h->Z; a.st = st; a.h = hs;
     a.nx = nx; a.ny = ny; a.lanes = h->L; a.lanes_per_b = h->Pl;
+    {
+      const double ks[4] = {0.25 * hs, hs / 3.0, 0.5 * hs, hs};
+      const double cf[5] = {st.cc, st.ce, st.cw, st.cs, st.cn};
+      for (int j = 0; j < 4; ++j)
+        for (int q = 0; q < 5; ++q) a.kc[j][q] = ks[j] * cf[q];
+    }
     // two RK4 steps per launch for large sweeps (PX_MARCH2=0 forces the one-step kernel); small
     // sweeps keep one step per launch: the 8-stage pipeline fill (16 rows per band) and the
     // 1-CTA-per-3-warps occupancy only pay off when each launch covers ≥ 2^28 lane-points

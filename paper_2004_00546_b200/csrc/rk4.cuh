@@ -31,23 +31,6 @@
 
 namespace px {
 
-// One RK4 stage on a column pair: base + k·(M·w), with M·w split so that the
-// north neighbour (produced by the previous stage in the SAME iteration) enters
-// last through one FMA: base + k·P + (k·cn)·n, P = cc·c + ce·e + cw·w + cs·s.
-// The dependent chain through a march iteration is then one DFMA per stage.
-__device__ __forceinline__ double2 rk_stage(const Stencil5& st, double2 base, double k, double kcn, double2 c,
-                                            double2 s, double2 nn, double l, double r) {
-  double px = st.cc * c.x;
-  px += st.ce * c.y;
-  px += st.cw * l;
-  px += st.cs * s.x;
-  double py = st.cc * c.y;
-  py += st.ce * r;
-  py += st.cw * c.x;
-  py += st.cs * s.y;
-  return make_double2(fma(kcn, nn.x, fma(k, px, base.x)), fma(kcn, nn.y, fma(k, py, base.y)));
-}
-
 constexpr int MARCH_NT = 288;          // 9 warps: pairs of columns per thread
 constexpr int MARCH_MAX_CW = 2 * MARCH_NT;
 constexpr int MARCH_STRIP = 512;       // useful strip width in strip mode
@@ -65,6 +48,8 @@ struct MarchArgs {
   int strip_w;   // useful width per strip (even)
   int halo;      // MARCH_HALO (strips) or 0 (whole periodic row in one CTA)
   int nstrips, band_rows, nbands;
+  // k_rk4_march2: stage-scaled stencil k·(cc, ce, cw, cs, cn) for k = h/4, h/3, h/2, h
+  double kc[4][5];
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -419,9 +404,22 @@ __global__ void __launch_bounds__(M2_NT, MINB) k_rk4_march2(MarchArgs a) {
   const int tr = (t + 1 >= T) ? (full_row ? 0 : T - 1) : t + 1;
   const bool store_ok = active && (2 * t >= a.halo) && (2 * t + 1 < CW - a.halo);
 
-  const Stencil5 st = a.st;
-  const double h = a.h, c1 = a.h * 0.25, c2 = a.h / 3.0, c3 = a.h * 0.5;
-  const double c1n = c1 * a.st.cn, c2n = c2 * a.st.cn, c3n = c3 * a.st.cn, hn = h * a.st.cn;
+  const double h = a.h;
+  // stage j: base + k_j·(M·w) as five FMAs with the pre-scaled coefficients (kernel
+  // parameters, used as constant-bank operands); the north neighbour (this
+  // iteration's previous stage) enters last, so the chain across stages is one DFMA
+  auto stage = [&](auto jc, double2 base, double2 c, double2 so, double2 nn, double l, double r) -> double2 {
+    constexpr int j = decltype(jc)::value;
+    double x = fma(a.kc[j][0], c.x, base.x);
+    x = fma(a.kc[j][1], c.y, x);
+    x = fma(a.kc[j][2], l, x);
+    x = fma(a.kc[j][3], so.x, x);
+    double y = fma(a.kc[j][0], c.y, base.y);
+    y = fma(a.kc[j][1], r, y);
+    y = fma(a.kc[j][2], c.x, y);
+    y = fma(a.kc[j][3], so.y, y);
+    return make_double2(fma(a.kc[j][4], nn.x, x), fma(a.kc[j][4], nn.y, y));
+  };
   const size_t member = (size_t)(lane / a.lanes_per_b);
   const double* __restrict__ bsrc = a.b + member * n;
   const double* __restrict__ ysrc = a.y_in ? a.y_in + (size_t)lane * n : bsrc;
@@ -489,34 +487,34 @@ __global__ void __launch_bounds__(M2_NT, MINB) k_rk4_march2(MarchArgs a) {
       }
       // ---- step A (rows r-1 .. r-4) ----
       if (!G || i >= 2) {
-        nw[1] = rk_stage(st, y3, c1, c1n, y3, y2, yr, pubO[pin][0][tl], pubE[pin][0][tr]);
+        nw[1] = stage(IC<0>{}, y3, y3, y2, yr, pubO[pin][0][tl], pubE[pin][0][tr]);
       }
       if (!G || i >= 4) {
-        nw[2] = rk_stage(st, y2, c2, c2n, wq[1][pp], wq[1][po], nw[1], pubO[pin][1][tl], pubE[pin][1][tr]);
+        nw[2] = stage(IC<1>{}, y2, wq[1][pp], wq[1][po], nw[1], pubO[pin][1][tl], pubE[pin][1][tr]);
       }
       if (!G || i >= 6) {
-        nw[3] = rk_stage(st, y1, c3, c3n, wq[2][pp], wq[2][po], nw[2], pubO[pin][2][tl], pubE[pin][2][tr]);
+        nw[3] = stage(IC<2>{}, y1, wq[2][pp], wq[2][po], nw[2], pubO[pin][2][tl], pubE[pin][2][tr]);
         if (ADJ) zs[((k + 3) % 6) * M2_NT + t] = make_double2(h * nw[3].x, h * nw[3].y);  // row r-3
       }
       if (!G || i >= 8) {  // y⁺ at row r-4
-        nw[4] = rk_stage(st, make_double2(y0.x + b4.x, y0.y + b4.y), h, hn, wq[3][pp], wq[3][po], nw[3],
+        nw[4] = stage(IC<3>{}, make_double2(y0.x + b4.x, y0.y + b4.y), wq[3][pp], wq[3][po], nw[3],
                          pubO[pin][3][tl], pubE[pin][3][tr]);
       }
       pq[(k + 2) % 6] = nw[4];  // y⁺ row r-4
       const double2 p4 = nw[4], p5 = pq[(k + 1) % 6], p6 = pq[k % 6], p7 = pq[(k + 5) % 6], p8 = pq[(k + 4) % 6];
       // ---- step B (rows r-5 .. r-8) on y⁺ ----
       if (!G || i >= 10) {
-        nw[5] = rk_stage(st, p5, c1, c1n, p5, p6, p4, pubO[pin][4][tl], pubE[pin][4][tr]);
+        nw[5] = stage(IC<0>{}, p5, p5, p6, p4, pubO[pin][4][tl], pubE[pin][4][tr]);
       }
       if (!G || i >= 12) {
-        nw[6] = rk_stage(st, p6, c2, c2n, wq[5][pp], wq[5][po], nw[5], pubO[pin][5][tl], pubE[pin][5][tr]);
+        nw[6] = stage(IC<1>{}, p6, wq[5][pp], wq[5][po], nw[5], pubO[pin][5][tl], pubE[pin][5][tr]);
       }
       if (!G || i >= 14) {
-        nw[7] = rk_stage(st, p7, c3, c3n, wq[6][pp], wq[6][po], nw[6], pubO[pin][6][tl], pubE[pin][6][tr]);
+        nw[7] = stage(IC<2>{}, p7, wq[6][pp], wq[6][po], nw[6], pubO[pin][6][tl], pubE[pin][6][tr]);
       }
       if (!G || i >= 16) {  // y⁺⁺ at row r-8
         const double2 w7c = wq[7][pp];
-        const double2 yn = rk_stage(st, make_double2(p8.x + b8.x, p8.y + b8.y), h, hn, w7c, wq[7][po], nw[7],
+        const double2 yn = stage(IC<3>{}, make_double2(p8.x + b8.x, p8.y + b8.y), w7c, wq[7][po], nw[7],
                                     pubO[pin][7][tl], pubE[pin][7][tr]);
         if (store_ok) {
           const size_t off = (size_t)rs * nx + coloff;

@@ -385,3 +385,18 @@ def test_nonlinear_full_config3_converges_to_serial():
     with pytest.raises(IterationDivergence):
         direct_adjoint_loop(c.system, ctrl, ut, "nonlinear", N=c.P, rk=RK4Config(c.dt), expaction=c.expaction,
                             u0=u0, eps=1e-14, max_iter=2)
+
+
+@pytest.mark.parametrize("var", ["3", "2"])
+def test_fused_two_step_march_forced(var):
+    """k_rk4_march2 (two RK4 steps per launch) forced on small/odd shapes in a child
+    process (the kernel choice is read from the environment once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PX_MARCH2="2", PX_M2_VAR=var)
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "_fused_child.py")], env=env, cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert r.stdout.count("ok ") == 5
