@@ -25,6 +25,7 @@ namespace px {
 constexpr int CM_NT = 160;  // 5 warps, pairs of columns: computed width ≤ 320
 constexpr int CM_MAXT = 4;  // terms per pass (template M ≤ CM_MAXT)
 constexpr int CM_DEPTH = 5; // cp.async ring depth (rows)
+constexpr int CM_MINB = 2;  // resident CTAs per SM (3 measured slower: spills + smaller bands)
 
 struct ChebMarchArgs {
   const double* u_prev; long long prev_bs;  // U_{k−1} (unused on the first pass)
@@ -37,6 +38,8 @@ struct ChebMarchArgs {
   Stencil5 st;
   double c0, d, two_over_d, sigma;
   double be[CM_MAXT + 1], bp[CM_MAXT + 1];  // coefficients of terms k … k+M
+  double g[5];  // (2/d)·(cc − c0, ce, cw, cs, cn): U_{j+1} = Σ g·U_j(stencil) + σ·U_{j−1}
+  double f[5];  // (1/d)·(cc − c0, ce, cw, cs, cn): U_1 of the first pass
   int first;
   int nx, ny, B;
   int strip_w, halo, nstrips, band_rows, nbands;
@@ -48,7 +51,7 @@ struct CmUnroll {
 };
 
 template <int M>
-__global__ void __launch_bounds__(CM_NT, 2) k_cheb_march(ChebMarchArgs a) {
+__global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) {
   __shared__ double pubE[2][M][CM_NT];
   __shared__ double pubO[2][M][CM_NT];
   // ring slots (dynamic smem): [depth][4 arrays: cur(r), prev(r−1), acc(r−1), pacc(r−1)][pairs]
@@ -82,7 +85,7 @@ __global__ void __launch_bounds__(CM_NT, 2) k_cheb_march(ChebMarchArgs a) {
   const bool write_u = a.out_cur != nullptr;
 
   const Stencil5 st = a.st;
-  const double c0 = a.c0, d = a.d, tod = a.two_over_d, sig = a.sigma;
+  const double sig = a.sigma;
   const double* __restrict__ cur = a.u_cur + b * a.cur_bs;
   const double* __restrict__ prv = first ? cur : a.u_prev + b * a.prev_bs;
   const double* __restrict__ accin = has_add ? a.addend + b * a.add_bs : a.acc + (size_t)b * n;
@@ -129,29 +132,25 @@ __global__ void __launch_bounds__(CM_NT, 2) k_cheb_march(ChebMarchArgs a) {
 #pragma unroll
   for (int s = 0; s < M; ++s) qa[s] = qp[s] = make_double2(0.0, 0.0);
 
-  // (M − c0)·u for the pair (c centre, s south, nn north, l/r x-neighbours)
-  auto shifted = [&](double2 c, double2 s, double2 nn, double l, double r) -> double2 {
-    double2 o;
-    o.x = st.cc * c.x;
-    o.x += st.ce * c.y;
-    o.x += st.cw * l;
-    o.x += st.cn * nn.x;
-    o.x += st.cs * s.x;
-    o.x -= c0 * c.x;
-    o.y = st.cc * c.y;
-    o.y += st.ce * r;
-    o.y += st.cw * c.x;
-    o.y += st.cn * nn.y;
-    o.y += st.cs * s.y;
-    o.y -= c0 * c.y;
-    return o;
+  // One Chebyshev term on a column pair: Σ_q coef_q·(stencil tap q) + base, the
+  // coefficients pre-scaled on the host (kernel parameters → constant-bank operands);
+  // the north neighbour (this iteration's previous term) enters last.
+  auto term = [&](const double* cf, double2 base, double2 c, double2 so, double2 nn, double l, double r) -> double2 {
+    double x = fma(cf[0], c.x, base.x);
+    x = fma(cf[1], c.y, x);
+    x = fma(cf[2], l, x);
+    x = fma(cf[3], so.x, x);
+    double y = fma(cf[0], c.y, base.y);
+    y = fma(cf[1], r, y);
+    y = fma(cf[2], c.x, y);
+    y = fma(cf[3], so.y, y);
+    return make_double2(fma(cf[4], nn.x, x), fma(cf[4], nn.y, y));
   };
 
-  for (int i0 = 0; i0 < iters; i0 += UN) {
-#pragma unroll
-    for (int k = 0; k < UN; ++k) {
-      const int i = i0 + k;
-      if (i >= iters) break;
+  // One iteration at ring phase k (compile time); G = guarded (pipeline fill/drain).
+  auto iter = [&](auto kc, auto gc, const int i) {
+    constexpr int k = decltype(kc)::value % UN;
+    constexpr bool G = decltype(gc)::value;
       const int pin = (k + 1) & 1;
       const int pout = k & 1;
       cp_async_wait<CM_DEPTH - 1>();
@@ -168,18 +167,17 @@ __global__ void __launch_bounds__(CM_NT, 2) k_cheb_march(ChebMarchArgs a) {
       double2 nq[M + 1];
       nq[0] = ur;
       // term 1 of the pass at row r−1 (creates the acc/pacc entry of that row)
-      if (i >= 2) {
+      if (!G || i >= 2) {
         const double l = pubO[pin][0][tl], r = pubE[pin][0][tr];
-        const double2 sh = shifted(u0m1, u0m2, ur, l, r);
         double2 u1, acc, pc;
         if (first) {
-          u1 = make_double2(sh.x / d, sh.y / d);
+          u1 = term(a.f, make_double2(0.0, 0.0), u0m1, u0m2, ur, l, r);
           acc.x = a.be[0] * u0m1.x + a.be[1] * u1.x + ain.x;
           acc.y = a.be[0] * u0m1.y + a.be[1] * u1.y + ain.y;
           pc.x = pin_v.x + (a.bp[0] * u0m1.x + a.bp[1] * u1.x);
           pc.y = pin_v.y + (a.bp[0] * u0m1.y + a.bp[1] * u1.y);
         } else {
-          u1 = make_double2(tod * sh.x + sig * upv.x, tod * sh.y + sig * upv.y);
+          u1 = term(a.g, make_double2(sig * upv.x, sig * upv.y), u0m1, u0m2, ur, l, r);
           acc = make_double2(ain.x + a.be[1] * u1.x, ain.y + a.be[1] * u1.y);
           pc = make_double2(pin_v.x + a.bp[1] * u1.x, pin_v.y + a.bp[1] * u1.y);
         }
@@ -192,13 +190,12 @@ __global__ void __launch_bounds__(CM_NT, 2) k_cheb_march(ChebMarchArgs a) {
       // terms 2 … M of the pass at rows r−s
 #pragma unroll
       for (int s = 2; s <= M; ++s) {
-        if (i >= 2 * s) {
+        if (!G || i >= 2 * s) {
           const double l = pubO[pin][s - 1][tl], r = pubE[pin][s - 1][tr];
           const double2 c = qs[s - 1][pp];        // row r−s
           const double2 so = qs[s - 1][po];       // row r−s−1
-          const double2 sh = shifted(c, so, nq[s - 1], l, r);
           const double2 pv = (s == 2) ? u0m2 : qs[s - 2][po];  // U_{k+s−2} at row r−s
-          const double2 u = make_double2(tod * sh.x + sig * pv.x, tod * sh.y + sig * pv.y);
+          const double2 u = term(a.g, make_double2(sig * pv.x, sig * pv.y), c, so, nq[s - 1], l, r);
           nq[s] = u;
           const int ai = (k - s + 1 + 2 * M) % M;  // acc slot of row r−s
           qa[ai].x += a.be[s] * u.x;
@@ -210,7 +207,7 @@ __global__ void __launch_bounds__(CM_NT, 2) k_cheb_march(ChebMarchArgs a) {
         }
       }
       // row r−M is complete: acc, pacc, and the pass's last two terms
-      if (i >= 2 * M && store_ok) {
+      if ((!G || i >= 2 * M) && store_ok) {
         const size_t off = (size_t)rs * nx + coloff;
         const int ai = (k - M + 1 + 2 * M) % M;
         __stcs(reinterpret_cast<double2*>(accout + off), qa[ai]);
@@ -232,7 +229,42 @@ __global__ void __launch_bounds__(CM_NT, 2) k_cheb_march(ChebMarchArgs a) {
         }
       }
       __syncthreads();
+  };
+  int i0 = 0;
+  // fill (stages switch on at i = 2, 4, …, 2M) — guarded groups until every stage is live
+  for (; i0 < 2 * M; i0 += UN) {
+    if (i0 + UN > iters) break;
+    iter(IC<0>{}, BC<true>{}, i0); iter(IC<1>{}, BC<true>{}, i0 + 1); iter(IC<2>{}, BC<true>{}, i0 + 2);
+    iter(IC<3>{}, BC<true>{}, i0 + 3); iter(IC<4>{}, BC<true>{}, i0 + 4); iter(IC<5>{}, BC<true>{}, i0 + 5);
+    if (UN == 12) {
+      iter(IC<6>{}, BC<true>{}, i0 + 6); iter(IC<7>{}, BC<true>{}, i0 + 7); iter(IC<8>{}, BC<true>{}, i0 + 8);
+      iter(IC<9>{}, BC<true>{}, i0 + 9); iter(IC<10>{}, BC<true>{}, i0 + 10); iter(IC<11>{}, BC<true>{}, i0 + 11);
     }
+  }
+  if (i0 >= 2 * M) {
+    for (; i0 + UN <= iters; i0 += UN) {  // steady state: no guards
+      iter(IC<0>{}, BC<false>{}, i0); iter(IC<1>{}, BC<false>{}, i0 + 1); iter(IC<2>{}, BC<false>{}, i0 + 2);
+      iter(IC<3>{}, BC<false>{}, i0 + 3); iter(IC<4>{}, BC<false>{}, i0 + 4); iter(IC<5>{}, BC<false>{}, i0 + 5);
+      if (UN == 12) {
+        iter(IC<6>{}, BC<false>{}, i0 + 6); iter(IC<7>{}, BC<false>{}, i0 + 7); iter(IC<8>{}, BC<false>{}, i0 + 8);
+        iter(IC<9>{}, BC<false>{}, i0 + 9); iter(IC<10>{}, BC<false>{}, i0 + 10); iter(IC<11>{}, BC<false>{}, i0 + 11);
+      }
+    }
+  }
+  // drain / short bands
+  if (i0 + 0 < iters) iter(IC<0>{}, BC<true>{}, i0);
+  if (i0 + 1 < iters) iter(IC<1>{}, BC<true>{}, i0 + 1);
+  if (i0 + 2 < iters) iter(IC<2>{}, BC<true>{}, i0 + 2);
+  if (i0 + 3 < iters) iter(IC<3>{}, BC<true>{}, i0 + 3);
+  if (i0 + 4 < iters) iter(IC<4>{}, BC<true>{}, i0 + 4);
+  if (i0 + 5 < iters) iter(IC<5>{}, BC<true>{}, i0 + 5);
+  if (UN == 12) {
+    if (i0 + 6 < iters) iter(IC<6>{}, BC<true>{}, i0 + 6);
+    if (i0 + 7 < iters) iter(IC<7>{}, BC<true>{}, i0 + 7);
+    if (i0 + 8 < iters) iter(IC<8>{}, BC<true>{}, i0 + 8);
+    if (i0 + 9 < iters) iter(IC<9>{}, BC<true>{}, i0 + 9);
+    if (i0 + 10 < iters) iter(IC<10>{}, BC<true>{}, i0 + 10);
+    if (i0 + 11 < iters) iter(IC<11>{}, BC<true>{}, i0 + 11);
   }
   cp_async_wait<0>();
 }

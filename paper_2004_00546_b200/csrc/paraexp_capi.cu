@@ -462,6 +462,13 @@ int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const d
   px::ChebMarchArgs a{};
   a.st = st;
   a.c0 = pl.center; a.d = pl.scale; a.two_over_d = 2.0 / pl.scale; a.sigma = (double)pl.sigma;
+  {
+    const double taps[5] = {st.cc - pl.center, st.ce, st.cw, st.cs, st.cn};
+    for (int q = 0; q < 5; ++q) {
+      a.g[q] = (2.0 / pl.scale) * taps[q];
+      a.f[q] = taps[q] / pl.scale;
+    }
+  }
   a.nx = nx; a.ny = ny; a.B = B;
   static int env_strip = -1, env_band = -1;
   if (env_strip < 0) {
@@ -483,7 +490,7 @@ int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const d
   } else {
     // about one full wave of 2 CTAs per SM, bands of ≥ 32 rows
     const size_t per_band_ctas = (size_t)a.nstrips * B;
-    const size_t target = 2 * 148;
+    const size_t target = (size_t)px::CM_MINB * 148;
     size_t nb_bands = std::max<size_t>(1, target / per_band_ctas);
     br = (int)((ny + nb_bands - 1) / nb_bands);
     if (br < 32) br = std::min(32, ny);
