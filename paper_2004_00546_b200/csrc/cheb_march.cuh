@@ -22,8 +22,8 @@
 
 namespace px {
 
-constexpr int CM_NT = 160;  // 5 warps, pairs of columns: computed width ≤ 320
-constexpr int CM_MAXT = 4;  // terms per pass (template M ≤ CM_MAXT)
+constexpr int CM_NT = 160;  // 5 warps, pairs of columns: computed width ≤ 320 (192 measured slower)
+constexpr int CM_MAXT = 6;  // terms per pass (template M ≤ CM_MAXT; 7+ would need 1 CTA/SM, ≥ 10 spill)
 constexpr int CM_DEPTH = 5; // cp.async ring depth (rows)
 constexpr int CM_MINB = 2;  // resident CTAs per SM (3 measured slower: spills + smaller bands)
 
@@ -46,8 +46,12 @@ struct ChebMarchArgs {
 };
 
 template <int M>
-struct CmUnroll {
-  static constexpr int value = (M == 4) ? 12 : 6;  // lcm(3, 2, M)
+struct CmUnroll {  // multiple of 3 (U_k rows), 2 (stage rows) and R
+  static constexpr int value = (M == 4) ? 12 : 6;
+};
+template <int M>
+struct CmRing {  // acc/pacc row slots (≥ M live rows; UN % R == 0)
+  static constexpr int value = (M <= 3) ? M : (M == 4 ? 4 : 6);
 };
 
 template <int M>
@@ -57,6 +61,7 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
   // ring slots (dynamic smem): [depth][4 arrays: cur(r), prev(r−1), acc(r−1), pacc(r−1)][pairs]
   extern __shared__ double2 cm_ring[];
   constexpr int UN = CmUnroll<M>::value;
+  constexpr int R = CmRing<M>::value;
 
   const int b = blockIdx.x % a.B;
   const int rest = blockIdx.x / a.B;
@@ -124,13 +129,13 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
 
   double2 q0[3];               // U_k rows (ring by phase mod 3)
   double2 qs[M + 1][2];        // stage-s outputs, last two rows (index 1..M)
-  double2 qa[M], qp[M];        // acc / pacc of rows r−1 … r−M (ring by phase mod M)
+  double2 qa[R], qp[R];        // acc / pacc of rows r−1 … r−M (ring by phase mod R)
 #pragma unroll
   for (int k = 0; k < 3; ++k) q0[k] = make_double2(0.0, 0.0);
 #pragma unroll
   for (int s = 0; s <= M; ++s) qs[s][0] = qs[s][1] = make_double2(0.0, 0.0);
 #pragma unroll
-  for (int s = 0; s < M; ++s) qa[s] = qp[s] = make_double2(0.0, 0.0);
+  for (int s = 0; s < R; ++s) qa[s] = qp[s] = make_double2(0.0, 0.0);
 
   // One Chebyshev term on a column pair: Σ_q coef_q·(stencil tap q) + base, the
   // coefficients pre-scaled on the host (kernel parameters → constant-bank operands);
@@ -182,8 +187,8 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
           pc = make_double2(pin_v.x + a.bp[1] * u1.x, pin_v.y + a.bp[1] * u1.y);
         }
         nq[1] = u1;
-        qa[k % M] = acc;
-        qp[k % M] = pc;
+        qa[k % R] = acc;
+        qp[k % R] = pc;
       } else {
         nq[1] = make_double2(0.0, 0.0);
       }
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
           const double2 pv = (s == 2) ? u0m2 : qs[s - 2][po];  // U_{k+s−2} at row r−s
           const double2 u = term(a.g, make_double2(sig * pv.x, sig * pv.y), c, so, nq[s - 1], l, r);
           nq[s] = u;
-          const int ai = (k - s + 1 + 2 * M) % M;  // acc slot of row r−s
+          const int ai = (k - s + 1 + 2 * R) % R;  // acc slot of row r−s
           qa[ai].x += a.be[s] * u.x;
           qa[ai].y += a.be[s] * u.y;
           qp[ai].x += a.bp[s] * u.x;
@@ -209,7 +214,7 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
       // row r−M is complete: acc, pacc, and the pass's last two terms
       if ((!G || i >= 2 * M) && store_ok) {
         const size_t off = (size_t)rs * nx + coloff;
-        const int ai = (k - M + 1 + 2 * M) % M;
+        const int ai = (k - M + 1 + 2 * R) % R;
         __stcs(reinterpret_cast<double2*>(accout + off), qa[ai]);
         if (has_p) __stcs(reinterpret_cast<double2*>(pac + off), qp[ai]);
         if (write_u) {

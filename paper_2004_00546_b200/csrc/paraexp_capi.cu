@@ -470,6 +470,11 @@ int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const d
     }
   }
   a.nx = nx; a.ny = ny; a.B = B;
+  static const int cm_terms = [] {  // fused terms per pass (≤ CM_MAXT)
+    const char* e = getenv("PX_CM_TERMS");
+    const int v = e ? atoi(e) : 6;
+    return std::max(1, std::min(px::CM_MAXT, v));
+  }();
   static int env_strip = -1, env_band = -1;
   if (env_strip < 0) {
     const char* e1 = getenv("PX_CM_STRIP");
@@ -480,8 +485,14 @@ int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const d
   if (nx <= 2 * px::CM_NT && env_strip == 0) {
     a.strip_w = nx; a.halo = 0; a.nstrips = 1;
   } else {
-    a.strip_w = env_strip > 0 ? env_strip : 256;
-    a.halo = px::CM_MAXT;
+    a.halo = cm_terms;  // ≥ the terms of any pass
+    if (env_strip > 0) {
+      a.strip_w = env_strip;
+    } else {  // fewest strips of ≤ 2·CM_NT computed columns, useful widths balanced (even)
+      const int maxw = 2 * px::CM_NT - 2 * a.halo;
+      const int ns = (nx + maxw - 1) / maxw;
+      a.strip_w = ((nx + ns - 1) / ns + 1) & ~1;
+    }
     a.nstrips = (nx + a.strip_w - 1) / a.strip_w;
   }
   int br;
@@ -509,7 +520,7 @@ int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const d
     int k = 0;  // terms done
     bool first = true;
     while (k < K || first) {
-      const int M = std::min(px::CM_MAXT, K - k);
+      const int M = std::min(cm_terms, K - k);
       a.first = first ? 1 : 0;
       a.u_prev = uprev; a.prev_bs = uprev_bs;
       a.u_cur = ucur; a.cur_bs = ucur_bs;
@@ -532,7 +543,9 @@ int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const d
         case 1: rc = launch_cm<1>(h, a, blocks, s); break;
         case 2: rc = launch_cm<2>(h, a, blocks, s); break;
         case 3: rc = launch_cm<3>(h, a, blocks, s); break;
-        default: rc = launch_cm<4>(h, a, blocks, s); break;
+        case 4: rc = launch_cm<4>(h, a, blocks, s); break;
+        case 5: rc = launch_cm<5>(h, a, blocks, s); break;
+        default: rc = launch_cm<6>(h, a, blocks, s); break;
       }
       if (rc != PX_OK) return rc;
       // algorithmic bytes of the pass (streams read + written once)
