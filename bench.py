@@ -355,6 +355,8 @@ def main():
                    "exp_direct": "k_cheb_march<M>" if two_d else "k_scan1d",
                    "exp_adjoint": "k_cheb_march<M>+phi" if two_d else "k_scan1d+phi",
                    "other": "reductions/projection"}[dom]
+    if type(c.expaction).__name__ == "KrylovConfig" and dom.startswith("exp"):
+        kernel_name = "Arnoldi CGS2 (k_kr_spmv_dots/k_kr_update/k_kr_expm/k_kr_combine)"
     if not c.system.is_linear:
         kernel_name = {"rk4_direct": "k_burgers_direct", "rk4_adjoint": "k_burgers_adjoint_rk4+k_burgers_scan"}.get(
             dom, kernel_name)

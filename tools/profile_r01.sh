@@ -4,11 +4,13 @@
 set -x
 mkdir -p gpurun_out
 CMD="python bench.py --profile-only --warmup 0 --steps 1"
-$CMD > gpurun_out/plain_c5.log 2>&1 && \
+$CMD > gpurun_out/plain_c5.log 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file gpurun_out/launches_c5.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 echo launches=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_rk4_march -s 3 -c 2 -o gpurun_out/prof_march_c5 $CMD > gpurun_out/ncu_march.log 2>&1
-echo march=$?
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_cheb_march -s 6 -c 3 -o gpurun_out/prof_cheb_c5 $CMD > gpurun_out/ncu_cheb.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_rk4_march2 -s 22 -c 1 -o gpurun_out/prof_march2_adj_c5 $CMD > gpurun_out/ncu_m2a.log 2>&1
+echo march2_adj=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_rk4_march2 -s 3 -c 1 -o gpurun_out/prof_march2_dir_c5 $CMD > gpurun_out/ncu_m2d.log 2>&1
+echo march2_dir=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_cheb_march -s 10 -c 2 -o gpurun_out/prof_cheb_c5 $CMD > gpurun_out/ncu_cheb.log 2>&1
 echo cheb=$?
 ls -la gpurun_out
