@@ -15,7 +15,8 @@ from ctypes import POINTER, c_double, c_int, c_size_t, c_uint64, c_void_p
 from .errors import NativeUnavailable, raise_for_status
 
 LIB_NAME = "libparaexp.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# PX_LIB: developer override (kernel-variant experiments); the default is the in-tree build
+LIB_PATH = os.environ.get("PX_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 PX_KIND_ADVDIFF, PX_KIND_BURGERS = 0, 1
 PX_EXP_CHEBYSHEV, PX_EXP_KRYLOV = 0, 1

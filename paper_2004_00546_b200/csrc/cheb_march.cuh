@@ -89,7 +89,6 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
   const bool has_p = a.pacc != nullptr;
   const bool write_u = a.out_cur != nullptr;
 
-  const Stencil5 st = a.st;
   const double sig = a.sigma;
   const double* __restrict__ cur = a.u_cur + b * a.cur_bs;
   const double* __restrict__ prv = first ? cur : a.u_prev + b * a.prev_bs;

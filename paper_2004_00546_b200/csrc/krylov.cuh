@@ -22,7 +22,10 @@ namespace px {
 
 constexpr int KRYLOV_MAX_M = 40;
 constexpr double KRYLOV_BREAKDOWN = 1e-13;
-constexpr int KR_PPT = 4;             // points per thread in the Arnoldi passes
+#ifndef PX_KR_PPT
+#define PX_KR_PPT 4
+#endif
+constexpr int KR_PPT = PX_KR_PPT;     // points per thread in the Arnoldi passes
 constexpr int KR_BLK = 256 * KR_PPT;  // points per block
 
 struct KrylovWork {
@@ -71,8 +74,8 @@ __global__ void __launch_bounds__(256) k_kr_sumsq(double* part, int nblk, const 
   const int b = blockIdx.y;
   double v = 0.0;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const size_t i = (size_t)blockIdx.x * 1024 + threadIdx.x + 256 * k;
+  for (int k = 0; k < KR_PPT; ++k) {
+    const size_t i = (size_t)blockIdx.x * KR_BLK + threadIdx.x + 256 * k;
     if (i < n) {
       const double t = y[b * ybs + i];
       v += t * t;
@@ -254,7 +257,6 @@ __device__ void expm_aug_block(double* coef, const double* Hb, double bt, int m,
   double* Aa = sm;            // N×N scaled matrix
   double* E = Aa + N * N;     // accumulator
   double* T = E + N * N;      // scratch
-  __shared__ double s_norm;
   __shared__ int s_sq;
   // meff: first zero subdiagonal
   for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
@@ -297,7 +299,6 @@ __device__ void expm_aug_block(double* coef, const double* Hb, double bt, int m,
       for (int r = 0; r < Ne; ++r) s += fabs(Aa[r * Ne + c]);
       nrm = fmax(nrm, s);
     }
-    s_norm = nrm;
     s_sq = nrm <= 0.5 ? 0 : (int)ceil(log2(nrm / 0.5));
   }
   __syncthreads();
