@@ -58,6 +58,7 @@ inline int krylov_alloc(KrylovWork& kw, int m, size_t n, int B, std::string* err
       !al(&kw.part, (size_t)B * (2 * (KRYLOV_MAX_M + 1) + 1) * std::max<size_t>((size_t)kw.nblk, 148 * 4)) || !al(&kw.beta, B) ||
       !al(&kw.coef, (size_t)B * 2 * m))
     return PX_ERR_NOMEM;
+
   return PX_OK;
 }
 
@@ -123,13 +124,31 @@ __device__ __forceinline__ void block_multi_sum(double (*red)[KRYLOV_MAX_M + 1],
   }
 }
 
+// part[b][q][blk] = Σ_{i in block} V_q[i]·ws[i] for q ≤ j: one warp per column q
+// (q = warp, warp+8, …), each lane streaming the block's chunk of V_q with 8 loads
+// in flight; fixed order (deterministic).
+__device__ __forceinline__ void warp_column_dots(const double* __restrict__ V, int B, int b, size_t n, int j,
+                                                 const double* ws, double* part, int nblk) {
+  const int wid = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  const size_t i0 = (size_t)blockIdx.x * KR_BLK;
+  const int cnt = (int)min((size_t)KR_BLK, n - i0);
+  for (int q = wid; q <= j; q += 8) {
+    const double* __restrict__ Vq = V + ((size_t)q * B + b) * n + i0;
+    double acc = 0.0;
+#pragma unroll 8
+    for (int t = ln; t < KR_BLK; t += 32)
+      if (t < cnt) acc += Vq[t] * ws[t];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if (ln == 0) part[((size_t)b * (KRYLOV_MAX_M + 1) + q) * nblk + blockIdx.x] = acc;
+  }
+}
+
 // Arnoldi step j, first pass: V_j = w_prev·inv (materialised, fused scale of the
 // previous step; j = 0 reads V_0 directly), w = M V_j, part[b][q][blk] = Σ V_q·w.
 template <int DIM>
 __global__ void __launch_bounds__(256) k_kr_spmv_dots(double* w, double* V, const double* w_prev,
                                                       const double* hcol, int j, Stencil5 st, double* part,
                                                       int nblk, int B, int nx, int ny) {
-  __shared__ double red[8][KRYLOV_MAX_M + 1];
   const size_t n = (size_t)nx * ny;
   const int b = blockIdx.y;
   double* Vj = V + ((size_t)j * B + b) * n;
@@ -139,64 +158,60 @@ __global__ void __launch_bounds__(256) k_kr_spmv_dots(double* w, double* V, cons
     src = w_prev + (size_t)b * n;
     inv = hcol[(size_t)b * (KRYLOV_MAX_M + 1)];
   }
-  double wv[KR_PPT], vq[KRYLOV_MAX_M + 1];
+  __shared__ double ws[KR_BLK];
 #pragma unroll
   for (int k = 0; k < KR_PPT; ++k) {
     const size_t i = (size_t)blockIdx.x * KR_BLK + threadIdx.x + 256 * k;
-    wv[k] = 0.0;
+    double wv = 0.0;
     if (i < n) {
       const int y = (int)(i / nx), x = (int)(i - (size_t)y * nx);
-      wv[k] = inv * stencil_at<DIM>(src, st, x, y, nx, ny);
-      w[(size_t)b * n + i] = wv[k];
+      wv = inv * stencil_at<DIM>(src, st, x, y, nx, ny);
+      w[(size_t)b * n + i] = wv;
       if (j > 0) Vj[i] = src[i] * inv;
     }
+    ws[threadIdx.x + 256 * k] = wv;
   }
-  for (int q = 0; q <= j; ++q) {
-    double acc = 0.0;
-    const double* Vq = V + ((size_t)q * B + b) * n;
-#pragma unroll
-    for (int k = 0; k < KR_PPT; ++k) {
-      const size_t i = (size_t)blockIdx.x * KR_BLK + threadIdx.x + 256 * k;
-      if (i < n) acc += (q == j ? src[i] * inv : Vq[i]) * wv[k];
-    }
-    vq[q] = acc;
-  }
-  block_multi_sum(red, j + 1, vq, part + ((size_t)b * (KRYLOV_MAX_M + 1)) * nblk + blockIdx.x, nblk);
+  __syncthreads();  // V_j (global) and w (smem) of this block complete
+  warp_column_dots(V, B, b, n, j, ws, part, nblk);
 }
 
 // w -= Σ_{q≤j} hcol[b][q] V_q; then part = dots (mode 0) or ‖w‖² (mode 1)
-__global__ void __launch_bounds__(256) k_kr_update(double* w, const double* V, int j, const double* hcol,
+__global__ void __launch_bounds__(256) k_kr_update(double* __restrict__ w, const double* __restrict__ V, int j,
+                                                   const double* __restrict__ hcol,
                                                    double* part, int nblk, int B, size_t n, int mode) {
   __shared__ double red[8][KRYLOV_MAX_M + 1];
   __shared__ double hs[KRYLOV_MAX_M + 1];
   const int b = blockIdx.y;
   if (threadIdx.x <= j) hs[threadIdx.x] = hcol[(size_t)b * (KRYLOV_MAX_M + 1) + threadIdx.x];
   __syncthreads();
+  __shared__ double ws[KR_BLK];
   double wv[KR_PPT];
 #pragma unroll
   for (int k = 0; k < KR_PPT; ++k) {
     const size_t i = (size_t)blockIdx.x * KR_BLK + threadIdx.x + 256 * k;
-    wv[k] = 0.0;
-    if (i < n) {
-      double x = w[(size_t)b * n + i];
-      for (int q = 0; q <= j; ++q) x -= hs[q] * V[((size_t)q * B + b) * n + i];
-      wv[k] = x;
-      w[(size_t)b * n + i] = x;
+    wv[k] = i < n ? w[(size_t)b * n + i] : 0.0;
+  }
+#pragma unroll 4
+  for (int q = 0; q <= j; ++q) {  // KR_PPT independent loads per column (× 4 columns in flight)
+    const double hq = hs[q];
+    const double* __restrict__ Vq = V + ((size_t)q * B + b) * n;
+#pragma unroll
+    for (int k = 0; k < KR_PPT; ++k) {
+      const size_t i = (size_t)blockIdx.x * KR_BLK + threadIdx.x + 256 * k;
+      if (i < n) wv[k] -= hq * Vq[i];
     }
   }
-  double vq[KRYLOV_MAX_M + 1];
-  if (mode == 0) {
-    for (int q = 0; q <= j; ++q) {
-      double acc = 0.0;
 #pragma unroll
-      for (int k = 0; k < KR_PPT; ++k) {
-        const size_t i = (size_t)blockIdx.x * KR_BLK + threadIdx.x + 256 * k;
-        if (i < n) acc += V[((size_t)q * B + b) * n + i] * wv[k];
-      }
-      vq[q] = acc;
-    }
-    block_multi_sum(red, j + 1, vq, part + ((size_t)b * (KRYLOV_MAX_M + 1)) * nblk + blockIdx.x, nblk);
+  for (int k = 0; k < KR_PPT; ++k) {
+    const size_t i = (size_t)blockIdx.x * KR_BLK + threadIdx.x + 256 * k;
+    if (i < n) w[(size_t)b * n + i] = wv[k];
+    ws[threadIdx.x + 256 * k] = wv[k];
+  }
+  if (mode == 0) {
+    __syncthreads();
+    warp_column_dots(V, B, b, n, j, ws, part, nblk);
   } else {
+    double vq[1];
     double acc = 0.0;
 #pragma unroll
     for (int k = 0; k < KR_PPT; ++k) acc += wv[k] * wv[k];
