@@ -347,7 +347,7 @@ def main():
     two_d = c.grid.dim == 2
     # two RK4 steps per launch (k_rk4_march2) when the phase launched fewer kernels than steps
     fused = two_d and ph["launches"] / args.steps < (c.nsteps - 1) * 0.75
-    m2 = "k_rk4_march2<{},128,3,3>"
+    m2 = "k_rk4_march2<{},128,3,3,tma>"
     kernel_name = {"rk4_direct": (m2.format("false") if fused else "k_rk4_march<false>") if two_d
                    else "k_rk4_lane1d<false>",
                    "rk4_adjoint": (m2.format("true") if fused else "k_rk4_march<true>") if two_d

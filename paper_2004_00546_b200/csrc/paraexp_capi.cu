@@ -330,23 +330,24 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
       a.nbands = (ny + a.band_rows - 1) / a.band_rows;
       const unsigned blocks = (unsigned)((size_t)h->L * a.nstrips * a.nbands);
       auto launch2 = [&]() -> int {
-#define PX_M2(NT, DEP, MB, TM)                                                                             \
+#define PX_M2(NT, DEP, MB, TM, ...)                                                                            \
   do {                                                                                                     \
     const size_t sm = px::march2_smem<NT, DEP>(adjoint);                                                   \
     static bool attr[2] = {false, false};                                                                  \
     if (!attr[adjoint]) {                                                                                  \
-      if (adjoint) PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march2<true, NT, DEP, MB, TM>,                \
+      if (adjoint) PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march2<true, NT, DEP, MB, TM, ##__VA_ARGS__>,                \
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
-      else PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march2<false, NT, DEP, MB, TM>,                       \
+      else PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march2<false, NT, DEP, MB, TM, ##__VA_ARGS__>,                       \
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));         \
       attr[adjoint] = true;                                                                                \
     }                                                                                                      \
-    if (adjoint) px::k_rk4_march2<true, NT, DEP, MB, TM><<<blocks, NT, sm, s>>>(a);                        \
-    else px::k_rk4_march2<false, NT, DEP, MB, TM><<<blocks, NT, sm, s>>>(a);                               \
+    if (adjoint) px::k_rk4_march2<true, NT, DEP, MB, TM, ##__VA_ARGS__><<<blocks, NT, sm, s>>>(a);                        \
+    else px::k_rk4_march2<false, NT, DEP, MB, TM, ##__VA_ARGS__><<<blocks, NT, sm, s>>>(a);                               \
   } while (0)
         static const int m2_tma = [] { const char* e = getenv("PX_M2_TMA"); return e ? atoi(e) : 1; }();
         if (m2_var == 2) PX_M2(192, 3, 2, false);  // 2 CTAs/SM
-        else if (m2_tma) PX_M2(128, 3, 3, true);   // 3 CTAs/SM, TMA row ring (default)
+        else if (m2_tma == 1) PX_M2(128, 3, 3, true, true);  // 3 CTAs/SM, TMA row ring, h·w3 in registers (default)
+        else if (m2_tma) PX_M2(128, 3, 3, true);             // TMA row ring, h·w3 rows in smem
         else PX_M2(128, 3, 3, false);              // 3 CTAs/SM, per-thread cp.async ring
 #undef PX_M2
         return PX_OK;

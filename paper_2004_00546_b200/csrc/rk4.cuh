@@ -401,7 +401,7 @@ template <int V> struct IC { static constexpr int value = V; };
 template <bool V> struct BC { static constexpr bool value = V; };
 
 // NT threads (2 columns each), DEPTH ring rows of y(r), b(r−4), b(r−8), z(r−8)
-template <bool ADJ, int M2_NT, int M2_DEPTH, int MINB, bool TMA>
+template <bool ADJ, int M2_NT, int M2_DEPTH, int MINB, bool TMA, bool ZREG = false>
 __global__ void __launch_bounds__(M2_NT, MINB) k_rk4_march2(MarchArgs a) {
   constexpr int NQ = ADJ ? 4 : 3;
   extern __shared__ double2 dyn2[];
@@ -520,6 +520,7 @@ __global__ void __launch_bounds__(M2_NT, MINB) k_rk4_march2(MarchArgs a) {
 
   // rings (phase k = i mod 6): y rows r-4..r, y⁺ rows r-8..r-4, h·w3 rows r-8..r-3
   double2 yq[6], pq[6];
+  double2 zq[6];  // ZREG: h·w3 rows r-8..r-3 in registers instead of smem (20 B of spill, 3% faster)
   double2 wq[8][2];  // stage outputs w1,w2,w3 (1..3) and w5,w6,w7 (5..7): last two rows
 #pragma unroll
   for (int k = 0; k < 6; ++k) yq[k] = pq[k] = make_double2(0.0, 0.0);
@@ -562,7 +563,10 @@ __global__ void __launch_bounds__(M2_NT, MINB) k_rk4_march2(MarchArgs a) {
       }
       if (!G || i >= 6) {
         nw[3] = stage(IC<2>{}, y1, wq[2][pp], wq[2][po], nw[2], pubO[pin][2][tl], pubE[pin][2][tr]);
-        if (ADJ) zs[((k + 3) % 6) * M2_NT + t] = make_double2(h * nw[3].x, h * nw[3].y);  // row r-3
+        if (ADJ) {
+          if constexpr (ZREG) zq[(k + 3) % 6] = make_double2(h * nw[3].x, h * nw[3].y);  // row r-3
+          else zs[((k + 3) % 6) * M2_NT + t] = make_double2(h * nw[3].x, h * nw[3].y);
+        }
       }
       if (!G || i >= 8) {  // y⁺ at row r-4
         nw[4] = stage(IC<3>{}, make_double2(y0.x + b4.x, y0.y + b4.y), wq[3][pp], wq[3][po], nw[3],
@@ -588,7 +592,7 @@ __global__ void __launch_bounds__(M2_NT, MINB) k_rk4_march2(MarchArgs a) {
           const size_t off = (size_t)rs * nx + coloff;
           __stcs(reinterpret_cast<double2*>(yout + off), yn);
           if (ADJ) {
-            const double2 za = zs[((k + 4) % 6) * M2_NT + t];  // h·w3 at row r-8
+            const double2 za = ZREG ? zq[(k + 4) % 6] : zs[((k + 4) % 6) * M2_NT + t];  // h·w3 at row r-8
             double2 zn;
             zn.x = zrow.x + za.x + h * w7c.x;
             zn.y = zrow.y + za.y + h * w7c.y;
