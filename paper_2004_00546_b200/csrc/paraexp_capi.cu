@@ -1001,6 +1001,7 @@ void px_destroy(void* handle) {
 
 int px_set_basis(void* handle, const double* tx, const double* ty, const int* ix, const int* iy) {
   Handle* h = static_cast<Handle*>(handle);
+  if (h) cudaSetDevice(h->device);  // the handle's device (static cudart: per-thread current device)
   if (!h || !tx || !ty || !ix || !iy) return fail(h, PX_ERR_ARG, "null argument");
   for (int k = 0; k < h->K; ++k)
     if (ix[k] < 0 || ix[k] >= h->rows_x || iy[k] < 0 || iy[k] >= h->rows_y)
@@ -1061,6 +1062,7 @@ int px_set_krylov_plan(void* handle, int slot, double span, int substeps) {
 int px_set_inputs(void* handle, const double* u0, const double* u_target, const double* ctrl, int mem,
                   void* stream) {
   Handle* h = static_cast<Handle*>(handle);
+  if (h) cudaSetDevice(h->device);  // the handle's device (static cudart: per-thread current device)
   if (!h || !u0 || !u_target || !ctrl) return fail(h, PX_ERR_ARG, "null argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const cudaMemcpyKind kind = mem == PX_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
@@ -1074,6 +1076,7 @@ int px_set_inputs(void* handle, const double* u0, const double* u_target, const 
 
 int px_direct(void* handle, void* stream) {
   Handle* h = static_cast<Handle*>(handle);
+  if (h) cudaSetDevice(h->device);  // the handle's device (static cudart: per-thread current device)
   if (!h) return fail(h, PX_ERR_ARG, "null handle");
   if (!h->basis_set || !h->inputs_set) return fail(h, PX_ERR_STATE, "basis/inputs not set");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1101,6 +1104,7 @@ int px_direct(void* handle, void* stream) {
 
 int px_finish_direct(void* handle, void* stream) {
   Handle* h = static_cast<Handle*>(handle);
+  if (h) cudaSetDevice(h->device);  // the handle's device (static cudart: per-thread current device)
   if (!h) return fail(h, PX_ERR_ARG, "null handle");
   if (h->stage != 1) return fail(h, PX_ERR_STATE, "px_finish_direct before px_direct");
   int rc = finish_direct_impl(h, static_cast<cudaStream_t>(stream));
@@ -1122,6 +1126,7 @@ px::NlPlan nl_plan(const Plan& pl) {
 
 int px_nl_init(void* handle, void* stream) {
   Handle* h = static_cast<Handle*>(handle);
+  if (h) cudaSetDevice(h->device);  // the handle's device (static cudart: per-thread current device)
   if (!h) return fail(h, PX_ERR_ARG, "null handle");
   if (h->d.kind != PX_KIND_BURGERS || !h->traj_b) return fail(h, PX_ERR_ARG, "iterative direct: Burgers, one rank");
   if (!h->inputs_set || !h->basis_set) return fail(h, PX_ERR_STATE, "basis/inputs not set");
@@ -1147,12 +1152,14 @@ int nl_means_bounds(Handle* h, cudaStream_t s) {
 
 int px_nl_prepare(void* handle, void* stream) {
   Handle* h = static_cast<Handle*>(handle);
+  if (h) cudaSetDevice(h->device);  // the handle's device (static cudart: per-thread current device)
   if (!h || !h->traj_b) return fail(h, PX_ERR_ARG, "iterative direct not available");
   return nl_means_bounds(h, static_cast<cudaStream_t>(stream));
 }
 
 int px_nl_sweep(void* handle, double* err_max, void* stream) {
   Handle* h = static_cast<Handle*>(handle);
+  if (h) cudaSetDevice(h->device);  // the handle's device (static cudart: per-thread current device)
   if (!h || !h->traj_b || !err_max) return fail(h, PX_ERR_ARG, "iterative direct not available");
   const Plan& ps = h->plans[PX_PLAN_NL_SLICE];
   const Plan& pt = h->plans[PX_PLAN_NL_STEP];
@@ -1209,6 +1216,7 @@ int px_nl_sweep(void* handle, double* err_max, void* stream) {
 
 int px_nl_finish(void* handle, void* stream) {
   Handle* h = static_cast<Handle*>(handle);
+  if (h) cudaSetDevice(h->device);  // the handle's device (static cudart: per-thread current device)
   if (!h || !h->traj_b) return fail(h, PX_ERR_ARG, "iterative direct not available");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t S = (size_t)h->d.P * h->d.nsteps;
@@ -1221,6 +1229,7 @@ int px_nl_finish(void* handle, void* stream) {
 
 int px_set_adjoint_terminal(void* handle, const double* qdag_T, int mem, void* stream) {
   Handle* h = static_cast<Handle*>(handle);
+  if (h) cudaSetDevice(h->device);  // the handle's device (static cudart: per-thread current device)
   if (!h || !qdag_T) return fail(h, PX_ERR_ARG, "null argument");
   if (!h->basis_set) return fail(h, PX_ERR_STATE, "basis not set");
   if (h->d.kind == PX_KIND_BURGERS && h->stage < 1)
@@ -1236,6 +1245,7 @@ int px_set_adjoint_terminal(void* handle, const double* qdag_T, int mem, void* s
 
 int px_adjoint(void* handle, void* stream) {
   Handle* h = static_cast<Handle*>(handle);
+  if (h) cudaSetDevice(h->device);  // the handle's device (static cudart: per-thread current device)
   if (!h) return fail(h, PX_ERR_ARG, "null handle");
   if (h->stage != 2) return fail(h, PX_ERR_STATE, "px_adjoint before px_finish_direct");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1270,6 +1280,7 @@ int px_adjoint(void* handle, void* stream) {
 
 int px_finish_adjoint(void* handle, void* stream) {
   Handle* h = static_cast<Handle*>(handle);
+  if (h) cudaSetDevice(h->device);  // the handle's device (static cudart: per-thread current device)
   if (!h) return fail(h, PX_ERR_ARG, "null handle");
   if (h->stage != 3) return fail(h, PX_ERR_STATE, "px_finish_adjoint before px_adjoint");
   int rc = finish_adjoint_impl(h, static_cast<cudaStream_t>(stream));
@@ -1316,6 +1327,7 @@ int capture_gradient(Handle* h) {
 
 int px_gradient(void* handle, void* stream) {
   Handle* h = static_cast<Handle*>(handle);
+  if (h) cudaSetDevice(h->device);  // the handle's device (static cudart: per-thread current device)
   if (!h) return fail(h, PX_ERR_ARG, "null handle");
   if (h->d.kind != PX_KIND_ADVDIFF) return fail(h, PX_ERR_ARG, "px_gradient: linear testbed only");
   if (!h->graphs) return gradient_phases(h, stream);
@@ -1395,6 +1407,7 @@ int px_buffer(void* handle, int field, double** dev_ptr, size_t* count) {
 
 int px_get(void* handle, int field, double* dst, size_t count, int mem, void* stream) {
   Handle* h = static_cast<Handle*>(handle);
+  if (h) cudaSetDevice(h->device);  // the handle's device (static cudart: per-thread current device)
   double* src = nullptr;
   size_t have = 0;
   PX_TRY(px_buffer(handle, field, &src, &have));

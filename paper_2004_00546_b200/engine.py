@@ -142,6 +142,13 @@ class ParaexpEngine:
         d.krylov_m = spec.expaction.m if krylov else 0
         d.flags = N.PX_FLAG_BOUNDARY_STATES if spec.boundary_states else 0
         self._desc = d
+        torch = _torch()
+        if torch is not None and torch.cuda.is_available():
+            # libparaexp links cudart statically: it allocates on the device whose primary
+            # context is current on this thread, so make torch's device (LOCAL_RANK under
+            # torchrun) current before the handle allocates
+            torch.cuda.set_device(torch.cuda.current_device())
+            torch.cuda.current_stream().synchronize()
         h = ctypes.c_void_p()
         N.check(self.lib, self.lib.px_create(ctypes.byref(d), ctypes.byref(h)))
         self.h = h
