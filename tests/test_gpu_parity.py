@@ -259,13 +259,15 @@ def test_device_inputs_match_host_inputs():
     assert np.array_equal(host["grad"], dev["grad"])
 
 
-def test_full_config5_gradient_vs_directional_fd():
-    """Full BASELINE size (2048², P = 512): J is quadratic in c, so the central
-    difference along a random direction is exact up to rounding; the adjoint
-    gradient must agree (size-independent property, oracle too slow at full size)."""
+@pytest.mark.parametrize("index", [4, 5])
+def test_full_config_gradient_vs_directional_fd(index):
+    """Full BASELINE size (config 5: 2048², P = 512; config 4: 512², P = 128, Krylov):
+    J is quadratic in c, so the central difference along a random direction is exact
+    up to rounding (and, for Krylov, the exp-action tolerance); the adjoint gradient
+    must agree (size-independent property, oracle too slow at full size)."""
     from paper_2004_00546_b200 import RK4Config, baseline
     from paper_2004_00546_b200.optimization import get_engine
-    c = baseline(5)
+    c = baseline(index)
     u0, ut, ctrl = c.inputs()
     eng = get_engine(c.system, c.P, RK4Config(c.dt), c.expaction, c.batch)
     eng.set_inputs(u0, ut, ctrl)
@@ -400,3 +402,74 @@ def test_fused_two_step_march_forced(var):
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert r.stdout.count("ok ") == 5
+
+
+def test_full_config5_every_lane_vs_oracle_rk4():
+    """Full BASELINE config 5 (2048², P = 512, 40 RK4 steps per slice) through the fused
+    two-step march kernels: all 512 direct lanes (and all 512 adjoint lanes) are bitwise
+    identical to each other (same slice problem, same kernel arithmetic in every strip and
+    band), and lane 0 equals the oracle's classical-RK4 slice solve at full size."""
+    import torch
+    from oracle.config_mode import rk4_linear, stencil_apply
+    from paper_2004_00546_b200 import RK4Config, _native as N, baseline
+    from paper_2004_00546_b200.optimization import get_engine
+    c = baseline(5)
+    u0, ut, ctrl = c.inputs()
+    nx, ny, n = c.grid.nx, c.grid.ny, c.n
+    A = c.system.A.as_tuple()
+    AT = tuple(np.asarray(A)[[0, 2, 1, 4, 3]])
+    h = c.spec.T / c.P / c.nsteps
+    eng = get_engine(c.system, c.P, RK4Config(c.dt), c.expaction, c.batch)
+    eng.set_inputs(u0, ut, ctrl)
+
+    def lanes_identical(field):
+        V = eng.device_view(field).view(c.P, n)
+        for p0 in range(0, c.P, 64):
+            assert torch.equal(V[p0:p0 + 64], V[0:1].expand(min(64, c.P - p0), n)), f"lanes {p0}.. differ"
+        return V[0].cpu().numpy()
+
+    eng.direct_partial()
+    torch.cuda.synchronize()
+    v0 = lanes_identical(N.PX_FIELD_VEND)
+    f = c.system.basis.field(np.atleast_2d(ctrl))[0]
+    g = stencil_apply(A, u0, nx, ny) + f
+    v_ref, _ = rk4_linear(lambda u: stencil_apply(A, u, nx, ny), g, h, c.nsteps)
+    assert rel_l2(v0, v_ref) <= 1e-12
+
+    eng.finish_direct()
+    eng.adjoint_partial()
+    torch.cuda.synchronize()
+    w0 = lanes_identical(N.PX_FIELD_WEND)
+    qT = eng.get(N.PX_FIELD_UT) - ut
+    gadj = stencil_apply(AT, qT, nx, ny)
+    w_ref, _ = rk4_linear(lambda u: stencil_apply(AT, u, nx, ny), gadj, h, c.nsteps)
+    assert rel_l2(w0, w_ref) <= 1e-12
+    eng.finish_adjoint()
+
+
+def test_full_config5_chebyshev_carry_vs_oracle():
+    """Full config 5: the summed-chain carry through the fused 6+5-term Chebyshev march
+    passes (7 strips of 294 columns, one wave of bands) — boundary states u(T_1), u(T_2),
+    u(T_3) from the GPU; the oracle applies the same planned series to the GPU's v."""
+    from oracle.config_mode import cheb_action, stencil_apply
+    from paper_2004_00546_b200 import RK4Config, _native as N, baseline, release_engines
+    from paper_2004_00546_b200.expaction import plan_for
+    from paper_2004_00546_b200.optimization import get_engine
+    release_engines()
+    c = baseline(5)
+    u0, ut, ctrl = c.inputs()
+    nx, ny, n = c.grid.nx, c.grid.ny, c.n
+    A = c.system.A.as_tuple()
+    eng = get_engine(c.system, c.P, RK4Config(c.dt), c.expaction, c.batch, boundary_states=True)
+    eng.set_inputs(u0, ut, ctrl)
+    eng.direct_partial()
+    U = eng.device_view(N.PX_FIELD_UBND).view(c.P + 1, n)
+    D = [U[p].cpu().numpy() - u0 for p in (1, 2, 3)]
+    plan = plan_for(c.system.region(), c.spec.T / c.P, c.expaction)
+    apply = lambda u: stencil_apply(A, u, nx, ny)
+    v = D[0]
+    d2 = cheb_action(apply, plan, D[0]) + v
+    assert rel_l2(D[1], d2) <= 1e-12
+    d3 = cheb_action(apply, plan, D[1]) + v
+    assert rel_l2(D[2], d3) <= 1e-12
+    release_engines()
