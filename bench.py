@@ -283,9 +283,16 @@ def main():
     import torch
     import torch.distributed as dist
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
+    dev_index = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # PX_BENCH_DIST_BACKEND=gloo: host-mediated collectives, for exercising the multi-rank
+        # path with fewer GPUs than ranks (no kernel waits on another rank); default NCCL
+        backend = os.environ.get("PX_BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
     from paper_2004_00546_b200 import RK4Config, baseline, direct_adjoint_loop
     from paper_2004_00546_b200.engine import EngineSpec, ParaexpEngine
 
@@ -315,7 +322,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev_index) as clk:
         start.record(stream)
         for _ in range(args.steps):
             step()

@@ -473,3 +473,32 @@ def test_full_config5_chebyshev_carry_vs_oracle():
     d3 = cheb_action(apply, plan, D[1]) + v
     assert rel_l2(D[2], d3) <= 1e-12
     release_engines()
+
+
+@pytest.mark.parametrize("kind", ["c5", "3"])
+def test_two_rank_gloo_on_one_gpu(kind, tmp_path):
+    """The real distributed path (torchrun, 2 processes, block-scan + torch.distributed
+    allreduce of the partials) on the one available GPU with gloo collectives, against the
+    single-process result: equal up to the block-scan's long-span truncation."""
+    import os
+    import subprocess
+    import sys
+    from paper_2004_00546_b200 import RK4Config, baseline, direct_adjoint_loop, scaled
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "r.npz")
+    port = str(29600 + (os.getpid() % 300))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", port, os.path.join(root, "tests", "_dist_child.py"),
+           out, kind]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    d = np.load(out)
+    c = scaled(baseline(5), nx=96, P=12, steps_per_slice=8, K=16) if kind == "c5" else baseline(int(kind))
+    u0, ut, ctrl = c.inputs()
+    loop = direct_adjoint_loop(c.system, ctrl, ut, "linear" if c.system.is_linear else "hybrid", N=c.P,
+                               rk=RK4Config(c.dt), expaction=c.expaction, u0=u0, distributed=False)
+    assert rel_l2(d["uT"], loop.direct.final_state) <= 1e-10
+    assert rel_l2(d["qdag0"], loop.adjoint.initial_state) <= 1e-10
+    assert rel_l2(d["G"], loop.adjoint.integral) <= 1e-10
+    assert rel_l2(d["grad"], np.ravel(loop.grad)) <= 1e-8
+    assert np.max(np.abs(d["J"] - np.ravel(loop.J)) / np.abs(np.ravel(loop.J))) <= 1e-10
