@@ -226,11 +226,13 @@ def _as_batch(a, n):
 
 def linear_gradient(grid_nx, grid_ny, A, basis, T, P, nsteps, u0, u_target, ctrl,
                     plan_slice, plan_long_direct=None, plan_long_adjoint=None,
-                    formulation: str = "scan", world: int = 1, want_boundary=False):
+                    formulation: str = "scan", world: int = 1, want_boundary=False, qdag_T=None):
     """One Paraexp direct-adjoint gradient for the linear testbed (App. B of SURVEY).
 
     ``A`` stencil tuple; ``basis`` ModeBasis; ``ctrl`` (B, K). ``plan_long_*``:
-    callables span → plan for the blockscan long spans (world > 1).
+    callables span → plan for the blockscan long spans (world > 1). ``qdag_T``
+    overrides the adjoint's terminal condition (a checkpointed segment's carried q†,
+    `checkpointing.py:192-251`); default u(T) − u_target.
     """
     nx, ny = grid_nx, grid_ny
     n = nx * ny
@@ -286,6 +288,8 @@ def linear_gradient(grid_nx, grid_ny, A, basis, T, P, nsteps, u0, u_target, ctrl
 
     qT = uT - ut
     J = 0.5 * np.sum(qT * qT, axis=1)
+    if qdag_T is not None:
+        qT = np.broadcast_to(_as_batch(qdag_T, n), (B, n)).copy()
 
     # adjoint: w' = Aᵀ(w + q†_T), zero data, per slice; z = ∫w
     gadj = applyAT(qT)
@@ -358,7 +362,7 @@ def slice_means(traj, P, nsteps):
 
 
 def burgers_gradient(nx, D, basis, T, P, nsteps, u0, u_target, ctrl, plan_for_region,
-                     region_fn, world: int = 1, traj=None):
+                     region_fn, world: int = 1, traj=None, qdag_T=None):
     """Config 3 (Option A of SURVEY §8(c)): absorbed final condition, exact Jᵀ(u(t))
     in the inhomogeneous solves, frozen J(ū_p)ᵀ in the homogeneous ones."""
     n = nx
@@ -375,6 +379,8 @@ def burgers_gradient(nx, D, basis, T, P, nsteps, u0, u_target, ctrl, plan_for_re
     uT = traj[-1]
     qT = uT - ut
     J = 0.5 * np.sum(qT * qT, axis=1)
+    if qdag_T is not None:   # checkpointed segment: carried q† (`checkpointing.py:192-251`)
+        qT = np.broadcast_to(_as_batch(qdag_T, n), (B, n)).copy()
 
     ubar = slice_means(traj, P, nsteps)                          # (P, B, n)
     region = region_fn(ubar)
@@ -594,3 +600,28 @@ def burgers_iterative_direct(nx, D, basis, T, P, nsteps, u0, ctrl, plan_for_regi
         if err < eps and it >= min_iter:
             return Q, it, history
     raise RuntimeError(f"no convergence after {max_iter} sweeps: {history}")
+
+
+# ---------------------------------------------------------------------------
+# Equispaced checkpointing (`checkpointing.py:119-267`) over the config-mode pieces
+# ---------------------------------------------------------------------------
+
+
+def checkpointed_gradient(segment_gradient, direct_final, u0, M: int):
+    """Rough forward sweep keeping M+1 segment-start states, then segments walked
+    backward, each solved by ``segment_gradient(u_start, qdag_T)`` (``qdag_T`` None on
+    the last segment: the objective's own terminal condition) and seeded with the
+    carried q†. ``direct_final(u_start)`` is a segment's direct final state.
+    Returns (J, grad, qdag0, G, uT, states)."""
+    states = [np.asarray(u0, dtype=np.float64)]
+    for _ in range(M):
+        states.append(direct_final(states[-1]))
+    grad = G = qd = J = uT = None
+    for m in range(M, -1, -1):
+        r = segment_gradient(states[m], qd)
+        if qd is None:
+            J, uT = r.J, r.uT
+        grad = r.grad if grad is None else grad + r.grad
+        G = r.G if G is None else G + r.G
+        qd = r.qdag0
+    return J, grad, qd, G, uT, states

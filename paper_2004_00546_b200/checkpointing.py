@@ -1,0 +1,202 @@
+"""Equispaced checkpointing on the GPU path.
+
+Mirror of `pkg/src/paradjoint/checkpointing.py:34-267` (`CheckpointSchedule`,
+`MemoryCounter`, `run_checkpointed_loop`) for the BASELINE objective
+J = ½‖u(T) − u_target‖² and time-constant controls:
+
+* phase 1 (`checkpointing.py:161-181`): a rough forward sweep over the M+1 segments
+  keeps only the M+1 segment-start states (the direct solve of each segment runs on
+  the device; only its final state is read back);
+* phase 2 (`checkpointing.py:192-251`): segments are walked backward; each segment's
+  direct solution is recomputed from its checkpoint (the Burgers dense trajectory of
+  that segment only is resident), its Paraexp adjoint is seeded with the carried
+  q† (`px_set_adjoint_terminal`), and the gradient, ∫q† dt and q†(t_m) accumulate.
+
+Each segment is a fresh [0, T/(M+1)] problem with ``N`` slices (the reference's
+`seg_partition`), so one engine (one set of HBM buffers sized for a segment) serves
+every segment: device memory for the Burgers trajectory falls from P·n_s + 1 to
+N·n_s + 1 nodes and, for the linear testbed, the lane buffers from P to N lanes.
+The forward sweep is the same step sequence as the unsegmented sweep (bitwise for
+the serial Burgers direct); the adjoint's Paraexp decomposition is per segment, so
+for M > 0 it differs from the unsegmented one by the Paraexp approximation
+(exp-action truncation; frozen-operator error for Burgers), and for M = 0 it is the
+plain loop.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as NV
+from .errors import ConfigError
+from .optimization import HYBRID, LINEAR, _default_expaction, get_engine
+from .partition import RK4Config
+from .systems import System
+
+
+@dataclass(frozen=True)
+class CheckpointSchedule:
+    """M equispaced checkpoints t_i = i·T/(M+1) inside (0, T) (`checkpointing.py:34-59`)."""
+
+    T: float
+    checkpoints: int
+
+    def __post_init__(self):
+        if self.T <= 0:
+            raise ValueError("T must be positive")
+        if self.checkpoints < 0:
+            raise ValueError("checkpoint count cannot be negative")
+
+    @property
+    def segment_count(self) -> int:
+        return self.checkpoints + 1
+
+    @property
+    def times(self) -> np.ndarray:
+        M = self.checkpoints
+        return self.T * np.arange(1, M + 1) / (M + 1)
+
+    @property
+    def segment_bounds(self) -> list[tuple[float, float]]:
+        edges = np.concatenate([[0.0], self.times, [self.T]])
+        return [(float(edges[i]), float(edges[i + 1])) for i in range(len(edges) - 1)]
+
+
+class MemoryCounter:
+    """Resident dense-trajectory nodes, peak and current (`checkpointing.py:62-76`)."""
+
+    def __init__(self):
+        self.current = 0
+        self.peak = 0
+        self.total_allocated = 0
+
+    def acquire(self, nodes: int):
+        self.current += nodes
+        self.total_allocated += nodes
+        self.peak = max(self.peak, self.current)
+
+    def release(self, nodes: int):
+        self.current -= nodes
+
+
+@dataclass
+class CheckpointRun:
+    """Result of `run_checkpointed_loop` (`checkpointing.py:79-91`, GPU fields)."""
+
+    gradient: np.ndarray            # (B, K) ∂J/∂c
+    qdag0: np.ndarray               # (B, n) q†(0)
+    cost: np.ndarray                # (B,) J
+    integral: np.ndarray            # (B, n) ∫₀ᵀ q† dt
+    final_state: np.ndarray         # (B, n) u(T)
+    segment_bounds: list[tuple[float, float]]
+    checkpoint_states: list[np.ndarray]           # u(t_m), m = 0 … M
+    adjoint_checkpoint_states: list[np.ndarray]   # q†(t_m), m = 0 … M
+    memory: MemoryCounter
+    segment_grads: list[np.ndarray] = field(default_factory=list)
+
+
+def segment_system(system: System, T_seg: float) -> System:
+    """The system on a segment in local time τ = t − t0 (the controls are time-constant,
+    so only the horizon changes; `checkpointing.py:94-101`)."""
+    return dataclasses.replace(system, spec=dataclasses.replace(system.spec, T=T_seg))
+
+
+def run_checkpointed_loop(
+    system: System,
+    f: np.ndarray,
+    q_true: np.ndarray,
+    sched: CheckpointSchedule,
+    algorithm: str | None = None,
+    N: int = 1,
+    rk: RK4Config | None = None,
+    expaction=None,
+    u0: np.ndarray | None = None,
+    backend: str = "cuda",
+) -> CheckpointRun:
+    """Direct-adjoint loop under equispaced checkpointing (`checkpointing.py:119-267`).
+
+    ``N`` is the number of Paraexp slices per segment (as the reference's
+    `seg_partition`); ``algorithm`` is "linear" (advection–diffusion) or "hybrid"
+    (Burgers: serial direct recomputed per segment + frozen-operator Paraexp adjoint).
+    """
+    if backend != "cuda":
+        raise ValueError(f"unknown backend {backend!r}; the B200 path provides ('cuda',)")
+    if rk is None:
+        raise ConfigError("rk: an RK4Config(dt) is required (fixed-step RK4)")
+    if abs(sched.T - system.spec.T) > 1e-12 * system.spec.T:
+        raise ValueError("schedule horizon differs from the system's T")
+    algorithm = algorithm or (LINEAR if system.is_linear else HYBRID)
+    if algorithm not in (LINEAR, HYBRID):
+        raise ValueError(f"checkpointed runs support 'linear' and 'hybrid', not {algorithm!r}")
+    if (algorithm == LINEAR) != system.is_linear:
+        raise ValueError(f"the {algorithm} algorithm does not match the testbed")
+    expaction = expaction or _default_expaction(system)
+    ctrl = np.atleast_2d(np.asarray(f, dtype=np.float64))
+    B = ctrl.shape[0]
+    if ctrl.shape[1] != system.basis.K:
+        raise ValueError("control coefficient count does not match the basis")
+    if B != 1:
+        # segment start states differ per control member; the handle takes one u0
+        raise ConfigError("checkpointed runs take one control (batch 1)")
+    n = system.n
+    u0 = np.zeros(n) if u0 is None else np.asarray(u0, dtype=np.float64).reshape(-1)
+    ut = np.asarray(q_true, dtype=np.float64).reshape(-1)
+
+    bounds = sched.segment_bounds
+    M1 = sched.segment_count
+    T_seg = sched.T / M1
+    seg = segment_system(system, T_seg)
+    eng = get_engine(seg, N, rk, expaction, B)
+    nodes_per_segment = N * eng.spec.nsteps + 1 if not system.is_linear else 0
+    memory = MemoryCounter()
+
+    # ---- phase 1: rough sweep, checkpoint states only ----------------------
+    states = [u0.reshape(1, n).copy()]
+    for m in range(M1 - 1):
+        eng.set_inputs(states[-1][0], ut, ctrl)
+        eng.direct_partial()
+        if system.is_linear:
+            eng.finish_direct()          # u(t_{m+1}) = u(t_m) + carries
+        states.append(eng.get(NV.PX_FIELD_UT).reshape(1, n))
+        # Burgers: this segment's dense trajectory is overwritten by the next one
+
+    # ---- phase 2: backward sweep with recompute ----------------------------
+    grad = np.zeros((1, system.basis.K))
+    integral = np.zeros((1, n))
+    qdag = None
+    cost = None
+    uT = None
+    adj_states: list[np.ndarray] = []
+    seg_grads: list[np.ndarray] = []
+    for m in range(M1 - 1, -1, -1):
+        eng.set_inputs(states[m][0], ut, ctrl)
+        last = qdag is None
+        if last or not system.is_linear:
+            # Burgers: recompute the segment's dense trajectory (the adjoint's Jᵀ(u(t)) and
+            # frozen operators need it); linear: only the last segment's u(T) is needed
+            eng.direct_partial()
+            memory.acquire(nodes_per_segment)
+        if last:   # q†(T) = u(T) − u_target, J
+            eng.finish_direct()
+            cost = eng.get(NV.PX_FIELD_J)
+            uT = eng.get(NV.PX_FIELD_UT).reshape(1, n)
+        else:
+            eng.set_adjoint_terminal(qdag)
+        eng.adjoint_partial()
+        eng.finish_adjoint()
+        g = eng.get(NV.PX_FIELD_GRAD).reshape(1, system.basis.K)
+        grad += g
+        seg_grads.append(g)
+        integral += eng.get(NV.PX_FIELD_G).reshape(1, n)
+        qdag = eng.get(NV.PX_FIELD_QDAG0).reshape(1, n)
+        adj_states.append(qdag.copy())
+        if last or not system.is_linear:
+            memory.release(nodes_per_segment)
+    return CheckpointRun(
+        gradient=grad, qdag0=qdag, cost=cost, integral=integral, final_state=uT,
+        segment_bounds=bounds, checkpoint_states=states, adjoint_checkpoint_states=adj_states[::-1],
+        memory=memory, segment_grads=seg_grads[::-1],
+    )

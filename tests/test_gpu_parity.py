@@ -502,3 +502,74 @@ def test_two_rank_gloo_on_one_gpu(kind, tmp_path):
     assert rel_l2(d["G"], loop.adjoint.integral) <= 1e-10
     assert rel_l2(d["grad"], np.ravel(loop.grad)) <= 1e-8
     assert np.max(np.abs(d["J"] - np.ravel(loop.J)) / np.abs(np.ravel(loop.J))) <= 1e-10
+
+
+@pytest.mark.parametrize("M", [0, 3])
+def test_checkpointed_burgers_vs_oracle(M):
+    """Equispaced checkpointing (`checkpointing.py:119-267`) on config 3 with M
+    checkpoints and P/(M+1) slices per segment: GPU vs the oracle's segment-by-segment
+    restatement; M = 0 equals the plain loop; the resident dense trajectory is one
+    segment's."""
+    from oracle.config_mode import burgers_direct, burgers_gradient, checkpointed_gradient
+    from paper_2004_00546_b200 import RK4Config, baseline, direct_adjoint_loop
+    from paper_2004_00546_b200.checkpointing import CheckpointSchedule, run_checkpointed_loop
+    from paper_2004_00546_b200.expaction import plan_chebyshev
+    from paper_2004_00546_b200.problems import burgers_frozen_region
+    c = baseline(3)
+    u0, ut, ctrl = c.inputs()
+    N = c.P // (M + 1)
+    run = run_checkpointed_loop(c.system, ctrl, ut, CheckpointSchedule(c.spec.T, M), "hybrid", N=N,
+                                rk=RK4Config(c.dt), expaction=c.expaction, u0=u0)
+    T_seg = c.spec.T / (M + 1)
+    h = T_seg / N / c.nsteps
+    f = c.system.basis.field(np.atleast_2d(ctrl))
+    seg = lambda u_start, qd: burgers_gradient(
+        c.grid.nx, c.spec.D, c.system.basis, T_seg, N, c.nsteps, u_start, ut, ctrl,
+        lambda region, span: plan_chebyshev(region, span, c.expaction),
+        lambda ub: burgers_frozen_region(ub, c.grid, c.spec.D), qdag_T=qd)
+    fin = lambda u_start: burgers_direct(np.atleast_2d(u_start), f, c.spec.D, 2 * np.pi / c.grid.nx, h,
+                                         N * c.nsteps)[-1][0]
+    J, grad, qdag0, G, uT, states = checkpointed_gradient(seg, fin, u0, M)
+    for a, b in zip(run.checkpoint_states, states):
+        assert rel_l2(a, b) <= 1e-12
+    assert rel_l2(run.final_state, uT) <= 1e-10
+    assert rel_l2(run.qdag0, qdag0) <= 1e-10
+    assert rel_l2(run.integral, G) <= 1e-10
+    assert rel_l2(run.gradient, grad) <= 1e-8
+    assert abs(float(run.cost[0]) - float(J[0])) <= 1e-10 * abs(float(J[0]))
+    assert run.memory.peak == N * c.nsteps + 1
+    if M == 0:
+        loop = direct_adjoint_loop(c.system, ctrl, ut, "hybrid", N=c.P, rk=RK4Config(c.dt),
+                                   expaction=c.expaction, u0=u0)
+        assert np.array_equal(np.ravel(run.gradient), np.ravel(loop.grad))
+        assert np.array_equal(np.ravel(run.qdag0), np.ravel(loop.adjoint.initial_state))
+
+
+def test_checkpointed_linear_vs_oracle():
+    """Linear testbed (2D, fused march + Chebyshev march), 3 segments: GPU vs the
+    oracle's segment-by-segment restatement. (The segmented result differs from the
+    unsegmented loop at the RK4-discretisation level, ~1e-7 here, because each segment
+    absorbs its own initial state into the RK4 slice sources.)"""
+    from oracle.config_mode import checkpointed_gradient, linear_gradient
+    from paper_2004_00546_b200 import RK4Config, baseline, scaled
+    from paper_2004_00546_b200.checkpointing import CheckpointSchedule, run_checkpointed_loop
+    from paper_2004_00546_b200.expaction import plan_for
+    c = scaled(baseline(5), nx=96, P=12, steps_per_slice=8, K=16)
+    u0, ut, ctrl = c.inputs()
+    M = 2
+    N = c.P // (M + 1)
+    run = run_checkpointed_loop(c.system, ctrl, ut, CheckpointSchedule(c.spec.T, M), "linear", N=N,
+                                rk=RK4Config(c.dt), expaction=c.expaction, u0=u0)
+    T_seg = c.spec.T / (M + 1)
+    plan = plan_for(c.system.region(), T_seg / N, c.expaction)
+    seg = lambda u_start, qd: linear_gradient(c.grid.nx, c.grid.ny, c.system.A.as_tuple(), c.system.basis, T_seg,
+                                              N, c.nsteps, u_start, ut, ctrl, plan, qdag_T=qd)
+    fin = lambda u_start: seg(u_start, None).uT[0]
+    J, grad, qdag0, G, uT, states = checkpointed_gradient(seg, fin, u0, M)
+    for a, b in zip(run.checkpoint_states, states):
+        assert rel_l2(a, b) <= 1e-12
+    assert rel_l2(run.final_state, uT) <= 1e-10
+    assert rel_l2(run.qdag0, qdag0) <= 1e-10
+    assert rel_l2(run.integral, G) <= 1e-10
+    assert rel_l2(run.gradient, grad) <= 1e-8
+    assert abs(float(run.cost[0]) - float(J[0])) <= 1e-10 * abs(float(J[0]))
