@@ -278,10 +278,16 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
     a.n = (int)h->n; a.lanes_per_b = h->Pl; a.nsteps = nsteps;
     const int ppt = h->n <= 1024 ? 1 : (h->n <= 2048 ? 2 : 4);
     const int nt = (int)((h->n + ppt - 1) / ppt);
-#define PX_L1(PP)                                                   \
-  do {                                                              \
-    if (adjoint) px::k_rk4_lane1d<PP, true><<<h->L, nt, 0, s>>>(a); \
-    else px::k_rk4_lane1d<PP, false><<<h->L, nt, 0, s>>>(a);        \
+    const bool full = h->n % ppt == 0;
+#define PX_L1(PP)                                                                   \
+  do {                                                                              \
+    if (full) {                                                                     \
+      if (adjoint) px::k_rk4_lane1d<PP, true, true><<<h->L, nt, 0, s>>>(a);         \
+      else px::k_rk4_lane1d<PP, false, true><<<h->L, nt, 0, s>>>(a);                \
+    } else {                                                                        \
+      if (adjoint) px::k_rk4_lane1d<PP, true><<<h->L, nt, 0, s>>>(a);               \
+      else px::k_rk4_lane1d<PP, false><<<h->L, nt, 0, s>>>(a);                      \
+    }                                                                               \
   } while (0)
     if (ppt == 1) PX_L1(1);
     else if (ppt == 2) PX_L1(2);
@@ -713,7 +719,7 @@ px::Scan1DPlan scan_plan(const Plan& pl) {
   sp.sigma = pl.sigma;
   sp.c0 = pl.center;
   sp.d = pl.scale;
-  return sp;
+  return sp;  // f, g filled by scan1d (they need the stencil)
 }
 
 int scan1d(Handle* h, bool adjoint, const double* lanes, double* out, double* pacc, int long_slot,
@@ -723,12 +729,21 @@ int scan1d(Handle* h, bool adjoint, const double* lanes, double* out, double* pa
   a.out = out;
   a.pacc = pacc;
   a.st = adjoint ? h->AT : h->A;
+  auto prescale = [&](px::Scan1DPlan& sp) {
+    const double taps[3] = {a.st.cc - sp.c0, a.st.ce, a.st.cw};
+    for (int q = 0; q < 3; ++q) {
+      sp.f[q] = sp.d != 0.0 ? taps[q] / sp.d : 0.0;
+      sp.g[q] = sp.d != 0.0 ? (2.0 / sp.d) * taps[q] : 0.0;
+    }
+  };
   a.slice = scan_plan(h->plans[PX_PLAN_SLICE]);
+  prescale(a.slice);
   a.use_long = long_slot >= 0 ? 1 : 0;
   if (long_slot >= 0) {
     if (!h->plans[long_slot].set || h->plans[long_slot].krylov)
       return fail(h, PX_ERR_STATE, "long-span Chebyshev plan not set");
     a.lng = scan_plan(h->plans[long_slot]);
+    prescale(a.lng);
   }
   a.adjoint = adjoint ? 1 : 0;
   a.n = (int)h->n;
@@ -736,12 +751,19 @@ int scan1d(Handle* h, bool adjoint, const double* lanes, double* out, double* pa
   if (h->Pl > 1 && !h->plans[PX_PLAN_SLICE].set) return fail(h, PX_ERR_STATE, "slice plan not set");
   const int ppt = h->n <= 512 ? 1 : (h->n <= 1024 ? 2 : (h->n <= 2048 ? 4 : 8));
   const int nt = (int)((h->n + ppt - 1) / ppt);
+  const bool full = h->n % ppt == 0;
+#define PX_S1(PP)                                              \
+  do {                                                         \
+    if (full) px::k_scan1d<PP, true><<<h->B, nt, 0, s>>>(a);   \
+    else px::k_scan1d<PP, false><<<h->B, nt, 0, s>>>(a);       \
+  } while (0)
   switch (ppt) {
-    case 1: px::k_scan1d<1><<<h->B, nt, 0, s>>>(a); break;
-    case 2: px::k_scan1d<2><<<h->B, nt, 0, s>>>(a); break;
-    case 4: px::k_scan1d<4><<<h->B, nt, 0, s>>>(a); break;
-    default: px::k_scan1d<8><<<h->B, nt, 0, s>>>(a); break;
+    case 1: PX_S1(1); break;
+    case 2: PX_S1(2); break;
+    case 4: PX_S1(4); break;
+    default: PX_S1(8); break;
   }
+#undef PX_S1
   PX_CHECK_LAUNCH(h);
   uint64_t terms = (uint64_t)(h->Pl - 1) * h->plans[PX_PLAN_SLICE].substeps * h->plans[PX_PLAN_SLICE].degree;
   if (long_slot >= 0) terms += (uint64_t)h->plans[long_slot].substeps * h->plans[long_slot].degree;

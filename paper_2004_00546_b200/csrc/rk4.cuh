@@ -253,7 +253,7 @@ struct Lane1DArgs {
   int n, lanes_per_b, nsteps;
 };
 
-template <int PPT, bool ADJ>
+template <int PPT, bool ADJ, bool FULL = false>
 __global__ void __launch_bounds__(1024) k_rk4_lane1d(Lane1DArgs a) {
   __shared__ double eL[2][1024];
   __shared__ double eR[2][1024];
@@ -284,8 +284,16 @@ __global__ void __launch_bounds__(1024) k_rk4_lane1d(Lane1DArgs a) {
 #pragma unroll
     for (int stage = 0; stage < 4; ++stage) {
       if (t <= last) {
+        // FULL (n a multiple of PPT): static last index; a run-time index would demote w
+        // to local memory
+        double wlast = w[PPT - 1];
+        if (!FULL) {
+#pragma unroll
+          for (int k = 0; k < PPT; ++k)
+            if (k == cnt - 1) wlast = w[k];
+        }
         eL[par][t] = w[0];
-        eR[par][t] = w[cnt > 0 ? cnt - 1 : 0];
+        eR[par][t] = wlast;
       }
       __syncthreads();
       const double left = eR[par][tl], right = eL[par][tr];
@@ -294,7 +302,7 @@ __global__ void __launch_bounds__(1024) k_rk4_lane1d(Lane1DArgs a) {
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
         const double wl = (k == 0) ? left : w[k - 1];
-        const double wr = (k + 1 == PPT || k + 1 >= cnt) ? right : w[k + 1];
+        const double wr = (k + 1 == PPT || (!FULL && k + 1 >= cnt)) ? right : w[k + 1];
         double v = st.cc * w[k];
         v += st.ce * wr;
         v += st.cw * wl;

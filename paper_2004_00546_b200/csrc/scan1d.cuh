@@ -22,6 +22,8 @@ struct Scan1DPlan {
   const double* bp;  // degree+1 (device), may be null
   int degree, substeps, sigma;
   double c0, d;
+  double f[3];  // (cc − c0, ce, cw)/d      : U_1 = f·(u, e, w)
+  double g[3];  // (2/d)(cc − c0, ce, cw)   : U_{j+1} = g·(U_j, e, w) + σ U_{j−1}
 };
 
 struct Scan1DArgs {
@@ -35,7 +37,7 @@ struct Scan1DArgs {
   int n, Pl;
 };
 
-template <int PPT>
+template <int PPT, bool FULL>
 __global__ void __launch_bounds__(512) k_scan1d(Scan1DArgs a) {
   __shared__ double eL[2][512];
   __shared__ double eR[2][512];
@@ -58,49 +60,79 @@ __global__ void __launch_bounds__(512) k_scan1d(Scan1DArgs a) {
     G[k] = (phi && k < cnt) ? a.pacc[(size_t)b * n + start + k] : 0.0;
   }
   int par = 0;
-  // (M u − c0 u) over the run, with the neighbours' edge values
-  auto shifted = [&](const double* u, double c0, double* out) {
+  // publish the run's edge values of u and return the neighbours' (left, right)
+  auto exchange = [&](double first, double lastv, double& left, double& right) {
     if (t <= last) {
-      eL[par][t] = u[0];
-      eR[par][t] = u[cnt > 0 ? cnt - 1 : 0];
+      eL[par][t] = first;
+      eR[par][t] = lastv;
     }
     __syncthreads();
-    const double left = eR[par][tl], right = eL[par][tr];
+    left = eR[par][tl];
+    right = eL[par][tr];
     par ^= 1;
-#pragma unroll
-    for (int k = 0; k < PPT; ++k) {
-      const double wl = (k == 0) ? left : u[k - 1];
-      const double wr = (k + 1 == PPT || k + 1 >= cnt) ? right : u[k + 1];
-      double v = st.cc * u[k];
-      v += st.ce * wr;
-      v += st.cw * wl;
-      out[k] = v - c0 * u[k];
-    }
   };
+  // Chebyshev terms with pre-scaled coefficients, every array indexed at compile time
+  // (no pointers to register arrays, so nothing is demoted to local memory):
+  //   U_1 = f·(u, e, w);  U_{j+1} = g·(U_j, e, w) + σ U_{j−1}
+  // last valid element of a run: selects over compile-time indices (an indexed read would
+  // demote the register array to local memory)
+// FULL (n a multiple of PPT): every run has PPT points and the last index is static.
+#define PX_RUN_LAST(arr, out)                                                                      \
+  do {                                                                                             \
+    if (FULL) {                                                                                    \
+      out = arr[PPT - 1];                                                                          \
+    } else {                                                                                       \
+      out = arr[0];                                                                                \
+      _Pragma("unroll") for (int kk = 1; kk < PPT; ++kk) out = (kk == cnt - 1) ? arr[kk] : out;    \
+    }                                                                                              \
+  } while (0)
   auto action = [&](const Scan1DPlan& pl) {
-    for (int sub = 0; sub < pl.substeps; ++sub) {
-      double up[PPT], uc[PPT], un[PPT], acc[PPT], pc[PPT];
-      const double b0 = __ldg(pl.be), b1 = __ldg(pl.be + 1);
-      const double p0 = phi ? __ldg(pl.bp) : 0.0, p1 = phi ? __ldg(pl.bp + 1) : 0.0;
-      shifted(C, pl.c0, un);
+    const double f0 = pl.f[0], f1 = pl.f[1], f2 = pl.f[2];
+    const double g0 = pl.g[0], g1 = pl.g[1], g2 = pl.g[2];
+    const double sg = (double)pl.sigma;
+    const double* __restrict__ be = pl.be;   // plan fields hoisted out of the term loop
+    const double* __restrict__ bp = pl.bp;
+    const int degree = pl.degree, substeps = pl.substeps;
+    for (int sub = 0; sub < substeps; ++sub) {
+      double up[PPT], uc[PPT], acc[PPT], pc[PPT];
+      const double b0 = __ldg(be), b1 = __ldg(be + 1);
+      const double p0 = phi ? __ldg(bp) : 0.0, p1 = phi ? __ldg(bp + 1) : 0.0;
+      double left, right, lastv;
+      PX_RUN_LAST(C, lastv);
+      exchange(C[0], lastv, left, right);
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        const double wl = (k == 0) ? left : C[k - 1];
+        const double wr = (k + 1 == PPT || (!FULL && k + 1 >= cnt)) ? right : C[k + 1];
+        double v = f0 * C[k];
+        v = fma(f1, wr, v);
+        uc[k] = fma(f2, wl, v);
+      }
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
         up[k] = C[k];
-        uc[k] = un[k] / pl.d;
         acc[k] = b0 * up[k] + b1 * uc[k];
         pc[k] = p0 * up[k] + p1 * uc[k];
       }
-      const double tod = 2.0 / pl.d, sg = (double)pl.sigma;
-      for (int j = 2; j <= pl.degree; ++j) {
-        shifted(uc, pl.c0, un);
-        const double bj = __ldg(pl.be + j), pj = phi ? __ldg(pl.bp + j) : 0.0;
+      for (int j = 2; j <= degree; ++j) {
+        PX_RUN_LAST(uc, lastv);
+        exchange(uc[0], lastv, left, right);
+        const double bj = __ldg(be + j), pj = phi ? __ldg(bp + j) : 0.0;
+        double un[PPT];
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
-          const double v = tod * un[k] + sg * up[k];
+          const double wl = (k == 0) ? left : uc[k - 1];
+          const double wr = (k + 1 == PPT || (!FULL && k + 1 >= cnt)) ? right : uc[k + 1];
+          double v = fma(g0, uc[k], sg * up[k]);
+          v = fma(g1, wr, v);
+          un[k] = fma(g2, wl, v);
+        }
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
           up[k] = uc[k];
-          uc[k] = v;
-          acc[k] += bj * v;
-          pc[k] += pj * v;
+          uc[k] = un[k];
+          acc[k] += bj * un[k];
+          if (phi) pc[k] += pj * un[k];
         }
       }
 #pragma unroll
@@ -110,14 +142,20 @@ __global__ void __launch_bounds__(512) k_scan1d(Scan1DArgs a) {
       }
     }
   };
-  for (int s = 1; s < a.Pl; ++s) {
-    const int q = a.adjoint ? a.Pl - 1 - s : s;
-    action(a.slice);
+  // one call site of `action` (a second one would out-line it and demote the captured
+  // register arrays C, G to local memory): Pl−1 slice carries, then the optional long span
+  const int n_act = a.Pl - 1 + (a.use_long ? 1 : 0);
+  for (int s = 1; s <= n_act; ++s) {
+    const bool lng = s == a.Pl;
+    action(lng ? a.lng : a.slice);
+    if (!lng) {
+      const int q = a.adjoint ? a.Pl - 1 - s : s;
 #pragma unroll
-    for (int k = 0; k < PPT; ++k)
-      if (k < cnt) C[k] += lanes[(size_t)q * n + start + k];
+      for (int k = 0; k < PPT; ++k)
+        if (k < cnt) C[k] += lanes[(size_t)q * n + start + k];
+    }
   }
-  if (a.use_long) action(a.lng);
+#undef PX_RUN_LAST
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
     if (k < cnt) {

@@ -148,6 +148,10 @@ def test_non_multiple_tile_grid():
     _check(_gpu_linear(c), _oracle_linear(c))
     c1 = scaled(baseline(1), nx=1500, P=3, steps_per_slice=400)  # h·ρ ≈ 1.9 < 2.78 (RK4 stable)
     _check(_gpu_linear(c1), _oracle_linear(c1))
+    # 1D runs of 4 points per thread with a partial last run (n % 4 = 2): the non-FULL
+    # variants of the on-chip lane and scan kernels
+    c2 = scaled(baseline(2), nx=4094, P=16, steps_per_slice=500, K=8)
+    _check(_gpu_linear(c2), _oracle_linear(c2))
 
 
 def test_strip_mode_2d():
