@@ -372,6 +372,10 @@ def main():
                 "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_s * 1e3,
                 "share_of_step": ph["ms"] / sum(p["ms"] for p in phases.values()),
                 "traffic": load_traffic(dom, args.config)}
+    if roofline["frac"] > 1.0:
+        roofline["note"] = ("on-chip kernel (state resident in shared memory / registers across steps or "
+                            "terms): the per-unit HBM model of SURVEY §8(d) counts bytes this kernel never "
+                            "moves, so frac > 1; its binding resources are the fp64 pipe and barrier latency")
     phase_gbs = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
                      "GB/s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None}
                  for k, v in phases.items()}
