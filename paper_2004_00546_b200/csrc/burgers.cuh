@@ -64,9 +64,13 @@ template <int PPT>
 __global__ void __launch_bounds__(BURGERS_NT) k_burgers_direct(BurgersDirectArgs a) {
   extern __shared__ double sm[];
   const int n = a.nx;
-  double* s_u = sm;
-  double* s_a = sm + n;
-  double* s_b = sm + 2 * n;
+  // stage inputs: s0 = u, s1 = u + (h/2)k1, s2 = u + (h/2)k2, s3 = u + h·k3 (aliases s1, whose
+  // last readers, stage 2, finished before the barrier after stage 2); the new state goes back
+  // into s0 (last read in stage 1): one barrier per stage, none for a separate state copy
+  double* s0 = sm;
+  double* s1 = sm + n;
+  double* s2 = sm + 2 * n;
+  double* s3 = s1;
   const int b = blockIdx.x;
   const double inv2h = 1.0 / (2.0 * a.hx);
   const double Dih2 = a.D / (a.hx * a.hx);
@@ -83,7 +87,7 @@ __global__ void __launch_bounds__(BURGERS_NT) k_burgers_direct(BurgersDirectArgs
       for (int k = 0; k < a.K; ++k) fv += c[k] * a.tx[(size_t)a.ix[k] * n + i];
       f[t] = fv;
       u[t] = a.u0[i];
-      s_u[i] = u[t];
+      s0[i] = u[t];
       a.traj[(size_t)b * n + i] = u[t];
     }
   }
@@ -95,9 +99,9 @@ __global__ void __launch_bounds__(BURGERS_NT) k_burgers_direct(BurgersDirectArgs
     for (int t = 0; t < PPT; ++t) {
       const int i = threadIdx.x + t * BURGERS_NT;
       if (i < n) {
-        const double k = burgers_rhs_at(s_u, i, n, inv2h, Dih2, f[t]);
+        const double k = burgers_rhs_at(s0, i, n, inv2h, Dih2, f[t]);
         acc[t] = k;
-        s_a[i] = u[t] + hh * k;
+        s1[i] = u[t] + hh * k;
       }
     }
     __syncthreads();
@@ -105,9 +109,9 @@ __global__ void __launch_bounds__(BURGERS_NT) k_burgers_direct(BurgersDirectArgs
     for (int t = 0; t < PPT; ++t) {
       const int i = threadIdx.x + t * BURGERS_NT;
       if (i < n) {
-        const double k = burgers_rhs_at(s_a, i, n, inv2h, Dih2, f[t]);
+        const double k = burgers_rhs_at(s1, i, n, inv2h, Dih2, f[t]);
         acc[t] += 2.0 * k;
-        s_b[i] = u[t] + hh * k;
+        s2[i] = u[t] + hh * k;
       }
     }
     __syncthreads();
@@ -115,9 +119,9 @@ __global__ void __launch_bounds__(BURGERS_NT) k_burgers_direct(BurgersDirectArgs
     for (int t = 0; t < PPT; ++t) {
       const int i = threadIdx.x + t * BURGERS_NT;
       if (i < n) {
-        const double k = burgers_rhs_at(s_b, i, n, inv2h, Dih2, f[t]);
+        const double k = burgers_rhs_at(s2, i, n, inv2h, Dih2, f[t]);
         acc[t] += 2.0 * k;
-        s_a[i] = u[t] + h * k;
+        s3[i] = u[t] + h * k;
       }
     }
     __syncthreads();
@@ -125,16 +129,11 @@ __global__ void __launch_bounds__(BURGERS_NT) k_burgers_direct(BurgersDirectArgs
     for (int t = 0; t < PPT; ++t) {
       const int i = threadIdx.x + t * BURGERS_NT;
       if (i < n) {
-        const double k = burgers_rhs_at(s_a, i, n, inv2h, Dih2, f[t]);
+        const double k = burgers_rhs_at(s3, i, n, inv2h, Dih2, f[t]);
         u[t] = u[t] + h6 * (acc[t] + k);
+        s0[i] = u[t];
         a.traj[(st + 1) * node_stride + (size_t)b * n + i] = u[t];
       }
-    }
-    __syncthreads();  // all reads of s_a done before s_u is overwritten
-#pragma unroll
-    for (int t = 0; t < PPT; ++t) {
-      const int i = threadIdx.x + t * BURGERS_NT;
-      if (i < n) s_u[i] = u[t];
     }
     __syncthreads();
   }
@@ -142,6 +141,100 @@ __global__ void __launch_bounds__(BURGERS_NT) k_burgers_direct(BurgersDirectArgs
   for (int t = 0; t < PPT; ++t) {
     const int i = threadIdx.x + t * BURGERS_NT;
     if (i < n) a.UT[(size_t)b * n + i] = u[t];
+  }
+}
+
+// Same sweep with each thread owning a contiguous run of PPT points (n = PPT·blockDim):
+// neighbours inside the run come from registers, only the run edges go through shared
+// memory (one vector store + two scalar loads per stage), and the right-hand side is
+// rearranged to 5 flops per point: rhs = D/h²·(u₊ + u₋) + f − u·(2D/h² + (u₊ − u₋)/(2h)).
+template <int PPT>
+__global__ void __launch_bounds__(BURGERS_NT) k_burgers_direct_run(BurgersDirectArgs a) {
+  extern __shared__ double sm[];
+  const int n = a.nx;
+  const int T = n / PPT;  // threads with points (blockDim ≥ T)
+  double* sA = sm;        // [2][n]: stage inputs, double buffered
+  const int b = blockIdx.x;
+  const int t = threadIdx.x;
+  const bool act = t < T;
+  const int i0 = t * PPT;
+  const int il = (i0 == 0) ? n - 1 : i0 - 1;            // left neighbour of the run
+  const int ir = (i0 + PPT >= n) ? 0 : i0 + PPT;        // right neighbour of the run
+  const double inv2h = 1.0 / (2.0 * a.hx);
+  const double Dih2 = a.D / (a.hx * a.hx), twoD = 2.0 * Dih2;
+  const double h = a.h, hh = 0.5 * a.h, h6 = a.h / 6.0;
+  double f[PPT], u[PPT], acc[PPT], x[PPT];
+  const double* c = a.ctrl + (size_t)b * a.K;
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    f[k] = 0.0;
+    u[k] = 0.0;
+    if (act) {
+      const int i = i0 + k;
+      double fv = 0.0;
+      for (int q = 0; q < a.K; ++q) fv += c[q] * a.tx[(size_t)a.ix[q] * n + i];
+      f[k] = fv;
+      u[k] = a.u0[i];
+      a.traj[(size_t)b * n + i] = u[k];
+    }
+  }
+  const size_t S = (size_t)a.P * a.nsteps;
+  const size_t node_stride = (size_t)a.B * n;
+  int par = 0;
+  // rhs of the stage input x (run in registers, edges from the other threads via smem)
+  auto rhs = [&](double* k_out) {
+    double* sx = sA + par * n;
+    if (act) {
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) sx[i0 + k] = x[k];
+    }
+    __syncthreads();
+    const double xl = act ? sx[il] : 0.0, xr = act ? sx[ir] : 0.0;
+    par ^= 1;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      const double um = (k == 0) ? xl : x[k - 1];
+      const double up = (k + 1 == PPT) ? xr : x[k + 1];
+      const double A = up + um, B = up - um;
+      const double t1 = fma(Dih2, A, f[k]);
+      const double t2 = fma(inv2h, B, twoD);
+      k_out[k] = fma(-x[k], t2, t1);
+    }
+  };
+  double kk[PPT];
+  for (size_t st = 0; st < S; ++st) {
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) x[k] = u[k];
+    rhs(kk);
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      acc[k] = kk[k];
+      x[k] = fma(hh, kk[k], u[k]);
+    }
+    rhs(kk);
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      acc[k] = fma(2.0, kk[k], acc[k]);
+      x[k] = fma(hh, kk[k], u[k]);
+    }
+    rhs(kk);
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      acc[k] = fma(2.0, kk[k], acc[k]);
+      x[k] = fma(h, kk[k], u[k]);
+    }
+    rhs(kk);
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) u[k] = fma(h6, acc[k] + kk[k], u[k]);
+    if (act) {
+      double* node = a.traj + (st + 1) * node_stride + (size_t)b * n + i0;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) node[k] = u[k];
+    }
+  }
+  if (act) {
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) a.UT[(size_t)b * n + i0 + k] = u[k];
   }
 }
 
@@ -355,16 +448,22 @@ template <int PPT>
 __global__ void __launch_bounds__(BURGERS_NT) k_burgers_scan(BurgersAdjointArgs a, const double* coef) {
   extern __shared__ double sm[];
   const int n = a.nx;
-  double* s_u = sm;          // ū_p
-  double* s_cur = sm + n;    // U_k
+  double* s_cur = sm;  // [2][n]: U_k, double buffered (one barrier per term)
   const int b = blockIdx.x;
   const int Pl = a.p_end - a.p_begin;
   const double inv2h = 1.0 / (2.0 * a.hx);
   const double Dih2 = a.D / (a.hx * a.hx);
-  const double c0 = a.center, d = a.scale, two_over = 2.0 / a.scale, sigma = (double)a.sigma;
-  const double* be = coef;
-  const double* bp = coef + a.degree + 1;
+  const double c0 = a.center, two_over = 2.0 / a.scale, sigma = (double)a.sigma;
+  const double* __restrict__ be = coef;
+  const double* __restrict__ bp = coef + a.degree + 1;
+  const int degree = a.degree, substeps = a.substeps;
   double C[PPT], Gp[PPT], prev[PPT], cur[PPT], acc[PPT], pac[PPT];
+  // per point, per slice: J(ū)ᵀy = kp·y₊ + km·y₋ + kc·y with kp = ū₊/(2h) + D/h²,
+  // km = −ū₋/(2h) + D/h², kc = −(ū₊ − ū₋)/(2h) − 2D/h² (problems.py:316-343), folded with the
+  // Chebyshev shift/scale: first term f·(y₊, y₋, y), later terms g·(y₊, y₋, y) + σ·U_{k−1}
+  double gp[PPT], gm[PPT], gc[PPT];  // the first term uses f = g/2
+  auto ipx = [&](int t) { const int i = threadIdx.x + t * BURGERS_NT; return (i + 1 >= n) ? 0 : i + 1; };
+  auto imx = [&](int t) { const int i = threadIdx.x + t * BURGERS_NT; return (i == 0) ? n - 1 : i - 1; };
 #pragma unroll
   for (int t = 0; t < PPT; ++t) {
     const int i = threadIdx.x + t * BURGERS_NT;
@@ -374,55 +473,65 @@ __global__ void __launch_bounds__(BURGERS_NT) k_burgers_scan(BurgersAdjointArgs 
       Gp[t] = a.G[(size_t)b * n + i];
     }
   }
+  int par = 0;
   for (int p = a.p_end - 2; p >= 0; --p) {
     const bool own = p >= a.p_begin;
     const double* ub = a.ubar + ((size_t)p * a.B + b) * n;
 #pragma unroll
     for (int t = 0; t < PPT; ++t) {
       const int i = threadIdx.x + t * BURGERS_NT;
-      if (i < n) s_u[i] = ub[i];
+      const double up = (i < n) ? ub[ipx(t)] : 0.0, um = (i < n) ? ub[imx(t)] : 0.0;
+      const double kp = up * inv2h + Dih2, km = Dih2 - um * inv2h, kc = -(up - um) * inv2h - 2.0 * Dih2;
+      gp[t] = two_over * kp;
+      gm[t] = two_over * km;
+      gc[t] = two_over * (kc - c0);
     }
-    for (int sub = 0; sub < a.substeps; ++sub) {
-      // k = 0, 1
+    for (int sub = 0; sub < substeps; ++sub) {
 #pragma unroll
       for (int t = 0; t < PPT; ++t) {
         const int i = threadIdx.x + t * BURGERS_NT;
-        if (i < n) s_cur[i] = C[t];
+        if (i < n) s_cur[par * n + i] = C[t];
       }
       __syncthreads();
+      {
+        const double b0 = __ldg(be), b1 = __ldg(be + 1), p0 = __ldg(bp), p1 = __ldg(bp + 1);
+        const double* sc = s_cur + par * n;
 #pragma unroll
-      for (int t = 0; t < PPT; ++t) {
-        const int i = threadIdx.x + t * BURGERS_NT;
-        if (i < n) {
+        for (int t = 0; t < PPT; ++t) {
+          if (threadIdx.x + t * BURGERS_NT >= n) continue;  // inactive point (n % BURGERS_NT ≠ 0)
           const double u0 = C[t];
-          const double u1 = (jt_at(s_u, s_cur, i, n, inv2h, Dih2) - c0 * u0) / d;
+          double u1 = gc[t] * u0;
+          u1 = fma(gp[t], sc[ipx(t)], u1);
+          u1 = 0.5 * fma(gm[t], sc[imx(t)], u1);
           prev[t] = u0;
           cur[t] = u1;
-          acc[t] = be[0] * u0 + be[1] * u1;
-          pac[t] = bp[0] * u0 + bp[1] * u1;
+          acc[t] = b0 * u0 + b1 * u1;
+          pac[t] = p0 * u0 + p1 * u1;
         }
       }
-      for (int k = 2; k <= a.degree; ++k) {
-        __syncthreads();
+      par ^= 1;
+      for (int k = 2; k <= degree; ++k) {
 #pragma unroll
         for (int t = 0; t < PPT; ++t) {
           const int i = threadIdx.x + t * BURGERS_NT;
-          if (i < n) s_cur[i] = cur[t];
+          if (i < n) s_cur[par * n + i] = cur[t];
         }
         __syncthreads();
+        const double bk = __ldg(be + k), pk = __ldg(bp + k);
+        const double* sc = s_cur + par * n;
 #pragma unroll
         for (int t = 0; t < PPT; ++t) {
-          const int i = threadIdx.x + t * BURGERS_NT;
-          if (i < n) {
-            const double un = two_over * (jt_at(s_u, s_cur, i, n, inv2h, Dih2) - c0 * cur[t]) + sigma * prev[t];
-            prev[t] = cur[t];
-            cur[t] = un;
-            acc[t] += be[k] * un;
-            pac[t] += bp[k] * un;
-          }
+          if (threadIdx.x + t * BURGERS_NT >= n) continue;
+          double un = fma(gc[t], cur[t], sigma * prev[t]);
+          un = fma(gp[t], sc[ipx(t)], un);
+          un = fma(gm[t], sc[imx(t)], un);
+          prev[t] = cur[t];
+          cur[t] = un;
+          acc[t] = fma(bk, un, acc[t]);
+          pac[t] = fma(pk, un, pac[t]);
         }
+        par ^= 1;
       }
-      __syncthreads();
 #pragma unroll
       for (int t = 0; t < PPT; ++t) {
         C[t] = acc[t];
@@ -456,11 +565,28 @@ inline int burgers_direct(const BurgersDirectArgs& a, cudaStream_t s, px_stats* 
     cudaFuncSetAttribute(k_burgers_direct<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     k_burgers_direct<PP><<<a.B, BURGERS_NT, smem, s>>>(a);                                     \
   } while (0)
-  if (ppt <= 1) PX_BD(1);
+#define PX_BR(PP)                                                                              \
+  do {                                                                                         \
+    const size_t sm2 = 2 * (size_t)a.nx * sizeof(double);                                     \
+    cudaFuncSetAttribute(k_burgers_direct_run<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2); \
+    k_burgers_direct_run<PP><<<a.B, ((a.nx / PP + 31) / 32) * 32, sm2, s>>>(a);                \
+  } while (0)
+  // contiguous runs when n is a multiple of the run length (the strided kernel otherwise)
+  static const int rp_env = [] { const char* e = getenv("PX_BURGERS_RUN"); return e ? atoi(e) : 0; }();
+  int rp = ppt <= 1 ? 1 : (ppt <= 2 ? 2 : (ppt <= 4 ? 4 : 8));
+  if (rp_env == 1 || rp_env == 2 || rp_env == 4 || rp_env == 8) rp = std::max(rp, rp_env);
+  static const bool strided = [] { const char* e = getenv("PX_BURGERS_STRIDED"); return e && atoi(e) != 0; }();
+  if (!strided && a.nx % rp == 0) {
+    if (rp == 1) PX_BR(1);
+    else if (rp == 2) PX_BR(2);
+    else if (rp == 4) PX_BR(4);
+    else PX_BR(8);
+  } else if (ppt <= 1) PX_BD(1);
   else if (ppt <= 2) PX_BD(2);
   else if (ppt <= 4) PX_BD(4);
   else PX_BD(8);
 #undef PX_BD
+#undef PX_BR
   const size_t total = (size_t)a.P * a.B * a.nx;
   k_slice_means<<<(unsigned)std::min<size_t>((total + 255) / 256, 4096), 256, 0, s>>>(a.ubar, a.traj, a.P,
                                                                                        a.nsteps, a.B, a.nx);
