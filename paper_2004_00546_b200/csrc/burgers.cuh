@@ -556,6 +556,115 @@ __global__ void __launch_bounds__(BURGERS_NT) k_burgers_scan(BurgersAdjointArgs 
   }
 }
 
+// The frozen-operator carry with contiguous runs of PPT points per thread (n = PPT·T):
+// run-interior neighbours from registers, only the two run edges through shared memory.
+template <int PPT>
+__global__ void __launch_bounds__(BURGERS_NT) k_burgers_scan_run(BurgersAdjointArgs a, const double* coef) {
+  extern __shared__ double sm[];
+  const int n = a.nx;
+  const int T = n / PPT;
+  double* sE = sm;  // [2][2][T]: (first, last) run values, double buffered
+  const int b = blockIdx.x;
+  const int t = threadIdx.x;
+  const bool act = t < T;
+  const int i0 = t * PPT;
+  const int tl = (t == 0) ? T - 1 : t - 1, tr = (t + 1 >= T) ? 0 : t + 1;
+  const int Pl = a.p_end - a.p_begin;
+  const double inv2h = 1.0 / (2.0 * a.hx);
+  const double Dih2 = a.D / (a.hx * a.hx);
+  const double c0 = a.center, two_over = 2.0 / a.scale, sigma = (double)a.sigma;
+  const double* __restrict__ be = coef;
+  const double* __restrict__ bp = coef + a.degree + 1;
+  const int degree = a.degree, substeps = a.substeps;
+  double C[PPT], Gp[PPT], prev[PPT], cur[PPT], acc[PPT], pac[PPT], gp[PPT], gm[PPT], gc[PPT];
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    C[k] = act ? a.W0[((size_t)b * Pl + (Pl - 1)) * n + i0 + k] : 0.0;
+    Gp[k] = act ? a.G[(size_t)b * n + i0 + k] : 0.0;
+  }
+  int par = 0;
+  // (left, right) neighbours of the run of v
+  auto edges = [&](const double* v, double& l, double& r) {
+    if (act) {
+      sE[(par * 2 + 0) * T + t] = v[0];
+      sE[(par * 2 + 1) * T + t] = v[PPT - 1];
+    }
+    __syncthreads();
+    l = act ? sE[(par * 2 + 1) * T + tl] : 0.0;
+    r = act ? sE[(par * 2 + 0) * T + tr] : 0.0;
+    par ^= 1;
+  };
+  for (int p = a.p_end - 2; p >= 0; --p) {
+    const bool own = p >= a.p_begin;
+    const double* ub = a.ubar + ((size_t)p * a.B + b) * n;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      const int i = i0 + k;
+      const int ip = (i + 1 >= n) ? 0 : i + 1, im = (i == 0) ? n - 1 : i - 1;
+      const double up = act ? ub[ip] : 0.0, um = act ? ub[im] : 0.0;
+      const double kp = up * inv2h + Dih2, km = Dih2 - um * inv2h, kc = -(up - um) * inv2h - 2.0 * Dih2;
+      gp[k] = two_over * kp;
+      gm[k] = two_over * km;
+      gc[k] = two_over * (kc - c0);
+    }
+    for (int sub = 0; sub < substeps; ++sub) {
+      double l, r;
+      edges(C, l, r);
+      {
+        const double b0 = __ldg(be), b1 = __ldg(be + 1), p0 = __ldg(bp), p1 = __ldg(bp + 1);
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          const double yp = (k + 1 == PPT) ? r : C[k + 1];
+          const double ym = (k == 0) ? l : C[k - 1];
+          double u1 = gc[k] * C[k];
+          u1 = fma(gp[k], yp, u1);
+          u1 = 0.5 * fma(gm[k], ym, u1);
+          prev[k] = C[k];
+          cur[k] = u1;
+          acc[k] = b0 * C[k] + b1 * u1;
+          pac[k] = p0 * C[k] + p1 * u1;
+        }
+      }
+      for (int j = 2; j <= degree; ++j) {
+        edges(cur, l, r);
+        const double bk = __ldg(be + j), pk = __ldg(bp + j);
+        double un[PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          const double yp = (k + 1 == PPT) ? r : cur[k + 1];
+          const double ym = (k == 0) ? l : cur[k - 1];
+          double v = fma(gc[k], cur[k], sigma * prev[k]);
+          v = fma(gp[k], yp, v);
+          un[k] = fma(gm[k], ym, v);
+        }
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          prev[k] = cur[k];
+          cur[k] = un[k];
+          acc[k] = fma(bk, un[k], acc[k]);
+          pac[k] = fma(pk, un[k], pac[k]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        C[k] = acc[k];
+        Gp[k] += pac[k];
+      }
+    }
+    if (own && act) {
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) C[k] += a.W0[((size_t)b * Pl + (p - a.p_begin)) * n + i0 + k];
+    }
+  }
+  if (act) {
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      a.QDAG0[(size_t)b * n + i0 + k] = C[k];
+      a.G[(size_t)b * n + i0 + k] = Gp[k];
+    }
+  }
+}
+
 inline int burgers_direct(const BurgersDirectArgs& a, cudaStream_t s, px_stats* stats) {
   if (a.nx > BURGERS_MAX_N) return PX_ERR_ARG;
   const size_t smem = 3 * (size_t)a.nx * sizeof(double);
@@ -633,11 +742,25 @@ inline int burgers_adjoint(const BurgersAdjointArgs& a, cudaStream_t s, px_stats
     cudaFuncSetAttribute(k_burgers_scan<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sc); \
     k_burgers_scan<PP><<<a.B, BURGERS_NT, smem_sc, s>>>(a, coef);                               \
   } while (0)
-  if (ppt <= 1) PX_BS(1);
+#define PX_BSR(PP)                                                                                   \
+  do {                                                                                             \
+    const size_t sm2 = 4 * (size_t)(a.nx / PP) * sizeof(double);                                   \
+    cudaFuncSetAttribute(k_burgers_scan_run<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2); \
+    k_burgers_scan_run<PP><<<a.B, ((a.nx / PP + 31) / 32) * 32, sm2, s>>>(a, coef);                \
+  } while (0)
+  static const bool strided_sc = [] { const char* e = getenv("PX_BURGERS_STRIDED"); return e && atoi(e) != 0; }();
+  const int rps = ppt <= 1 ? 1 : (ppt <= 2 ? 2 : (ppt <= 4 ? 4 : 8));
+  if (!strided_sc && a.nx % rps == 0) {
+    if (rps == 1) PX_BSR(1);
+    else if (rps == 2) PX_BSR(2);
+    else if (rps == 4) PX_BSR(4);
+    else PX_BSR(8);
+  } else if (ppt <= 1) PX_BS(1);
   else if (ppt <= 2) PX_BS(2);
   else if (ppt <= 4) PX_BS(4);
   else PX_BS(8);
 #undef PX_BS
+#undef PX_BSR
   if (cudaGetLastError() != cudaSuccess) return PX_ERR_CUDA;
   *wend = a.W0;
   if (stats) {
