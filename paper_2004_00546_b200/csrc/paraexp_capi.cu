@@ -751,6 +751,27 @@ int scan1d(Handle* h, bool adjoint, const double* lanes, double* out, double* pa
   if (h->Pl > 1 && !h->plans[PX_PLAN_SLICE].set) return fail(h, PX_ERR_STATE, "slice plan not set");
   const int ppt = h->n <= 512 ? 1 : (h->n <= 1024 ? 2 : (h->n <= 2048 ? 4 : 8));
   const int nt = (int)((h->n + ppt - 1) / ppt);
+  // cluster version (8 CTAs = 8 SMs per member, DSMEM ghost-zone refresh every 8 terms)
+  // for the larger 1D grids; one CTA per member otherwise
+  static const int s1c = [] { const char* e = getenv("PX_SCAN1D_CLUSTER"); return e ? atoi(e) : 1; }();
+  constexpr int kCS = 8, kPPT = 4, kG = 8;
+  const int Wc = (int)(h->n / kCS);
+  if (s1c && h->n >= 2048 && h->n % (kCS * kPPT) == 0 && Wc >= kG && Wc / kPPT + 2 * (kG / kPPT) <= 256) {
+    const int nr = Wc / kPPT + 2 * (kG / kPPT);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(h->B * kCS));
+    cfg.blockDim = dim3((unsigned)(((nr + 31) / 32) * 32));
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kCS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, kG>, a));
+  } else {
   const bool full = h->n % ppt == 0;
 #define PX_S1(PP)                                              \
   do {                                                         \
@@ -764,6 +785,7 @@ int scan1d(Handle* h, bool adjoint, const double* lanes, double* out, double* pa
     default: PX_S1(8); break;
   }
 #undef PX_S1
+  }
   PX_CHECK_LAUNCH(h);
   uint64_t terms = (uint64_t)(h->Pl - 1) * h->plans[PX_PLAN_SLICE].substeps * h->plans[PX_PLAN_SLICE].degree;
   if (long_slot >= 0) terms += (uint64_t)h->plans[long_slot].substeps * h->plans[long_slot].degree;

@@ -13,6 +13,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
 
 namespace px {
@@ -163,6 +165,179 @@ __global__ void __launch_bounds__(512) k_scan1d(Scan1DArgs a) {
       if (phi) a.pacc[(size_t)b * n + start + k] = G[k];
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Thread-block-cluster version: one member's carry recursion spread over the CS CTAs
+// of a cluster (CS SMs instead of one). CTA r owns W = n/CS points and also computes a
+// ghost zone of G points on each side (redundantly), so the Chebyshev terms run with
+// CTA-local barriers only; every G terms (and at the start of every action) the ghost
+// zones are refreshed from the neighbouring CTAs' shared memory (DSMEM) after one
+// cluster barrier. Exchange buffers are double buffered, so one cluster barrier per
+// refresh suffices. Same arithmetic per point as k_scan1d (pre-scaled terms).
+// ---------------------------------------------------------------------------
+template <int PPT, int CS, int G>
+__global__ void __launch_bounds__(256) k_scan1d_cluster(Scan1DArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  static_assert(G % PPT == 0, "ghost width must be whole runs");
+  constexpr int GR = G / PPT;            // ghost runs per side
+  __shared__ double eL[2][256];
+  __shared__ double eR[2][256];
+  __shared__ double xbuf[2][2][2][G];    // [parity][side 0 = my left edge, 1 = right][cur/prev][G]
+  const int n = a.n;
+  const int W = n / CS;                  // owned points
+  const int rank = (int)cluster.block_rank();
+  const int b = blockIdx.x / CS;
+  const int t = threadIdx.x;
+  const int NR = W / PPT + 2 * GR;       // runs in the local domain (threads with points)
+  const bool act = t < NR;
+  // local run t covers global points g0 + k, g0 = rank·W − G + t·PPT (mod n)
+  const int g0 = rank * W - G + t * PPT;
+  const bool owned = act && t >= GR && t < NR - GR;
+  const int tl = (t == 0) ? 0 : t - 1, tr = (t + 1 >= NR) ? NR - 1 : t + 1;  // domain ends: clamped
+  const bool phi = a.adjoint && a.pacc != nullptr;
+  const double* lanes = a.lanes + (size_t)b * a.Pl * n;
+  auto gidx = [&](int k) { int g = g0 + k; g %= n; return g < 0 ? g + n : g; };
+  double C[PPT], G_[PPT];
+  const int q0 = a.adjoint ? a.Pl - 1 : 0;
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    C[k] = act ? lanes[(size_t)q0 * n + gidx(k)] : 0.0;
+    G_[k] = (phi && owned) ? a.pacc[(size_t)b * n + gidx(k)] : 0.0;
+  }
+  int par = 0, xpar = 0;
+  auto exchange = [&](double first, double lastv, double& left, double& right) {
+    if (act) {
+      eL[par][t] = first;
+      eR[par][t] = lastv;
+    }
+    __syncthreads();
+    left = eR[par][tl];
+    right = eL[par][tr];
+    par ^= 1;
+  };
+  // refresh the ghost runs of u (and v, when given) from the neighbouring CTAs
+  auto refresh = [&](double* u, double* v) {
+    // publish my owned edge runs: left edge = local runs GR … 2GR−1, right = NR−2GR … NR−GR−1
+    if (act) {
+      if (t >= GR && t < 2 * GR) {
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          xbuf[xpar][0][0][(t - GR) * PPT + k] = u[k];
+          if (v) xbuf[xpar][0][1][(t - GR) * PPT + k] = v[k];
+        }
+      }
+      if (t >= NR - 2 * GR && t < NR - GR) {
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          xbuf[xpar][1][0][(t - (NR - 2 * GR)) * PPT + k] = u[k];
+          if (v) xbuf[xpar][1][1][(t - (NR - 2 * GR)) * PPT + k] = v[k];
+        }
+      }
+    }
+    cluster.sync();
+    // my left ghosts = left neighbour's right edge; my right ghosts = right neighbour's left edge
+    if (act && t < GR) {
+      const double* src = cluster.map_shared_rank(&xbuf[xpar][1][0][0], (unsigned)((rank + CS - 1) % CS));
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        u[k] = src[t * PPT + k];
+        if (v) v[k] = src[G + t * PPT + k];
+      }
+    }
+    if (act && t >= NR - GR) {
+      const double* src = cluster.map_shared_rank(&xbuf[xpar][0][0][0], (unsigned)((rank + 1) % CS));
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        u[k] = src[(t - (NR - GR)) * PPT + k];
+        if (v) v[k] = src[G + (t - (NR - GR)) * PPT + k];
+      }
+    }
+    xpar ^= 1;
+  };
+  auto action = [&](const Scan1DPlan& pl) {
+    const double f0 = pl.f[0], f1 = pl.f[1], f2 = pl.f[2];
+    const double g0c = pl.g[0], g1 = pl.g[1], g2 = pl.g[2];
+    const double sg = (double)pl.sigma;
+    const double* __restrict__ be = pl.be;
+    const double* __restrict__ bp = pl.bp;
+    const int degree = pl.degree, substeps = pl.substeps;
+    for (int sub = 0; sub < substeps; ++sub) {
+      double up[PPT], uc[PPT], acc[PPT], pc[PPT];
+      refresh(C, nullptr);
+      int valid = G;  // ghost depth still exact
+      const double b0 = __ldg(be), b1 = __ldg(be + 1);
+      const double p0 = phi ? __ldg(bp) : 0.0, p1 = phi ? __ldg(bp + 1) : 0.0;
+      double left, right;
+      exchange(C[0], C[PPT - 1], left, right);
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        const double wl = (k == 0) ? left : C[k - 1];
+        const double wr = (k + 1 == PPT) ? right : C[k + 1];
+        double v = f0 * C[k];
+        v = fma(f1, wr, v);
+        uc[k] = fma(f2, wl, v);
+      }
+      --valid;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        up[k] = C[k];
+        acc[k] = b0 * up[k] + b1 * uc[k];
+        pc[k] = p0 * up[k] + p1 * uc[k];
+      }
+      for (int j = 2; j <= degree; ++j) {
+        if (valid == 0) {
+          refresh(uc, up);
+          valid = G;
+        }
+        exchange(uc[0], uc[PPT - 1], left, right);
+        const double bj = __ldg(be + j), pj = phi ? __ldg(bp + j) : 0.0;
+        double un[PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          const double wl = (k == 0) ? left : uc[k - 1];
+          const double wr = (k + 1 == PPT) ? right : uc[k + 1];
+          double v = fma(g0c, uc[k], sg * up[k]);
+          v = fma(g1, wr, v);
+          un[k] = fma(g2, wl, v);
+        }
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          up[k] = uc[k];
+          uc[k] = un[k];
+          acc[k] += bj * un[k];
+          if (phi) pc[k] += pj * un[k];
+        }
+        --valid;
+      }
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        C[k] = acc[k];
+        G_[k] += pc[k];
+      }
+    }
+  };
+  const int n_act = a.Pl - 1 + (a.use_long ? 1 : 0);
+  for (int s = 1; s <= n_act; ++s) {
+    const bool lng = s == a.Pl;
+    action(lng ? a.lng : a.slice);
+    if (!lng) {
+      const int q = a.adjoint ? a.Pl - 1 - s : s;
+      if (act) {
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) C[k] += lanes[(size_t)q * n + gidx(k)];
+      }
+    }
+  }
+  if (owned) {
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      a.out[(size_t)b * n + gidx(k)] = C[k];
+      if (phi) a.pacc[(size_t)b * n + gidx(k)] = G_[k];
+    }
+  }
+  cluster.sync();  // no CTA leaves while a neighbour may still read its exchange buffers
 }
 
 }  // namespace px
