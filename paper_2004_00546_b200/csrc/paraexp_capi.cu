@@ -759,7 +759,9 @@ int scan1d(Handle* h, bool adjoint, const double* lanes, double* out, double* pa
   if (s1c && h->n >= 2048 && h->n % (kCS * kPPT) == 0 && Wc >= kG && Wc / kPPT + 2 * (kG / kPPT) <= 256) {
     const int nr = Wc / kPPT + 2 * (kG / kPPT);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(h->B * kCS));
+    static const int kmb = [] { const char* e = getenv("PX_SCAN1D_MB"); return e ? atoi(e) : 2; }();
+    const int mb = kmb >= 4 ? 4 : (kmb >= 2 ? 2 : 1);
+    cfg.gridDim = dim3((unsigned)(((h->B + mb - 1) / mb) * kCS));
     cfg.blockDim = dim3((unsigned)(((nr + 31) / 32) * 32));
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
@@ -770,7 +772,10 @@ int scan1d(Handle* h, bool adjoint, const double* lanes, double* out, double* pa
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, kG>, a));
+    const int Bm = h->B;
+    if (mb == 4) PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, kG, 4>, a, Bm));
+    else if (mb == 2) PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, kG, 2>, a, Bm));
+    else PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, kG, 1>, a, Bm));
   } else {
   const bool full = h->n % ppt == 0;
 #define PX_S1(PP)                                              \

@@ -176,19 +176,21 @@ __global__ void __launch_bounds__(512) k_scan1d(Scan1DArgs a) {
 // cluster barrier. Exchange buffers are double buffered, so one cluster barrier per
 // refresh suffices. Same arithmetic per point as k_scan1d (pre-scaled terms).
 // ---------------------------------------------------------------------------
-template <int PPT, int CS, int G>
-__global__ void __launch_bounds__(256) k_scan1d_cluster(Scan1DArgs a) {
+template <int PPT, int CS, int G, int MB>
+__global__ void __launch_bounds__(256) k_scan1d_cluster(Scan1DArgs a, int B) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   static_assert(G % PPT == 0, "ghost width must be whole runs");
   constexpr int GR = G / PPT;            // ghost runs per side
-  __shared__ double eL[2][256];
-  __shared__ double eR[2][256];
-  __shared__ double xbuf[2][2][2][G];    // [parity][side 0 = my left edge, 1 = right][cur/prev][G]
+  // MB members per CTA: their recurrences are independent, so interleaving them hides the
+  // per-term latency chain (edge store → barrier → neighbour load → 3 FMAs) MB-fold
+  __shared__ double eL[2][MB][256];
+  __shared__ double eR[2][MB][256];
+  __shared__ double xbuf[2][2][2][MB][G];  // [parity][side 0 = my left edge, 1 = right][cur/prev][member][G]
   const int n = a.n;
   const int W = n / CS;                  // owned points
   const int rank = (int)cluster.block_rank();
-  const int b = blockIdx.x / CS;
+  const int bb = (blockIdx.x / CS) * MB; // first member of this CTA
   const int t = threadIdx.x;
   const int NR = W / PPT + 2 * GR;       // runs in the local domain (threads with points)
   const bool act = t < NR;
@@ -197,62 +199,80 @@ __global__ void __launch_bounds__(256) k_scan1d_cluster(Scan1DArgs a) {
   const bool owned = act && t >= GR && t < NR - GR;
   const int tl = (t == 0) ? 0 : t - 1, tr = (t + 1 >= NR) ? NR - 1 : t + 1;  // domain ends: clamped
   const bool phi = a.adjoint && a.pacc != nullptr;
-  const double* lanes = a.lanes + (size_t)b * a.Pl * n;
   auto gidx = [&](int k) { int g = g0 + k; g %= n; return g < 0 ? g + n : g; };
-  double C[PPT], G_[PPT];
+  auto mact = [&](int m) { return bb + m < B; };
+  double C[MB][PPT], G_[MB][PPT];
   const int q0 = a.adjoint ? a.Pl - 1 : 0;
 #pragma unroll
-  for (int k = 0; k < PPT; ++k) {
-    C[k] = act ? lanes[(size_t)q0 * n + gidx(k)] : 0.0;
-    G_[k] = (phi && owned) ? a.pacc[(size_t)b * n + gidx(k)] : 0.0;
+  for (int m = 0; m < MB; ++m) {
+    const double* lanes = a.lanes + (size_t)(bb + m) * a.Pl * n;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      C[m][k] = (act && mact(m)) ? lanes[(size_t)q0 * n + gidx(k)] : 0.0;
+      G_[m][k] = (phi && owned && mact(m)) ? a.pacc[(size_t)(bb + m) * n + gidx(k)] : 0.0;
+    }
   }
   int par = 0, xpar = 0;
-  auto exchange = [&](double first, double lastv, double& left, double& right) {
+  // run-edge exchange inside the CTA for all members: (left, right) neighbours
+  auto exchange = [&](double (*u)[PPT], double* left, double* right) {
     if (act) {
-      eL[par][t] = first;
-      eR[par][t] = lastv;
+#pragma unroll
+      for (int m = 0; m < MB; ++m) {
+        eL[par][m][t] = u[m][0];
+        eR[par][m][t] = u[m][PPT - 1];
+      }
     }
     __syncthreads();
-    left = eR[par][tl];
-    right = eL[par][tr];
+#pragma unroll
+    for (int m = 0; m < MB; ++m) {
+      left[m] = eR[par][m][tl];
+      right[m] = eL[par][m][tr];
+    }
     par ^= 1;
   };
   // refresh the ghost runs of u (and v, when given) from the neighbouring CTAs
-  auto refresh = [&](double* u, double* v) {
-    // publish my owned edge runs: left edge = local runs GR … 2GR−1, right = NR−2GR … NR−GR−1
+  auto refresh = [&](double (*u)[PPT], double (*v)[PPT]) {
     if (act) {
       if (t >= GR && t < 2 * GR) {
 #pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-          xbuf[xpar][0][0][(t - GR) * PPT + k] = u[k];
-          if (v) xbuf[xpar][0][1][(t - GR) * PPT + k] = v[k];
-        }
+        for (int m = 0; m < MB; ++m)
+#pragma unroll
+          for (int k = 0; k < PPT; ++k) {
+            xbuf[xpar][0][0][m][(t - GR) * PPT + k] = u[m][k];
+            if (v) xbuf[xpar][0][1][m][(t - GR) * PPT + k] = v[m][k];
+          }
       }
       if (t >= NR - 2 * GR && t < NR - GR) {
 #pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-          xbuf[xpar][1][0][(t - (NR - 2 * GR)) * PPT + k] = u[k];
-          if (v) xbuf[xpar][1][1][(t - (NR - 2 * GR)) * PPT + k] = v[k];
-        }
+        for (int m = 0; m < MB; ++m)
+#pragma unroll
+          for (int k = 0; k < PPT; ++k) {
+            xbuf[xpar][1][0][m][(t - (NR - 2 * GR)) * PPT + k] = u[m][k];
+            if (v) xbuf[xpar][1][1][m][(t - (NR - 2 * GR)) * PPT + k] = v[m][k];
+          }
       }
     }
     cluster.sync();
     // my left ghosts = left neighbour's right edge; my right ghosts = right neighbour's left edge
     if (act && t < GR) {
-      const double* src = cluster.map_shared_rank(&xbuf[xpar][1][0][0], (unsigned)((rank + CS - 1) % CS));
+      const double* src = cluster.map_shared_rank(&xbuf[xpar][1][0][0][0], (unsigned)((rank + CS - 1) % CS));
 #pragma unroll
-      for (int k = 0; k < PPT; ++k) {
-        u[k] = src[t * PPT + k];
-        if (v) v[k] = src[G + t * PPT + k];
-      }
+      for (int m = 0; m < MB; ++m)
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          u[m][k] = src[m * G + t * PPT + k];
+          if (v) v[m][k] = src[MB * G + m * G + t * PPT + k];
+        }
     }
     if (act && t >= NR - GR) {
-      const double* src = cluster.map_shared_rank(&xbuf[xpar][0][0][0], (unsigned)((rank + 1) % CS));
+      const double* src = cluster.map_shared_rank(&xbuf[xpar][0][0][0][0], (unsigned)((rank + 1) % CS));
 #pragma unroll
-      for (int k = 0; k < PPT; ++k) {
-        u[k] = src[(t - (NR - GR)) * PPT + k];
-        if (v) v[k] = src[G + (t - (NR - GR)) * PPT + k];
-      }
+      for (int m = 0; m < MB; ++m)
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          u[m][k] = src[m * G + (t - (NR - GR)) * PPT + k];
+          if (v) v[m][k] = src[MB * G + m * G + (t - (NR - GR)) * PPT + k];
+        }
     }
     xpar ^= 1;
   };
@@ -264,58 +284,62 @@ __global__ void __launch_bounds__(256) k_scan1d_cluster(Scan1DArgs a) {
     const double* __restrict__ bp = pl.bp;
     const int degree = pl.degree, substeps = pl.substeps;
     for (int sub = 0; sub < substeps; ++sub) {
-      double up[PPT], uc[PPT], acc[PPT], pc[PPT];
+      double up[MB][PPT], uc[MB][PPT], acc[MB][PPT], pc[MB][PPT];
       refresh(C, nullptr);
       int valid = G;  // ghost depth still exact
       const double b0 = __ldg(be), b1 = __ldg(be + 1);
       const double p0 = phi ? __ldg(bp) : 0.0, p1 = phi ? __ldg(bp + 1) : 0.0;
-      double left, right;
-      exchange(C[0], C[PPT - 1], left, right);
+      double left[MB], right[MB];
+      exchange(C, left, right);
 #pragma unroll
-      for (int k = 0; k < PPT; ++k) {
-        const double wl = (k == 0) ? left : C[k - 1];
-        const double wr = (k + 1 == PPT) ? right : C[k + 1];
-        double v = f0 * C[k];
-        v = fma(f1, wr, v);
-        uc[k] = fma(f2, wl, v);
-      }
+      for (int m = 0; m < MB; ++m)
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          const double wl = (k == 0) ? left[m] : C[m][k - 1];
+          const double wr = (k + 1 == PPT) ? right[m] : C[m][k + 1];
+          double v = f0 * C[m][k];
+          v = fma(f1, wr, v);
+          uc[m][k] = fma(f2, wl, v);
+          up[m][k] = C[m][k];
+          acc[m][k] = b0 * up[m][k] + b1 * uc[m][k];
+          pc[m][k] = p0 * up[m][k] + p1 * uc[m][k];
+        }
       --valid;
-#pragma unroll
-      for (int k = 0; k < PPT; ++k) {
-        up[k] = C[k];
-        acc[k] = b0 * up[k] + b1 * uc[k];
-        pc[k] = p0 * up[k] + p1 * uc[k];
-      }
       for (int j = 2; j <= degree; ++j) {
         if (valid == 0) {
           refresh(uc, up);
           valid = G;
         }
-        exchange(uc[0], uc[PPT - 1], left, right);
+        exchange(uc, left, right);
         const double bj = __ldg(be + j), pj = phi ? __ldg(bp + j) : 0.0;
-        double un[PPT];
 #pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-          const double wl = (k == 0) ? left : uc[k - 1];
-          const double wr = (k + 1 == PPT) ? right : uc[k + 1];
-          double v = fma(g0c, uc[k], sg * up[k]);
-          v = fma(g1, wr, v);
-          un[k] = fma(g2, wl, v);
-        }
+        for (int m = 0; m < MB; ++m) {
+          double un[PPT];
 #pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-          up[k] = uc[k];
-          uc[k] = un[k];
-          acc[k] += bj * un[k];
-          if (phi) pc[k] += pj * un[k];
+          for (int k = 0; k < PPT; ++k) {
+            const double wl = (k == 0) ? left[m] : uc[m][k - 1];
+            const double wr = (k + 1 == PPT) ? right[m] : uc[m][k + 1];
+            double v = fma(g0c, uc[m][k], sg * up[m][k]);
+            v = fma(g1, wr, v);
+            un[k] = fma(g2, wl, v);
+          }
+#pragma unroll
+          for (int k = 0; k < PPT; ++k) {
+            up[m][k] = uc[m][k];
+            uc[m][k] = un[k];
+            acc[m][k] += bj * un[k];
+            if (phi) pc[m][k] += pj * un[k];
+          }
         }
         --valid;
       }
 #pragma unroll
-      for (int k = 0; k < PPT; ++k) {
-        C[k] = acc[k];
-        G_[k] += pc[k];
-      }
+      for (int m = 0; m < MB; ++m)
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          C[m][k] = acc[m][k];
+          G_[m][k] += pc[m][k];
+        }
     }
   };
   const int n_act = a.Pl - 1 + (a.use_long ? 1 : 0);
@@ -326,15 +350,24 @@ __global__ void __launch_bounds__(256) k_scan1d_cluster(Scan1DArgs a) {
       const int q = a.adjoint ? a.Pl - 1 - s : s;
       if (act) {
 #pragma unroll
-        for (int k = 0; k < PPT; ++k) C[k] += lanes[(size_t)q * n + gidx(k)];
+        for (int m = 0; m < MB; ++m) {
+          if (!mact(m)) continue;
+          const double* lanes = a.lanes + (size_t)(bb + m) * a.Pl * n;
+#pragma unroll
+          for (int k = 0; k < PPT; ++k) C[m][k] += lanes[(size_t)q * n + gidx(k)];
+        }
       }
     }
   }
   if (owned) {
 #pragma unroll
-    for (int k = 0; k < PPT; ++k) {
-      a.out[(size_t)b * n + gidx(k)] = C[k];
-      if (phi) a.pacc[(size_t)b * n + gidx(k)] = G_[k];
+    for (int m = 0; m < MB; ++m) {
+      if (!mact(m)) continue;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        a.out[(size_t)(bb + m) * n + gidx(k)] = C[m][k];
+        if (phi) a.pacc[(size_t)(bb + m) * n + gidx(k)] = G_[m][k];
+      }
     }
   }
   cluster.sync();  // no CTA leaves while a neighbour may still read its exchange buffers
