@@ -35,6 +35,8 @@ def cmd_run(args) -> int:
     c = _case(args.config)
     u0, ut, ctrl = c.inputs()
     algo = "linear" if c.system.is_linear else ("nonlinear" if args.nonlinear else "hybrid")
+    if args.algorithm:
+        algo = args.algorithm
     rk = RK4Config(c.dt)
     rows, t = [], []
     if args.checkpoints:
@@ -140,6 +142,8 @@ def main(argv=None) -> int:
     r.add_argument("--output", default="results")
     r.add_argument("--single", action="store_true", help="one gradient even for descent configs")
     r.add_argument("--nonlinear", action="store_true", help="Burgers: Algorithm 2 direct instead of serial")
+    r.add_argument("--algorithm", choices=["serial", "linear", "nonlinear", "hybrid"], default=None,
+                   help="override the config's algorithm (serial = the reference loop, no Paraexp)")
     r.add_argument("--checkpoints", type=int, default=0,
                    help="M equispaced checkpoints (run_checkpointed_loop; P/(M+1) slices per segment)")
     p = sub.add_parser("predict", help="measure per-unit kernel times, print the multi-GPU scaling model")

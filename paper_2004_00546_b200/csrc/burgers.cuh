@@ -734,8 +734,10 @@ inline int burgers_adjoint(const BurgersAdjointArgs& a, cudaStream_t s, px_stats
   double* coef = a.Wk[2];
   const size_t ncoef = 2 * (size_t)(a.degree + 1);
   if ((size_t)a.B * a.nx < ncoef) return PX_ERR_ARG;
-  cudaMemcpyAsync(coef, a.be, sizeof(double) * (a.degree + 1), cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(coef + a.degree + 1, a.bp, sizeof(double) * (a.degree + 1), cudaMemcpyHostToDevice, s);
+  if (a.be && a.bp) {  // no plan: one slice, no carry (the scan only finalises q†(0) and G)
+    cudaMemcpyAsync(coef, a.be, sizeof(double) * (a.degree + 1), cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(coef + a.degree + 1, a.bp, sizeof(double) * (a.degree + 1), cudaMemcpyHostToDevice, s);
+  }
   const size_t smem_sc = 2 * (size_t)a.nx * sizeof(double);
 #define PX_BS(PP)                                                                               \
   do {                                                                                          \

@@ -1305,7 +1305,10 @@ int px_adjoint(void* handle, void* stream) {
     rc = adjoint_linear(h, s);
   } else {
     const Plan& pl = h->plans[PX_PLAN_FROZEN];
-    if (!pl.set || pl.krylov) return fail(h, PX_ERR_STATE, "frozen-operator plan not set");
+    // one slice and no earlier ranks (the serial loop): no homogeneous carry, no plan needed
+    const bool no_carry = h->Pl == 1 && h->d.p_begin == 0;
+    if ((!pl.set || pl.krylov) && !no_carry) return fail(h, PX_ERR_STATE, "frozen-operator plan not set");
+    const bool use_plan = pl.set && !pl.krylov;
     px::BurgersAdjointArgs a{};
     a.traj = h->traj; a.ubar = h->ubar; a.QT = h->QT;
     a.W0 = h->Y0; a.W1 = h->Y1; a.Z = h->Z;
@@ -1315,8 +1318,13 @@ int px_adjoint(void* handle, void* stream) {
     a.D = h->d.D; a.hx = h->d.hx; a.h = (h->d.T / h->d.P) / h->d.nsteps;
     a.nx = h->d.nx; a.B = h->B; a.P = h->d.P; a.nsteps = h->d.nsteps;
     a.p_begin = h->d.p_begin; a.p_end = h->d.p_end;
-    a.substeps = pl.substeps; a.degree = pl.degree; a.center = pl.center; a.scale = pl.scale;
-    a.sigma = pl.sigma; a.be = pl.be.data(); a.bp = pl.bp.data();
+    if (use_plan) {
+      a.substeps = pl.substeps; a.degree = pl.degree; a.center = pl.center; a.scale = pl.scale;
+      a.sigma = pl.sigma; a.be = pl.be.data(); a.bp = pl.bp.data();
+    } else {
+      a.substeps = 0; a.degree = 0; a.center = 0.0; a.scale = 1.0; a.sigma = 1;
+      a.be = a.bp = nullptr;
+    }
     const int tm = tbegin(h, PX_PHASE_RK4_ADJOINT, s);
     rc = px::burgers_adjoint(a, s, &h->stats, &h->wend);
     tend(h, tm, s);

@@ -167,7 +167,7 @@ class ParaexpEngine:
         if sysm.is_linear:
             region = sysm.region()
             delta = sysm.spec.T / spec.P
-            if p1 - p0 > 1 or spec.world == 1:
+            if p1 - p0 > 1:  # carries between this rank's slices (none for one slice: serial)
                 self._set_plan(N.PX_PLAN_SLICE, self._plan(region, delta))
             if p1 < spec.P:
                 self._set_plan(N.PX_PLAN_LONG_DIRECT, self._plan(region, (spec.P - p1) * delta))
@@ -310,8 +310,8 @@ class ParaexpEngine:
 
     def adjoint_partial(self, stream: int | None = None) -> None:
         s = current_stream_handle() if stream is None else stream
-        if not self.spec.system.is_linear:
-            self.plan_frozen(s)
+        if not self.spec.system.is_linear and (self.p1 - self.p0 > 1 or self.p0 > 0):
+            self.plan_frozen(s)  # no carry for a single slice (the serial loop)
         N.check(self.lib, self.lib.px_adjoint(self.h, s), self.h)
 
     def finish_adjoint(self, stream: int | None = None) -> None:

@@ -14,8 +14,10 @@ initial state ``u0`` is passed through (the reference hard-wires q0 = 0,
 advection–diffusion), "hybrid" (serial direct sweep + Paraexp adjoint with
 frozen linearisation, Burgers) or "nonlinear" (Algorithm 2: iterative
 Jacobian-augmented Paraexp direct, then the same frozen-linearisation adjoint,
-Burgers; ``eps``/``min_iter``/``max_iter`` as `optimization.py:162-164`). The only
-backend is "cuda": there is no CPU fallback.
+Burgers; ``eps``/``min_iter``/``max_iter`` as `optimization.py:162-164`) or "serial"
+(`optimization.py:197-203`: one RK4 sweep over the whole horizon for the direct and one for
+the adjoint, no exponential actions — the one-slice case of the same kernels; ``N`` is
+ignored). The only backend is "cuda": there is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -31,10 +33,11 @@ from .expaction import ChebyshevConfig, KrylovConfig
 from .partition import RK4Config, TimePartition, partition_equidistant
 from .systems import System
 
+SERIAL = "serial"
 LINEAR = "linear"
 NONLINEAR = "nonlinear"
 HYBRID = "hybrid"
-ALGORITHMS = (LINEAR, NONLINEAR, HYBRID)
+ALGORITHMS = (SERIAL, LINEAR, NONLINEAR, HYBRID)
 BACKENDS = ("cuda",)
 
 
@@ -153,6 +156,10 @@ def direct_adjoint_loop(
         raise ValueError(f"unknown algorithm {algorithm!r}")
     if algorithm == LINEAR and not system.is_linear:
         raise ValueError("linear algorithm requires a linear testbed")
+    if algorithm == SERIAL:
+        # serial reference loop: a single "slice" spanning [0, T] (no exp-actions); for Burgers
+        # the serial direct sweep and one time-varying adjoint lane over the whole horizon
+        N = 1
     if algorithm in (HYBRID, NONLINEAR) and system.is_linear:
         raise ValueError(f"the {algorithm} path is the Burgers testbed's")
     if rk is None:
@@ -164,8 +171,8 @@ def direct_adjoint_loop(
         raise ValueError("control coefficient count does not match the basis")
     u0 = np.zeros(system.n) if u0 is None else np.asarray(u0, dtype=np.float64)
     rank, world = _dist_rank_world() if distributed else (0, 1)
-    if algorithm == NONLINEAR:
-        rank, world = 0, 1  # Algorithm 2 runs on one rank (every rank computes it identically)
+    if algorithm in (NONLINEAR, SERIAL):
+        rank, world = 0, 1  # one rank (every rank computes it identically): nothing to shard
     eng = get_engine(system, N, rk, expaction, B, rank, world, boundary_states and world == 1,
                      "iterative" if algorithm == NONLINEAR else "serial", eps, max_iter, min_iter)
     tick = time.perf_counter()
@@ -196,7 +203,7 @@ def descend(
     q_true: np.ndarray,
     steps: int,
     lr: float,
-    algorithm: str = LINEAR,
+    algorithm: str = SERIAL,
     N: int = 1,
     rk: RK4Config | None = None,
     expaction=None,

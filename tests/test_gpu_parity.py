@@ -102,7 +102,8 @@ def test_config2_descent_two_steps():
     from paper_2004_00546_b200 import RK4Config, baseline, descend
     c = baseline(2)
     u0, ut, ctrl = c.inputs()
-    res = descend(c.system, ctrl, ut, steps=2, lr=c.lr, N=c.P, rk=RK4Config(c.dt), expaction=c.expaction, u0=u0)
+    res = descend(c.system, ctrl, ut, steps=2, lr=c.lr, algorithm="linear", N=c.P, rk=RK4Config(c.dt),
+                  expaction=c.expaction, u0=u0)
     sp, _ = _plans(c)
     f = ctrl.copy()
     for it in range(2):
@@ -577,3 +578,26 @@ def test_checkpointed_linear_vs_oracle():
     assert rel_l2(run.integral, G) <= 1e-10
     assert rel_l2(run.gradient, grad) <= 1e-8
     assert abs(float(run.cost[0]) - float(J[0])) <= 1e-10 * abs(float(J[0]))
+
+
+@pytest.mark.parametrize("index", [1, 3, 5])
+def test_serial_algorithm_vs_oracle(index):
+    """algorithm="serial" (the reference's default loop, `optimization.py:197-203`): one RK4
+    sweep over [0, T] for the direct and one for the adjoint, no exp-actions — the one-slice
+    case of the same kernels (config 5 scaled: the single-step 2D march over all steps)."""
+    from oracle.config_mode import burgers_gradient, linear_gradient
+    from paper_2004_00546_b200 import RK4Config, baseline, direct_adjoint_loop, scaled
+    from paper_2004_00546_b200.problems import burgers_frozen_region
+    c = baseline(index) if index != 5 else scaled(baseline(5), nx=96, P=12, steps_per_slice=8, K=16)
+    from paper_2004_00546_b200.partition import slice_steps
+    u0, ut, ctrl = c.inputs()
+    steps = slice_steps(c.spec.T, c.dt)  # one slice over [0, T]: ⌈T/dt⌉ uniform steps
+    loop = direct_adjoint_loop(c.system, ctrl, ut, "serial", N=c.P, rk=RK4Config(c.dt), expaction=c.expaction,
+                               u0=u0)
+    if c.system.is_linear:
+        ref = linear_gradient(c.grid.nx, c.grid.ny, c.system.A.as_tuple(), c.system.basis, c.spec.T, 1, steps,
+                              u0, ut, ctrl, None)
+    else:
+        ref = burgers_gradient(c.grid.nx, c.spec.D, c.system.basis, c.spec.T, 1, steps, u0, ut, ctrl,
+                               lambda region, span: None, lambda ub: burgers_frozen_region(ub, c.grid, c.spec.D))
+    _check(loop, ref)
