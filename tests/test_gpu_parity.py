@@ -601,3 +601,36 @@ def test_serial_algorithm_vs_oracle(index):
         ref = burgers_gradient(c.grid.nx, c.spec.D, c.system.basis, c.spec.T, 1, steps, u0, ut, ctrl,
                                lambda region, span: None, lambda ub: burgers_frozen_region(ub, c.grid, c.spec.D))
     _check(loop, ref)
+
+
+def test_solver_level_api_vs_oracle():
+    """solve_direct_linear / solve_adjoint_linear / solve_hybrid (the reference's solver-level
+    entry points) against the oracle's pieces: u(T) from u0, and the adjoint for a given
+    terminal condition q†(T)."""
+    from oracle.config_mode import burgers_gradient, linear_gradient
+    from paper_2004_00546_b200 import (RK4Config, baseline, scaled, solve_adjoint_linear, solve_direct_linear,
+                                       solve_hybrid)
+    from paper_2004_00546_b200.expaction import plan_chebyshev
+    from paper_2004_00546_b200.problems import burgers_frozen_region
+    c = scaled(baseline(5), nx=96, P=12, steps_per_slice=8, K=16)
+    u0, ut, ctrl = c.inputs()
+    sp, _ = _plans(c)
+    qT = np.random.default_rng(3).normal(size=c.n)
+    ref = linear_gradient(c.grid.nx, c.grid.ny, c.system.A.as_tuple(), c.system.basis, c.spec.T, c.P, c.nsteps,
+                          u0, ut, ctrl, sp, qdag_T=qT)
+    d = solve_direct_linear(c.system, u0, ctrl, c.P, RK4Config(c.dt), c.expaction, boundary_states=True)
+    assert rel_l2(d.final_state, ref.uT) <= 1e-10
+    assert rel_l2(d.boundary_states[:, -1], ref.uT) <= 1e-10
+    a = solve_adjoint_linear(c.system, qT, c.P, RK4Config(c.dt), c.expaction)
+    assert rel_l2(a.initial_state, ref.qdag0) <= 1e-10
+    assert rel_l2(a.integral, ref.G) <= 1e-10
+    c3 = scaled(baseline(3), nx=256, P=8, steps_per_slice=16)
+    u0, ut, ctrl = c3.inputs()
+    qT = np.random.default_rng(4).normal(size=c3.n)
+    ref = burgers_gradient(c3.grid.nx, c3.spec.D, c3.system.basis, c3.spec.T, c3.P, c3.nsteps, u0, ut, ctrl,
+                           lambda region, span: plan_chebyshev(region, span, c3.expaction),
+                           lambda ub: burgers_frozen_region(ub, c3.grid, c3.spec.D), qdag_T=qT)
+    d, a = solve_hybrid(c3.system, u0, ctrl, qT, c3.P, RK4Config(c3.dt), c3.expaction)
+    assert rel_l2(d.final_state, ref.uT) <= 1e-10
+    assert rel_l2(a.initial_state, ref.qdag0) <= 1e-10
+    assert rel_l2(a.integral, ref.G) <= 1e-10
