@@ -57,7 +57,7 @@ from .problems import (
     burgers_frozen_region,
     mode_basis,
 )
-from .solvers import solve_adjoint_linear, solve_direct_linear, solve_hybrid
+from .solvers import solve_adjoint_linear, solve_direct_linear, solve_hybrid, synthesize_truth
 from .systems import System, build_system
 
 __all__ = [name for name in dir() if not name.startswith("_")]

@@ -103,3 +103,21 @@ def solve_hybrid(system: System, u0, f, qdag_T, N: int, rk: RK4Config, expaction
     adjoint = AdjointSolution(part, eng.get(NV.PX_FIELD_QDAG0).reshape(B, system.n),
                               eng.get(NV.PX_FIELD_G).reshape(B, system.n))
     return direct, adjoint
+
+
+def synthesize_truth(system: System, f_true, rk: RK4Config, algorithm: str = "serial", N: int = 1,
+                     expaction=None, u0=None) -> DirectSolution:
+    """Evolve the system under the control ``f_true`` to produce the target
+    (`optimization.py:66-80`); for the terminal objective the target is its u(T)
+    (``final_state``). ``algorithm`` "serial" is one sweep; otherwise Paraexp over N slices."""
+    u0 = np.zeros(system.n) if u0 is None else np.asarray(u0, dtype=np.float64).reshape(-1)
+    if algorithm == "serial":
+        N = 1
+    if system.is_linear:
+        return solve_direct_linear(system, u0, f_true, N, rk, expaction)
+    ctrl, expaction = _prepare(system, f_true, rk, expaction)
+    eng = get_engine(system, N, rk, expaction, ctrl.shape[0])
+    eng.set_inputs(u0, np.zeros(system.n), ctrl)
+    eng.direct_partial()
+    return DirectSolution(partition_equidistant(system.spec.T, N),
+                          eng.get(NV.PX_FIELD_UT).reshape(ctrl.shape[0], system.n))

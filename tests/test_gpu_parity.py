@@ -632,5 +632,8 @@ def test_solver_level_api_vs_oracle():
                            lambda ub: burgers_frozen_region(ub, c3.grid, c3.spec.D), qdag_T=qT)
     d, a = solve_hybrid(c3.system, u0, ctrl, qT, c3.P, RK4Config(c3.dt), c3.expaction)
     assert rel_l2(d.final_state, ref.uT) <= 1e-10
+    from paper_2004_00546_b200 import synthesize_truth
+    tr = synthesize_truth(c3.system, ctrl, RK4Config(c3.dt), "hybrid", N=c3.P, expaction=c3.expaction, u0=u0)
+    assert np.array_equal(tr.final_state, d.final_state)
     assert rel_l2(a.initial_state, ref.qdag0) <= 1e-10
     assert rel_l2(a.integral, ref.G) <= 1e-10
