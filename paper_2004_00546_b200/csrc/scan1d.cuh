@@ -51,7 +51,6 @@ __global__ void __launch_bounds__(512) k_scan1d(Scan1DArgs a) {
   const int last = (n + PPT - 1) / PPT - 1;
   const int tl = (t == 0) ? last : t - 1;
   const int tr = (t >= last) ? 0 : t + 1;
-  const Stencil5 st = a.st;
   const bool phi = a.adjoint && a.pacc != nullptr;
   const double* lanes = a.lanes + (size_t)b * a.Pl * n;
   double C[PPT], G[PPT];
