@@ -22,6 +22,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys / Nsight timelines
+
 #include "../../include/paraexp.h"
 #include "kernels.cuh"
 #include "burgers.cuh"
@@ -161,14 +163,29 @@ void drop_segments(Handle* h) {
   h->segs.clear();
 }
 
+const char* phase_name(int phase) {
+  static const char* names[] = {"px.rk4_direct", "px.rk4_adjoint", "px.exp_direct", "px.exp_adjoint", "px.other"};
+  return (phase >= 0 && phase < PX_PHASE_COUNT) ? names[phase] : "px.phase";
+}
+
+// RAII NVTX range (the reference's recorder hooks, `workers.py:26-36`, become timeline ranges)
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+  NvtxScope(const NvtxScope&) = delete;
+  NvtxScope& operator=(const NvtxScope&) = delete;
+};
+
 // Open a timing window for `phase` (returns -1 when timing is off; while capturing a
-// graph the window becomes its own graph segment, timed at replay).
+// graph the window becomes its own graph segment, timed at replay). Eager windows are
+// also NVTX ranges.
 int tbegin(Handle* h, int phase, cudaStream_t s) {
   if (h->capturing) {
     seg_close(h);
     seg_open(h, phase);
     return -2;
   }
+  nvtxRangePushA(phase_name(phase));
   if (!h->timing) return -1;
   Handle::TMark m{phase, take_event(h), take_event(h), h->stats.kernel_launches, h->stats.algorithmic_bytes};
   cudaEventRecord(m.a, s);
@@ -182,6 +199,7 @@ void tend(Handle* h, int idx, cudaStream_t s) {
     seg_open(h, -1);
     return;
   }
+  nvtxRangePop();
   if (idx < 0) return;
   Handle::TMark& m = h->marks[idx];
   cudaEventRecord(m.b, s);
@@ -1399,7 +1417,9 @@ int px_gradient(void* handle, void* stream) {
   // order: caller's stream -> graph stream -> caller's stream
   PX_CUDA(h, cudaEventRecord(h->ev_in, s));
   PX_CUDA(h, cudaStreamWaitEvent(h->gstream, h->ev_in, 0));
+  NvtxScope gradient_range("px.gradient(graph)");
   for (auto& sg : h->segs) {
+    if (sg.phase >= 0) nvtxRangePushA(phase_name(sg.phase));
     if (h->timing && sg.phase >= 0) {
       Handle::TMark m{sg.phase, take_event(h), take_event(h), sg.launches, sg.bytes};
       PX_CUDA(h, cudaEventRecord(m.a, h->gstream));
@@ -1409,6 +1429,7 @@ int px_gradient(void* handle, void* stream) {
     } else {
       PX_CUDA(h, cudaGraphLaunch(sg.exec, h->gstream));
     }
+    if (sg.phase >= 0) nvtxRangePop();
   }
   PX_CUDA(h, cudaEventRecord(h->ev_out, h->gstream));
   PX_CUDA(h, cudaStreamWaitEvent(s, h->ev_out, 0));
