@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from .errors import ConfigError, IntegrationFailure, IterationDivergence, NativeUnavailable
+from .errors import CollectiveFailure, ConfigError, IntegrationFailure, IterationDivergence, NativeUnavailable
 from .expaction import ChebPlan, ChebyshevConfig, KrylovConfig, KrylovPlan, plan_chebyshev, plan_for
 from .partition import partition_equidistant, rank_block, slice_steps
 from .problems import ADVECTION_DIFFUSION, frozen_region_from_bounds
@@ -97,12 +97,23 @@ def distributed_gradient(eng, stream=None, group=None, want_fields: bool = True,
     the partial conventions are the C ABI's (`px_finish_*` add the q0 / q†_T terms
     once, after the reduction).
     """
-    eng.direct_partial(stream)
-    reduce([eng.view(f) for f in eng.direct_reduce_fields()], group)
-    eng.finish_direct(stream)
-    eng.adjoint_partial(stream)
-    reduce([eng.view(f) for f in eng.adjoint_reduce_fields(want_fields)], group)
-    eng.finish_adjoint(stream)
+    rank = getattr(getattr(eng, "spec", None), "rank", 0)
+    phases = (
+        ("direct", lambda: eng.direct_partial(stream)),
+        ("direct allreduce", lambda: reduce([eng.view(f) for f in eng.direct_reduce_fields()], group)),
+        ("finish direct", lambda: eng.finish_direct(stream)),
+        ("adjoint", lambda: eng.adjoint_partial(stream)),
+        ("adjoint allreduce",
+         lambda: reduce([eng.view(f) for f in eng.adjoint_reduce_fields(want_fields)], group)),
+        ("finish adjoint", lambda: eng.finish_adjoint(stream)),
+    )
+    for name, run in phases:
+        try:
+            run()
+        except CollectiveFailure:
+            raise
+        except Exception as e:  # the reference's fail-fast convention (`workers.py:140-160`)
+            raise CollectiveFailure(rank, name, e) from e
 
 
 class ParaexpEngine:

@@ -88,3 +88,32 @@ def test_rank_blocks_cover_slices_contiguously():
                 assert a1 == b0 and a1 > a0
             sizes = [b - a for a, b in blocks]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_phase_failure_maps_to_collective_failure():
+    """A failing phase on a rank surfaces as CollectiveFailure(worker, subproblem, cause)
+    (the reference's fail-fast convention, `workers.py:140-160`, `errors.py:39-49`)."""
+    from types import SimpleNamespace
+
+    from paper_2004_00546_b200.engine import distributed_gradient
+    from paper_2004_00546_b200.errors import CollectiveFailure
+
+    calls = []
+
+    class Fake:
+        spec = SimpleNamespace(rank=3)
+
+        def direct_partial(self, s): calls.append("direct")
+        def direct_reduce_fields(self): return []
+        def view(self, f): return f
+        def finish_direct(self, s): calls.append("finish_direct")
+        def adjoint_partial(self, s): raise RuntimeError("boom")
+        @staticmethod
+        def adjoint_reduce_fields(w=True): return []
+        def finish_adjoint(self, s): calls.append("finish_adjoint")
+
+    with pytest.raises(CollectiveFailure) as ei:
+        distributed_gradient(Fake(), reduce=lambda ts, g: None)
+    assert ei.value.worker == 3 and ei.value.subproblem == "adjoint"
+    assert isinstance(ei.value.cause, RuntimeError)
+    assert calls == ["direct", "finish_direct"]
