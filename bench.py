@@ -404,8 +404,9 @@ def main():
         el = float(el.item())
         e2e = {"value": args.e2e_steps * c.batch / el, "unit": UNIT,
                "h2d_bytes_per_step": (2 * c.n + c.batch * c.K) * 8,
-               "d2h_bytes_per_step": (c.batch + c.batch * c.K + 3 * c.batch * c.n) * 8,
-               "api": "direct_adjoint_loop(numpy host arrays)"}
+               "d2h_bytes_per_step": (c.batch + c.batch * c.K) * 8,
+               "api": "direct_adjoint_loop(numpy host arrays); J and dJ/dc read to the host each step, "
+                      "u(T) / q†(0) / ∫q† kept as device snapshots copied on first access"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -371,17 +371,25 @@ class ParaexpEngine:
             return
         distributed_gradient(self, s, group, want_fields)
 
-    def results(self, stream: int | None = None) -> dict:
+    def results(self, stream: int | None = None, fields: bool = True) -> dict:
         J = self.get(N.PX_FIELD_J, stream)
         if not np.all(np.isfinite(J)):
             raise IntegrationFailure(self.spec.system.spec.T, "non-finite objective")
-        return {
-            "J": J,
-            "grad": self.get(N.PX_FIELD_GRAD, stream).reshape(self.B, self.K),
-            "uT": self.get(N.PX_FIELD_UT, stream).reshape(self.B, self.n),
-            "qdag0": self.get(N.PX_FIELD_QDAG0, stream).reshape(self.B, self.n),
-            "G": self.get(N.PX_FIELD_G, stream).reshape(self.B, self.n),
-        }
+        out = {"J": J, "grad": self.get(N.PX_FIELD_GRAD, stream).reshape(self.B, self.K)}
+        if fields:
+            out["uT"] = self.get(N.PX_FIELD_UT, stream).reshape(self.B, self.n)
+            out["qdag0"] = self.get(N.PX_FIELD_QDAG0, stream).reshape(self.B, self.n)
+            out["G"] = self.get(N.PX_FIELD_G, stream).reshape(self.B, self.n)
+        return out
+
+    def snapshot(self, field: int, shape):
+        """A device-side copy of a result field, read to the host on first use
+        (`optimization.DeviceField`); a host array when torch/CUDA is unavailable."""
+        from .optimization import DeviceField
+        torch = _torch()
+        if torch is None or not torch.cuda.is_available():
+            return self.get(field).reshape(shape)
+        return DeviceField(self.device_view(field).clone(), shape)
 
     def close(self) -> None:
         if getattr(self, "h", None):

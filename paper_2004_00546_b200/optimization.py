@@ -42,12 +42,40 @@ BACKENDS = ("cuda",)
 
 
 @dataclass
+class DeviceField:
+    """A result field kept on the device (a snapshot of the native buffer, so later
+    gradients cannot overwrite it) and copied to the host on first use. The loop's
+    scalar outputs (J, ∂J/∂c) are read eagerly; the n-sized fields only when asked
+    for, like the reference's lazily evaluated `PiecewiseSolution`s."""
+
+    def __init__(self, tensor, shape):
+        self._t = tensor
+        self._shape = shape
+        self._host = None
+
+    def numpy(self) -> np.ndarray:
+        if self._host is None:
+            self._host = self._t.cpu().numpy().reshape(self._shape)
+            self._t = None
+        return self._host
+
+
+def _host(v):
+    return v.numpy() if isinstance(v, DeviceField) else v
+
+
+@dataclass
 class DirectSolution:
     """u(T) (and, when requested, the boundary states u(T_p))."""
 
     partition: TimePartition
-    final_state: np.ndarray
+    _final: object
     boundary_states: np.ndarray | None = None
+
+    @property
+    def final_state(self) -> np.ndarray:
+        self._final = _host(self._final)
+        return self._final
 
 
 @dataclass
@@ -55,8 +83,18 @@ class AdjointSolution:
     """q†(0) and G = ∫₀ᵀ q† dt (the gradient with respect to a full control field)."""
 
     partition: TimePartition
-    initial_state: np.ndarray
-    integral: np.ndarray
+    _initial: object
+    _integral: object
+
+    @property
+    def initial_state(self) -> np.ndarray:
+        self._initial = _host(self._initial)
+        return self._initial
+
+    @property
+    def integral(self) -> np.ndarray:
+        self._integral = _host(self._integral)
+        return self._integral
 
 
 @dataclass
@@ -178,18 +216,20 @@ def direct_adjoint_loop(
     tick = time.perf_counter()
     eng.set_inputs(u0, np.asarray(q_true, dtype=np.float64), ctrl)
     eng.gradient()
-    res = eng.results()
+    from . import _native as NN
+    res = eng.results(fields=False)  # J and ∂J/∂c to the host; the n-sized fields stay on the device
     part = partition_equidistant(system.spec.T, N)
     bnd = None
     if boundary_states and world == 1:
-        from . import _native as NN
         bnd = eng.get(NN.PX_FIELD_UBND).reshape(B, N + 1, system.n)
     J = res["J"] if B > 1 or np.ndim(f) > 1 else float(res["J"][0])
     grad = res["grad"] if B > 1 or np.ndim(f) > 1 else res["grad"][0]
+    fields = {k: eng.snapshot(fld, (B, system.n))
+              for k, fld in (("uT", NN.PX_FIELD_UT), ("qdag0", NN.PX_FIELD_QDAG0), ("G", NN.PX_FIELD_G))}
     return LoopResult(
         J, grad,
-        DirectSolution(part, res["uT"], bnd),
-        AdjointSolution(part, res["qdag0"], res["G"]),
+        DirectSolution(part, fields["uT"], bnd),
+        AdjointSolution(part, fields["qdag0"], fields["G"]),
         iterations=len(eng.nl_history) if algorithm == NONLINEAR else 1,
         seconds=time.perf_counter() - tick,
         error_history=list(eng.nl_history) if algorithm == NONLINEAR else [],
