@@ -301,6 +301,8 @@ class ParaexpEngine:
         for it in range(1, spec.nl_max_iter + 1):
             N.check(self.lib, self.lib.px_nl_prepare(self.h, s), self.h)
             lo, hi, im = self.get(N.PX_FIELD_FROZEN_BOUNDS, s)
+            if not np.all(np.isfinite([lo, hi, im])):
+                raise IntegrationFailure(spec.system.spec.T, "non-finite iterate")
             region = frozen_region_from_bounds(float(lo), float(hi), float(im))
             self._set_plan(N.PX_PLAN_NL_SLICE, plan_chebyshev(region, delta, cfg))
             self._set_plan(N.PX_PLAN_NL_STEP, plan_chebyshev(region, hstep, cfg))
@@ -340,6 +342,8 @@ class ParaexpEngine:
     def plan_frozen(self, stream: int | None = None) -> ChebPlan:
         """Burgers: read the frozen-operator FOV union, plan on the host (cached)."""
         lo, hi, im = self.get(N.PX_FIELD_FROZEN_BOUNDS, stream)
+        if not np.all(np.isfinite([lo, hi, im])):  # a non-finite direct trajectory
+            raise IntegrationFailure(self.spec.system.spec.T, "non-finite Burgers trajectory")
         region = frozen_region_from_bounds(float(lo), float(hi), float(im))
         cfg = self.spec.expaction
         if not isinstance(cfg, ChebyshevConfig):

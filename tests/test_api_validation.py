@@ -55,3 +55,14 @@ def test_unstable_step_is_a_config_error():
     c = scaled(baseline(5), nx=640, P=4, steps_per_slice=10, K=16)
     with pytest.raises(ConfigError):
         check_rk4_stability(c.system.region(), c.dt)
+
+
+def test_planner_failure_is_propagation_failure():
+    """An exp-action that no admissible Chebyshev plan can deliver raises the reference's
+    PropagationFailure (`errors.py:18-19`) on the host, before any GPU work."""
+    from paper_2004_00546_b200 import ChebyshevConfig
+    from paper_2004_00546_b200.errors import PropagationFailure
+    from paper_2004_00546_b200.expaction import plan_chebyshev
+    c = baseline(2)
+    with pytest.raises(PropagationFailure):
+        plan_chebyshev(c.system.region(), 50.0 * c.spec.T, ChebyshevConfig(tol=1e-14, max_degree=8))

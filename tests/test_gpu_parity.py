@@ -637,3 +637,26 @@ def test_solver_level_api_vs_oracle():
     assert np.array_equal(tr.final_state, d.final_state)
     assert rel_l2(a.initial_state, ref.qdag0) <= 1e-10
     assert rel_l2(a.integral, ref.G) <= 1e-10
+
+
+def test_nonfinite_input_raises_integration_failure():
+    """A non-finite state surfaces as the reference's IntegrationFailure (`errors.py:4-15`),
+    for the linear (graph-replayed) and the Burgers paths."""
+    from paper_2004_00546_b200 import RK4Config, baseline, direct_adjoint_loop, scaled
+    from paper_2004_00546_b200.errors import IntegrationFailure
+    c = scaled(baseline(5), nx=32, P=4, steps_per_slice=4, K=4)
+    u0, ut, ctrl = c.inputs()
+    bad = u0.copy()
+    bad[7] = np.nan
+    with pytest.raises(IntegrationFailure):
+        direct_adjoint_loop(c.system, ctrl, ut, "linear", N=c.P, rk=RK4Config(c.dt), expaction=c.expaction, u0=bad)
+    # the handle recovers: the next finite evaluation is unaffected
+    loop = direct_adjoint_loop(c.system, ctrl, ut, "linear", N=c.P, rk=RK4Config(c.dt), expaction=c.expaction,
+                               u0=u0)
+    assert np.all(np.isfinite(loop.grad))
+    b = scaled(baseline(3), nx=128, P=4, steps_per_slice=8)
+    u0, ut, ctrl = b.inputs()
+    bad = u0.copy()
+    bad[3] = np.inf
+    with pytest.raises(IntegrationFailure):
+        direct_adjoint_loop(b.system, ctrl, ut, "hybrid", N=b.P, rk=RK4Config(b.dt), expaction=b.expaction, u0=bad)
