@@ -48,15 +48,19 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def load_traffic(phase_kernel: str, config: int):
-    """ncu dram bytes per launch for the dominant kernel, from the committed profile summary."""
+def load_profile(phase_kernel: str, config: int) -> dict:
+    """The committed ncu summary (per-launch DRAM bytes, limiter) for the dominant kernel."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
-        return None
+        return {}
     with open(p) as f:
         d = json.load(f)
-    ent = d.get(f"c{config}", {}).get(phase_kernel)
-    return None if ent is None else ent.get("dram_bytes_per_launch")
+    return d.get(f"c{config}", {}).get(phase_kernel) or {}
+
+
+def load_traffic(phase_kernel: str, config: int):
+    """ncu dram bytes per launch for the dominant kernel, from the committed profile summary."""
+    return load_profile(phase_kernel, config).get("dram_bytes_per_launch")
 
 
 class ClockSampler:
@@ -372,6 +376,9 @@ def main():
                 "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_s * 1e3,
                 "share_of_step": ph["ms"] / sum(p["ms"] for p in phases.values()),
                 "traffic": load_traffic(dom, args.config)}
+    lim = load_profile(dom, args.config).get("limiter")
+    if lim:
+        roofline["limiter"] = lim
     if roofline["frac"] > 1.0:
         roofline["note"] = ("on-chip kernel (state resident in shared memory / registers across steps or "
                             "terms): the per-unit HBM model of SURVEY §8(d) counts bytes this kernel never "
