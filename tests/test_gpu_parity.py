@@ -660,3 +660,47 @@ def test_nonfinite_input_raises_integration_failure():
     bad[3] = np.inf
     with pytest.raises(IntegrationFailure):
         direct_adjoint_loop(b.system, ctrl, ut, "hybrid", N=b.P, rk=RK4Config(b.dt), expaction=b.expaction, u0=bad)
+
+
+def test_raw_c_abi_gradient_matches_python_api():
+    """The drop-in boundary on its own: one gradient driven purely through the C ABI
+    (ctypes, as INTEGRATION.md §2 shows a reference maintainer binding it) equals the
+    Python API's result bit for bit."""
+    import ctypes
+    from paper_2004_00546_b200 import RK4Config, _native as N, baseline, direct_adjoint_loop, scaled
+    from paper_2004_00546_b200.expaction import plan_for
+    c = scaled(baseline(5), nx=64, P=8, steps_per_slice=6, K=16)
+    u0, ut, ctrl = c.inputs()
+    lib = N.load()
+    d = N.ProblemDesc()
+    d.kind, d.nx, d.ny = N.PX_KIND_ADVDIFF, c.grid.nx, c.grid.ny
+    for i, v in enumerate(c.system.A.as_tuple()):
+        d.stencil[i] = v
+    d.D, d.hx, d.T = c.spec.D, c.grid.hx, c.spec.T
+    d.P, d.nsteps, d.p_begin, d.p_end = c.P, c.nsteps, 0, c.P
+    d.batch, d.K = 1, c.K
+    d.basis_rows_x, d.basis_rows_y = c.system.basis.tx.shape[0], c.system.basis.ty.shape[0]
+    d.expaction, d.krylov_m, d.flags = N.PX_EXP_CHEBYSHEV, 0, 0
+    h = ctypes.c_void_p()
+    N.check(lib, lib.px_create(ctypes.byref(d), ctypes.byref(h)))
+    try:
+        keep = [N.dptr(c.system.basis.tx), N.dptr(c.system.basis.ty), N.iptr(c.system.basis.ix),
+                N.iptr(c.system.basis.iy)]
+        N.check(lib, lib.px_set_basis(h, keep[0][0], keep[1][0], keep[2][0], keep[3][0]), h)
+        pl = plan_for(c.system.region(), c.spec.T / c.P, c.expaction)
+        be, pb = N.dptr(pl.coef_exp), N.dptr(pl.coef_phi)
+        cp = N.ChebPlanC(pl.span, pl.substeps, pl.degree, pl.center, pl.scale, pl.sigma, be[0], pb[0])
+        N.check(lib, lib.px_set_cheb_plan(h, N.PX_PLAN_SLICE, ctypes.byref(cp)), h)
+        a0, a1, a2 = (np.ascontiguousarray(x, dtype=np.float64) for x in (u0, ut, np.ravel(ctrl)))
+        N.check(lib, lib.px_set_inputs(h, a0.ctypes.data, a1.ctypes.data, a2.ctypes.data, N.PX_MEM_HOST, None), h)
+        N.check(lib, lib.px_gradient(h, None), h)
+        J = np.zeros(1)
+        grad = np.zeros(c.K)
+        N.check(lib, lib.px_get(h, N.PX_FIELD_J, J.ctypes.data, 1, N.PX_MEM_HOST, None), h)
+        N.check(lib, lib.px_get(h, N.PX_FIELD_GRAD, grad.ctypes.data, c.K, N.PX_MEM_HOST, None), h)
+    finally:
+        lib.px_destroy(h)
+    loop = direct_adjoint_loop(c.system, ctrl, ut, "linear", N=c.P, rk=RK4Config(c.dt), expaction=c.expaction,
+                               u0=u0)
+    assert J[0] == float(np.ravel(loop.J)[0])
+    assert np.array_equal(grad, np.ravel(loop.grad))
