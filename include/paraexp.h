@@ -55,7 +55,10 @@ enum {
   PX_PLAN_FROZEN = 3,       /* Burgers: slice width, frozen J(ū_p)ᵀ */
   PX_PLAN_NL_SLICE = 4,     /* Burgers iterative direct: slice width, J(ū_p) */
   PX_PLAN_NL_STEP = 5,      /* Burgers iterative direct: one RK4 step h, J(ū_p) (node recording) */
-  PX_PLAN_COUNT = 6
+  PX_PLAN_BLOCK_LONG = 6,   /* local blocks (px_set_local_blocks): slot 6 + k - 1 holds the span
+                               k·(Pl/blocks)·Δ, k = 1 … blocks - 1 (block carry -> block edge) */
+  PX_MAX_LOCAL_BLOCKS = 16,
+  PX_PLAN_COUNT = PX_PLAN_BLOCK_LONG + PX_MAX_LOCAL_BLOCKS - 1
 };
 
 /* fields for px_get / px_buffer */
@@ -132,6 +135,14 @@ int px_set_basis(void* handle, const double* tx, const double* ty, const int* ix
  * (timestepping.py:360-423) by the host planner's a-priori plan. */
 int px_set_cheb_plan(void* handle, int slot, const px_cheb_plan* plan);
 int px_set_krylov_plan(void* handle, int slot, double span, int substeps);
+
+/* Split this rank's slices into `blocks` equal contiguous blocks whose summed-chain carries
+ * run concurrently on side streams of one GPU (the multi-GPU block-scan of SURVEY.md §8(e)
+ * inside one handle: block carries meet through one long-span action each, plans in slots
+ * PX_PLAN_BLOCK_LONG + k - 1). Pays off when the exp-action kernels leave the GPU idle
+ * (Krylov, small fields). 1 = the sequential scan (default). Replaces: the reference's
+ * per-worker chains running concurrently (`workers.py:298-346`). */
+int px_set_local_blocks(void* handle, int blocks);
 
 /* Inputs: u0 (n), u_target (n), ctrl (B×K); host or device memory. Replaces the
  * q0 / q_true / f arguments of direct_adjoint_loop (optimization.py:154-169). */

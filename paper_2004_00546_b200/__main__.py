@@ -114,7 +114,7 @@ def cmd_predict(args) -> int:
     from .scaling import profile_from_timing, scaling_table
     c = _case(args.config)
     u0, ut, ctrl = c.inputs()
-    eng = ParaexpEngine(EngineSpec(c.system, c.P, c.dt, c.expaction, c.batch))
+    eng = ParaexpEngine(EngineSpec(c.system, c.P, c.dt, c.expaction, c.batch, local_blocks=1))  # per-unit costs
     eng.set_inputs(u0, ut, ctrl)
     eng.gradient()
     eng.get(0)

@@ -22,6 +22,8 @@ PX_KIND_ADVDIFF, PX_KIND_BURGERS = 0, 1
 PX_EXP_CHEBYSHEV, PX_EXP_KRYLOV = 0, 1
 PX_MEM_HOST, PX_MEM_DEVICE = 0, 1
 PX_PLAN_SLICE, PX_PLAN_LONG_DIRECT, PX_PLAN_LONG_ADJOINT, PX_PLAN_FROZEN, PX_PLAN_NL_SLICE, PX_PLAN_NL_STEP = range(6)
+PX_PLAN_BLOCK_LONG = 6
+PX_MAX_LOCAL_BLOCKS = 16
 (PX_FIELD_J, PX_FIELD_GRAD, PX_FIELD_UT, PX_FIELD_QDAG0, PX_FIELD_G, PX_FIELD_UBND,
  PX_FIELD_FROZEN_BOUNDS, PX_FIELD_VEND, PX_FIELD_WEND, PX_FIELD_TRAJ) = range(10)
 PX_FLAG_BOUNDARY_STATES = 1
@@ -99,6 +101,7 @@ SIGNATURES = {
     "px_set_basis": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double), POINTER(c_int), POINTER(c_int)]),
     "px_set_cheb_plan": (c_int, [c_void_p, c_int, POINTER(ChebPlanC)]),
     "px_set_krylov_plan": (c_int, [c_void_p, c_int, c_double, c_int]),
+    "px_set_local_blocks": (c_int, [c_void_p, c_int]),
     "px_set_inputs": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     "px_direct": (c_int, [c_void_p, c_void_p]),
     "px_finish_direct": (c_int, [c_void_p, c_void_p]),

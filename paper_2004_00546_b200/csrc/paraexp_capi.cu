@@ -87,6 +87,20 @@ struct Handle {
   std::vector<double> nl_err_host;
   // Krylov
   px::KrylovWork kw{};
+  // local blocks (px_set_local_blocks): concurrent block carries on side streams
+  struct Block {
+    double* Wk[4] = {nullptr, nullptr, nullptr, nullptr};
+    double* ACC[2] = {nullptr, nullptr};
+    px::KrylovWork kw{};
+    double* D = nullptr;   // block carry at the block edge (B × n)
+    double* Gp = nullptr;  // block φ accumulator (adjoint, B × n)
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev = nullptr;
+    int q0 = 0, q1 = 0;
+  };
+  int lb = 1;
+  std::vector<Block> blocks;
+  cudaEvent_t ev_fork = nullptr;
 
   Plan plans[PX_PLAN_COUNT];
   px_stats stats{};
@@ -820,6 +834,115 @@ int scan1d(Handle* h, bool adjoint, const double* lanes, double* out, double* pa
   return PX_OK;
 }
 
+// Point the handle's exp-action scratch (Wk, ACC, Krylov work) at a block's own buffers
+// while that block's launches are enqueued (kernels capture the pointer values).
+struct ScratchSwap {
+  Handle* h;
+  double* Wk[4];
+  double* ACC[2];
+  px::KrylovWork kw;
+  ScratchSwap(Handle* hh, const Handle::Block& b) : h(hh), kw(hh->kw) {
+    for (int i = 0; i < 4; ++i) { Wk[i] = h->Wk[i]; h->Wk[i] = b.Wk[i]; }
+    for (int i = 0; i < 2; ++i) { ACC[i] = h->ACC[i]; h->ACC[i] = b.ACC[i]; }
+    h->kw = b.kw;
+  }
+  ~ScratchSwap() {
+    for (int i = 0; i < 4; ++i) h->Wk[i] = Wk[i];
+    for (int i = 0; i < 2; ++i) h->ACC[i] = ACC[i];
+    h->kw = kw;
+  }
+};
+
+void free_blocks(Handle* h) {
+  for (auto& b : h->blocks) {
+    for (double* p : b.Wk) cudaFree(p);
+    for (double* p : b.ACC) cudaFree(p);
+    cudaFree(b.D);
+    cudaFree(b.Gp);
+    px::krylov_free(b.kw);
+    if (b.st) cudaStreamDestroy(b.st);
+    if (b.ev) cudaEventDestroy(b.ev);
+  }
+  h->blocks.clear();
+  h->lb = 1;
+}
+
+bool use_blocks(const Handle* h) {
+  return h->lb > 1 && h->dim == 2 && !(h->d.flags & PX_FLAG_BOUNDARY_STATES);
+}
+
+// Block-scan of the direct carry inside one handle: block g scans its lanes from a zero
+// carry and propagates the result to the rank's last slice edge with one long-span action
+// (slot PX_PLAN_BLOCK_LONG + (lb-1-g) - 1); the block results are summed into `out`.
+int direct_blocks(Handle* h, const double* vend, double* out, cudaStream_t s) {
+  const long long nb = (long long)h->n;
+  const long long lane_bs = (long long)h->Pl * nb;
+  PX_CUDA(h, cudaEventRecord(h->ev_fork, s));
+  for (int g = 0; g < h->lb; ++g) {
+    Handle::Block& b = h->blocks[g];
+    PX_CUDA(h, cudaStreamWaitEvent(b.st, h->ev_fork, 0));
+    ScratchSwap sw(h, b);
+    const double* D = vend + (size_t)b.q0 * h->n;
+    long long D_bs = lane_bs;
+    for (int q = b.q0 + 1; q < b.q1; ++q) {
+      double* res = nullptr;
+      PX_TRY(exp_action(h, PX_PLAN_SLICE, h->A, D, D_bs, vend + (size_t)q * h->n, lane_bs, nullptr, &res, b.st));
+      D = res;
+      D_bs = nb;
+    }
+    if (g < h->lb - 1) {
+      double* res = nullptr;
+      PX_TRY(exp_action(h, PX_PLAN_BLOCK_LONG + (h->lb - 1 - g) - 1, h->A, D, D_bs, nullptr, 0, nullptr, &res, b.st));
+      D = res;
+      D_bs = nb;
+    }
+    PX_TRY(axpby(h, b.D, nb, D, D_bs, 1.0, nullptr, 0, 0.0, b.st));
+    PX_CUDA(h, cudaEventRecord(b.ev, b.st));
+  }
+  for (int g = 0; g < h->lb; ++g) {
+    PX_CUDA(h, cudaStreamWaitEvent(s, h->blocks[g].ev, 0));
+    PX_TRY(axpby(h, out, nb, h->blocks[g].D, nb, 1.0, g == 0 ? nullptr : out, nb, g == 0 ? 0.0 : 1.0, s));
+  }
+  return PX_OK;
+}
+
+// Adjoint counterpart: block g scans its lanes backwards (φ into its own accumulator) and
+// propagates to the rank's first slice edge (slot PX_PLAN_BLOCK_LONG + g - 1); the carries
+// are summed into `out` and the φ accumulators added to `gacc`.
+int adjoint_blocks(Handle* h, const double* wend, double* out, double* gacc, cudaStream_t s) {
+  const long long nb = (long long)h->n;
+  const long long lane_bs = (long long)h->Pl * nb;
+  PX_CUDA(h, cudaEventRecord(h->ev_fork, s));
+  for (int g = 0; g < h->lb; ++g) {
+    Handle::Block& b = h->blocks[g];
+    PX_CUDA(h, cudaStreamWaitEvent(b.st, h->ev_fork, 0));
+    ScratchSwap sw(h, b);
+    PX_CUDA(h, cudaMemsetAsync(b.Gp, 0, sizeof(double) * h->B * h->n, b.st));
+    const double* C = wend + (size_t)(b.q1 - 1) * h->n;
+    long long C_bs = lane_bs;
+    for (int q = b.q1 - 2; q >= b.q0; --q) {
+      double* res = nullptr;
+      PX_TRY(exp_action(h, PX_PLAN_SLICE, h->AT, C, C_bs, wend + (size_t)q * h->n, lane_bs, b.Gp, &res, b.st));
+      C = res;
+      C_bs = nb;
+    }
+    if (g > 0) {
+      double* res = nullptr;
+      PX_TRY(exp_action(h, PX_PLAN_BLOCK_LONG + g - 1, h->AT, C, C_bs, nullptr, 0, b.Gp, &res, b.st));
+      C = res;
+      C_bs = nb;
+    }
+    PX_TRY(axpby(h, b.D, nb, C, C_bs, 1.0, nullptr, 0, 0.0, b.st));
+    PX_CUDA(h, cudaEventRecord(b.ev, b.st));
+  }
+  for (int g = 0; g < h->lb; ++g) {
+    PX_CUDA(h, cudaStreamWaitEvent(s, h->blocks[g].ev, 0));
+    PX_TRY(axpby(h, out, nb, h->blocks[g].D, nb, 1.0, g == 0 ? nullptr : out, nb, g == 0 ? 0.0 : 1.0, s));
+    PX_TRY(axpby(h, gacc, nb, gacc, nb, 1.0, h->blocks[g].Gp, nb, 1.0, s));
+  }
+  return PX_OK;
+}
+
 int direct_linear(Handle* h, cudaStream_t s) {
   const long long nb = (long long)h->n;
   const long long lane_bs = (long long)h->Pl * nb;  // stride between batch members in lanes
@@ -840,6 +963,16 @@ int direct_linear(Handle* h, cudaStream_t s) {
   const long long ubs = (long long)(h->d.P + 1) * nb;
   if (bnd) {
     PX_TRY(axpby(h, h->UBND, ubs, h->u0, 0, 1.0, nullptr, 0, 0.0, s));
+  }
+  if (use_blocks(h)) {
+    PX_TRY(direct_blocks(h, vend, h->UT, s));
+    if (h->d.p_end < h->d.P) {
+      double* res = nullptr;
+      PX_TRY(exp_action(h, PX_PLAN_LONG_DIRECT, h->A, h->UT, nb, nullptr, 0, nullptr, &res, s));
+      PX_TRY(axpby(h, h->UT, nb, res, nb, 1.0, nullptr, 0, 0.0, s));
+    }
+    tend(h, tm, s);
+    return PX_OK;
   }
   // summed-chain carry over the local block
   const double* D = vend;  // lane p0 of each member
@@ -879,6 +1012,19 @@ int adjoint_linear(Handle* h, cudaStream_t s) {
   PX_CHECK_LAUNCH(h);
   if (use_scan1d(h)) {
     PX_TRY(scan1d(h, true, wend, h->QDAG0, h->G, h->d.p_begin > 0 ? PX_PLAN_LONG_ADJOINT : -1, s));
+    tend(h, tm, s);
+    tm = tbegin(h, PX_PHASE_OTHER, s);
+    PX_TRY(project(h, h->GRAD, h->G, nb, 1.0, 0.0, s));
+    tend(h, tm, s);
+    return PX_OK;
+  }
+  if (use_blocks(h)) {
+    PX_TRY(adjoint_blocks(h, wend, h->QDAG0, h->G, s));
+    if (h->d.p_begin > 0) {
+      double* res = nullptr;
+      PX_TRY(exp_action(h, PX_PLAN_LONG_ADJOINT, h->AT, h->QDAG0, nb, nullptr, 0, h->G, &res, s));
+      PX_TRY(axpby(h, h->QDAG0, nb, res, nb, 1.0, nullptr, 0, 0.0, s));
+    }
     tend(h, tm, s);
     tm = tbegin(h, PX_PHASE_OTHER, s);
     PX_TRY(project(h, h->GRAD, h->G, nb, 1.0, 0.0, s));
@@ -1063,6 +1209,8 @@ void px_destroy(void* handle) {
   if (h->ev_out) cudaEventDestroy(h->ev_out);
   for (auto e : h->event_pool) cudaEventDestroy(e);
   px::krylov_free(h->kw);
+  free_blocks(h);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   delete h;
 }
 
@@ -1123,6 +1271,42 @@ int px_set_krylov_plan(void* handle, int slot, double span, int substeps) {
   pl.span = span;
   pl.substeps = substeps;
   pl.degree = h->d.krylov_m;
+  return PX_OK;
+}
+
+int px_set_local_blocks(void* handle, int blocks) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (h) cudaSetDevice(h->device);
+  if (!h) return fail(h, PX_ERR_ARG, "null handle");
+  if (blocks < 1 || blocks > PX_MAX_LOCAL_BLOCKS || blocks > h->Pl || h->Pl % blocks != 0)
+    return fail(h, PX_ERR_ARG, "local blocks must divide the rank's slice count (1 … 16)");
+  if (blocks == h->lb) return PX_OK;
+  free_blocks(h);
+  h->graph_valid = false;
+  if (blocks == 1) return PX_OK;
+  if (!h->ev_fork) PX_CUDA(h, cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+  const size_t Bn = (size_t)h->B * h->n;
+  const int per = h->Pl / blocks;
+  h->blocks.resize(blocks);
+  for (int g = 0; g < blocks; ++g) {
+    Handle::Block& b = h->blocks[g];
+    b.q0 = g * per;
+    b.q1 = (g + 1) * per;
+    for (auto& p : b.Wk) PX_CUDA(h, cudaMalloc(&p, sizeof(double) * Bn));
+    for (auto& p : b.ACC) PX_CUDA(h, cudaMalloc(&p, sizeof(double) * Bn));
+    PX_CUDA(h, cudaMalloc(&b.D, sizeof(double) * Bn));
+    PX_CUDA(h, cudaMalloc(&b.Gp, sizeof(double) * Bn));
+    if (h->d.expaction == PX_EXP_KRYLOV) {
+      std::string err;
+      if (px::krylov_alloc(b.kw, h->d.krylov_m, h->n, h->B, &err) != PX_OK) {
+        free_blocks(h);
+        return fail(h, PX_ERR_NOMEM, err);
+      }
+    }
+    PX_CUDA(h, cudaStreamCreateWithFlags(&b.st, cudaStreamNonBlocking));
+    PX_CUDA(h, cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming));
+  }
+  h->lb = blocks;
   return PX_OK;
 }
 

@@ -74,6 +74,7 @@ class EngineSpec:
     nl_eps: float = 1e-3
     nl_max_iter: int = 25
     nl_min_iter: int = 2
+    local_blocks: int = 0       # 0: automatic (concurrent block carries for Krylov); 1: sequential scan
 
     @property
     def nsteps(self) -> int:
@@ -184,6 +185,33 @@ class ParaexpEngine:
                 self._set_plan(N.PX_PLAN_LONG_DIRECT, self._plan(region, (spec.P - p1) * delta))
             if p0 > 0:
                 self._set_plan(N.PX_PLAN_LONG_ADJOINT, self._plan(region, p0 * delta))
+            lb = self._local_blocks(p1 - p0)
+            if lb > 1:
+                per = (p1 - p0) // lb
+                for k in range(1, lb):
+                    self._set_plan(N.PX_PLAN_BLOCK_LONG + k - 1, self._plan(region, k * per * delta))
+                N.check(self.lib, self.lib.px_set_local_blocks(self.h, lb), self.h)
+            self.local_blocks = lb
+
+    def _local_blocks(self, Pl: int) -> int:
+        """Concurrent block carries inside this GPU (`px_set_local_blocks`). Automatic: 4
+        blocks for the Krylov path (its Arnoldi kernels are latency-bound and leave the GPU
+        mostly idle, and a Krylov long span costs ≈ 1/8 of the slices it spans); the
+        Chebyshev march already fills the GPU and stays sequential. PX_LOCAL_BLOCKS overrides."""
+        import os
+        spec = self.spec
+        env = os.environ.get("PX_LOCAL_BLOCKS")
+        want = int(env) if env else spec.local_blocks
+        if os.environ.get("PX_KRYLOV_COOP") == "1":
+            return 1  # concurrent cooperative grids could not all be co-resident
+        if want == 0:
+            want = 4 if isinstance(spec.expaction, KrylovConfig) else 1
+        if self.spec.system.grid.dim != 2 or spec.boundary_states:
+            return 1
+        want = max(1, min(want, N.PX_MAX_LOCAL_BLOCKS, Pl))
+        while want > 1 and Pl % want:
+            want -= 1
+        return want
 
     # -- plans ---------------------------------------------------------------
 

@@ -131,9 +131,23 @@ def test_config3_burgers_full():
 
 
 def test_config4_krylov_scaled():
+    """Krylov path: by default the carries run as 4 concurrent local blocks (in-GPU
+    block-scan, `px_set_local_blocks`) — equal to the oracle's 4-block block-scan."""
     from paper_2004_00546_b200 import baseline, scaled
     c = scaled(baseline(4), nx=96, P=12, steps_per_slice=5, K=16)
-    _check(_gpu_linear(c), _oracle_linear(c))
+    _check(_gpu_linear(c), _oracle_linear(c, world=4))
+
+
+@pytest.mark.parametrize("blocks", [1, 3])
+def test_local_blocks_chebyshev(blocks, monkeypatch):
+    """Concurrent local block carries for the Chebyshev march (forced): the sequential scan
+    for 1 block, the oracle's block-scan for 3."""
+    from paper_2004_00546_b200 import baseline, release_engines, scaled
+    release_engines()
+    monkeypatch.setenv("PX_LOCAL_BLOCKS", str(blocks))
+    c = scaled(baseline(5), nx=96, P=12, steps_per_slice=8, K=16)
+    _check(_gpu_linear(c), _oracle_linear(c, world=blocks))
+    release_engines()
 
 
 def test_config5_scaled():
@@ -327,7 +341,7 @@ def test_config4_krylov_cooperative_kernel():
             "c = scaled(baseline(4), nx=96, P=12, steps_per_slice=5, K=16); _check(_gpu_linear(c), _oracle_linear(c))")
     from tests.conftest import ROOT
     import os
-    env = dict(os.environ, PX_KRYLOV_COOP="1")
+    env = dict(os.environ, PX_KRYLOV_COOP="1")  # (forces one local block)
     r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
 
