@@ -241,4 +241,69 @@ __global__ void __launch_bounds__(256) k_project_cols(double* grad, const double
   }
 }
 
+// ---------------------------------------------------------------------------
+// Closed-form adjoint ∫ for circulant (periodic, constant-coefficient) operators:
+//   Σ_{k<n} h·S(hM)·y_k = M⁻¹(y_n − n·b)   (from y_{k+1} − y_k = hM·S(hM)·y_k + b, y_0 = 0)
+// on the non-constant Fourier modes; the constant mode (M·1 = 0) has y_k = k·b̄, hence
+// h·b̄·n(n−1)/2. One FFT solve per gradient replaces a per-step, per-lane accumulator.
+// ---------------------------------------------------------------------------
+
+// f[b][i] = (Σ_p lanes[b·Pl + p][i] − nscale·b[b][i], 0)
+__global__ void k_zsrc_cplx(double2* f, const double* lanes, int lanes_per_b, const double* bsrc, double nscale,
+                            size_t n) {
+  const int b = blockIdx.y;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double* src = lanes + (size_t)b * lanes_per_b * n + i;
+    double r = 0.0;
+    for (int p = 0; p < lanes_per_b; ++p) r += src[(size_t)p * n];
+    f[(size_t)b * n + i] = make_double2(r - nscale * bsrc[(size_t)b * n + i], 0.0);
+  }
+}
+
+// f̂(kx, ky) /= n·λ(kx, ky), λ = cc + ce·e^{iθx} + cw·e^{−iθx} + cn·e^{iθy} + cs·e^{−iθy}
+// (the stencil's eigenvalues; θ = 2πk/N, cuFFT's forward sign); the constant mode -> 0
+__global__ void k_circ_solve(double2* f, Stencil5 st, int nx, int ny, int B) {
+  const size_t n = (size_t)nx * ny;
+  const double inv_n = 1.0 / (double)n;
+  const double two_pi = 6.283185307179586476925286766559;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n * B;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t i = idx % n;
+    const int kx = (int)(i % nx), ky = (int)(i / nx);
+    if (kx == 0 && ky == 0) {
+      f[idx] = make_double2(0.0, 0.0);
+      continue;
+    }
+    double sx, cx, sy, cy;
+    sincos(two_pi * kx / nx, &sx, &cx);
+    sincos(two_pi * ky / ny, &sy, &cy);
+    const double lr = st.cc + (st.ce + st.cw) * cx + (st.cn + st.cs) * cy;
+    const double li = (st.ce - st.cw) * sx + (st.cn - st.cs) * sy;
+    const double den = (lr * lr + li * li) * (double)n;
+    const double2 v = f[idx];
+    // v / λ = v·conj(λ) / |λ|², and the inverse transform's 1/n
+    f[idx] = make_double2((v.x * lr + v.y * li) / den, (v.y * lr - v.x * li) / den);
+    (void)inv_n;
+  }
+}
+
+// G[b][i] = Re f[b][i] + cscale·c[b][i] + kconst·bsum[b]
+__global__ void k_z_finish(double* G, const double2* f, const double* c, double cscale, const double* bsum,
+                           double kconst, size_t n) {
+  const int b = blockIdx.y;
+  const double kb = kconst * bsum[b];
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    G[(size_t)b * n + i] = f[(size_t)b * n + i].x + cscale * c[(size_t)b * n + i] + kb;
+}
+
+// partial[b][blk] = Σ_{i in blk's grid-stride set} x[b][i]
+__global__ void __launch_bounds__(256) k_sum_partial(double* partial, const double* x, size_t n) {
+  __shared__ double red[8];
+  const int b = blockIdx.y;
+  double v = 0.0;
+  for (size_t i = (size_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (size_t)gridDim.x * 256) v += x[(size_t)b * n + i];
+  v = block_sum<256>(v, red);
+  if (threadIdx.x == 0) partial[(size_t)b * gridDim.x + blockIdx.x] = v;
+}
+
 }  // namespace px

@@ -14,6 +14,7 @@
 //   outputs: u(T), J, q†(0), G = ∫q†dt, grad_k = ⟨φ_k, G⟩.
 // Everything is enqueued on the caller's stream; no host synchronisation.
 #include <cuda_runtime.h>
+#include <cufft.h>
 
 #include <algorithm>
 #include <cmath>
@@ -69,6 +70,11 @@ struct Handle {
   double *bsrc = nullptr, *cz = nullptr;  // h·S(hM)·g and h²·U(hM)·g (RK4 Horner constants)
   bool z_valid = false;
   double *Y0 = nullptr, *Y1 = nullptr, *Z = nullptr;
+  // closed-form adjoint ∫ (2D circulant operator): Σ_p z_p = (Aᵀ)⁻¹(Σ_p y_n,p − Pl·n·b) + …
+  bool z_closed = false;
+  cufftHandle fft = 0;
+  double2* fbuf = nullptr;  // B × n complex
+  double* bsum = nullptr;   // B: Σ_i b[b][i]
   const double *vend = nullptr, *wend = nullptr;
   // exp-action work
   double* Wk[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -335,6 +341,9 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
     PX_CHECK_LAUNCH(h);
     cur = h->Y0;
   } else {
+    // adjoint lanes without the ∫ accumulator when it is recovered in closed form
+    // afterwards (z_closed: Σ_k h·S(hAᵀ)y_k = (Aᵀ)⁻¹(y_n − n·b), one FFT solve per gradient)
+    const bool zlanes = adjoint && !h->z_closed;
     if (h->dim == 2 && (nx & 1)) return fail(h, PX_ERR_ARG, "2D grids need an even nx");
     px::MarchArgs a{};
     a.b = h->bsrc; a.z = h->Z; a.st = st; a.h = hs;
@@ -370,16 +379,16 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
       auto launch2 = [&]() -> int {
 #define PX_M2(NT, DEP, MB, TM, ...)                                                                            \
   do {                                                                                                     \
-    const size_t sm = px::march2_smem<NT, DEP>(adjoint);                                                   \
+    const size_t sm = px::march2_smem<NT, DEP>(zlanes);                                                   \
     static bool attr[2] = {false, false};                                                                  \
-    if (!attr[adjoint]) {                                                                                  \
-      if (adjoint) PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march2<true, NT, DEP, MB, TM, ##__VA_ARGS__>,                \
+    if (!attr[zlanes]) {                                                                                  \
+      if (zlanes) PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march2<true, NT, DEP, MB, TM, ##__VA_ARGS__>,                \
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
       else PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march2<false, NT, DEP, MB, TM, ##__VA_ARGS__>,                       \
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));         \
-      attr[adjoint] = true;                                                                                \
+      attr[zlanes] = true;                                                                                \
     }                                                                                                      \
-    if (adjoint) px::k_rk4_march2<true, NT, DEP, MB, TM, ##__VA_ARGS__><<<blocks, NT, sm, s>>>(a);                        \
+    if (zlanes) px::k_rk4_march2<true, NT, DEP, MB, TM, ##__VA_ARGS__><<<blocks, NT, sm, s>>>(a);                        \
     else px::k_rk4_march2<false, NT, DEP, MB, TM, ##__VA_ARGS__><<<blocks, NT, sm, s>>>(a);                               \
   } while (0)
         static const int m2_tma = [] { const char* e = getenv("PX_M2_TMA"); return e ? atoi(e) : 1; }();
@@ -412,14 +421,14 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
           b1.band_rows = std::min(ny, 256);
           b1.nbands = (ny + b1.band_rows - 1) / b1.band_rows;
           const unsigned blk1 = (unsigned)((size_t)h->L * b1.nstrips * b1.nbands);
-          const size_t sm1 = px::march_smem(adjoint);
+          const size_t sm1 = px::march_smem(zlanes);
           static bool attr1 = false;
           if (!attr1) {
             PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)px::march_smem(true)));
             PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)px::march_smem(false)));
             attr1 = true;
           }
-          if (adjoint) px::k_rk4_march<true><<<blk1, px::MARCH_NT, sm1, s>>>(b1);
+          if (zlanes) px::k_rk4_march<true><<<blk1, px::MARCH_NT, sm1, s>>>(b1);
           else px::k_rk4_march<false><<<blk1, px::MARCH_NT, sm1, s>>>(b1);
           st_i += 1;
         }
@@ -427,7 +436,7 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
         cur = out;
       }
       launched_steps = nsteps - 1;
-      h->z_valid = adjoint;
+      h->z_valid = zlanes;
     } else {
     if (nx <= px::MARCH_MAX_CW) {
       a.strip_w = nx; a.halo = 0; a.nstrips = 1;
@@ -442,28 +451,28 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
     a.band_rows = br;
     a.nbands = (ny + br - 1) / br;
     const unsigned blocks = (unsigned)((size_t)h->L * a.nstrips * a.nbands);
-    const size_t smem = px::march_smem(adjoint);
+    const size_t smem = px::march_smem(zlanes);
     static bool attr_done[2] = {false, false};
-    if (!attr_done[adjoint]) {
-      if (adjoint) PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (!attr_done[zlanes]) {
+      if (zlanes) PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       else PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_done[adjoint] = true;
+      attr_done[zlanes] = true;
     }
     for (int st_i = 1; st_i < nsteps; ++st_i) {
       double* out = (cur == h->Y0) ? h->Y1 : h->Y0;
       a.y_in = cur;
       a.y_out = out;
       a.z_zero = (st_i == 1);
-      if (adjoint) px::k_rk4_march<true><<<blocks, px::MARCH_NT, smem, s>>>(a);
+      if (zlanes) px::k_rk4_march<true><<<blocks, px::MARCH_NT, smem, s>>>(a);
       else px::k_rk4_march<false><<<blocks, px::MARCH_NT, smem, s>>>(a);
       PX_CHECK_LAUNCH(h);
       cur = out;
     }
     launched_steps = nsteps - 1;
-    h->z_valid = adjoint;
+    h->z_valid = zlanes;
     }
   }
-  const double bytes_per_point = adjoint ? 40.0 : 24.0;  // y, b, y' (+ z in/out)
+  const double bytes_per_point = (adjoint && !h->z_closed) ? 40.0 : 24.0;  // y, b, y' (+ z in/out)
   h->stats.rk4_lane_steps += (uint64_t)h->L * launched_steps;
   // algorithmic bytes per launch: y, b, y_out (+ z in/out) once per point, whether the
   // launch advances one step or two
@@ -996,6 +1005,36 @@ int direct_linear(Handle* h, cudaStream_t s) {
   return PX_OK;
 }
 
+// G partial <- Σ_p z_p without per-lane accumulators (circulant 2D operator):
+// Σ_p z_p = (Aᵀ)⁻¹₀(Σ_p w_n,p − Pl·n·b) + Pl·n·c + Pl·h·b̄·n(n−1)/2, the pseudo-inverse on the
+// non-constant Fourier modes by one batched Z2Z FFT solve (kernels.cuh, k_circ_solve).
+int z_closed_form(Handle* h, const double* wend, cudaStream_t s) {
+  const double hs = (h->d.T / h->d.P) / h->d.nsteps;
+  const double ns = (double)h->d.nsteps;
+  const dim3 gs = grid_stride(h->n, h->B);
+  px::k_zsrc_cplx<<<gs, 256, 0, s>>>(h->fbuf, wend, h->Pl, h->bsrc, (double)h->Pl * ns, h->n);
+  PX_CHECK_LAUNCH(h);
+  px::k_sum_partial<<<dim3(h->red_blocks, h->B), 256, 0, s>>>(h->partial, h->bsrc, h->n);
+  PX_CHECK_LAUNCH(h);
+  px::k_finalize_sum<<<h->B, 256, 0, s>>>(h->bsum, h->partial, h->red_blocks, 1.0, nullptr);
+  PX_CHECK_LAUNCH(h);
+  if (cufftSetStream(h->fft, s) != CUFFT_SUCCESS ||
+      cufftExecZ2Z(h->fft, reinterpret_cast<cufftDoubleComplex*>(h->fbuf),
+                   reinterpret_cast<cufftDoubleComplex*>(h->fbuf), CUFFT_FORWARD) != CUFFT_SUCCESS)
+    return fail(h, PX_ERR_CUDA, "cufft forward failed");
+  px::k_circ_solve<<<(unsigned)std::min<size_t>((h->n * h->B + 255) / 256, 148 * 16), 256, 0, s>>>(
+      h->fbuf, h->AT, h->d.nx, h->d.ny, h->B);
+  PX_CHECK_LAUNCH(h);
+  if (cufftExecZ2Z(h->fft, reinterpret_cast<cufftDoubleComplex*>(h->fbuf),
+                   reinterpret_cast<cufftDoubleComplex*>(h->fbuf), CUFFT_INVERSE) != CUFFT_SUCCESS)
+    return fail(h, PX_ERR_CUDA, "cufft inverse failed");
+  const double kconst = (double)h->Pl * hs * ns * (ns - 1.0) / 2.0 / (double)h->n;
+  px::k_z_finish<<<gs, 256, 0, s>>>(h->G, h->fbuf, h->cz, (double)h->Pl * ns, h->bsum, kconst, h->n);
+  PX_CHECK_LAUNCH(h);
+  h->stats.kernel_launches += 2;  // the two cuFFT executions
+  return PX_OK;
+}
+
 int adjoint_linear(Handle* h, cudaStream_t s) {
   const long long nb = (long long)h->n;
   const long long lane_bs = (long long)h->Pl * nb;
@@ -1006,10 +1045,14 @@ int adjoint_linear(Handle* h, cudaStream_t s) {
   h->wend = wend;
   tm = tbegin(h, PX_PHASE_EXP_ADJOINT, s);
   // G partial <- Σ_p z_p  (z_p = Σ_steps h·w3 + nsteps·c)
-  px::k_lane_sum_plus<<<grid_stride(h->n, h->B), 256, 0, s>>>(h->G, h->Z, h->Pl, h->cz,
-                                                              (double)h->Pl * h->d.nsteps, h->n,
-                                                              h->z_valid ? 1 : 0);
-  PX_CHECK_LAUNCH(h);
+  if (h->z_closed) {
+    PX_TRY(z_closed_form(h, wend, s));
+  } else {
+    px::k_lane_sum_plus<<<grid_stride(h->n, h->B), 256, 0, s>>>(h->G, h->Z, h->Pl, h->cz,
+                                                                (double)h->Pl * h->d.nsteps, h->n,
+                                                                h->z_valid ? 1 : 0);
+    PX_CHECK_LAUNCH(h);
+  }
   if (use_scan1d(h)) {
     PX_TRY(scan1d(h, true, wend, h->QDAG0, h->G, h->d.p_begin > 0 ? PX_PLAN_LONG_ADJOINT : -1, s));
     tend(h, tm, s);
@@ -1162,7 +1205,20 @@ int px_create(const px_problem_desc* desc, void** out_handle) {
     A(&h->cz, B * n);
     A(&h->Y0, (size_t)h->L * n);
     A(&h->Y1, (size_t)h->L * n);
-    A(&h->Z, (size_t)h->L * n);
+    // 2D: the adjoint ∫ in closed form (one FFT solve), no per-lane accumulator in HBM
+    static const bool z_accum = [] { const char* e = getenv("PX_Z_ACCUM"); return e && atoi(e) != 0; }();
+    h->z_closed = h->dim == 2 && !z_accum;
+    if (h->z_closed) {
+      A(reinterpret_cast<double**>(&h->fbuf), 2 * B * n);
+      A(&h->bsum, B);
+      int dims[2] = {d.ny, d.nx};
+      if (rc == PX_OK && cufftPlanMany(&h->fft, 2, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2Z, (int)B) != CUFFT_SUCCESS) {
+        g_last_error = "cufftPlanMany failed";
+        rc = PX_ERR_CUDA;
+      }
+    } else {
+      A(&h->Z, (size_t)h->L * n);
+    }
     if ((d.flags & PX_FLAG_BOUNDARY_STATES) && d.p_begin == 0 && d.p_end == d.P)
       A(&h->UBND, B * (size_t)(d.P + 1) * n);
   } else {
@@ -1209,6 +1265,7 @@ void px_destroy(void* handle) {
   if (h->ev_out) cudaEventDestroy(h->ev_out);
   for (auto e : h->event_pool) cudaEventDestroy(e);
   px::krylov_free(h->kw);
+  if (h->fft) cufftDestroy(h->fft);
   free_blocks(h);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   delete h;
