@@ -361,8 +361,10 @@ def main():
     m2 = "k_rk4_march2<{},128,3,3,tma>"
     kernel_name = {"rk4_direct": (m2.format("false") if fused else "k_rk4_march<false>") if two_d
                    else "k_rk4_lane1d<false>",
-                   "rk4_adjoint": (m2.format("true") if fused else "k_rk4_march<true>") if two_d
-                   else "k_rk4_lane1d<true>",
+                   # 2D adjoint lanes run the direct kernel: their ∫ is recovered in closed form
+                   # (one cuFFT solve, `z_closed_form`) instead of a per-lane accumulator
+                   "rk4_adjoint": (m2.format("false") + " (adjoint lanes)" if fused else "k_rk4_march<false>")
+                   if two_d else "k_rk4_lane1d<true>",
                    "exp_direct": "k_cheb_march<M>" if two_d else "k_scan1d",
                    "exp_adjoint": "k_cheb_march<M>+phi" if two_d else "k_scan1d+phi",
                    "other": "reductions/projection"}[dom]
