@@ -358,12 +358,15 @@ def main():
     two_d = c.grid.dim == 2
     # two RK4 steps per launch (k_rk4_march2) when the phase launched fewer kernels than steps
     fused = two_d and ph["launches"] / args.steps < (c.nsteps - 1) * 0.75
-    m2 = "k_rk4_march2<{},128,3,3,tma>"
-    kernel_name = {"rk4_direct": (m2.format("false") if fused else "k_rk4_march<false>") if two_d
+    # (the library's default variant: three columns per thread, 64-thread CTAs, in strip
+    # mode; PX_M2_COLS=2 selects the two-column k_rk4_march2)
+    cols = int(os.environ.get("PX_M2_COLS", "3"))
+    m2 = "k_rk4_marchc<3,64,3,4>" if cols == 3 and c.grid.nx > 192 else "k_rk4_march2<false,128,3,3,tma>"
+    kernel_name = {"rk4_direct": (m2 if fused else "k_rk4_march<false>") if two_d
                    else "k_rk4_lane1d<false>",
                    # 2D adjoint lanes run the direct kernel: their ∫ is recovered in closed form
                    # (one cuFFT solve, `z_closed_form`) instead of a per-lane accumulator
-                   "rk4_adjoint": (m2.format("false") + " (adjoint lanes)" if fused else "k_rk4_march<false>")
+                   "rk4_adjoint": (m2 + " (adjoint lanes)" if fused else "k_rk4_march<false>")
                    if two_d else "k_rk4_lane1d<true>",
                    "exp_direct": "k_cheb_march<M>" if two_d else "k_scan1d",
                    "exp_adjoint": "k_cheb_march<M>+phi" if two_d else "k_scan1d+phi",

@@ -361,15 +361,27 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
     if (m2_mode && nsteps >= 3 && (m2_mode == 2 || (double)h->L * (double)h->n >= 268435456.0)) {
       // two steps per launch: halo 8 (one column per stage and side)
       static const int m2_var = [] { const char* e = getenv("PX_M2_VAR"); return e ? atoi(e) : 3; }();
+      static const int m2_cols = [] { const char* e = getenv("PX_M2_COLS"); return e ? atoi(e) : 3; }();
       const int m2_nt = m2_var == 2 ? 192 : 128;
       const int cw_max = 2 * m2_nt;
-      if (nx <= cw_max) {
+      // NC columns per thread (k_rk4_marchc): direct lanes, strip mode
+      const int mc_nc = (!zlanes && m2_cols >= 3) ? m2_cols : 0;
+      static const int mc_var = [] { const char* e = getenv("PX_MC_VAR"); return e ? atoi(e) : 3; }();
+      const int mc_nt = mc_var == 3 ? 64 : (mc_nc == 4 ? 96 : 128);
+      if (mc_nc && nx > mc_nc * mc_nt) {
+        a.halo = 8;
+        const int maxu = mc_nc * mc_nt - 16;
+        const int ns = (nx + maxu - 1) / maxu;
+        a.strip_w = (((nx + ns - 1) / ns) + 1) & ~1;
+        a.nstrips = (nx + a.strip_w - 1) / a.strip_w;
+      } else if (nx <= cw_max) {
         a.strip_w = nx; a.halo = 0; a.nstrips = 1;
       } else {
         a.halo = 8; a.strip_w = cw_max - 16;
         a.nstrips = (nx + a.strip_w - 1) / a.strip_w;
       }
-      static const int m2_band = [] { const char* e = getenv("PX_M2_BAND"); return e ? atoi(e) : 512; }();
+      static const int m2_band_env = [] { const char* e = getenv("PX_M2_BAND"); return e ? atoi(e) : 0; }();
+      const int m2_band = m2_band_env ? m2_band_env : (mc_nc ? 1024 : 512);
       // bands of rows (16 rows of pipeline fill each): ≥ 4 waves at 2 CTAs/SM, ≥ 128 rows per band
       int br = std::min(ny, m2_band);
       while (br > 128 && (size_t)h->L * a.nstrips * ((ny + br - 1) / br) < 4 * 3 * 148) br = (br + 1) / 2;
@@ -391,6 +403,28 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
     if (zlanes) px::k_rk4_march2<true, NT, DEP, MB, TM, ##__VA_ARGS__><<<blocks, NT, sm, s>>>(a);                        \
     else px::k_rk4_march2<false, NT, DEP, MB, TM, ##__VA_ARGS__><<<blocks, NT, sm, s>>>(a);                               \
   } while (0)
+#define PX_MC(NC, NT, DEP, MB)                                                                                \
+  do {                                                                                                     \
+    const size_t sm = px::marchc_smem<NC, NT, DEP>();                                                     \
+    static bool attr = false;                                                                              \
+    if (!attr) {                                                                                           \
+      PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_marchc<NC, NT, DEP, MB>,                                    \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));              \
+      attr = true;                                                                                         \
+    }                                                                                                      \
+    px::k_rk4_marchc<NC, NT, DEP, MB><<<blocks, NT, sm, s>>>(a);                                          \
+  } while (0)
+        if (a.halo > 0 && mc_nc == 3) {
+          if (mc_var == 3) PX_MC(3, 64, 3, 4);  // default: 4 CTAs of 2 warps per SM
+          else PX_MC(3, 128, 3, 2);
+          return PX_OK;
+        }
+        if (a.halo > 0 && mc_nc == 4) {
+          if (mc_var == 3) PX_MC(4, 64, 3, 4);
+          else PX_MC(4, 96, 3, 2);
+          return PX_OK;
+        }
+#undef PX_MC
         static const int m2_tma = [] { const char* e = getenv("PX_M2_TMA"); return e ? atoi(e) : 1; }();
         if (m2_var == 2) PX_M2(192, 3, 2, false);  // 2 CTAs/SM
         else if (m2_tma == 1) PX_M2(128, 3, 3, true, true);  // 3 CTAs/SM, TMA row ring, h·w3 in registers (default)

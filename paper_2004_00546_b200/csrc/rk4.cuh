@@ -654,6 +654,219 @@ __global__ void __launch_bounds__(M2_NT, MINB) k_rk4_march2(MarchArgs a) {
   if constexpr (!TMA) cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------------------
+// k_rk4_marchc: the two-step march with NC (≥ 3) contiguous columns per thread.
+// The x-neighbour exchange moves 16 B out and 16 B in per thread and stage
+// whatever NC is, so its shared-memory bytes per point fall as 2/NC — the
+// limiter of the two-column kernel (≈ 70% of its LSU wavefronts). Direct lanes
+// only (no ∫ accumulator: the 2D adjoint integral is recovered in closed form),
+// strip mode only (halo 8), TMA row ring of y(r), b(r−4), b(r−8).
+// ---------------------------------------------------------------------------
+template <int NC>
+struct ColV {
+  double v[NC];
+};
+
+template <int NC, int NT, int DEP, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
+  constexpr int NQ = 3;
+  constexpr int RW = NT * NC;  // ring row width (doubles)
+  using V = ColV<NC>;
+  extern __shared__ double dynd[];
+  double* ring = dynd;                                                        // [DEP][NQ][RW]
+  double (*pubE)[8][NT] = reinterpret_cast<double (*)[8][NT]>(ring + DEP * NQ * RW);
+  double (*pubO)[8][NT] = pubE + 2;
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(pubE + 4);  // [DEP]
+
+  const int lane = blockIdx.x % a.lanes;
+  const int rest = blockIdx.x / a.lanes;
+  const int strip = rest % a.nstrips;
+  const int band = rest / a.nstrips;
+  const int nx = a.nx, ny = a.ny;
+  const size_t n = (size_t)nx * ny;
+  const int x0 = strip * a.strip_w;
+  const int U = min(a.strip_w, nx - x0);
+  const int CW = U + 2 * a.halo;
+  const int t = threadIdx.x;
+  const int T = (CW + NC - 1) / NC;
+  const int tl = t == 0 ? 0 : t - 1;
+  const int tr = t + 1 >= T ? T - 1 : t + 1;
+  const int j0 = band * a.band_rows;
+  const int rows_out = min(a.band_rows, ny - j0);
+  const int iters = rows_out + 16;
+  const int c0 = NC * t;                                  // first strip column of this thread
+  const int gxs = (((x0 - a.halo + c0) % nx) + nx) % nx;  // its global column (no wrap inside a thread's run: nx % 2 == 0, runs are checked below)
+
+  auto stage = [&](auto jc, const V& base, const V& c, const V& so, const V& nn, double l, double r) -> V {
+    constexpr int j = decltype(jc)::value;
+    V o;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      const double e = q + 1 < NC ? c.v[q + 1] : r;
+      const double w = q > 0 ? c.v[q - 1] : l;
+      double x = fma(a.kc[j][0], c.v[q], base.v[q]);
+      x = fma(a.kc[j][1], e, x);
+      x = fma(a.kc[j][2], w, x);
+      x = fma(a.kc[j][3], so.v[q], x);
+      o.v[q] = fma(a.kc[j][4], nn.v[q], x);
+    }
+    return o;
+  };
+  auto vadd = [](const V& x, const V& y) {
+    V o;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) o.v[q] = x.v[q] + y.v[q];
+    return o;
+  };
+  const size_t member = (size_t)(lane / a.lanes_per_b);
+  const double* __restrict__ bsrc = a.b + member * n;
+  const double* __restrict__ ysrc = a.y_in ? a.y_in + (size_t)lane * n : bsrc;
+  double* __restrict__ yout = a.y_out + (size_t)lane * n;
+
+  auto wrapr = [&](int row) -> int {
+    row %= ny;
+    return row < 0 ? row + ny : row;
+  };
+  const int r0 = j0 - 8;
+  int iss_k = 0, iss_slot = 0;
+  int ry = wrapr(r0), rb4 = wrapr(r0 - 4), rb8 = wrapr(r0 - 8);
+  const int gx0 = (((x0 - a.halo) % nx) + nx) % nx;
+  const int lenA = min(CW, nx - gx0);
+  const unsigned row_bytes = (unsigned)CW * 8u;
+  auto issue = [&]() {
+    if (t == 0 && iss_k < iters) {
+      double* slot = ring + (size_t)iss_slot * NQ * RW;
+      unsigned long long* bar = mbar + iss_slot;
+      mbar_expect_tx(bar, row_bytes * (unsigned)NQ);
+      const double* rows[3] = {ysrc + (size_t)ry * nx, bsrc + (size_t)rb4 * nx, bsrc + (size_t)rb8 * nx};
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        double* dst = slot + q * RW;
+        bulk_g2s(dst, rows[q] + gx0, (unsigned)lenA * 8u, bar);
+        if (lenA < CW) bulk_g2s(dst + lenA, rows[q], (unsigned)(CW - lenA) * 8u, bar);
+      }
+    }
+    ++iss_k;
+    iss_slot = (iss_slot + 1 == DEP) ? 0 : iss_slot + 1;
+    ry = (ry + 1 == ny) ? 0 : ry + 1;
+    rb4 = (rb4 + 1 == ny) ? 0 : rb4 + 1;
+    rb8 = (rb8 + 1 == ny) ? 0 : rb8 + 1;
+  };
+  if (t == 0) {
+    for (int k = 0; k < DEP; ++k) mbar_init(mbar + k, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < DEP; ++k) issue();
+  int rslot = 0;
+  unsigned rphase = 0;
+  int rs = wrapr(r0 - 8);
+  // columns of this thread that are written back: strip columns [halo, CW − halo)
+  bool st_ok[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) st_ok[q] = (c0 + q >= a.halo) && (c0 + q < CW - a.halo);
+  int gxq[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) gxq[q] = (gxs + q) % nx;
+
+  V yq[6], pq[6];
+  V wq[8][2];
+#pragma unroll
+  for (int k = 0; k < 6; ++k)
+#pragma unroll
+    for (int q = 0; q < NC; ++q) yq[k].v[q] = pq[k].v[q] = 0.0;
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+#pragma unroll
+    for (int q = 0; q < NC; ++q) wq[s][0].v[q] = wq[s][1].v[q] = 0.0;
+
+  auto iter = [&](auto kc, auto gc, const int i) {
+    constexpr int k = decltype(kc)::value;
+    constexpr bool G = decltype(gc)::value;
+    const int pin = (k + 1) & 1, pout = k & 1;
+    const int po = k & 1, pp = (k + 1) & 1;
+    mbar_wait(mbar + rslot, rphase);
+    const double* slot = ring + (size_t)rslot * NQ * RW;
+    rslot = (rslot + 1 == DEP) ? 0 : rslot + 1;
+    if (rslot == 0) rphase ^= 1u;
+    V yr, b4, b8;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      yr.v[q] = slot[c0 + q];
+      b4.v[q] = slot[RW + c0 + q];
+      b8.v[q] = slot[2 * RW + c0 + q];
+    }
+    yq[k] = yr;
+    const V& y0 = yq[(k + 2) % 6];
+    const V& y1 = yq[(k + 3) % 6];
+    const V& y2 = yq[(k + 4) % 6];
+    const V& y3 = yq[(k + 5) % 6];
+    V nw[9];
+    if (G) {
+#pragma unroll
+      for (int s = 0; s < 9; ++s)
+#pragma unroll
+        for (int q = 0; q < NC; ++q) nw[s].v[q] = 0.0;
+    }
+    if (!G || i >= 2) nw[1] = stage(IC<0>{}, y3, y3, y2, yr, pubO[pin][0][tl], pubE[pin][0][tr]);
+    if (!G || i >= 4) nw[2] = stage(IC<1>{}, y2, wq[1][pp], wq[1][po], nw[1], pubO[pin][1][tl], pubE[pin][1][tr]);
+    if (!G || i >= 6) nw[3] = stage(IC<2>{}, y1, wq[2][pp], wq[2][po], nw[2], pubO[pin][2][tl], pubE[pin][2][tr]);
+    if (!G || i >= 8) nw[4] = stage(IC<3>{}, vadd(y0, b4), wq[3][pp], wq[3][po], nw[3], pubO[pin][3][tl], pubE[pin][3][tr]);
+    pq[(k + 2) % 6] = nw[4];
+    const V& p5 = pq[(k + 1) % 6];
+    const V& p6 = pq[k % 6];
+    const V& p7 = pq[(k + 5) % 6];
+    const V& p8 = pq[(k + 4) % 6];
+    if (!G || i >= 10) nw[5] = stage(IC<0>{}, p5, p5, p6, nw[4], pubO[pin][4][tl], pubE[pin][4][tr]);
+    if (!G || i >= 12) nw[6] = stage(IC<1>{}, p6, wq[5][pp], wq[5][po], nw[5], pubO[pin][5][tl], pubE[pin][5][tr]);
+    if (!G || i >= 14) nw[7] = stage(IC<2>{}, p7, wq[6][pp], wq[6][po], nw[6], pubO[pin][6][tl], pubE[pin][6][tr]);
+    if (!G || i >= 16) {
+      const V yn = stage(IC<3>{}, vadd(p8, b8), wq[7][pp], wq[7][po], nw[7], pubO[pin][7][tl], pubE[pin][7][tr]);
+      double* orow = yout + (size_t)rs * nx;
+#pragma unroll
+      for (int q = 0; q < NC; ++q)
+        if (st_ok[q]) __stcs(orow + gxq[q], yn.v[q]);
+    }
+    rs = (rs + 1 == ny) ? 0 : rs + 1;
+#pragma unroll
+    for (int s = 1; s <= 7; ++s)
+      if (s != 4) wq[s][po] = nw[s];
+    pubE[pout][0][t] = yr.v[0];     pubO[pout][0][t] = yr.v[NC - 1];
+#pragma unroll
+    for (int s = 1; s <= 7; ++s) {
+      pubE[pout][s][t] = nw[s].v[0];
+      pubO[pout][s][t] = nw[s].v[NC - 1];
+    }
+    __syncthreads();
+    if (t == 0) fence_proxy_async_smem();
+    issue();
+  };
+  int i0 = 0;
+  for (; i0 < 18; i0 += 6) {
+    if (i0 + 6 > iters) break;
+    iter(IC<0>{}, BC<true>{}, i0); iter(IC<1>{}, BC<true>{}, i0 + 1); iter(IC<2>{}, BC<true>{}, i0 + 2);
+    iter(IC<3>{}, BC<true>{}, i0 + 3); iter(IC<4>{}, BC<true>{}, i0 + 4); iter(IC<5>{}, BC<true>{}, i0 + 5);
+  }
+  if (i0 >= 18) {
+    for (; i0 + 6 <= iters; i0 += 6) {
+      iter(IC<0>{}, BC<false>{}, i0); iter(IC<1>{}, BC<false>{}, i0 + 1); iter(IC<2>{}, BC<false>{}, i0 + 2);
+      iter(IC<3>{}, BC<false>{}, i0 + 3); iter(IC<4>{}, BC<false>{}, i0 + 4); iter(IC<5>{}, BC<false>{}, i0 + 5);
+    }
+  }
+  if (i0 + 0 < iters) iter(IC<0>{}, BC<true>{}, i0);
+  if (i0 + 1 < iters) iter(IC<1>{}, BC<true>{}, i0 + 1);
+  if (i0 + 2 < iters) iter(IC<2>{}, BC<true>{}, i0 + 2);
+  if (i0 + 3 < iters) iter(IC<3>{}, BC<true>{}, i0 + 3);
+  if (i0 + 4 < iters) iter(IC<4>{}, BC<true>{}, i0 + 4);
+  if (i0 + 5 < iters) iter(IC<5>{}, BC<true>{}, i0 + 5);
+}
+
+template <int NC, int NT, int DEP>
+inline size_t marchc_smem() {
+  return (size_t)DEP * 3 * NT * NC * sizeof(double) + 4 * 8 * NT * sizeof(double) + DEP * sizeof(unsigned long long);
+}
+
 template <int M2_NT, int M2_DEPTH>
 inline size_t march2_smem(bool adj) {
   return (size_t)M2_DEPTH * (adj ? 4 : 3) * M2_NT * sizeof(double2) + 4 * 8 * M2_NT * sizeof(double) +

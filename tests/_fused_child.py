@@ -22,6 +22,7 @@ def main() -> int:
         dict(nx=12, P=2, steps_per_slice=7, K=4),     # rows < pipeline depth: bands wrap the torus
         dict(nx=300, P=4, steps_per_slice=11, K=8),   # strips (VAR 3: 240/368 useful columns), partial last
         dict(nx=640, P=8, steps_per_slice=11, K=16),  # several strips + odd remainder
+        dict(nx=1026, P=2, steps_per_slice=6, K=8, T=0.05), # uneven strips of the 3-/4-column kernels
     ]
     for kw in cases:
         c = scaled(baseline(5), **kw)

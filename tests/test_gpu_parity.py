@@ -408,19 +408,20 @@ def test_nonlinear_full_config3_converges_to_serial():
                             u0=u0, eps=1e-14, max_iter=2)
 
 
-@pytest.mark.parametrize("var", ["3", "2"])
-def test_fused_two_step_march_forced(var):
-    """k_rk4_march2 (two RK4 steps per launch) forced on small/odd shapes in a child
-    process (the kernel choice is read from the environment once per process)."""
+@pytest.mark.parametrize("var,cols", [("3", "2"), ("2", "2"), ("3", "3"), ("3", "4")])
+def test_fused_two_step_march_forced(var, cols):
+    """k_rk4_march2 / k_rk4_marchc (two RK4 steps per launch; 2, 3 or 4 columns per
+    thread) forced on small/odd shapes in a child process (the kernel choice is read
+    from the environment once per process)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PX_MARCH2="2", PX_M2_VAR=var)
+    env = dict(os.environ, PX_MARCH2="2", PX_M2_VAR=var, PX_M2_COLS=cols)
     r = subprocess.run([sys.executable, os.path.join(root, "tests", "_fused_child.py")], env=env, cwd=root,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
-    assert r.stdout.count("ok ") == 5
+    assert r.stdout.count("ok ") == 6
 
 
 def test_full_config5_every_lane_vs_oracle_rk4():
