@@ -361,7 +361,7 @@ def main():
     # (the library's default variant: three columns per thread, 64-thread CTAs, in strip
     # mode; PX_M2_COLS=2 selects the two-column k_rk4_march2)
     cols = int(os.environ.get("PX_M2_COLS", "3"))
-    m2 = "k_rk4_marchc<3,64,3,4>" if cols == 3 and c.grid.nx > 192 else "k_rk4_march2<false,128,3,3,tma>"
+    m2 = "k_rk4_marchc<3,64,3,4,br>" if cols == 3 and c.grid.nx > 192 else "k_rk4_march2<false,128,3,3,tma>"
     kernel_name = {"rk4_direct": (m2 if fused else "k_rk4_march<false>") if two_d
                    else "k_rk4_lane1d<false>",
                    # 2D adjoint lanes run the direct kernel: their ∫ is recovered in closed form

@@ -366,8 +366,8 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
       const int cw_max = 2 * m2_nt;
       // NC columns per thread (k_rk4_marchc): direct lanes, strip mode
       const int mc_nc = (!zlanes && m2_cols >= 3) ? m2_cols : 0;
-      static const int mc_var = [] { const char* e = getenv("PX_MC_VAR"); return e ? atoi(e) : 3; }();
-      const int mc_nt = mc_var == 3 ? 64 : (mc_nc == 4 ? 96 : 128);
+      static const int mc_var = [] { const char* e = getenv("PX_MC_VAR"); return e ? atoi(e) : 6; }();
+      const int mc_nt = mc_var >= 3 ? 64 : (mc_nc == 4 ? 96 : 128);
       if (mc_nc && nx > mc_nc * mc_nt) {
         a.halo = 8;
         const int maxu = mc_nc * mc_nt - 16;
@@ -403,19 +403,23 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
     if (zlanes) px::k_rk4_march2<true, NT, DEP, MB, TM, ##__VA_ARGS__><<<blocks, NT, sm, s>>>(a);                        \
     else px::k_rk4_march2<false, NT, DEP, MB, TM, ##__VA_ARGS__><<<blocks, NT, sm, s>>>(a);                               \
   } while (0)
-#define PX_MC(NC, NT, DEP, MB)                                                                                \
+#define PX_MC(NC, NT, DEP, MB, ...)                                                                           \
   do {                                                                                                     \
     const size_t sm = px::marchc_smem<NC, NT, DEP>();                                                     \
     static bool attr = false;                                                                              \
     if (!attr) {                                                                                           \
-      PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_marchc<NC, NT, DEP, MB>,                                    \
+      PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_marchc<NC, NT, DEP, MB, ##__VA_ARGS__>,                     \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));              \
       attr = true;                                                                                         \
     }                                                                                                      \
-    px::k_rk4_marchc<NC, NT, DEP, MB><<<blocks, NT, sm, s>>>(a);                                          \
+    px::k_rk4_marchc<NC, NT, DEP, MB, ##__VA_ARGS__><<<blocks, NT, sm, s>>>(a);                           \
   } while (0)
         if (a.halo > 0 && mc_nc == 3) {
-          if (mc_var == 3) PX_MC(3, 64, 3, 4);  // default: 4 CTAs of 2 warps per SM
+          // default (6): 4 CTAs of 2 warps per SM, b(r−8) from a register ring (two TMA
+          // streams), slots refilled after the barrier without a proxy fence (write-after-read
+          // only: the generic-proxy reads of the slot are complete at the barrier)
+          if (mc_var == 6) PX_MC(3, 64, 3, 4, true, false);
+          else if (mc_var == 3) PX_MC(3, 64, 3, 4);  // three streams, proxy fence
           else PX_MC(3, 128, 3, 2);
           return PX_OK;
         }

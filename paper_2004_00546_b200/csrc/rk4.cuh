@@ -667,9 +667,11 @@ struct ColV {
   double v[NC];
 };
 
-template <int NC, int NT, int DEP, int MINB>
+template <int NC, int NT, int DEP, int MINB, bool BR = false, bool PF = true>
 __global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
-  constexpr int NQ = 3;
+  // BR: b(r−8) from a register ring of b(r−4) rows (two streams instead of three)
+  // PF: proxy fence before refilling a slot
+  constexpr int NQ = BR ? 2 : 3;
   constexpr int RW = NT * NC;  // ring row width (doubles)
   using V = ColV<NC>;
   extern __shared__ double dynd[];
@@ -738,7 +740,7 @@ __global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
       double* slot = ring + (size_t)iss_slot * NQ * RW;
       unsigned long long* bar = mbar + iss_slot;
       mbar_expect_tx(bar, row_bytes * (unsigned)NQ);
-      const double* rows[3] = {ysrc + (size_t)ry * nx, bsrc + (size_t)rb4 * nx, bsrc + (size_t)rb8 * nx};
+      const double* rows[3] = {ysrc + (size_t)ry * nx, bsrc + (size_t)rb4 * nx, bsrc + (size_t)rb8 * nx};  // (BR: first two)
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         double* dst = slot + q * RW;
@@ -771,11 +773,16 @@ __global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
   for (int q = 0; q < NC; ++q) gxq[q] = (gxs + q) % nx;
 
   V yq[6], pq[6];
+  V bq[BR ? 6 : 1];  // BR: b(r−4) of the last six iterations
   V wq[8][2];
 #pragma unroll
   for (int k = 0; k < 6; ++k)
 #pragma unroll
     for (int q = 0; q < NC; ++q) yq[k].v[q] = pq[k].v[q] = 0.0;
+#pragma unroll
+  for (int k = 0; k < (BR ? 6 : 1); ++k)
+#pragma unroll
+    for (int q = 0; q < NC; ++q) bq[k].v[q] = 0.0;
 #pragma unroll
   for (int s = 0; s < 8; ++s)
 #pragma unroll
@@ -795,7 +802,11 @@ __global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
     for (int q = 0; q < NC; ++q) {
       yr.v[q] = slot[c0 + q];
       b4.v[q] = slot[RW + c0 + q];
-      b8.v[q] = slot[2 * RW + c0 + q];
+      if constexpr (!BR) b8.v[q] = slot[2 * RW + c0 + q];
+    }
+    if constexpr (BR) {
+      bq[k] = b4;
+      b8 = bq[(k + 2) % 6];  // b4 of iteration i − 4 = b(r − 8)
     }
     yq[k] = yr;
     const V& y0 = yq[(k + 2) % 6];
@@ -839,7 +850,7 @@ __global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
       pubO[pout][s][t] = nw[s].v[NC - 1];
     }
     __syncthreads();
-    if (t == 0) fence_proxy_async_smem();
+    if (PF && t == 0) fence_proxy_async_smem();
     issue();
   };
   int i0 = 0;
@@ -864,6 +875,7 @@ __global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
 
 template <int NC, int NT, int DEP>
 inline size_t marchc_smem() {
+  // (sized for three streams; the BR variant uses two)
   return (size_t)DEP * 3 * NT * NC * sizeof(double) + 4 * 8 * NT * sizeof(double) + DEP * sizeof(unsigned long long);
 }
 
