@@ -388,7 +388,7 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
       a.band_rows = br;
       a.nbands = (ny + a.band_rows - 1) / a.band_rows;
       const unsigned blocks = (unsigned)((size_t)h->L * a.nstrips * a.nbands);
-      auto launch2 = [&]() -> int {
+      auto launch2 = [&](bool one_step) -> int {
 #define PX_M2(NT, DEP, MB, TM, ...)                                                                            \
   do {                                                                                                     \
     const size_t sm = px::march2_smem<NT, DEP>(zlanes);                                                   \
@@ -403,29 +403,31 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
     if (zlanes) px::k_rk4_march2<true, NT, DEP, MB, TM, ##__VA_ARGS__><<<blocks, NT, sm, s>>>(a);                        \
     else px::k_rk4_march2<false, NT, DEP, MB, TM, ##__VA_ARGS__><<<blocks, NT, sm, s>>>(a);                               \
   } while (0)
-#define PX_MC(NC, NT, DEP, MB, ...)                                                                           \
+#define PX_MC(NC, NT, DEP, MB, BR, PF, ...)                                                                   \
   do {                                                                                                     \
-    const size_t sm = px::marchc_smem<NC, NT, DEP>();                                                     \
+    const size_t sm = px::marchc_smem<NC, NT, DEP>(BR);                                                   \
     static bool attr = false;                                                                              \
     if (!attr) {                                                                                           \
-      PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_marchc<NC, NT, DEP, MB, ##__VA_ARGS__>,                     \
+      PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_marchc<NC, NT, DEP, MB, BR, PF, ##__VA_ARGS__>,             \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));              \
       attr = true;                                                                                         \
     }                                                                                                      \
-    px::k_rk4_marchc<NC, NT, DEP, MB, ##__VA_ARGS__><<<blocks, NT, sm, s>>>(a);                           \
+    px::k_rk4_marchc<NC, NT, DEP, MB, BR, PF, ##__VA_ARGS__><<<blocks, NT, sm, s>>>(a);                   \
   } while (0)
         if (a.halo > 0 && mc_nc == 3) {
           // default (6): 4 CTAs of 2 warps per SM, b(r−8) from a register ring (two TMA
           // streams), slots refilled after the barrier without a proxy fence (write-after-read
           // only: the generic-proxy reads of the slot are complete at the barrier)
-          if (mc_var == 6) PX_MC(3, 64, 3, 4, true, false);
-          else if (mc_var == 3) PX_MC(3, 64, 3, 4);  // three streams, proxy fence
-          else PX_MC(3, 128, 3, 2);
+          if (mc_var == 6) {
+            if (one_step) PX_MC(3, 64, 3, 4, false, false, false);  // odd remainder step
+            else PX_MC(3, 64, 3, 4, true, false);
+          } else if (mc_var == 3) PX_MC(3, 64, 3, 4, false, true);  // three streams, proxy fence
+          else PX_MC(3, 128, 3, 2, false, true);
           return PX_OK;
         }
         if (a.halo > 0 && mc_nc == 4) {
-          if (mc_var == 3) PX_MC(4, 64, 3, 4);
-          else PX_MC(4, 96, 3, 2);
+          if (mc_var >= 3) PX_MC(4, 64, 3, 4, false, true);
+          else PX_MC(4, 96, 3, 2, false, true);
           return PX_OK;
         }
 #undef PX_MC
@@ -446,8 +448,11 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
         a.y_out = out;
         a.z_zero = (st_i == 1);
         if (nsteps - st_i >= 2) {
-          PX_TRY(launch2());
+          PX_TRY(launch2(false));
           st_i += 2;
+        } else if (a.halo > 0 && mc_nc == 3 && mc_var == 6) {
+          PX_TRY(launch2(true));  // the three-column kernel, one step
+          st_i += 1;
         } else {
           px::MarchArgs b1 = a;  // odd remainder: one single-step launch
           if (nx <= px::MARCH_MAX_CW) {

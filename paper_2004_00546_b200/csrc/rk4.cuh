@@ -667,11 +667,13 @@ struct ColV {
   double v[NC];
 };
 
-template <int NC, int NT, int DEP, int MINB, bool BR = false, bool PF = true>
+template <int NC, int NT, int DEP, int MINB, bool BR = false, bool PF = true, bool S2 = true>
 __global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
   // BR: b(r−8) from a register ring of b(r−4) rows (two streams instead of three)
   // PF: proxy fence before refilling a slot
-  constexpr int NQ = BR ? 2 : 3;
+  // S2: two RK4 steps per launch; otherwise one (the odd remainder step of a sweep)
+  constexpr int NQ = (BR || !S2) ? 2 : 3;
+  constexpr int LAG = S2 ? 8 : 4;  // pipeline depth in rows (output row r − LAG)
   constexpr int RW = NT * NC;  // ring row width (doubles)
   using V = ColV<NC>;
   extern __shared__ double dynd[];
@@ -695,7 +697,7 @@ __global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
   const int tr = t + 1 >= T ? T - 1 : t + 1;
   const int j0 = band * a.band_rows;
   const int rows_out = min(a.band_rows, ny - j0);
-  const int iters = rows_out + 16;
+  const int iters = rows_out + 2 * LAG;
   const int c0 = NC * t;                                  // first strip column of this thread
   const int gxs = (((x0 - a.halo + c0) % nx) + nx) % nx;  // its global column (no wrap inside a thread's run: nx % 2 == 0, runs are checked below)
 
@@ -729,7 +731,7 @@ __global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
     row %= ny;
     return row < 0 ? row + ny : row;
   };
-  const int r0 = j0 - 8;
+  const int r0 = j0 - LAG;
   int iss_k = 0, iss_slot = 0;
   int ry = wrapr(r0), rb4 = wrapr(r0 - 4), rb8 = wrapr(r0 - 8);
   const int gx0 = (((x0 - a.halo) % nx) + nx) % nx;
@@ -763,7 +765,7 @@ __global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
   for (int k = 0; k < DEP; ++k) issue();
   int rslot = 0;
   unsigned rphase = 0;
-  int rs = wrapr(r0 - 8);
+  int rs = wrapr(r0 - LAG);
   // columns of this thread that are written back: strip columns [halo, CW − halo)
   bool st_ok[NC];
 #pragma unroll
@@ -802,9 +804,9 @@ __global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
     for (int q = 0; q < NC; ++q) {
       yr.v[q] = slot[c0 + q];
       b4.v[q] = slot[RW + c0 + q];
-      if constexpr (!BR) b8.v[q] = slot[2 * RW + c0 + q];
+      if constexpr (NQ == 3) b8.v[q] = slot[2 * RW + c0 + q];
     }
-    if constexpr (BR) {
+    if constexpr (BR && S2) {
       bq[k] = b4;
       b8 = bq[(k + 2) % 6];  // b4 of iteration i − 4 = b(r − 8)
     }
@@ -824,6 +826,14 @@ __global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
     if (!G || i >= 4) nw[2] = stage(IC<1>{}, y2, wq[1][pp], wq[1][po], nw[1], pubO[pin][1][tl], pubE[pin][1][tr]);
     if (!G || i >= 6) nw[3] = stage(IC<2>{}, y1, wq[2][pp], wq[2][po], nw[2], pubO[pin][2][tl], pubE[pin][2][tr]);
     if (!G || i >= 8) nw[4] = stage(IC<3>{}, vadd(y0, b4), wq[3][pp], wq[3][po], nw[3], pubO[pin][3][tl], pubE[pin][3][tr]);
+    if constexpr (!S2) {
+      if (!G || i >= 8) {  // y⁺ at row r − 4
+        double* orow = yout + (size_t)rs * nx;
+#pragma unroll
+        for (int q = 0; q < NC; ++q)
+          if (st_ok[q]) __stcs(orow + gxq[q], nw[4].v[q]);
+      }
+    } else {
     pq[(k + 2) % 6] = nw[4];
     const V& p5 = pq[(k + 1) % 6];
     const V& p6 = pq[k % 6];
@@ -839,13 +849,14 @@ __global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
       for (int q = 0; q < NC; ++q)
         if (st_ok[q]) __stcs(orow + gxq[q], yn.v[q]);
     }
+    }  // S2
     rs = (rs + 1 == ny) ? 0 : rs + 1;
 #pragma unroll
-    for (int s = 1; s <= 7; ++s)
+    for (int s = 1; s <= (S2 ? 7 : 3); ++s)
       if (s != 4) wq[s][po] = nw[s];
     pubE[pout][0][t] = yr.v[0];     pubO[pout][0][t] = yr.v[NC - 1];
 #pragma unroll
-    for (int s = 1; s <= 7; ++s) {
+    for (int s = 1; s <= (S2 ? 7 : 3); ++s) {
       pubE[pout][s][t] = nw[s].v[0];
       pubO[pout][s][t] = nw[s].v[NC - 1];
     }
@@ -854,12 +865,13 @@ __global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
     issue();
   };
   int i0 = 0;
-  for (; i0 < 18; i0 += 6) {
+  constexpr int FILL = S2 ? 18 : 12;  // guarded groups until every stage is live (i ≥ 2·LAG)
+  for (; i0 < FILL; i0 += 6) {
     if (i0 + 6 > iters) break;
     iter(IC<0>{}, BC<true>{}, i0); iter(IC<1>{}, BC<true>{}, i0 + 1); iter(IC<2>{}, BC<true>{}, i0 + 2);
     iter(IC<3>{}, BC<true>{}, i0 + 3); iter(IC<4>{}, BC<true>{}, i0 + 4); iter(IC<5>{}, BC<true>{}, i0 + 5);
   }
-  if (i0 >= 18) {
+  if (i0 >= FILL) {
     for (; i0 + 6 <= iters; i0 += 6) {
       iter(IC<0>{}, BC<false>{}, i0); iter(IC<1>{}, BC<false>{}, i0 + 1); iter(IC<2>{}, BC<false>{}, i0 + 2);
       iter(IC<3>{}, BC<false>{}, i0 + 3); iter(IC<4>{}, BC<false>{}, i0 + 4); iter(IC<5>{}, BC<false>{}, i0 + 5);
@@ -874,9 +886,9 @@ __global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
 }
 
 template <int NC, int NT, int DEP>
-inline size_t marchc_smem() {
-  // (sized for three streams; the BR variant uses two)
-  return (size_t)DEP * 3 * NT * NC * sizeof(double) + 4 * 8 * NT * sizeof(double) + DEP * sizeof(unsigned long long);
+inline size_t marchc_smem(bool br) {
+  return (size_t)DEP * (br ? 2 : 3) * NT * NC * sizeof(double) + 4 * 8 * NT * sizeof(double) +
+         DEP * sizeof(unsigned long long);
 }
 
 template <int M2_NT, int M2_DEPTH>
