@@ -54,7 +54,10 @@ struct CmRing {  // acc/pacc row slots (≥ M live rows; UN % R == 0)
   static constexpr int value = (M <= 3) ? M : (M == 4 ? 4 : 6);
 };
 
-template <int M>
+// SG: the recurrence sign σ (±1) as a compile-time constant (0: runtime a.sigma);
+// TM: row ring filled by 1D bulk copies (TMA engine) issued by one thread and completing
+// on per-slot mbarriers, refilled after the row barrier; otherwise per-thread cp.async.
+template <int M, int SG = 0, bool TM = false>
 __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) {
   __shared__ double pubE[2][M][CM_NT];
   __shared__ double pubO[2][M][CM_NT];
@@ -90,6 +93,12 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
   const bool write_u = a.out_cur != nullptr;
 
   const double sig = a.sigma;
+  auto sgm = [&](double v) -> double {
+    if constexpr (SG == 1) return v;
+    else if constexpr (SG == -1) return -v;
+    else return sig * v;
+  };
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(cm_ring + (size_t)CM_DEPTH * 4 * CM_NT);
   const double* __restrict__ cur = a.u_cur + b * a.cur_bs;
   const double* __restrict__ prv = first ? cur : a.u_prev + b * a.prev_bs;
   const double* __restrict__ accin = has_add ? a.addend + b * a.add_bs : a.acc + (size_t)b * n;
@@ -107,23 +116,51 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
   const size_t coloff = (size_t)gx;
   int iss_k = 0, iss_slot = 0;
   int rc = wrapr(r0), rl = wrapr(r0 - 1);  // streams: cur row r, lagged rows r−1
+  const int gx0 = (((x0 - a.halo) % nx) + nx) % nx;
+  const int lenA = min(CW, nx - gx0);  // columns before the periodic wrap
+  const unsigned row_bytes = (unsigned)CW * 8u;
   auto issue = [&]() {
-    if (iss_k < iters) {
+    if constexpr (TM) {
+      if (t == 0 && iss_k < iters) {
+        double* sl = reinterpret_cast<double*>(cm_ring + (size_t)iss_slot * 4 * CM_NT);
+        unsigned long long* bar = mbar + iss_slot;
+        const double* rows[4] = {cur + (size_t)rc * nx, prv + (size_t)rl * nx, accin + (size_t)rl * nx,
+                                 has_p ? pac + (size_t)rl * nx : nullptr};
+        const bool use[4] = {true, !first, read_acc, has_p};
+        mbar_expect_tx(bar, row_bytes * (unsigned)(1 + (!first) + read_acc + has_p));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (use[q]) {
+            double* dst = sl + q * 2 * CM_NT;
+            bulk_g2s(dst, rows[q] + gx0, (unsigned)lenA * 8u, bar);
+            if (lenA < CW) bulk_g2s(dst + lenA, rows[q], (unsigned)(CW - lenA) * 8u, bar);
+          }
+        }
+      }
+    } else if (iss_k < iters) {
       double2* sl = cm_ring + (size_t)iss_slot * 4 * CM_NT;
       cp_async16(sl + t, cur + (size_t)rc * nx + coloff);
       if (!first) cp_async16(sl + CM_NT + t, prv + (size_t)rl * nx + coloff);
       if (read_acc) cp_async16(sl + 2 * CM_NT + t, accin + (size_t)rl * nx + coloff);
       if (has_p) cp_async16(sl + 3 * CM_NT + t, pac + (size_t)rl * nx + coloff);
     }
-    cp_async_commit();
+    if constexpr (!TM) cp_async_commit();
     ++iss_k;
     iss_slot = (iss_slot + 1 == CM_DEPTH) ? 0 : iss_slot + 1;
     rc = (rc + 1 == ny) ? 0 : rc + 1;
     rl = (rl + 1 == ny) ? 0 : rl + 1;
   };
+  if constexpr (TM) {
+    if (t == 0) {
+      for (int k = 0; k < CM_DEPTH; ++k) mbar_init(mbar + k, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+  }
 #pragma unroll
   for (int k = 0; k < CM_DEPTH; ++k) issue();
   int rslot = 0;
+  unsigned rphase = 0;
   int rs = wrapr(r0 - M);  // output row r − M
 
   double2 q0[3];               // U_k rows (ring by phase mod 3)
@@ -157,14 +194,16 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
     constexpr bool G = decltype(gc)::value;
       const int pin = (k + 1) & 1;
       const int pout = k & 1;
-      cp_async_wait<CM_DEPTH - 1>();
+      if constexpr (TM) mbar_wait(mbar + rslot, rphase);
+      else cp_async_wait<CM_DEPTH - 1>();
       const double2* sl = cm_ring + (size_t)rslot * 4 * CM_NT;
       rslot = (rslot + 1 == CM_DEPTH) ? 0 : rslot + 1;
+      if (TM && rslot == 0) rphase ^= 1u;
       const double2 ur = sl[t];
       const double2 upv = first ? make_double2(0.0, 0.0) : sl[CM_NT + t];
       const double2 ain = read_acc ? sl[2 * CM_NT + t] : make_double2(0.0, 0.0);
       const double2 pin_v = has_p ? sl[3 * CM_NT + t] : make_double2(0.0, 0.0);
-      issue();
+      if constexpr (!TM) issue();
       q0[k % 3] = ur;
       const double2 u0m2 = q0[(k + 1) % 3], u0m1 = q0[(k + 2) % 3];  // rows r−2, r−1
       const int po = k & 1, pp = (k + 1) & 1;  // qs[s][po]: row of iteration i−2, [pp]: i−1
@@ -181,7 +220,7 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
           pc.x = pin_v.x + (a.bp[0] * u0m1.x + a.bp[1] * u1.x);
           pc.y = pin_v.y + (a.bp[0] * u0m1.y + a.bp[1] * u1.y);
         } else {
-          u1 = term(a.g, make_double2(sig * upv.x, sig * upv.y), u0m1, u0m2, ur, l, r);
+          u1 = term(a.g, make_double2(sgm(upv.x), sgm(upv.y)), u0m1, u0m2, ur, l, r);
           acc = make_double2(ain.x + a.be[1] * u1.x, ain.y + a.be[1] * u1.y);
           pc = make_double2(pin_v.x + a.bp[1] * u1.x, pin_v.y + a.bp[1] * u1.y);
         }
@@ -199,7 +238,7 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
           const double2 c = qs[s - 1][pp];        // row r−s
           const double2 so = qs[s - 1][po];       // row r−s−1
           const double2 pv = (s == 2) ? u0m2 : qs[s - 2][po];  // U_{k+s−2} at row r−s
-          const double2 u = term(a.g, make_double2(sig * pv.x, sig * pv.y), c, so, nq[s - 1], l, r);
+          const double2 u = term(a.g, make_double2(sgm(pv.x), sgm(pv.y)), c, so, nq[s - 1], l, r);
           nq[s] = u;
           const int ai = (k - s + 1 + 2 * R) % R;  // acc slot of row r−s
           qa[ai].x += a.be[s] * u.x;
@@ -233,6 +272,7 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
         }
       }
       __syncthreads();
+      if constexpr (TM) issue();  // every thread has read this iteration's slot: refill it
   };
   int i0 = 0;
   // fill (stages switch on at i = 2, 4, …, 2M) — guarded groups until every stage is live
@@ -270,9 +310,9 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
     if (i0 + 10 < iters) iter(IC<10>{}, BC<true>{}, i0 + 10);
     if (i0 + 11 < iters) iter(IC<11>{}, BC<true>{}, i0 + 11);
   }
-  cp_async_wait<0>();
+  if constexpr (!TM) cp_async_wait<0>();
 }
 
-constexpr size_t CM_SMEM = (size_t)CM_DEPTH * 4 * CM_NT * sizeof(double2);
+constexpr size_t CM_SMEM = (size_t)CM_DEPTH * 4 * CM_NT * sizeof(double2) + CM_DEPTH * sizeof(unsigned long long);
 
 }  // namespace px

@@ -533,17 +533,26 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
 
 
 // 2D: Chebyshev action by row-marching passes of up to CM_MAXT fused terms (cheb_march.cuh)
-template <int M>
-int launch_cm(Handle* h, const px::ChebMarchArgs& a, unsigned blocks, cudaStream_t s) {
+template <int M, int SG, bool TM>
+int launch_cm_v(Handle* h, const px::ChebMarchArgs& a, unsigned blocks, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    PX_CUDA(h, cudaFuncSetAttribute(px::k_cheb_march<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PX_CUDA(h, cudaFuncSetAttribute(px::k_cheb_march<M, SG, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)px::CM_SMEM));
     attr = true;
   }
-  px::k_cheb_march<M><<<blocks, px::CM_NT, px::CM_SMEM, s>>>(a);
+  px::k_cheb_march<M, SG, TM><<<blocks, px::CM_NT, px::CM_SMEM, s>>>(a);
   PX_CHECK_LAUNCH(h);
   return PX_OK;
+}
+// σ = ±1 as a template constant; PX_CM_VAR: 1 per-thread cp.async ring (default), 0 TMA row
+// ring (measured 15% slower here: one-thread issue after the row barrier, short bands)
+template <int M>
+int launch_cm(Handle* h, const px::ChebMarchArgs& a, unsigned blocks, cudaStream_t s) {
+  static const int var = [] { const char* e = getenv("PX_CM_VAR"); return e ? atoi(e) : 1; }();
+  const bool neg = a.sigma < 0;
+  if (var == 0) return neg ? launch_cm_v<M, -1, true>(h, a, blocks, s) : launch_cm_v<M, 1, true>(h, a, blocks, s);
+  return neg ? launch_cm_v<M, -1, false>(h, a, blocks, s) : launch_cm_v<M, 1, false>(h, a, blocks, s);
 }
 
 int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const double* src, long long src_bs,
@@ -578,7 +587,7 @@ int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const d
   if (nx <= 2 * px::CM_NT && env_strip == 0) {
     a.strip_w = nx; a.halo = 0; a.nstrips = 1;
   } else {
-    a.halo = cm_terms;  // ≥ the terms of any pass
+    a.halo = (cm_terms + 1) & ~1;  // ≥ the terms of any pass; even (16-byte aligned row segments)
     if (env_strip > 0) {
       a.strip_w = env_strip;
     } else {  // fewest strips of ≤ 2·CM_NT computed columns, useful widths balanced (even)
