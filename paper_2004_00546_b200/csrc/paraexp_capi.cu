@@ -517,10 +517,11 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
   }
   const double bytes_per_point = (adjoint && !h->z_closed) ? 40.0 : 24.0;  // y, b, y' (+ z in/out)
   h->stats.rk4_lane_steps += (uint64_t)h->L * launched_steps;
-  // algorithmic bytes per launch: y, b, y_out (+ z in/out) once per point, whether the
-  // launch advances one step or two
-  const double bytes = bytes_per_point * (double)h->n * h->L *
-                       (double)(fused_launches >= 0 ? (uint64_t)fused_launches : launched_steps);
+  // algorithmic bytes: 24n (40n with the ∫ accumulator) per lane and RK4
+  // step — per step also when one launch advances two steps (the fused launch streams
+  // y, b, y_out once for both, i.e. half the model's bytes: temporal blocking)
+  (void)fused_launches;
+  const double bytes = bytes_per_point * (double)h->n * h->L * (double)launched_steps;
   h->stats.rk4_bytes += bytes;
   h->stats.algorithmic_bytes += bytes;
   *final_out = cur;
@@ -650,10 +651,9 @@ int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const d
         default: rc = launch_cm<6>(h, a, blocks, s); break;
       }
       if (rc != PX_OK) return rc;
-      // algorithmic bytes of the pass (streams read + written once)
-      const int nrd = 1 + (first ? 0 : 1) + ((!first || a.addend) ? 1 : 0) + (pacc ? 1 : 0);
-      const int nwr = 1 + (pacc ? 1 : 0) + (last ? 0 : 2);
-      const double bytes = 8.0 * (nrd + nwr) * (double)n * B;
+      // algorithmic bytes: 40n per Chebyshev term (+16n with the φ₁
+      // accumulator); the fused pass streams its arrays once for all M terms
+      const double bytes = (pacc ? 56.0 : 40.0) * (double)n * B * (double)M;  // Σ M = degree
       h->stats.exp_bytes += bytes;
       h->stats.algorithmic_bytes += bytes;
       uprev = o0; uprev_bs = nb;
