@@ -22,6 +22,13 @@
 // whole periodic row when nx ≤ 576); bands of rows add 8 pipeline-fill rows.
 // HBM traffic ≈ 24n per step (y, b in; y⁺ out) + 16n with z.
 //
+// Two-step kernels (k_rk4_march2, k_rk4_marchc): the same march with the 8 Horner
+// stages of two consecutive steps pipelined (y⁺⁺ at row r−8), so y, b and y_out
+// cross DRAM once per two steps. k_rk4_marchc (the large-grid default) gives each
+// thread three contiguous columns — the x-neighbour exchange, which bounds these
+// kernels on the shared-memory data pipe, costs the same per thread for any column
+// count — and streams the rows with 1D bulk copies (TMA) into an mbarrier ring.
+//
 // 1D kernel (k_rk4_lane1d): a lane (≤ 8192 points) lives on chip; one CTA runs
 // all nsteps of its lane, exchanging only the edge values of each thread's run.
 #pragma once
