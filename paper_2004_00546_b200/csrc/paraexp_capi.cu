@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -249,6 +250,20 @@ void tend(Handle* h, int idx, cudaStream_t s) {
     if (_rc != PX_OK) return _rc; \
   } while (0)
 
+// Opt a kernel into `bytes` of dynamic shared memory once per (kernel, device): the
+// attribute belongs to the device's context, so a process driving several GPUs needs it
+// on each (handles are single-threaded, like the rest of the ABI).
+int smem_attr(Handle* h, const void* kernel, size_t bytes) {
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  PX_CUDA(h, cudaGetDevice(&dev));
+  size_t& have = done[{kernel, dev}];
+  if (have >= bytes) return PX_OK;
+  PX_CUDA(h, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  have = bytes;
+  return PX_OK;
+}
+
 int dalloc(Handle* h, void** p, size_t bytes) {
   if (bytes == 0) bytes = 8;
   cudaError_t e = cudaMalloc(p, bytes);
@@ -392,26 +407,15 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
 #define PX_M2(NT, DEP, MB, TM, ...)                                                                            \
   do {                                                                                                     \
     const size_t sm = px::march2_smem<NT, DEP>(zlanes);                                                   \
-    static bool attr[2] = {false, false};                                                                  \
-    if (!attr[zlanes]) {                                                                                  \
-      if (zlanes) PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march2<true, NT, DEP, MB, TM, ##__VA_ARGS__>,                \
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
-      else PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march2<false, NT, DEP, MB, TM, ##__VA_ARGS__>,                       \
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));         \
-      attr[zlanes] = true;                                                                                \
-    }                                                                                                      \
+    if (zlanes) PX_TRY(smem_attr(h, (const void*)px::k_rk4_march2<true, NT, DEP, MB, TM, ##__VA_ARGS__>, sm));  \
+    else PX_TRY(smem_attr(h, (const void*)px::k_rk4_march2<false, NT, DEP, MB, TM, ##__VA_ARGS__>, sm));        \
     if (zlanes) px::k_rk4_march2<true, NT, DEP, MB, TM, ##__VA_ARGS__><<<blocks, NT, sm, s>>>(a);                        \
     else px::k_rk4_march2<false, NT, DEP, MB, TM, ##__VA_ARGS__><<<blocks, NT, sm, s>>>(a);                               \
   } while (0)
 #define PX_MC(NC, NT, DEP, MB, BR, PF, ...)                                                                   \
   do {                                                                                                     \
     const size_t sm = px::marchc_smem<NC, NT, DEP>(BR);                                                   \
-    static bool attr = false;                                                                              \
-    if (!attr) {                                                                                           \
-      PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_marchc<NC, NT, DEP, MB, BR, PF, ##__VA_ARGS__>,             \
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));              \
-      attr = true;                                                                                         \
-    }                                                                                                      \
+    PX_TRY(smem_attr(h, (const void*)px::k_rk4_marchc<NC, NT, DEP, MB, BR, PF, ##__VA_ARGS__>, sm));      \
     px::k_rk4_marchc<NC, NT, DEP, MB, BR, PF, ##__VA_ARGS__><<<blocks, NT, sm, s>>>(a);                   \
   } while (0)
         if (a.halo > 0 && mc_nc == 3) {
@@ -465,12 +469,8 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
           b1.nbands = (ny + b1.band_rows - 1) / b1.band_rows;
           const unsigned blk1 = (unsigned)((size_t)h->L * b1.nstrips * b1.nbands);
           const size_t sm1 = px::march_smem(zlanes);
-          static bool attr1 = false;
-          if (!attr1) {
-            PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)px::march_smem(true)));
-            PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)px::march_smem(false)));
-            attr1 = true;
-          }
+          PX_TRY(smem_attr(h, (const void*)px::k_rk4_march<true>, px::march_smem(true)));
+          PX_TRY(smem_attr(h, (const void*)px::k_rk4_march<false>, px::march_smem(false)));
           if (zlanes) px::k_rk4_march<true><<<blk1, px::MARCH_NT, sm1, s>>>(b1);
           else px::k_rk4_march<false><<<blk1, px::MARCH_NT, sm1, s>>>(b1);
           st_i += 1;
@@ -495,12 +495,8 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
     a.nbands = (ny + br - 1) / br;
     const unsigned blocks = (unsigned)((size_t)h->L * a.nstrips * a.nbands);
     const size_t smem = px::march_smem(zlanes);
-    static bool attr_done[2] = {false, false};
-    if (!attr_done[zlanes]) {
-      if (zlanes) PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      else PX_CUDA(h, cudaFuncSetAttribute(px::k_rk4_march<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_done[zlanes] = true;
-    }
+    if (zlanes) PX_TRY(smem_attr(h, (const void*)px::k_rk4_march<true>, smem));
+    else PX_TRY(smem_attr(h, (const void*)px::k_rk4_march<false>, smem));
     for (int st_i = 1; st_i < nsteps; ++st_i) {
       double* out = (cur == h->Y0) ? h->Y1 : h->Y0;
       a.y_in = cur;
@@ -536,12 +532,7 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
 // 2D: Chebyshev action by row-marching passes of up to CM_MAXT fused terms (cheb_march.cuh)
 template <int M, int SG, bool TM>
 int launch_cm_v(Handle* h, const px::ChebMarchArgs& a, unsigned blocks, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    PX_CUDA(h, cudaFuncSetAttribute(px::k_cheb_march<M, SG, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)px::CM_SMEM));
-    attr = true;
-  }
+  PX_TRY(smem_attr(h, (const void*)px::k_cheb_march<M, SG, TM>, px::CM_SMEM));
   px::k_cheb_march<M, SG, TM><<<blocks, px::CM_NT, px::CM_SMEM, s>>>(a);
   PX_CHECK_LAUNCH(h);
   return PX_OK;
