@@ -77,6 +77,7 @@ enum {
 };
 
 enum { PX_FLAG_BOUNDARY_STATES = 1 };
+enum { PX_ADJOINT_ABSORBED = 0, PX_ADJOINT_FROZEN_SPAN = 1 };  /* px_set_adjoint_mode */
 
 typedef struct px_problem_desc {
   int kind;             /* PX_KIND_* */
@@ -143,6 +144,17 @@ int px_set_krylov_plan(void* handle, int slot, double span, int substeps);
  * (Krylov, small fields). 1 = the sequential scan (default). Replaces: the reference's
  * per-worker chains running concurrently (`workers.py:298-346`). */
 int px_set_local_blocks(void* handle, int blocks);
+
+/* Burgers adjoint formulation. PX_ADJOINT_ABSORBED (default): the final condition is absorbed
+ * into the inhomogeneous solves, exact Jᵀ(u(t)) there and frozen J(ū_p)ᵀ in the carry
+ * (solve_adjoint_varying, paraexp.py:329-353 — SURVEY §8(c) Option A, config 3).
+ * PX_ADJOINT_FROZEN_SPAN: the reference's solve_hybrid (hybrid.py:194-237, Option B): the
+ * inhomogeneous solves start from zero terminal data and, with no adjoint source, vanish;
+ * q†_T is propagated over [T, 0] through the frozen J(ū_p)ᵀ (propagate_span, the final span
+ * hybrid.py:232-233), ∫q† dt from its φ₁ series. One rank only. Replaces: the choice between
+ * direct_adjoint_loop's "hybrid" (solve_hybrid) and "linear"/"nonlinear" (solve_adjoint_varying)
+ * adjoints (optimization.py:183-220). */
+int px_set_adjoint_mode(void* handle, int mode);
 
 /* Inputs: u0 (n), u_target (n), ctrl (B×K); host or device memory. Replaces the
  * q0 / q_true / f arguments of direct_adjoint_loop (optimization.py:154-169). */

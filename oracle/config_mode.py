@@ -362,9 +362,16 @@ def slice_means(traj, P, nsteps):
 
 
 def burgers_gradient(nx, D, basis, T, P, nsteps, u0, u_target, ctrl, plan_for_region,
-                     region_fn, world: int = 1, traj=None, qdag_T=None):
+                     region_fn, world: int = 1, traj=None, qdag_T=None, adjoint: str = "absorbed"):
     """Config 3 (Option A of SURVEY §8(c)): absorbed final condition, exact Jᵀ(u(t))
-    in the inhomogeneous solves, frozen J(ū_p)ᵀ in the homogeneous ones."""
+    in the inhomogeneous solves, frozen J(ū_p)ᵀ in the homogeneous ones.
+
+    ``adjoint="frozen_span"``: the reference's `solve_hybrid` (Option B,
+    `hybrid.py:194-237`): the inhomogeneous solves start from zero terminal data
+    (`hybrid.py:194-203`) and, with the terminal objective's zero adjoint source, vanish;
+    q† is q†_T propagated over [T, 0] through the frozen J(ū_p)ᵀ slice by slice
+    (`propagate_span`, `hybrid.py:212-225`; the final span `hybrid.py:232-233`), and
+    ∫q† dt is the φ₁ series of the same actions."""
     n = nx
     hg = 2.0 * np.pi / nx
     ctrl = np.atleast_2d(np.asarray(ctrl, dtype=np.float64))
@@ -385,6 +392,18 @@ def burgers_gradient(nx, D, basis, T, P, nsteps, u0, u_target, ctrl, plan_for_re
     ubar = slice_means(traj, P, nsteps)                          # (P, B, n)
     region = region_fn(ubar)
     plan = plan_for_region(region, delta)
+
+    if adjoint == "frozen_span":
+        C = qT.copy()
+        Gh = np.zeros((B, n))
+        for p in range(P - 1, -1, -1):
+            ub = ubar[p]
+            C = exp_action(lambda y, ub=ub: burgers_adjoint_apply(ub, y, D, hg), plan, C, Gh)
+        grad = basis.project(Gh)
+        return OracleResult(J=J, grad=grad, uT=uT, qdag0=C, G=Gh,
+                            extras={"traj": traj, "ubar": ubar, "plan": plan})
+    if adjoint != "absorbed":
+        raise ValueError(adjoint)
 
     w_end = np.empty((P, B, n))
     zsum = np.zeros((B, n))

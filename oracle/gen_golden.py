@@ -17,7 +17,9 @@ these files; nothing at test time reads /root/reference. The fixtures pin:
 * `leja_points`, `spectral_interval`, `relpm_propagate(record=m)` (`:235-423`);
 * `solve_direct_linear` / `solve_adjoint_linear` pieces for N ∈ {1, 2, 3}
   (`paraexp.py:221-326`) — the Paraexp superposition structure;
-* `Trajectory.eval_many` linear interpolation (`timestepping.py:64-75`).
+* `Trajectory.eval_many` linear interpolation (`timestepping.py:64-75`);
+* `solve_hybrid` with a final condition and no adjoint source (`hybrid.py:194-237`):
+  q† at the slice edges of a geometric partition, with the slices' trapezoid means ū_p.
 """
 
 from __future__ import annotations
@@ -113,6 +115,36 @@ def main():
             out[f"a{N}_{p}_nodes"] = a.pieces[p].nodes
             out[f"a{N}_{p}_states"] = a.pieces[p].states
     np.savez_compressed(os.path.join(OUT, "reference_paraexp.npz"), **out)
+
+    # 6. solve_hybrid with a final condition and no adjoint source (hybrid.py:194-237) --
+    # the terminal objective's case: the inhomogeneous adjoint solves vanish and q† is
+    # q†_T carried back through the frozen interval operators (`propagate_span`)
+    nh = 12
+    gh = R.Grid2D(nh, 3)
+    n3h = gh.npoints
+    xh = 2.0 * np.pi * np.arange(nh) / nh
+    f_h = np.concatenate([np.tile(0.3 * np.sin(2.0 * xh), 3), np.zeros(n3h)])
+    spec_h = R.ProblemSpec(R.BURGERS, a=1.0, D=0.2, omega=1.0, T=1.0, f_spatial=f_h)
+    sys_h = R.build_system(gh, spec_h)
+    q0_h = np.concatenate([np.tile(0.5 * np.sin(xh), 3), np.zeros(n3h)])
+    qT1 = rng.standard_normal(nh)
+    qT_h = np.concatenate([np.tile(qT1, 3), np.zeros(n3h)])
+    plan_h = R.make_hybrid_plan(1.0, 3, 1.5)
+    res = R.solve_hybrid(sys_h, q0_h, qT_h, lambda t, q: np.zeros_like(q), plan_h,
+                         R.RKConfig(rtol=1e-10), R.LejaConfig(tol=1e-12))
+    bnd = plan_h.partition.boundaries
+    ubar = []
+    for piece in res.direct.pieces:  # the trapezoid mean of each slice (average_jacobian's weights)
+        w = np.zeros(len(piece.nodes))
+        gaps = np.diff(piece.nodes)
+        w[:-1] += 0.5 * gaps
+        w[1:] += 0.5 * gaps
+        ubar.append((w @ piece.states)[:nh] / (piece.nodes[-1] - piece.nodes[0]))
+    qstart = np.stack([pc.states[0][:nh] for pc in res.adjoint.pieces])   # q†(T_m)
+    qend = np.stack([pc.states[-1][:nh] for pc in res.adjoint.pieces])    # q†(T_{m+1}⁻)
+    vmax = max(float(np.max(np.abs(pc.states[:, n3h:]))) for pc in res.adjoint.pieces)
+    np.savez_compressed(os.path.join(OUT, "reference_hybrid.npz"), nx=nh, D=0.2, boundaries=bnd,
+                        ubar=np.stack(ubar), qT=qT1, qstart=qstart, qend=qend, vmax=vmax)
     print("wrote", sorted(f for f in os.listdir(OUT) if f.startswith("reference_")))
 
 

@@ -41,8 +41,9 @@ def cmd_run(args) -> int:
     rows, t = [], []
     if args.checkpoints:
         return _run_checkpointed(args, c, u0, ut, ctrl, rk)
+    extra = {"hybrid_adjoint": args.hybrid_adjoint} if algo == "hybrid" else {}
     # warm-up outside the timed region: plans, HBM allocation, graph capture
-    direct_adjoint_loop(c.system, ctrl, ut, algo, N=c.P, rk=rk, expaction=c.expaction, u0=u0)
+    direct_adjoint_loop(c.system, ctrl, ut, algo, N=c.P, rk=rk, expaction=c.expaction, u0=u0, **extra)
     if c.descent_steps and not args.single:
         tick = time.perf_counter()
         res = descend(c.system, ctrl, ut, steps=c.descent_steps, lr=c.lr, algorithm=algo, N=c.P, rk=rk,
@@ -55,7 +56,8 @@ def cmd_run(args) -> int:
     else:
         for rep in range(args.repeats):
             tick = time.perf_counter()
-            loop = direct_adjoint_loop(c.system, ctrl, ut, algo, N=c.P, rk=rk, expaction=c.expaction, u0=u0)
+            loop = direct_adjoint_loop(c.system, ctrl, ut, algo, N=c.P, rk=rk, expaction=c.expaction, u0=u0,
+                                       **extra)
             t.append(time.perf_counter() - tick)
         for b, (Jb, gb) in enumerate(zip(np.ravel(loop.J), np.atleast_2d(loop.grad))):
             rows.append([0, b, f"{Jb:.17g}", f"{np.linalg.norm(gb):.17g}"])
@@ -65,7 +67,7 @@ def cmd_run(args) -> int:
         w = csv.writer(f)
         w.writerow(["iteration", "member", "J", "grad_norm"])
         w.writerows(rows)
-    summary = {"config": c.name, "algorithm": algo, "backend": "cuda", "grid": [c.grid.nx, c.grid.ny],
+    summary = {"config": c.name, "algorithm": algo, **extra, "backend": "cuda", "grid": [c.grid.nx, c.grid.ny],
                "P": c.P, "steps_per_slice": c.nsteps, "batch": c.batch,
                "timing": {"seconds_median": float(np.median(t)), "repeats": len(t),
                           "gradient_evals_per_s": evals / float(np.median(t))}}
@@ -144,6 +146,8 @@ def main(argv=None) -> int:
     r.add_argument("--nonlinear", action="store_true", help="Burgers: Algorithm 2 direct instead of serial")
     r.add_argument("--algorithm", choices=["serial", "linear", "nonlinear", "hybrid"], default=None,
                    help="override the config's algorithm (serial = the reference loop, no Paraexp)")
+    r.add_argument("--hybrid-adjoint", choices=["absorbed", "frozen_span"], default="absorbed",
+                   help="Burgers hybrid: config 3's absorbed adjoint or the reference solve_hybrid's frozen span")
     r.add_argument("--checkpoints", type=int, default=0,
                    help="M equispaced checkpoints (run_checkpointed_loop; P/(M+1) slices per segment)")
     p = sub.add_parser("predict", help="measure per-unit kernel times, print the multi-GPU scaling model")

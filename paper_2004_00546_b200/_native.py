@@ -27,6 +27,7 @@ PX_MAX_LOCAL_BLOCKS = 16
 (PX_FIELD_J, PX_FIELD_GRAD, PX_FIELD_UT, PX_FIELD_QDAG0, PX_FIELD_G, PX_FIELD_UBND,
  PX_FIELD_FROZEN_BOUNDS, PX_FIELD_VEND, PX_FIELD_WEND, PX_FIELD_TRAJ) = range(10)
 PX_FLAG_BOUNDARY_STATES = 1
+PX_ADJOINT_ABSORBED, PX_ADJOINT_FROZEN_SPAN = 0, 1
 
 
 class ProblemDesc(ctypes.Structure):
@@ -102,6 +103,7 @@ SIGNATURES = {
     "px_set_cheb_plan": (c_int, [c_void_p, c_int, POINTER(ChebPlanC)]),
     "px_set_krylov_plan": (c_int, [c_void_p, c_int, c_double, c_int]),
     "px_set_local_blocks": (c_int, [c_void_p, c_int]),
+    "px_set_adjoint_mode": (c_int, [c_void_p, c_int]),
     "px_set_inputs": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     "px_direct": (c_int, [c_void_p, c_void_p]),
     "px_finish_direct": (c_int, [c_void_p, c_void_p]),

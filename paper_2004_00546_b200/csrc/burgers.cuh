@@ -46,6 +46,10 @@ struct BurgersAdjointArgs {
   int substeps, degree, sigma;
   double center, scale;
   const double *be, *bp;
+  // 1: the reference's solve_hybrid adjoint (hybrid.py:212-237) for a terminal objective:
+  // no adjoint source, so the inhomogeneous solves (zero terminal data) vanish and q† is
+  // q†_T propagated over [T, 0] through the frozen J(ū_p)ᵀ; 0: absorbed final condition
+  int terminal_span;
 };
 
 // rhs(u)_i = −u_i·(u_{i+1} − u_{i−1})/(2h) + D·(u_{i+1} − 2u_i + u_{i−1})/h² + f_i
@@ -469,12 +473,12 @@ __global__ void __launch_bounds__(BURGERS_NT) k_burgers_scan(BurgersAdjointArgs 
     const int i = threadIdx.x + t * BURGERS_NT;
     C[t] = Gp[t] = 0.0;
     if (i < n) {
-      C[t] = a.W0[((size_t)b * Pl + (Pl - 1)) * n + i];
-      Gp[t] = a.G[(size_t)b * n + i];
+      C[t] = a.terminal_span ? a.QT[(size_t)b * n + i] : a.W0[((size_t)b * Pl + (Pl - 1)) * n + i];
+      Gp[t] = a.terminal_span ? 0.0 : a.G[(size_t)b * n + i];
     }
   }
   int par = 0;
-  for (int p = a.p_end - 2; p >= 0; --p) {
+  for (int p = a.p_end - (a.terminal_span ? 1 : 2); p >= 0; --p) {
     const bool own = p >= a.p_begin;
     const double* ub = a.ubar + ((size_t)p * a.B + b) * n;
 #pragma unroll
@@ -542,7 +546,7 @@ __global__ void __launch_bounds__(BURGERS_NT) k_burgers_scan(BurgersAdjointArgs 
 #pragma unroll
       for (int t = 0; t < PPT; ++t) {
         const int i = threadIdx.x + t * BURGERS_NT;
-        if (i < n) C[t] += a.W0[((size_t)b * Pl + (p - a.p_begin)) * n + i];
+        if (i < n && !a.terminal_span) C[t] += a.W0[((size_t)b * Pl + (p - a.p_begin)) * n + i];
       }
     }
   }
@@ -579,8 +583,8 @@ __global__ void __launch_bounds__(BURGERS_NT) k_burgers_scan_run(BurgersAdjointA
   double C[PPT], Gp[PPT], prev[PPT], cur[PPT], acc[PPT], pac[PPT], gp[PPT], gm[PPT], gc[PPT];
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
-    C[k] = act ? a.W0[((size_t)b * Pl + (Pl - 1)) * n + i0 + k] : 0.0;
-    Gp[k] = act ? a.G[(size_t)b * n + i0 + k] : 0.0;
+    C[k] = !act ? 0.0 : a.terminal_span ? a.QT[(size_t)b * n + i0 + k] : a.W0[((size_t)b * Pl + (Pl - 1)) * n + i0 + k];
+    Gp[k] = (act && !a.terminal_span) ? a.G[(size_t)b * n + i0 + k] : 0.0;
   }
   int par = 0;
   // (left, right) neighbours of the run of v
@@ -594,7 +598,7 @@ __global__ void __launch_bounds__(BURGERS_NT) k_burgers_scan_run(BurgersAdjointA
     r = act ? sE[(par * 2 + 0) * T + tr] : 0.0;
     par ^= 1;
   };
-  for (int p = a.p_end - 2; p >= 0; --p) {
+  for (int p = a.p_end - (a.terminal_span ? 1 : 2); p >= 0; --p) {
     const bool own = p >= a.p_begin;
     const double* ub = a.ubar + ((size_t)p * a.B + b) * n;
 #pragma unroll
@@ -651,7 +655,7 @@ __global__ void __launch_bounds__(BURGERS_NT) k_burgers_scan_run(BurgersAdjointA
         Gp[k] += pac[k];
       }
     }
-    if (own && act) {
+    if (own && act && !a.terminal_span) {
 #pragma unroll
       for (int k = 0; k < PPT; ++k) C[k] += a.W0[((size_t)b * Pl + (p - a.p_begin)) * n + i0 + k];
     }
@@ -723,13 +727,15 @@ inline int burgers_adjoint(const BurgersAdjointArgs& a, cudaStream_t s, px_stats
     cudaFuncSetAttribute(k_burgers_adjoint_rk4<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rk); \
     k_burgers_adjoint_rk4<PP><<<a.B * Pl, BURGERS_NT, smem_rk, s>>>(a);                            \
   } while (0)
-  if (ppt <= 1) PX_BA(1);
-  else if (ppt <= 2) PX_BA(2);
-  else if (ppt <= 4) PX_BA(4);
-  else PX_BA(8);
+  if (!a.terminal_span) {  // terminal span: the inhomogeneous solves are identically zero
+    if (ppt <= 1) PX_BA(1);
+    else if (ppt <= 2) PX_BA(2);
+    else if (ppt <= 4) PX_BA(4);
+    else PX_BA(8);
+    k_lane_sum<<<dim3((unsigned)std::min<size_t>(((size_t)a.nx + 255) / 256, 64), a.B), 256, 0, s>>>(
+        a.G, a.Z, Pl, (size_t)a.nx);
+  }
 #undef PX_BA
-  k_lane_sum<<<dim3((unsigned)std::min<size_t>(((size_t)a.nx + 255) / 256, 64), a.B), 256, 0, s>>>(
-      a.G, a.Z, Pl, (size_t)a.nx);
   // coefficients to device (scratch ACC[0] is free here: n ≥ 2·(degree+1) not guaranteed, use Wk[2])
   double* coef = a.Wk[2];
   const size_t ncoef = 2 * (size_t)(a.degree + 1);
@@ -766,11 +772,11 @@ inline int burgers_adjoint(const BurgersAdjointArgs& a, cudaStream_t s, px_stats
   if (cudaGetLastError() != cudaSuccess) return PX_ERR_CUDA;
   *wend = a.W0;
   if (stats) {
-    stats->kernel_launches += 3;
-    stats->rk4_lane_steps += (uint64_t)a.B * Pl * a.nsteps;
-    const double rb = 40.0 * a.nx * (double)a.B * Pl * a.nsteps;  // y, q†_T, node, y', z
+    stats->kernel_launches += a.terminal_span ? 1 : 3;
+    if (!a.terminal_span) stats->rk4_lane_steps += (uint64_t)a.B * Pl * a.nsteps;
+    const double rb = a.terminal_span ? 0.0 : 40.0 * a.nx * (double)a.B * Pl * a.nsteps;  // y, q†_T, node, y', z
     stats->rk4_bytes += rb;
-    const uint64_t acts = (uint64_t)(a.p_end - 1);
+    const uint64_t acts = (uint64_t)(a.p_end - (a.terminal_span ? 0 : 1));
     const uint64_t terms = acts * a.substeps * a.degree * a.B;
     stats->exp_terms += terms;
     const double eb = 56.0 * a.nx * (double)terms;

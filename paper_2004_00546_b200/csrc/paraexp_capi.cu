@@ -73,6 +73,7 @@ struct Handle {
   double *Y0 = nullptr, *Y1 = nullptr, *Z = nullptr;
   // closed-form adjoint ∫ (2D circulant operator): Σ_p z_p = (Aᵀ)⁻¹(Σ_p y_n,p − Pl·n·b) + …
   bool z_closed = false;
+  int adjoint_mode = PX_ADJOINT_ABSORBED;  // Burgers: PX_ADJOINT_FROZEN_SPAN = reference solve_hybrid
   cufftHandle fft = 0;
   double2* fbuf = nullptr;  // B × n complex
   double* bsum = nullptr;   // B: Σ_i b[b][i]
@@ -1158,7 +1159,9 @@ int finish_direct_impl(Handle* h, cudaStream_t s) {
 
 int finish_adjoint_impl(Handle* h, cudaStream_t s) {
   const long long nb = (long long)h->n;
+  if (h->adjoint_mode == PX_ADJOINT_FROZEN_SPAN) return PX_OK;  // q†_T is not absorbed: nothing to add
   const int tm = tbegin(h, PX_PHASE_OTHER, s);
+  // absorbed final condition: q† = q†_T + the solved part (paraexp.py:268-270)
   PX_TRY(axpby(h, h->QDAG0, nb, h->QDAG0, nb, 1.0, h->QT, nb, 1.0, s));
   PX_TRY(axpby(h, h->G, nb, h->G, nb, 1.0, h->QT, nb, h->d.T, s));
   PX_TRY(project(h, h->GRAD, h->QT, nb, h->d.T, 1.0, s));
@@ -1371,6 +1374,20 @@ int px_set_krylov_plan(void* handle, int slot, double span, int substeps) {
   pl.span = span;
   pl.substeps = substeps;
   pl.degree = h->d.krylov_m;
+  return PX_OK;
+}
+
+int px_set_adjoint_mode(void* handle, int mode) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (h) cudaSetDevice(h->device);
+  if (!h) return fail(h, PX_ERR_ARG, "null handle");
+  if (mode != PX_ADJOINT_ABSORBED && mode != PX_ADJOINT_FROZEN_SPAN) return fail(h, PX_ERR_ARG, "unknown adjoint mode");
+  if (mode == PX_ADJOINT_FROZEN_SPAN && h->d.kind != PX_KIND_BURGERS)
+    return fail(h, PX_ERR_ARG, "the frozen-span adjoint is the Burgers hybrid's (solve_hybrid)");
+  if (mode != h->adjoint_mode) {
+    h->adjoint_mode = mode;
+    h->graph_valid = false;
+  }
   return PX_OK;
 }
 
@@ -1607,8 +1624,11 @@ int px_adjoint(void* handle, void* stream) {
     rc = adjoint_linear(h, s);
   } else {
     const Plan& pl = h->plans[PX_PLAN_FROZEN];
+    const bool span = h->adjoint_mode == PX_ADJOINT_FROZEN_SPAN;
+    if (span && (h->d.p_begin != 0 || h->d.p_end != h->d.P))
+      return fail(h, PX_ERR_ARG, "the frozen-span adjoint runs on one rank (it is one sequential chain)");
     // one slice and no earlier ranks (the serial loop): no homogeneous carry, no plan needed
-    const bool no_carry = h->Pl == 1 && h->d.p_begin == 0;
+    const bool no_carry = h->Pl == 1 && h->d.p_begin == 0 && !span;
     if ((!pl.set || pl.krylov) && !no_carry) return fail(h, PX_ERR_STATE, "frozen-operator plan not set");
     const bool use_plan = pl.set && !pl.krylov;
     px::BurgersAdjointArgs a{};
@@ -1620,6 +1640,7 @@ int px_adjoint(void* handle, void* stream) {
     a.D = h->d.D; a.hx = h->d.hx; a.h = (h->d.T / h->d.P) / h->d.nsteps;
     a.nx = h->d.nx; a.B = h->B; a.P = h->d.P; a.nsteps = h->d.nsteps;
     a.p_begin = h->d.p_begin; a.p_end = h->d.p_end;
+    a.terminal_span = span ? 1 : 0;
     if (use_plan) {
       a.substeps = pl.substeps; a.degree = pl.degree; a.center = pl.center; a.scale = pl.scale;
       a.sigma = pl.sigma; a.be = pl.be.data(); a.bp = pl.bp.data();

@@ -171,6 +171,7 @@ class ParaexpEngine:
         N.check(self.lib, self.lib.px_set_basis(h, tx, ty, ix, iy), h)
         self.plans: dict[int, ChebPlan | KrylovPlan] = {}
         self._keep = []
+        self._adjoint_mode = "absorbed"
         self.nl_history: list[float] = []
         if spec.direct not in ("serial", "iterative"):
             raise ConfigError(f"unknown direct solver {spec.direct!r}")
@@ -349,10 +350,21 @@ class ParaexpEngine:
         s = current_stream_handle() if stream is None else stream
         N.check(self.lib, self.lib.px_finish_direct(self.h, s), self.h)
 
+    def set_adjoint_mode(self, mode: str) -> None:
+        """Burgers adjoint formulation (`px_set_adjoint_mode`): "absorbed" (Option A,
+        `solve_adjoint_varying`, config 3) or "frozen_span" (the reference's `solve_hybrid`:
+        q†_T propagated through the frozen J(ū_p)ᵀ, `hybrid.py:212-237`)."""
+        code = {"absorbed": N.PX_ADJOINT_ABSORBED, "frozen_span": N.PX_ADJOINT_FROZEN_SPAN}.get(mode)
+        if code is None:
+            raise ValueError(f"adjoint mode must be 'absorbed' or 'frozen_span', not {mode!r}")
+        N.check(self.lib, self.lib.px_set_adjoint_mode(self.h, code), self.h)
+        self._adjoint_mode = mode
+
     def adjoint_partial(self, stream: int | None = None) -> None:
         s = current_stream_handle() if stream is None else stream
-        if not self.spec.system.is_linear and (self.p1 - self.p0 > 1 or self.p0 > 0):
-            self.plan_frozen(s)  # no carry for a single slice (the serial loop)
+        span = self._adjoint_mode == "frozen_span"
+        if not self.spec.system.is_linear and (self.p1 - self.p0 > 1 or self.p0 > 0 or span):
+            self.plan_frozen(s)  # no carry for a single absorbed slice (the serial loop)
         N.check(self.lib, self.lib.px_adjoint(self.h, s), self.h)
 
     def finish_adjoint(self, stream: int | None = None) -> None:

@@ -180,13 +180,17 @@ def direct_adjoint_loop(
     eps: float = 1e-3,
     min_iter: int = 2,
     max_iter: int = 25,
+    hybrid_adjoint: str = "absorbed",
 ) -> LoopResult:
     """One direct solve plus one adjoint solve, yielding J and ∂J/∂c (`optimization.py:154-231`).
 
     ``f``: control coefficients (K,) or (B, K); ``q_true``: u_target (n,);
     ``N``: number of time slices; with ``torch.distributed`` initialised the
     slices are sharded over the ranks (contiguous blocks) unless
-    ``distributed=False``.
+    ``distributed=False``. ``hybrid_adjoint`` (Burgers, ``algorithm="hybrid"``):
+    "absorbed" — config 3's Option A (`solve_adjoint_varying` driven by the serial
+    trajectory); "frozen_span" — the reference's `solve_hybrid` adjoint
+    (`hybrid.py:194-237`: q†_T through the frozen J(ū_p)ᵀ; one rank).
     """
     if backend not in BACKENDS:
         raise ValueError(f"unknown backend {backend!r}; the B200 path provides {BACKENDS}")
@@ -200,6 +204,10 @@ def direct_adjoint_loop(
         N = 1
     if algorithm in (HYBRID, NONLINEAR) and system.is_linear:
         raise ValueError(f"the {algorithm} path is the Burgers testbed's")
+    if hybrid_adjoint not in ("absorbed", "frozen_span"):
+        raise ValueError(f"hybrid_adjoint must be 'absorbed' or 'frozen_span', not {hybrid_adjoint!r}")
+    if hybrid_adjoint == "frozen_span" and algorithm != HYBRID:
+        raise ValueError("the frozen-span adjoint is the hybrid algorithm's (solve_hybrid)")
     if rk is None:
         raise ConfigError("rk: an RK4Config(dt) is required (fixed-step RK4)")
     expaction = expaction or _default_expaction(system)
@@ -209,13 +217,20 @@ def direct_adjoint_loop(
         raise ValueError("control coefficient count does not match the basis")
     u0 = np.zeros(system.n) if u0 is None else np.asarray(u0, dtype=np.float64)
     rank, world = _dist_rank_world() if distributed else (0, 1)
-    if algorithm in (NONLINEAR, SERIAL):
+    if algorithm in (NONLINEAR, SERIAL) or hybrid_adjoint == "frozen_span":
         rank, world = 0, 1  # one rank (every rank computes it identically): nothing to shard
     eng = get_engine(system, N, rk, expaction, B, rank, world, boundary_states and world == 1,
                      "iterative" if algorithm == NONLINEAR else "serial", eps, max_iter, min_iter)
     tick = time.perf_counter()
     eng.set_inputs(u0, np.asarray(q_true, dtype=np.float64), ctrl)
-    eng.gradient()
+    if hybrid_adjoint != "absorbed":
+        eng.set_adjoint_mode(hybrid_adjoint)
+        try:
+            eng.gradient()
+        finally:
+            eng.set_adjoint_mode("absorbed")  # cached engines default to the absorbed form
+    else:
+        eng.gradient()
     from . import _native as NN
     res = eng.results(fields=False)  # J and ∂J/∂c to the host; the n-sized fields stay on the device
     part = partition_equidistant(system.spec.T, N)

@@ -11,9 +11,10 @@ for callers that compose their own loops:
 * `solve_adjoint_linear(system, qdag_T, N, rk, …)` → `AdjointSolution` (q†(0) and
   ∫₀ᵀ q† dt for the terminal condition q†(T) = ``qdag_T``; the BASELINE objective has
   no adjoint source);
-* `solve_hybrid(system, u0, f, qdag_T, N, rk, …)` → (`DirectSolution`,
+* `solve_hybrid(system, u0, f, qdag_T, N, rk, …, adjoint="frozen_span")` → (`DirectSolution`,
   `AdjointSolution`) for Burgers: serial direct sweep (trajectory in HBM), then the
-  frozen-operator Paraexp adjoint driven by it. ``qdag_T=None`` uses u(T) − ``u_target``.
+  Paraexp adjoint driven by it — the reference's frozen-span form by default, config 3's
+  absorbed form (Option A) with ``adjoint="absorbed"``. ``qdag_T=None`` uses u(T) − ``u_target``.
 
 Differences from the reference, as for the loop: time-constant Fourier-mode controls
 ``f`` (coefficients), fixed-step RK4 (`RK4Config`), planned Chebyshev/Krylov actions,
@@ -77,10 +78,15 @@ def solve_adjoint_linear(system: System, qdag_T, N: int, rk: RK4Config, expactio
 
 
 def solve_hybrid(system: System, u0, f, qdag_T, N: int, rk: RK4Config, expaction=None,
-                 u_target=None) -> tuple[DirectSolution, AdjointSolution]:
-    """Burgers: serial direct sweep keeping the trajectory, then the time-varying adjoint
-    lanes and the frozen J(ū_p)ᵀ Paraexp carry (`hybrid.py:185-237`, Option A).
-    ``qdag_T=None`` takes q†(T) = u(T) − ``u_target``."""
+                 u_target=None, adjoint: str = "frozen_span") -> tuple[DirectSolution, AdjointSolution]:
+    """Burgers: serial direct sweep keeping the trajectory (`hybrid.py:185-191`), then the
+    Paraexp adjoint driven by it. ``qdag_T=None`` takes q†(T) = u(T) − ``u_target``.
+
+    ``adjoint="frozen_span"`` (default, the reference's `solve_hybrid`, `hybrid.py:194-237`):
+    the inhomogeneous solves start from zero terminal data and, without an adjoint source,
+    vanish; q†_T is propagated over [T, 0] through the frozen J(ū_p)ᵀ. ``"absorbed"``:
+    config 3's Option A — exact Jᵀ(u(t)) lanes with the final condition absorbed and the
+    frozen-operator carry (`solve_adjoint_varying`, `paraexp.py:329-353`)."""
     if system.is_linear:
         raise ValueError("solve_hybrid is the Burgers testbed's")
     ctrl, expaction = _prepare(system, f, rk, expaction)
@@ -88,21 +94,25 @@ def solve_hybrid(system: System, u0, f, qdag_T, N: int, rk: RK4Config, expaction
     if qdag_T is None and u_target is None:
         raise ValueError("give qdag_T or u_target")
     eng = get_engine(system, N, rk, expaction, B)
-    ut = np.zeros(system.n) if u_target is None else np.asarray(u_target, dtype=np.float64).reshape(-1)
-    eng.set_inputs(np.asarray(u0, dtype=np.float64).reshape(-1), ut, ctrl)
-    eng.direct_partial()
-    if qdag_T is None:
-        eng.finish_direct()
-    else:
-        q = np.broadcast_to(np.asarray(qdag_T, dtype=np.float64).reshape(-1, system.n), (B, system.n))
-        eng.set_adjoint_terminal(np.ascontiguousarray(q))
-    eng.adjoint_partial()
-    eng.finish_adjoint()
-    part = partition_equidistant(system.spec.T, N)
-    direct = DirectSolution(part, eng.get(NV.PX_FIELD_UT).reshape(B, system.n))
-    adjoint = AdjointSolution(part, eng.get(NV.PX_FIELD_QDAG0).reshape(B, system.n),
-                              eng.get(NV.PX_FIELD_G).reshape(B, system.n))
-    return direct, adjoint
+    eng.set_adjoint_mode(adjoint)
+    try:
+        ut = np.zeros(system.n) if u_target is None else np.asarray(u_target, dtype=np.float64).reshape(-1)
+        eng.set_inputs(np.asarray(u0, dtype=np.float64).reshape(-1), ut, ctrl)
+        eng.direct_partial()
+        if qdag_T is None:
+            eng.finish_direct()
+        else:
+            q = np.broadcast_to(np.asarray(qdag_T, dtype=np.float64).reshape(-1, system.n), (B, system.n))
+            eng.set_adjoint_terminal(np.ascontiguousarray(q))
+        eng.adjoint_partial()
+        eng.finish_adjoint()
+        part = partition_equidistant(system.spec.T, N)
+        direct = DirectSolution(part, eng.get(NV.PX_FIELD_UT).reshape(B, system.n))
+        adjoint_sol = AdjointSolution(part, eng.get(NV.PX_FIELD_QDAG0).reshape(B, system.n),
+                                      eng.get(NV.PX_FIELD_G).reshape(B, system.n))
+    finally:
+        eng.set_adjoint_mode("absorbed")  # cached engines default to the absorbed form
+    return direct, adjoint_sol
 
 
 def synthesize_truth(system: System, f_true, rk: RK4Config, algorithm: str = "serial", N: int = 1,

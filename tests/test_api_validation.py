@@ -33,6 +33,12 @@ def test_loop_rejects_bad_arguments():
         direct_adjoint_loop(b.system, b.inputs()[2], b.inputs()[1], "linear", N=b.P, rk=RK4Config(b.dt))
     with pytest.raises(ValueError):
         descend(c.system, ctrl, ut, steps=1, lr=0.0, N=c.P, rk=rk)
+    brk = RK4Config(b.dt)
+    with pytest.raises(ValueError):   # unknown Burgers adjoint form
+        direct_adjoint_loop(b.system, b.inputs()[2], b.inputs()[1], "hybrid", N=b.P, rk=brk, hybrid_adjoint="x")
+    with pytest.raises(ValueError):   # the frozen-span adjoint is solve_hybrid's (the hybrid algorithm)
+        direct_adjoint_loop(b.system, b.inputs()[2], b.inputs()[1], "nonlinear", N=b.P, rk=brk,
+                            hybrid_adjoint="frozen_span")
 
 
 def test_solver_level_rejects_wrong_testbed():

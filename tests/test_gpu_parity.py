@@ -645,13 +645,48 @@ def test_solver_level_api_vs_oracle():
     ref = burgers_gradient(c3.grid.nx, c3.spec.D, c3.system.basis, c3.spec.T, c3.P, c3.nsteps, u0, ut, ctrl,
                            lambda region, span: plan_chebyshev(region, span, c3.expaction),
                            lambda ub: burgers_frozen_region(ub, c3.grid, c3.spec.D), qdag_T=qT)
-    d, a = solve_hybrid(c3.system, u0, ctrl, qT, c3.P, RK4Config(c3.dt), c3.expaction)
+    d, a = solve_hybrid(c3.system, u0, ctrl, qT, c3.P, RK4Config(c3.dt), c3.expaction, adjoint="absorbed")
     assert rel_l2(d.final_state, ref.uT) <= 1e-10
     from paper_2004_00546_b200 import synthesize_truth
     tr = synthesize_truth(c3.system, ctrl, RK4Config(c3.dt), "hybrid", N=c3.P, expaction=c3.expaction, u0=u0)
     assert np.array_equal(tr.final_state, d.final_state)
     assert rel_l2(a.initial_state, ref.qdag0) <= 1e-10
     assert rel_l2(a.integral, ref.G) <= 1e-10
+    # the reference's solve_hybrid form (default): q†_T through the frozen spans only
+    refB = burgers_gradient(c3.grid.nx, c3.spec.D, c3.system.basis, c3.spec.T, c3.P, c3.nsteps, u0, ut, ctrl,
+                            lambda region, span: plan_chebyshev(region, span, c3.expaction),
+                            lambda ub: burgers_frozen_region(ub, c3.grid, c3.spec.D), qdag_T=qT,
+                            adjoint="frozen_span")
+    d, a = solve_hybrid(c3.system, u0, ctrl, qT, c3.P, RK4Config(c3.dt), c3.expaction)
+    assert rel_l2(a.initial_state, refB.qdag0) <= 1e-10
+    assert rel_l2(a.integral, refB.G) <= 1e-10
+    assert rel_l2(a.initial_state, ref.qdag0) > 1e-8  # a different (model) adjoint than Option A
+
+
+@pytest.mark.parametrize("P", [64, 1])
+def test_hybrid_frozen_span_loop_vs_oracle(P):
+    """direct_adjoint_loop(..., "hybrid", hybrid_adjoint="frozen_span") — the reference's
+    solve_hybrid adjoint for the terminal objective — at config 3's full size (and one slice
+    of a shorter, coarser case: the frozen operator's plan at tol 1e-12 needs spans ≲ 1/8 at
+    full size) against the oracle's frozen-span restatement; the absorbed (config 3) loop
+    afterwards still matches its own oracle on the same cached engine."""
+    from oracle.config_mode import burgers_gradient
+    from paper_2004_00546_b200 import RK4Config, baseline, direct_adjoint_loop, scaled
+    from paper_2004_00546_b200.expaction import plan_chebyshev
+    from paper_2004_00546_b200.problems import burgers_frozen_region
+    c = baseline(3) if P == 64 else scaled(baseline(3), nx=256, P=1, steps_per_slice=200, T=0.2)
+    u0, ut, ctrl = c.inputs()
+    args = (c.grid.nx, c.spec.D, c.system.basis, c.spec.T, c.P, c.nsteps, u0, ut, ctrl,
+            lambda region, span: plan_chebyshev(region, span, c.expaction),
+            lambda ub: burgers_frozen_region(ub, c.grid, c.spec.D))
+    refB = burgers_gradient(*args, adjoint="frozen_span")
+    loop = direct_adjoint_loop(c.system, ctrl, ut, "hybrid", N=c.P, rk=RK4Config(c.dt), expaction=c.expaction,
+                               u0=u0, hybrid_adjoint="frozen_span")
+    _check(loop, refB)
+    refA = burgers_gradient(*args)
+    loop = direct_adjoint_loop(c.system, ctrl, ut, "hybrid", N=c.P, rk=RK4Config(c.dt), expaction=c.expaction,
+                               u0=u0)
+    _check(loop, refA)
 
 
 def test_nonfinite_input_raises_integration_failure():

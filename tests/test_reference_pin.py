@@ -133,3 +133,25 @@ def test_config_mode_chains_use_the_pinned_structure():
     import inspect
     src = inspect.getsource(C.linear_gradient)
     assert "chains_direct" in src and "chains_adjoint" in src
+
+
+def test_hybrid_frozen_span_matches_solve_hybrid():
+    """The frozen-span adjoint (the product's `solve_hybrid(..., adjoint="frozen_span")`,
+    config-mode oracle `burgers_gradient(..., adjoint="frozen_span")`) has the structure of
+    the reference's `solve_hybrid` with a final condition and no adjoint source
+    (`hybrid.py:194-237`): zero inhomogeneous solves, q†_T carried back slice by slice through
+    exp((T_{m+1} − T_m)·J(ū_m)ᵀ) (`propagate_span`). Restated here with exact dense
+    exponentials of the oracle's Jᵀ at the reference's own slice means ū_m."""
+    from scipy.linalg import expm
+    f = load("hybrid")
+    nx, D = int(f["nx"]), float(f["D"])
+    h = 2.0 * np.pi / nx
+    bnd, ubar = f["boundaries"], f["ubar"]
+    assert float(f["vmax"]) <= 1e-15  # the V component stays zero (y-invariant, V ≡ 0)
+    q = f["qT"].copy()
+    N = len(bnd) - 1
+    for m in range(N - 1, -1, -1):
+        JT = np.stack([C.burgers_adjoint_apply(ubar[m], e, D, h) for e in np.eye(nx)], axis=1)
+        assert rel_l2(f["qend"][m], q) <= 1e-13     # q† entering slice m from above
+        q = expm((bnd[m + 1] - bnd[m]) * JT) @ q
+        assert rel_l2(f["qstart"][m], q) <= 1e-13   # q†(T_m)
