@@ -219,6 +219,57 @@ def test_blockscan_ranks_emulated(world):
         e.close()
 
 
+def _emulated_world(c, world):
+    """One gradient with world-`world` sharding emulated on one GPU (ranks run one after
+    another, partials summed as NCCL's allreduce would); rank 0's results."""
+    import torch
+    from paper_2004_00546_b200.engine import EngineSpec, ParaexpEngine
+    u0, ut, ctrl = c.inputs()
+    engs = [ParaexpEngine(EngineSpec(c.system, c.P, c.dt, c.expaction, c.batch, r, world)) for r in range(world)]
+
+    def allreduce(fields):
+        for f in fields:
+            views = [e.device_view(f) for e in engs]
+            total = torch.stack(views).sum(0)
+            for v in views:
+                v.copy_(total)
+
+    for e in engs:
+        e.set_inputs(u0, ut, ctrl)
+        e.direct_partial()
+    allreduce(engs[0].direct_reduce_fields())
+    for e in engs:
+        e.finish_direct()
+        e.adjoint_partial()
+    allreduce(engs[0].adjoint_reduce_fields(True))
+    for e in engs:
+        e.finish_adjoint()
+    r = {k: np.array(v) for k, v in engs[0].results().items()}
+    for e in engs:
+        e.close()
+    torch.cuda.empty_cache()
+    return r
+
+
+@pytest.mark.parametrize("tol,bound", [(1e-10, 5e-9), (1e-12, 1e-10)])
+def test_g_invariance_full_config5(tol, bound):
+    """the block-scan over G ranks against the single-rank scan at config 5's
+    full size. The spread is the slice plan's truncation accumulated over the hundreds of
+    sequential carries the single-rank scan applies where a rank applies one long span:
+    ≈ 1e-9 at the config's tol 1e-10, ≈ 3e-11 at tol 1e-12."""
+    from dataclasses import replace
+    from paper_2004_00546_b200 import baseline, release_engines
+    release_engines()
+    c = baseline(5)
+    c = replace(c, expaction=replace(c.expaction, tol=tol))
+    one = _emulated_world(c, 1)
+    for world in (2, 8):
+        r = _emulated_world(c, world)
+        for k in ("uT", "qdag0", "grad"):
+            assert rel_l2(r[k], one[k]) <= bound, (world, k)
+        assert np.max(np.abs(r["J"] - one["J"]) / np.abs(one["J"])) <= bound
+
+
 def test_burgers_blockscan_emulated():
     import torch
     from oracle.config_mode import burgers_gradient
