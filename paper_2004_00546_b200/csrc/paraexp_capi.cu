@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -253,11 +254,14 @@ void tend(Handle* h, int idx, cudaStream_t s) {
 
 // Opt a kernel into `bytes` of dynamic shared memory once per (kernel, device): the
 // attribute belongs to the device's context, so a process driving several GPUs needs it
-// on each (handles are single-threaded, like the rest of the ABI).
+// on each. The table is shared by all handles (one per device, possibly on different
+// host threads), hence the lock.
 int smem_attr(Handle* h, const void* kernel, size_t bytes) {
+  static std::mutex mu;
   static std::map<std::pair<const void*, int>, size_t> done;
   int dev = 0;
   PX_CUDA(h, cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
   size_t& have = done[{kernel, dev}];
   if (have >= bytes) return PX_OK;
   PX_CUDA(h, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
