@@ -11,4 +11,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_rk
 echo marchc_dir=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_rk4_marchc -s 21 -c 1 -o gpurun_out/prof_marchc_adj_c5 $CMD > gpurun_out/ncu_mca.log 2>&1
 echo marchc_adj=$?
-ls -la gpurun_out
+
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_cheb_march -s 10 -c 2 -o gpurun_out/prof_cheb_e_c5 $CMD > gpurun_out/ncu_cheb_e.log 2>&1
+echo cheb=$?
