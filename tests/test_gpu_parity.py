@@ -358,6 +358,31 @@ def test_full_config_gradient_vs_directional_fd(index):
     assert np.all(np.isfinite(r["grad"])) and r["J"][0] > 0
 
 
+def test_full_config5_gradient_affine_in_controls():
+    """Full config 5: u(T) is affine in the control coefficients c and the adjoint linear
+    in q†(T), so ∂J/∂c is affine in c — every RK4 step, Chebyshev term and projection is a
+    linear operation — and u(T) too: at c_m = (c_a + c_b)/2 both equal the mean of their
+    values at c_a and c_b to rounding (size-independent property at the full size)."""
+    from paper_2004_00546_b200 import RK4Config, baseline
+    from paper_2004_00546_b200.optimization import get_engine
+    c = baseline(5)
+    u0, ut, ctrl = c.inputs()
+    eng = get_engine(c.system, c.P, RK4Config(c.dt), c.expaction, c.batch)
+    rng = np.random.default_rng(11)
+    ca = ctrl
+    cb = ctrl + rng.normal(0.0, 0.05, ctrl.shape)
+    out = []
+    for cc in (ca, cb, 0.5 * (ca + cb)):
+        eng.set_inputs(u0, ut, cc)
+        eng.gradient()
+        r = eng.results()
+        out.append((np.array(r["grad"]), np.array(r["uT"])))
+    (ga, ua), (gb, ub), (gm, um) = out
+    assert rel_l2(gm, 0.5 * (ga + gb)) <= 1e-11
+    assert rel_l2(um, 0.5 * (ua + ub)) <= 1e-12
+    assert rel_l2(ga, gb) > 1e-3  # the two controls are genuinely different
+
+
 @pytest.mark.parametrize("index", [4, 5])
 def test_graph_replay_matches_stream_launches(index):
     """px_gradient's CUDA-graph replay runs the identical kernel sequence: results are
