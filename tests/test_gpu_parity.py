@@ -765,6 +765,20 @@ def test_hybrid_frozen_span_loop_vs_oracle(P):
     _check(loop, refA)
 
 
+def test_adjoint_mode_validation():
+    """px_set_adjoint_mode: the frozen-span form is the Burgers hybrid's; unknown modes are
+    rejected before reaching the library."""
+    from paper_2004_00546_b200 import RK4Config, baseline, scaled
+    from paper_2004_00546_b200.optimization import get_engine
+    c = scaled(baseline(5), nx=32, P=2, steps_per_slice=4, K=4)
+    eng = get_engine(c.system, c.P, RK4Config(c.dt), c.expaction, c.batch)
+    with pytest.raises(ValueError):
+        eng.set_adjoint_mode("frozen_span")   # linear testbed: PX_ERR_ARG → ValueError
+    with pytest.raises(ValueError):
+        eng.set_adjoint_mode("bogus")
+    eng.set_adjoint_mode("absorbed")
+
+
 def test_nonfinite_input_raises_integration_failure():
     """A non-finite state surfaces as the reference's IntegrationFailure (`errors.py:4-15`),
     for the linear (graph-replayed) and the Burgers paths."""
