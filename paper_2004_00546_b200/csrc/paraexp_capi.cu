@@ -328,7 +328,6 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
   const int nsteps = h->d.nsteps;
   double* cur = nullptr;
   uint64_t launched_steps = 0;
-  int64_t fused_launches = -1;  // march launches when some cover two steps (bytes are per launch)
   h->z_valid = false;
   if (h->dim == 1 && h->n <= 4096) {
     px::Lane1DArgs a{};
@@ -449,9 +448,7 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
         return PX_OK;
       };
       int st_i = 1;
-      fused_launches = 0;
       while (st_i < nsteps) {
-        ++fused_launches;
         double* out = (cur == h->Y0) ? h->Y1 : h->Y0;
         a.y_in = cur;
         a.y_out = out;
@@ -521,7 +518,6 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
   // algorithmic bytes: 24n (40n with the ∫ accumulator) per lane and RK4
   // step — per step also when one launch advances two steps (the fused launch streams
   // y, b, y_out once for both, i.e. half the model's bytes: temporal blocking)
-  (void)fused_launches;
   const double bytes = bytes_per_point * (double)h->n * h->L * (double)launched_steps;
   h->stats.rk4_bytes += bytes;
   h->stats.algorithmic_bytes += bytes;
