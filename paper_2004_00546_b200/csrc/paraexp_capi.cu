@@ -836,13 +836,21 @@ int scan1d(Handle* h, bool adjoint, const double* lanes, double* out, double* pa
   if (h->Pl > 1 && !h->plans[PX_PLAN_SLICE].set) return fail(h, PX_ERR_STATE, "slice plan not set");
   const int ppt = h->n <= 512 ? 1 : (h->n <= 1024 ? 2 : (h->n <= 2048 ? 4 : 8));
   const int nt = (int)((h->n + ppt - 1) / ppt);
-  // cluster version (8 CTAs = 8 SMs per member, DSMEM ghost-zone refresh every 8 terms)
+  // cluster version (8 CTAs = 8 SMs per member, DSMEM ghost-zone refresh every G terms)
   // for the larger 1D grids; one CTA per member otherwise
   static const int s1c = [] { const char* e = getenv("PX_SCAN1D_CLUSTER"); return e ? atoi(e) : 1; }();
-  constexpr int kCS = 8, kPPT = 4, kG = 8;
+  constexpr int kCS = 8, kPPT = 4;
+  // ghost width G: the cluster refreshes its DSMEM ghost zones every G terms (a cluster barrier
+  // costs ≈ 4× a CTA barrier) and recomputes G points per side; 64 measured best (config 2:
+  // 8 → 16 → 32 → 64 gave 1814 → 2056 → 2204 → 2300 gradient evals/s)
+  static const int kGv = [] {
+    const char* e = getenv("PX_SCAN1D_G");
+    const int v = e ? atoi(e) : 64;
+    return v == 32 ? 32 : (v == 16 ? 16 : (v == 8 ? 8 : 64));
+  }();
   const int Wc = (int)(h->n / kCS);
-  if (s1c && h->n >= 2048 && h->n % (kCS * kPPT) == 0 && Wc >= kG && Wc / kPPT + 2 * (kG / kPPT) <= 256) {
-    const int nr = Wc / kPPT + 2 * (kG / kPPT);
+  if (s1c && h->n >= 2048 && h->n % (kCS * kPPT) == 0 && Wc >= kGv && Wc / kPPT + 2 * (kGv / kPPT) <= 256) {
+    const int nr = Wc / kPPT + 2 * (kGv / kPPT);
     cudaLaunchConfig_t cfg = {};
     static const int kmb = [] { const char* e = getenv("PX_SCAN1D_MB"); return e ? atoi(e) : 2; }();
     const int mb = kmb >= 4 ? 4 : (kmb >= 2 ? 2 : 1);
@@ -858,9 +866,23 @@ int scan1d(Handle* h, bool adjoint, const double* lanes, double* out, double* pa
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const int Bm = h->B;
-    if (mb == 4) PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, kG, 4>, a, Bm));
-    else if (mb == 2) PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, kG, 2>, a, Bm));
-    else PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, kG, 1>, a, Bm));
+    if (kGv == 64) {
+      if (mb == 4) PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, 64, 4>, a, Bm));
+      else if (mb == 2) PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, 64, 2>, a, Bm));
+      else PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, 64, 1>, a, Bm));
+    } else if (kGv == 32) {
+      if (mb == 4) PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, 32, 4>, a, Bm));
+      else if (mb == 2) PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, 32, 2>, a, Bm));
+      else PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, 32, 1>, a, Bm));
+    } else if (kGv == 16) {  // ghost zones refreshed every 16 terms (half the cluster barriers)
+      if (mb == 4) PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, 16, 4>, a, Bm));
+      else if (mb == 2) PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, 16, 2>, a, Bm));
+      else PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, 16, 1>, a, Bm));
+    } else {
+      if (mb == 4) PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, 8, 4>, a, Bm));
+      else if (mb == 2) PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, 8, 2>, a, Bm));
+      else PX_CUDA(h, cudaLaunchKernelEx(&cfg, px::k_scan1d_cluster<kPPT, kCS, 8, 1>, a, Bm));
+    }
   } else {
   const bool full = h->n % ppt == 0;
 #define PX_S1(PP)                                              \
