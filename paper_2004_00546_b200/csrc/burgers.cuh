@@ -14,6 +14,7 @@
 // P·nsteps times, the adjoint slice solves are one CTA per (member, slice), and
 // the homogeneous carry over all slices is one persistent CTA per member.
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -669,6 +670,174 @@ __global__ void __launch_bounds__(BURGERS_NT) k_burgers_scan_run(BurgersAdjointA
   }
 }
 
+// The frozen-operator carry spread over the CS CTAs of a thread-block cluster (CS SMs
+// instead of one): CTA r owns W = n/CS points plus a ghost zone of G points per side that it
+// recomputes redundantly (with the ghost points' own J(ū_p)ᵀ coefficients), so the Chebyshev
+// terms need CTA barriers only; the ghost zones are refreshed from the neighbouring CTAs'
+// shared memory (DSMEM) after one cluster barrier every G terms and at every action start
+// (the k_scan1d_cluster scheme with per-point, per-slice coefficients). Same arithmetic per
+// point as k_burgers_scan_run.
+template <int PPT, int CS, int G>
+__global__ void __launch_bounds__(256) k_burgers_scan_cluster(BurgersAdjointArgs a, const double* coef) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  static_assert(G % PPT == 0, "ghost width must be whole runs");
+  constexpr int GR = G / PPT;
+  __shared__ double eL[2][256], eR[2][256];
+  __shared__ double xbuf[2][2][2][G];  // [parity][side: 0 my left edge, 1 right][cur/prev][G]
+  const int n = a.nx;
+  const int W = n / CS;
+  const int rank = (int)cluster.block_rank();
+  const int b = blockIdx.x / CS;  // member
+  const int t = threadIdx.x;
+  const int NR = W / PPT + 2 * GR;
+  const bool act = t < NR;
+  const int g0 = rank * W - G + t * PPT;
+  const bool owned = act && t >= GR && t < NR - GR;
+  const int tl = (t == 0) ? 0 : t - 1, tr = (t + 1 >= NR) ? NR - 1 : t + 1;
+  auto gidx = [&](int k) { int g = g0 + k; g %= n; return g < 0 ? g + n : g; };
+  const int Pl = a.p_end - a.p_begin;
+  const double inv2h = 1.0 / (2.0 * a.hx);
+  const double Dih2 = a.D / (a.hx * a.hx);
+  const double c0 = a.center, two_over = 2.0 / a.scale, sigma = (double)a.sigma;
+  const double* __restrict__ be = coef;
+  const double* __restrict__ bp = coef + a.degree + 1;
+  const int degree = a.degree, substeps = a.substeps;
+  double C[PPT], Gp[PPT], gp[PPT], gm[PPT], gc[PPT];
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    const int i = gidx(k);
+    C[k] = !act ? 0.0 : a.terminal_span ? a.QT[(size_t)b * n + i] : a.W0[((size_t)b * Pl + (Pl - 1)) * n + i];
+    Gp[k] = (owned && !a.terminal_span) ? a.G[(size_t)b * n + i] : 0.0;
+  }
+  int par = 0, xpar = 0;
+  auto exchange = [&](const double* u, double& l, double& r) {
+    if (act) {
+      eL[par][t] = u[0];
+      eR[par][t] = u[PPT - 1];
+    }
+    __syncthreads();
+    l = eR[par][tl];
+    r = eL[par][tr];
+    par ^= 1;
+  };
+  auto refresh = [&](double* u, double* v) {
+    if (act) {
+      if (t >= GR && t < 2 * GR) {
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          xbuf[xpar][0][0][(t - GR) * PPT + k] = u[k];
+          if (v) xbuf[xpar][0][1][(t - GR) * PPT + k] = v[k];
+        }
+      }
+      if (t >= NR - 2 * GR && t < NR - GR) {
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          xbuf[xpar][1][0][(t - (NR - 2 * GR)) * PPT + k] = u[k];
+          if (v) xbuf[xpar][1][1][(t - (NR - 2 * GR)) * PPT + k] = v[k];
+        }
+      }
+    }
+    cluster.sync();
+    if (act && t < GR) {
+      const double* src = cluster.map_shared_rank(&xbuf[xpar][1][0][0], (unsigned)((rank + CS - 1) % CS));
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        u[k] = src[t * PPT + k];
+        if (v) v[k] = src[G + t * PPT + k];
+      }
+    }
+    if (act && t >= NR - GR) {
+      const double* src = cluster.map_shared_rank(&xbuf[xpar][0][0][0], (unsigned)((rank + 1) % CS));
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        u[k] = src[(t - (NR - GR)) * PPT + k];
+        if (v) v[k] = src[G + (t - (NR - GR)) * PPT + k];
+      }
+    }
+    xpar ^= 1;
+  };
+  for (int p = a.p_end - (a.terminal_span ? 1 : 2); p >= 0; --p) {
+    const bool own = p >= a.p_begin;
+    const double* ub = a.ubar + ((size_t)p * a.B + b) * n;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      const int i = gidx(k);
+      const int ip = (i + 1 >= n) ? 0 : i + 1, im = (i == 0) ? n - 1 : i - 1;
+      const double up = act ? ub[ip] : 0.0, um = act ? ub[im] : 0.0;
+      const double kp = up * inv2h + Dih2, km = Dih2 - um * inv2h, kc = -(up - um) * inv2h - 2.0 * Dih2;
+      gp[k] = two_over * kp;
+      gm[k] = two_over * km;
+      gc[k] = two_over * (kc - c0);
+    }
+    for (int sub = 0; sub < substeps; ++sub) {
+      double prev[PPT], cur[PPT], acc[PPT], pac[PPT];
+      refresh(C, nullptr);
+      int valid = G;
+      double l, r;
+      exchange(C, l, r);
+      {
+        const double b0 = __ldg(be), b1 = __ldg(be + 1), p0 = __ldg(bp), p1 = __ldg(bp + 1);
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          const double yp = (k + 1 == PPT) ? r : C[k + 1];
+          const double ym = (k == 0) ? l : C[k - 1];
+          double u1 = gc[k] * C[k];
+          u1 = fma(gp[k], yp, u1);
+          u1 = 0.5 * fma(gm[k], ym, u1);
+          prev[k] = C[k];
+          cur[k] = u1;
+          acc[k] = b0 * C[k] + b1 * u1;
+          pac[k] = p0 * C[k] + p1 * u1;
+        }
+      }
+      --valid;
+      for (int j = 2; j <= degree; ++j) {
+        if (valid == 0) {
+          refresh(cur, prev);
+          valid = G;
+        }
+        exchange(cur, l, r);
+        const double bk = __ldg(be + j), pk = __ldg(bp + j);
+        double un[PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          const double yp = (k + 1 == PPT) ? r : cur[k + 1];
+          const double ym = (k == 0) ? l : cur[k - 1];
+          double v = fma(gc[k], cur[k], sigma * prev[k]);
+          v = fma(gp[k], yp, v);
+          un[k] = fma(gm[k], ym, v);
+        }
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          prev[k] = cur[k];
+          cur[k] = un[k];
+          acc[k] = fma(bk, un[k], acc[k]);
+          pac[k] = fma(pk, un[k], pac[k]);
+        }
+        --valid;
+      }
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        C[k] = acc[k];
+        Gp[k] += pac[k];
+      }
+    }
+    if (own && act && !a.terminal_span) {
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) C[k] += a.W0[((size_t)b * Pl + (p - a.p_begin)) * n + gidx(k)];
+    }
+  }
+  if (owned) {
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      a.QDAG0[(size_t)b * n + gidx(k)] = C[k];
+      a.G[(size_t)b * n + gidx(k)] = Gp[k];
+    }
+  }
+  cluster.sync();  // no CTA leaves while a neighbour may still read its exchange buffers
+}
+
 inline int burgers_direct(const BurgersDirectArgs& a, cudaStream_t s, px_stats* stats) {
   if (a.nx > BURGERS_MAX_N) return PX_ERR_ARG;
   const size_t smem = 3 * (size_t)a.nx * sizeof(double);
@@ -757,8 +926,26 @@ inline int burgers_adjoint(const BurgersAdjointArgs& a, cudaStream_t s, px_stats
     k_burgers_scan_run<PP><<<a.B, ((a.nx / PP + 31) / 32) * 32, sm2, s>>>(a, coef);                \
   } while (0)
   static const bool strided_sc = [] { const char* e = getenv("PX_BURGERS_STRIDED"); return e && atoi(e) != 0; }();
+  // cluster scan (8 CTAs per member, 64-point DSMEM ghost zones) for the larger grids
+  static const int bcl = [] { const char* e = getenv("PX_BURGERS_CLUSTER"); return e ? atoi(e) : 1; }();
+  constexpr int kCS = 8, kPPT = 4, kG = 64;
   const int rps = ppt <= 1 ? 1 : (ppt <= 2 ? 2 : (ppt <= 4 ? 4 : 8));
-  if (!strided_sc && a.nx % rps == 0) {
+  if (bcl && !strided_sc && a.nx >= 2048 && a.nx % (kCS * kPPT) == 0 && a.nx / kCS >= kG &&
+      a.nx / kCS / kPPT + 2 * (kG / kPPT) <= 256 && a.degree >= 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(a.B * kCS));
+    cfg.blockDim = dim3((unsigned)(((a.nx / kCS / kPPT + 2 * (kG / kPPT) + 31) / 32) * 32));
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kCS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, k_burgers_scan_cluster<kPPT, kCS, kG>, a, (const double*)coef) != cudaSuccess)
+      return PX_ERR_CUDA;
+  } else if (!strided_sc && a.nx % rps == 0) {
     if (rps == 1) PX_BSR(1);
     else if (rps == 2) PX_BSR(2);
     else if (rps == 4) PX_BSR(4);

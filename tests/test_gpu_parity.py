@@ -270,14 +270,17 @@ def test_g_invariance_full_config5(tol, bound):
         assert np.max(np.abs(r["J"] - one["J"]) / np.abs(one["J"])) <= bound
 
 
-def test_burgers_blockscan_emulated():
+@pytest.mark.parametrize("full", [False, True])
+def test_burgers_blockscan_emulated(full):
+    """Burgers world-3 block-scan on one GPU vs the oracle; at config 3's full size (2048
+    points) the frozen carry runs on the 8-CTA cluster kernel, on the 256-point case on one CTA."""
     import torch
     from oracle.config_mode import burgers_gradient
     from paper_2004_00546_b200 import baseline, scaled
     from paper_2004_00546_b200.engine import EngineSpec, ParaexpEngine
     from paper_2004_00546_b200.expaction import plan_chebyshev
     from paper_2004_00546_b200.problems import burgers_frozen_region
-    c = scaled(baseline(3), nx=256, P=8, steps_per_slice=16)
+    c = baseline(3) if full else scaled(baseline(3), nx=256, P=8, steps_per_slice=16)
     u0, ut, ctrl = c.inputs()
     world = 3
     engs = [ParaexpEngine(EngineSpec(c.system, c.P, c.dt, c.expaction, c.batch, r, world)) for r in range(world)]
