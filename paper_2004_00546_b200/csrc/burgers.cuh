@@ -838,6 +838,138 @@ __global__ void __launch_bounds__(256) k_burgers_scan_cluster(BurgersAdjointArgs
   cluster.sync();  // no CTA leaves while a neighbour may still read its exchange buffers
 }
 
+// The serial direct sweep spread over the CS CTAs of a thread-block cluster: CTA r owns
+// W = n/CS points plus G ghost points per side, recomputed redundantly (each RK4 stage
+// consumes one ghost layer per side), so the 4·G/4 stages between refreshes need CTA
+// barriers only; every G/4 steps the ghost zones of u are refreshed from the neighbouring
+// CTAs' shared memory (DSMEM) after one cluster barrier. Nodes and u(T) are written for the
+// owned points. Same arithmetic per point as k_burgers_direct_run.
+template <int PPT, int CS, int G>
+__global__ void __launch_bounds__(256) k_burgers_direct_cluster(BurgersDirectArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  static_assert(G % (4 * PPT) == 0, "ghost width: whole runs, whole steps");
+  constexpr int GR = G / PPT;
+  constexpr int STEPS_PER_REFRESH = G / 4;
+  __shared__ double eL[2][256], eR[2][256];
+  __shared__ double xbuf[2][2][G];  // [parity][side: 0 my left edge, 1 my right edge][G]
+  const int n = a.nx;
+  const int W = n / CS;
+  const int rank = (int)cluster.block_rank();
+  const int b = blockIdx.x / CS;
+  const int t = threadIdx.x;
+  const int NR = W / PPT + 2 * GR;
+  const bool act = t < NR;
+  const int g0 = rank * W - G + t * PPT;
+  const bool owned = act && t >= GR && t < NR - GR;
+  const int tl = (t == 0) ? 0 : t - 1, tr = (t + 1 >= NR) ? NR - 1 : t + 1;
+  auto gidx = [&](int k) { int g = g0 + k; g %= n; return g < 0 ? g + n : g; };
+  const double inv2h = 1.0 / (2.0 * a.hx);
+  const double Dih2 = a.D / (a.hx * a.hx), twoD = 2.0 * Dih2;
+  const double h = a.h, hh = 0.5 * a.h, h6 = a.h / 6.0;
+  double f[PPT], u[PPT], acc[PPT], x[PPT], kk[PPT];
+  const double* c = a.ctrl + (size_t)b * a.K;
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    f[k] = 0.0;
+    u[k] = 0.0;
+    if (act) {
+      const int i = gidx(k);
+      double fv = 0.0;
+      for (int q = 0; q < a.K; ++q) fv += c[q] * a.tx[(size_t)a.ix[q] * n + i];
+      f[k] = fv;
+      u[k] = a.u0[i];
+      if (owned) a.traj[(size_t)b * n + i] = u[k];
+    }
+  }
+  const size_t S = (size_t)a.P * a.nsteps;
+  const size_t node_stride = (size_t)a.B * n;
+  int par = 0, xpar = 0;
+  auto rhs = [&](double* k_out) {
+    if (act) {
+      eL[par][t] = x[0];
+      eR[par][t] = x[PPT - 1];
+    }
+    __syncthreads();
+    const double xl = eR[par][tl], xr = eL[par][tr];
+    par ^= 1;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      const double um = (k == 0) ? xl : x[k - 1];
+      const double up = (k + 1 == PPT) ? xr : x[k + 1];
+      const double A = up + um, B = up - um;
+      const double t1 = fma(Dih2, A, f[k]);
+      const double t2 = fma(inv2h, B, twoD);
+      k_out[k] = fma(-x[k], t2, t1);
+    }
+  };
+  auto refresh = [&]() {
+    if (act) {
+      if (t >= GR && t < 2 * GR) {
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) xbuf[xpar][0][(t - GR) * PPT + k] = u[k];
+      }
+      if (t >= NR - 2 * GR && t < NR - GR) {
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) xbuf[xpar][1][(t - (NR - 2 * GR)) * PPT + k] = u[k];
+      }
+    }
+    cluster.sync();
+    if (act && t < GR) {
+      const double* src = cluster.map_shared_rank(&xbuf[xpar][1][0], (unsigned)((rank + CS - 1) % CS));
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) u[k] = src[t * PPT + k];
+    }
+    if (act && t >= NR - GR) {
+      const double* src = cluster.map_shared_rank(&xbuf[xpar][0][0], (unsigned)((rank + 1) % CS));
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) u[k] = src[(t - (NR - GR)) * PPT + k];
+    }
+    xpar ^= 1;
+  };
+  int valid = STEPS_PER_REFRESH;  // the ghost zones start exact (u0 read at global indices)
+  for (size_t st = 0; st < S; ++st) {
+    if (valid == 0) {
+      refresh();
+      valid = STEPS_PER_REFRESH;
+    }
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) x[k] = u[k];
+    rhs(kk);
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      acc[k] = kk[k];
+      x[k] = fma(hh, kk[k], u[k]);
+    }
+    rhs(kk);
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      acc[k] = fma(2.0, kk[k], acc[k]);
+      x[k] = fma(hh, kk[k], u[k]);
+    }
+    rhs(kk);
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      acc[k] = fma(2.0, kk[k], acc[k]);
+      x[k] = fma(h, kk[k], u[k]);
+    }
+    rhs(kk);
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) u[k] = fma(h6, acc[k] + kk[k], u[k]);
+    --valid;
+    if (owned) {
+      double* node = a.traj + (st + 1) * node_stride + (size_t)b * n;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) node[gidx(k)] = u[k];
+    }
+  }
+  if (owned) {
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) a.UT[(size_t)b * n + gidx(k)] = u[k];
+  }
+  cluster.sync();  // no CTA leaves while a neighbour may still read its exchange buffers
+}
+
 inline int burgers_direct(const BurgersDirectArgs& a, cudaStream_t s, px_stats* stats) {
   if (a.nx > BURGERS_MAX_N) return PX_ERR_ARG;
   const size_t smem = 3 * (size_t)a.nx * sizeof(double);
@@ -858,7 +990,25 @@ inline int burgers_direct(const BurgersDirectArgs& a, cudaStream_t s, px_stats* 
   int rp = ppt <= 1 ? 1 : (ppt <= 2 ? 2 : (ppt <= 4 ? 4 : 8));
   if (rp_env == 1 || rp_env == 2 || rp_env == 4 || rp_env == 8) rp = std::max(rp, rp_env);
   static const bool strided = [] { const char* e = getenv("PX_BURGERS_STRIDED"); return e && atoi(e) != 0; }();
-  if (!strided && a.nx % rp == 0) {
+  // cluster sweep (8 CTAs per member, 64-point ghost zones refreshed every 16 steps) for the
+  // larger grids
+  static const int bcl = [] { const char* e = getenv("PX_BURGERS_CLUSTER"); return e ? atoi(e) : 1; }();
+  constexpr int kCS = 8, kPPT = 4, kG = 64;
+  if (bcl && !strided && a.nx >= 2048 && a.nx % (kCS * kPPT) == 0 && a.nx / kCS >= kG &&
+      a.nx / kCS / kPPT + 2 * (kG / kPPT) <= 256) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(a.B * kCS));
+    cfg.blockDim = dim3((unsigned)(((a.nx / kCS / kPPT + 2 * (kG / kPPT) + 31) / 32) * 32));
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kCS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, k_burgers_direct_cluster<kPPT, kCS, kG>, a) != cudaSuccess) return PX_ERR_CUDA;
+  } else if (!strided && a.nx % rp == 0) {
     if (rp == 1) PX_BR(1);
     else if (rp == 2) PX_BR(2);
     else if (rp == 4) PX_BR(4);
