@@ -97,6 +97,15 @@ def test_config2_full_batch16():
     _check(_gpu_linear(c), _oracle_linear(c))
 
 
+@pytest.mark.parametrize("nx", [2048, 6144])
+def test_1d_cluster_scan_widths(nx):
+    """The 1D cluster scan (8 CTAs per member, 64-point ghost zones) at the smallest and a
+    large owned width (256 / 768 points per CTA), against the oracle."""
+    from paper_2004_00546_b200 import baseline, scaled
+    c = scaled(baseline(2), nx=nx, P=8, steps_per_slice=800, batch=2, T=0.5)
+    _check(_gpu_linear(c), _oracle_linear(c))
+
+
 def test_config2_descent_two_steps():
     from oracle.config_mode import linear_gradient
     from paper_2004_00546_b200 import RK4Config, baseline, descend
