@@ -279,6 +279,23 @@ def test_g_invariance_full_config5(tol, bound):
         assert np.max(np.abs(r["J"] - one["J"]) / np.abs(one["J"])) <= bound
 
 
+def test_burgers_cluster_kernels_wider_grid():
+    """The Burgers cluster kernels (serial sweep and frozen carry, 8 CTAs per member) at 4096
+    points (512 owned per CTA) against the oracle."""
+    from oracle.config_mode import burgers_gradient
+    from paper_2004_00546_b200 import RK4Config, baseline, direct_adjoint_loop, scaled
+    from paper_2004_00546_b200.expaction import plan_chebyshev
+    from paper_2004_00546_b200.problems import burgers_frozen_region
+    c = scaled(baseline(3), nx=4096, P=8, steps_per_slice=128, T=0.25)
+    u0, ut, ctrl = c.inputs()
+    ref = burgers_gradient(c.grid.nx, c.spec.D, c.system.basis, c.spec.T, c.P, c.nsteps, u0, ut, ctrl,
+                           lambda region, span: plan_chebyshev(region, span, c.expaction),
+                           lambda ub: burgers_frozen_region(ub, c.grid, c.spec.D))
+    loop = direct_adjoint_loop(c.system, ctrl, ut, "hybrid", N=c.P, rk=RK4Config(c.dt), expaction=c.expaction,
+                               u0=u0)
+    _check(loop, ref)
+
+
 @pytest.mark.parametrize("full", [False, True])
 def test_burgers_blockscan_emulated(full):
     """Burgers world-3 block-scan on one GPU vs the oracle; at config 3's full size (2048
