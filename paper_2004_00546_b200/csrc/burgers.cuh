@@ -295,17 +295,38 @@ __global__ void __launch_bounds__(256) k_frozen_bounds(double* bpart, const doub
   }
 }
 
-__global__ void k_frozen_bounds_final(double* bounds, const double* bpart, int m) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// one CTA of 256 threads: min / max are order-independent, so the result is exact and
+// deterministic whatever the reduction tree
+__global__ void __launch_bounds__(256) k_frozen_bounds_final(double* bounds, const double* bpart, int m) {
+  __shared__ double r0[8], r1[8], r2[8];
   double lo = 1e300, hi = -1e300, im = 0.0;
-  for (int k = 0; k < m; ++k) {
+  for (int k = threadIdx.x; k < m; k += blockDim.x) {
     lo = fmin(lo, bpart[3 * k]);
     hi = fmax(hi, bpart[3 * k + 1]);
     im = fmax(im, bpart[3 * k + 2]);
   }
-  bounds[0] = lo;
-  bounds[1] = hi;
-  bounds[2] = im;
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_down_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_down_sync(0xffffffffu, hi, o));
+    im = fmax(im, __shfl_down_sync(0xffffffffu, im, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    r0[w] = lo;
+    r1[w] = hi;
+    r2[w] = im;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      lo = fmin(lo, r0[k]);
+      hi = fmax(hi, r1[k]);
+      im = fmax(im, r2[k]);
+    }
+    bounds[0] = lo;
+    bounds[1] = hi;
+    bounds[2] = im;
+  }
 }
 
 // (Jᵀ(u) y)_i = (u_{i+1}y_{i+1} − u_{i−1}y_{i−1})/(2h) − (u_{i+1} − u_{i−1})/(2h)·y_i
@@ -1023,7 +1044,7 @@ inline int burgers_direct(const BurgersDirectArgs& a, cudaStream_t s, px_stats* 
   k_slice_means<<<(unsigned)std::min<size_t>((total + 255) / 256, 4096), 256, 0, s>>>(a.ubar, a.traj, a.P,
                                                                                        a.nsteps, a.B, a.nx);
   k_frozen_bounds<<<a.bounds_blocks, 256, 0, s>>>(a.bpart, a.ubar, total, a.nx, a.hx, a.D);
-  k_frozen_bounds_final<<<1, 32, 0, s>>>(a.bounds, a.bpart, a.bounds_blocks);
+  k_frozen_bounds_final<<<1, 256, 0, s>>>(a.bounds, a.bpart, a.bounds_blocks);
   if (cudaGetLastError() != cudaSuccess) return PX_ERR_CUDA;
   if (stats) {
     stats->kernel_launches += 4;

@@ -1535,7 +1535,7 @@ int nl_means_bounds(Handle* h, cudaStream_t s) {
   PX_CHECK_LAUNCH(h);
   px::k_frozen_bounds<<<h->bounds_blocks, 256, 0, s>>>(h->bpart, h->ubar, total, (int)h->n, h->d.hx, h->d.D);
   PX_CHECK_LAUNCH(h);
-  px::k_frozen_bounds_final<<<1, 32, 0, s>>>(h->bounds, h->bpart, h->bounds_blocks);
+  px::k_frozen_bounds_final<<<1, 256, 0, s>>>(h->bounds, h->bpart, h->bounds_blocks);
   PX_CHECK_LAUNCH(h);
   return PX_OK;
 }
