@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define PX_ABI_VERSION 1
+#define PX_ABI_VERSION 2
 
 enum {
   PX_OK = 0,
@@ -76,7 +76,24 @@ enum {
   PX_FIELD_COUNT = 10
 };
 
-enum { PX_FLAG_BOUNDARY_STATES = 1 };
+enum {
+  PX_FLAG_BOUNDARY_STATES = 1, /* keep u(T_p) for every slice edge (PX_FIELD_UBND; world = 1) */
+  PX_FLAG_Z_ACCUM = 2          /* 2D adjoint ∫: per-lane RK4 accumulator instead of the closed form */
+};
+
+/* Kernel-variant keys for px_set_variant / px_get_variant (per handle; defaults are the
+ * measured-best variants, the alternatives exist for parity tests and tuning). */
+enum {
+  PX_VAR_MARCH2 = 0,          /* 0 one RK4 step per launch; 1 (default) two-step launches for sweeps of
+                                 ≥ 2^28 lane-points; 2 two-step launches at any size */
+  PX_VAR_MARCH_COLS = 1,      /* columns per thread of the two-step march: 3 (default) or 2 */
+  PX_VAR_MARCH_BAND = 2,      /* rows per band of the two-step march (0: automatic) */
+  PX_VAR_CHEB_TERMS = 3,      /* Chebyshev terms fused per 2D pass, 1 … 6 (default 6) */
+  PX_VAR_CHEB_STRIP = 4,      /* strip width of the 2D Chebyshev passes (0: balanced) */
+  PX_VAR_CHEB_BAND = 5,       /* rows per band of the 2D Chebyshev passes (0: one wave) */
+  PX_VAR_SCAN1D_CLUSTER = 6,  /* 1D scans on 8-CTA clusters for n ≥ 2048 (default 1) */
+  PX_VAR_BURGERS_CLUSTER = 7  /* Burgers sweeps on 8-CTA clusters for n ≥ 2048 (default 1) */
+};
 enum { PX_ADJOINT_ABSORBED = 0, PX_ADJOINT_FROZEN_SPAN = 1 };  /* px_set_adjoint_mode */
 
 typedef struct px_problem_desc {
@@ -136,6 +153,10 @@ int px_set_basis(void* handle, const double* tx, const double* ty, const int* ix
  * (timestepping.py:360-423) by the host planner's a-priori plan. */
 int px_set_cheb_plan(void* handle, int slot, const px_cheb_plan* plan);
 int px_set_krylov_plan(void* handle, int slot, double span, int substeps);
+
+/* Kernel-variant selection (PX_VAR_*), per handle; invalidates the captured gradient graph. */
+int px_set_variant(void* handle, int key, int value);
+int px_get_variant(void* handle, int key, int* value);
 
 /* Split this rank's slices into `blocks` equal contiguous blocks whose summed-chain carries
  * run concurrently on side streams of one GPU (the multi-GPU block-scan of SURVEY.md §8(e)

@@ -26,7 +26,11 @@ PX_PLAN_BLOCK_LONG = 6
 PX_MAX_LOCAL_BLOCKS = 16
 (PX_FIELD_J, PX_FIELD_GRAD, PX_FIELD_UT, PX_FIELD_QDAG0, PX_FIELD_G, PX_FIELD_UBND,
  PX_FIELD_FROZEN_BOUNDS, PX_FIELD_VEND, PX_FIELD_WEND, PX_FIELD_TRAJ) = range(10)
-PX_FLAG_BOUNDARY_STATES = 1
+PX_FLAG_BOUNDARY_STATES, PX_FLAG_Z_ACCUM = 1, 2
+ABI_VERSION = 2
+# kernel-variant keys (px_set_variant)
+VARIANTS = {"march2": 0, "march_cols": 1, "march_band": 2, "cheb_terms": 3, "cheb_strip": 4, "cheb_band": 5,
+            "scan1d_cluster": 6, "burgers_cluster": 7}
 PX_ADJOINT_ABSORBED, PX_ADJOINT_FROZEN_SPAN = 0, 1
 
 
@@ -103,6 +107,8 @@ SIGNATURES = {
     "px_set_cheb_plan": (c_int, [c_void_p, c_int, POINTER(ChebPlanC)]),
     "px_set_krylov_plan": (c_int, [c_void_p, c_int, c_double, c_int]),
     "px_set_local_blocks": (c_int, [c_void_p, c_int]),
+    "px_set_variant": (c_int, [c_void_p, c_int, c_int]),
+    "px_get_variant": (c_int, [c_void_p, c_int, POINTER(c_int)]),
     "px_set_adjoint_mode": (c_int, [c_void_p, c_int]),
     "px_set_inputs": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     "px_direct": (c_int, [c_void_p, c_void_p]),
@@ -142,7 +148,7 @@ def load(path: str | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.px_abi_version() != 1:
+    if lib.px_abi_version() != ABI_VERSION:
         raise NativeUnavailable("libparaexp.so ABI version mismatch")
     if path is None:
         _lib = lib

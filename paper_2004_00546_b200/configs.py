@@ -14,7 +14,10 @@ bench:
 * slice rule n_p = ⌈Δ/dt⌉ (``partition.slice_steps``);
 * config 2 descent step lr = 1/(T²·n) (the Hessian of J in the low modes is
   ≈ T²·n/2 because ∂u(T)/∂c_k ≈ T·φ_k); config 3 exp-action tol 1e-12;
-  config 5's "10 gradient evaluations" are 10 repeated evaluations of one control.
+  config 5's "10 gradient evaluations" are 10 repeated evaluations of one control;
+* configs 4 and 5 (the multi-GPU cases) read their exp-action tol 1e-10 as the error budget of
+  the whole sweep's carries (``horizon`` = T): each slice carry is planned to tol/(10·P), so
+  the 1-GPU scan and every G-GPU block-scan agree to well below 1e-10.
 
 ``scaled(cfg, ...)`` shrinks a config for tests while keeping its structure.
 """
@@ -128,11 +131,12 @@ def baseline(index: int) -> BaselineCase:
     if index == 4:
         return BaselineCase(4, "c4_advdiff2d_512_krylov", Grid(512, 512),
                             ProblemSpec(ADVECTION_DIFFUSION, (1.0, 0.5), 1e-3, 1.0),
-                            K=64, P=128, dt=2e-4, expaction=KrylovConfig(m=30, tol=1e-10), target_modes=16)
+                            K=64, P=128, dt=2e-4, expaction=KrylovConfig(m=30, tol=1e-10, horizon=1.0),
+                            target_modes=16)
     if index == 5:
         return BaselineCase(5, "c5_advdiff2d_2048_p512", Grid(2048, 2048),
                             ProblemSpec(ADVECTION_DIFFUSION, (1.0, 0.5), 5e-4, 1.0),
-                            K=256, P=512, dt=5e-5, expaction=ChebyshevConfig(tol=1e-10),
+                            K=256, P=512, dt=5e-5, expaction=ChebyshevConfig(tol=1e-10, horizon=1.0),
                             evaluations=10, target_modes=16)
     raise ValueError("config index must be 1..5")
 
@@ -153,5 +157,6 @@ def scaled(c: BaselineCase, nx: int | None = None, P: int | None = None, steps_p
     if grid.dim == 2:
         M = int(math.isqrt(K // 4))
         K = 4 * M * M
-    return replace(c, grid=grid, spec=spec, P=P, dt=dt, K=K, batch=batch or c.batch,
+    ex = c.expaction if c.expaction.horizon <= 0 else replace(c.expaction, horizon=spec.T)
+    return replace(c, grid=grid, spec=spec, P=P, dt=dt, K=K, batch=batch or c.batch, expaction=ex,
                    target_modes=min(c.target_modes, K if grid.dim == 1 else 16))

@@ -20,12 +20,24 @@
 #include <algorithm>
 
 #include "../../include/paraexp.h"
-#include "kernels.cuh"
+#include "common.cuh"
 
 namespace px {
 
 constexpr int BURGERS_MAX_N = 8192;
 constexpr int BURGERS_NT = 1024;
+
+// out[b][i] = Σ_{p<lanes_per_b} lanes[b*lanes_per_b + p][i]  (fixed order)
+__global__ void k_lane_sum(double* out, const double* lanes, int lanes_per_b, size_t n) {
+  const int b = blockIdx.y;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const double* src = lanes + (size_t)b * lanes_per_b * n + i;
+    double r = 0.0;
+    for (int p = 0; p < lanes_per_b; ++p) r += src[(size_t)p * n];
+    out[(size_t)b * n + i] = r;
+  }
+}
 
 struct BurgersDirectArgs {
   const double *u0, *ctrl, *tx;
@@ -259,6 +271,11 @@ __global__ void k_slice_means(double* ubar, const double* traj, int P, int nstep
   }
 }
 
+// min / max that propagate NaN (fmin/fmax drop it): a non-finite trajectory must reach the
+// host as a non-finite bound, not as a silently smaller box
+__device__ __forceinline__ double nan_min(double a, double b) { return (a < b || a != a) ? a : b; }
+__device__ __forceinline__ double nan_max(double a, double b) { return (a > b || a != a) ? a : b; }
+
 // Field-of-values box of B̄ = J(ū)ᵀ, union over slices and members (see
 // problems.burgers_frozen_region): (min re_lo, max re_hi, max im) partials.
 __global__ void __launch_bounds__(256) k_frozen_bounds(double* bpart, const double* ubar, size_t total, int n,
@@ -275,20 +292,20 @@ __global__ void __launch_bounds__(256) k_frozen_bounds(double* bpart, const doub
     const double dxu = (up - um) * inv2h;
     const double diag = -dxu - dh2;
     const double rad = (fabs(up - uc) + fabs(uc - um)) * inv4h + dh2;
-    lo = fmin(lo, diag - rad);
-    hi = fmax(hi, diag + rad);
-    im = fmax(im, (fabs(up + uc) + fabs(uc + um)) * inv4h);
+    lo = nan_min(lo, diag - rad);
+    hi = nan_max(hi, diag + rad);
+    im = nan_max(im, (fabs(up + uc) + fabs(uc + um)) * inv4h);
   }
   for (int o = 16; o > 0; o >>= 1) {
-    lo = fmin(lo, __shfl_down_sync(0xffffffffu, lo, o));
-    hi = fmax(hi, __shfl_down_sync(0xffffffffu, hi, o));
-    im = fmax(im, __shfl_down_sync(0xffffffffu, im, o));
+    lo = nan_min(lo, __shfl_down_sync(0xffffffffu, lo, o));
+    hi = nan_max(hi, __shfl_down_sync(0xffffffffu, hi, o));
+    im = nan_max(im, __shfl_down_sync(0xffffffffu, im, o));
   }
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   if (l == 0) { r0[w] = lo; r1[w] = hi; r2[w] = im; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int k = 1; k < 8; ++k) { lo = fmin(lo, r0[k]); hi = fmax(hi, r1[k]); im = fmax(im, r2[k]); }
+    for (int k = 1; k < 8; ++k) { lo = nan_min(lo, r0[k]); hi = nan_max(hi, r1[k]); im = nan_max(im, r2[k]); }
     bpart[3 * blockIdx.x + 0] = lo;
     bpart[3 * blockIdx.x + 1] = hi;
     bpart[3 * blockIdx.x + 2] = im;
@@ -301,14 +318,14 @@ __global__ void __launch_bounds__(256) k_frozen_bounds_final(double* bounds, con
   __shared__ double r0[8], r1[8], r2[8];
   double lo = 1e300, hi = -1e300, im = 0.0;
   for (int k = threadIdx.x; k < m; k += blockDim.x) {
-    lo = fmin(lo, bpart[3 * k]);
-    hi = fmax(hi, bpart[3 * k + 1]);
-    im = fmax(im, bpart[3 * k + 2]);
+    lo = nan_min(lo, bpart[3 * k]);
+    hi = nan_max(hi, bpart[3 * k + 1]);
+    im = nan_max(im, bpart[3 * k + 2]);
   }
   for (int o = 16; o > 0; o >>= 1) {
-    lo = fmin(lo, __shfl_down_sync(0xffffffffu, lo, o));
-    hi = fmax(hi, __shfl_down_sync(0xffffffffu, hi, o));
-    im = fmax(im, __shfl_down_sync(0xffffffffu, im, o));
+    lo = nan_min(lo, __shfl_down_sync(0xffffffffu, lo, o));
+    hi = nan_max(hi, __shfl_down_sync(0xffffffffu, hi, o));
+    im = nan_max(im, __shfl_down_sync(0xffffffffu, im, o));
   }
   const int w = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) {
@@ -319,9 +336,9 @@ __global__ void __launch_bounds__(256) k_frozen_bounds_final(double* bounds, con
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
-      lo = fmin(lo, r0[k]);
-      hi = fmax(hi, r1[k]);
-      im = fmax(im, r2[k]);
+      lo = nan_min(lo, r0[k]);
+      hi = nan_max(hi, r1[k]);
+      im = nan_max(im, r2[k]);
     }
     bounds[0] = lo;
     bounds[1] = hi;
@@ -991,7 +1008,7 @@ __global__ void __launch_bounds__(256) k_burgers_direct_cluster(BurgersDirectArg
   cluster.sync();  // no CTA leaves while a neighbour may still read its exchange buffers
 }
 
-inline int burgers_direct(const BurgersDirectArgs& a, cudaStream_t s, px_stats* stats) {
+inline int burgers_direct(const BurgersDirectArgs& a, cudaStream_t s, px_stats* stats, bool use_cluster) {
   if (a.nx > BURGERS_MAX_N) return PX_ERR_ARG;
   const size_t smem = 3 * (size_t)a.nx * sizeof(double);
   const int ppt = (a.nx + BURGERS_NT - 1) / BURGERS_NT;
@@ -1007,15 +1024,11 @@ inline int burgers_direct(const BurgersDirectArgs& a, cudaStream_t s, px_stats* 
     k_burgers_direct_run<PP><<<a.B, ((a.nx / PP + 31) / 32) * 32, sm2, s>>>(a);                \
   } while (0)
   // contiguous runs when n is a multiple of the run length (the strided kernel otherwise)
-  static const int rp_env = [] { const char* e = getenv("PX_BURGERS_RUN"); return e ? atoi(e) : 0; }();
-  int rp = ppt <= 1 ? 1 : (ppt <= 2 ? 2 : (ppt <= 4 ? 4 : 8));
-  if (rp_env == 1 || rp_env == 2 || rp_env == 4 || rp_env == 8) rp = std::max(rp, rp_env);
-  static const bool strided = [] { const char* e = getenv("PX_BURGERS_STRIDED"); return e && atoi(e) != 0; }();
+  const int rp = ppt <= 1 ? 1 : (ppt <= 2 ? 2 : (ppt <= 4 ? 4 : 8));
   // cluster sweep (8 CTAs per member, 64-point ghost zones refreshed every 16 steps) for the
   // larger grids
-  static const int bcl = [] { const char* e = getenv("PX_BURGERS_CLUSTER"); return e ? atoi(e) : 1; }();
   constexpr int kCS = 8, kPPT = 4, kG = 64;
-  if (bcl && !strided && a.nx >= 2048 && a.nx % (kCS * kPPT) == 0 && a.nx / kCS >= kG &&
+  if (use_cluster && a.nx >= 2048 && a.nx % (kCS * kPPT) == 0 && a.nx / kCS >= kG &&
       a.nx / kCS / kPPT + 2 * (kG / kPPT) <= 256) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.B * kCS));
@@ -1029,7 +1042,7 @@ inline int burgers_direct(const BurgersDirectArgs& a, cudaStream_t s, px_stats* 
     cfg.attrs = at;
     cfg.numAttrs = 1;
     if (cudaLaunchKernelEx(&cfg, k_burgers_direct_cluster<kPPT, kCS, kG>, a) != cudaSuccess) return PX_ERR_CUDA;
-  } else if (!strided && a.nx % rp == 0) {
+  } else if (a.nx % rp == 0) {
     if (rp == 1) PX_BR(1);
     else if (rp == 2) PX_BR(2);
     else if (rp == 4) PX_BR(4);
@@ -1057,7 +1070,8 @@ inline int burgers_direct(const BurgersDirectArgs& a, cudaStream_t s, px_stats* 
   return PX_OK;
 }
 
-inline int burgers_adjoint(const BurgersAdjointArgs& a, cudaStream_t s, px_stats* stats, const double** wend) {
+inline int burgers_adjoint(const BurgersAdjointArgs& a, cudaStream_t s, px_stats* stats, const double** wend,
+                           bool use_cluster) {
   if (a.nx > BURGERS_MAX_N) return PX_ERR_ARG;
   const int Pl = a.p_end - a.p_begin;
   const int ppt = (a.nx + BURGERS_NT - 1) / BURGERS_NT;
@@ -1096,12 +1110,10 @@ inline int burgers_adjoint(const BurgersAdjointArgs& a, cudaStream_t s, px_stats
     cudaFuncSetAttribute(k_burgers_scan_run<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2); \
     k_burgers_scan_run<PP><<<a.B, ((a.nx / PP + 31) / 32) * 32, sm2, s>>>(a, coef);                \
   } while (0)
-  static const bool strided_sc = [] { const char* e = getenv("PX_BURGERS_STRIDED"); return e && atoi(e) != 0; }();
   // cluster scan (8 CTAs per member, 64-point DSMEM ghost zones) for the larger grids
-  static const int bcl = [] { const char* e = getenv("PX_BURGERS_CLUSTER"); return e ? atoi(e) : 1; }();
   constexpr int kCS = 8, kPPT = 4, kG = 64;
   const int rps = ppt <= 1 ? 1 : (ppt <= 2 ? 2 : (ppt <= 4 ? 4 : 8));
-  if (bcl && !strided_sc && a.nx >= 2048 && a.nx % (kCS * kPPT) == 0 && a.nx / kCS >= kG &&
+  if (use_cluster && a.nx >= 2048 && a.nx % (kCS * kPPT) == 0 && a.nx / kCS >= kG &&
       a.nx / kCS / kPPT + 2 * (kG / kPPT) <= 256 && a.degree >= 1) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.B * kCS));
@@ -1116,7 +1128,7 @@ inline int burgers_adjoint(const BurgersAdjointArgs& a, cudaStream_t s, px_stats
     cfg.numAttrs = 1;
     if (cudaLaunchKernelEx(&cfg, k_burgers_scan_cluster<kPPT, kCS, kG>, a, (const double*)coef) != cudaSuccess)
       return PX_ERR_CUDA;
-  } else if (!strided_sc && a.nx % rps == 0) {
+  } else if (a.nx % rps == 0) {
     if (rps == 1) PX_BSR(1);
     else if (rps == 2) PX_BSR(2);
     else if (rps == 4) PX_BSR(4);

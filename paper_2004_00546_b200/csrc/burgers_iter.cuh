@@ -17,7 +17,7 @@
 #include <cuda_runtime.h>
 
 #include "burgers.cuh"
-#include "kernels.cuh"
+#include "common.cuh"
 
 namespace px {
 

@@ -17,10 +17,72 @@
 #pragma once
 #include <cuda_runtime.h>
 
-#include "kernels.cuh"
-#include "rk4.cuh"
+#include "common.cuh"
 
 namespace px {
+
+// ---------------------------------------------------------------------------
+// Chebyshev exponential action: stencil fused with the three-term recurrence
+// ---------------------------------------------------------------------------
+
+struct ChebFirstArgs {
+  const double* u0; long long u0_bstride;     // U_0 (batch-strided)
+  double* u1;                                 // U_1 = (M U_0 − c0 U_0)/d  (B × n)
+  double* acc;                                // b0 U_0 + b1 U_1 (+ addend)
+  const double* addend; long long add_bstride;  // may be nullptr
+  double* pacc;                               // += p0 U_0 + p1 U_1 (may be nullptr)
+  Stencil5 st;
+  double c0, d, b0, b1, p0, p1;
+  int nx, ny;
+};
+
+template <int DIM>
+__global__ void __launch_bounds__(256) k_cheb_first(ChebFirstArgs a) {
+  const size_t n = (size_t)a.nx * a.ny;
+  const int b = blockIdx.y;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int y = (int)(i / a.nx), x = (int)(i - (size_t)y * a.nx);
+  const double* u0 = a.u0 + b * a.u0_bstride;
+  const double u = u0[i];
+  const double v1 = (stencil_at<DIM>(u0, a.st, x, y, a.nx, a.ny) - a.c0 * u) / a.d;
+  const size_t o = (size_t)b * n + i;
+  a.u1[o] = v1;
+  double r = a.b0 * u + a.b1 * v1;
+  if (a.addend) r += a.addend[b * a.add_bstride + i];
+  a.acc[o] = r;
+  if (a.pacc) a.pacc[o] += a.p0 * u + a.p1 * v1;
+}
+
+struct ChebTermArgs {
+  const double* ucur; long long ucur_bstride;
+  const double* uprev; long long uprev_bstride;
+  double* unext;      // B × n
+  double* acc;        // B × n
+  double* pacc;       // may be nullptr
+  Stencil5 st;
+  double c0, two_over_d, sigma, bk, pk;
+  int nx, ny;
+};
+
+template <int DIM>
+__global__ void __launch_bounds__(256) k_cheb_term(ChebTermArgs a) {
+  const size_t n = (size_t)a.nx * a.ny;
+  const int b = blockIdx.y;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int y = (int)(i / a.nx), x = (int)(i - (size_t)y * a.nx);
+  const double* uc = a.ucur + b * a.ucur_bstride;
+  const double* up = a.uprev + b * a.uprev_bstride;
+  const double u = uc[i];
+  const double un = a.two_over_d * (stencil_at<DIM>(uc, a.st, x, y, a.nx, a.ny) - a.c0 * u) +
+                    a.sigma * up[i];
+  const size_t o = (size_t)b * n + i;
+  a.unext[o] = un;
+  a.acc[o] += a.bk * un;
+  if (a.pacc) a.pacc[o] += a.pk * un;
+}
+
 
 constexpr int CM_NT = 160;  // 5 warps, pairs of columns: computed width ≤ 320 (192 measured slower)
 constexpr int CM_MAXT = 6;  // terms per pass (template M ≤ CM_MAXT; 7+ would need 1 CTA/SM, ≥ 10 spill)
@@ -54,10 +116,10 @@ struct CmRing {  // acc/pacc row slots (≥ M live rows; UN % R == 0)
   static constexpr int value = (M <= 3) ? M : (M == 4 ? 4 : 6);
 };
 
-// SG: the recurrence sign σ (±1) as a compile-time constant (0: runtime a.sigma);
-// TM: row ring filled by 1D bulk copies (TMA engine) issued by one thread and completing
-// on per-slot mbarriers, refilled after the row barrier; otherwise per-thread cp.async.
-template <int M, int SG = 0, bool TM = false>
+// SG: the recurrence sign σ (±1) as a compile-time constant (0: runtime a.sigma). The row
+// ring is filled by per-thread cp.async (a one-thread TMA bulk-copy ring issued after the
+// row barrier was measured 15% slower on the scan's short bands).
+template <int M, int SG = 0>
 __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) {
   __shared__ double pubE[2][M][CM_NT];
   __shared__ double pubO[2][M][CM_NT];
@@ -98,7 +160,6 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
     else if constexpr (SG == -1) return -v;
     else return sig * v;
   };
-  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(cm_ring + (size_t)CM_DEPTH * 4 * CM_NT);
   const double* __restrict__ cur = a.u_cur + b * a.cur_bs;
   const double* __restrict__ prv = first ? cur : a.u_prev + b * a.prev_bs;
   const double* __restrict__ accin = has_add ? a.addend + b * a.add_bs : a.acc + (size_t)b * n;
@@ -116,51 +177,23 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
   const size_t coloff = (size_t)gx;
   int iss_k = 0, iss_slot = 0;
   int rc = wrapr(r0), rl = wrapr(r0 - 1);  // streams: cur row r, lagged rows r−1
-  const int gx0 = (((x0 - a.halo) % nx) + nx) % nx;
-  const int lenA = min(CW, nx - gx0);  // columns before the periodic wrap
-  const unsigned row_bytes = (unsigned)CW * 8u;
   auto issue = [&]() {
-    if constexpr (TM) {
-      if (t == 0 && iss_k < iters) {
-        double* sl = reinterpret_cast<double*>(cm_ring + (size_t)iss_slot * 4 * CM_NT);
-        unsigned long long* bar = mbar + iss_slot;
-        const double* rows[4] = {cur + (size_t)rc * nx, prv + (size_t)rl * nx, accin + (size_t)rl * nx,
-                                 has_p ? pac + (size_t)rl * nx : nullptr};
-        const bool use[4] = {true, !first, read_acc, has_p};
-        mbar_expect_tx(bar, row_bytes * (unsigned)(1 + (!first) + read_acc + has_p));
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (use[q]) {
-            double* dst = sl + q * 2 * CM_NT;
-            bulk_g2s(dst, rows[q] + gx0, (unsigned)lenA * 8u, bar);
-            if (lenA < CW) bulk_g2s(dst + lenA, rows[q], (unsigned)(CW - lenA) * 8u, bar);
-          }
-        }
-      }
-    } else if (iss_k < iters) {
+    if (iss_k < iters) {
       double2* sl = cm_ring + (size_t)iss_slot * 4 * CM_NT;
       cp_async16(sl + t, cur + (size_t)rc * nx + coloff);
       if (!first) cp_async16(sl + CM_NT + t, prv + (size_t)rl * nx + coloff);
       if (read_acc) cp_async16(sl + 2 * CM_NT + t, accin + (size_t)rl * nx + coloff);
       if (has_p) cp_async16(sl + 3 * CM_NT + t, pac + (size_t)rl * nx + coloff);
     }
-    if constexpr (!TM) cp_async_commit();
+    cp_async_commit();
     ++iss_k;
     iss_slot = (iss_slot + 1 == CM_DEPTH) ? 0 : iss_slot + 1;
     rc = (rc + 1 == ny) ? 0 : rc + 1;
     rl = (rl + 1 == ny) ? 0 : rl + 1;
   };
-  if constexpr (TM) {
-    if (t == 0) {
-      for (int k = 0; k < CM_DEPTH; ++k) mbar_init(mbar + k, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-  }
 #pragma unroll
   for (int k = 0; k < CM_DEPTH; ++k) issue();
   int rslot = 0;
-  unsigned rphase = 0;
   int rs = wrapr(r0 - M);  // output row r − M
 
   double2 q0[3];               // U_k rows (ring by phase mod 3)
@@ -194,16 +227,14 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
     constexpr bool G = decltype(gc)::value;
       const int pin = (k + 1) & 1;
       const int pout = k & 1;
-      if constexpr (TM) mbar_wait(mbar + rslot, rphase);
-      else cp_async_wait<CM_DEPTH - 1>();
+      cp_async_wait<CM_DEPTH - 1>();
       const double2* sl = cm_ring + (size_t)rslot * 4 * CM_NT;
       rslot = (rslot + 1 == CM_DEPTH) ? 0 : rslot + 1;
-      if (TM && rslot == 0) rphase ^= 1u;
       const double2 ur = sl[t];
       const double2 upv = first ? make_double2(0.0, 0.0) : sl[CM_NT + t];
       const double2 ain = read_acc ? sl[2 * CM_NT + t] : make_double2(0.0, 0.0);
       const double2 pin_v = has_p ? sl[3 * CM_NT + t] : make_double2(0.0, 0.0);
-      if constexpr (!TM) issue();
+      issue();
       q0[k % 3] = ur;
       const double2 u0m2 = q0[(k + 1) % 3], u0m1 = q0[(k + 2) % 3];  // rows r−2, r−1
       const int po = k & 1, pp = (k + 1) & 1;  // qs[s][po]: row of iteration i−2, [pp]: i−1
@@ -272,7 +303,6 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
         }
       }
       __syncthreads();
-      if constexpr (TM) issue();  // every thread has read this iteration's slot: refill it
   };
   int i0 = 0;
   // fill (stages switch on at i = 2, 4, …, 2M) — guarded groups until every stage is live
@@ -310,9 +340,9 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
     if (i0 + 10 < iters) iter(IC<10>{}, BC<true>{}, i0 + 10);
     if (i0 + 11 < iters) iter(IC<11>{}, BC<true>{}, i0 + 11);
   }
-  if constexpr (!TM) cp_async_wait<0>();
+  cp_async_wait<0>();
 }
 
-constexpr size_t CM_SMEM = (size_t)CM_DEPTH * 4 * CM_NT * sizeof(double2) + CM_DEPTH * sizeof(unsigned long long);
+constexpr size_t CM_SMEM = (size_t)CM_DEPTH * 4 * CM_NT * sizeof(double2);
 
 }  // namespace px

@@ -3,9 +3,6 @@
 // Replaces the reference's per-stage Python/scipy arithmetic:
 //   rk45_integrate stage loop (timestepping.py:162-201) + csr_matvec (linalg.py:70-74)
 //     -> rk4.cuh (row-marching fused RK4 steps over all batch × slice lanes);
-//   _LejaInterpolant.step Newton loop (timestepping.py:343-356)
-//     -> k_cheb_first / k_cheb_term: stencil fused with the Chebyshev three-term
-//        recurrence and the exp and φ₁ accumulators;
 //   superposition / cost / gradient quadrature (paraexp.py:202-218,
 //   optimization.py:84-112) -> elementwise, reduction and projection kernels with
 //   fixed-order (deterministic) reductions.
@@ -14,98 +11,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "common.cuh"
+
 namespace px {
-
-struct Stencil5 {
-  double cc, ce, cw, cn, cs;
-};
-
-// periodic wrap for halo coordinates (tiles may be wider than the grid)
-__device__ __forceinline__ int wrapi(int v, int n) {
-  v %= n;
-  return v < 0 ? v + n : v;
-}
-
-// (M u) at flat index i of a periodic nx×ny field (global memory, L1/L2 cached).
-template <int DIM>
-__device__ __forceinline__ double stencil_at(const double* __restrict__ u, const Stencil5& s,
-                                             int x, int y, int nx, int ny) {
-  const size_t row = (size_t)y * nx;
-  const int xe = (x + 1 == nx) ? 0 : x + 1;
-  const int xw = (x == 0) ? nx - 1 : x - 1;
-  double r = s.cc * u[row + x];
-  r += s.ce * __ldg(u + row + xe);
-  r += s.cw * __ldg(u + row + xw);
-  if (DIM == 2) {
-    const int yn = (y + 1 == ny) ? 0 : y + 1;
-    const int ys = (y == 0) ? ny - 1 : y - 1;
-    r += s.cn * __ldg(u + (size_t)yn * nx + x);
-    r += s.cs * __ldg(u + (size_t)ys * nx + x);
-  }
-  return r;
-}
-
-// ---------------------------------------------------------------------------
-// Chebyshev exponential action: stencil fused with the three-term recurrence
-// ---------------------------------------------------------------------------
-
-struct ChebFirstArgs {
-  const double* u0; long long u0_bstride;     // U_0 (batch-strided)
-  double* u1;                                 // U_1 = (M U_0 − c0 U_0)/d  (B × n)
-  double* acc;                                // b0 U_0 + b1 U_1 (+ addend)
-  const double* addend; long long add_bstride;  // may be nullptr
-  double* pacc;                               // += p0 U_0 + p1 U_1 (may be nullptr)
-  Stencil5 st;
-  double c0, d, b0, b1, p0, p1;
-  int nx, ny;
-};
-
-template <int DIM>
-__global__ void __launch_bounds__(256) k_cheb_first(ChebFirstArgs a) {
-  const size_t n = (size_t)a.nx * a.ny;
-  const int b = blockIdx.y;
-  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int y = (int)(i / a.nx), x = (int)(i - (size_t)y * a.nx);
-  const double* u0 = a.u0 + b * a.u0_bstride;
-  const double u = u0[i];
-  const double v1 = (stencil_at<DIM>(u0, a.st, x, y, a.nx, a.ny) - a.c0 * u) / a.d;
-  const size_t o = (size_t)b * n + i;
-  a.u1[o] = v1;
-  double r = a.b0 * u + a.b1 * v1;
-  if (a.addend) r += a.addend[b * a.add_bstride + i];
-  a.acc[o] = r;
-  if (a.pacc) a.pacc[o] += a.p0 * u + a.p1 * v1;
-}
-
-struct ChebTermArgs {
-  const double* ucur; long long ucur_bstride;
-  const double* uprev; long long uprev_bstride;
-  double* unext;      // B × n
-  double* acc;        // B × n
-  double* pacc;       // may be nullptr
-  Stencil5 st;
-  double c0, two_over_d, sigma, bk, pk;
-  int nx, ny;
-};
-
-template <int DIM>
-__global__ void __launch_bounds__(256) k_cheb_term(ChebTermArgs a) {
-  const size_t n = (size_t)a.nx * a.ny;
-  const int b = blockIdx.y;
-  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int y = (int)(i / a.nx), x = (int)(i - (size_t)y * a.nx);
-  const double* uc = a.ucur + b * a.ucur_bstride;
-  const double* up = a.uprev + b * a.uprev_bstride;
-  const double u = uc[i];
-  const double un = a.two_over_d * (stencil_at<DIM>(uc, a.st, x, y, a.nx, a.ny) - a.c0 * u) +
-                    a.sigma * up[i];
-  const size_t o = (size_t)b * n + i;
-  a.unext[o] = un;
-  a.acc[o] += a.bk * un;
-  if (a.pacc) a.pacc[o] += a.pk * un;
-}
 
 // ---------------------------------------------------------------------------
 // Elementwise helpers (batch in blockIdx.y)
@@ -143,36 +51,10 @@ __global__ void k_apply_plus_control(double* out, const double* src, long long s
   out[(size_t)b * n + i] = r;
 }
 
-// out[b][i] = Σ_{p<lanes_per_b} lanes[b*lanes_per_b + p][i]  (fixed order)
-__global__ void k_lane_sum(double* out, const double* lanes, int lanes_per_b, size_t n) {
-  const int b = blockIdx.y;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const double* src = lanes + (size_t)b * lanes_per_b * n + i;
-    double r = 0.0;
-    for (int p = 0; p < lanes_per_b; ++p) r += src[(size_t)p * n];
-    out[(size_t)b * n + i] = r;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Deterministic reductions
 // ---------------------------------------------------------------------------
 
-template <int NT>
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  double r = 0.0;
-  if (threadIdx.x < 32) {
-    r = (threadIdx.x < NT / 32) ? red[threadIdx.x] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
-  }
-  __syncthreads();
-  return r;  // valid in thread 0
-}
 
 // partial[b][blk] = Σ_{i in blk's grid-stride set} x[b][i]²
 __global__ void __launch_bounds__(256) k_sumsq_partial(double* partial, const double* x, size_t n) {

@@ -16,11 +16,10 @@
 #include <string>
 
 #include "../../include/paraexp.h"
-#include "kernels.cuh"
+#include "common.cuh"
 
 namespace px {
 
-constexpr int KRYLOV_MAX_M = 40;
 constexpr double KRYLOV_BREAKDOWN = 1e-13;
 #ifndef PX_KR_PPT
 #define PX_KR_PPT 4
@@ -28,17 +27,6 @@ constexpr double KRYLOV_BREAKDOWN = 1e-13;
 constexpr int KR_PPT = PX_KR_PPT;     // points per thread in the Arnoldi passes
 constexpr int KR_BLK = 256 * KR_PPT;  // points per block
 
-struct KrylovWork {
-  int m = 0, B = 0, nblk = 0;
-  size_t n = 0;
-  double* V = nullptr;        // (m+1) × B × n
-  double* w = nullptr;        // 2 × B × n (ping-pong: step j's w feeds V_{j+1} at step j+1)
-  double* H = nullptr;        // B × (m+1) × m   (row i, col j at i*m + j)
-  double* hcol = nullptr;     // B × (MAX_M+1)  current column pass values
-  double* part = nullptr;     // B × (MAX_M+1) × nblk partial dots
-  double* beta = nullptr;     // B
-  double* coef = nullptr;     // B × 2 × m  (exp column, φ column), β-scaled
-};
 
 inline int krylov_alloc(KrylovWork& kw, int m, size_t n, int B, std::string* err) {
   kw.m = m;

@@ -34,7 +34,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
-#include "kernels.cuh"
+#include "common.cuh"
 
 namespace px {
 
@@ -58,16 +58,6 @@ struct MarchArgs {
   // k_rk4_march2: stage-scaled stencil k·(cc, ce, cw, cs, cn) for k = h/4, h/3, h/2, h
   double kc[4][5];
 };
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
 
 // Row ring: each thread streams its own column pair of the y, b (and z) rows
 // MARCH_DEPTH rows ahead with cp.async (LDGSTS) into shared memory, so ~6 rows
@@ -384,47 +374,15 @@ __global__ void k_lane_sum_plus(double* out, const double* lanes, int lanes_per_
 // cost of 8 pipelined stages of register queues (one CTA per SM). Same
 // arithmetic per step as k_rk4_march.
 // ---------------------------------------------------------------------------
-// --- 1D bulk copies (TMA engine, cp.async.bulk) completing on an mbarrier -------------
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(a),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, unsigned long long* bar) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
-  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(d),
-               "l"(gmem), "r"(bytes), "r"(b)
-               : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-
-template <int V> struct IC { static constexpr int value = V; };
-template <bool V> struct BC { static constexpr bool value = V; };
-
 // NT threads (2 columns each), DEPTH ring rows of y(r), b(r−4), b(r−8), z(r−8)
-template <bool ADJ, int M2_NT, int M2_DEPTH, int MINB, bool TMA, bool ZREG = false>
+template <bool ADJ, int M2_NT, int M2_DEPTH, int MINB>
 __global__ void __launch_bounds__(M2_NT, MINB) k_rk4_march2(MarchArgs a) {
   constexpr int NQ = ADJ ? 4 : 3;
   extern __shared__ double2 dyn2[];
   double2* ring2 = dyn2;                                                        // [M2_DEPTH][NQ][M2_NT]
   double (*pubE)[8][M2_NT] = reinterpret_cast<double (*)[8][M2_NT]>(dyn2 + M2_DEPTH * NQ * M2_NT);
   double (*pubO)[8][M2_NT] = pubE + 2;
-  double2* zs = reinterpret_cast<double2*>(pubE + 4);                           // [6][M2_NT]: h·w3 rows
-  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(zs + (ADJ ? 6 * M2_NT : 0));  // [M2_DEPTH]
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(pubE + 4);  // [M2_DEPTH]
 
   const int lane = blockIdx.x % a.lanes;
   const int rest = blockIdx.x / a.lanes;
@@ -481,37 +439,26 @@ __global__ void __launch_bounds__(M2_NT, MINB) k_rk4_march2(MarchArgs a) {
   int ry = wrapr(r0), rb4 = wrapr(r0 - 4), rb8 = wrapr(r0 - 8);
   // TMA ring: one thread copies each stream's row segment [x0 − halo, x0 + U + halo) (two
   // pieces when it wraps the periodic x boundary) into the slot; completion on the
-  // slot's mbarrier. Otherwise every thread cp.async's its own 16 bytes.
+  // slot's mbarrier (a per-thread cp.async ring was measured slower).
   const int gx0 = (((x0 - a.halo) % nx) + nx) % nx;
   const int lenA = min(CW, nx - gx0);  // columns before the wrap
   const unsigned row_bytes = (unsigned)CW * 8u;
   auto issue = [&]() {
-    if constexpr (TMA) {
-      if (t == 0 && iss_k < iters) {
-        double2* slot = ring2 + (size_t)iss_slot * NQ * M2_NT;
-        unsigned long long* bar = mbar + iss_slot;
-        const int nq = zread ? 4 : 3;
-        mbar_expect_tx(bar, row_bytes * (unsigned)nq);
-        const double* rows[4] = {ysrc + (size_t)ry * nx, bsrc + (size_t)rb4 * nx, bsrc + (size_t)rb8 * nx,
-                                 zread ? zl + (size_t)rb8 * nx : nullptr};
+    if (t == 0 && iss_k < iters) {
+      double2* slot = ring2 + (size_t)iss_slot * NQ * M2_NT;
+      unsigned long long* bar = mbar + iss_slot;
+      const int nq = zread ? 4 : 3;
+      mbar_expect_tx(bar, row_bytes * (unsigned)nq);
+      const double* rows[4] = {ysrc + (size_t)ry * nx, bsrc + (size_t)rb4 * nx, bsrc + (size_t)rb8 * nx,
+                               zread ? zl + (size_t)rb8 * nx : nullptr};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (q < nq) {
-            double2* dst = slot + q * M2_NT;
-            bulk_g2s(dst, rows[q] + gx0, (unsigned)lenA * 8u, bar);
-            if (lenA < CW) bulk_g2s(reinterpret_cast<double*>(dst) + lenA, rows[q], (unsigned)(CW - lenA) * 8u, bar);
-          }
+      for (int q = 0; q < 4; ++q) {
+        if (q < nq) {
+          double2* dst = slot + q * M2_NT;
+          bulk_g2s(dst, rows[q] + gx0, (unsigned)lenA * 8u, bar);
+          if (lenA < CW) bulk_g2s(reinterpret_cast<double*>(dst) + lenA, rows[q], (unsigned)(CW - lenA) * 8u, bar);
         }
       }
-    } else {
-      if (iss_k < iters) {
-        double2* slot = ring2 + (size_t)iss_slot * NQ * M2_NT;
-        cp_async16(slot + t, ysrc + (size_t)ry * nx + coloff);
-        cp_async16(slot + M2_NT + t, bsrc + (size_t)rb4 * nx + coloff);
-        cp_async16(slot + 2 * M2_NT + t, bsrc + (size_t)rb8 * nx + coloff);
-        if (zread) cp_async16(slot + 3 * M2_NT + t, zl + (size_t)rb8 * nx + coloff);
-      }
-      cp_async_commit();
     }
     ++iss_k;
     iss_slot = (iss_slot + 1 == M2_DEPTH) ? 0 : iss_slot + 1;
@@ -519,23 +466,21 @@ __global__ void __launch_bounds__(M2_NT, MINB) k_rk4_march2(MarchArgs a) {
     rb4 = (rb4 + 1 == ny) ? 0 : rb4 + 1;
     rb8 = (rb8 + 1 == ny) ? 0 : rb8 + 1;
   };
-  if constexpr (TMA) {
-    if (t == 0) {
-      for (int k = 0; k < M2_DEPTH; ++k) mbar_init(mbar + k, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
+  if (t == 0) {
+    for (int k = 0; k < M2_DEPTH; ++k) mbar_init(mbar + k, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  __syncthreads();
 
 #pragma unroll
   for (int k = 0; k < M2_DEPTH; ++k) issue();
   int rslot = 0;
-  unsigned rphase = 0;  // TMA: parity of the slot's current fill
+  unsigned rphase = 0;  // parity of the slot's current fill
   int rs = wrapr(r0 - 8);  // output row r − 8
 
   // rings (phase k = i mod 6): y rows r-4..r, y⁺ rows r-8..r-4, h·w3 rows r-8..r-3
   double2 yq[6], pq[6];
-  double2 zq[6];  // ZREG: h·w3 rows r-8..r-3 in registers instead of smem (20 B of spill, 3% faster)
+  double2 zq[6];  // h·w3 rows r-8..r-3 in registers (measured 3% faster than a shared-memory ring)
 #pragma unroll
   for (int k = 0; k < 6; ++k) zq[k] = make_double2(0.0, 0.0);
   double2 wq[8][2];  // stage outputs w1,w2,w3 (1..3) and w5,w6,w7 (5..7): last two rows
@@ -551,19 +496,14 @@ __global__ void __launch_bounds__(M2_NT, MINB) k_rk4_march2(MarchArgs a) {
     constexpr bool G = decltype(gc)::value;
       const int pin = (k + 1) & 1, pout = k & 1;
       const int po = k & 1, pp = (k + 1) & 1;
-      if constexpr (TMA) {
-        mbar_wait(mbar + rslot, rphase);
-      } else {
-        cp_async_wait<M2_DEPTH - 1>();
-      }
+      mbar_wait(mbar + rslot, rphase);
       const double2* slot = ring2 + (size_t)rslot * NQ * M2_NT;
       rslot = (rslot + 1 == M2_DEPTH) ? 0 : rslot + 1;
-      if (TMA && rslot == 0) rphase ^= 1u;
+      if (rslot == 0) rphase ^= 1u;
       const double2 yr = slot[t];
       const double2 b4 = slot[M2_NT + t];
       const double2 b8 = slot[2 * M2_NT + t];
       const double2 zrow = zread ? slot[3 * M2_NT + t] : make_double2(0.0, 0.0);
-      if constexpr (!TMA) issue();
       yq[k] = yr;
       const double2 y0 = yq[(k + 2) % 6], y1 = yq[(k + 3) % 6], y2 = yq[(k + 4) % 6], y3 = yq[(k + 5) % 6];
       double2 nw[9];
@@ -580,10 +520,7 @@ __global__ void __launch_bounds__(M2_NT, MINB) k_rk4_march2(MarchArgs a) {
       }
       if (!G || i >= 6) {
         nw[3] = stage(IC<2>{}, y1, wq[2][pp], wq[2][po], nw[2], pubO[pin][2][tl], pubE[pin][2][tr]);
-        if (ADJ) {
-          if constexpr (ZREG) zq[(k + 3) % 6] = make_double2(h * nw[3].x, h * nw[3].y);  // row r-3
-          else zs[((k + 3) % 6) * M2_NT + t] = make_double2(h * nw[3].x, h * nw[3].y);
-        }
+        if (ADJ) zq[(k + 3) % 6] = make_double2(h * nw[3].x, h * nw[3].y);  // row r-3
       }
       if (!G || i >= 8) {  // y⁺ at row r-4
         nw[4] = stage(IC<3>{}, make_double2(y0.x + b4.x, y0.y + b4.y), wq[3][pp], wq[3][po], nw[3],
@@ -609,7 +546,7 @@ __global__ void __launch_bounds__(M2_NT, MINB) k_rk4_march2(MarchArgs a) {
           const size_t off = (size_t)rs * nx + coloff;
           __stcs(reinterpret_cast<double2*>(yout + off), yn);
           if (ADJ) {
-            const double2 za = ZREG ? zq[(k + 4) % 6] : zs[((k + 4) % 6) * M2_NT + t];  // h·w3 at row r-8
+            const double2 za = zq[(k + 4) % 6];  // h·w3 at row r-8
             double2 zn;
             zn.x = zrow.x + za.x + h * w7c.x;
             zn.y = zrow.y + za.y + h * w7c.y;
@@ -632,10 +569,8 @@ __global__ void __launch_bounds__(M2_NT, MINB) k_rk4_march2(MarchArgs a) {
         pubE[pout][7][t] = nw[7].x;  pubO[pout][7][t] = nw[7].y;
       }
       __syncthreads();
-      if constexpr (TMA) {  // every thread has read this iteration's slot: refill it
-        if (t == 0) fence_proxy_async_smem();
-        issue();
-      }
+      if (t == 0) fence_proxy_async_smem();  // every thread has read this iteration's slot: refill it
+      issue();
   };
   int i0 = 0;
   // fill: the first 18 iterations (stages switch on at i = 2, 4, …, 16)
@@ -658,7 +593,6 @@ __global__ void __launch_bounds__(M2_NT, MINB) k_rk4_march2(MarchArgs a) {
   if (i0 + 3 < iters) iter(IC<3>{}, BC<true>{}, i0 + 3);
   if (i0 + 4 < iters) iter(IC<4>{}, BC<true>{}, i0 + 4);
   if (i0 + 5 < iters) iter(IC<5>{}, BC<true>{}, i0 + 5);
-  if constexpr (!TMA) cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------
@@ -674,10 +608,11 @@ struct ColV {
   double v[NC];
 };
 
-template <int NC, int NT, int DEP, int MINB, bool BR = false, bool PF = true, bool S2 = true>
+template <int NC, int NT, int DEP, int MINB, bool BR = true, bool S2 = true>
 __global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
   // BR: b(r−8) from a register ring of b(r−4) rows (two streams instead of three)
-  // PF: proxy fence before refilling a slot
+  // (no proxy fence before a slot refill: the slot's generic-proxy reads are complete at
+  // the barrier, and write-after-read needs no cross-proxy fence)
   // S2: two RK4 steps per launch; otherwise one (the odd remainder step of a sweep)
   constexpr int NQ = (BR || !S2) ? 2 : 3;
   constexpr int LAG = S2 ? 8 : 4;  // pipeline depth in rows (output row r − LAG)
@@ -868,7 +803,6 @@ __global__ void __launch_bounds__(NT, MINB) k_rk4_marchc(MarchArgs a) {
       pubO[pout][s][t] = nw[s].v[NC - 1];
     }
     __syncthreads();
-    if (PF && t == 0) fence_proxy_async_smem();
     issue();
   };
   int i0 = 0;
@@ -901,7 +835,7 @@ inline size_t marchc_smem(bool br) {
 template <int M2_NT, int M2_DEPTH>
 inline size_t march2_smem(bool adj) {
   return (size_t)M2_DEPTH * (adj ? 4 : 3) * M2_NT * sizeof(double2) + 4 * 8 * M2_NT * sizeof(double) +
-         (adj ? 6 * M2_NT * sizeof(double2) : 0) + M2_DEPTH * sizeof(unsigned long long);
+         M2_DEPTH * sizeof(unsigned long long);
 }
 
 }  // namespace px

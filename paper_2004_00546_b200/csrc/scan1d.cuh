@@ -15,7 +15,7 @@
 
 #include <cooperative_groups.h>
 
-#include "kernels.cuh"
+#include "common.cuh"
 
 namespace px {
 

@@ -12,6 +12,7 @@ buffers when ``world > 1``.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -75,10 +76,18 @@ class EngineSpec:
     nl_max_iter: int = 25
     nl_min_iter: int = 2
     local_blocks: int = 0       # 0: automatic (concurrent block carries for Krylov); 1: sequential scan
+    variants: tuple = ()        # ((name, value), …) kernel variants (_native.VARIANTS), e.g. (("march2", 2),)
+    z_accum: bool = False       # 2D adjoint ∫ by a per-lane accumulator instead of the closed form
 
     @property
     def nsteps(self) -> int:
         return slice_steps(self.system.spec.T / self.P, self.dt)
+
+
+# developer overrides of the kernel variants (tools/ experiments); tests use EngineSpec.variants
+ENV_VARIANTS = {"PX_MARCH2": "march2", "PX_M2_COLS": "march_cols", "PX_M2_BAND": "march_band",
+                "PX_CM_TERMS": "cheb_terms", "PX_CM_STRIP": "cheb_strip", "PX_CM_BAND": "cheb_band",
+                "PX_SCAN1D_CLUSTER": "scan1d_cluster", "PX_BURGERS_CLUSTER": "burgers_cluster"}
 
 
 def allreduce_sum(tensors, group=None) -> None:
@@ -152,7 +161,8 @@ class ParaexpEngine:
         krylov = isinstance(spec.expaction, KrylovConfig)
         d.expaction = N.PX_EXP_KRYLOV if krylov else N.PX_EXP_CHEBYSHEV
         d.krylov_m = spec.expaction.m if krylov else 0
-        d.flags = N.PX_FLAG_BOUNDARY_STATES if spec.boundary_states else 0
+        d.flags = (N.PX_FLAG_BOUNDARY_STATES if spec.boundary_states else 0) | (
+            N.PX_FLAG_Z_ACCUM if spec.z_accum or os.environ.get("PX_Z_ACCUM") == "1" else 0)
         self._desc = d
         torch = _torch()
         if torch is not None and torch.cuda.is_available():
@@ -164,6 +174,11 @@ class ParaexpEngine:
         h = ctypes.c_void_p()
         N.check(self.lib, self.lib.px_create(ctypes.byref(d), ctypes.byref(h)))
         self.h = h
+        for env, name in ENV_VARIANTS.items():
+            if os.environ.get(env):
+                self.set_variant(name, int(os.environ[env]))
+        for name, value in spec.variants:
+            self.set_variant(name, value)
         tx, _a = N.dptr(sysm.basis.tx)
         ty, _b = N.dptr(sysm.basis.ty)
         ix, _c = N.iptr(sysm.basis.ix)
@@ -199,12 +214,9 @@ class ParaexpEngine:
         blocks for the Krylov path (its Arnoldi kernels are latency-bound and leave the GPU
         mostly idle, and a Krylov long span costs ≈ 1/8 of the slices it spans); the
         Chebyshev march already fills the GPU and stays sequential. PX_LOCAL_BLOCKS overrides."""
-        import os
         spec = self.spec
         env = os.environ.get("PX_LOCAL_BLOCKS")
         want = int(env) if env else spec.local_blocks
-        if os.environ.get("PX_KRYLOV_COOP") == "1":
-            return 1  # concurrent cooperative grids could not all be co-resident
         if want == 0:
             want = 4 if isinstance(spec.expaction, KrylovConfig) else 1
         if self.spec.system.grid.dim != 2 or spec.boundary_states:
@@ -213,6 +225,17 @@ class ParaexpEngine:
         while want > 1 and Pl % want:
             want -= 1
         return want
+
+    def set_variant(self, name: str, value: int) -> None:
+        """Select a kernel variant of this handle (``_native.VARIANTS``; px_set_variant)."""
+        if name not in N.VARIANTS:
+            raise ValueError(f"unknown kernel variant {name!r}; known: {sorted(N.VARIANTS)}")
+        N.check(self.lib, self.lib.px_set_variant(self.h, N.VARIANTS[name], int(value)), self.h)
+
+    def variant(self, name: str) -> int:
+        v = ctypes.c_int()
+        N.check(self.lib, self.lib.px_get_variant(self.h, N.VARIANTS[name], ctypes.byref(v)), self.h)
+        return int(v.value)
 
     # -- plans ---------------------------------------------------------------
 

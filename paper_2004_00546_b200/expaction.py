@@ -27,7 +27,7 @@ needs ∫ q† dt, i.e. τ·φ₁(τB)·C alongside exp(τB)·C (SURVEY.md App. 
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 from functools import lru_cache
 
 import numpy as np
@@ -45,12 +45,19 @@ class ChebyshevConfig:
     tol: float = 1e-12
     max_degree: int = 120
     substep_limit: int = 1 << 16
+    # 0: ``tol`` bounds each action. > 0: ``tol`` is the error budget of the composite
+    # propagation over this horizon (the P sequential slice carries of a sweep): an action of
+    # span τ is planned to tol·(τ/horizon)/HORIZON_MARGIN, so the scan and every block-scan
+    # decomposition of it agree to well below ``tol`` (SURVEY §8(e) G-invariance)
+    horizon: float = 0.0
 
     def __post_init__(self):
         if self.tol <= 0:
             raise ValueError("tol must be positive")
         if self.max_degree < 2:
             raise ValueError("max_degree must be at least 2")
+        if self.horizon < 0:
+            raise ValueError("horizon must be non-negative")
 
 
 @dataclass(frozen=True)
@@ -60,12 +67,15 @@ class KrylovConfig:
     m: int = 30
     tol: float = 1e-10
     substep_limit: int = 1 << 16
+    horizon: float = 0.0  # as ChebyshevConfig.horizon
 
     def __post_init__(self):
         if self.m < 2:
             raise ValueError("need at least 2 Krylov vectors")
         if self.tol <= 0:
             raise ValueError("tol must be positive")
+        if self.horizon < 0:
+            raise ValueError("horizon must be non-negative")
 
 
 @dataclass(frozen=True)
@@ -341,11 +351,24 @@ def chained(plan, k: int):
                     err_bound=plan.err_bound * k)
 
 
+HORIZON_MARGIN = 10.0
+
+
+def action_config(cfg, span: float):
+    """The per-action settings for an action of ``span``: ``cfg`` itself, or with a
+    horizon budget (``cfg.horizon`` > 0) the tolerance tol·(span/horizon)/HORIZON_MARGIN."""
+    if cfg.horizon <= 0:
+        return cfg
+    return replace(cfg, tol=cfg.tol * min(1.0, span / cfg.horizon) / HORIZON_MARGIN, horizon=0.0)
+
+
 def plan_for(region: SpectralRegion, span: float, cfg, base_span: float | None = None):
     """Plan for ``span``; when ``span`` is an integer multiple k of ``base_span``
     (block-scan long spans are multiples of the slice width), the k-fold chained
-    base plan is also considered and the cheaper feasible plan is returned."""
-    one = plan_krylov if isinstance(cfg, KrylovConfig) else plan_chebyshev
+    base plan is also considered and the cheaper feasible plan is returned. A horizon
+    budget (``cfg.horizon``) is split over the actions in proportion to their spans."""
+    one_cfg = plan_krylov if isinstance(cfg, KrylovConfig) else plan_chebyshev
+    one = lambda reg, sp, c: one_cfg(reg, sp, action_config(c, sp))
     k = None
     if base_span is not None and span > base_span:
         q = span / base_span

@@ -45,7 +45,8 @@ def test_bindings_cover_the_header(lib):
 
 
 def test_abi_version_and_build_info(lib):
-    assert lib.px_abi_version() == 1
+    from paper_2004_00546_b200 import _native as N
+    assert lib.px_abi_version() == N.ABI_VERSION == 2
     assert b"sm_100a" in lib.px_build_info()
 
 
