@@ -106,22 +106,71 @@ def test_1d_cluster_scan_widths(nx):
     _check(_gpu_linear(c), _oracle_linear(c))
 
 
-def test_config2_descent_two_steps():
+def test_config2_descent_all_steps():
+    """Config 2's full loop: 20 steepest-descent iterations of the batch of 16 controls
+    (`optimization.py:242-281`) against the oracle's 20 iterations, every J and the final
+    controls."""
     from oracle.config_mode import linear_gradient
     from paper_2004_00546_b200 import RK4Config, baseline, descend
     c = baseline(2)
+    assert c.descent_steps == 20 and c.batch == 16
     u0, ut, ctrl = c.inputs()
-    res = descend(c.system, ctrl, ut, steps=2, lr=c.lr, algorithm="linear", N=c.P, rk=RK4Config(c.dt),
-                  expaction=c.expaction, u0=u0)
+    res = descend(c.system, ctrl, ut, steps=c.descent_steps, lr=c.lr, algorithm="linear", N=c.P,
+                  rk=RK4Config(c.dt), expaction=c.expaction, u0=u0)
     sp, _ = _plans(c)
     f = ctrl.copy()
-    for it in range(2):
+    for it in range(c.descent_steps):
         r = linear_gradient(c.grid.nx, 1, c.system.A.as_tuple(), c.system.basis, c.spec.T, c.P, c.nsteps,
                             u0, ut, f, sp)
-        assert np.max(np.abs(np.ravel(res.J_history[it]) - r.J) / r.J) <= 1e-10
+        assert np.max(np.abs(np.ravel(res.J_history[it]) - r.J) / r.J) <= 1e-10, it
+        assert np.max(np.abs(np.ravel(res.grad_norms[it]) - np.linalg.norm(r.grad, axis=-1))
+                      / np.linalg.norm(r.grad, axis=-1)) <= 1e-8, it
         f = f - c.lr * r.grad
     assert rel_l2(res.f_final, f) <= 1e-8
-    assert np.all(np.ravel(res.J_history[1]) < np.ravel(res.J_history[0]))
+    J = np.array([np.ravel(j) for j in res.J_history])
+    assert np.all(J[-1] < J[0])
+
+
+def _fullsize_check(index):
+    """One BASELINE-size gradient through the public API against the committed full-size
+    oracle fixture (oracle/gen_fullsize.py): J ≤ 1e-10, ∂J/∂c ≤ 1e-8, the u(T) / q†(0) / ∫q†
+    norms and sums and every s-th point of each field ≤ 1e-10."""
+    import os
+    from paper_2004_00546_b200 import RK4Config, baseline, direct_adjoint_loop, release_engines
+    from paper_2004_00546_b200.optimization import get_engine
+    from tests.conftest import ROOT
+    path = os.path.join(ROOT, "tests", "golden", f"fullsize_c{index}.npz")
+    assert os.path.exists(path), "full-size fixture missing: run oracle/gen_fullsize.py"
+    ref = np.load(path)
+    release_engines()
+    c = baseline(index)
+    u0, ut, ctrl = c.inputs()
+    eng = get_engine(c.system, c.P, RK4Config(c.dt), c.expaction, c.batch)
+    want = str(ref["formulation"])
+    assert want == ("scan" if eng.local_blocks == 1 else f"blockscan({eng.local_blocks})")
+    loop = direct_adjoint_loop(c.system, ctrl, ut, "linear", N=c.P, rk=RK4Config(c.dt), expaction=c.expaction,
+                               u0=u0)
+    assert np.max(np.abs(np.ravel(loop.J) - ref["J"]) / np.abs(ref["J"])) <= 1e-10
+    assert rel_l2(loop.grad, ref["grad"]) <= 1e-8
+    s = int(ref["stride"])
+    fields = {"uT": loop.direct.final_state, "qdag0": loop.adjoint.initial_state, "G": loop.adjoint.integral}
+    for k, v in fields.items():
+        v = np.reshape(np.asarray(v), (c.grid.ny, c.grid.nx))
+        assert abs(np.linalg.norm(v) - ref[k + "_norm"]) <= 1e-10 * ref[k + "_norm"], k
+        assert abs(np.sum(v) - ref[k + "_sum"]) <= 1e-10 * ref[k + "_norm"] * np.sqrt(v.size), k
+        assert rel_l2(v[::s, ::s], ref[k + "_sub"]) <= 1e-10, k
+    release_engines()
+
+
+def test_fullsize_config5_vs_oracle():
+    """Config 5 at BASELINE size (2048², P = 512, Chebyshev): the GPU's scan vs the oracle's."""
+    _fullsize_check(5)
+
+
+def test_fullsize_config4_vs_oracle():
+    """Config 4 at BASELINE size (512², P = 128, Krylov m = 30): 4 local blocks vs the
+    oracle's 4-block block-scan."""
+    _fullsize_check(4)
 
 
 def test_config3_burgers_full():
