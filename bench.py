@@ -1,30 +1,38 @@
 #!/usr/bin/env python
 """Benchmark: Paraexp direct-adjoint gradient evaluations per second on B200.
 
-One *step* = one full direct-adjoint gradient evaluation (direct Paraexp sweep,
-objective, adjoint Paraexp sweep, gradient projection) of BASELINE config 5
-(2D advection–diffusion 2048², P = 512 slices, Chebyshev tol 1e-10; the largest
-config and the one BASELINE names for 1/2/4/8 GPUs). Multi-GPU (torchrun): the
-P slices are sharded in contiguous blocks, partials allreduced over NCCL
-(strong scaling: total work fixed). ``--config k`` benches another config.
+One *step* = one full direct-adjoint gradient evaluation (direct Paraexp sweep, objective,
+adjoint Paraexp sweep, gradient projection) of BASELINE config 5 (2D advection–diffusion 2048²,
+P = 512 slices, Chebyshev, tol 1e-10 as the sweep's error budget; the largest config and the one
+BASELINE names for 1/2/4/8 GPUs). Multi-GPU (torchrun): the P slices are sharded in contiguous
+blocks, partials allreduced over NCCL (strong scaling: total work fixed). ``--config k`` benches
+another config.
 
-Line fields (see the task contract): ``value`` = gradient evals/s with inputs
-resident in HBM (device-timed with CUDA events, max over ranks); ``e2e`` = the
-same metric through the public API ``direct_adjoint_loop`` with host numpy
-inputs/outputs (H2D/D2H inside the timed region, host wall clock);
-``roofline`` = the dominant kernel class's algorithmic bytes per launch (SURVEY §8(d)
-per-unit bytes × the units a launch processes: 24n per lane and RK4 step) ÷ its
-average launch duration (CUDA events around the phase on the work stream) vs the
-measured HBM peak — above 1 for kernels that fuse two steps per launch, with the DRAM
-they actually move (committed ncu capture) beside it; ``cpu_baseline`` = the numpy oracle port on this host's cores
-(bounded sample, extrapolated); ``--impl reference`` prints the CPU arm alone.
+Line fields (see the task contract):
+
+* ``value`` — gradient evals/s with inputs resident in HBM (CUDA events on the work stream,
+  max over ranks);
+* ``e2e`` — the same metric through the public API ``direct_adjoint_loop`` with host numpy
+  inputs/outputs (H2D/D2H inside the timed region, host wall clock);
+* ``roofline`` — the dominant kernel (the fused two-step RK4 march, ≈ 75% of a gradient):
+  ``achieved`` = its algorithmic bytes per launch (each distinct operand once: y in and y out per
+  lane, the source b per member) ÷ its average launch time, measured in this run
+  with CUDA events around every launch; ``traffic`` = the DRAM bytes ncu measured per launch
+  (profiles/ncu_traffic.json); ``model_frac`` = the SURVEY per-step model (24n per lane and RK4
+  step, two steps per launch) for comparison; ``fp64`` = DFMA rate against the measured fp64
+  peak (profiles/r02_fp64_peak.json); ``binding`` = the limiter from the ncu capture;
+* ``cpu_baseline`` — the CPU reference path (oracle/cpu_reference.py: the oracle's arithmetic,
+  every slice solved, W host processes) on this host: full gradients for configs 1–3, a bounded
+  sample for configs 4/5 (every worker times each unit kind on the full-size field; one gradient
+  = the slowest worker's units × unit times), validated offline against a full CPU gradient
+  (profiles/r02_cpu_reference_c*.json);
+* ``--impl reference`` prints the CPU arm alone (rank 0; other ranks exit).
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -39,6 +47,7 @@ import numpy as np  # noqa: E402
 
 METRIC = "Paraexp direct-adjoint gradient evals/s"
 UNIT = "gradient evals/s"
+FP64_FALLBACK_TFLOPS = 37.0  # B200 datasheet order of magnitude; used only without the measured file
 
 
 def load_peaks():
@@ -46,23 +55,26 @@ def load_peaks():
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    return 6650.0, "fallback (B200_PROFILING.md)"
+        hbm, src = float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    else:
+        hbm, src = 6650.0, "fallback (B200_PROFILING.md)"
+    q = os.path.join(ROOT, "profiles", "r02_fp64_peak.json")
+    if os.path.exists(q):
+        with open(q) as f:
+            fp = json.load(f)
+        fp64, fsrc = float(fp["fp64_tflops_avg"]), "measured (profiles/r02_fp64_peak.json, tools/mb/fp64_peak.cu)"
+    else:
+        fp64, fsrc = FP64_FALLBACK_TFLOPS, "fallback (datasheet order)"
+    return hbm, src, fp64, fsrc
 
 
-def load_profile(phase_kernel: str, config: int) -> dict:
-    """The committed ncu summary (per-launch DRAM bytes, limiter) for the dominant kernel."""
+def load_profile(config: int) -> dict:
+    """The committed ncu summary (per-launch DRAM bytes, limiter) of the dominant kernel."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return {}
     with open(p) as f:
-        d = json.load(f)
-    return d.get(f"c{config}", {}).get(phase_kernel) or {}
-
-
-def load_traffic(phase_kernel: str, config: int):
-    """ncu dram bytes per launch for the dominant kernel, from the committed profile summary."""
-    return load_profile(phase_kernel, config).get("dram_bytes_per_launch")
+        return json.load(f).get(f"c{config}", {})
 
 
 class ClockSampler:
@@ -121,106 +133,85 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the numpy oracle port on the host cores (bounded sample)
+# CPU reference path (oracle port, host cores)
 # ---------------------------------------------------------------------------
 
 
-def _cpu_worker(args):
-    """Time per-unit oracle costs on the full-size field: RK4 step (direct, adjoint
-    with ∫), Chebyshev term with and without the φ₁ accumulator."""
-    cfg_index, reps = args
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    from oracle.config_mode import stencil_apply
+def cpu_workers() -> int:
+    return max(1, os.cpu_count() or 1)
+
+
+def cpu_reference(index: int, workers: int) -> dict:
+    """One CPU measurement of the config: a full gradient (configs 1–3) or one bounded sample
+    (configs 4, 5). Returns the rate, the seconds this step took and what it was."""
+    from oracle.cpu_reference import full_gradient, host_info, sampled_rate
     from paper_2004_00546_b200 import baseline
-    c = baseline(cfg_index)
-    st = c.system.A.as_tuple()
-    nx, ny = c.grid.nx, c.grid.ny
-    n = c.n
-    rng = np.random.default_rng(0)
-    y = rng.standard_normal(n)
-    g = rng.standard_normal(n)
-    z = np.zeros(n)
-    apply = lambda u: stencil_apply(st, u, nx, ny)
-    h = 1e-5
-
-    def rk4(y, z, want_z):
-        k1 = apply(y) + g
-        Y2 = y + (0.5 * h) * k1
-        k2 = apply(Y2) + g
-        Y3 = y + (0.5 * h) * k2
-        k3 = apply(Y3) + g
-        Y4 = y + h * k3
-        k4 = apply(Y4) + g
-        if want_z:
-            z = z + (h / 6.0) * (y + 2.0 * Y2 + 2.0 * Y3 + Y4)
-        return y + (h / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4), z
-
-    out = {}
-    t = time.perf_counter()
-    for _ in range(reps):
-        y, _ = rk4(y, z, False)
-    out["rk4_direct"] = (time.perf_counter() - t) / reps
-    t = time.perf_counter()
-    for _ in range(reps):
-        y, z = rk4(y, z, True)
-    out["rk4_adjoint"] = (time.perf_counter() - t) / reps
-    up, uc, acc, pac = rng.standard_normal(n), rng.standard_normal(n), np.zeros(n), np.zeros(n)
-    t = time.perf_counter()
-    for _ in range(2 * reps):
-        un = 2e-3 * (apply(uc) - 1.0 * uc) + up
-        up, uc = uc, un
-        acc = acc + 0.1 * uc
-    out["term"] = (time.perf_counter() - t) / (2 * reps)
-    t = time.perf_counter()
-    for _ in range(2 * reps):
-        un = 2e-3 * (apply(uc) - 1.0 * uc) + up
-        up, uc = uc, un
-        acc = acc + 0.1 * uc
-        pac = pac + 0.1 * uc
-    out["term_phi"] = (time.perf_counter() - t) / (2 * reps)
-    return out
-
-
-def cpu_reference_rate(cfg_index: int, reps: int = 1, workers: int | None = None):
-    """Gradient evals/s of the oracle port with W host processes, each owning a
-    contiguous slice block (the GPU decomposition); per-unit costs
-    measured concurrently on the full-size field, then the block-scan critical
-    path (own slices + long span) extrapolated from the planner's term counts."""
-    import multiprocessing as mp
-    from paper_2004_00546_b200 import baseline
-    from paper_2004_00546_b200.expaction import KrylovPlan, plan_for
-    from paper_2004_00546_b200.partition import rank_block
-    c = baseline(cfg_index)
-    W = workers or os.cpu_count() or 1
-    W = max(1, min(W, c.P))
+    c = baseline(index)
+    if index in (4, 5):
+        rate, wall, units, frac = sampled_rate(c, workers)
+        w = max(1, min(workers, c.P))
+        sample = (f"bounded sample: each of {w} concurrent worker processes (slice block of a {w}-way "
+                  f"block-scan) times 2 direct and 2 adjoint RK4 steps, one slice action with and one "
+                  f"without the φ₁ accumulator on the full {c.grid.nx}x{c.grid.ny} field; one gradient = "
+                  f"the slowest worker's unit counts × unit times ({frac:.4f} of a gradient per step)")
+        return {"value": rate, "seconds": wall, "cores": w, "sample": sample, "gradient_fraction": frac,
+                "unit_seconds": units, "host": host_info()}
     t0 = time.perf_counter()
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(W) as pool:
-        res = pool.map(_cpu_worker, [(cfg_index, reps)] * W)
+    if index == 3:
+        from oracle.config_mode import burgers_gradient
+        from paper_2004_00546_b200.expaction import plan_chebyshev
+        from paper_2004_00546_b200.problems import burgers_frozen_region
+        u0, ut, ctrl = c.inputs()
+        burgers_gradient(c.grid.nx, c.spec.D, c.system.basis, c.spec.T, c.P, c.nsteps, u0, ut, ctrl,
+                         lambda region, span: plan_chebyshev(region, span, c.expaction),
+                         lambda ub: burgers_frozen_region(ub, c.grid, c.spec.D))
+        w = 1
+        what = "one full gradient (serial direct sweep + every adjoint slice), one process"
+    else:
+        w = max(1, min(workers, c.P))
+        full_gradient(c, w)
+        what = f"one full gradient, every slice solved, {w}-process block-scan"
     wall = time.perf_counter() - t0
-    u = {k: max(r[k] for r in res) for k in res[0]}  # contended per-unit cost (slowest worker)
-    region = c.system.region() if c.system.is_linear else None
-    delta = c.spec.T / c.P
-    worst = 0.0
-    for r in range(W):
-        p0, p1 = rank_block(c.P, r, W)
-        Pl = p1 - p0
-        t = Pl * c.nsteps * (u["rk4_direct"] + u["rk4_adjoint"])
-        if region is not None:
-            sp = plan_for(region, delta, c.expaction)
-            per = sp.terms if not isinstance(sp, KrylovPlan) else sp.terms * 4  # Arnoldi ≈ 4 vector passes/step
-            t += (Pl - 1) * per * (u["term"] + u["term_phi"])
-            if p1 < c.P:
-                t += plan_for(region, (c.P - p1) * delta, c.expaction, base_span=delta).terms * u["term"]
-            if p0 > 0:
-                t += plan_for(region, p0 * delta, c.expaction, base_span=delta).terms * u["term_phi"]
-        worst = max(worst, t)
-    rate = c.batch / worst
-    sample = (f"per-unit oracle costs timed on the full {c.grid.nx}x{c.grid.ny} field by {W} concurrent "
-              f"numpy processes ({reps} RK4 steps direct+adjoint, {4 * reps} Chebyshev terms each; "
-              f"{wall:.1f}s wall), extrapolated to one gradient = max over workers of own-slice RK4 "
-              f"({c.nsteps} steps/slice) + block scan + long span (blockscan over W workers)")
-    return rate, W, sample, u
+    return {"value": c.batch / wall, "seconds": wall, "cores": w, "sample": what, "gradient_fraction": 1.0,
+            "host": host_info()}
+
+
+def load_cpu_validation(index: int):
+    p = os.path.join(ROOT, "profiles", f"r02_cpu_reference_c{index}.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return None
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    W = cpu_workers()
+    runs = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference(args.config, W)
+        if i >= args.warmup:
+            runs.append(r)
+    v = statistics.median(r["value"] for r in runs)
+    last = runs[-1]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.mean(r["seconds"] for r in runs),
+        "gradient_fraction_per_step": last["gradient_fraction"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, paper_2004_00546_b200/configs.py)", "config": config_block(args.config, world),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": "port", "sample": last["sample"],
+                         "host": last["host"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    val = load_cpu_validation(args.config)
+    if val:
+        line["cpu_baseline"]["validation"] = val
+    print(json.dumps(line), flush=True)
+    return 0
 
 
 # ---------------------------------------------------------------------------
@@ -235,37 +226,58 @@ def dist_env():
     return rank, world, local
 
 
-def run_reference(args):
-    rank, world, local = dist_env()
-    if rank != 0:
-        return 0
-    rates = []
-    for i in range(args.warmup + args.steps):
-        rate, W, sample, _ = cpu_reference_rate(args.config, reps=args.cpu_reps)
-        if i >= args.warmup:
-            rates.append(rate)
-    v = statistics.median(rates)
-    line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, configs.py)",
-        "config": config_block(args.config, world),
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": W, "kind": "port", "sample": sample},
-        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-    return 0
-
-
 def config_block(index, world):
     from paper_2004_00546_b200 import baseline
     c = baseline(index)
     return {"workload": c.name, "grid": [c.grid.nx, c.grid.ny], "P": c.P, "steps_per_slice": c.nsteps,
             "T": c.spec.T, "dt": c.spec.T / c.P / c.nsteps, "batch": c.batch, "K": c.K,
             "expaction": type(c.expaction).__name__, "tol": c.expaction.tol,
+            "tol_horizon": c.expaction.horizon or None,
             "parallelism": f"slices{world}" if world > 1 else "single",
             "l2": "inputs larger than L2 (lane buffers of P×n fp64)" if c.n * c.P * 8 > 126e6 else
                   "working set fits L2 (not flushed)"}
+
+
+def roofline_2d(eng, c, peak, peak_src, fp64_peak, fp64_src, prof, world):
+    """The fused two-step RK4 march: bytes and DFMA per launch over its measured launch time."""
+    import torch
+    from paper_2004_00546_b200 import _native as N
+    s = int(torch.cuda.current_stream().cuda_stream)
+    eng.kernel_timing(N.PX_KCLASS_MARCH2)
+    eng.kernel_timing(N.PX_KCLASS_CHEB)
+    eng.set_timing(True, kernels=True)
+    for _ in range(2):
+        eng.gradient(s, want_fields=False)
+    torch.cuda.synchronize()
+    eng.set_timing(False)
+    eng.timing()
+    ms, cnt = eng.kernel_timing(N.PX_KCLASS_MARCH2)
+    cms, ccnt = eng.kernel_timing(N.PX_KCLASS_CHEB)
+    if cnt == 0:
+        return None
+    t = ms / cnt / 1e3
+    n, L, B = c.n, eng.B * (eng.p1 - eng.p0), eng.B
+    alg = 16.0 * n * L + 8.0 * n * B      # y in + y out per lane, b per member: distinct operands once
+    model = 2 * 24.0 * n * L              # SURVEY §8(d): 24n per lane and RK4 step, two steps
+    dfma = 2 * 21.0 * n * L               # 4 Horner stages × 5 stencil FMAs + the source add, per step
+    pr = prof.get("rk4_direct", {})
+    traffic = pr.get("dram_bytes_per_launch")
+    out = {"bound": "hbm", "kernel": "k_rk4_marchc<3,64,3,4,br> (two RK4 steps per launch)",
+           "achieved": alg / t / 1e9, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+           "frac": alg / t / 1e9 / peak, "traffic": traffic,
+           "algorithmic_bytes_per_launch": alg, "avg_launch_ms": t * 1e3, "launches_timed": cnt,
+           "model_bytes_per_launch": model, "model_frac": model / t / 1e9 / peak,
+           "fp64": {"dfma_per_launch": dfma, "achieved_tflops": 2 * dfma / t / 1e12, "peak_tflops": fp64_peak,
+                    "peak_source": fp64_src, "frac": 2 * dfma / t / 1e12 / fp64_peak}}
+    if traffic:
+        out["dram_achieved"] = traffic / t / 1e9
+        out["dram_frac"] = traffic / t / 1e9 / peak
+        out["traffic_source"] = pr.get("source")
+    if pr.get("limiter"):
+        out["binding"] = pr["limiter"]
+    if ccnt:
+        out["chebyshev_pass_avg_ms"] = cms / ccnt
+    return out
 
 
 def main():
@@ -276,7 +288,6 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-reps", type=int, default=3, help="oracle unit repetitions per CPU worker (~3 s each)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="warmup+steps only (for ncu); no extras")
     args = ap.parse_args()
@@ -347,63 +358,32 @@ def main():
     phases = eng.timing()
     stats = eng.stats()
     launches = int(stats["kernel_launches"])
-    gpu_evals = args.steps * c.batch
-    value = gpu_evals / (ms_max / 1e3)
+    value = args.steps * c.batch / (ms_max / 1e3)
 
-    # dominant kernel class: the phase with the largest device time
-    dom = max(phases, key=lambda k: phases[k]["ms"])
-    ph = phases[dom]
-    peak, peak_src = load_peaks()
-    avg_launch_s = (ph["ms"] / 1e3) / max(ph["launches"], 1)
-    bytes_per_launch = ph["bytes"] / max(ph["launches"], 1)
-    achieved = bytes_per_launch / avg_launch_s / 1e9 if avg_launch_s > 0 else 0.0
-    two_d = c.grid.dim == 2
-    # two RK4 steps per launch (k_rk4_march2) when the phase launched fewer kernels than steps
-    fused = two_d and ph["launches"] / args.steps < (c.nsteps - 1) * 0.75
-    # (the library's default variant: three columns per thread, 64-thread CTAs, in strip
-    # mode; PX_M2_COLS=2 selects the two-column k_rk4_march2)
-    cols = int(os.environ.get("PX_M2_COLS", "3"))
-    m2 = "k_rk4_marchc<3,64,3,4,br>" if cols == 3 and c.grid.nx > 192 else "k_rk4_march2<false,128,3,3,tma>"
-    kernel_name = {"rk4_direct": (m2 if fused else "k_rk4_march<false>") if two_d
-                   else "k_rk4_lane1d<false>",
-                   # 2D adjoint lanes run the direct kernel: their ∫ is recovered in closed form
-                   # (one cuFFT solve, `z_closed_form`) instead of a per-lane accumulator
-                   "rk4_adjoint": (m2 + " (adjoint lanes)" if fused else "k_rk4_march<false>")
-                   if two_d else "k_rk4_lane1d<true>",
-                   "exp_direct": "k_cheb_march<M>" if two_d else "k_scan1d",
-                   "exp_adjoint": "k_cheb_march<M>+phi" if two_d else "k_scan1d+phi",
-                   "other": "reductions/projection"}[dom]
-    if type(c.expaction).__name__ == "KrylovConfig" and dom.startswith("exp"):
-        kernel_name = "Arnoldi CGS2 (k_kr_spmv_dots/k_kr_update/k_kr_expm/k_kr_combine)"
-    if not c.system.is_linear:
-        kernel_name = {"rk4_direct": "k_burgers_direct", "rk4_adjoint": "k_burgers_adjoint_rk4+k_burgers_scan"}.get(
-            dom, kernel_name)
-    roofline = {"bound": "hbm", "kernel": kernel_name, "phase": dom, "achieved": achieved, "peak": peak,
-                "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-                "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_s * 1e3,
-                "share_of_step": ph["ms"] / sum(p["ms"] for p in phases.values()),
-                "traffic": load_traffic(dom, args.config)}
-    prof = load_profile(dom, args.config)
-    if prof.get("limiter"):
-        roofline["limiter"] = prof["limiter"]
-    if prof.get("dram_bytes_per_launch") and prof.get("duration_ms"):
-        # what the kernel actually moves, from the committed ncu capture (its own clock)
-        dgbs = prof["dram_bytes_per_launch"] / (prof["duration_ms"] / 1e3) / 1e9
-        roofline["dram_achieved_ncu"] = dgbs
-        roofline["dram_frac_ncu"] = dgbs / peak
-    if roofline["frac"] > 1.0 and fused and dom.startswith("rk4"):
-        roofline["note"] = ("temporal blocking: each launch advances two RK4 steps and streams y, b and y_out "
-                            "once (24n per lane per launch, half the SURVEY §8(d) model of 24n per lane-step), "
-                            "so frac on the model exceeds 1; the DRAM actually moved is `traffic` "
-                            "(dram_frac_ncu), and the binding resource is the shared-memory data pipe (limiter)")
-    elif roofline["frac"] > 1.0:
-        roofline["note"] = ("on-chip kernel (state resident in shared memory / registers across steps or "
-                            "terms): the per-unit HBM model of SURVEY §8(d) counts bytes this kernel never "
-                            "moves, so frac > 1; its binding resources are the fp64 pipe and barrier latency")
-    phase_gbs = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
-                     "GB/s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None}
-                 for k, v in phases.items()}
-    whole = stats["algorithmic_bytes"] / (ms_max / 1e3) / 1e9
+    peak, peak_src, fp64_peak, fp64_src = load_peaks()
+    prof = load_profile(args.config)
+    roofline = None
+    if c.grid.dim == 2 and c.system.is_linear:
+        roofline = roofline_2d(eng, c, peak, peak_src, fp64_peak, fp64_src, prof, world)
+    if roofline is None:
+        # on-chip configs (1D lanes and scans, Burgers): phase-level algorithmic bytes
+        dom = max(phases, key=lambda k: phases[k]["ms"])
+        ph = phases[dom]
+        tl = (ph["ms"] / 1e3) / max(ph["launches"], 1)
+        bpl = ph["bytes"] / max(ph["launches"], 1)
+        roofline = {"bound": "hbm", "phase": dom, "achieved": bpl / tl / 1e9 if tl > 0 else 0.0, "peak": peak,
+                    "peak_source": peak_src, "unit": "GB/s", "frac": (bpl / tl / 1e9 / peak) if tl > 0 else 0.0,
+                    "traffic": None, "bytes_per_launch": bpl, "avg_launch_ms": tl * 1e3,
+                    "note": "on-chip kernels (state in shared memory / registers across steps or terms): "
+                            "the SURVEY §8(d) per-unit model counts bytes these kernels never move; the "
+                            "binding resources are the fp64 pipe and barrier latency"}
+    roofline["share_of_step"] = None
+    total_ms = sum(p["ms"] for p in phases.values())
+    if total_ms > 0:
+        roofline["share_of_step"] = (phases["rk4_direct"]["ms"] + phases["rk4_adjoint"]["ms"]) / total_ms
+    phase_ms = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+                    "algorithmic_GB/s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None}
+                for k, v in phases.items()}
 
     eng.close()  # the public-API leg below owns its own engine (HBM scratch)
     del dev
@@ -412,15 +392,14 @@ def main():
     e2e = None
     if args.e2e_steps > 0:
         rk = RK4Config(c.dt)
-        direct_adjoint_loop(c.system, ctrl, ut, "linear" if c.system.is_linear else "hybrid", N=c.P, rk=rk,
-                            expaction=c.expaction, u0=u0)
+        algo = "linear" if c.system.is_linear else "hybrid"
+        direct_adjoint_loop(c.system, ctrl, ut, algo, N=c.P, rk=rk, expaction=c.expaction, u0=u0)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            direct_adjoint_loop(c.system, ctrl, ut, "linear" if c.system.is_linear else "hybrid", N=c.P,
-                                rk=rk, expaction=c.expaction, u0=u0)
+            direct_adjoint_loop(c.system, ctrl, ut, algo, N=c.P, rk=rk, expaction=c.expaction, u0=u0)
         torch.cuda.synchronize()
         el = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
         if world > 1:
@@ -434,9 +413,14 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, W, sample, units = cpu_reference_rate(args.config, reps=args.cpu_reps)
-        cpu = {"value": rate, "unit": UNIT, "cores": W, "kind": "port", "sample": sample,
-               "unit_seconds": units}
+        r = cpu_reference(args.config, cpu_workers())
+        cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port", "sample": r["sample"],
+               "host": r["host"]}
+        if "unit_seconds" in r:
+            cpu["unit_seconds"] = r["unit_seconds"]
+        val = load_cpu_validation(args.config)
+        if val:
+            cpu["validation"] = val
 
     if rank == 0:
         line = {
@@ -445,7 +429,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded inputs, paper_2004_00546_b200/configs.py)",
             "config": config_block(args.config, world),
-            "roofline": roofline, "whole_step_algorithmic_GBps": whole, "phases": phase_gbs,
+            "roofline": roofline, "phases": phase_ms,
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
             "J": float(J[0]),
         }

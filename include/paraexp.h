@@ -88,11 +88,12 @@ enum {
                                  ≥ 2^28 lane-points; 2 two-step launches at any size */
   PX_VAR_MARCH_COLS = 1,      /* columns per thread of the two-step march: 3 (default) or 2 */
   PX_VAR_MARCH_BAND = 2,      /* rows per band of the two-step march (0: automatic) */
-  PX_VAR_CHEB_TERMS = 3,      /* Chebyshev terms fused per 2D pass, 1 … 6 (default 6) */
+  PX_VAR_CHEB_TERMS = 3,      /* most Chebyshev terms fused per 2D pass, 1 … 7 (default 7; passes balanced) */
   PX_VAR_CHEB_STRIP = 4,      /* strip width of the 2D Chebyshev passes (0: balanced) */
   PX_VAR_CHEB_BAND = 5,       /* rows per band of the 2D Chebyshev passes (0: one wave) */
   PX_VAR_SCAN1D_CLUSTER = 6,  /* 1D scans on 8-CTA clusters for n ≥ 2048 (default 1) */
-  PX_VAR_BURGERS_CLUSTER = 7  /* Burgers sweeps on 8-CTA clusters for n ≥ 2048 (default 1) */
+  PX_VAR_BURGERS_CLUSTER = 7, /* Burgers sweeps on 8-CTA clusters for n ≥ 2048 (default 1) */
+  PX_VAR_CHEB_TERMS_PHI = 8   /* as PX_VAR_CHEB_TERMS for passes with the φ₁ accumulator (default 5) */
 };
 enum { PX_ADJOINT_ABSORBED = 0, PX_ADJOINT_FROZEN_SPAN = 1 };  /* px_set_adjoint_mode */
 
@@ -243,8 +244,17 @@ typedef struct px_timing {
   uint64_t launches[PX_PHASE_COUNT];
   double bytes[PX_PHASE_COUNT];   /* algorithmic bytes executed inside each phase */
 } px_timing;
+/* enable: 0 off, 1 phase windows (graph replay keeps running), 2 phase windows plus CUDA events
+ * around every launch of the kernel classes below (px_gradient then runs eagerly, no graph). */
 int px_set_timing(void* handle, int enable);
 int px_get_timing(void* handle, px_timing* out);
+enum {
+  PX_KCLASS_MARCH2 = 0,   /* the two-step fused RK4 march launches (k_rk4_marchc / k_rk4_march2) */
+  PX_KCLASS_CHEB = 1,     /* the 2D Chebyshev passes (k_cheb_march) */
+  PX_KCLASS_COUNT = 2
+};
+/* Summed device ms and launch count of one kernel class since the last call (timing mode 2). */
+int px_get_kernel_timing(void* handle, int kclass, double* ms, uint64_t* launches);
 
 int px_get_stats(void* handle, px_stats* out);
 int px_reset_stats(void* handle);

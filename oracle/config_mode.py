@@ -473,6 +473,8 @@ class OracleRank:
         self.ut = np.broadcast_to(_as_batch(u_target, n), (B, n))
         self.plan_slice, self.plan_long = plan_slice, plan_long
         self.p0, self.p1 = rank_block(P, rank, world)
+        from types import SimpleNamespace
+        self.spec = SimpleNamespace(rank=rank, world=world)  # the engine's (rank, world) for fail-fast
         self.buf = {k: torch.zeros(B * (basis.K if k == "GRAD" else (1 if k == "J" else n)), dtype=torch.float64)
                     for k in self.FIELDS}
         self.B, self.n = B, n

@@ -30,7 +30,7 @@ PX_FLAG_BOUNDARY_STATES, PX_FLAG_Z_ACCUM = 1, 2
 ABI_VERSION = 2
 # kernel-variant keys (px_set_variant)
 VARIANTS = {"march2": 0, "march_cols": 1, "march_band": 2, "cheb_terms": 3, "cheb_strip": 4, "cheb_band": 5,
-            "scan1d_cluster": 6, "burgers_cluster": 7}
+            "scan1d_cluster": 6, "burgers_cluster": 7, "cheb_terms_phi": 8}
 PX_ADJOINT_ABSORBED, PX_ADJOINT_FROZEN_SPAN = 0, 1
 
 
@@ -86,6 +86,7 @@ class Stats(ctypes.Structure):
 
 
 PX_PHASES = ("rk4_direct", "rk4_adjoint", "exp_direct", "exp_adjoint", "other")
+PX_KCLASS_MARCH2, PX_KCLASS_CHEB = 0, 1
 
 
 class Timing(ctypes.Structure):
@@ -126,6 +127,7 @@ SIGNATURES = {
     "px_get": (c_int, [c_void_p, c_int, c_void_p, c_size_t, c_int, c_void_p]),
     "px_set_timing": (c_int, [c_void_p, c_int]),
     "px_get_timing": (c_int, [c_void_p, POINTER(Timing)]),
+    "px_get_kernel_timing": (c_int, [c_void_p, c_int, POINTER(c_double), POINTER(c_uint64)]),
     "px_get_stats": (c_int, [c_void_p, POINTER(Stats)]),
     "px_reset_stats": (c_int, [c_void_p]),
 }

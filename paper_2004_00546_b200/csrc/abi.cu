@@ -121,6 +121,7 @@ int px_create(const px_problem_desc* desc, void** out_handle) {
   if (rc == PX_OK) rc = pxi::dalloc_t(h, &h->nonfinite, 1);
   for (int i = 0; i < 4; ++i) A(&h->Wk[i], B * n);
   for (int i = 0; i < 2; ++i) A(&h->ACC[i], B * n);
+  if (d.kind == PX_KIND_ADVDIFF && h->dim == 2) A(&h->S, B * n);
   if (d.kind == PX_KIND_ADVDIFF) {
     A(&h->g, B * n);
     A(&h->gadj, B * n);
@@ -182,6 +183,10 @@ void px_destroy(void* handle) {
   for (auto& pl : h->plans)
     if (pl.dcoef) cudaFree(pl.dcoef);
   for (auto& m : h->marks) {
+    cudaEventDestroy(m.a);
+    cudaEventDestroy(m.b);
+  }
+  for (auto& m : h->kmarks) {
     cudaEventDestroy(m.a);
     cudaEventDestroy(m.b);
   }
@@ -270,8 +275,11 @@ int px_set_variant(void* handle, int key, int value) {
       if (value < 0) return fail(h, PX_ERR_ARG, "PX_VAR_MARCH_BAND must be ≥ 0");
       v.march_band = value; break;
     case PX_VAR_CHEB_TERMS:
-      if (value < 1 || value > 6) return fail(h, PX_ERR_ARG, "PX_VAR_CHEB_TERMS must be 1 … 6");
+      if (value < 1 || value > 7) return fail(h, PX_ERR_ARG, "PX_VAR_CHEB_TERMS must be 1 … 7");
       v.cheb_terms = value; break;
+    case PX_VAR_CHEB_TERMS_PHI:
+      if (value < 1 || value > 7) return fail(h, PX_ERR_ARG, "PX_VAR_CHEB_TERMS_PHI must be 1 … 7");
+      v.cheb_terms_phi = value; break;
     case PX_VAR_CHEB_STRIP:
       if (value < 0 || (value & 1)) return fail(h, PX_ERR_ARG, "PX_VAR_CHEB_STRIP must be even and ≥ 0");
       v.cheb_strip = value; break;
@@ -295,6 +303,7 @@ int px_get_variant(void* handle, int key, int* value) {
     case PX_VAR_MARCH_COLS: *value = v.march_cols; break;
     case PX_VAR_MARCH_BAND: *value = v.march_band; break;
     case PX_VAR_CHEB_TERMS: *value = v.cheb_terms; break;
+    case PX_VAR_CHEB_TERMS_PHI: *value = v.cheb_terms_phi; break;
     case PX_VAR_CHEB_STRIP: *value = v.cheb_strip; break;
     case PX_VAR_CHEB_BAND: *value = v.cheb_band; break;
     case PX_VAR_SCAN1D_CLUSTER: *value = v.scan1d_cluster; break;
@@ -450,7 +459,7 @@ int px_gradient(void* handle, void* stream) {
   Handle* h = bind(handle);
   if (!h) return fail(h, PX_ERR_ARG, "null handle");
   if (h->d.kind != PX_KIND_ADVDIFF) return fail(h, PX_ERR_ARG, "px_gradient: linear testbed only");
-  if (!h->graphs) return gradient_phases(h, stream);
+  if (!h->graphs || h->timing >= 2) return gradient_phases(h, stream);
   if (!h->basis_set || !h->inputs_set) return fail(h, PX_ERR_STATE, "basis/inputs not set");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (!h->gstream) {
@@ -558,7 +567,29 @@ int px_get(void* handle, int field, double* dst, size_t count, int mem, void* st
 int px_set_timing(void* handle, int enable) {
   Handle* h = static_cast<Handle*>(handle);
   if (!h) return fail(h, PX_ERR_ARG, "null handle");
-  h->timing = enable != 0;
+  if (enable < 0 || enable > 2) return fail(h, PX_ERR_ARG, "timing mode must be 0, 1 or 2");
+  h->timing = enable;
+  return PX_OK;
+}
+
+int px_get_kernel_timing(void* handle, int kclass, double* ms, uint64_t* launches) {
+  Handle* h = bind(handle);
+  if (!h || !ms || !launches) return fail(h, PX_ERR_ARG, "null argument");
+  if (kclass < 0 || kclass >= PX_KCLASS_COUNT) return fail(h, PX_ERR_ARG, "bad kernel class");
+  for (auto& m : h->kmarks) {
+    PX_CUDA(h, cudaEventSynchronize(m.b));
+    float t = 0.f;
+    PX_CUDA(h, cudaEventElapsedTime(&t, m.a, m.b));
+    h->kms[m.cls] += t;
+    h->kcount[m.cls] += 1;
+    h->event_pool.push_back(m.a);
+    h->event_pool.push_back(m.b);
+  }
+  h->kmarks.clear();
+  *ms = h->kms[kclass];
+  *launches = h->kcount[kclass];
+  h->kms[kclass] = 0.0;
+  h->kcount[kclass] = 0;
   return PX_OK;
 }
 

@@ -11,23 +11,29 @@ namespace pxi {
 
 namespace {
 
-// 2D passes: σ = ±1 as a template constant
-template <int M>
-int launch_cm(Handle* h, const px::ChebMarchArgs& a, unsigned blocks, cudaStream_t s) {
-  if (a.sigma < 0) {
-    PX_TRY(smem_attr(h, (const void*)px::k_cheb_march<M, -1>, px::CM_SMEM));
-    px::k_cheb_march<M, -1><<<blocks, px::CM_NT, px::CM_SMEM, s>>>(a);
-  } else {
-    PX_TRY(smem_attr(h, (const void*)px::k_cheb_march<M, 1>, px::CM_SMEM));
-    px::k_cheb_march<M, 1><<<blocks, px::CM_NT, px::CM_SMEM, s>>>(a);
-  }
+// 2D passes: σ = ±1, the φ₁ accumulator and the carry-input sum as template constants
+template <int M, int SG, bool PH, bool SS>
+int launch_cm_v(Handle* h, const px::ChebMarchArgs& a, unsigned blocks, cudaStream_t s) {
+  PX_TRY(smem_attr(h, (const void*)px::k_cheb_march<M, SG, PH, SS>, px::CM_SMEM));
+  px::k_cheb_march<M, SG, PH, SS><<<blocks, px::CM_NT, px::CM_SMEM, s>>>(a);
   PX_CHECK_LAUNCH(h);
   return PX_OK;
+}
+template <int M, int SG>
+int launch_cm_s(Handle* h, const px::ChebMarchArgs& a, unsigned blocks, cudaStream_t s) {
+  if (a.pacc) return launch_cm_v<M, SG, true, false>(h, a, blocks, s);
+  if (a.ssum) return launch_cm_v<M, SG, false, true>(h, a, blocks, s);
+  return launch_cm_v<M, SG, false, false>(h, a, blocks, s);
+}
+template <int M>
+int launch_cm(Handle* h, const px::ChebMarchArgs& a, unsigned blocks, cudaStream_t s) {
+  return a.sigma < 0 ? launch_cm_s<M, -1>(h, a, blocks, s) : launch_cm_s<M, 1>(h, a, blocks, s);
 }
 
 // 2D: Chebyshev action by row-marching passes of up to CM_MAXT fused terms
 int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const double* src, long long src_bs,
-                      const double* addend, long long add_bs, double* pacc, double** result, cudaStream_t s) {
+                      const double* addend, long long add_bs, double* pacc, double* ssum, double** result,
+                      cudaStream_t s) {
   const size_t n = h->n;
   const int B = h->B;
   const long long nb = (long long)n;
@@ -43,7 +49,11 @@ int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const d
     }
   }
   a.nx = nx; a.ny = ny; a.B = B;
-  const int cm_terms = std::max(1, std::min(px::CM_MAXT, h->var.cheb_terms));
+  // the degree is split into the fewest passes of ≤ cheb_terms terms, sizes balanced
+  const int K = pl.degree;
+  const int tmax = std::max(1, std::min(px::CM_MAXT, pacc ? h->var.cheb_terms_phi : h->var.cheb_terms));
+  const int npass = (K + tmax - 1) / tmax;
+  const int cm_terms = (K + npass - 1) / npass;
   if (nx <= 2 * px::CM_NT && h->var.cheb_strip == 0) {
     a.strip_w = nx; a.halo = 0; a.nstrips = 1;
   } else {
@@ -71,7 +81,6 @@ int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const d
   a.band_rows = br;
   a.nbands = (ny + br - 1) / br;
   const unsigned blocks = (unsigned)((size_t)B * a.nstrips * a.nbands);
-  const int K = pl.degree;
   int wsel = 0;  // rotating pair of U output buffers
   for (int sub = 0; sub < pl.substeps; ++sub) {
     double* acc = (src == h->ACC[0]) ? h->ACC[1] : h->ACC[0];
@@ -95,21 +104,25 @@ int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const d
       double* o1 = h->Wk[2 * wsel + 1];
       a.out_prev = last ? nullptr : o0;
       a.out_cur = last ? nullptr : o1;
+      a.ssum = (last && sub == pl.substeps - 1) ? ssum : nullptr;
       for (int j = 0; j <= px::CM_MAXT; ++j) {
         const int term = k + j;
         a.be[j] = (j <= M && term <= K && (j > 0 || first)) ? pl.be[term] : 0.0;
         a.bp[j] = (pacc && j <= M && term <= K && (j > 0 || first)) ? pl.bp[term] : 0.0;
       }
       int rc;
+      const int km = kbegin(h, PX_KCLASS_CHEB, s);
       switch (M) {
         case 1: rc = launch_cm<1>(h, a, blocks, s); break;
         case 2: rc = launch_cm<2>(h, a, blocks, s); break;
         case 3: rc = launch_cm<3>(h, a, blocks, s); break;
         case 4: rc = launch_cm<4>(h, a, blocks, s); break;
         case 5: rc = launch_cm<5>(h, a, blocks, s); break;
-        default: rc = launch_cm<6>(h, a, blocks, s); break;
+        case 6: rc = launch_cm<6>(h, a, blocks, s); break;
+        default: rc = launch_cm<7>(h, a, blocks, s); break;
       }
       if (rc != PX_OK) return rc;
+      kend(h, km, s);
       // algorithmic bytes: 40n per Chebyshev term (+16n with the φ₁
       // accumulator); the fused pass streams its arrays once for all M terms
       const double bytes = (pacc ? 56.0 : 40.0) * (double)n * B * (double)M;  // Σ M = degree
@@ -144,12 +157,17 @@ px::Scan1DPlan scan_plan(const Plan& pl) {
 
 }  // namespace
 
-// result <- exp(span·M)·src (+ addend);  pacc += span·φ₁(span·M)·src  (if pacc)
+bool cheb_has_ssum(const Handle* h) { return h->dim == 2 && (h->d.nx % 2) == 0; }
+
+// result <- exp(span·M)·src (+ addend);  pacc += span·φ₁(span·M)·src  (if pacc);
+// ssum += result (if ssum; the 2D passes only, cheb_has_ssum)
 int cheb_action(Handle* h, const Plan& pl, const px::Stencil5& st, const double* src, long long src_bs,
-                const double* addend, long long add_bs, double* pacc, double** result, cudaStream_t s) {
+                const double* addend, long long add_bs, double* pacc, double** result, cudaStream_t s,
+                double* ssum) {
   if (!pl.set || pl.krylov) return fail(h, PX_ERR_STATE, "Chebyshev plan not set");
+  if (ssum && (pacc || !cheb_has_ssum(h))) return fail(h, PX_ERR_STATE, "carry-input sum: 2D passes without φ₁");
   if (h->dim == 2 && (h->d.nx % 2) == 0)
-    return cheb_action_march(h, pl, st, src, src_bs, addend, add_bs, pacc, result, s);
+    return cheb_action_march(h, pl, st, src, src_bs, addend, add_bs, pacc, ssum, result, s);
   const size_t n = h->n;
   const int B = h->B;
   const dim3 grid = grid1(n, B);

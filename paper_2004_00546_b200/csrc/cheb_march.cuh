@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(256) k_cheb_term(ChebTermArgs a) {
 
 
 constexpr int CM_NT = 160;  // 5 warps, pairs of columns: computed width ≤ 320 (192 measured slower)
-constexpr int CM_MAXT = 6;  // terms per pass (template M ≤ CM_MAXT; 7+ would need 1 CTA/SM, ≥ 10 spill)
+constexpr int CM_MAXT = 7;  // terms per pass (template M ≤ CM_MAXT)
 constexpr int CM_DEPTH = 5; // cp.async ring depth (rows)
 constexpr int CM_MINB = 2;  // resident CTAs per SM (3 measured slower: spills + smaller bands)
 
@@ -97,6 +97,7 @@ struct ChebMarchArgs {
   double* pacc;                             // B × n in/out, may be null
   double* out_prev;                         // U_{k+M−1} (null on the last pass)
   double* out_cur;                          // U_{k+M}
+  double* ssum;                             // SS passes: S += acc at every completed row (B × n)
   Stencil5 st;
   double c0, d, two_over_d, sigma;
   double be[CM_MAXT + 1], bp[CM_MAXT + 1];  // coefficients of terms k … k+M
@@ -111,22 +112,35 @@ template <int M>
 struct CmUnroll {  // multiple of 3 (U_k rows), 2 (stage rows) and R
   static constexpr int value = (M == 4) ? 12 : 6;
 };
+// acc/pacc row slots: M live rows (r−1 … r−M), UN % R == 0. M = 7 keeps M − 1 = 6 slots: the
+// new row r−1 (term 1) waits in a temporary until term M has completed and stored row r−M,
+// whose slot it then takes (same slot index), so the unroll stays 6.
 template <int M>
-struct CmRing {  // acc/pacc row slots (≥ M live rows; UN % R == 0)
+struct CmRing {
   static constexpr int value = (M <= 3) ? M : (M == 4 ? 4 : 6);
 };
+template <int M>
+struct CmTemp {
+  static constexpr bool value = CmRing<M>::value == M - 1;
+};
 
-// SG: the recurrence sign σ (±1) as a compile-time constant (0: runtime a.sigma). The row
-// ring is filled by per-thread cp.async (a one-thread TMA bulk-copy ring issued after the
+// SG: the recurrence sign σ (±1) as a compile-time constant (0: runtime a.sigma); PH: the φ₁
+// accumulator is updated (a.pacc must be non-null), compiled out otherwise; SS (last pass of an
+// adjoint carry, not with PH): the completed acc rows (the next carry's input) are also added
+// into a.ssum, streamed through the ring's fourth slot at lag M (Σ of the carry inputs: the
+// adjoint's φ₁ integral is one action on that sum, sweeps.cu). The
+// row ring is filled by per-thread cp.async (a one-thread TMA bulk-copy ring issued after the
 // row barrier was measured 15% slower on the scan's short bands).
-template <int M, int SG = 0>
+template <int M, int SG, bool PH, bool SS = false>
 __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) {
+  static_assert(!(PH && SS), "the ring has one spare slot: φ accumulator or the carry-input sum");
   __shared__ double pubE[2][M][CM_NT];
   __shared__ double pubO[2][M][CM_NT];
   // ring slots (dynamic smem): [depth][4 arrays: cur(r), prev(r−1), acc(r−1), pacc(r−1)][pairs]
   extern __shared__ double2 cm_ring[];
   constexpr int UN = CmUnroll<M>::value;
   constexpr int R = CmRing<M>::value;
+  constexpr bool TEMP = CmTemp<M>::value;
 
   const int b = blockIdx.x % a.B;
   const int rest = blockIdx.x / a.B;
@@ -151,7 +165,7 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
   const bool store_ok = active && (2 * t >= a.halo) && (2 * t + 1 < CW - a.halo);
   const bool first = a.first != 0;
   const bool has_add = first && a.addend != nullptr;
-  const bool has_p = a.pacc != nullptr;
+  constexpr bool has_p = PH;
   const bool write_u = a.out_cur != nullptr;
 
   const double sig = a.sigma;
@@ -167,6 +181,7 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
   double* __restrict__ pac = has_p ? a.pacc + (size_t)b * n : nullptr;
   double* __restrict__ oprev = write_u ? a.out_prev + (size_t)b * n : nullptr;
   double* __restrict__ ocur = write_u ? a.out_cur + (size_t)b * n : nullptr;
+  double* __restrict__ ssm = SS ? a.ssum + (size_t)b * n : nullptr;
   const bool read_acc = !first || has_add;
 
   auto wrapr = [&](int row) -> int {
@@ -176,7 +191,8 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
   const int r0 = j0 - M;
   const size_t coloff = (size_t)gx;
   int iss_k = 0, iss_slot = 0;
-  int rc = wrapr(r0), rl = wrapr(r0 - 1);  // streams: cur row r, lagged rows r−1
+  // streams: cur row r, lagged rows r−1 (SS: the sum at row r−M, the row completing)
+  int rc = wrapr(r0), rl = wrapr(r0 - 1), rm = wrapr(r0 - M);
   auto issue = [&]() {
     if (iss_k < iters) {
       double2* sl = cm_ring + (size_t)iss_slot * 4 * CM_NT;
@@ -184,11 +200,13 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
       if (!first) cp_async16(sl + CM_NT + t, prv + (size_t)rl * nx + coloff);
       if (read_acc) cp_async16(sl + 2 * CM_NT + t, accin + (size_t)rl * nx + coloff);
       if (has_p) cp_async16(sl + 3 * CM_NT + t, pac + (size_t)rl * nx + coloff);
+      if constexpr (SS) cp_async16(sl + 3 * CM_NT + t, ssm + (size_t)rm * nx + coloff);
     }
     cp_async_commit();
     ++iss_k;
     iss_slot = (iss_slot + 1 == CM_DEPTH) ? 0 : iss_slot + 1;
     rc = (rc + 1 == ny) ? 0 : rc + 1;
+    if constexpr (SS) rm = (rm + 1 == ny) ? 0 : rm + 1;
     rl = (rl + 1 == ny) ? 0 : rl + 1;
   };
 #pragma unroll
@@ -198,13 +216,15 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
 
   double2 q0[3];               // U_k rows (ring by phase mod 3)
   double2 qs[M + 1][2];        // stage-s outputs, last two rows (index 1..M)
-  double2 qa[R], qp[R];        // acc / pacc of rows r−1 … r−M (ring by phase mod R)
+  double2 qa[R], qp[PH ? R : 1];  // acc / pacc of rows r−1 … r−M (ring by phase mod R)
 #pragma unroll
   for (int k = 0; k < 3; ++k) q0[k] = make_double2(0.0, 0.0);
 #pragma unroll
   for (int s = 0; s <= M; ++s) qs[s][0] = qs[s][1] = make_double2(0.0, 0.0);
 #pragma unroll
-  for (int s = 0; s < R; ++s) qa[s] = qp[s] = make_double2(0.0, 0.0);
+  for (int s = 0; s < R; ++s) qa[s] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int s = 0; s < (PH ? R : 1); ++s) qp[s] = make_double2(0.0, 0.0);
 
   // One Chebyshev term on a column pair: Σ_q coef_q·(stencil tap q) + base, the
   // coefficients pre-scaled on the host (kernel parameters → constant-bank operands);
@@ -233,13 +253,14 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
       const double2 ur = sl[t];
       const double2 upv = first ? make_double2(0.0, 0.0) : sl[CM_NT + t];
       const double2 ain = read_acc ? sl[2 * CM_NT + t] : make_double2(0.0, 0.0);
-      const double2 pin_v = has_p ? sl[3 * CM_NT + t] : make_double2(0.0, 0.0);
+      const double2 pin_v = (has_p || SS) ? sl[3 * CM_NT + t] : make_double2(0.0, 0.0);  // SS: S(r−M)
       issue();
       q0[k % 3] = ur;
       const double2 u0m2 = q0[(k + 1) % 3], u0m1 = q0[(k + 2) % 3];  // rows r−2, r−1
       const int po = k & 1, pp = (k + 1) & 1;  // qs[s][po]: row of iteration i−2, [pp]: i−1
       double2 nq[M + 1];
       nq[0] = ur;
+      double2 acc1 = make_double2(0.0, 0.0), pc1 = make_double2(0.0, 0.0);  // TEMP: row r−1's entry
       // term 1 of the pass at row r−1 (creates the acc/pacc entry of that row)
       if (!G || i >= 2) {
         const double l = pubO[pin][0][tl], r = pubE[pin][0][tr];
@@ -256,8 +277,13 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
           pc = make_double2(pin_v.x + a.bp[1] * u1.x, pin_v.y + a.bp[1] * u1.y);
         }
         nq[1] = u1;
-        qa[k % R] = acc;
-        qp[k % R] = pc;
+        if constexpr (TEMP) {
+          acc1 = acc;
+          pc1 = pc;
+        } else {
+          qa[k % R] = acc;
+          if constexpr (PH) qp[k % R] = pc;
+        }
       } else {
         nq[1] = make_double2(0.0, 0.0);
       }
@@ -274,8 +300,10 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
           const int ai = (k - s + 1 + 2 * R) % R;  // acc slot of row r−s
           qa[ai].x += a.be[s] * u.x;
           qa[ai].y += a.be[s] * u.y;
-          qp[ai].x += a.bp[s] * u.x;
-          qp[ai].y += a.bp[s] * u.y;
+          if constexpr (PH) {
+            qp[ai].x += a.bp[s] * u.x;
+            qp[ai].y += a.bp[s] * u.y;
+          }
         } else {
           nq[s] = make_double2(0.0, 0.0);
         }
@@ -285,12 +313,17 @@ __global__ void __launch_bounds__(CM_NT, CM_MINB) k_cheb_march(ChebMarchArgs a) 
         const size_t off = (size_t)rs * nx + coloff;
         const int ai = (k - M + 1 + 2 * R) % R;
         __stcs(reinterpret_cast<double2*>(accout + off), qa[ai]);
-        if (has_p) __stcs(reinterpret_cast<double2*>(pac + off), qp[ai]);
+        if constexpr (PH) __stcs(reinterpret_cast<double2*>(pac + off), qp[ai]);
+        if constexpr (SS) __stcs(reinterpret_cast<double2*>(ssm + off), make_double2(pin_v.x + qa[ai].x, pin_v.y + qa[ai].y));
         if (write_u) {
           const double2 up = (M == 1) ? u0m1 : qs[M - 1][pp];
           __stcs(reinterpret_cast<double2*>(oprev + off), up);
           __stcs(reinterpret_cast<double2*>(ocur + off), nq[M]);
         }
+      }
+      if constexpr (TEMP) {  // row r−M is out: its slot (k mod R) takes row r−1
+        qa[k % R] = acc1;
+        if constexpr (PH) qp[k % R] = pc1;
       }
       rs = (rs + 1 == ny) ? 0 : rs + 1;
 #pragma unroll

@@ -32,7 +32,8 @@ struct Variants {
   int march_cols = 3;       // PX_VAR_MARCH_COLS: columns per thread of the two-step march (3: k_rk4_marchc
                             // in strip mode; 2: k_rk4_march2)
   int march_band = 0;       // PX_VAR_MARCH_BAND: rows per band of the two-step march (0: automatic)
-  int cheb_terms = 6;       // PX_VAR_CHEB_TERMS: Chebyshev terms fused per 2D pass (1 … 6)
+  int cheb_terms = 7;       // PX_VAR_CHEB_TERMS: at most this many Chebyshev terms per 2D pass (1 … 7)
+  int cheb_terms_phi = 5;   // PX_VAR_CHEB_TERMS_PHI: the same for passes with the φ₁ accumulator (7 spills)
   int cheb_strip = 0;       // PX_VAR_CHEB_STRIP: strip width of the 2D passes (0: balanced)
   int cheb_band = 0;        // PX_VAR_CHEB_BAND: rows per band of the 2D passes (0: one wave)
   int scan1d_cluster = 1;   // PX_VAR_SCAN1D_CLUSTER: 8-CTA cluster scans for 1D n ≥ 2048
@@ -79,6 +80,7 @@ struct Handle {
   // exp-action work
   double* Wk[4] = {nullptr, nullptr, nullptr, nullptr};
   double* ACC[2] = {nullptr, nullptr};
+  double* S = nullptr;  // Σ of the adjoint carries' inputs (2D Chebyshev: one φ₁ action on it)
   // outputs
   double *UT = nullptr, *QT = nullptr, *QDAG0 = nullptr, *G = nullptr;
   double *J = nullptr, *GRAD = nullptr, *R = nullptr, *partial = nullptr;
@@ -100,6 +102,7 @@ struct Handle {
     px::KrylovWork kw{};
     double* D = nullptr;   // block carry at the block edge (B × n)
     double* Gp = nullptr;  // block φ accumulator (adjoint, B × n)
+    double* S = nullptr;   // block's Σ of carry inputs (2D Chebyshev adjoint)
     cudaStream_t st = nullptr;
     cudaEvent_t ev = nullptr;
     int q0 = 0, q1 = 0;
@@ -112,8 +115,12 @@ struct Handle {
   px_stats stats{};
   // phase timing (CUDA events on the work stream)
   struct TMark { int phase; cudaEvent_t a, b; uint64_t launches; double bytes; };
-  bool timing = false;
+  int timing = 0;  // 0 off, 1 phase windows, 2 phase windows + per-launch kernel-class events (eager)
   std::vector<TMark> marks;
+  struct KMark { int cls; cudaEvent_t a, b; };
+  std::vector<KMark> kmarks;
+  double kms[PX_KCLASS_COUNT] = {0.0};
+  uint64_t kcount[PX_KCLASS_COUNT] = {0};
   std::vector<cudaEvent_t> event_pool;
   px_timing tacc{};
   // CUDA-graph replay of px_gradient (linear testbed): captured once per
@@ -149,6 +156,9 @@ int smem_attr(Handle* h, const void* kernel, size_t bytes);
 int tbegin(Handle* h, int phase, cudaStream_t s);
 void tend(Handle* h, int idx, cudaStream_t s);
 cudaEvent_t take_event(Handle* h);
+// per-launch events around one kernel of class `cls` (timing mode 2); kbegin returns −1 when off
+int kbegin(Handle* h, int cls, cudaStream_t s);
+void kend(Handle* h, int idx, cudaStream_t s);
 void seg_open(Handle* h, int phase);
 void seg_close(Handle* h);
 void drop_segments(Handle* h);
@@ -181,7 +191,9 @@ int lane_sum_plus(Handle* h, double* out, const double* lanes, const double* c, 
 
 // ---- cheb.cu / krylov.cu --------------------------------------------------------------
 int cheb_action(Handle* h, const Plan& pl, const px::Stencil5& st, const double* src, long long src_bs,
-                const double* addend, long long add_bs, double* pacc, double** result, cudaStream_t s);
+                const double* addend, long long add_bs, double* pacc, double** result, cudaStream_t s,
+                double* ssum = nullptr);
+bool cheb_has_ssum(const Handle* h);
 bool use_scan1d(const Handle* h);
 int scan1d(Handle* h, bool adjoint, const double* lanes, double* out, double* pacc, int long_slot, cudaStream_t s);
 int krylov_action(Handle* h, const Plan& pl, const px::Stencil5& st, const double* src, long long src_bs,
@@ -191,7 +203,8 @@ void krylov_free(px::KrylovWork& kw);
 
 // ---- sweeps.cu ------------------------------------------------------------------------
 int exp_action(Handle* h, int slot, const px::Stencil5& st, const double* src, long long src_bs,
-               const double* addend, long long add_bs, double* pacc, double** result, cudaStream_t s);
+               const double* addend, long long add_bs, double* pacc, double** result, cudaStream_t s,
+               double* ssum = nullptr);
 int direct_linear(Handle* h, cudaStream_t s);
 int adjoint_linear(Handle* h, cudaStream_t s);
 int finish_direct_impl(Handle* h, cudaStream_t s);

@@ -178,7 +178,9 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
         a.y_out = out;
         a.z_zero = (st_i == 1);
         if (nsteps - st_i >= 2) {
+          const int km = kbegin(h, PX_KCLASS_MARCH2, s);
           PX_TRY(cols3 ? launch_marchc(h, a, blocks, false, s) : launch_march2(h, a, blocks, zlanes, s));
+          kend(h, km, s);
           st_i += 2;
         } else if (cols3) {
           PX_TRY(launch_marchc(h, a, blocks, true, s));  // the three-column kernel, one step

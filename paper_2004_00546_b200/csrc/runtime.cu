@@ -122,4 +122,17 @@ void tend(Handle* h, int idx, cudaStream_t s) {
   m.bytes = h->stats.algorithmic_bytes - m.bytes;
 }
 
+int kbegin(Handle* h, int cls, cudaStream_t s) {
+  if (h->timing < 2 || h->capturing) return -1;
+  Handle::KMark m{cls, take_event(h), take_event(h)};
+  cudaEventRecord(m.a, s);
+  h->kmarks.push_back(m);
+  return (int)h->kmarks.size() - 1;
+}
+
+void kend(Handle* h, int idx, cudaStream_t s) {
+  if (idx < 0) return;
+  cudaEventRecord(h->kmarks[idx].b, s);
+}
+
 }  // namespace pxi

@@ -16,11 +16,15 @@
 namespace pxi {
 
 int exp_action(Handle* h, int slot, const px::Stencil5& st, const double* src, long long src_bs,
-               const double* addend, long long add_bs, double* pacc, double** result, cudaStream_t s) {
+               const double* addend, long long add_bs, double* pacc, double** result, cudaStream_t s,
+               double* ssum) {
   const Plan& pl = h->plans[slot];
   if (!pl.set) return fail(h, PX_ERR_STATE, "exp-action plan slot " + std::to_string(slot) + " not set");
-  if (pl.krylov) return krylov_action(h, pl, st, src, src_bs, addend, add_bs, pacc, result, s);
-  return cheb_action(h, pl, st, src, src_bs, addend, add_bs, pacc, result, s);
+  if (pl.krylov) {
+    if (ssum) return fail(h, PX_ERR_STATE, "carry-input sum: Chebyshev passes only");
+    return krylov_action(h, pl, st, src, src_bs, addend, add_bs, pacc, result, s);
+  }
+  return cheb_action(h, pl, st, src, src_bs, addend, add_bs, pacc, result, s, ssum);
 }
 
 namespace {
@@ -45,6 +49,16 @@ struct ScratchSwap {
 };
 
 bool use_blocks(const Handle* h) { return h->lb > 1 && h->dim == 2 && !(h->d.flags & PX_FLAG_BOUNDARY_STATES); }
+
+// The adjoint's φ₁ integral of the slice carries, Σ_q Δ·φ₁(ΔAᵀ)·C_q, is linear in the carry
+// inputs and every carry applies the same operator: it equals ONE φ₁ action on S = Σ_q C_q.
+// With the 2D Chebyshev passes the carries accumulate S in their last pass (SS passes, one
+// extra stream) instead of carrying a φ₁ accumulator through every pass — which also frees
+// the registers for seven-term passes. Krylov and 1D keep the per-carry accumulator.
+bool use_ssum(const Handle* h) {
+  const Plan& pl = h->plans[PX_PLAN_SLICE];
+  return pl.set && !pl.krylov && cheb_has_ssum(h);
+}
 
 // Block-scan of the direct carry inside one handle: block g scans its lanes from a zero
 // carry and propagates the result to the rank's last slice edge with one long-span action
@@ -95,9 +109,12 @@ int adjoint_blocks(Handle* h, const double* wend, double* out, double* gacc, cud
     PX_CUDA(h, cudaMemsetAsync(b.Gp, 0, sizeof(double) * h->B * h->n, b.st));
     const double* C = wend + (size_t)(b.q1 - 1) * h->n;
     long long C_bs = lane_bs;
+    const bool ss = use_ssum(h) && b.q1 - b.q0 > 1;
+    if (ss) PX_TRY(axpby(h, b.S, nb, C, C_bs, 1.0, nullptr, 0, 0.0, b.st));
     for (int q = b.q1 - 2; q >= b.q0; --q) {
       double* res = nullptr;
-      PX_TRY(exp_action(h, PX_PLAN_SLICE, h->AT, C, C_bs, wend + (size_t)q * h->n, lane_bs, b.Gp, &res, b.st));
+      PX_TRY(exp_action(h, PX_PLAN_SLICE, h->AT, C, C_bs, wend + (size_t)q * h->n, lane_bs, ss ? nullptr : b.Gp, &res,
+                        b.st, ss && q > b.q0 ? b.S : nullptr));
       C = res;
       C_bs = nb;
     }
@@ -108,6 +125,10 @@ int adjoint_blocks(Handle* h, const double* wend, double* out, double* gacc, cud
       C_bs = nb;
     }
     PX_TRY(axpby(h, b.D, nb, C, C_bs, 1.0, nullptr, 0, 0.0, b.st));
+    if (ss) {  // Gp += Δ·φ₁(ΔAᵀ)·S (the exp result of this action is not used)
+      double* res = nullptr;
+      PX_TRY(exp_action(h, PX_PLAN_SLICE, h->AT, b.S, nb, nullptr, 0, b.Gp, &res, b.st));
+    }
     PX_CUDA(h, cudaEventRecord(b.ev, b.st));
   }
   for (int g = 0; g < h->lb; ++g) {
@@ -126,6 +147,7 @@ void free_blocks(Handle* h) {
     for (double* p : b.ACC) cudaFree(p);
     cudaFree(b.D);
     cudaFree(b.Gp);
+    cudaFree(b.S);
     krylov_free(b.kw);
     if (b.st) cudaStreamDestroy(b.st);
     if (b.ev) cudaEventDestroy(b.ev);
@@ -151,6 +173,7 @@ int set_local_blocks(Handle* h, int blocks) {
     for (auto& p : b.ACC) PX_CUDA(h, cudaMalloc(&p, sizeof(double) * Bn));
     PX_CUDA(h, cudaMalloc(&b.D, sizeof(double) * Bn));
     PX_CUDA(h, cudaMalloc(&b.Gp, sizeof(double) * Bn));
+    PX_CUDA(h, cudaMalloc(&b.S, sizeof(double) * Bn));
     if (h->d.expaction == PX_EXP_KRYLOV) {
       std::string err;
       if (krylov_alloc(b.kw, h->d.krylov_m, h->n, h->B, &err) != PX_OK) {
@@ -240,9 +263,12 @@ int adjoint_linear(Handle* h, cudaStream_t s) {
   } else {
     const double* C = wend + (size_t)(h->Pl - 1) * h->n;
     long long C_bs = lane_bs;
+    const bool ss = use_ssum(h) && h->Pl > 1;
+    if (ss) PX_TRY(axpby(h, h->S, nb, C, C_bs, 1.0, nullptr, 0, 0.0, s));
     for (int q = h->Pl - 2; q >= 0; --q) {
       double* res = nullptr;
-      PX_TRY(exp_action(h, PX_PLAN_SLICE, h->AT, C, C_bs, wend + (size_t)q * h->n, lane_bs, h->G, &res, s));
+      PX_TRY(exp_action(h, PX_PLAN_SLICE, h->AT, C, C_bs, wend + (size_t)q * h->n, lane_bs, ss ? nullptr : h->G, &res,
+                        s, ss && q > 0 ? h->S : nullptr));
       C = res;
       C_bs = nb;
     }
@@ -253,6 +279,10 @@ int adjoint_linear(Handle* h, cudaStream_t s) {
       C_bs = nb;
     }
     PX_TRY(axpby(h, h->QDAG0, nb, C, C_bs, 1.0, nullptr, 0, 0.0, s));
+    if (ss) {  // G += Δ·φ₁(ΔAᵀ)·S (the exp result of this action is not used)
+      double* res = nullptr;
+      PX_TRY(exp_action(h, PX_PLAN_SLICE, h->AT, h->S, nb, nullptr, 0, h->G, &res, s));
+    }
   }
   tend(h, tm, s);
   tm = tbegin(h, PX_PHASE_OTHER, s);

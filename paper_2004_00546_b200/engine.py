@@ -86,18 +86,44 @@ class EngineSpec:
 
 # developer overrides of the kernel variants (tools/ experiments); tests use EngineSpec.variants
 ENV_VARIANTS = {"PX_MARCH2": "march2", "PX_M2_COLS": "march_cols", "PX_M2_BAND": "march_band",
-                "PX_CM_TERMS": "cheb_terms", "PX_CM_STRIP": "cheb_strip", "PX_CM_BAND": "cheb_band",
+                "PX_CM_TERMS": "cheb_terms", "PX_CM_TERMS_PHI": "cheb_terms_phi", "PX_CM_STRIP": "cheb_strip", "PX_CM_BAND": "cheb_band",
                 "PX_SCAN1D_CLUSTER": "scan1d_cluster", "PX_BURGERS_CLUSTER": "burgers_cluster"}
 
 
-def allreduce_sum(tensors, group=None) -> None:
-    """In-place SUM allreduce of each tensor over the process group (NCCL on GPU)."""
+def allreduce_sum(tensors, group=None, stream=None) -> None:
+    """In-place SUM allreduce of each tensor over the process group (NCCL on GPU), ordered
+    after the work enqueued on ``stream`` (the native kernels' stream) when one is given."""
+    import torch
     import torch.distributed as dist
-    for t in tensors:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    ctx = None
+    if stream and torch.cuda.is_available() and any(t.is_cuda for t in tensors):
+        ctx = torch.cuda.stream(torch.cuda.ExternalStream(stream))
+    if ctx is None:
+        for t in tensors:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        return
+    with ctx:
+        for t in tensors:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
 
 
-def distributed_gradient(eng, stream=None, group=None, want_fields: bool = True, reduce=allreduce_sum) -> None:
+def agree_status(code: int, group=None) -> int:
+    """Every rank contributes ``code`` (its failure code, or a large sentinel when healthy);
+    returns the MIN over ranks, the same value on every rank. On a CUDA (NCCL) group the
+    flag travels in a device tensor."""
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([code], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return int(t.item())
+
+
+_HEALTHY = 1 << 62
+
+
+def distributed_gradient(eng, stream=None, group=None, want_fields: bool = True, reduce=allreduce_sum,
+                         agree=agree_status) -> None:
     """One sharded gradient evaluation: each rank runs its slice
     block, the u(T) partials are summed, every rank finishes the direct sweep
     identically, runs its adjoint block and the adjoint partials are summed.
@@ -106,24 +132,49 @@ def distributed_gradient(eng, stream=None, group=None, want_fields: bool = True,
     finish_adjoint`` and ``view(field)`` (a tensor aliasing the field's buffer);
     the partial conventions are the C ABI's (`px_finish_*` add the q0 / q†_T terms
     once, after the reduction).
+
+    Fail-fast on every rank (the reference aborts all workers, `workers.py:140-160`): before
+    each collective the ranks agree on a status word (``agree``: MIN over ranks of
+    phase·world + rank for a failed rank); if any rank failed, every rank raises
+    ``CollectiveFailure(first failing rank, phase, cause)`` instead of entering the reduction
+    its peer will never join.
     """
     rank = getattr(getattr(eng, "spec", None), "rank", 0)
-    phases = (
-        ("direct", lambda: eng.direct_partial(stream)),
-        ("direct allreduce", lambda: reduce([eng.view(f) for f in eng.direct_reduce_fields()], group)),
-        ("finish direct", lambda: eng.finish_direct(stream)),
-        ("adjoint", lambda: eng.adjoint_partial(stream)),
-        ("adjoint allreduce",
-         lambda: reduce([eng.view(f) for f in eng.adjoint_reduce_fields(want_fields)], group)),
-        ("finish adjoint", lambda: eng.finish_adjoint(stream)),
+    world = max(1, getattr(getattr(eng, "spec", None), "world", 1))
+    stages = (
+        (("direct", lambda: eng.direct_partial(stream)),),
+        (("finish direct", lambda: eng.finish_direct(stream)), ("adjoint", lambda: eng.adjoint_partial(stream))),
+        (("finish adjoint", lambda: eng.finish_adjoint(stream)),),
     )
-    for name, run in phases:
+    collectives = (
+        ("direct allreduce", lambda: reduce([eng.view(f) for f in eng.direct_reduce_fields()], group, stream)),
+        ("adjoint allreduce",
+         lambda: reduce([eng.view(f) for f in eng.adjoint_reduce_fields(want_fields)], group, stream)),
+    )
+    names = [n for st in stages for n, _ in st] + [n for n, _ in collectives]
+    for i, stage in enumerate(stages):
+        code, cause = _HEALTHY, None
+        for name, run in stage:
+            try:
+                run()
+            except Exception as e:  # noqa: BLE001 - mapped onto the reference's CollectiveFailure
+                code, cause = names.index(name) * world + rank, e
+                break
+        if i == len(stages) - 1:
+            if cause is not None:
+                raise CollectiveFailure(rank, names[code // world], cause) from cause
+            return
+        cname, crun = collectives[i]
+        first = agree(code, group)
+        if first != _HEALTHY:
+            failed_rank, phase = first % world, names[first // world]
+            err = cause if failed_rank == rank and cause is not None else RuntimeError(
+                f"rank {failed_rank} failed in {phase}; aborting the collective solve")
+            raise CollectiveFailure(failed_rank, phase, err) from cause
         try:
-            run()
-        except CollectiveFailure:
-            raise
-        except Exception as e:  # the reference's fail-fast convention (`workers.py:140-160`)
-            raise CollectiveFailure(rank, name, e) from e
+            crun()
+        except Exception as e:  # noqa: BLE001
+            raise CollectiveFailure(rank, cname, e) from e
 
 
 class ParaexpEngine:
@@ -312,8 +363,18 @@ class ParaexpEngine:
         """CUDA-graph replay of the single-rank gradient (default on)."""
         N.check(self.lib, self.lib.px_set_graphs(self.h, 1 if enable else 0), self.h)
 
-    def set_timing(self, enable: bool) -> None:
-        N.check(self.lib, self.lib.px_set_timing(self.h, 1 if enable else 0), self.h)
+    def set_timing(self, enable, kernels: bool = False) -> None:
+        """Phase timing (CUDA events around each sweep phase); ``kernels`` adds events around
+        every launch of the fused RK4 march and the Chebyshev passes (eager, no graph)."""
+        mode = (2 if kernels else 1) if enable else 0
+        N.check(self.lib, self.lib.px_set_timing(self.h, mode), self.h)
+
+    def kernel_timing(self, kclass: int) -> tuple[float, int]:
+        """(device ms, launches) of one kernel class since the last call (timing with kernels)."""
+        ms = ctypes.c_double()
+        cnt = ctypes.c_uint64()
+        N.check(self.lib, self.lib.px_get_kernel_timing(self.h, kclass, ctypes.byref(ms), ctypes.byref(cnt)), self.h)
+        return float(ms.value), int(cnt.value)
 
     def timing(self) -> dict:
         """Per-phase device time (CUDA events around each sweep phase) since the last call."""

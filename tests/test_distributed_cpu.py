@@ -101,7 +101,7 @@ def test_phase_failure_maps_to_collective_failure():
     calls = []
 
     class Fake:
-        spec = SimpleNamespace(rank=3)
+        spec = SimpleNamespace(rank=3, world=4)
 
         def direct_partial(self, s): calls.append("direct")
         def direct_reduce_fields(self): return []
@@ -113,7 +113,49 @@ def test_phase_failure_maps_to_collective_failure():
         def finish_adjoint(self, s): calls.append("finish_adjoint")
 
     with pytest.raises(CollectiveFailure) as ei:
-        distributed_gradient(Fake(), reduce=lambda ts, g: None)
+        distributed_gradient(Fake(), reduce=lambda ts, g, s: None, agree=lambda code, g: code)
     assert ei.value.worker == 3 and ei.value.subproblem == "adjoint"
     assert isinstance(ei.value.cause, RuntimeError)
     assert calls == ["direct", "finish_direct"]
+
+
+def _failing_worker(rank, world, port, out_dir, bad_rank, bad_phase):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.config_mode import OracleRank
+    from paper_2004_00546_b200.engine import distributed_gradient
+    from paper_2004_00546_b200.errors import CollectiveFailure
+    c, ps, pl = _case()
+    u0, ut, ctrl = c.inputs()
+    eng = OracleRank(c.grid.nx, c.grid.ny, c.system.A.as_tuple(), c.system.basis, c.spec.T, c.P, c.nsteps,
+                     u0, ut, ctrl, ps, pl, rank, world)
+    if rank == bad_rank:
+        def boom(stream=None):
+            raise MemoryError("injected failure")
+        setattr(eng, bad_phase, boom)
+    outcome = "ok"
+    try:
+        distributed_gradient(eng)
+    except CollectiveFailure as e:
+        outcome = f"{e.worker}|{e.subproblem}|{type(e.cause).__name__}"
+    with open(os.path.join(out_dir, f"rank{rank}.txt"), "w") as f:
+        f.write(outcome)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("bad_phase,label", [("direct_partial", "direct"), ("adjoint_partial", "adjoint")])
+def test_rank_failure_aborts_every_rank(bad_phase, label, tmp_path):
+    """One rank fails before a collective: every rank raises CollectiveFailure naming that rank
+    and phase (none is left blocked in the allreduce; the reference's abort of all workers,
+    `workers.py:140-160`)."""
+    world, bad = 2, 1
+    mp.start_processes(_failing_worker, args=(world, _free_port(), str(tmp_path), bad, bad_phase), nprocs=world,
+                       start_method="spawn")
+    for r in range(world):
+        worker, phase, cause = open(os.path.join(tmp_path, f"rank{r}.txt")).read().split("|")
+        assert int(worker) == bad and phase == label
+        assert cause == ("MemoryError" if r == bad else "RuntimeError")

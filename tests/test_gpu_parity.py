@@ -208,6 +208,21 @@ def test_local_blocks_chebyshev(blocks, monkeypatch):
     release_engines()
 
 
+@pytest.mark.parametrize("terms", [1, 2, 3, 4, 5, 6, 7])
+def test_chebyshev_pass_sizes(terms):
+    """The 2D Chebyshev passes with at most `terms` fused terms (balanced split of the degree;
+    7 uses the (M−1)-slot accumulator ring) against the oracle, strip mode, direct and φ₁."""
+    from paper_2004_00546_b200 import RK4Config, baseline, release_engines, scaled
+    from paper_2004_00546_b200.optimization import get_engine
+    release_engines()
+    c = scaled(baseline(5), nx=704, P=6, steps_per_slice=4, K=16, T=0.05)
+    eng = get_engine(c.system, c.P, RK4Config(c.dt), c.expaction, c.batch)
+    eng.set_variant("cheb_terms", terms)
+    eng.set_variant("cheb_terms_phi", terms)
+    _check(_gpu_linear(c), _oracle_linear(c))
+    release_engines()
+
+
 def test_config5_scaled():
     from paper_2004_00546_b200 import baseline, scaled
     c = scaled(baseline(5), nx=128, P=16, steps_per_slice=8, K=64)

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--tols", type=float, nargs="+", default=[None])
     ap.add_argument("--blocks", type=int, nargs="+", default=[1])
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--variants", nargs="*", default=[], help="kernel variants name=value (_native.VARIANTS)")
     args = ap.parse_args()
     import torch
     from paper_2004_00546_b200 import baseline
@@ -33,7 +34,8 @@ def main():
     for tol in args.tols:
         c = c0 if tol is None else replace(c0, expaction=replace(c0.expaction, tol=tol))
         for lb in args.blocks:
-            eng = ParaexpEngine(EngineSpec(c.system, c.P, c.dt, c.expaction, c.batch, local_blocks=lb))
+            var = tuple((kv.split("=")[0], int(kv.split("=")[1])) for kv in args.variants)
+            eng = ParaexpEngine(EngineSpec(c.system, c.P, c.dt, c.expaction, c.batch, local_blocks=lb, variants=var))
             eng.set_inputs(*dev)
             s = int(torch.cuda.current_stream().cuda_stream)
             for _ in range(2):
@@ -52,6 +54,7 @@ def main():
             plan = eng.plans.get(0)
             print(json.dumps({
                 "config": args.config, "tol": c.expaction.tol, "local_blocks": eng.local_blocks,
+                "variants": dict(var),
                 "ms_per_gradient": e0.elapsed_time(e1) / args.steps,
                 "slice_plan": None if plan is None else [plan.substeps, getattr(plan, "degree", None)],
                 "phases": {k: {"ms": v["ms"] / args.steps, "launches": v["launches"] / args.steps}
