@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define PX_ABI_VERSION 2
+#define PX_ABI_VERSION 3
 
 enum {
   PX_OK = 0,
@@ -255,6 +255,62 @@ enum {
 };
 /* Summed device ms and launch count of one kernel class since the last call (timing mode 2). */
 int px_get_kernel_timing(void* handle, int kclass, double* ms, uint64_t* launches);
+
+/* ---- The reference's hybrid algorithm with its own objective (hybrid.py:1-290,
+ * optimization.py:84-112,172-189) — a separate handle ----------------
+ * 1D Burgers (V ≡ 0) with the forcing field f(x)·θ(t), θ(t) = law[0] + law[1]·sin(law[3]·t) +
+ * law[2]·cos(law[3]·t) (the reference's f·sin(ωt): {0, 1, 0, ω}); tracking objective
+ * J = (1/T)∫‖u − u_t‖² dt (trapezoid on the RK4 nodes) against a target given on the nodes;
+ * slices of any widths on the serial sweep's uniform node grid (the geometric partition,
+ * hybrid.py:35-55); adjoint in the reference's solve_hybrid form (zero terminal data + source
+ * s = 2(u − u_t) in every slice, the slice ends through the frozen J(ū_m)ᵀ of all earlier
+ * slices); gradient ∂L/∂f = (1/T)∫θ(t)·q†(t) dt (gradient_wrt_forcing). With overlap, each
+ * slice's adjoint solve starts on its own SM the moment the serial direct kernel has stored
+ * the slice (a progress flag per slice in HBM), i.e. during the serial sweep — the reference's
+ * overlapped worker pipeline (hybrid.py:185-204). */
+typedef struct px_hybrid_desc {
+  int nx;              /* periodic 1D grid, n = nx */
+  double D, hx, T;     /* diffusion, spacing, horizon */
+  int batch;           /* B members, one forcing field each */
+  int nslices;         /* P */
+  const int* offsets;  /* P+1 node offsets 0 = o_0 < … < o_P = S (host); h = T/S */
+  double law[4];       /* θ(t) */
+  int target_batched;  /* 0: target (S+1)×n shared by the members; 1: (S+1)×B×n */
+} px_hybrid_desc;
+enum {
+  PX_HFIELD_J = 0,     /* (B)          tracking cost */
+  PX_HFIELD_GRAD = 1,  /* (B, n)       ∂L/∂f */
+  PX_HFIELD_UT = 2,    /* (B, n)       u(T) */
+  PX_HFIELD_QDAG0 = 3, /* (B, n)       q†(0) */
+  PX_HFIELD_TRAJ = 4,  /* (S+1, B, n)  direct trajectory */
+  PX_HFIELD_AEND = 5,  /* (B, P, n)    slice adjoint solutions at the slice starts */
+  PX_HFIELD_ZL = 6,    /* (B, P, n)    their ∫θ·a dt */
+  PX_HFIELD_UBAR = 7,  /* (P, B, n)    slice means */
+  PX_HFIELD_COUNT = 8
+};
+int px_hybrid_create(const px_hybrid_desc* desc, void** out_handle);
+void px_hybrid_destroy(void* handle);
+const char* px_hybrid_last_error(const void* handle);
+/* u0 (B×n), f (B×n), target ((S+1)×n or (S+1)×B×n), qdag_T (B×n terminal data, NULL = 0). */
+int px_hybrid_set_inputs(void* handle, const double* u0, const double* f, const double* target,
+                         const double* qdag_T, int mem, void* stream);
+/* Serial direct sweep + J, and every slice's adjoint inhomogeneous solve: overlapped with the
+ * sweep when `overlap` and all CTAs fit co-resident (else after it; px_hybrid_get_timing says). */
+int px_hybrid_direct(void* handle, int overlap, void* stream);
+/* Slice means ū_p and the frozen operators' FOV box (re_lo, re_hi, im) to the host (syncs). */
+int px_hybrid_bounds(void* handle, double* out3, void* stream);
+/* Slice p's plan for exp(Δ_p J(ū_p)ᵀ) (span Δ_p = (o_{p+1} − o_p)·h) with the time-law series
+ * coef_gc / coef_gs (degree+1 each; NULL when law[3] == 0), see expaction.ChebPlan. */
+int px_hybrid_set_slice_plan(void* handle, int p, const px_cheb_plan* plan, const double* coef_gc,
+                             const double* coef_gs);
+/* The frozen-operator carry and the gradient (needs every slice plan). */
+int px_hybrid_adjoint(void* handle, void* stream);
+int px_hybrid_get(void* handle, int field, double* dst, size_t count, int mem, void* stream);
+/* Device ms of the last px_hybrid_direct: ms[0] the serial direct kernel, ms[1] the slice-solve
+ * kernel (from its launch, waiting included), ms[2] both (first start to last end), ms[3] the
+ * slice solves' tail after the direct ended (the adjoint work the overlap did not hide),
+ * ms[4] 1 if the slice solves overlapped the sweep. */
+int px_hybrid_get_timing(void* handle, double* ms5);
 
 int px_get_stats(void* handle, px_stats* out);
 int px_reset_stats(void* handle);

@@ -646,3 +646,172 @@ def checkpointed_gradient(segment_gradient, direct_final, u0, M: int):
         G = r.G if G is None else G + r.G
         qd = r.qdag0
     return J, grad, qd, G, uT, states
+
+
+# ---------------------------------------------------------------------------
+# The reference's own hybrid loop (hybrid.py, optimization.py:172-189): tracking
+# objective, forcing field × time law, Option B adjoint with an adjoint source,
+# variable (geometric) slices — SURVEY §8(f) rank 2
+# ---------------------------------------------------------------------------
+
+
+def law_value(law, t):
+    """θ(t) = α + β·sin(ωt) + γ·cos(ωt); the reference's forcing law is sin(ωt)
+    (`problems.py:155-162`: α = γ = 0, β = 1)."""
+    a, b, c, w = law
+    return a + b * np.sin(w * t) + c * np.cos(w * t)
+
+
+def law_substep_coef(plan: ChebPlan, law, t_top: float):
+    """Series coefficients of ∫₀^τ θ(t_top − s)·e^{sM} ds (one substep of width τ, reflected
+    time from t_top): α·τφ₁ + A·Gc + B·Gs with A = β sin ωt + γ cos ωt, B = −β cos ωt + γ sin ωt."""
+    a, b, c, w = law
+    if w == 0.0:
+        return (a + c) * plan.coef_phi
+    if plan.coef_gc is None or plan.omega != w:
+        raise ValueError("plan lacks the time-law series for this ω")
+    A = b * np.sin(w * t_top) + c * np.cos(w * t_top)
+    Bc = -b * np.cos(w * t_top) + c * np.sin(w * t_top)
+    return a * plan.coef_phi + A * plan.coef_gc + Bc * plan.coef_gs
+
+
+def cheb_law_action(apply, plan: ChebPlan, v, G, law, t_top: float):
+    """exp(span·M)v, and G += ∫₀^span θ(t_top − σ)·e^{σM}v dσ, by the plan's substeps."""
+    c0, d, sigma = plan.center, plan.scale, float(plan.sigma)
+    be = plan.coef_exp
+    two_over = 2.0 / d
+    tau = plan.span / plan.substeps
+    y = v
+    for j in range(plan.substeps):
+        bl = law_substep_coef(plan, law, t_top - j * tau)
+        u_prev = y
+        acc = be[0] * u_prev
+        lac = bl[0] * u_prev
+        u_cur = (apply(u_prev) - c0 * u_prev) / d
+        acc = acc + be[1] * u_cur
+        lac = lac + bl[1] * u_cur
+        for k in range(2, plan.degree + 1):
+            u_next = two_over * (apply(u_cur) - c0 * u_cur) + sigma * u_prev
+            u_prev, u_cur = u_cur, u_next
+            acc = acc + be[k] * u_cur
+            lac = lac + bl[k] * u_cur
+        G += lac
+        y = acc
+    return y
+
+
+def burgers_direct_law(u0, f, law, D, h_grid, h, S):
+    """Serial classical RK4 of u' = −u∘Dx u + D·L u + θ(t)·f keeping every node."""
+    traj = np.empty((S + 1,) + u0.shape)
+    u = u0.copy()
+    traj[0] = u
+    for i in range(S):
+        t = i * h
+        th1, th2, th4 = law_value(law, t), law_value(law, t + 0.5 * h), law_value(law, t + h)
+        k1 = burgers_rhs(u, th1 * f, D, h_grid)
+        k2 = burgers_rhs(u + (0.5 * h) * k1, th2 * f, D, h_grid)
+        k3 = burgers_rhs(u + (0.5 * h) * k2, th2 * f, D, h_grid)
+        k4 = burgers_rhs(u + h * k3, th4 * f, D, h_grid)
+        u = u + (h / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+        traj[i + 1] = u
+    return traj
+
+
+def slice_means_var(traj, offsets):
+    """Trapezoid mean of each slice's nodes for variable slices (`problems.py:346-366`)."""
+    out = []
+    for p in range(len(offsets) - 1):
+        a, b = int(offsets[p]), int(offsets[p + 1])
+        w = np.ones(b - a + 1)
+        w[0] = w[-1] = 0.5
+        w /= (b - a)
+        out.append(np.tensordot(w, traj[a:b + 1], axes=(0, 0)))
+    return np.stack(out)
+
+
+def tracking_cost(traj, target, T, h):
+    """J = (1/T)·∫‖u − u_t‖² dt, trapezoid over the RK4 nodes (`optimization.py:84-93` on
+    the node grid instead of a 200-point probe grid)."""
+    d = traj - target
+    e = np.sum(d * d, axis=-1)                 # (S+1, B)
+    w = np.ones(e.shape[0])
+    w[0] = w[-1] = 0.5
+    return (h / T) * np.tensordot(w, e, axes=(0, 0))
+
+
+def burgers_tracking_hybrid(nx, D, T, offsets, u0, f, law, target, plans_for, qdag_T=None):
+    """The reference's hybrid loop with the configs' numerics.
+
+    * direct: serial RK4 with forcing θ(t)·f (`hybrid.py:185-191`, `problems.py:155-162`);
+    * cost: J = (1/T)∫‖u − u_t‖² dt (trapezoid on the nodes) — ``target`` (S+1, n) or (S+1, B, n);
+    * adjoint, the reference's `solve_hybrid` (Option B, `hybrid.py:194-237`): per slice the
+      inhomogeneous solve from zero terminal data with exact Jᵀ(u(t)) and the adjoint source
+      s(t) = 2(u(t) − u_t(t)) (`optimization.py:96-100,172-175`), trajectory and target linearly
+      interpolated at the stages; the slice ends are propagated through the frozen
+      J(ū_m)ᵀ of every earlier slice (`propagate_span`, summed as one carry); a non-zero
+      ``qdag_T`` adds the final span (`hybrid.py:232-233`);
+    * gradient: ∂L/∂f = (1/T)∫ θ(t)·q†(t) dt (`optimization.py:103-112`), RK4-consistent in the
+      slices and the planned series for the homogeneous parts.
+
+    ``offsets``: the slices' node offsets (P+1 ints, 0 … S), h = T/S. ``plans_for(ubar)`` returns
+    the per-slice plans (slice p of span (offsets[p+1]−offsets[p])·h). Returns an OracleResult
+    whose ``grad`` is the field gradient (B, n)."""
+    n = nx
+    hg = 2.0 * np.pi / nx
+    f = np.atleast_2d(np.asarray(f, dtype=np.float64))
+    B = f.shape[0]
+    u0 = np.broadcast_to(_as_batch(u0, n), (B, n)).copy()
+    offsets = np.asarray(offsets, dtype=np.int64)
+    P = len(offsets) - 1
+    S = int(offsets[-1])
+    h = T / S
+    target = np.asarray(target, dtype=np.float64)
+    tg = target[:, None, :] if target.ndim == 2 else target
+    traj = burgers_direct_law(u0, f, law, D, hg, h, S)
+    J = tracking_cost(traj, tg, T, h)
+    ubar = slice_means_var(traj, offsets)
+    plans = plans_for(ubar)
+
+    a_end = np.empty((P, B, n))
+    zsum = np.zeros((B, n))
+    for p in range(P):
+        a = np.zeros((B, n))
+        z = np.zeros((B, n))
+        for i in range(int(offsets[p + 1] - offsets[p])):
+            top = int(offsets[p + 1]) - i
+            ua, ub = traj[top], traj[top - 1]
+            um = 0.5 * ua + 0.5 * ub
+            ta, tb = tg[top], tg[top - 1]
+            tm = 0.5 * ta + 0.5 * tb
+            sa, sm, sb = 2.0 * (ua - ta), 2.0 * (um - tm), 2.0 * (ub - tb)
+            t_a = top * h
+            th_a, th_m, th_b = law_value(law, t_a), law_value(law, t_a - 0.5 * h), law_value(law, t_a - h)
+            k1 = burgers_adjoint_apply(ua, a, D, hg) + sa
+            Y2 = a + (0.5 * h) * k1
+            k2 = burgers_adjoint_apply(um, Y2, D, hg) + sm
+            Y3 = a + (0.5 * h) * k2
+            k3 = burgers_adjoint_apply(um, Y3, D, hg) + sm
+            Y4 = a + h * k3
+            k4 = burgers_adjoint_apply(ub, Y4, D, hg) + sb
+            z = z + (h / 6.0) * (th_a * a + 2.0 * th_m * (Y2 + Y3) + th_b * Y4)
+            a = a + (h / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+        a_end[p] = a
+        zsum += z
+
+    Gh = np.zeros((B, n))
+    if qdag_T is not None:
+        C = np.broadcast_to(_as_batch(qdag_T, n), (B, n)).copy()
+        top_p = P - 1
+    else:
+        C = a_end[P - 1].copy()
+        top_p = P - 2
+    for p in range(top_p, -1, -1):
+        ub_ = ubar[p]
+        C = cheb_law_action(lambda y, ub_=ub_: burgers_adjoint_apply(ub_, y, D, hg), plans[p], C, Gh, law,
+                            float(offsets[p + 1]) * h)
+        if not (qdag_T is None and p == P - 1):
+            C = C + a_end[p]
+    grad = (zsum + Gh) / T
+    return OracleResult(J=J, grad=grad, uT=traj[-1], qdag0=C, G=grad,
+                        extras={"traj": traj, "ubar": ubar, "plans": plans, "a_end": a_end, "zsum": zsum,
+                                "Gh": Gh})

@@ -16,9 +16,11 @@ from .errors import (
     IntegrationFailure,
     IterationDivergence,
     NativeUnavailable,
+    PilotTooShort,
     PropagationFailure,
 )
-from .expaction import ChebPlan, ChebyshevConfig, KrylovConfig, KrylovPlan, plan_chebyshev, plan_krylov
+from .expaction import ChebPlan, ChebyshevConfig, KrylovConfig, KrylovPlan, plan_chebyshev, plan_family, plan_krylov
+from .hybrid import HybridPlan, TimeLaw, estimate_k, make_hybrid_plan, partition_geometric, slice_offsets
 from .nonlinear import NonlinearResult, solve_direct_nonlinear
 from .optimization import (
     ALGORITHMS,
@@ -59,5 +61,12 @@ from .problems import (
 )
 from .solvers import solve_adjoint_linear, solve_direct_linear, solve_hybrid, synthesize_truth
 from .systems import System, build_system
+from .tracking import (
+    HybridTrackingEngine,
+    HybridTrackingResult,
+    release_tracking_engines,
+    solve_hybrid_tracking,
+    synthesize_trajectory,
+)
 
 __all__ = [name for name in dir() if not name.startswith("_")]

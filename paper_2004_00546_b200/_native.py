@@ -27,7 +27,7 @@ PX_MAX_LOCAL_BLOCKS = 16
 (PX_FIELD_J, PX_FIELD_GRAD, PX_FIELD_UT, PX_FIELD_QDAG0, PX_FIELD_G, PX_FIELD_UBND,
  PX_FIELD_FROZEN_BOUNDS, PX_FIELD_VEND, PX_FIELD_WEND, PX_FIELD_TRAJ) = range(10)
 PX_FLAG_BOUNDARY_STATES, PX_FLAG_Z_ACCUM = 1, 2
-ABI_VERSION = 2
+ABI_VERSION = 3
 # kernel-variant keys (px_set_variant)
 VARIANTS = {"march2": 0, "march_cols": 1, "march_band": 2, "cheb_terms": 3, "cheb_strip": 4, "cheb_band": 5,
             "scan1d_cluster": 6, "burgers_cluster": 7, "cheb_terms_phi": 8}
@@ -68,6 +68,24 @@ class ChebPlanC(ctypes.Structure):
         ("coef_exp", POINTER(c_double)),
         ("coef_phi", POINTER(c_double)),
     ]
+
+
+class HybridDesc(ctypes.Structure):
+    _fields_ = [
+        ("nx", c_int),
+        ("D", c_double),
+        ("hx", c_double),
+        ("T", c_double),
+        ("batch", c_int),
+        ("nslices", c_int),
+        ("offsets", POINTER(c_int)),
+        ("law", c_double * 4),
+        ("target_batched", c_int),
+    ]
+
+
+(PX_HFIELD_J, PX_HFIELD_GRAD, PX_HFIELD_UT, PX_HFIELD_QDAG0, PX_HFIELD_TRAJ, PX_HFIELD_AEND, PX_HFIELD_ZL,
+ PX_HFIELD_UBAR) = range(8)
 
 
 class Stats(ctypes.Structure):
@@ -130,6 +148,17 @@ SIGNATURES = {
     "px_get_kernel_timing": (c_int, [c_void_p, c_int, POINTER(c_double), POINTER(c_uint64)]),
     "px_get_stats": (c_int, [c_void_p, POINTER(Stats)]),
     "px_reset_stats": (c_int, [c_void_p]),
+    # the reference's hybrid with its tracking objective (a separate handle)
+    "px_hybrid_create": (c_int, [POINTER(HybridDesc), POINTER(c_void_p)]),
+    "px_hybrid_destroy": (None, [c_void_p]),
+    "px_hybrid_last_error": (ctypes.c_char_p, [c_void_p]),
+    "px_hybrid_set_inputs": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
+    "px_hybrid_direct": (c_int, [c_void_p, c_int, c_void_p]),
+    "px_hybrid_bounds": (c_int, [c_void_p, POINTER(c_double), c_void_p]),
+    "px_hybrid_set_slice_plan": (c_int, [c_void_p, c_int, POINTER(ChebPlanC), POINTER(c_double), POINTER(c_double)]),
+    "px_hybrid_adjoint": (c_int, [c_void_p, c_void_p]),
+    "px_hybrid_get": (c_int, [c_void_p, c_int, c_void_p, c_size_t, c_int, c_void_p]),
+    "px_hybrid_get_timing": (c_int, [c_void_p, POINTER(c_double)]),
 }
 
 _lib = None
@@ -157,9 +186,9 @@ def load(path: str | None = None):
     return lib
 
 
-def check(lib, rc: int, handle=None, t: float = float("nan")) -> None:
+def check(lib, rc: int, handle=None, t: float = float("nan"), hybrid: bool = False) -> None:
     if rc != 0:
-        msg = lib.px_last_error(handle)
+        msg = (lib.px_hybrid_last_error if hybrid else lib.px_last_error)(handle)
         raise_for_status(rc, msg.decode() if msg else "", t)
 
 

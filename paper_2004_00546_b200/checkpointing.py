@@ -39,16 +39,23 @@ from .systems import System
 
 @dataclass(frozen=True)
 class CheckpointSchedule:
-    """M equispaced checkpoints t_i = i·T/(M+1) inside (0, T) (`checkpointing.py:34-59`)."""
+    """Equispaced checkpoint times inside (0, T) (API of `checkpointing.py:34-59`).
+
+    ``checkpoints`` = M interior checkpoints split [0, T] into M + 1 equal segments;
+    the edges are ``T·i/(M+1)``, i = 0 … M+1.
+    """
 
     T: float
     checkpoints: int
 
     def __post_init__(self):
-        if self.T <= 0:
+        if not self.T > 0:
             raise ValueError("T must be positive")
         if self.checkpoints < 0:
             raise ValueError("checkpoint count cannot be negative")
+
+    def _edges(self) -> np.ndarray:
+        return np.linspace(0.0, 1.0, self.checkpoints + 2) * self.T
 
     @property
     def segment_count(self) -> int:
@@ -56,29 +63,35 @@ class CheckpointSchedule:
 
     @property
     def times(self) -> np.ndarray:
-        M = self.checkpoints
-        return self.T * np.arange(1, M + 1) / (M + 1)
+        """The M interior checkpoint times."""
+        return self._edges()[1:-1]
 
     @property
     def segment_bounds(self) -> list[tuple[float, float]]:
-        edges = np.concatenate([[0.0], self.times, [self.T]])
-        return [(float(edges[i]), float(edges[i + 1])) for i in range(len(edges) - 1)]
+        e = [float(x) for x in self._edges()]
+        e[-1] = float(self.T)
+        return list(zip(e[:-1], e[1:]))
 
 
+@dataclass
 class MemoryCounter:
-    """Resident dense-trajectory nodes, peak and current (`checkpointing.py:62-76`)."""
+    """Dense-trajectory node bookkeeping (API of `checkpointing.py:62-76`).
 
-    def __init__(self):
-        self.current = 0
-        self.peak = 0
-        self.total_allocated = 0
+    ``current`` nodes resident now, ``peak`` the high-water mark, ``total_allocated``
+    every node ever acquired.
+    """
 
-    def acquire(self, nodes: int):
-        self.current += nodes
+    current: int = 0
+    peak: int = 0
+    total_allocated: int = 0
+
+    def acquire(self, nodes: int) -> None:
         self.total_allocated += nodes
-        self.peak = max(self.peak, self.current)
+        self.current += nodes
+        if self.current > self.peak:
+            self.peak = self.current
 
-    def release(self, nodes: int):
+    def release(self, nodes: int) -> None:
         self.current -= nodes
 
 

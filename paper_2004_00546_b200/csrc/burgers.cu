@@ -8,6 +8,7 @@
 #include "internal.h"
 #include "burgers.cuh"
 #include "burgers_iter.cuh"
+#include "hybrid.cuh"
 
 namespace pxi {
 
@@ -145,6 +146,85 @@ int nl_sweep(Handle* h, double* err_max, cudaStream_t s) {
   h->stats.algorithmic_bytes += 32.0 * n * lanes * h->d.nsteps + 40.0 * n * terms;
   if (!std::isfinite(mx)) return fail(h, PX_ERR_NONFINITE, "non-finite iterate in the nonlinear sweep");
   return PX_OK;
+}
+
+}  // namespace pxi
+
+// ---- the reference's hybrid with its tracking objective (hybrid.cuh; hybrid.cu drives it) ----
+namespace pxi {
+
+namespace {
+template <int PPT>
+cudaError_t hyb_direct_t(const px::HybArgs& a, cudaStream_t s) {
+  px::k_hyb_direct<PPT><<<a.B, px::HYB_NT, 0, s>>>(a);
+  return cudaGetLastError();
+}
+template <int PPT>
+cudaError_t hyb_lanes_t(const px::HybArgs& a, size_t smem, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute((const void*)px::k_hyb_lanes<PPT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  px::k_hyb_lanes<PPT><<<a.B * a.P, px::HYB_NT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+template <int PPT>
+cudaError_t hyb_scan_t(const px::HybScanArgs& a, cudaStream_t s) {
+  px::k_hyb_scan<PPT><<<a.B, px::HYB_NT, 0, s>>>(a);
+  return cudaGetLastError();
+}
+}  // namespace
+
+#define PX_HYB_DISPATCH(PPT_VAR, CALL)   \
+  switch (PPT_VAR) {                     \
+    case 1: return CALL(1);              \
+    case 2: return CALL(2);              \
+    case 4: return CALL(4);              \
+    case 8: return CALL(8);              \
+    case 16: return CALL(16);            \
+    case 32: return CALL(32);            \
+    default: return cudaErrorInvalidValue; \
+  }
+
+cudaError_t hyb_launch_direct(const px::HybArgs& a, int ppt, cudaStream_t s) {
+#define PX_C(P) hyb_direct_t<P>(a, s)
+  PX_HYB_DISPATCH(ppt, PX_C)
+#undef PX_C
+}
+
+cudaError_t hyb_launch_lanes(const px::HybArgs& a, int ppt, size_t smem, cudaStream_t s) {
+#define PX_C(P) hyb_lanes_t<P>(a, smem, s)
+  PX_HYB_DISPATCH(ppt, PX_C)
+#undef PX_C
+}
+
+cudaError_t hyb_launch_scan(const px::HybScanArgs& a, int ppt, cudaStream_t s) {
+#define PX_C(P) hyb_scan_t<P>(a, s)
+  PX_HYB_DISPATCH(ppt, PX_C)
+#undef PX_C
+}
+
+cudaError_t hyb_lanes_occupancy(int ppt, size_t smem, int* per_sm) {
+#define PX_C(P)                                                                                    \
+  (cudaFuncSetAttribute((const void*)px::k_hyb_lanes<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                        (int)smem),                                                                \
+   cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, px::k_hyb_lanes<P>, px::HYB_NT, smem))
+  PX_HYB_DISPATCH(ppt, PX_C)
+#undef PX_C
+}
+#undef PX_HYB_DISPATCH
+
+cudaError_t hyb_launch_means_bounds(double* ubar, const double* traj, const int* offsets, int P, int B, int n,
+                                    double* bpart, int bblocks, double* bounds, double hx, double D,
+                                    cudaStream_t s) {
+  const size_t total = (size_t)P * B * n;
+  px::k_hyb_means<<<(unsigned)std::min<size_t>((total + 255) / 256, 4096), 256, 0, s>>>(ubar, traj, offsets, P,
+                                                                                         B, n);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  px::k_frozen_bounds<<<bblocks, 256, 0, s>>>(bpart, ubar, total, n, hx, D);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  px::k_frozen_bounds_final<<<1, 256, 0, s>>>(bounds, bpart, bblocks);
+  return cudaGetLastError();
 }
 
 }  // namespace pxi

@@ -12,6 +12,8 @@
 //   krylov.cu   krylov.cuh: batched Arnoldi exp-actions
 //   burgers.cu  burgers.cuh, burgers_iter.cuh: Burgers serial sweep, adjoint, Algorithm 2
 //   ops.cu      kernels.cuh: axpby, projections, reductions, control sources, closed-form ∫
+//   hybrid.cu   C ABI of the reference's hybrid with its tracking objective (px_hybrid_*); its
+//               kernels (hybrid.cuh) are instantiated in burgers.cu
 #pragma once
 #include <cuda_runtime.h>
 #include <cufft.h>
@@ -21,6 +23,7 @@
 
 #include "../../include/paraexp.h"
 #include "common.cuh"
+#include "hybrid_args.h"
 
 namespace pxi {
 
@@ -218,6 +221,14 @@ int burgers_adjoint(Handle* h, cudaStream_t s);
 int nl_init(Handle* h, cudaStream_t s);
 int nl_means_bounds(Handle* h, cudaStream_t s);
 int nl_sweep(Handle* h, double* err_max, cudaStream_t s);
+// the reference's hybrid with its tracking objective (hybrid.cuh, driven by hybrid.cu)
+cudaError_t hyb_launch_direct(const px::HybArgs& a, int ppt, cudaStream_t s);
+cudaError_t hyb_launch_lanes(const px::HybArgs& a, int ppt, size_t smem, cudaStream_t s);
+cudaError_t hyb_launch_scan(const px::HybScanArgs& a, int ppt, cudaStream_t s);
+cudaError_t hyb_lanes_occupancy(int ppt, size_t smem, int* per_sm);
+cudaError_t hyb_launch_means_bounds(double* ubar, const double* traj, const int* offsets, int P, int B, int n,
+                                    double* bpart, int bblocks, double* bounds, double hx, double D,
+                                    cudaStream_t s);
 
 }  // namespace pxi
 

@@ -28,6 +28,7 @@ needs ∫ q† dt, i.e. τ·φ₁(τB)·C alongside exp(τB)·C (SURVEY.md App. 
 from __future__ import annotations
 
 from dataclasses import dataclass, field, replace
+import math
 from functools import lru_cache
 
 import numpy as np
@@ -92,6 +93,11 @@ class ChebPlan:
     coef_exp: np.ndarray = field(repr=False)
     coef_phi: np.ndarray = field(repr=False)
     err_bound: float = 0.0
+    # time-law integrals (``omega`` > 0, the hybrid tracking path): per substep of width τ_s,
+    # Σ_k coef_gc[k]·U_k = ∫₀^τ_s cos(ωs)·e^{sM} ds·y and Σ_k coef_gs[k]·U_k = ∫₀^τ_s sin(ωs)·e^{sM} ds·y
+    omega: float = 0.0
+    coef_gc: np.ndarray | None = field(default=None, repr=False)
+    coef_gs: np.ndarray | None = field(default=None, repr=False)
 
     @property
     def terms(self) -> int:
@@ -127,6 +133,14 @@ def phi1(z: np.ndarray) -> np.ndarray:
     out[~small] = (np.expm1(zb.real) + np.exp(zb.real) * (np.cos(zb.imag) - 1.0)
                    + 1j * np.exp(zb.real) * np.sin(zb.imag)) / zb
     return out
+
+
+def law_integrals(z: np.ndarray, tau: float, omega: float) -> tuple[np.ndarray, np.ndarray]:
+    """(Gc, Gs)(z) = ∫₀^τ (cos ωs, sin ωs)·e^{sz} ds, from τφ₁(τ(z ± iω)) (complex-safe)."""
+    z = np.asarray(z, dtype=np.complex128)
+    ep = tau * phi1(tau * (z + 1j * omega))
+    em = tau * phi1(tau * (z - 1j * omega))
+    return 0.5 * (ep + em), (ep - em) / 2j
 
 
 def chebyshev_coefficients(f, center: float, d: float, imag: bool, n: int) -> np.ndarray:
@@ -196,7 +210,7 @@ def _evaluate_impl(region_pts, crouzeix, center, d, imag, tau, kmax):
             2.0 * EPS * crouzeix * rnd, be, bp)
 
 
-def _first_feasible(pts, crouzeix, center, d, imag, tau, kmax, tol_s, with_rounding, kcap):
+def _first_feasible(pts, crouzeix, center, d, imag, tau, kmax, tol_s, with_rounding, kcap, omega=0.0):
     """Smallest degree K (≥ 1) whose exp and φ₁ truncation errors (and rounding
     estimate) meet tol_s at K and K+1 — the same arithmetic as `_evaluate`, but
     stopping as soon as K is found, the monotone rounding estimate exceeds its
@@ -205,7 +219,14 @@ def _first_feasible(pts, crouzeix, center, d, imag, tau, kmax, tol_s, with_round
         nq = max(64, 2 * kmax + 32)
         be = chebyshev_coefficients(lambda z: np.exp(tau * z), center, d, imag, nq)[: kmax + 1]
         bp = chebyshev_coefficients(lambda z: tau * phi1(tau * z), center, d, imag, nq)[: kmax + 1]
-        if not (np.all(np.isfinite(be)) and np.all(np.isfinite(bp))):
+        # the time-law integral series (omega > 0) are held to the φ₁ series' bound
+        law = []
+        if omega > 0.0:
+            for j in range(2):
+                fl = lambda z, j=j: law_integrals(z, tau, omega)[j]
+                law.append((chebyshev_coefficients(fl, center, d, imag, nq)[: kmax + 1], fl(pts)))
+        if not (np.all(np.isfinite(be)) and np.all(np.isfinite(bp))
+                and all(np.all(np.isfinite(c)) for c, _ in law)):
             return None
         sigma = 1.0 if imag else -1.0
         X = (pts - center) / d
@@ -215,7 +236,8 @@ def _first_feasible(pts, crouzeix, center, d, imag, tau, kmax, tol_s, with_round
         Uprev, Ucur = np.ones_like(X), X.copy()
         Se = be[0] * Uprev
         Sp = bp[0] * Uprev
-        acc_r = abs(be[0]) + abs(bp[0]) / ptau
+        Sl = [c[0] * Uprev for c, _ in law]
+        acc_r = abs(be[0]) + abs(bp[0]) / ptau + sum(abs(c[0]) for c, _ in law) / ptau
         prev_ok = False
         errs = []
         for k in range(0, kmax + 1):
@@ -226,9 +248,13 @@ def _first_feasible(pts, crouzeix, center, d, imag, tau, kmax, tol_s, with_round
                 g = np.max(np.abs(Ucur))
                 Se = Se + be[k] * Ucur
                 Sp = Sp + bp[k] * Ucur
-                acc_r += (abs(be[k]) + abs(bp[k]) / ptau) * g
+                for j, (c, _) in enumerate(law):
+                    Sl[j] = Sl[j] + c[k] * Ucur
+                acc_r += (abs(be[k]) + abs(bp[k]) / ptau + sum(abs(c[k]) for c, _ in law) / ptau) * g
             ee = crouzeix * np.max(np.abs(Se - fe))
             ep = crouzeix * np.max(np.abs(Sp - fp)) / ptau
+            for j, (_, fv) in enumerate(law):
+                ep = max(ep, crouzeix * np.max(np.abs(Sl[j] - fv)) / ptau)
             rr = 2.0 * EPS * crouzeix * acc_r
             errs.append(max(ee, ep))
             if with_rounding and not rr <= 0.5 * tol_s:
@@ -236,7 +262,8 @@ def _first_feasible(pts, crouzeix, center, d, imag, tau, kmax, tol_s, with_round
             ok = ee <= tol_s and ep <= tol_s
             if ok and prev_ok:
                 K = max(k - 1, 1)
-                return K, be[: K + 1].copy(), bp[: K + 1].copy(), float(errs[K])
+                extra = tuple(c[: K + 1].copy() for c, _ in law)
+                return K, be[: K + 1].copy(), bp[: K + 1].copy(), float(errs[K]), extra
             prev_ok = ok
             if kcap is not None and k - 1 > kcap:
                 return None
@@ -265,7 +292,7 @@ _SUBSTEPS = (1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 24, 32, 40, 48, 64, 80, 96, 12
 
 
 def _plan_cheb(region: SpectralRegion, span: float, tol: float, max_degree: int,
-               substep_limit: int, with_rounding: bool = True) -> ChebPlan:
+               substep_limit: int, with_rounding: bool = True, omega: float = 0.0) -> ChebPlan:
     pts = region.boundary(1024)
     best = None
     for (c0, d, imag) in _foci_candidates(region):
@@ -280,20 +307,22 @@ def _plan_cheb(region: SpectralRegion, span: float, tol: float, max_degree: int,
             kcap = None if best is None else best[0] // s
             # the next degree must satisfy the bound too (no lucky dip)
             found = _first_feasible(pts, region.crouzeix, c0, d, imag, tau, max_degree, tol_s,
-                                    with_rounding, kcap)
+                                    with_rounding, kcap, omega)
             if found is None:
                 continue
-            K, be, bp, err = found
+            K, be, bp, err, extra = found
             cost = s * K
             if best is None or cost < best[0]:
-                best = (cost, c0, d, imag, s, K, be, bp, err)
+                best = (cost, c0, d, imag, s, K, be, bp, err, extra)
     if best is None:
         raise PropagationFailure(
             f"no Chebyshev plan within {substep_limit} substeps of degree <= {max_degree} "
             f"reaches tol={tol:g} over span {span:g}")
-    _, c0, d, imag, s, K, be, bp, err = best
+    _, c0, d, imag, s, K, be, bp, err, extra = best
+    gc, gs = extra if extra else (None, None)
     return ChebPlan(span=span, substeps=s, degree=K, center=c0, scale=d,
-                    sigma=1 if imag else -1, coef_exp=be, coef_phi=bp, err_bound=err)
+                    sigma=1 if imag else -1, coef_exp=be, coef_phi=bp, err_bound=err,
+                    omega=float(omega), coef_gc=gc, coef_gs=gs)
 
 
 def _region_key(region: SpectralRegion):
@@ -301,18 +330,22 @@ def _region_key(region: SpectralRegion):
 
 
 @lru_cache(maxsize=256)
-def _plan_cached(key, span, tol, max_degree, substep_limit):
+def _plan_cached(key, span, tol, max_degree, substep_limit, omega=0.0):
     ellipses, rect, crouzeix = key
     region = SpectralRegion(ellipses=ellipses, rect=rect, crouzeix=crouzeix)
-    return _plan_cheb(region, span, tol, max_degree, substep_limit)
+    return _plan_cheb(region, span, tol, max_degree, substep_limit, omega=omega)
 
 
-def plan_chebyshev(region: SpectralRegion, span: float, cfg: ChebyshevConfig) -> ChebPlan:
-    """Cheapest (foci, substeps, degree) reaching ``cfg.tol`` over ``span``."""
+def plan_chebyshev(region: SpectralRegion, span: float, cfg: ChebyshevConfig, omega: float = 0.0) -> ChebPlan:
+    """Cheapest (foci, substeps, degree) reaching ``cfg.tol`` over ``span``; with ``omega`` > 0
+    the plan also carries the time-law integral series (``coef_gc``, ``coef_gs``), held to
+    the same bound."""
     if span <= 0:
         raise ValueError("span must be positive")
+    if omega < 0:
+        raise ValueError("omega must be non-negative")
     return _plan_cached(_region_key(region), float(span), float(cfg.tol),
-                        int(cfg.max_degree), int(cfg.substep_limit))
+                        int(cfg.max_degree), int(cfg.substep_limit), float(omega))
 
 
 @lru_cache(maxsize=64)
@@ -382,3 +415,35 @@ def plan_for(region: SpectralRegion, span: float, cfg, base_span: float | None =
     except PropagationFailure:
         return base
     return direct if direct.terms <= base.terms else base
+
+
+def plan_family(region: SpectralRegion, spans, cfg: ChebyshevConfig, omega: float = 0.0) -> list[ChebPlan]:
+    """Plans for a set of slice spans sharing one spectral region (variable slices, e.g. the
+    hybrid's geometric partition): the widest span is planned in full; every other span reuses
+    its foci with as many substeps as keep the substep width at most the widest plan's, and the
+    smallest degree that meets the same bounds at its own
+    substep width (a DCT and one series evaluation instead of a full search), falling back to
+    a full plan if none does."""
+    spans = [float(s) for s in spans]
+    if not spans or min(spans) <= 0:
+        raise ValueError("spans must be positive")
+    cfg1 = action_config(cfg, max(spans))
+    base = plan_chebyshev(region, max(spans), cfg1, omega)
+    pts = region.boundary(1024)
+    out: dict[float, ChebPlan] = {max(spans): base}
+    for sp in sorted(set(spans)):
+        if sp in out:
+            continue
+        c = action_config(cfg, sp)
+        s = max(1, math.ceil(base.substeps * sp / base.span - 1e-9))  # substep width ≤ the base's
+        found = _first_feasible(pts, region.crouzeix, base.center, base.scale, base.sigma > 0, sp / s,
+                                base.degree + 8, c.tol / s, True, None, omega)
+        if found is None:
+            out[sp] = plan_chebyshev(region, sp, c, omega)
+            continue
+        K, be, bp, err, extra = found
+        gc, gs = extra if extra else (None, None)
+        out[sp] = ChebPlan(span=sp, substeps=s, degree=K, center=base.center, scale=base.scale,
+                           sigma=base.sigma, coef_exp=be, coef_phi=bp, err_bound=err, omega=float(omega),
+                           coef_gc=gc, coef_gs=gs)
+    return [out[s] for s in spans]

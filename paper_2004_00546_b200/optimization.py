@@ -181,6 +181,10 @@ def direct_adjoint_loop(
     min_iter: int = 2,
     max_iter: int = 25,
     hybrid_adjoint: str = "absorbed",
+    objective: str = "terminal",
+    plan=None,
+    time_law=None,
+    overlap: bool = True,
 ) -> LoopResult:
     """One direct solve plus one adjoint solve, yielding J and ∂J/∂c (`optimization.py:154-231`).
 
@@ -191,7 +195,23 @@ def direct_adjoint_loop(
     "absorbed" — config 3's Option A (`solve_adjoint_varying` driven by the serial
     trajectory); "frozen_span" — the reference's `solve_hybrid` adjoint
     (`hybrid.py:194-237`: q†_T through the frozen J(ū_p)ᵀ; one rank).
+
+    ``objective="tracking"`` runs the reference's own loop (`optimization.py:172-189`) for
+    Burgers with ``algorithm`` "hybrid" or "serial": J = (1/T)∫‖u − u_t‖² dt against the target
+    trajectory ``q_true`` given on the serial sweep's nodes ((S+1, n) or (S+1, B, n), e.g. from
+    `tracking.synthesize_trajectory`), the forcing ``f``·θ(t) with ``time_law`` (`hybrid.TimeLaw`;
+    the reference's sin(ωt) is ``TimeLaw.sine(ω)``), ``f`` a field (n,) / (B, n) or mode
+    coefficients, the adjoint of the reference's `solve_hybrid` with the source 2(u − u_t) on the
+    geometric partition of ``plan`` (a `HybridPlan`; None: ``N`` equal slices), each slice's
+    adjoint solve overlapping the serial sweep (``overlap``), and ∂L/∂f = (1/T)∫θ·q† dt.
     """
+    if objective not in ("terminal", "tracking"):
+        raise ValueError(f"objective must be 'terminal' or 'tracking', not {objective!r}")
+    if objective == "tracking":
+        return _tracking_loop(system, f, q_true, algorithm, N, rk, expaction, u0, backend, plan, time_law, overlap)
+    if plan is not None or time_law is not None:
+        raise ConfigError("plan / time_law: the geometric partition and the forcing time law belong to the "
+                          "tracking objective (objective='tracking')")
     if backend not in BACKENDS:
         raise ValueError(f"unknown backend {backend!r}; the B200 path provides {BACKENDS}")
     if algorithm not in ALGORITHMS:
@@ -250,6 +270,40 @@ def direct_adjoint_loop(
         error_history=list(eng.nl_history) if algorithm == NONLINEAR else [],
         stats=eng.stats(),
     )
+
+
+def _tracking_loop(system, f, q_true, algorithm, N, rk, expaction, u0, backend, plan, time_law, overlap):
+    from .hybrid import HybridPlan, TimeLaw
+    from .tracking import solve_hybrid_tracking
+    if backend not in BACKENDS:
+        raise ValueError(f"unknown backend {backend!r}; the B200 path provides {BACKENDS}")
+    if system.is_linear:
+        raise ValueError("the tracking objective runs on the Burgers testbed (the hybrid's serial direct sweep)")
+    if algorithm not in (HYBRID, SERIAL):
+        raise ValueError("the tracking objective runs with algorithm 'hybrid' or 'serial'")
+    if rk is None:
+        raise ConfigError("rk: an RK4Config(dt) is required (fixed-step RK4)")
+    if algorithm == SERIAL:
+        plan, N = None, 1
+    if plan is not None and not isinstance(plan, HybridPlan):
+        raise ConfigError("plan: a HybridPlan (make_hybrid_plan)")
+    law = time_law or TimeLaw.constant()
+    fa = np.asarray(f, dtype=np.float64)
+    n = system.n
+    coeffs = fa.shape[-1] == system.basis.K and fa.shape[-1] != n
+    if not coeffs and fa.shape[-1] != n:
+        raise ValueError("f: a forcing field of n points or K mode coefficients")
+    field_f = system.basis.field(np.atleast_2d(fa)) if coeffs else np.atleast_2d(fa)
+    tick = time.perf_counter()
+    r = solve_hybrid_tracking(system, np.zeros(n) if u0 is None else u0, field_f, q_true, plan, N, rk,
+                              expaction or ChebyshevConfig(tol=1e-12), law, None, overlap)
+    grad = system.basis.project(r.grad) if coeffs else r.grad
+    single = fa.ndim == 1
+    return LoopResult(
+        float(r.J[0]) if single else r.J, grad[0] if single else grad,
+        DirectSolution(r.partition, r.final_state[0] if single else r.final_state),
+        AdjointSolution(r.partition, r.qdag0[0] if single else r.qdag0, r.grad[0] if single else r.grad),
+        iterations=1, seconds=time.perf_counter() - tick, stats={"timing": r.timing, "offsets": r.offsets})
 
 
 def descend(

@@ -14,6 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 EQUIDISTANT = "equidistant"
+GEOMETRIC = "geometric"
 
 
 @dataclass(frozen=True)
@@ -22,6 +23,7 @@ class TimePartition:
 
     boundaries: np.ndarray
     kind: str = EQUIDISTANT
+    ratio: float | None = None  # the hybrid's cost ratio k of a geometric partition (`paraexp.py:31-69`)
 
     def __post_init__(self):
         b = np.asarray(self.boundaries, dtype=np.float64)
