@@ -78,7 +78,10 @@ enum {
 
 enum {
   PX_FLAG_BOUNDARY_STATES = 1, /* keep u(T_p) for every slice edge (PX_FIELD_UBND; world = 1) */
-  PX_FLAG_Z_ACCUM = 2          /* 2D adjoint ∫: per-lane RK4 accumulator instead of the closed form */
+  PX_FLAG_Z_ACCUM = 2,         /* 2D adjoint ∫: per-lane RK4 accumulator instead of the closed form */
+  PX_FLAG_FIELD_CONTROL = 4    /* advection–diffusion: the control is a full spatial field f (B×n, K = n;
+                                  no basis tables) and PX_FIELD_GRAD is the field gradient ∫q† dt —
+                                  the reference's forcing field f_spatial (problems.py:155-162) */
 };
 
 /* Kernel-variant keys for px_set_variant / px_get_variant (per handle; defaults are the
@@ -154,6 +157,20 @@ int px_set_basis(void* handle, const double* tx, const double* ty, const int* ix
  * (timestepping.py:360-423) by the host planner's a-priori plan. */
 int px_set_cheb_plan(void* handle, int slot, const px_cheb_plan* plan);
 int px_set_krylov_plan(void* handle, int slot, double span, int substeps);
+/* Time-law series of the Chebyshev plan in `slot` (set it first): coef_gc / coef_gs (degree+1 host
+ * values each) are the series of ∫₀^τ_s cos(ωs)·e^{sz} ds and ∫₀^τ_s sin(ωs)·e^{sz} ds (ω of the
+ * handle's time law). Needed for every adjoint plan when the law has ω > 0. */
+int px_set_cheb_plan_law(void* handle, int slot, const double* coef_gc, const double* coef_gs);
+
+/* Forcing time law of the linear testbed: the control field f (from the coefficients and basis,
+ * or PX_FLAG_FIELD_CONTROL) is applied as f·θ(t), θ(t) = law[0] + law[1]·sin(law[3]·t) +
+ * law[2]·cos(law[3]·t) — the reference's f·sin(ωt) is {0, 1, 0, ω} (problems.py:155-162,
+ * systems.py:56-60). Every slice's RK4 lanes evaluate θ at their own stage times; the gradient
+ * becomes ∂J/∂f = ∫θ(t)·q†(t) dt (gradient_wrt_forcing, optimization.py:103-112, without the
+ * tracking objective's 1/T). {1, 0, 0, 0} restores the time-constant control. Chebyshev only
+ * (Krylov plans: PX_ERR_ARG); lanes run one RK4 step per launch and the adjoint keeps a per-lane
+ * θ-weighted ∫ accumulator. */
+int px_set_time_law(void* handle, const double* law4);
 
 /* Kernel-variant selection (PX_VAR_*), per handle; invalidates the captured gradient graph. */
 int px_set_variant(void* handle, int key, int value);

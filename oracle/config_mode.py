@@ -815,3 +815,91 @@ def burgers_tracking_hybrid(nx, D, T, offsets, u0, f, law, target, plans_for, qd
     return OracleResult(J=J, grad=grad, uT=traj[-1], qdag0=C, G=grad,
                         extras={"traj": traj, "ubar": ubar, "plans": plans, "a_end": a_end, "zsum": zsum,
                                 "Gh": Gh})
+
+
+# ---------------------------------------------------------------------------
+# Linear testbed with a forcing time law θ(t) (the reference's f·sin(ωt),
+# `problems.py:155-162`) and the terminal objective
+# ---------------------------------------------------------------------------
+
+
+def rk4_linear_law(apply, g0, f, law, t0: float, h: float, nsteps: int):
+    """Zero-data classical RK4 for y' = M y + g0 + θ(t)·f from t0 (θ at the stage times)."""
+    y = np.zeros_like(f)
+    for k in range(nsteps):
+        t = t0 + k * h
+        th1, th2, th4 = law_value(law, t), law_value(law, t + 0.5 * h), law_value(law, t + h)
+        k1 = apply(y) + g0 + th1 * f
+        k2 = apply(y + (0.5 * h) * k1) + g0 + th2 * f
+        k3 = apply(y + (0.5 * h) * k2) + g0 + th2 * f
+        k4 = apply(y + h * k3) + g0 + th4 * f
+        y = y + (h / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+    return y
+
+
+def rk4_adjoint_law(apply, c, law, t_top: float, h: float, nsteps: int):
+    """Zero-data RK4 in reflected time of w' = M w + c from t_top down, with the θ-weighted
+    RK4-consistent integral z = ∫θ(t)·w dt (RK4 on (w, z)' = (M w + c, θ(t_top − σ)·w))."""
+    w = np.zeros_like(c)
+    z = np.zeros_like(c)
+    for k in range(nsteps):
+        t = t_top - k * h
+        ta, tm, tb = law_value(law, t), law_value(law, t - 0.5 * h), law_value(law, t - h)
+        k1 = apply(w) + c
+        Y2 = w + (0.5 * h) * k1
+        k2 = apply(Y2) + c
+        Y3 = w + (0.5 * h) * k2
+        k3 = apply(Y3) + c
+        Y4 = w + h * k3
+        k4 = apply(Y4) + c
+        z = z + (h / 6.0) * (ta * w + 2.0 * tm * (Y2 + Y3) + tb * Y4)
+        w = w + (h / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+    return w, z
+
+
+def law_integral(law, T: float) -> float:
+    """∫₀ᵀ θ(t) dt."""
+    a, b, c, w = law
+    if w == 0.0:
+        return (a + c) * T
+    return a * T + b * (1.0 - np.cos(w * T)) / w + c * np.sin(w * T) / w
+
+
+def linear_gradient_law(grid_nx, grid_ny, A, basis, T, P, nsteps, u0, u_target, ctrl, law, plan_slice):
+    """One Paraexp direct-adjoint gradient of the linear testbed with the forcing f·θ(t) and the
+    terminal objective (single-rank scan). Every slice solves its own RK4 problem (θ shifts with
+    T_p); the carry is unchanged; the adjoint's ∂J/∂f = ∫θ(t)·q†(t) dt gathers the θ-weighted
+    lane integrals, ∫θ dt·q†_T and the law series of every carry (`law_substep_coef`)."""
+    nx, ny = grid_nx, grid_ny
+    n = nx * ny
+    ctrl = np.atleast_2d(np.asarray(ctrl, dtype=np.float64))
+    B = ctrl.shape[0]
+    u0 = np.broadcast_to(_as_batch(u0, n), (B, n))
+    ut = np.broadcast_to(_as_batch(u_target, n), (B, n))
+    AT = tuple(np.asarray(A)[[0, 2, 1, 4, 3]])
+    applyA = lambda u: stencil_apply(A, u, nx, ny)
+    applyAT = lambda u: stencil_apply(AT, u, nx, ny)
+    delta = T / P
+    h = delta / nsteps
+    f = basis.field(ctrl)
+    g0 = applyA(u0)
+    D = None
+    for p in range(P):
+        v = rk4_linear_law(applyA, g0, f, law, p * delta, h, nsteps)
+        D = v if p == 0 else exp_action(applyA, plan_slice, D) + v
+    uT = u0 + D
+    qT = uT - ut
+    J = 0.5 * np.sum(qT * qT, axis=1)
+    c = applyAT(qT)
+    C = None
+    G = law_integral(law, T) * qT
+    for p in range(P - 1, -1, -1):
+        w, z = rk4_adjoint_law(applyAT, c, law, (p + 1) * delta, h, nsteps)
+        G = G + z
+        if p == P - 1:
+            C = w
+        else:
+            C = cheb_law_action(applyAT, plan_slice, C, G, law, (p + 1) * delta) + w
+    qdag0 = qT + C
+    grad = basis.project(G)
+    return OracleResult(J=J, grad=grad, uT=uT, qdag0=qdag0, G=G)

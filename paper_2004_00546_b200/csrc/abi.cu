@@ -81,6 +81,9 @@ int px_create(const px_problem_desc* desc, void** out_handle) {
     return fail(nullptr, PX_ERR_ARG, "krylov_m out of range");
   if (d.basis_rows_x < 1 || d.basis_rows_x > 64 || d.basis_rows_y < 1)
     return fail(nullptr, PX_ERR_ARG, "bad basis table sizes");
+  if ((d.flags & PX_FLAG_FIELD_CONTROL) &&
+      (d.kind != PX_KIND_ADVDIFF || (size_t)d.K != (size_t)d.nx * d.ny))
+    return fail(nullptr, PX_ERR_ARG, "field control: advection–diffusion with K = n");
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess || ndev == 0)
@@ -105,17 +108,19 @@ int px_create(const px_problem_desc* desc, void** out_handle) {
   A(&h->u0, n);
   A(&h->ut, n);
   A(&h->ctrl, B * h->K);
-  A(&h->tx, (size_t)h->rows_x * d.nx);
-  A(&h->ty, (size_t)h->rows_y * d.ny);
-  if (rc == PX_OK) rc = pxi::dalloc_t(h, &h->ix, h->K);
-  if (rc == PX_OK) rc = pxi::dalloc_t(h, &h->iy, h->K);
+  const bool field_ctl = (d.flags & PX_FLAG_FIELD_CONTROL) != 0;
+  A(&h->tx, field_ctl ? 1 : (size_t)h->rows_x * d.nx);
+  A(&h->ty, field_ctl ? 1 : (size_t)h->rows_y * d.ny);
+  if (rc == PX_OK) rc = pxi::dalloc_t(h, &h->ix, field_ctl ? 1 : h->K);
+  if (rc == PX_OK) rc = pxi::dalloc_t(h, &h->iy, field_ctl ? 1 : h->K);
+  h->basis_set = field_ctl;  // a field control needs no basis tables
   A(&h->UT, B * n);
   A(&h->QT, B * n);
   A(&h->QDAG0, B * n);
   A(&h->G, B * n);
   A(&h->J, B);
   A(&h->GRAD, B * h->K);
-  A(&h->R, B * h->rows_x * d.ny);
+  A(&h->R, field_ctl ? 1 : B * h->rows_x * d.ny);
   h->red_blocks = (int)std::min<size_t>((n + 255) / 256, 1024);
   A(&h->partial, B * h->red_blocks);
   if (rc == PX_OK) rc = pxi::dalloc_t(h, &h->nonfinite, 1);
@@ -205,6 +210,7 @@ void px_destroy(void* handle) {
 int px_set_basis(void* handle, const double* tx, const double* ty, const int* ix, const int* iy) {
   Handle* h = bind(handle);
   if (!h || !tx || !ty || !ix || !iy) return fail(h, PX_ERR_ARG, "null argument");
+  if (h->d.flags & PX_FLAG_FIELD_CONTROL) return fail(h, PX_ERR_STATE, "field control has no basis tables");
   for (int k = 0; k < h->K; ++k)
     if (ix[k] < 0 || ix[k] >= h->rows_x || iy[k] < 0 || iy[k] >= h->rows_y)
       return fail(h, PX_ERR_ARG, "basis index out of range");
@@ -241,6 +247,39 @@ int px_set_cheb_plan(void* handle, int slot, const px_cheb_plan* p) {
   PX_CUDA(h, cudaMemcpy(pl.dcoef, pl.be.data(), sizeof(double) * (p->degree + 1), cudaMemcpyHostToDevice));
   PX_CUDA(h, cudaMemcpy(pl.dcoef + p->degree + 1, pl.bp.data(), sizeof(double) * (p->degree + 1),
                         cudaMemcpyHostToDevice));
+  return PX_OK;
+}
+
+int px_set_cheb_plan_law(void* handle, int slot, const double* gc, const double* gs) {
+  Handle* h = bind(handle);
+  if (!h || !gc || !gs) return fail(h, PX_ERR_ARG, "null argument");
+  if (slot < 0 || slot >= PX_PLAN_COUNT) return fail(h, PX_ERR_ARG, "bad plan slot");
+  Plan& pl = h->plans[slot];
+  if (!pl.set || pl.krylov) return fail(h, PX_ERR_STATE, "set the Chebyshev plan of this slot first");
+  pl.gc.assign(gc, gc + pl.degree + 1);
+  pl.gs.assign(gs, gs + pl.degree + 1);
+  h->graph_valid = false;
+  return PX_OK;
+}
+
+int px_set_time_law(void* handle, const double* law) {
+  Handle* h = bind(handle);
+  if (!h || !law) return fail(h, PX_ERR_ARG, "null argument");
+  for (int k = 0; k < 4; ++k)
+    if (!std::isfinite(law[k])) return fail(h, PX_ERR_ARG, "time law: non-finite coefficient");
+  if (law[3] < 0) return fail(h, PX_ERR_ARG, "time law: ω must be non-negative");
+  const bool constant = law[0] == 1.0 && law[1] == 0.0 && law[2] == 0.0;
+  if (!constant && h->d.kind != PX_KIND_ADVDIFF)
+    return fail(h, PX_ERR_ARG, "time law: the linear testbed (Burgers: the px_hybrid handle)");
+  if (!constant && h->d.expaction != PX_EXP_CHEBYSHEV)
+    return fail(h, PX_ERR_ARG, "time law: Chebyshev exp-actions only");
+  if (!constant && !h->fctl) PX_TRY(pxi::dalloc_t(h, &h->fctl, (size_t)h->B * h->n));
+  for (int k = 0; k < 4; ++k) h->law[k] = law[k];
+  h->has_law = !constant;
+  // the closed-form adjoint ∫ holds for the time-constant weight only
+  h->z_closed = !h->has_law && h->dim == 2 && !(h->d.flags & PX_FLAG_Z_ACCUM);
+  if (h->has_law && h->dim == 2 && !h->Z) PX_TRY(pxi::dalloc_t(h, &h->Z, (size_t)h->L * h->n));
+  h->graph_valid = false;
   return PX_OK;
 }
 

@@ -2,6 +2,8 @@
 // reference's Newton–Leja propagator (timestepping.py:306-423) with the host planner's
 // a-priori Chebyshev series, the stencil fused into the three-term recurrence.
 #include <algorithm>
+#include <cmath>
+#include <vector>
 
 #include "internal.h"
 #include "cheb_march.cuh"
@@ -33,7 +35,9 @@ int launch_cm(Handle* h, const px::ChebMarchArgs& a, unsigned blocks, cudaStream
 // 2D: Chebyshev action by row-marching passes of up to CM_MAXT fused terms
 int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const double* src, long long src_bs,
                       const double* addend, long long add_bs, double* pacc, double* ssum, double** result,
-                      cudaStream_t s) {
+                      cudaStream_t s, double ttop) {
+  std::vector<double> lawc;  // the time law's series of the current substep (pacc with a law)
+  const bool law = pacc && h->has_law;
   const size_t n = h->n;
   const int B = h->B;
   const long long nb = (long long)n;
@@ -83,6 +87,11 @@ int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const d
   const unsigned blocks = (unsigned)((size_t)B * a.nstrips * a.nbands);
   int wsel = 0;  // rotating pair of U output buffers
   for (int sub = 0; sub < pl.substeps; ++sub) {
+    if (law) {
+      lawc.resize(pl.degree + 1);
+      law_coefficients(h, pl, ttop, sub, lawc.data());
+    }
+    const std::vector<double>& bpv = law ? lawc : pl.bp;
     double* acc = (src == h->ACC[0]) ? h->ACC[1] : h->ACC[0];
     const double* uprev = nullptr;
     long long uprev_bs = 0;
@@ -108,7 +117,7 @@ int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const d
       for (int j = 0; j <= px::CM_MAXT; ++j) {
         const int term = k + j;
         a.be[j] = (j <= M && term <= K && (j > 0 || first)) ? pl.be[term] : 0.0;
-        a.bp[j] = (pacc && j <= M && term <= K && (j > 0 || first)) ? pl.bp[term] : 0.0;
+        a.bp[j] = (pacc && j <= M && term <= K && (j > 0 || first)) ? bpv[term] : 0.0;
       }
       int rc;
       const int km = kbegin(h, PX_KCLASS_CHEB, s);
@@ -161,18 +170,39 @@ bool cheb_has_ssum(const Handle* h) { return h->dim == 2 && (h->d.nx % 2) == 0; 
 
 // result <- exp(span·M)·src (+ addend);  pacc += span·φ₁(span·M)·src  (if pacc);
 // ssum += result (if ssum; the 2D passes only, cheb_has_ssum)
+void law_coefficients(const Handle* h, const Plan& pl, double ttop, int sub, double* out) {
+  // ∫₀^τ θ(t − s)·e^{sM} ds at t = ttop − sub·τ: α·τφ₁ + A·Gc + B·Gs with
+  // A = β sin ωt + γ cos ωt, B = −β cos ωt + γ sin ωt (oracle.config_mode.law_substep_coef)
+  const double a = h->law[0], b = h->law[1], c = h->law[2], w = h->law[3];
+  const int K = pl.degree;
+  if (w == 0.0 || pl.gc.empty()) {
+    for (int k = 0; k <= K; ++k) out[k] = (w == 0.0 ? a + c : a) * pl.bp[k];
+    return;
+  }
+  const double t = ttop - sub * (pl.span / pl.substeps);
+  const double A = b * std::sin(w * t) + c * std::cos(w * t);
+  const double Bc = -b * std::cos(w * t) + c * std::sin(w * t);
+  for (int k = 0; k <= K; ++k) out[k] = a * pl.bp[k] + A * pl.gc[k] + Bc * pl.gs[k];
+}
+
 int cheb_action(Handle* h, const Plan& pl, const px::Stencil5& st, const double* src, long long src_bs,
                 const double* addend, long long add_bs, double* pacc, double** result, cudaStream_t s,
-                double* ssum) {
+                double* ssum, double ttop) {
   if (!pl.set || pl.krylov) return fail(h, PX_ERR_STATE, "Chebyshev plan not set");
   if (ssum && (pacc || !cheb_has_ssum(h))) return fail(h, PX_ERR_STATE, "carry-input sum: 2D passes without φ₁");
+  if (pacc && h->has_law && h->law[3] != 0.0 && pl.gc.empty())
+    return fail(h, PX_ERR_STATE, "time law: the plan lacks its law series (px_set_cheb_plan_law)");
   if (h->dim == 2 && (h->d.nx % 2) == 0)
-    return cheb_action_march(h, pl, st, src, src_bs, addend, add_bs, pacc, ssum, result, s);
+    return cheb_action_march(h, pl, st, src, src_bs, addend, add_bs, pacc, ssum, result, s, ttop);
+  const bool law = pacc && h->has_law;
+  std::vector<double> lawc(pl.degree + 1);
   const size_t n = h->n;
   const int B = h->B;
   const dim3 grid = grid1(n, B);
   const long long nb = (long long)n;
   for (int sub = 0; sub < pl.substeps; ++sub) {
+    if (law) law_coefficients(h, pl, ttop, sub, lawc.data());
+    const double* bpv = law ? lawc.data() : pl.bp.data();
     double* acc = (src == h->ACC[0]) ? h->ACC[1] : h->ACC[0];
     px::ChebFirstArgs fa{};
     fa.u0 = src; fa.u0_bstride = src_bs;
@@ -184,7 +214,7 @@ int cheb_action(Handle* h, const Plan& pl, const px::Stencil5& st, const double*
     fa.st = st;
     fa.c0 = pl.center; fa.d = pl.scale;
     fa.b0 = pl.be[0]; fa.b1 = pl.be[1];
-    fa.p0 = pacc ? pl.bp[0] : 0.0; fa.p1 = pacc ? pl.bp[1] : 0.0;
+    fa.p0 = pacc ? bpv[0] : 0.0; fa.p1 = pacc ? bpv[1] : 0.0;
     fa.nx = h->d.nx; fa.ny = h->d.ny;
     if (h->dim == 2) px::k_cheb_first<2><<<grid, 256, 0, s>>>(fa);
     else px::k_cheb_first<1><<<grid, 256, 0, s>>>(fa);
@@ -203,7 +233,7 @@ int cheb_action(Handle* h, const Plan& pl, const px::Stencil5& st, const double*
       ta.pacc = pacc;
       ta.st = st;
       ta.c0 = pl.center; ta.two_over_d = 2.0 / pl.scale; ta.sigma = (double)pl.sigma;
-      ta.bk = pl.be[k]; ta.pk = pacc ? pl.bp[k] : 0.0;
+      ta.bk = pl.be[k]; ta.pk = pacc ? bpv[k] : 0.0;
       ta.nx = h->d.nx; ta.ny = h->d.ny;
       if (h->dim == 2) px::k_cheb_term<2><<<grid, 256, 0, s>>>(ta);
       else px::k_cheb_term<1><<<grid, 256, 0, s>>>(ta);

@@ -22,6 +22,7 @@ struct Hybrid {
   std::vector<int> offs;
   int* d_offs = nullptr;
   int* flags = nullptr;
+  double* theta = nullptr;  // θ(k·h/2), k = 0 … 2S
   double *u0 = nullptr, *f = nullptr, *target = nullptr, *qT = nullptr;
   double *traj = nullptr, *J = nullptr, *aend = nullptr, *zl = nullptr, *ubar = nullptr;
   double *qdag0 = nullptr, *grad = nullptr, *bpart = nullptr, *bounds = nullptr;
@@ -126,6 +127,16 @@ int px_hybrid_create(const px_hybrid_desc* d, void** out) {
   if (rc == PX_OK) rc = dalloc_t(hb, &hy->d_plans, (size_t)P);
   if (rc == PX_OK && cudaMemcpy(hy->d_offs, d->offsets, sizeof(int) * (P + 1), cudaMemcpyHostToDevice) != cudaSuccess)
     rc = fail(hb, PX_ERR_CUDA, "hybrid: offsets upload");
+  if (rc == PX_OK) rc = dalloc_t(hb, &hy->theta, 2 * S + 1);
+  if (rc == PX_OK) {
+    std::vector<double> th(2 * S + 1);
+    for (size_t k = 0; k <= 2 * S; ++k) {
+      const double t = (double)k * (0.5 * hy->h);
+      th[k] = hy->law[0] + hy->law[1] * std::sin(hy->law[3] * t) + hy->law[2] * std::cos(hy->law[3] * t);
+    }
+    if (cudaMemcpy(hy->theta, th.data(), sizeof(double) * th.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+      rc = fail(hb, PX_ERR_CUDA, "hybrid: law table upload");
+  }
   if (rc == PX_OK && (cudaStreamCreateWithFlags(&hy->side, cudaStreamNonBlocking) != cudaSuccess ||
                       cudaEventCreateWithFlags(&hy->ev_fork, cudaEventDisableTiming) != cudaSuccess))
     rc = fail(hb, PX_ERR_CUDA, "hybrid: stream/event creation");
@@ -187,6 +198,7 @@ int px_hybrid_direct(void* p, int overlap, void* stream) {
   a.traj = hy->traj; a.J = hy->J; a.flags = hy->flags; a.offsets = hy->d_offs;
   a.aend = hy->aend; a.zl = hy->zl;
   a.la = hy->law[0]; a.lb = hy->law[1]; a.lc = hy->law[2]; a.lw = hy->law[3];
+  a.theta = hy->theta;
   a.D = hy->D; a.hx = hy->hx; a.h = hy->h; a.T = hy->T;
   a.nx = hy->nx; a.B = hy->B; a.P = hy->P; a.S = hy->S;
   // overlap only when every lane CTA and every direct CTA can be resident at once even if each

@@ -23,9 +23,8 @@
 
 namespace px {
 
-__device__ __forceinline__ double hyb_law(const HybArgs& a, double t) {
-  return a.la + a.lb * sin(a.lw * t) + a.lc * cos(a.lw * t);
-}
+// θ at half-step k (t = k·h/2): the host tabulates the law once per handle
+__device__ __forceinline__ double hyb_theta(const HybArgs& a, int k) { return __ldg(a.theta + k); }
 
 // Exchange the run edges of y (PPT values per thread) and return the left / right neighbours
 // of the run; `par` selects the buffer (double buffering: one barrier per call).
@@ -89,8 +88,7 @@ __global__ void __launch_bounds__(HYB_NT) k_hyb_direct(HybArgs a) {
   int p = 0;
   int next = a.offsets[1];
   for (int s = 0; s < a.S; ++s) {
-    const double t0 = s * a.h;
-    const double th1 = hyb_law(a, t0), th2 = hyb_law(a, t0 + 0.5 * a.h), th4 = hyb_law(a, t0 + a.h);
+    const double th1 = hyb_theta(a, 2 * s), th2 = hyb_theta(a, 2 * s + 1), th4 = hyb_theta(a, 2 * s + 2);
     double k[PPT], Y[PPT], acc[PPT];
     rhs(u, th1, k);
 #pragma unroll
@@ -183,8 +181,7 @@ __global__ void __launch_bounds__(HYB_NT) k_hyb_lanes(HybArgs a) {
 #pragma unroll
     for (int q = 0; q < PPT; ++q) tgb[q] = act ? tg[(size_t)(top - 1) * tstride + i0 + q] : 0.0;
     __syncthreads();
-    const double ta = top * h;
-    const double tha = hyb_law(a, ta), thm = hyb_law(a, ta - hh), thb = hyb_law(a, ta - h);
+    const double tha = hyb_theta(a, 2 * top), thm = hyb_theta(a, 2 * top - 1), thb = hyb_theta(a, 2 * top - 2);
     double sa[PPT], sm[PPT], sb[PPT];
 #pragma unroll
     for (int q = 0; q < PPT; ++q) {

@@ -18,6 +18,7 @@ struct HybArgs {
   double* aend;          // (B·P) × n adjoint slice solutions at the slice starts
   double* zl;            // (B·P) × n their θ-weighted integrals
   double la, lb, lc, lw; // time law
+  const double* theta;   // θ(k·h/2), k = 0 … 2S (host-evaluated once per handle: no trig per step)
   double D, hx, h, T;
   int nx, B, P, S;
   int wait;              // lanes: wait for the direct's progress flags

@@ -50,6 +50,7 @@ struct Plan {
   int substeps = 0, degree = 0, sigma = -1;
   double center = 0.0, scale = 1.0;
   std::vector<double> be, bp;
+  std::vector<double> gc, gs;  // time-law series (px_set_cheb_plan_law): ∫₀^τ (cos ωs, sin ωs)·e^{sM} ds
   double* dcoef = nullptr;  // device copy: be[0..K], bp[0..K]
 };
 
@@ -76,6 +77,11 @@ struct Handle {
   // closed-form adjoint ∫ (2D circulant operator): Σ_p z_p = (Aᵀ)⁻¹(Σ_p y_n,p − Pl·n·b) + …
   bool z_closed = false;
   int adjoint_mode = PX_ADJOINT_ABSORBED;  // Burgers: PX_ADJOINT_FROZEN_SPAN = reference solve_hybrid
+  // forcing time law (px_set_time_law, linear testbed): f·θ(t), θ = law[0] + law[1] sin(law[3] t) +
+  // law[2] cos(law[3] t); fctl holds f (B × n), the adjoint's ∫ becomes ∫θ·q† dt
+  bool has_law = false;
+  double law[4] = {1.0, 0.0, 0.0, 0.0};
+  double* fctl = nullptr;
   cufftHandle fft = 0;
   double2* fbuf = nullptr;  // B × n complex
   double* bsum = nullptr;   // B: Σ_i b[b][i]
@@ -193,9 +199,13 @@ int lane_sum_plus(Handle* h, double* out, const double* lanes, const double* c, 
                   cudaStream_t s);
 
 // ---- cheb.cu / krylov.cu --------------------------------------------------------------
+// ttop (time law only): the physical time at which the action's reflected-time span starts;
+// pacc then accumulates ∫₀^span θ(ttop − σ)·e^{σM}·src dσ instead of span·φ₁(span·M)·src
 int cheb_action(Handle* h, const Plan& pl, const px::Stencil5& st, const double* src, long long src_bs,
                 const double* addend, long long add_bs, double* pacc, double** result, cudaStream_t s,
-                double* ssum = nullptr);
+                double* ssum = nullptr, double ttop = 0.0);
+// the law series of substep `sub` of plan `pl` started at ttop (K+1 values)
+void law_coefficients(const Handle* h, const Plan& pl, double ttop, int sub, double* out);
 bool cheb_has_ssum(const Handle* h);
 bool use_scan1d(const Handle* h);
 int scan1d(Handle* h, bool adjoint, const double* lanes, double* out, double* pacc, int long_slot, cudaStream_t s);
@@ -207,7 +217,7 @@ void krylov_free(px::KrylovWork& kw);
 // ---- sweeps.cu ------------------------------------------------------------------------
 int exp_action(Handle* h, int slot, const px::Stencil5& st, const double* src, long long src_bs,
                const double* addend, long long add_bs, double* pacc, double** result, cudaStream_t s,
-               double* ssum = nullptr);
+               double* ssum = nullptr, double ttop = 0.0);
 int direct_linear(Handle* h, cudaStream_t s);
 int adjoint_linear(Handle* h, cudaStream_t s);
 int finish_direct_impl(Handle* h, cudaStream_t s);

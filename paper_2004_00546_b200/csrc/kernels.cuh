@@ -42,7 +42,9 @@ __global__ void k_apply_plus_control(double* out, const double* src, long long s
   if (i >= n) return;
   const int y = (int)(i / nx), x = (int)(i - (size_t)y * nx);
   double r = stencil_at<DIM>(src + b * src_bstride, st, x, y, nx, ny);
-  if (ctrl) {
+  if (ctrl && K < 0) {  // field control (PX_FLAG_FIELD_CONTROL): f is given point by point
+    r += ctrl[(size_t)b * n + i];
+  } else if (ctrl) {
     const double* c = ctrl + (size_t)b * K;
     double f = 0.0;
     for (int k = 0; k < K; ++k) f += c[k] * (tx[(size_t)ix[k] * nx + x] * ty[(size_t)iy[k] * ny + y]);

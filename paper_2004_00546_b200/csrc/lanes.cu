@@ -2,6 +2,7 @@
 // per-worker rk45_integrate calls of the reference's direct / adjoint workers
 // (paraexp.py:193-198, :268-274) with one batched sweep over B members × Pl slices.
 #include <algorithm>
+#include <cmath>
 
 #include "internal.h"
 #include "rk4.cuh"
@@ -41,8 +42,10 @@ int launch_march2(Handle* h, const px::MarchArgs& a, unsigned blocks, bool zlane
   return PX_OK;
 }
 
-// One RK4 step per launch (small sweeps, PX_VAR_MARCH2 = 0, odd remainders of the two-column march).
+// One RK4 step per launch (small sweeps, PX_VAR_MARCH2 = 0, odd remainders of the two-column march,
+// time-law sweeps).
 int launch_march1(Handle* h, px::MarchArgs a, int L, bool zlanes, bool remainder, cudaStream_t s) {
+  const bool law = h->has_law;
   const int nx = a.nx, ny = a.ny;
   if (nx <= px::MARCH_MAX_CW) {
     a.strip_w = nx; a.halo = 0; a.nstrips = 1;
@@ -62,10 +65,16 @@ int launch_march1(Handle* h, px::MarchArgs a, int L, bool zlanes, bool remainder
   a.band_rows = br;
   a.nbands = (ny + br - 1) / br;
   const unsigned blocks = (unsigned)((size_t)L * a.nstrips * a.nbands);
-  const size_t smem = px::march_smem(zlanes);
-  if (zlanes) {
+  const size_t smem = px::march_smem(zlanes, law);
+  if (zlanes && law) {
+    PX_TRY(smem_attr(h, (const void*)px::k_rk4_march<true, true>, smem));
+    px::k_rk4_march<true, true><<<blocks, px::MARCH_NT, smem, s>>>(a);
+  } else if (zlanes) {
     PX_TRY(smem_attr(h, (const void*)px::k_rk4_march<true>, smem));
     px::k_rk4_march<true><<<blocks, px::MARCH_NT, smem, s>>>(a);
+  } else if (law) {
+    PX_TRY(smem_attr(h, (const void*)px::k_rk4_march<false, true>, smem));
+    px::k_rk4_march<false, true><<<blocks, px::MARCH_NT, smem, s>>>(a);
   } else {
     PX_TRY(smem_attr(h, (const void*)px::k_rk4_march<false>, smem));
     px::k_rk4_march<false><<<blocks, px::MARCH_NT, smem, s>>>(a);
@@ -92,8 +101,29 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
   PX_TRY(sax(h->Wk[0], g, g, 0.25 * hs, 1.0));
   PX_TRY(sax(h->Wk[1], g, h->Wk[0], hs / 3.0, 1.0));
   PX_TRY(sax(h->bsrc, g, h->Wk[1], 0.5 * hs, hs));
-  if (adjoint)
+  const bool law = h->has_law;
+  if (adjoint && !law)
     PX_TRY(axpby(h, h->cz, (long long)h->n, h->Wk[1], (long long)h->n, 0.5 * hs * hs, nullptr, 0, 0.0, s));
+  if (adjoint && law) {
+    // the source part of the θ-weighted lane integrals summed over every local lane and step:
+    // Σ h/6[2θm(Y2 + Y3) + θb·Y4]_source = S0·g + S1·Mg + S2·M²g
+    double S0 = 0.0, S1 = 0.0, S2 = 0.0;
+    const double delta = h->d.T / h->d.P;
+    auto th = [&](double t) { return h->law[0] + h->law[1] * std::sin(h->law[3] * t) + h->law[2] * std::cos(h->law[3] * t); };
+    for (int p = h->d.p_begin; p < h->d.p_end; ++p)
+      for (int k = 0; k < h->d.nsteps; ++k) {
+        const double t = (p + 1) * delta - k * hs;
+        const double tm = th(t - 0.5 * hs), tb = th(t - hs);
+        S0 += hs * hs * (2.0 * tm + tb) / 6.0;
+        S1 += hs * hs * hs * (tm + tb) / 12.0;
+        S2 += hs * hs * hs * hs * tb / 24.0;
+      }
+    const long long nb = (long long)h->n;
+    PX_TRY(sax(h->Wk[2], g, g, 1.0, 1.0));                                   // g + Mg
+    PX_TRY(axpby(h, h->Wk[3], nb, g, nb, S1 - S2, h->Wk[2], nb, S2, s));     // S1·g + S2·Mg
+    PX_TRY(sax(h->Wk[2], g, h->Wk[3], 1.0, 1.0));                            // g + M(S1·g + S2·Mg)
+    PX_TRY(axpby(h, h->cz, nb, h->Wk[2], nb, 1.0, g, nb, S0 - 1.0, s));      // + (S0 − 1)·g
+  }
 
   const int nsteps = h->d.nsteps;
   double* cur = nullptr;
@@ -104,28 +134,36 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
     px::Lane1DArgs a{};
     a.y_out = h->Y0; a.b = h->bsrc; a.z = h->Z; a.st = st; a.h = hs;
     a.n = (int)h->n; a.lanes_per_b = h->Pl; a.nsteps = nsteps;
+    a.f = h->fctl; a.delta = h->d.T / h->d.P; a.p_begin = h->d.p_begin;
+    for (int k = 0; k < 4; ++k) a.law[k] = h->law[k];
     const int ppt = h->n <= 1024 ? 1 : (h->n <= 2048 ? 2 : 4);
     const int nt = (int)((h->n + ppt - 1) / ppt);
     const bool full = h->n % ppt == 0;
-#define PX_L1(PP)                                                                   \
-  do {                                                                              \
-    if (full) {                                                                     \
-      if (adjoint) px::k_rk4_lane1d<PP, true, true><<<h->L, nt, 0, s>>>(a);         \
-      else px::k_rk4_lane1d<PP, false, true><<<h->L, nt, 0, s>>>(a);                \
-    } else {                                                                        \
-      if (adjoint) px::k_rk4_lane1d<PP, true><<<h->L, nt, 0, s>>>(a);               \
-      else px::k_rk4_lane1d<PP, false><<<h->L, nt, 0, s>>>(a);                      \
-    }                                                                               \
+#define PX_L1W(PP, LW)                                                                  \
+  do {                                                                                  \
+    if (full) {                                                                         \
+      if (adjoint) px::k_rk4_lane1d<PP, true, true, LW><<<h->L, nt, 0, s>>>(a);         \
+      else px::k_rk4_lane1d<PP, false, true, LW><<<h->L, nt, 0, s>>>(a);                \
+    } else {                                                                            \
+      if (adjoint) px::k_rk4_lane1d<PP, true, false, LW><<<h->L, nt, 0, s>>>(a);        \
+      else px::k_rk4_lane1d<PP, false, false, LW><<<h->L, nt, 0, s>>>(a);               \
+    }                                                                                   \
+  } while (0)
+#define PX_L1(PP)                  \
+  do {                             \
+    if (law) PX_L1W(PP, true);     \
+    else PX_L1W(PP, false);        \
   } while (0)
     if (ppt == 1) PX_L1(1);
     else if (ppt == 2) PX_L1(2);
     else PX_L1(4);
 #undef PX_L1
+#undef PX_L1W
     PX_CHECK_LAUNCH(h);
     cur = h->Y0;
     launched_steps = nsteps;
     h->z_valid = adjoint;
-  } else if (nsteps == 1) {
+  } else if (nsteps == 1 && !(law && !adjoint)) {
     px::k_broadcast_lanes<<<dim3((unsigned)std::min<size_t>((h->n + 255) / 256, 1024), h->L), 256, 0, s>>>(
         h->Y0, h->bsrc, h->Pl, h->n);
     PX_CHECK_LAUNCH(h);
@@ -138,6 +176,8 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
     px::MarchArgs a{};
     a.b = h->bsrc; a.z = h->Z; a.st = st; a.h = hs;
     a.nx = nx; a.ny = ny; a.lanes = h->L; a.lanes_per_b = h->Pl;
+    a.f = h->fctl; a.delta = h->d.T / h->d.P; a.p_begin = h->d.p_begin;
+    for (int k = 0; k < 4; ++k) a.law[k] = h->law[k];
     {
       const double ks[4] = {0.25 * hs, hs / 3.0, 0.5 * hs, hs};
       const double cf[5] = {st.cc, st.ce, st.cw, st.cs, st.cn};
@@ -148,7 +188,21 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
     // 8-stage pipeline fill (16 rows per band) only pays off when each launch covers ≥ 2^28
     // lane-points
     const int m2 = h->var.march2;
-    if (m2 && nsteps >= 3 && (m2 == 2 || (double)h->L * (double)h->n >= 268435456.0)) {
+    if (law && !adjoint) {
+      // time-law direct lanes: θ·f enters at every stage, so the lanes start from zero (no
+      // y₁ = b shortcut) and run one step per launch
+      PX_CUDA(h, cudaMemsetAsync(h->Y0, 0, sizeof(double) * h->L * h->n, s));
+      cur = h->Y0;
+      for (int st_i = 0; st_i < nsteps; ++st_i) {
+        double* out = (cur == h->Y0) ? h->Y1 : h->Y0;
+        a.y_in = cur;
+        a.y_out = out;
+        a.step = st_i;
+        PX_TRY(launch_march1(h, a, h->L, false, false, s));
+        PX_CHECK_LAUNCH(h);
+        cur = out;
+      }
+    } else if (m2 && !law && nsteps >= 3 && (m2 == 2 || (double)h->L * (double)h->n >= 268435456.0)) {
       constexpr int cw2 = 2 * 128;  // computed width of the two-column kernel
       // three columns per thread (k_rk4_marchc): direct lanes, strip mode
       const bool cols3 = !zlanes && h->var.march_cols == 3 && nx > 3 * 64;
@@ -198,12 +252,13 @@ int rk4_sweep(Handle* h, bool adjoint, const double** final_out, cudaStream_t s)
         a.y_in = cur;
         a.y_out = out;
         a.z_zero = (st_i == 1);
+        a.step = st_i;
         PX_TRY(launch_march1(h, a, h->L, zlanes, false, s));
         PX_CHECK_LAUNCH(h);
         cur = out;
       }
     }
-    launched_steps = nsteps - 1;
+    launched_steps = (law && !adjoint) ? nsteps : nsteps - 1;
     h->z_valid = zlanes;
   }
   const double bytes_per_point = (adjoint && !h->z_closed) ? 40.0 : 24.0;  // y, b, y' (+ z in/out)

@@ -17,6 +17,8 @@ int axpby(Handle* h, double* out, long long obs, const double* x, long long xbs,
 
 // grad[b][k] = alpha·⟨φ_k, F[b]⟩ + beta·grad[b][k] (separable basis: rows then columns)
 int project(Handle* h, double* grad, const double* F, long long Fbs, double alpha, double beta, cudaStream_t s) {
+  if (h->d.flags & PX_FLAG_FIELD_CONTROL)  // field control: the gradient is the field itself
+    return axpby(h, grad, (long long)h->n, F, Fbs, alpha, grad, (long long)h->n, beta, s);
   const int rx = h->rows_x;
   const dim3 g(h->d.ny, h->B);
   if (rx <= 8) px::k_project_rows<8><<<g, 256, 0, s>>>(h->R, F, Fbs, h->tx, rx, h->d.nx, h->d.ny);
@@ -35,11 +37,12 @@ int apply_plus_control(Handle* h, double* out, const double* x, long long xbs, c
                        bool with_control, cudaStream_t s) {
   const dim3 grid = grid1(h->n, h->B);
   const double* c = with_control ? h->ctrl : nullptr;
+  const int K = (h->d.flags & PX_FLAG_FIELD_CONTROL) ? -1 : h->K;
   if (h->dim == 2)
-    px::k_apply_plus_control<2><<<grid, 256, 0, s>>>(out, x, xbs, st, c, h->tx, h->ty, h->ix, h->iy, h->K, h->d.nx,
+    px::k_apply_plus_control<2><<<grid, 256, 0, s>>>(out, x, xbs, st, c, h->tx, h->ty, h->ix, h->iy, K, h->d.nx,
                                                      h->d.ny);
   else
-    px::k_apply_plus_control<1><<<grid, 256, 0, s>>>(out, x, xbs, st, c, h->tx, h->ty, h->ix, h->iy, h->K, h->d.nx,
+    px::k_apply_plus_control<1><<<grid, 256, 0, s>>>(out, x, xbs, st, c, h->tx, h->ty, h->ix, h->iy, K, h->d.nx,
                                                      h->d.ny);
   PX_CHECK_LAUNCH(h);
   return PX_OK;

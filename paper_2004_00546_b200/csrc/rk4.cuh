@@ -57,7 +57,47 @@ struct MarchArgs {
   int nstrips, band_rows, nbands;
   // k_rk4_march2: stage-scaled stencil k·(cc, ce, cw, cs, cn) for k = h/4, h/3, h/2, h
   double kc[4][5];
+  // time law (k_rk4_march<·, true>): forcing θ(t)·f with θ = law[0] + law[1] sin(law[3] t) +
+  // law[2] cos(law[3] t); lane p of the rank starts at (p_begin + p)·delta; `step` is the
+  // launch's step within the lanes
+  const double* f;     // B × n control field (direct lanes)
+  double law[4];
+  double delta;
+  int p_begin, step;
 };
+
+__device__ __forceinline__ double law_at(const double* law, double t) {
+  return law[0] + law[1] * sin(law[3] * t) + law[2] * cos(law[3] * t);
+}
+
+// Per-step scalars of the time law. Direct lanes (forcing θ·f at the stage times of the step
+// from t): the Horner stages take +α_s·f and the update +γ·f,
+//   α1 = hθ1/4, α2 = h(θ1+θ2)/6, α3 = h(θ1+2θ2)/6, γ = h(θ1+4θ2+θ4)/6
+// (θ1 = θ(t), θ2 = θ(t+h/2), θ4 = θ(t+h)) — exactly classical RK4 with a time-dependent source.
+// Adjoint lanes (reflected time from t down): the θ-weighted RK4-consistent ∫ of the state,
+// h/6[θa·Y1 + 2θm(Y2 + Y3) + θb·Y4], is β0·y + β2·w2 + β3·w3 in the Horner stages
+// (Y2 = 2w1 − y, Y3 = 3w2 − 2w1, Y4 = y + 6w3 − 6w2 without the source, whose part is summed
+// once per sweep on the host), β0 = h(θa − 2θm + θb)/6, β2 = h(θm − θb), β3 = h·θb.
+struct LawStep {
+  double c0, c1, c2, c3;  // direct: α1, α2, α3, γ; adjoint: β0, β2, β3, unused
+};
+__device__ __forceinline__ LawStep law_step(const double* law, bool adjoint, double t, double h) {
+  LawStep r;
+  if (!adjoint) {
+    const double t1 = law_at(law, t), t2 = law_at(law, t + 0.5 * h), t4 = law_at(law, t + h);
+    r.c0 = h * t1 * 0.25;
+    r.c1 = h * (t1 + t2) / 6.0;
+    r.c2 = h * (t1 + 2.0 * t2) / 6.0;
+    r.c3 = h * (t1 + 4.0 * t2 + t4) / 6.0;
+  } else {
+    const double ta = law_at(law, t), tm = law_at(law, t - 0.5 * h), tb = law_at(law, t - h);
+    r.c0 = h * (ta - 2.0 * tm + tb) / 6.0;
+    r.c1 = h * (tm - tb);
+    r.c2 = h * tb;
+    r.c3 = 0.0;
+  }
+  return r;
+}
 
 // Row ring: each thread streams its own column pair of the y, b (and z) rows
 // MARCH_DEPTH rows ahead with cp.async (LDGSTS) into shared memory, so ~6 rows
@@ -69,9 +109,11 @@ struct MarchDepth {
   static constexpr int value = ADJ ? 4 : 6;
 };
 
-template <bool ADJ>
+// LAW: time-law forcing (direct: a third ring stream f at row r−1, kept four rows deep in
+// registers; adjoint: the θ-weighted ∫ instead of z += h·w3)
+template <bool ADJ, bool LAW = false>
 __global__ void __launch_bounds__(MARCH_NT, 2) k_rk4_march(MarchArgs a) {
-  constexpr int NQ = ADJ ? 3 : 2;  // streamed arrays: y, b (, z)
+  constexpr int NQ = (ADJ || LAW) ? 3 : 2;  // streamed arrays: y, b (, z | f)
   constexpr int MARCH_DEPTH = MarchDepth<ADJ>::value;
   // publish area: [parity][quantity: y, w1, w2, w3][pair] split in even / odd columns
   __shared__ double pubE[2][4][MARCH_NT];
@@ -108,6 +150,13 @@ __global__ void __launch_bounds__(MARCH_NT, 2) k_rk4_march(MarchArgs a) {
   double* __restrict__ yout = a.y_out + (size_t)lane * n;
   double* __restrict__ zl = ADJ ? a.z + (size_t)lane * n : nullptr;
   const bool zread = ADJ && !a.z_zero;
+  const double* __restrict__ fsrc = (LAW && !ADJ) ? a.f + member * n : nullptr;
+  LawStep ls{0.0, 0.0, 0.0, 0.0};
+  if (LAW) {
+    const int p = a.p_begin + lane % a.lanes_per_b;
+    ls = ADJ ? law_step(a.law, true, (p + 1) * a.delta - a.step * h, h)
+             : law_step(a.law, false, p * a.delta + a.step * h, h);
+  }
 
   // incremental periodic row counters (no per-row integer division)
   auto wrapr = [&](int row) -> int {
@@ -117,7 +166,7 @@ __global__ void __launch_bounds__(MARCH_NT, 2) k_rk4_march(MarchArgs a) {
   const int r0 = j0 - 4;
   // issue stream: y row r0+k and b/z rows r0+k-4 for the k-th issued iteration
   int iss_k = 0, iss_slot = 0;
-  int ry = wrapr(r0), rb = wrapr(r0 - 4);
+  int ry = wrapr(r0), rb = wrapr(r0 - 4), rf = wrapr(r0 - 1);
   const size_t coloff = (size_t)gx;
   auto issue = [&]() {
     if (iss_k < iters) {
@@ -125,12 +174,14 @@ __global__ void __launch_bounds__(MARCH_NT, 2) k_rk4_march(MarchArgs a) {
       cp_async16(slot + t, ysrc + (size_t)ry * nx + coloff);
       cp_async16(slot + MARCH_NT + t, bsrc + (size_t)rb * nx + coloff);
       if (zread) cp_async16(slot + 2 * MARCH_NT + t, zl + (size_t)rb * nx + coloff);
+      if (LAW && !ADJ) cp_async16(slot + 2 * MARCH_NT + t, fsrc + (size_t)rf * nx + coloff);
     }
     cp_async_commit();
     ++iss_k;
     iss_slot = (iss_slot + 1 == MARCH_DEPTH) ? 0 : iss_slot + 1;
     ry = (ry + 1 == ny) ? 0 : ry + 1;
     rb = (rb + 1 == ny) ? 0 : rb + 1;
+    rf = (rf + 1 == ny) ? 0 : rf + 1;
   };
 #pragma unroll
   for (int k = 0; k < MARCH_DEPTH; ++k) issue();
@@ -142,8 +193,11 @@ __global__ void __launch_bounds__(MARCH_NT, 2) k_rk4_march(MarchArgs a) {
   // two rows in wq[(k-2) mod 2], wq[(k-1) mod 2]. Unrolling by 6 turns the queue
   // rotation into register renaming (no moves).
   double2 yq[6], w1q[2], w2q[2], w3q[2];
+  double2 fq[LAW && !ADJ ? 6 : 1];  // f rows r-1 .. r-4 (ring by phase, like yq)
 #pragma unroll
   for (int k = 0; k < 6; ++k) yq[k] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int k = 0; k < (LAW && !ADJ ? 6 : 1); ++k) fq[k] = make_double2(0.0, 0.0);
 #pragma unroll
   for (int k = 0; k < 2; ++k) w1q[k] = w2q[k] = w3q[k] = make_double2(0.0, 0.0);
 
@@ -175,8 +229,14 @@ __global__ void __launch_bounds__(MARCH_NT, 2) k_rk4_march(MarchArgs a) {
       const double2 yr = slot[t];
       const double2 brow = slot[MARCH_NT + t];  // row r-4
       const double2 zrow = zread ? slot[2 * MARCH_NT + t] : make_double2(0.0, 0.0);
+      if constexpr (LAW && !ADJ) fq[k] = slot[2 * MARCH_NT + t];  // f row r-1
       issue();  // refills the slot just consumed (its values are in registers)
       yq[k] = yr;
+      // f at the stage rows r-1 .. r-4 (time law; zero otherwise)
+      auto frow = [&](int back) -> double2 {
+        if constexpr (LAW && !ADJ) return fq[(k + 6 - back) % 6];
+        else return make_double2(0.0, 0.0);
+      };
       // rows r-4 .. r-1 (yr = row r)
       const double2 y0 = yq[(k + 2) % 6], y1 = yq[(k + 3) % 6], y2 = yq[(k + 4) % 6], y3 = yq[(k + 5) % 6];
       const int po = k & 1, pp = (k + 1) & 1;  // w?q[po]: row of iteration i-2, [pp]: i-1
@@ -186,16 +246,31 @@ __global__ void __launch_bounds__(MARCH_NT, 2) k_rk4_march(MarchArgs a) {
         const double l = pubO[pin][0][tl], rr = pubE[pin][0][tr];
         const double2 m = apply(y3, y2, yr, l, rr);
         nw1 = make_double2(y3.x + c1 * m.x, y3.y + c1 * m.y);
+        if constexpr (LAW && !ADJ) {
+          const double2 fv = frow(0);
+          nw1.x = fma(ls.c0, fv.x, nw1.x);
+          nw1.y = fma(ls.c0, fv.y, nw1.y);
+        }
       }
       if (i >= 4) {  // stage 2 at row r-2: w2 = y + (h/3)·M·w1  (w1 rows r-3, r-2, r-1)
         const double l = pubO[pin][1][tl], rr = pubE[pin][1][tr];
         const double2 m = apply(w1q[pp], w1q[po], nw1, l, rr);
         nw2 = make_double2(y2.x + c2 * m.x, y2.y + c2 * m.y);
+        if constexpr (LAW && !ADJ) {
+          const double2 fv = frow(1);
+          nw2.x = fma(ls.c1, fv.x, nw2.x);
+          nw2.y = fma(ls.c1, fv.y, nw2.y);
+        }
       }
       if (i >= 6) {  // stage 3 at row r-3: w3 = y + (h/2)·M·w2  (w2 rows r-4, r-3, r-2)
         const double l = pubO[pin][2][tl], rr = pubE[pin][2][tr];
         const double2 m = apply(w2q[pp], w2q[po], nw2, l, rr);
         nw3 = make_double2(y1.x + c3 * m.x, y1.y + c3 * m.y);
+        if constexpr (LAW && !ADJ) {
+          const double2 fv = frow(2);
+          nw3.x = fma(ls.c2, fv.x, nw3.x);
+          nw3.y = fma(ls.c2, fv.y, nw3.y);
+        }
       }
       if (i >= 8) {  // stage 4 at row r-4: y⁺ = y + h·M·w3 + b  (w3 rows r-5, r-4, r-3)
         const double l = pubO[pin][3][tl], rr = pubE[pin][3][tr];
@@ -206,11 +281,22 @@ __global__ void __launch_bounds__(MARCH_NT, 2) k_rk4_march(MarchArgs a) {
           double2 yn;
           yn.x = y0.x + h * m.x + brow.x;
           yn.y = y0.y + h * m.y + brow.y;
+          if constexpr (LAW && !ADJ) {
+            const double2 fv = frow(3);
+            yn.x = fma(ls.c3, fv.x, yn.x);
+            yn.y = fma(ls.c3, fv.y, yn.y);
+          }
           __stcs(reinterpret_cast<double2*>(yout + off), yn);
           if (ADJ) {
             double2 zn;
-            zn.x = zrow.x + h * w3c.x;
-            zn.y = zrow.y + h * w3c.y;
+            if constexpr (LAW) {  // θ-weighted ∫: β0·y + β2·w2 + β3·w3 at row r-4
+              const double2 w2c = w2q[po];
+              zn.x = fma(ls.c2, w3c.x, fma(ls.c1, w2c.x, fma(ls.c0, y0.x, zrow.x)));
+              zn.y = fma(ls.c2, w3c.y, fma(ls.c1, w2c.y, fma(ls.c0, y0.y, zrow.y)));
+            } else {
+              zn.x = zrow.x + h * w3c.x;
+              zn.y = zrow.y + h * w3c.y;
+            }
             __stcs(reinterpret_cast<double2*>(zl + off), zn);
           }
         }
@@ -231,8 +317,9 @@ __global__ void __launch_bounds__(MARCH_NT, 2) k_rk4_march(MarchArgs a) {
   cp_async_wait<0>();
 }
 
-inline size_t march_smem(bool adj) {
-  return (size_t)(adj ? MarchDepth<true>::value * 3 : MarchDepth<false>::value * 2) * MARCH_NT * sizeof(double2);
+inline size_t march_smem(bool adj, bool law = false) {
+  return (size_t)(adj ? MarchDepth<true>::value * 3 : MarchDepth<false>::value * (law ? 3 : 2)) * MARCH_NT *
+         sizeof(double2);
 }
 
 // ---------------------------------------------------------------------------
@@ -248,9 +335,14 @@ struct Lane1DArgs {
   Stencil5 st;
   double h;
   int n, lanes_per_b, nsteps;
+  // LAW (time-law forcing; see law_step): control field, law, slice width, first slice
+  const double* f;
+  double law[4];
+  double delta;
+  int p_begin;
 };
 
-template <int PPT, bool ADJ, bool FULL = false>
+template <int PPT, bool ADJ, bool FULL = false, bool LAW = false>
 __global__ void __launch_bounds__(1024) k_rk4_lane1d(Lane1DArgs a) {
   __shared__ double eL[2][1024];
   __shared__ double eR[2][1024];
@@ -268,14 +360,21 @@ __global__ void __launch_bounds__(1024) k_rk4_lane1d(Lane1DArgs a) {
   const double cs[4] = {a.h * 0.25, a.h / 3.0, a.h * 0.5, a.h};
   const double* bm = a.b + (size_t)(lane / a.lanes_per_b) * n;
   double y[PPT], b[PPT], w[PPT], z[PPT];
+  double fl[LAW && !ADJ ? PPT : 1], w2s[LAW && ADJ ? PPT : 1];
+  const int pl = a.p_begin + lane % a.lanes_per_b;
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
     y[k] = 0.0;
     z[k] = 0.0;
     b[k] = (k < cnt) ? bm[start + k] : 0.0;
+    if constexpr (LAW && !ADJ) fl[k] = (k < cnt) ? a.f[(size_t)(lane / a.lanes_per_b) * n + start + k] : 0.0;
   }
   int par = 0;
   for (int s = 0; s < a.nsteps; ++s) {
+    LawStep ls{0.0, 0.0, 0.0, 0.0};
+    if constexpr (LAW)
+      ls = ADJ ? law_step(a.law, true, (pl + 1) * a.delta - s * h, h) : law_step(a.law, false, pl * a.delta + s * h, h);
+    const double lc[4] = {ls.c0, ls.c1, ls.c2, ls.c3};
 #pragma unroll
     for (int k = 0; k < PPT; ++k) w[k] = y[k];
 #pragma unroll
@@ -308,12 +407,20 @@ __global__ void __launch_bounds__(1024) k_rk4_lane1d(Lane1DArgs a) {
       const double c = cs[stage];
       if (stage < 3) {
 #pragma unroll
-        for (int k = 0; k < PPT; ++k) w[k] = y[k] + c * m[k];
+        for (int k = 0; k < PPT; ++k) {
+          if constexpr (LAW && ADJ) {
+            if (stage == 2) w2s[k] = w[k];  // w2 (this stage reads it; w becomes w3)
+          }
+          w[k] = y[k] + c * m[k];
+          if constexpr (LAW && !ADJ) w[k] = fma(lc[stage], fl[k], w[k]);
+        }
       } else {
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
-          if (ADJ) z[k] += h * w[k];
+          if constexpr (LAW && ADJ) z[k] = fma(ls.c2, w[k], fma(ls.c1, w2s[k], fma(ls.c0, y[k], z[k])));
+          else if (ADJ) z[k] += h * w[k];
           y[k] = y[k] + h * m[k] + b[k];
+          if constexpr (LAW && !ADJ) y[k] = fma(ls.c3, fl[k], y[k]);
         }
       }
     }

@@ -11,20 +11,23 @@
 //            C <- exp(p0Δ·Aᵀ)·C (+φ₁)            (blockscan long span)
 //   outputs: u(T), J, q†(0), G = ∫q†dt, grad_k = ⟨φ_k, G⟩.
 // Everything is enqueued on the caller's stream; no host synchronisation.
+#include <cmath>
+
 #include "internal.h"
 
 namespace pxi {
 
 int exp_action(Handle* h, int slot, const px::Stencil5& st, const double* src, long long src_bs,
                const double* addend, long long add_bs, double* pacc, double** result, cudaStream_t s,
-               double* ssum) {
+               double* ssum, double ttop) {
   const Plan& pl = h->plans[slot];
   if (!pl.set) return fail(h, PX_ERR_STATE, "exp-action plan slot " + std::to_string(slot) + " not set");
   if (pl.krylov) {
     if (ssum) return fail(h, PX_ERR_STATE, "carry-input sum: Chebyshev passes only");
+    if (pacc && h->has_law) return fail(h, PX_ERR_STATE, "time law: Chebyshev exp-actions only");
     return krylov_action(h, pl, st, src, src_bs, addend, add_bs, pacc, result, s);
   }
-  return cheb_action(h, pl, st, src, src_bs, addend, add_bs, pacc, result, s, ssum);
+  return cheb_action(h, pl, st, src, src_bs, addend, add_bs, pacc, result, s, ssum, ttop);
 }
 
 namespace {
@@ -57,8 +60,12 @@ bool use_blocks(const Handle* h) { return h->lb > 1 && h->dim == 2 && !(h->d.fla
 // the registers for seven-term passes. Krylov and 1D keep the per-carry accumulator.
 bool use_ssum(const Handle* h) {
   const Plan& pl = h->plans[PX_PLAN_SLICE];
-  return pl.set && !pl.krylov && cheb_has_ssum(h);
+  return pl.set && !pl.krylov && cheb_has_ssum(h) && !h->has_law;  // a time law weighs each carry differently
 }
+
+// start time (physical) of the reflected-time span that propagates a carry through local
+// slices q0 … q1−1 down to slice q0's lower edge, i.e. the upper edge of slice q1 − 1
+double top_time(const Handle* h, int q1) { return (h->d.p_begin + q1) * (h->d.T / h->d.P); }
 
 // Block-scan of the direct carry inside one handle: block g scans its lanes from a zero
 // carry and propagates the result to the rank's last slice edge with one long-span action
@@ -114,13 +121,14 @@ int adjoint_blocks(Handle* h, const double* wend, double* out, double* gacc, cud
     for (int q = b.q1 - 2; q >= b.q0; --q) {
       double* res = nullptr;
       PX_TRY(exp_action(h, PX_PLAN_SLICE, h->AT, C, C_bs, wend + (size_t)q * h->n, lane_bs, ss ? nullptr : b.Gp, &res,
-                        b.st, ss && q > b.q0 ? b.S : nullptr));
+                        b.st, ss && q > b.q0 ? b.S : nullptr, top_time(h, q + 1)));
       C = res;
       C_bs = nb;
     }
     if (g > 0) {
       double* res = nullptr;
-      PX_TRY(exp_action(h, PX_PLAN_BLOCK_LONG + g - 1, h->AT, C, C_bs, nullptr, 0, b.Gp, &res, b.st));
+      PX_TRY(exp_action(h, PX_PLAN_BLOCK_LONG + g - 1, h->AT, C, C_bs, nullptr, 0, b.Gp, &res, b.st, nullptr,
+                        top_time(h, b.q0)));
       C = res;
       C_bs = nb;
     }
@@ -191,8 +199,13 @@ int set_local_blocks(Handle* h, int blocks) {
 int direct_linear(Handle* h, cudaStream_t s) {
   const long long nb = (long long)h->n;
   const long long lane_bs = (long long)h->Pl * nb;  // stride between batch members in lanes
-  // g = A·u0 + f  (u0 shared by all members)
-  PX_TRY(apply_plus_control(h, h->g, h->u0, 0, h->A, true, s));
+  // g = A·u0 + f  (u0 shared by all members); with a time law g = A·u0 and the lanes add θ(t)·f
+  if (h->has_law) {
+    PX_TRY(apply_plus_control(h, h->g, h->u0, 0, h->A, false, s));
+    PX_TRY(apply_plus_control(h, h->fctl, h->u0, 0, px::Stencil5{0.0, 0.0, 0.0, 0.0, 0.0}, true, s));
+  } else {
+    PX_TRY(apply_plus_control(h, h->g, h->u0, 0, h->A, true, s));
+  }
   const double* vend = nullptr;
   int tm = tbegin(h, PX_PHASE_RK4_DIRECT, s);
   PX_TRY(rk4_sweep(h, false, &vend, s));
@@ -248,16 +261,18 @@ int adjoint_linear(Handle* h, cudaStream_t s) {
   tend(h, tm, s);
   h->wend = wend;
   tm = tbegin(h, PX_PHASE_EXP_ADJOINT, s);
-  // G partial <- Σ_p z_p  (z_p = Σ_steps h·w3 + nsteps·c)
+  // G partial <- Σ_p z_p  (z_p = Σ_steps h·w3 + nsteps·c; with a time law the θ-weighted lane
+  // integrals and the summed source part in cz, lanes.cu)
   if (h->z_closed) PX_TRY(z_closed_form(h, wend, s));
-  else PX_TRY(lane_sum_plus(h, h->G, h->Z, h->cz, (double)h->Pl * h->d.nsteps, h->z_valid, s));
-  if (use_scan1d(h)) {
+  else PX_TRY(lane_sum_plus(h, h->G, h->Z, h->cz, h->has_law ? 1.0 : (double)h->Pl * h->d.nsteps, h->z_valid, s));
+  if (use_scan1d(h) && !h->has_law) {
     PX_TRY(scan1d(h, true, wend, h->QDAG0, h->G, h->d.p_begin > 0 ? PX_PLAN_LONG_ADJOINT : -1, s));
   } else if (use_blocks(h)) {
     PX_TRY(adjoint_blocks(h, wend, h->QDAG0, h->G, s));
     if (h->d.p_begin > 0) {
       double* res = nullptr;
-      PX_TRY(exp_action(h, PX_PLAN_LONG_ADJOINT, h->AT, h->QDAG0, nb, nullptr, 0, h->G, &res, s));
+      PX_TRY(exp_action(h, PX_PLAN_LONG_ADJOINT, h->AT, h->QDAG0, nb, nullptr, 0, h->G, &res, s, nullptr,
+                        top_time(h, 0)));
       PX_TRY(axpby(h, h->QDAG0, nb, res, nb, 1.0, nullptr, 0, 0.0, s));
     }
   } else {
@@ -268,13 +283,13 @@ int adjoint_linear(Handle* h, cudaStream_t s) {
     for (int q = h->Pl - 2; q >= 0; --q) {
       double* res = nullptr;
       PX_TRY(exp_action(h, PX_PLAN_SLICE, h->AT, C, C_bs, wend + (size_t)q * h->n, lane_bs, ss ? nullptr : h->G, &res,
-                        s, ss && q > 0 ? h->S : nullptr));
+                        s, ss && q > 0 ? h->S : nullptr, top_time(h, q + 1)));
       C = res;
       C_bs = nb;
     }
     if (h->d.p_begin > 0) {
       double* res = nullptr;
-      PX_TRY(exp_action(h, PX_PLAN_LONG_ADJOINT, h->AT, C, C_bs, nullptr, 0, h->G, &res, s));
+      PX_TRY(exp_action(h, PX_PLAN_LONG_ADJOINT, h->AT, C, C_bs, nullptr, 0, h->G, &res, s, nullptr, top_time(h, 0)));
       C = res;
       C_bs = nb;
     }
@@ -309,8 +324,14 @@ int finish_adjoint_impl(Handle* h, cudaStream_t s) {
   const int tm = tbegin(h, PX_PHASE_OTHER, s);
   // absorbed final condition: q† = q†_T + the solved part (paraexp.py:268-270)
   PX_TRY(axpby(h, h->QDAG0, nb, h->QDAG0, nb, 1.0, h->QT, nb, 1.0, s));
-  PX_TRY(axpby(h, h->G, nb, h->G, nb, 1.0, h->QT, nb, h->d.T, s));
-  PX_TRY(project(h, h->GRAD, h->QT, nb, h->d.T, 1.0, s));
+  // ∫₀ᵀ θ dt·q†_T (T without a time law)
+  double wT = h->d.T;
+  if (h->has_law) {
+    const double a = h->law[0], b = h->law[1], c = h->law[2], w = h->law[3], T = h->d.T;
+    wT = (w == 0.0) ? (a + c) * T : a * T + b * (1.0 - std::cos(w * T)) / w + c * std::sin(w * T) / w;
+  }
+  PX_TRY(axpby(h, h->G, nb, h->G, nb, 1.0, h->QT, nb, wT, s));
+  PX_TRY(project(h, h->GRAD, h->QT, nb, wT, 1.0, s));
   tend(h, tm, s);
   return PX_OK;
 }

@@ -78,6 +78,11 @@ class EngineSpec:
     local_blocks: int = 0       # 0: automatic (concurrent block carries for Krylov); 1: sequential scan
     variants: tuple = ()        # ((name, value), …) kernel variants (_native.VARIANTS), e.g. (("march2", 2),)
     z_accum: bool = False       # 2D adjoint ∫ by a per-lane accumulator instead of the closed form
+    law: tuple = (1.0, 0.0, 0.0, 0.0)  # forcing time law θ(t) = α + β sin ωt + γ cos ωt (linear testbed)
+
+    @property
+    def has_law(self) -> bool:
+        return tuple(self.law[:3]) != (1.0, 0.0, 0.0)
 
     @property
     def nsteps(self) -> int:
@@ -212,8 +217,14 @@ class ParaexpEngine:
         krylov = isinstance(spec.expaction, KrylovConfig)
         d.expaction = N.PX_EXP_KRYLOV if krylov else N.PX_EXP_CHEBYSHEV
         d.krylov_m = spec.expaction.m if krylov else 0
+        field_ctl = getattr(sysm.basis, "is_field", False)
         d.flags = (N.PX_FLAG_BOUNDARY_STATES if spec.boundary_states else 0) | (
-            N.PX_FLAG_Z_ACCUM if spec.z_accum or os.environ.get("PX_Z_ACCUM") == "1" else 0)
+            N.PX_FLAG_Z_ACCUM if spec.z_accum or os.environ.get("PX_Z_ACCUM") == "1" else 0) | (
+            N.PX_FLAG_FIELD_CONTROL if field_ctl else 0)
+        if spec.has_law and not sysm.is_linear:
+            raise ConfigError("time_law: the linear testbed's loop (Burgers: objective='tracking', hybrid)")
+        if spec.has_law and isinstance(spec.expaction, KrylovConfig):
+            raise ConfigError("time_law: needs Chebyshev exp-actions (their time-law integral series)")
         self._desc = d
         torch = _torch()
         if torch is not None and torch.cuda.is_available():
@@ -230,11 +241,15 @@ class ParaexpEngine:
                 self.set_variant(name, int(os.environ[env]))
         for name, value in spec.variants:
             self.set_variant(name, value)
-        tx, _a = N.dptr(sysm.basis.tx)
-        ty, _b = N.dptr(sysm.basis.ty)
-        ix, _c = N.iptr(sysm.basis.ix)
-        iy, _d = N.iptr(sysm.basis.iy)
-        N.check(self.lib, self.lib.px_set_basis(h, tx, ty, ix, iy), h)
+        if not field_ctl:
+            tx, _a = N.dptr(sysm.basis.tx)
+            ty, _b = N.dptr(sysm.basis.ty)
+            ix, _c = N.iptr(sysm.basis.ix)
+            iy, _d = N.iptr(sysm.basis.iy)
+            N.check(self.lib, self.lib.px_set_basis(h, tx, ty, ix, iy), h)
+        if spec.has_law:
+            law, _e = N.dptr(np.asarray(spec.law, dtype=np.float64))
+            N.check(self.lib, self.lib.px_set_time_law(h, law), h)
         self.plans: dict[int, ChebPlan | KrylovPlan] = {}
         self._keep = []
         self._adjoint_mode = "absorbed"
@@ -291,7 +306,8 @@ class ParaexpEngine:
     # -- plans ---------------------------------------------------------------
 
     def _plan(self, region, span):
-        return plan_for(region, span, self.spec.expaction, base_span=self.spec.system.spec.T / self.spec.P)
+        return plan_for(region, span, self.spec.expaction, base_span=self.spec.system.spec.T / self.spec.P,
+                        omega=self.spec.law[3] if self.spec.has_law else 0.0)
 
     def _set_plan(self, slot: int, plan) -> None:
         self.plans[slot] = plan
@@ -302,6 +318,10 @@ class ParaexpEngine:
         bp, kb = N.dptr(plan.coef_phi)
         c = N.ChebPlanC(plan.span, plan.substeps, plan.degree, plan.center, plan.scale, plan.sigma, be, bp)
         N.check(self.lib, self.lib.px_set_cheb_plan(self.h, slot, ctypes.byref(c)), self.h)
+        if plan.coef_gc is not None:
+            gc, kc = N.dptr(plan.coef_gc)
+            gs, kd = N.dptr(plan.coef_gs)
+            N.check(self.lib, self.lib.px_set_cheb_plan_law(self.h, slot, gc, gs), self.h)
 
     # -- inputs / outputs ----------------------------------------------------
 

@@ -381,7 +381,7 @@ def chained(plan, k: int):
         return KrylovPlan(span=plan.span * k, substeps=plan.substeps * k, m=plan.m)
     return ChebPlan(span=plan.span * k, substeps=plan.substeps * k, degree=plan.degree, center=plan.center,
                     scale=plan.scale, sigma=plan.sigma, coef_exp=plan.coef_exp, coef_phi=plan.coef_phi,
-                    err_bound=plan.err_bound * k)
+                    err_bound=plan.err_bound * k, omega=plan.omega, coef_gc=plan.coef_gc, coef_gs=plan.coef_gs)
 
 
 HORIZON_MARGIN = 10.0
@@ -395,13 +395,17 @@ def action_config(cfg, span: float):
     return replace(cfg, tol=cfg.tol * min(1.0, span / cfg.horizon) / HORIZON_MARGIN, horizon=0.0)
 
 
-def plan_for(region: SpectralRegion, span: float, cfg, base_span: float | None = None):
+def plan_for(region: SpectralRegion, span: float, cfg, base_span: float | None = None, omega: float = 0.0):
     """Plan for ``span``; when ``span`` is an integer multiple k of ``base_span``
     (block-scan long spans are multiples of the slice width), the k-fold chained
     base plan is also considered and the cheaper feasible plan is returned. A horizon
     budget (``cfg.horizon``) is split over the actions in proportion to their spans."""
-    one_cfg = plan_krylov if isinstance(cfg, KrylovConfig) else plan_chebyshev
-    one = lambda reg, sp, c: one_cfg(reg, sp, action_config(c, sp))
+    if isinstance(cfg, KrylovConfig):
+        if omega:
+            raise PropagationFailure("a forcing time law needs Chebyshev exp-actions (its integral series)")
+        one = lambda reg, sp, c: plan_krylov(reg, sp, action_config(c, sp))
+    else:
+        one = lambda reg, sp, c: plan_chebyshev(reg, sp, action_config(c, sp), omega)
     k = None
     if base_span is not None and span > base_span:
         q = span / base_span
@@ -418,6 +422,19 @@ def plan_for(region: SpectralRegion, span: float, cfg, base_span: float | None =
 
 
 def plan_family(region: SpectralRegion, spans, cfg: ChebyshevConfig, omega: float = 0.0) -> list[ChebPlan]:
+    """Cached `_plan_family` (the frozen-operator regions are quantised, so repeated loops on
+    the same problem reuse the plans)."""
+    spans = tuple(float(s) for s in spans)
+    return list(_plan_family_cached(_region_key(region), spans, cfg, float(omega)))
+
+
+@lru_cache(maxsize=64)
+def _plan_family_cached(key, spans, cfg, omega):
+    ellipses, rect, crouzeix = key
+    return tuple(_plan_family(SpectralRegion(ellipses=ellipses, rect=rect, crouzeix=crouzeix), spans, cfg, omega))
+
+
+def _plan_family(region: SpectralRegion, spans, cfg: ChebyshevConfig, omega: float = 0.0) -> list[ChebPlan]:
     """Plans for a set of slice spans sharing one spectral region (variable slices, e.g. the
     hybrid's geometric partition): the widest span is planned in full; every other span reuses
     its foci with as many substeps as keep the substep width at most the widest plan's, and the

@@ -137,14 +137,14 @@ def _default_expaction(system: System):
 
 def get_engine(system: System, N: int, rk: RK4Config, expaction, batch: int, rank: int = 0, world: int = 1,
                boundary_states: bool = False, direct: str = "serial", eps: float = 1e-3, max_iter: int = 25,
-               min_iter: int = 2) -> ParaexpEngine:
+               min_iter: int = 2, law: tuple = (1.0, 0.0, 0.0, 0.0)) -> ParaexpEngine:
     """Cached engine per (problem, partition, numerics, rank): handles own HBM scratch."""
-    key = (system.grid, system.spec, system.basis.K, N, rk.dt, expaction, batch, rank, world, boundary_states,
-           direct, eps, max_iter, min_iter)
+    key = (system.grid, system.spec, type(system.basis).__name__, system.basis.K, N, rk.dt, expaction, batch, rank,
+           world, boundary_states, direct, eps, max_iter, min_iter, tuple(law))
     eng = _ENGINES.get(key)
     if eng is None:
         eng = ParaexpEngine(EngineSpec(system, N, rk.dt, expaction, batch, rank, world, boundary_states,
-                                       direct, eps, max_iter, min_iter))
+                                       direct, eps, max_iter, min_iter, law=tuple(law)))
         _ENGINES[key] = eng
     return eng
 
@@ -196,6 +196,11 @@ def direct_adjoint_loop(
     trajectory); "frozen_span" — the reference's `solve_hybrid` adjoint
     (`hybrid.py:194-237`: q†_T through the frozen J(ū_p)ᵀ; one rank).
 
+    ``time_law`` (`hybrid.TimeLaw`, linear testbed, terminal objective): the control acts as
+    f·θ(t) — the reference's f·sin(ωt) is ``TimeLaw.sine(ω)`` — and ∂J/∂f = ∫θ·q† dt. With a
+    field system (`systems.build_field_system`) ``f`` is the forcing field and ``grad`` its field
+    gradient.
+
     ``objective="tracking"`` runs the reference's own loop (`optimization.py:172-189`) for
     Burgers with ``algorithm`` "hybrid" or "serial": J = (1/T)∫‖u − u_t‖² dt against the target
     trajectory ``q_true`` given on the serial sweep's nodes ((S+1, n) or (S+1, B, n), e.g. from
@@ -209,9 +214,11 @@ def direct_adjoint_loop(
         raise ValueError(f"objective must be 'terminal' or 'tracking', not {objective!r}")
     if objective == "tracking":
         return _tracking_loop(system, f, q_true, algorithm, N, rk, expaction, u0, backend, plan, time_law, overlap)
-    if plan is not None or time_law is not None:
-        raise ConfigError("plan / time_law: the geometric partition and the forcing time law belong to the "
-                          "tracking objective (objective='tracking')")
+    if plan is not None:
+        raise ConfigError("plan: the geometric partition belongs to the hybrid tracking loop (objective='tracking')")
+    law = tuple(float(v) for v in time_law.as_tuple()) if time_law is not None else (1.0, 0.0, 0.0, 0.0)
+    if law[:3] != (1.0, 0.0, 0.0) and not system.is_linear:
+        raise ConfigError("time_law with the terminal objective: the linear testbed (Burgers: objective='tracking')")
     if backend not in BACKENDS:
         raise ValueError(f"unknown backend {backend!r}; the B200 path provides {BACKENDS}")
     if algorithm not in ALGORITHMS:
@@ -240,7 +247,7 @@ def direct_adjoint_loop(
     if algorithm in (NONLINEAR, SERIAL) or hybrid_adjoint == "frozen_span":
         rank, world = 0, 1  # one rank (every rank computes it identically): nothing to shard
     eng = get_engine(system, N, rk, expaction, B, rank, world, boundary_states and world == 1,
-                     "iterative" if algorithm == NONLINEAR else "serial", eps, max_iter, min_iter)
+                     "iterative" if algorithm == NONLINEAR else "serial", eps, max_iter, min_iter, law)
     tick = time.perf_counter()
     eng.set_inputs(u0, np.asarray(q_true, dtype=np.float64), ctrl)
     if hybrid_adjoint != "absorbed":

@@ -175,6 +175,30 @@ class ModeBasis:
         return out
 
 
+@dataclass(frozen=True)
+class FieldBasis:
+    """The control as a full spatial field (K = n, the reference's forcing field f_spatial,
+    `problems.py:155-162`): ``field`` and ``project`` are the identity, and the gradient is the
+    field ∂J/∂f itself. The device runs it with PX_FLAG_FIELD_CONTROL (no factor tables)."""
+
+    K: int
+    tx: np.ndarray = field(default_factory=lambda: np.ones((1, 1)), repr=False)
+    ty: np.ndarray = field(default_factory=lambda: np.ones((1, 1)), repr=False)
+    ix: np.ndarray = field(default_factory=lambda: np.zeros(1, dtype=np.int32), repr=False)
+    iy: np.ndarray = field(default_factory=lambda: np.zeros(1, dtype=np.int32), repr=False)
+
+    is_field = True
+
+    def field(self, coeffs: np.ndarray) -> np.ndarray:
+        return np.asarray(coeffs, dtype=np.float64)
+
+    def project(self, G: np.ndarray) -> np.ndarray:
+        return np.asarray(G, dtype=np.float64)
+
+    def matrix(self) -> np.ndarray:
+        return np.eye(self.K)
+
+
 def mode_basis(grid: Grid, K: int) -> ModeBasis:
     x = grid.x1()
     if grid.dim == 1:

@@ -42,14 +42,19 @@ def _prepare(system: System, f, rk, expaction):
     return ctrl, expaction or _default_expaction(system)
 
 
+def _law(time_law):
+    return tuple(float(v) for v in time_law.as_tuple()) if time_law is not None else (1.0, 0.0, 0.0, 0.0)
+
+
 def solve_direct_linear(system: System, u0, f, N: int, rk: RK4Config, expaction=None,
-                        boundary_states: bool = False) -> DirectSolution:
-    """u(T) of u' = A u + Σ c_k φ_k, u(0) = u0, by Paraexp over N slices (`paraexp.py:221-248`)."""
+                        boundary_states: bool = False, time_law=None) -> DirectSolution:
+    """u(T) of u' = A u + f·θ(t), u(0) = u0, by Paraexp over N slices (`paraexp.py:221-248`);
+    f = Σ c_k φ_k (or the field itself with a field system), θ ≡ 1 unless ``time_law``."""
     if not system.is_linear:
         raise ValueError("solve_direct_linear requires a linear testbed")
     ctrl, expaction = _prepare(system, f, rk, expaction)
     B = ctrl.shape[0]
-    eng = get_engine(system, N, rk, expaction, B, boundary_states=boundary_states)
+    eng = get_engine(system, N, rk, expaction, B, boundary_states=boundary_states, law=_law(time_law))
     u0 = np.asarray(u0, dtype=np.float64).reshape(-1)
     eng.set_inputs(u0, np.zeros(system.n), ctrl)
     eng.direct_partial()
@@ -60,14 +65,14 @@ def solve_direct_linear(system: System, u0, f, N: int, rk: RK4Config, expaction=
 
 
 def solve_adjoint_linear(system: System, qdag_T, N: int, rk: RK4Config, expaction=None,
-                         batch: int = 1) -> AdjointSolution:
-    """q†(0) and ∫₀ᵀ q† dt of −q†' = Aᵀ q†, q†(T) = ``qdag_T`` by Paraexp over N slices
-    in reflected time (`paraexp.py:298-326`, absorbed final condition)."""
+                         batch: int = 1, time_law=None) -> AdjointSolution:
+    """q†(0) and ∫₀ᵀ θ(t)·q† dt (θ ≡ 1 unless ``time_law``) of −q†' = Aᵀ q†, q†(T) = ``qdag_T``
+    by Paraexp over N slices in reflected time (`paraexp.py:298-326`, absorbed final condition)."""
     if not system.is_linear:
         raise ValueError("solve_adjoint_linear requires a linear testbed (Burgers: solve_hybrid)")
     ctrl, expaction = _prepare(system, np.zeros((batch, system.basis.K)), rk, expaction)
     q = np.broadcast_to(np.asarray(qdag_T, dtype=np.float64).reshape(-1, system.n), (batch, system.n))
-    eng = get_engine(system, N, rk, expaction, batch)
+    eng = get_engine(system, N, rk, expaction, batch, law=_law(time_law))
     eng.set_inputs(np.zeros(system.n), np.zeros(system.n), ctrl)
     eng.set_adjoint_terminal(np.ascontiguousarray(q))
     eng.adjoint_partial()

@@ -12,6 +12,7 @@ from dataclasses import dataclass
 
 from .problems import (
     ADVECTION_DIFFUSION,
+    FieldBasis,
     BURGERS,
     Grid,
     ModeBasis,
@@ -58,3 +59,11 @@ def build_system(grid: Grid, spec: ProblemSpec, K: int) -> System:
     if spec.kind == BURGERS and grid.dim != 1:
         raise ValueError("the Burgers path is 1D (the reference's 2D system with V ≡ 0)")
     return System(grid, spec, mode_basis(grid, K))
+
+
+def build_field_system(grid: Grid, spec: ProblemSpec) -> System:
+    """The linear testbed with the control as a full spatial field (the reference's
+    `ProblemSpec.f_spatial`, `problems.py:59-83,155-162`): ∂J/∂f is returned as a field."""
+    if spec.kind != ADVECTION_DIFFUSION:
+        raise ValueError("field controls: the advection–diffusion testbed (Burgers: tracking.solve_hybrid_tracking)")
+    return System(grid, spec, FieldBasis(grid.npoints))
