@@ -186,9 +186,32 @@ cudaError_t hyb_scan_t(const px::HybScanArgs& a, cudaStream_t s) {
   }
 
 cudaError_t hyb_launch_direct(const px::HybArgs& a, int ppt, cudaStream_t s) {
+  // the cluster sweep (8 CTAs per member, 64-point ghost zones refreshed every 16 steps) for the
+  // larger grids, as the config-3 direct sweep
+  constexpr int kCS = 8, kPPT = 4, kG = 64;
+  if (a.nx >= 2048 && a.nx % (kCS * kPPT) == 0 && a.nx / kCS >= kG && a.nx / kCS / kPPT + 2 * (kG / kPPT) <= 256) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(a.B * kCS));
+    cfg.blockDim = dim3((unsigned)(((a.nx / kCS / kPPT + 2 * (kG / kPPT) + 31) / 32) * 32));
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kCS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, px::k_hyb_direct_cluster<kPPT, kCS, kG>, a);
+  }
 #define PX_C(P) hyb_direct_t<P>(a, s)
   PX_HYB_DISPATCH(ppt, PX_C)
 #undef PX_C
+}
+
+int hyb_direct_ctas(int nx, int B) {
+  constexpr int kCS = 8, kPPT = 4, kG = 64;
+  const bool cl = nx >= 2048 && nx % (kCS * kPPT) == 0 && nx / kCS >= kG && nx / kCS / kPPT + 2 * (kG / kPPT) <= 256;
+  return cl ? B * kCS : B;
 }
 
 cudaError_t hyb_launch_lanes(const px::HybArgs& a, int ppt, size_t smem, cudaStream_t s) {

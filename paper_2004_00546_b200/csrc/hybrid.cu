@@ -208,7 +208,7 @@ int px_hybrid_direct(void* p, int overlap, void* stream) {
   HY_CUDA(hy, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, hy->base.device));
   HY_CUDA(hy, hyb_lanes_occupancy(hy->ppt, hy->lane_smem, &per_sm));
   if (per_sm < 1) return fail(&hy->base, PX_ERR_ARG, "hybrid: the slice kernel does not fit an SM");
-  const bool ov = overlap && (long long)hy->B * hy->P + hy->B <= sms;
+  const bool ov = overlap && (long long)hy->B * hy->P + hyb_direct_ctas(hy->nx, hy->B) <= sms;
   HY_CUDA(hy, cudaMemsetAsync(hy->flags, 0, sizeof(int) * hy->B * hy->P, s));
   HY_CUDA(hy, cudaEventRecord(hy->ev[0], s));
   if (ov) {

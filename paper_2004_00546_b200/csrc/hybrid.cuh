@@ -16,6 +16,7 @@
 // Every thread owns a contiguous run of PPT points; run edges are exchanged through double-
 // buffered shared arrays (one CTA barrier per stage / term).
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -114,6 +115,144 @@ __global__ void __launch_bounds__(HYB_NT) k_hyb_direct(HybArgs a) {
   }
   const double tot = block_sum<HYB_NT>(jacc, red);
   if (t == 0) a.J[b] = (a.h / a.T) * tot;
+}
+
+// The serial sweep of k_hyb_direct spread over the CS CTAs of a thread-block cluster (the
+// k_burgers_direct_cluster scheme): CTA r owns W = n/CS points plus G ghost points per side,
+// recomputed redundantly (one ghost layer per RK4 stage), the ghost zones of u refreshed from
+// the neighbouring CTAs' shared memory (DSMEM) after one cluster barrier every G/4 steps. A slice
+// is published when every CTA of the cluster has stored its part of the slice's last node (each
+// writer fences, one cluster barrier, one flag store); the tracking cost is reduced over the
+// cluster through DSMEM in a fixed order.
+template <int PPT, int CS, int G>
+__global__ void __launch_bounds__(256) k_hyb_direct_cluster(HybArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  static_assert(G % (4 * PPT) == 0, "ghost width: whole runs, whole steps");
+  constexpr int GR = G / PPT;
+  constexpr int STEPS_PER_REFRESH = G / 4;
+  __shared__ double eL[2][256], eR[2][256];
+  __shared__ double xbuf[2][2][G];
+  __shared__ double red[8];
+  __shared__ double jpart;
+  const int n = a.nx;
+  const int W = n / CS;
+  const int rank = (int)cluster.block_rank();
+  const int b = blockIdx.x / CS;
+  const int t = threadIdx.x;
+  const int NR = W / PPT + 2 * GR;
+  const bool act = t < NR;
+  const int g0 = rank * W - G + t * PPT;
+  const bool owned = act && t >= GR && t < NR - GR;
+  const int tl = (t == 0) ? 0 : t - 1, tr = (t + 1 >= NR) ? NR - 1 : t + 1;
+  auto gidx = [&](int k) { int g = g0 + k; g %= n; return g < 0 ? g + n : g; };
+  const double inv2h = 1.0 / (2.0 * a.hx);
+  const double Dih2 = a.D / (a.hx * a.hx);
+  const double h = a.h, hh = 0.5 * a.h, h6 = a.h / 6.0;
+  const size_t ns = (size_t)a.B * n;
+  const size_t tstride = (size_t)a.target_b * n;
+  const double* tg = a.target + (a.target_b > 1 ? (size_t)b * n : 0);
+  double f[PPT], u[PPT], acc[PPT], x[PPT], kk[PPT];
+  double jacc = 0.0;
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    f[k] = act ? a.f[(size_t)b * n + gidx(k)] : 0.0;
+    u[k] = act ? a.u0[(size_t)b * n + gidx(k)] : 0.0;
+  }
+  auto node = [&](int s, double w) {
+    if (!owned) return;
+    double e = 0.0;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      const int i = gidx(k);
+      a.traj[(size_t)s * ns + (size_t)b * n + i] = u[k];
+      const double d = u[k] - tg[(size_t)s * tstride + i];
+      e = fma(d, d, e);
+    }
+    jacc = fma(w, e, jacc);
+  };
+  node(0, 0.5);
+  int par = 0, xpar = 0;
+  auto rhs = [&](double th, double* k_out) {
+    if (act) {
+      eL[par][t] = x[0];
+      eR[par][t] = x[PPT - 1];
+    }
+    __syncthreads();
+    const double xl = eR[par][tl], xr = eL[par][tr];
+    par ^= 1;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      const double ym = (k == 0) ? xl : x[k - 1];
+      const double yp = (k + 1 == PPT) ? xr : x[k + 1];
+      k_out[k] = fma(th, f[k], fma(-x[k], (yp - ym) * inv2h, (yp - 2.0 * x[k] + ym) * Dih2));
+    }
+  };
+  auto refresh = [&]() {
+    if (act) {
+      if (t >= GR && t < 2 * GR) {
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) xbuf[xpar][0][(t - GR) * PPT + k] = u[k];
+      }
+      if (t >= NR - 2 * GR && t < NR - GR) {
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) xbuf[xpar][1][(t - (NR - 2 * GR)) * PPT + k] = u[k];
+      }
+    }
+    cluster.sync();
+    if (act && t < GR) {
+      const double* src = cluster.map_shared_rank(&xbuf[xpar][1][0], (unsigned)((rank + CS - 1) % CS));
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) u[k] = src[t * PPT + k];
+    }
+    if (act && t >= NR - GR) {
+      const double* src = cluster.map_shared_rank(&xbuf[xpar][0][0], (unsigned)((rank + 1) % CS));
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) u[k] = src[(t - (NR - GR)) * PPT + k];
+    }
+    xpar ^= 1;
+  };
+  int valid = STEPS_PER_REFRESH;
+  int p = 0, next = a.offsets[1];
+  for (int st = 0; st < a.S; ++st) {
+    if (valid == 0) {
+      refresh();
+      valid = STEPS_PER_REFRESH;
+    }
+    const double th1 = hyb_theta(a, 2 * st), th2 = hyb_theta(a, 2 * st + 1), th4 = hyb_theta(a, 2 * st + 2);
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) x[k] = u[k];
+    rhs(th1, kk);
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) { acc[k] = kk[k]; x[k] = fma(hh, kk[k], u[k]); }
+    rhs(th2, kk);
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) { acc[k] = fma(2.0, kk[k], acc[k]); x[k] = fma(hh, kk[k], u[k]); }
+    rhs(th2, kk);
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) { acc[k] = fma(2.0, kk[k], acc[k]); x[k] = fma(h, kk[k], u[k]); }
+    rhs(th4, kk);
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) u[k] = fma(h6, acc[k] + kk[k], u[k]);
+    --valid;
+    node(st + 1, st + 1 == a.S ? 0.5 : 1.0);
+    if (st + 1 == next) {
+      __threadfence();
+      cluster.sync();
+      if (rank == 0 && t == 0) atomicExch(a.flags + (size_t)b * a.P + p, 1);
+      ++p;
+      next = (p < a.P) ? a.offsets[p + 1] : -1;
+    }
+  }
+  const double tot = block_sum<256>(jacc, red);
+  if (t == 0) jpart = tot;
+  cluster.sync();
+  if (rank == 0 && t == 0) {
+    double s = 0.0;
+    for (int r = 0; r < CS; ++r) s += *cluster.map_shared_rank(&jpart, (unsigned)r);
+    a.J[b] = (a.h / a.T) * s;
+  }
+  cluster.sync();  // no CTA leaves while a neighbour may still read its exchange buffers
 }
 
 // The adjoint slice solve of lane (b, p) in reflected time, nodes o_{p+1} → o_p:

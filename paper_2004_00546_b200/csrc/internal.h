@@ -233,6 +233,7 @@ int nl_means_bounds(Handle* h, cudaStream_t s);
 int nl_sweep(Handle* h, double* err_max, cudaStream_t s);
 // the reference's hybrid with its tracking objective (hybrid.cuh, driven by hybrid.cu)
 cudaError_t hyb_launch_direct(const px::HybArgs& a, int ppt, cudaStream_t s);
+int hyb_direct_ctas(int nx, int B);  // CTAs of the serial sweep (8 per member on a cluster)
 cudaError_t hyb_launch_lanes(const px::HybArgs& a, int ppt, size_t smem, cudaStream_t s);
 cudaError_t hyb_launch_scan(const px::HybScanArgs& a, int ppt, cudaStream_t s);
 cudaError_t hyb_lanes_occupancy(int ppt, size_t smem, int* per_sm);

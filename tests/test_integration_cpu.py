@@ -1,0 +1,123 @@
+"""The reference-side binding (paper_2004_00546_b200.integration) executed
+against the reference itself — development container only (the reference is importable from
+/root/reference here; the GPU box has no reference, where tests/test_gpu_hybrid.py checks the
+binding's GPU run against the reference's golden numbers). Each conversion is checked on the
+reference's own objects, and the converted problem, solved by the oracle restatement, is held to
+the reference's solvers and loop."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from tests.conftest import rel_l2
+
+REF = "/root/reference/pkg/src"
+
+
+@pytest.fixture(scope="module")
+def R():
+    if not os.path.isdir(REF):
+        pytest.skip("reference not present (GPU box / CI): the binding is covered by the golden GPU test")
+    sys.path.insert(0, REF)
+    try:
+        import paradjoint
+    except Exception as e:  # pragma: no cover
+        pytest.skip(f"reference not importable: {e}")
+    return paradjoint
+
+
+def _advdiff(R, omega=3.0):
+    grid = R.Grid2D(12, 10)
+    f = np.random.default_rng(4).standard_normal(grid.npoints) * 0.3
+    spec = R.ProblemSpec("advection_diffusion", 0.7, 0.05, omega, 0.4, f)
+    return R.build_system(grid, spec)
+
+
+def test_advdiff_system_conversion(R):
+    from oracle.config_mode import stencil_apply
+    from paper_2004_00546_b200.integration import system_from_reference
+    ref = _advdiff(R)
+    sysm, f, law, emb = system_from_reference(ref)
+    x = np.random.default_rng(5).standard_normal(ref.n)
+    assert rel_l2(stencil_apply(sysm.A.as_tuple(), x, 12, 10), ref.A.apply(x)) <= 1e-14
+    assert rel_l2(stencil_apply(sysm.A.transpose().as_tuple(), x, 12, 10), ref.A.transpose_apply(x)) <= 1e-14
+    assert np.array_equal(f, ref.spec.f_spatial) and law.as_tuple() == (0.0, 1.0, 0.0, 3.0)
+    assert getattr(sysm.basis, "is_field", False) and emb.kind == "field"
+    t = 0.3
+    assert np.allclose(law(t) * f, ref.forcing(t), rtol=0, atol=1e-15)
+
+
+def test_advdiff_solvers_through_the_binding_vs_the_reference(R):
+    """u(T) of the reference's `solve_direct_linear` (its forcing f·sin ωt) and q†(0), ∫sin(ωt)q† dt
+    of its `solve_adjoint_linear` (terminal data, no source; `gradient_wrt_forcing`·T) — the
+    converted problem solved by the oracle's RK4 + Chebyshev restatement of the GPU path."""
+    from oracle.config_mode import linear_gradient_law
+    from paper_2004_00546_b200.expaction import ChebyshevConfig, plan_chebyshev
+    from paper_2004_00546_b200.integration import system_from_reference
+    ref = _advdiff(R)
+    sysm, f, law, _ = system_from_reference(ref)
+    T, N, steps = 0.4, 2, 200
+    part = R.partition_equidistant(T, N)
+    rk = R.RKConfig(rtol=1e-11, atol=1e-14)
+    leja = R.LejaConfig(tol=1e-13)
+    q0 = np.cos(np.arange(ref.n) * 0.1)
+    d = R.solve_direct_linear(ref.A, q0, ref.forcing, part, rk, leja)
+    pl = plan_chebyshev(sysm.region(), T / N, ChebyshevConfig(tol=1e-13), omega=law.omega)
+    args = (12, 10, sysm.A.as_tuple(), sysm.basis, T, N, steps, q0)
+    o = linear_gradient_law(*args, np.zeros(ref.n), f[None, :], law.as_tuple(), pl)
+    assert rel_l2(o.uT[0], d.eval(T)) <= 1e-9
+    qT = np.sin(np.arange(ref.n) * 0.37)
+    a = R.solve_adjoint_linear(ref.A, qT, lambda t: np.zeros(ref.n), part, rk, leja)
+    o2 = linear_gradient_law(*args, o.uT[0] - qT, f[None, :], law.as_tuple(), pl)   # q†_T = u(T) − (u(T) − qT)
+    assert rel_l2(o2.qdag0[0], a.eval(0.0)) <= 1e-9
+    g_ref = R.gradient_wrt_forcing(a, law.omega, T, probe_nodes=8001) * T
+    assert rel_l2(o2.G[0], g_ref) <= 1e-6   # the reference's probe-grid trapezoid vs RK4-consistent ∫
+
+
+def test_burgers_loop_conversion_vs_the_reference_loop(R):
+    """The reference's own hybrid loop (tracking objective, f·sin ωt, geometric plan) against the
+    binding's conversion (1D system, law, target on the nodes, plan) solved by the oracle."""
+    from oracle.config_mode import burgers_tracking_hybrid
+    from paper_2004_00546_b200.expaction import ChebyshevConfig, plan_family
+    from paper_2004_00546_b200.hybrid import make_hybrid_plan, slice_offsets
+    from paper_2004_00546_b200.integration import _node_trajectory, system_from_reference
+    from paper_2004_00546_b200.problems import frozen_bounds, frozen_region_from_bounds
+    nx, T, D, w = 16, 0.5, 0.05, 2 * np.pi
+    x = np.arange(nx) * 2 * np.pi / nx
+    emb = lambda u: np.concatenate([np.tile(u, 3), np.zeros(3 * nx)])
+    grid = R.Grid2D(nx, 3)
+    ref = R.build_system(grid, R.ProblemSpec("burgers", 0.0, D, w, T, emb(np.zeros(nx))))
+    f1 = 0.3 * np.cos(2 * x) + 0.4 * np.sin(x)
+    q_true = R.synthesize_truth(ref, emb(0.5 * np.sin(x)), R.RKConfig(rtol=1e-10, atol=1e-13, h_max=2.5e-4),
+                                algorithm="serial")
+    plan = R.make_hybrid_plan(T, 3, 1.5)
+    res = R.direct_adjoint_loop(ref, emb(f1), q_true, "hybrid", N=3, rk=R.RKConfig(rtol=1e-10, atol=1e-13),
+                                leja=R.LejaConfig(tol=1e-12), plan=plan, probe_nodes=4001)
+    sysm, f, law, e = system_from_reference(ref.with_forcing_field(emb(f1)))
+    assert e.kind == "burgers1d" and e.ny == 3 and np.array_equal(f, f1)
+    S = 500
+    target = _node_trajectory(q_true, e, T, S)
+    offs = slice_offsets(make_hybrid_plan(T, plan.N, plan.k).partition, T / S)
+    h = T / S
+
+    def pf(ubar):
+        reg = frozen_region_from_bounds(*frozen_bounds(ubar, sysm.grid, D))
+        return plan_family(reg, [(offs[p + 1] - offs[p]) * h for p in range(3)], ChebyshevConfig(tol=1e-12), w)
+
+    o = burgers_tracking_hybrid(nx, D, T, offs, np.zeros(nx), f, law.as_tuple(), target, pf)
+    assert abs(3 * o.J[0] - res.J) <= 1e-6 * abs(res.J)
+    assert rel_l2(e.to_reference(o.grad[0]), res.grad) <= 1e-5
+
+
+def test_binding_refuses_what_the_path_cannot_express(R):
+    from paper_2004_00546_b200.errors import ConfigError
+    from paper_2004_00546_b200.integration import direct_adjoint_loop, system_from_reference
+    grid = R.Grid2D(8, 3)
+    f = np.concatenate([np.arange(24) * 0.1, np.zeros(24)])      # not y-invariant
+    bad = R.build_system(grid, R.ProblemSpec("burgers", 0.0, 0.05, 1.0, 0.5, f))
+    with pytest.raises(ConfigError):
+        system_from_reference(bad)
+    with pytest.raises(ConfigError):   # the linear loop's tracking objective
+        direct_adjoint_loop(_advdiff(R), np.zeros(120), None, "linear", dt=1e-3)
