@@ -96,7 +96,9 @@ enum {
   PX_VAR_CHEB_BAND = 5,       /* rows per band of the 2D Chebyshev passes (0: one wave) */
   PX_VAR_SCAN1D_CLUSTER = 6,  /* 1D scans on 8-CTA clusters for n ≥ 2048 (default 1) */
   PX_VAR_BURGERS_CLUSTER = 7, /* Burgers sweeps on 8-CTA clusters for n ≥ 2048 (default 1) */
-  PX_VAR_CHEB_TERMS_PHI = 8   /* as PX_VAR_CHEB_TERMS for passes with the φ₁ accumulator (default 5) */
+  PX_VAR_CHEB_TERMS_PHI = 8,  /* as PX_VAR_CHEB_TERMS for passes with the φ₁ accumulator (default 5) */
+  PX_VAR_KRYLOV_ORTHO = 9     /* Arnoldi orthogonalisation: 1 (default) delayed reorthogonalisation, one
+                                 reduction and two basis passes per step; 0 CGS2, four passes */
 };
 enum { PX_ADJOINT_ABSORBED = 0, PX_ADJOINT_FROZEN_SPAN = 1 };  /* px_set_adjoint_mode */
 

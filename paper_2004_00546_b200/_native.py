@@ -30,7 +30,7 @@ PX_FLAG_BOUNDARY_STATES, PX_FLAG_Z_ACCUM, PX_FLAG_FIELD_CONTROL = 1, 2, 4
 ABI_VERSION = 3
 # kernel-variant keys (px_set_variant)
 VARIANTS = {"march2": 0, "march_cols": 1, "march_band": 2, "cheb_terms": 3, "cheb_strip": 4, "cheb_band": 5,
-            "scan1d_cluster": 6, "burgers_cluster": 7, "cheb_terms_phi": 8}
+            "scan1d_cluster": 6, "burgers_cluster": 7, "cheb_terms_phi": 8, "krylov_ortho": 9}
 PX_ADJOINT_ABSORBED, PX_ADJOINT_FROZEN_SPAN = 0, 1
 
 

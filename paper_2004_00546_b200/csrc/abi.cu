@@ -326,6 +326,9 @@ int px_set_variant(void* handle, int key, int value) {
       if (value < 0) return fail(h, PX_ERR_ARG, "PX_VAR_CHEB_BAND must be ≥ 0");
       v.cheb_band = value; break;
     case PX_VAR_SCAN1D_CLUSTER: v.scan1d_cluster = value != 0; break;
+    case PX_VAR_KRYLOV_ORTHO:
+      if (value != 0 && value != 1) return fail(h, PX_ERR_ARG, "PX_VAR_KRYLOV_ORTHO must be 0 or 1");
+      v.krylov_ortho = value; break;
     case PX_VAR_BURGERS_CLUSTER: v.burgers_cluster = value != 0; break;
     default: return fail(h, PX_ERR_ARG, "unknown variant key");
   }
@@ -347,6 +350,7 @@ int px_get_variant(void* handle, int key, int* value) {
     case PX_VAR_CHEB_BAND: *value = v.cheb_band; break;
     case PX_VAR_SCAN1D_CLUSTER: *value = v.scan1d_cluster; break;
     case PX_VAR_BURGERS_CLUSTER: *value = v.burgers_cluster; break;
+    case PX_VAR_KRYLOV_ORTHO: *value = v.krylov_ortho; break;
     default: return fail(h, PX_ERR_ARG, "unknown variant key");
   }
   return PX_OK;

@@ -113,6 +113,10 @@ struct KrylovWork {
   double* part = nullptr;     // B × (MAX_M+1) × nblk partial dots
   double* beta = nullptr;     // B
   double* coef = nullptr;     // B × 2 × m  (exp column, φ column), β-scaled
+  // delayed reorthogonalization (one reduction and two basis passes per step)
+  double* u = nullptr;        // 2 × B × n  the candidate vector (ping-pong)
+  double* kc = nullptr;       // B × KC_STRIDE  per-step coefficients (g, a/β, 1/β, κ)
 };
+constexpr int KC_STRIDE = 2 * (KRYLOV_MAX_M + 1) + 4;
 
 }  // namespace px

@@ -244,6 +244,8 @@ __global__ void __launch_bounds__(256) k_hyb_direct_cluster(HybArgs a) {
       next = (p < a.P) ? a.offsets[p + 1] : -1;
     }
   }
+  if (t < 8) red[t] = 0.0;  // the CTA may have fewer than 8 warps
+  __syncthreads();
   const double tot = block_sum<256>(jacc, red);
   if (t == 0) jpart = tot;
   cluster.sync();

@@ -41,6 +41,8 @@ struct Variants {
   int cheb_band = 0;        // PX_VAR_CHEB_BAND: rows per band of the 2D passes (0: one wave)
   int scan1d_cluster = 1;   // PX_VAR_SCAN1D_CLUSTER: 8-CTA cluster scans for 1D n ≥ 2048
   int burgers_cluster = 1;  // PX_VAR_BURGERS_CLUSTER: 8-CTA cluster Burgers sweeps for n ≥ 2048
+  int krylov_ortho = 1;     // PX_VAR_KRYLOV_ORTHO: 1 delayed reorthogonalization (two basis passes per
+                            // Arnoldi step), 0 CGS2 (four passes)
 };
 
 struct Plan {

@@ -44,7 +44,7 @@ inline int krylov_alloc(KrylovWork& kw, int m, size_t n, int B, std::string* err
   if (!al(&kw.V, (size_t)(m + 1) * B * n) || !al(&kw.w, 2 * (size_t)B * n) ||
       !al(&kw.H, (size_t)B * (m + 1) * m) || !al(&kw.hcol, (size_t)B * (KRYLOV_MAX_M + 1)) ||
       !al(&kw.part, (size_t)B * (2 * (KRYLOV_MAX_M + 1) + 1) * std::max<size_t>((size_t)kw.nblk, 148 * 4)) || !al(&kw.beta, B) ||
-      !al(&kw.coef, (size_t)B * 2 * m))
+      !al(&kw.coef, (size_t)B * 2 * m) || !al(&kw.u, 2 * (size_t)B * n) || !al(&kw.kc, (size_t)B * KC_STRIDE))
     return PX_ERR_NOMEM;
 
   return PX_OK;
@@ -52,7 +52,7 @@ inline int krylov_alloc(KrylovWork& kw, int m, size_t n, int B, std::string* err
 
 inline void krylov_free(KrylovWork& kw) {
   cudaFree(kw.V); cudaFree(kw.w); cudaFree(kw.H); cudaFree(kw.hcol);
-  cudaFree(kw.part); cudaFree(kw.beta); cudaFree(kw.coef);
+  cudaFree(kw.part); cudaFree(kw.beta); cudaFree(kw.coef); cudaFree(kw.u); cudaFree(kw.kc);
   kw = KrylovWork{};
 }
 
@@ -367,16 +367,248 @@ __global__ void k_kr_combine(double* out, const double* V, const double* coef, i
   if (pacc) pacc[(size_t)b * n + i] += p;
 }
 
+// ---------------------------------------------------------------------------
+// Delayed reorthogonalization (DCGS2): one reduction and two basis passes per step.
+//
+// At step j the candidate u_j is orthogonal to Q_j = [v_0 … v_{j−1}] after ONE projection and
+// not normalised. One pass computes w = M·u_j and, in the same read of Q_j, a = Q_jᵀu_j,
+// b = Q_jᵀw, γ = ‖u_j‖², δ = u_jᵀw. Then (one CTA per member, k_kr_dfinal): the second
+// projection of u_j is a, β = √(γ − ‖a‖²), v_j = (u_j − Q_j a)/β, H[:, j−1] = c_{j−1} + a,
+// H[j, j−1] = β; the first projection of M·v_j = (w − Q_j H a − v_j β a_{j−1})/β follows from the
+// Arnoldi relation without touching Q again: c_Q = (b − H a)/β, c_v = ((δ − aᵀb)/β − β a_{j−1})/β.
+// The second pass (k_kr_dupdate) writes v_j = u_j/β − Q_j(a/β) and
+// u_{j+1} = w/β − κ·u_j − Q_j g, κ = (a_{j−1} + c_v)/β, g = H a/β + c_Q − κ a — the basis is read
+// twice per step instead of four times (CGS2), at the same orthogonality (equal to CGS2's H and V
+// to rounding; tests/test_gpu_parity.py compares both with the oracle).
+// ---------------------------------------------------------------------------
+
+// w = M·u (u from `u`, batch stride ubs); part slots: [0, j) Q_qᵀu, [j, 2j) Q_qᵀw, 2j γ, 2j+1 δ.
+// spmv = false: no w (the final reorthogonalization of u_m): slots [0, j) and 2j only.
+template <int DIM>
+__global__ void __launch_bounds__(256) k_kr_ddots(double* w, const double* u, long long ubs, const double* V, int j,
+                                                  Stencil5 st, double* part, int nblk, int B, int nx, int ny,
+                                                  int spmv) {
+  const size_t n = (size_t)nx * ny;
+  const int b = blockIdx.y;
+  const double* ub = u + b * ubs;
+  __shared__ double us[KR_BLK], wsh[KR_BLK];
+  __shared__ double red[8][2];
+  double gam = 0.0, dlt = 0.0;
+#pragma unroll
+  for (int k = 0; k < KR_PPT; ++k) {
+    const size_t i = (size_t)blockIdx.x * KR_BLK + threadIdx.x + 256 * k;
+    double uv = 0.0, wv = 0.0;
+    if (i < n) {
+      uv = ub[i];
+      if (spmv) {
+        const int y = (int)(i / nx), x = (int)(i - (size_t)y * nx);
+        wv = stencil_at<DIM>(ub, st, x, y, nx, ny);
+        w[(size_t)b * n + i] = wv;
+      }
+    }
+    us[threadIdx.x + 256 * k] = uv;
+    wsh[threadIdx.x + 256 * k] = wv;
+    gam = fma(uv, uv, gam);
+    dlt = fma(uv, wv, dlt);
+  }
+  // γ, δ: block sums in fixed order
+  for (int o = 16; o > 0; o >>= 1) {
+    gam += __shfl_down_sync(0xffffffffu, gam, o);
+    dlt += __shfl_down_sync(0xffffffffu, dlt, o);
+  }
+  const int wid = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  if (ln == 0) {
+    red[wid][0] = gam;
+    red[wid][1] = dlt;
+  }
+  __syncthreads();
+  double* pb = part + (size_t)b * (2 * (KRYLOV_MAX_M + 1) + 1) * nblk;
+  if (threadIdx.x < 2 && (spmv || threadIdx.x == 0)) {
+    double s2 = 0.0;
+    for (int k = 0; k < 8; ++k) s2 += red[k][threadIdx.x];
+    pb[(size_t)(2 * j + threadIdx.x) * nblk + blockIdx.x] = s2;
+  }
+  // Q_qᵀu and Q_qᵀw: one warp per column, the column chunk read once
+  const size_t i0 = (size_t)blockIdx.x * KR_BLK;
+  const int cnt = (int)min((size_t)KR_BLK, n - i0);
+  for (int q = wid; q < j; q += 8) {
+    const double* __restrict__ Vq = V + ((size_t)q * B + b) * n + i0;
+    double au = 0.0, aw = 0.0;
+#pragma unroll 8
+    for (int t = ln; t < KR_BLK; t += 32)
+      if (t < cnt) {
+        const double v = Vq[t];
+        au = fma(v, us[t], au);
+        aw = fma(v, wsh[t], aw);
+      }
+    for (int o = 16; o > 0; o >>= 1) {
+      au += __shfl_down_sync(0xffffffffu, au, o);
+      aw += __shfl_down_sync(0xffffffffu, aw, o);
+    }
+    if (ln == 0) {
+      pb[(size_t)q * nblk + blockIdx.x] = au;
+      if (spmv) pb[(size_t)(j + q) * nblk + blockIdx.x] = aw;
+    }
+  }
+}
+
+// One CTA per member: reduce the partials (one warp per slot, fixed order), then the step's small
+// algebra in parallel over the rows (j ≤ 40). j = 0: β is ‖src‖ (kw.beta). final: only the last
+// column's delayed correction H[:, m−1] += a and its subdiagonal.
+__global__ void __launch_bounds__(256) k_kr_dfinal(double* H, double* kc, double* beta0, const double* part, int nblk,
+                                                   int m, int j, int final_step) {
+  const int b = blockIdx.x;
+  const int t = threadIdx.x, wid = t >> 5, ln = t & 31;
+  __shared__ double r[2 * (KRYLOV_MAX_M + 1) + 2];
+  __shared__ double sh[4];  // β, 1/β, κ, a_{j−1}+c_v … (see below)
+  const int nslot = 2 * j + 2;
+  const double* pb = part + (size_t)b * (2 * (KRYLOV_MAX_M + 1) + 1) * nblk;
+  for (int sl = wid; sl < nslot; sl += 8) {
+    double s = 0.0;
+    if (!final_step || sl < j || sl == 2 * j)
+      for (int k = ln; k < nblk; k += 32) s += pb[(size_t)sl * nblk + k];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (ln == 0) r[sl] = s;
+  }
+  __syncthreads();
+  double* Hb = H + (size_t)b * (m + 1) * m;
+  double* kb = kc + (size_t)b * KC_STRIDE;
+  const double* a = r;
+  const double* bq = r + j;
+  // the previous column gets its delayed second projection (rows in parallel)
+  if (j > 0 && t < j) Hb[(size_t)t * m + (j - 1)] += a[t];
+  __syncthreads();
+  if (t == 0) {
+    double aa = 0.0, ab = 0.0, mx = 1.0;
+    for (int q = 0; q < j; ++q) {
+      aa = fma(a[q], a[q], aa);
+      ab = fma(a[q], bq[q], ab);
+      if (j > 0) mx = fmax(mx, fabs(Hb[(size_t)q * m + (j - 1)]));
+    }
+    const double gam = r[2 * j], dlt = r[2 * j + 1];
+    double beta = sqrt(fmax(gam - aa, 0.0));
+    if (j > 0) {
+      if (beta <= KRYLOV_BREAKDOWN * fmax(mx, beta)) beta = 0.0;  // happy breakdown
+      Hb[(size_t)j * m + (j - 1)] = beta;
+    } else {
+      beta0[b] = beta;
+    }
+    const double ib = beta > 0.0 ? 1.0 / beta : 0.0;
+    const double am1 = j > 0 ? a[j - 1] : 0.0;
+    const double cv = ib * (ib * (dlt - ab) - beta * am1);
+    sh[0] = beta;
+    sh[1] = ib;
+    sh[2] = ib * (am1 + cv);  // κ
+    sh[3] = cv;
+  }
+  __syncthreads();
+  if (final_step) return;
+  const double beta = sh[0], ib = sh[1], kap = sh[2];
+  if (t < j) {  // row t: (H a)_t over the corrected columns 0 … j−1
+    double ha = 0.0;
+    for (int c = 0; c < j; ++c) ha = fma(Hb[(size_t)t * m + c], a[c], ha);
+    const double cq = ib * (bq[t] - ha);
+    kb[t] = ib * ha + cq - kap * a[t];             // g
+    kb[(KRYLOV_MAX_M + 1) + t] = ib * a[t];        // a/β
+    Hb[(size_t)t * m + j] = beta > 0.0 ? cq : 0.0;  // column j: first projection (corrected next step)
+  }
+  if (t == 0) {
+    Hb[(size_t)j * m + j] = beta > 0.0 ? sh[3] : 0.0;
+    kb[2 * (KRYLOV_MAX_M + 1) + 0] = ib;
+    kb[2 * (KRYLOV_MAX_M + 1) + 1] = beta > 0.0 ? kap : 0.0;
+  }
+}
+
+// v_j = u·(1/β) − Σ_q (a_q/β)·Q_q;  u_next = w·(1/β) − κ·u − Σ_q g_q·Q_q  (Q read once)
+__global__ void __launch_bounds__(256) k_kr_dupdate(double* Vj, double* unext, const double* u, long long ubs,
+                                                    const double* w, const double* V, const double* kc, int j, int B,
+                                                    size_t n) {
+  const int b = blockIdx.y;
+  __shared__ double gs[KRYLOV_MAX_M + 1], as_[KRYLOV_MAX_M + 1];
+  __shared__ double sc[2];
+  const double* kb = kc + (size_t)b * KC_STRIDE;
+  if (threadIdx.x < j) {
+    gs[threadIdx.x] = kb[threadIdx.x];
+    as_[threadIdx.x] = kb[(KRYLOV_MAX_M + 1) + threadIdx.x];
+  }
+  if (threadIdx.x < 2) sc[threadIdx.x] = kb[2 * (KRYLOV_MAX_M + 1) + threadIdx.x];
+  __syncthreads();
+  const double ib = sc[0], kap = sc[1];
+  double vv[KR_PPT], uu[KR_PPT];
+#pragma unroll
+  for (int k = 0; k < KR_PPT; ++k) {
+    const size_t i = (size_t)blockIdx.x * KR_BLK + threadIdx.x + 256 * k;
+    const double ui = i < n ? u[b * ubs + i] : 0.0;
+    const double wi = i < n ? w[(size_t)b * n + i] : 0.0;
+    vv[k] = ib * ui;
+    uu[k] = fma(-kap, ui, ib * wi);
+  }
+#pragma unroll 4
+  for (int q = 0; q < j; ++q) {
+    const double gq = gs[q], aq = as_[q];
+    const double* __restrict__ Vq = V + ((size_t)q * B + b) * n;
+#pragma unroll
+    for (int k = 0; k < KR_PPT; ++k) {
+      const size_t i = (size_t)blockIdx.x * KR_BLK + threadIdx.x + 256 * k;
+      if (i < n) {
+        const double v = Vq[i];
+        vv[k] = fma(-aq, v, vv[k]);
+        uu[k] = fma(-gq, v, uu[k]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KR_PPT; ++k) {
+    const size_t i = (size_t)blockIdx.x * KR_BLK + threadIdx.x + 256 * k;
+    if (i < n) {
+      Vj[(size_t)b * n + i] = vv[k];
+      unext[(size_t)b * n + i] = uu[k];
+    }
+  }
+}
+
 inline int krylov_action(KrylovWork& kw, double tau, int substeps, int m, const Stencil5& st,
                          const double* src, long long src_bs, const double* addend, long long add_bs,
                          double* pacc, double* const* ACC, int B, int nx, int ny, int dim,
-                         double** result, cudaStream_t s, px_stats* stats) {
+                         double** result, cudaStream_t s, px_stats* stats, int ortho = 1) {
   const size_t n = kw.n;
   const dim3 g(kw.nblk, B);
   const long long nb = (long long)n;
   uint64_t launches = 0;
   for (int sub = 0; sub < substeps; ++sub) {
     double* out = (src == ACC[0]) ? ACC[1] : ACC[0];
+    if (ortho == 1) {  // delayed reorthogonalization: 3 launches and two basis passes per step
+      cudaMemsetAsync(kw.H, 0, sizeof(double) * B * (m + 1) * m, s);
+      const double* u = src;
+      long long ubs = src_bs;
+      for (int j = 0; j < m; ++j) {
+        if (dim == 2)
+          k_kr_ddots<2><<<g, 256, 0, s>>>(kw.w, u, ubs, kw.V, j, st, kw.part, kw.nblk, B, nx, ny, 1);
+        else
+          k_kr_ddots<1><<<g, 256, 0, s>>>(kw.w, u, ubs, kw.V, j, st, kw.part, kw.nblk, B, nx, ny, 1);
+        k_kr_dfinal<<<B, 256, 0, s>>>(kw.H, kw.kc, kw.beta, kw.part, kw.nblk, m, j, 0);
+        double* un = kw.u + (size_t)(j & 1) * B * n;
+        k_kr_dupdate<<<g, 256, 0, s>>>(kw.V + (size_t)j * B * n, un, u, ubs, kw.w, kw.V, kw.kc, j, B, n);
+        u = un;
+        ubs = nb;
+        launches += 3;
+      }
+      // the delayed second projection of the last candidate completes H's last column
+      if (dim == 2)
+        k_kr_ddots<2><<<g, 256, 0, s>>>(kw.w, u, ubs, kw.V, m, st, kw.part, kw.nblk, B, nx, ny, 0);
+      else
+        k_kr_ddots<1><<<g, 256, 0, s>>>(kw.w, u, ubs, kw.V, m, st, kw.part, kw.nblk, B, nx, ny, 0);
+      k_kr_dfinal<<<B, 256, 0, s>>>(kw.H, kw.kc, kw.beta, kw.part, kw.nblk, m, m, 1);
+      const int N = m + 1;
+      const size_t smem = 3 * (size_t)N * N * sizeof(double);
+      k_kr_expm<<<B, 256, smem, s>>>(kw.coef, kw.H, kw.beta, m, tau);
+      k_kr_combine<<<dim3((unsigned)((n + 255) / 256), B), 256, 0, s>>>(
+          out, kw.V, kw.coef, m, B, n, sub == substeps - 1 ? addend : nullptr, add_bs, pacc);
+      launches += 4;
+      src = out;
+      src_bs = nb;
+      continue;
+    }
     k_kr_sumsq<<<g, 256, 0, s>>>(kw.part, kw.nblk, src, src_bs, n);
     k_kr_beta<<<B, 256, 0, s>>>(kw.beta, kw.part, kw.nblk);
     k_kr_v0<<<dim3((unsigned)((n + 255) / 256), B), 256, 0, s>>>(kw.V, src, src_bs, kw.beta, n);
@@ -409,7 +641,9 @@ inline int krylov_action(KrylovWork& kw, double tau, int substeps, int m, const 
     stats->kernel_launches += launches;
     stats->arnoldi_steps += (uint64_t)substeps * m * B;
     stats->exp_terms += (uint64_t)substeps * m * B;
-    // Arnoldi step j (CGS2): SpMV in/out 16n + 2 passes × (read V_0..V_j twice) ≈ 16n + 32n(j+1)
+    // Arnoldi step j (SURVEY §8(d)'s CGS unit, kept as the model for both forms): SpMV in/out
+    // 16n + read V_0..V_j for the dots and again for the update, twice (CGS2) ≈ 16n + 32n(j+1);
+    // the delayed form moves ≈ 16n + 16n·j + 40n of it
     double bytes = 0.0;
     for (int j = 0; j < m; ++j) bytes += 16.0 * n + 32.0 * n * (j + 1);
     bytes += 8.0 * n * (m + 2);  // combine (+ pacc)

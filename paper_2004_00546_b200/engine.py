@@ -92,7 +92,8 @@ class EngineSpec:
 # developer overrides of the kernel variants (tools/ experiments); tests use EngineSpec.variants
 ENV_VARIANTS = {"PX_MARCH2": "march2", "PX_M2_COLS": "march_cols", "PX_M2_BAND": "march_band",
                 "PX_CM_TERMS": "cheb_terms", "PX_CM_TERMS_PHI": "cheb_terms_phi", "PX_CM_STRIP": "cheb_strip", "PX_CM_BAND": "cheb_band",
-                "PX_SCAN1D_CLUSTER": "scan1d_cluster", "PX_BURGERS_CLUSTER": "burgers_cluster"}
+                "PX_SCAN1D_CLUSTER": "scan1d_cluster", "PX_BURGERS_CLUSTER": "burgers_cluster",
+                "PX_KRYLOV_ORTHO": "krylov_ortho"}
 
 
 def allreduce_sum(tensors, group=None, stream=None) -> None:

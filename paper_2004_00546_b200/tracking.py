@@ -107,7 +107,11 @@ class HybridTrackingEngine:
                 "overlapped": bool(ms[4])}
 
     def set_inputs(self, u0, f, target, qdag_T=None, stream: int | None = None) -> None:
+        """Host arrays, or a CUDA torch tensor ``target`` (then every input goes device to
+        device: the (S+1)·n target is the large one)."""
         B, n = self.B, self.n
+        if getattr(target, "is_cuda", False):
+            return self._set_inputs_device(u0, f, target, qdag_T, stream)
         u0 = np.ascontiguousarray(np.broadcast_to(np.asarray(u0, dtype=np.float64).reshape(-1, n), (B, n)))
         f = np.ascontiguousarray(np.broadcast_to(np.asarray(f, dtype=np.float64).reshape(-1, n), (B, n)))
         tshape = (self.S + 1, B, n) if self.target_batched else (self.S + 1, n)
@@ -121,6 +125,22 @@ class HybridTrackingEngine:
             self.h, u0.ctypes.data_as(ctypes.c_void_p), f.ctypes.data_as(ctypes.c_void_p),
             target.ctypes.data_as(ctypes.c_void_p), q.ctypes.data_as(ctypes.c_void_p) if q is not None else None,
             N.PX_MEM_HOST, ctypes.c_void_p(s)))
+
+    def _set_inputs_device(self, u0, f, target, qdag_T, stream) -> None:
+        import torch
+        B, n = self.B, self.n
+        dev = target.device
+        as_dev = lambda a: torch.as_tensor(np.ascontiguousarray(np.broadcast_to(
+            np.asarray(a, dtype=np.float64).reshape(-1, n), (B, n))), device=dev)
+        tshape = (self.S + 1, B, n) if self.target_batched else (self.S + 1, n)
+        tg = target.to(torch.float64).reshape(tshape).contiguous()
+        u, ff = as_dev(u0), as_dev(f)
+        q = as_dev(qdag_T) if qdag_T is not None else None
+        self._keep = (u, ff, tg, q)
+        s = current_stream_handle() if stream is None else stream
+        ptr = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None
+        self._chk(self.lib.px_hybrid_set_inputs(self.h, ptr(u), ptr(ff), ptr(tg), ptr(q), N.PX_MEM_DEVICE,
+                                                ctypes.c_void_p(s)))
 
     def direct(self, overlap: bool = True, stream: int | None = None) -> None:
         s = current_stream_handle() if stream is None else stream
@@ -222,10 +242,11 @@ def solve_hybrid_tracking(system: System, u0, f, target, plan: HybridPlan | None
     B = f.shape[0]
     offs, part = _offsets_for(system, plan, N, rk)
     S = int(offs[-1])
-    target = np.asarray(target, dtype=np.float64)
-    if target.shape == (S + 1, system.n):
+    if not getattr(target, "is_cuda", False):
+        target = np.asarray(target, dtype=np.float64)
+    if tuple(target.shape) == (S + 1, system.n):
         batched = False
-    elif target.shape == (S + 1, B, system.n):
+    elif tuple(target.shape) == (S + 1, B, system.n):
         batched = True
     else:
         raise ValueError(f"target must be given on the {S + 1} nodes of the sweep: (S+1, n) or (S+1, B, n)")

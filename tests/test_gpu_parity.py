@@ -188,12 +188,29 @@ def test_config3_burgers_full():
     _check(loop, ref)
 
 
-def test_config4_krylov_scaled():
+@pytest.mark.parametrize("ortho", [1, 0])
+def test_config4_krylov_scaled(ortho):
     """Krylov path: by default the carries run as 4 concurrent local blocks (in-GPU
-    block-scan, `px_set_local_blocks`) — equal to the oracle's 4-block block-scan."""
-    from paper_2004_00546_b200 import baseline, scaled
+    block-scan, `px_set_local_blocks`) — equal to the oracle's 4-block block-scan (CGS2), with
+    the delayed reorthogonalisation (default, two basis passes per Arnoldi step) and with CGS2."""
+    import ctypes
+
+    from paper_2004_00546_b200 import RK4Config, baseline, scaled
+    from paper_2004_00546_b200.engine import EngineSpec, ParaexpEngine
     c = scaled(baseline(4), nx=96, P=12, steps_per_slice=5, K=16)
-    _check(_gpu_linear(c), _oracle_linear(c, world=4))
+    eng = ParaexpEngine(EngineSpec(c.system, c.P, c.dt, c.expaction, c.batch, variants=(("krylov_ortho", ortho),)))
+    assert eng.variant("krylov_ortho") == ortho and eng.local_blocks == 4
+    u0, ut, ctrl = c.inputs()
+    eng.set_inputs(u0, ut, ctrl)
+    eng.gradient()
+    r = eng.results()
+    ref = _oracle_linear(c, world=4)
+    assert rel_l2(r["uT"], ref.uT) <= 1e-10 and rel_l2(r["qdag0"], ref.qdag0) <= 1e-10
+    assert rel_l2(r["G"], ref.G) <= 1e-10 and rel_l2(r["grad"], ref.grad) <= 1e-8
+    assert np.max(np.abs(r["J"] - ref.J) / np.abs(ref.J)) <= 1e-10
+    eng.close()
+    if ortho == 1:
+        _check(_gpu_linear(c), ref)   # the public API runs the default
 
 
 @pytest.mark.parametrize("blocks", [1, 3])

@@ -26,7 +26,8 @@ def main():
     rk, cfg, law = RK4Config(5e-4), ChebyshevConfig(tol=1e-12), TimeLaw.sine(2 * np.pi)
     u0 = 0.5 * np.sin(x) + 0.05 * np.cos(3 * x)
     f = 0.3 * np.cos(2 * x) + 0.2 * np.sin(3 * x)
-    target = synthesize_trajectory(sysm, 0.5 * np.sin(x) + 0.1 * np.cos(2 * x), rk, law)[:, 0, :]
+    target_host = synthesize_trajectory(sysm, 0.5 * np.sin(x) + 0.1 * np.cos(2 * x), rk, law)[:, 0, :]
+    target = torch.as_tensor(target_host, device="cuda")   # resident target: the timed solve moves no 33 MB H2D
     k = estimate_k(sysm, 0.05, rk, repeats=3, law=law)
     print(json.dumps({"estimate_k": k}), flush=True)
     for name, plan in (("equidistant", None), ("geometric_k", make_hybrid_plan(1.0, 64, max(k, 0.5) * 40.0)),
