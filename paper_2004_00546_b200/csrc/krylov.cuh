@@ -21,6 +21,7 @@
 namespace px {
 
 constexpr double KRYLOV_BREAKDOWN = 1e-13;
+constexpr int KR_EXPM_MATS = 12;  // N×N matrices in k_kr_expm's shared memory (A … A⁶, 3 blocks, E, T)
 #ifndef PX_KR_PPT
 #define PX_KR_PPT 4
 #endif
@@ -307,22 +308,51 @@ __device__ void expm_aug_block(double* coef, const double* Hb, double bt, int m,
   __syncthreads();
   const int sq = s_sq;
   const double scale = ldexp(1.0, -sq);
-  for (int idx = threadIdx.x; idx < Ne * Ne; idx += blockDim.x) {
-    Aa[idx] *= scale;
-    E[idx] = (idx / Ne == idx % Ne) ? 1.0 : 0.0;
-  }
+  const int NN = Ne * Ne;
+  for (int idx = threadIdx.x; idx < NN; idx += blockDim.x) Aa[idx] *= scale;
   __syncthreads();
-  for (int k = 18; k >= 1; --k) {
-    for (int idx = threadIdx.x; idx < Ne * Ne; idx += blockDim.x) {
+  // Taylor degree 18 by Paterson–Stockmeyer: p(A) = B0 + A⁶(B1 + A⁶(B2 + A⁶/18!)),
+  // B_i = Σ_{l<6} A^l/(6i+l)!  — 7 matrix products instead of 18 (same polynomial)
+  double* P[7];  // P[l] = A^l, l = 1 … 6
+  P[1] = Aa;
+  for (int l = 2; l <= 6; ++l) P[l] = sm + (size_t)(l + 1) * N * N;  // slots 3 … 8 (E, T: slots 1, 2)
+  auto mul = [&](double* C, const double* X, const double* Y) {
+    for (int idx = threadIdx.x; idx < NN; idx += blockDim.x) {
       const int r = idx / Ne, c = idx - r * Ne;
-      double s = 0.0;
-      for (int q = 0; q < Ne; ++q) s += Aa[r * Ne + q] * E[q * Ne + c];
-      T[idx] = ((r == c) ? 1.0 : 0.0) + s / k;
+      double acc = 0.0;
+      for (int q = 0; q < Ne; ++q) acc = fma(X[r * Ne + q], Y[q * Ne + c], acc);
+      C[idx] = acc;
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < Ne * Ne; idx += blockDim.x) E[idx] = T[idx];
+  };
+  mul(P[2], P[1], P[1]);
+  mul(P[3], P[2], P[1]);
+  mul(P[4], P[2], P[2]);
+  mul(P[5], P[4], P[1]);
+  mul(P[6], P[3], P[3]);
+  double* Bs[3] = {sm + 9 * (size_t)N * N, sm + 10 * (size_t)N * N, sm + 11 * (size_t)N * N};
+  {
+    double inv_fact[19];
+    inv_fact[0] = 1.0;
+    for (int k = 1; k <= 18; ++k) inv_fact[k] = inv_fact[k - 1] / k;
+    for (int idx = threadIdx.x; idx < NN; idx += blockDim.x) {
+      const double id = (idx / Ne == idx % Ne) ? 1.0 : 0.0;
+      for (int i = 0; i < 3; ++i) {
+        double v = inv_fact[6 * i] * id;
+        for (int l = 1; l < 6; ++l) v = fma(inv_fact[6 * i + l], P[l][idx], v);
+        Bs[i][idx] = v;
+      }
+      // X = B2 + A⁶/18!
+      Bs[2][idx] = fma(inv_fact[18], P[6][idx], Bs[2][idx]);
+    }
     __syncthreads();
   }
+  mul(T, P[6], Bs[2]);  // A⁶·X
+  for (int idx = threadIdx.x; idx < NN; idx += blockDim.x) Bs[1][idx] += T[idx];  // Y = B1 + A⁶X
+  __syncthreads();
+  mul(T, P[6], Bs[1]);  // A⁶·Y
+  for (int idx = threadIdx.x; idx < NN; idx += blockDim.x) E[idx] = Bs[0][idx] + T[idx];
+  __syncthreads();
   for (int it = 0; it < sq; ++it) {
     for (int idx = threadIdx.x; idx < Ne * Ne; idx += blockDim.x) {
       const int r = idx / Ne, c = idx - r * Ne;
@@ -463,27 +493,47 @@ __global__ void __launch_bounds__(256) k_kr_dfinal(double* H, double* kc, double
   __shared__ double sh[4];  // β, 1/β, κ, a_{j−1}+c_v … (see below)
   const int nslot = 2 * j + 2;
   const double* pb = part + (size_t)b * (2 * (KRYLOV_MAX_M + 1) + 1) * nblk;
-  for (int sl = wid; sl < nslot; sl += 8) {
+  // four threads per slot, each over a quarter of the block partials (independent loads in
+  // flight), combined in a fixed order
+  for (int base = 0; base < nslot; base += 64) {
+    const int sl = base + (t >> 2), sub = t & 3;
     double s = 0.0;
-    if (!final_step || sl < j || sl == 2 * j)
-      for (int k = ln; k < nblk; k += 32) s += pb[(size_t)sl * nblk + k];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-    if (ln == 0) r[sl] = s;
+    if (sl < nslot && (!final_step || sl < j || sl == 2 * j)) {
+      const double* src = pb + (size_t)sl * nblk;
+#pragma unroll 16
+      for (int k = sub; k < nblk; k += 4) s += src[k];
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (sub == 0 && sl < nslot) r[sl] = s;
   }
+  (void)wid;
+  (void)ln;
   __syncthreads();
   double* Hb = H + (size_t)b * (m + 1) * m;
   double* kb = kc + (size_t)b * KC_STRIDE;
   const double* a = r;
   const double* bq = r + j;
+  // H's leading j×j block in shared memory (one parallel load; every later access is on chip)
+  __shared__ double Hs[KRYLOV_MAX_M * KRYLOV_MAX_M];
+  for (int idx = t; idx < j * j; idx += blockDim.x) {
+    const int q = idx / j, c = idx - q * j;
+    Hs[idx] = Hb[(size_t)q * m + c];
+  }
+  __syncthreads();
   // the previous column gets its delayed second projection (rows in parallel)
-  if (j > 0 && t < j) Hb[(size_t)t * m + (j - 1)] += a[t];
+  if (j > 0 && t < j) {
+    const double v = Hs[t * j + (j - 1)] + a[t];
+    Hs[t * j + (j - 1)] = v;
+    Hb[(size_t)t * m + (j - 1)] = v;
+  }
   __syncthreads();
   if (t == 0) {
     double aa = 0.0, ab = 0.0, mx = 1.0;
     for (int q = 0; q < j; ++q) {
       aa = fma(a[q], a[q], aa);
       ab = fma(a[q], bq[q], ab);
-      if (j > 0) mx = fmax(mx, fabs(Hb[(size_t)q * m + (j - 1)]));
+      mx = fmax(mx, fabs(Hs[q * j + (j - 1)]));
     }
     const double gam = r[2 * j], dlt = r[2 * j + 1];
     double beta = sqrt(fmax(gam - aa, 0.0));
@@ -506,7 +556,7 @@ __global__ void __launch_bounds__(256) k_kr_dfinal(double* H, double* kc, double
   const double beta = sh[0], ib = sh[1], kap = sh[2];
   if (t < j) {  // row t: (H a)_t over the corrected columns 0 … j−1
     double ha = 0.0;
-    for (int c = 0; c < j; ++c) ha = fma(Hb[(size_t)t * m + c], a[c], ha);
+    for (int c = 0; c < j; ++c) ha = fma(Hs[t * j + c], a[c], ha);
     const double cq = ib * (bq[t] - ha);
     kb[t] = ib * ha + cq - kap * a[t];             // g
     kb[(KRYLOV_MAX_M + 1) + t] = ib * a[t];        // a/β
@@ -600,7 +650,8 @@ inline int krylov_action(KrylovWork& kw, double tau, int substeps, int m, const 
         k_kr_ddots<1><<<g, 256, 0, s>>>(kw.w, u, ubs, kw.V, m, st, kw.part, kw.nblk, B, nx, ny, 0);
       k_kr_dfinal<<<B, 256, 0, s>>>(kw.H, kw.kc, kw.beta, kw.part, kw.nblk, m, m, 1);
       const int N = m + 1;
-      const size_t smem = 3 * (size_t)N * N * sizeof(double);
+      const size_t smem = KR_EXPM_MATS * (size_t)N * N * sizeof(double);
+      cudaFuncSetAttribute(k_kr_expm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       k_kr_expm<<<B, 256, smem, s>>>(kw.coef, kw.H, kw.beta, m, tau);
       k_kr_combine<<<dim3((unsigned)((n + 255) / 256), B), 256, 0, s>>>(
           out, kw.V, kw.coef, m, B, n, sub == substeps - 1 ? addend : nullptr, add_bs, pacc);
@@ -629,7 +680,8 @@ inline int krylov_action(KrylovWork& kw, double tau, int substeps, int m, const 
       launches += 6;
     }
     const int N = m + 1;
-    const size_t smem = 3 * (size_t)N * N * sizeof(double);
+    const size_t smem = KR_EXPM_MATS * (size_t)N * N * sizeof(double);
+    cudaFuncSetAttribute(k_kr_expm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_kr_expm<<<B, 256, smem, s>>>(kw.coef, kw.H, kw.beta, m, tau);
     k_kr_combine<<<dim3((unsigned)((n + 255) / 256), B), 256, 0, s>>>(
         out, kw.V, kw.coef, m, B, n, sub == substeps - 1 ? addend : nullptr, add_bs, pacc);
