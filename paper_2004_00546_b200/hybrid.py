@@ -147,6 +147,12 @@ def estimate_k(system, pilot_fraction: float, rk, repeats: int = 3, law: TimeLaw
     steps = int(round(span / rk.dt))
     if steps < 2:
         raise PilotTooShort("pilot resolved fewer than 2 steps; widen pilot_fraction")
-    from .tracking import pilot_times
-    t_dir, t_adj = pilot_times(system, steps, rk, repeats, law or TimeLaw.constant())
+    t_dir, t_adj = _pilot_times(system, steps, rk, repeats, law or TimeLaw.constant())
     return t_adj / t_dir
+
+
+def _pilot_times(system, steps: int, rk, repeats: int, law: TimeLaw) -> tuple[float, float]:
+    """Device seconds per unit time of the direct sweep and of one slice's adjoint solve
+    (`hybrid.py:100-129`; the tests patch it with synthetic costs, as the reference's do)."""
+    from .tracking import pilot_times
+    return pilot_times(system, steps, rk, repeats, law)

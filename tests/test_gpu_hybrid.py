@@ -143,7 +143,7 @@ def test_tracking_loop_api_and_estimate_k(cuda_ok):
     o = _oracle(sysm, u0, f[:1], target, np.array([0, int(round(sysm.spec.T / rk.dt))]), law, cfg)
     assert ser.J == pytest.approx(float(o.J[0]), rel=1e-10) and rel_l2(ser.grad, o.grad[0]) <= 1e-8
     k = estimate_k(sysm, 0.1, rk, repeats=2, law=law)
-    assert 0.05 < k < 100.0
+    assert k > 1.0   # the adjoint slice step costs more than a direct step (test_hybrid.py:102-105)
 
 
 def test_reference_binding_on_the_gpu(cuda_ok):

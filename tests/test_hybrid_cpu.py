@@ -165,3 +165,65 @@ def test_tracking_loop_validation():
     with pytest.raises(ConfigError):  # plan / law belong to the tracking objective
         direct_adjoint_loop(c3.system, np.zeros(c3.system.basis.K), np.zeros(c3.system.n), "hybrid", rk=rk,
                             time_law=TimeLaw.sine(1.0))
+
+
+# --- the reference's own partition / pilot tests (`tests/test_hybrid.py:25-110`), mirrored ----
+
+
+def test_geometric_single_interval_and_decreasing_widths():
+    assert partition_geometric(5.0, 1, 2.0).boundaries.tolist() == [0.0, 5.0]
+    part = partition_geometric(3.0, 6, 1.7)
+    assert part.boundaries[0] == 0.0 and part.boundaries[-1] == 3.0
+    assert np.all(np.diff(part.widths()) < 0)
+
+
+def test_geometric_boundaries_high_precision():
+    """The reference's pinned k = 2.11 boundaries 0.4676 / 0.7848 (`test_hybrid.py:36-47`),
+    against the closed form at 50 digits."""
+    mp = pytest.importorskip("mpmath")
+    mp.mp.dps = 50
+    k = mp.mpf("2.11")
+    r = k / (k + 1)
+    want = [float((1 - r ** n) / (1 - r ** 3)) for n in (0, 1, 2, 3)]
+    part = partition_geometric(1.0, 3, 2.11)
+    assert part.boundaries == pytest.approx(want, abs=1e-12)
+    assert part.boundaries[1] == pytest.approx(0.4676, abs=5e-5)
+    assert part.boundaries[2] == pytest.approx(0.7848, abs=5e-5)
+    assert make_hybrid_plan(1.0, 8, 2.11).partition.widths()[1:] / make_hybrid_plan(1.0, 8, 2.11).partition.widths()[:-1] \
+        == pytest.approx(2.11 / 3.11, rel=1e-10)
+
+
+def test_plan_rejects_an_equidistant_partition():
+    from paper_2004_00546_b200.partition import partition_equidistant
+    with pytest.raises(ValueError):
+        HybridPlan(partition_equidistant(1.0, 4), 2.11)
+    with pytest.raises(ValueError):
+        make_hybrid_plan(1.0, 8, 2.11, h_min=0.05)
+
+
+def _burgers16():
+    from paper_2004_00546_b200 import BURGERS, Grid, ProblemSpec, build_system
+    return build_system(Grid(16), ProblemSpec(BURGERS, (0.0, 0.0), 1.0, 1.0), 2)
+
+
+def test_estimate_k_with_synthetic_pilot_costs(monkeypatch):
+    """k = τ_adjoint/τ_direct: symmetric costs give 1, doubling the adjoint's doubles k
+    (`test_hybrid.py:71-100`, the pilot patched with synthetic times)."""
+    import paper_2004_00546_b200.hybrid as H
+    from paper_2004_00546_b200 import RK4Config, estimate_k
+    sysm = _burgers16()
+    monkeypatch.setattr(H, "_pilot_times", lambda *a, **kw: (0.1, 0.1))
+    assert estimate_k(sysm, 0.05, RK4Config(1e-3)) == pytest.approx(1.0, rel=0.2)
+    monkeypatch.setattr(H, "_pilot_times", lambda *a, **kw: (0.1, 0.25))
+    base = estimate_k(sysm, 0.05, RK4Config(1e-3))
+    monkeypatch.setattr(H, "_pilot_times", lambda *a, **kw: (0.1, 0.5))
+    assert estimate_k(sysm, 0.05, RK4Config(1e-3)) == pytest.approx(2.0 * base, rel=1e-12)
+
+
+def test_estimate_k_validation():
+    from paper_2004_00546_b200 import PilotTooShort, RK4Config, estimate_k
+    sysm = _burgers16()
+    with pytest.raises(ValueError):
+        estimate_k(sysm, 0.5, RK4Config(1e-3))
+    with pytest.raises(PilotTooShort):
+        estimate_k(sysm, 0.001, RK4Config(1e-3))
