@@ -62,18 +62,27 @@ __global__ void __launch_bounds__(HYB_NT) k_hyb_direct(HybArgs a) {
     f[k] = act ? a.f[(size_t)b * n + i0 + k] : 0.0;
   }
   double jacc = 0.0;
+  // the target row of the node a step is about to produce is loaded one step ahead, so its
+  // latency overlaps the step's four stages instead of stalling the sweep at every node
+  double tnext[PPT];
+  auto load_target = [&](int s) {
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) tnext[k] = (act && s <= a.S) ? __ldg(tg + (size_t)s * tstride + i0 + k) : 0.0;
+  };
   auto node = [&](int s, double w) {
     if (!act) return;
     double e = 0.0;
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
       a.traj[(size_t)s * ns + (size_t)b * n + i0 + k] = u[k];
-      const double d = u[k] - tg[(size_t)s * tstride + i0 + k];
+      const double d = u[k] - tnext[k];
       e = fma(d, d, e);
     }
     jacc = fma(w, e, jacc);
   };
+  load_target(0);
   node(0, 0.5);
+  load_target(1);
   int par = 0;
   // k = −y∘Dx y + D·L y + θ·f (problems.py:177-185, V ≡ 0)
   auto rhs = [&](const double* y, double th, double* k) {
@@ -104,6 +113,7 @@ __global__ void __launch_bounds__(HYB_NT) k_hyb_direct(HybArgs a) {
 #pragma unroll
     for (int q = 0; q < PPT; ++q) u[q] = fma(a.h / 6.0, acc[q] + k[q], u[q]);
     node(s + 1, s + 1 == a.S ? 0.5 : 1.0);
+    load_target(s + 2);
     if (s + 1 == next) {
       // slice p's nodes are stored: publish (every writer fences, then one release flag)
       __threadfence();
@@ -159,6 +169,11 @@ __global__ void __launch_bounds__(256) k_hyb_direct_cluster(HybArgs a) {
     f[k] = act ? a.f[(size_t)b * n + gidx(k)] : 0.0;
     u[k] = act ? a.u0[(size_t)b * n + gidx(k)] : 0.0;
   }
+  double tnext[PPT];  // the next node's target row, loaded a step ahead (see k_hyb_direct)
+  auto load_target = [&](int s) {
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) tnext[k] = (owned && s <= a.S) ? __ldg(tg + (size_t)s * tstride + gidx(k)) : 0.0;
+  };
   auto node = [&](int s, double w) {
     if (!owned) return;
     double e = 0.0;
@@ -166,12 +181,14 @@ __global__ void __launch_bounds__(256) k_hyb_direct_cluster(HybArgs a) {
     for (int k = 0; k < PPT; ++k) {
       const int i = gidx(k);
       a.traj[(size_t)s * ns + (size_t)b * n + i] = u[k];
-      const double d = u[k] - tg[(size_t)s * tstride + i];
+      const double d = u[k] - tnext[k];
       e = fma(d, d, e);
     }
     jacc = fma(w, e, jacc);
   };
+  load_target(0);
   node(0, 0.5);
+  load_target(1);
   int par = 0, xpar = 0;
   auto rhs = [&](double th, double* k_out) {
     if (act) {
@@ -214,12 +231,18 @@ __global__ void __launch_bounds__(256) k_hyb_direct_cluster(HybArgs a) {
   };
   int valid = STEPS_PER_REFRESH;
   int p = 0, next = a.offsets[1];
+  double n1 = hyb_theta(a, 0), n2 = hyb_theta(a, 1), n4 = hyb_theta(a, 2);  // θ of the next step
   for (int st = 0; st < a.S; ++st) {
     if (valid == 0) {
       refresh();
       valid = STEPS_PER_REFRESH;
     }
-    const double th1 = hyb_theta(a, 2 * st), th2 = hyb_theta(a, 2 * st + 1), th4 = hyb_theta(a, 2 * st + 2);
+    const double th1 = n1, th2 = n2, th4 = n4;
+    if (st + 1 < a.S) {
+      n1 = hyb_theta(a, 2 * st + 2);
+      n2 = hyb_theta(a, 2 * st + 3);
+      n4 = hyb_theta(a, 2 * st + 4);
+    }
 #pragma unroll
     for (int k = 0; k < PPT; ++k) x[k] = u[k];
     rhs(th1, kk);
@@ -236,6 +259,7 @@ __global__ void __launch_bounds__(256) k_hyb_direct_cluster(HybArgs a) {
     for (int k = 0; k < PPT; ++k) u[k] = fma(h6, acc[k] + kk[k], u[k]);
     --valid;
     node(st + 1, st + 1 == a.S ? 0.5 : 1.0);
+    load_target(st + 2);
     if (st + 1 == next) {
       __threadfence();
       cluster.sync();
@@ -316,11 +340,27 @@ __global__ void __launch_bounds__(HYB_NT) k_hyb_lanes(HybArgs a) {
     }
   };
   const double h = a.h, hh = 0.5 * a.h, h6 = a.h / 6.0;
+  // the next node row and its target values are fetched one step ahead (registers), so their
+  // latency overlaps the current step's stages
+  double rnext[PPT], tnext[PPT];
+  auto prefetch = [&](int node) {
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const int j = t + q * HYB_NT;
+      rnext[q] = (j < n) ? __ldcg(nb + (size_t)node * ns + j) : 0.0;
+      tnext[q] = act ? __ldg(tg + (size_t)node * tstride + i0 + q) : 0.0;
+    }
+  };
+  prefetch(o1 - 1);
   for (int it = 0; it < o1 - o0; ++it) {
     const int top = o1 - it;
-    for (int j = t; j < n; j += HYB_NT) ub[j] = __ldcg(nb + (size_t)(top - 1) * ns + j);
 #pragma unroll
-    for (int q = 0; q < PPT; ++q) tgb[q] = act ? tg[(size_t)(top - 1) * tstride + i0 + q] : 0.0;
+    for (int q = 0; q < PPT; ++q) {
+      const int j = t + q * HYB_NT;
+      if (j < n) ub[j] = rnext[q];
+      tgb[q] = tnext[q];
+    }
+    if (top - 2 >= o0) prefetch(top - 2);
     __syncthreads();
     const double tha = hyb_theta(a, 2 * top), thm = hyb_theta(a, 2 * top - 1), thb = hyb_theta(a, 2 * top - 2);
     double sa[PPT], sm[PPT], sb[PPT];
