@@ -185,6 +185,10 @@ int px_get_variant(void* handle, int key, int* value);
  * (Krylov, small fields). 1 = the sequential scan (default). Replaces: the reference's
  * per-worker chains running concurrently (`workers.py:298-346`). */
 int px_set_local_blocks(void* handle, int blocks);
+/* Local blocks of unequal sizes (slice order, summing to the rank's slices) for the direct sweep;
+ * the adjoint uses the mirrored partition. The long-span plan in slot PX_PLAN_BLOCK_LONG + k − 1
+ * must then cover the last k direct blocks (= the first k adjoint blocks). */
+int px_set_local_block_sizes(void* handle, int blocks, const int* sizes);
 
 /* Burgers adjoint formulation. PX_ADJOINT_ABSORBED (default): the final condition is absorbed
  * into the inhomogeneous solves, exact Jᵀ(u(t)) there and frozen J(ū_p)ᵀ in the carry

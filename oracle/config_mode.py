@@ -224,9 +224,23 @@ def _as_batch(a, n):
     return a.reshape(-1, n) if a.ndim > 1 else a[None, :]
 
 
+def _block_bounds(P, world, sizes=None, mirrored=False):
+    """Contiguous slice blocks: `rank_block` (equal) or explicit sizes; the adjoint of the GPU's
+    local blocks uses the mirrored partition (engine._block_sizes)."""
+    if sizes is None:
+        return [rank_block(P, r, world) for r in range(world)]
+    sz = list(sizes)[::-1] if mirrored else list(sizes)
+    out, q = [], 0
+    for s_ in sz:
+        out.append((q, q + s_))
+        q += s_
+    return out
+
+
 def linear_gradient(grid_nx, grid_ny, A, basis, T, P, nsteps, u0, u_target, ctrl,
                     plan_slice, plan_long_direct=None, plan_long_adjoint=None,
-                    formulation: str = "scan", world: int = 1, want_boundary=False, qdag_T=None):
+                    formulation: str = "scan", world: int = 1, want_boundary=False, qdag_T=None,
+                    block_sizes=None):
     """One Paraexp direct-adjoint gradient for the linear testbed (App. B of SURVEY).
 
     ``A`` stencil tuple; ``basis`` ModeBasis; ``ctrl`` (B, K). ``plan_long_*``:
@@ -276,8 +290,7 @@ def linear_gradient(grid_nx, grid_ny, A, basis, T, P, nsteps, u0, u_target, ctrl
         uT = u0 + D
     else:  # blockscan over `world` contiguous blocks, summed as an allreduce would
         partial = np.zeros_like(v_end)
-        for r in range(world):
-            p0, p1 = rank_block(P, r, world)
+        for p0, p1 in _block_bounds(P, world, block_sizes):
             D = np.zeros_like(v_end)
             for p in range(p0, p1):
                 D = v_end.copy() if p == p0 else exp_action(applyA, plan_slice, D) + v_end
@@ -315,8 +328,7 @@ def linear_gradient(grid_nx, grid_ny, A, basis, T, P, nsteps, u0, u_target, ctrl
     else:
         qd = np.zeros_like(w_end)
         Gh = np.zeros_like(w_end)
-        for r in range(world):
-            p0, p1 = rank_block(P, r, world)
+        for p0, p1 in _block_bounds(P, world, block_sizes, mirrored=True):
             C = np.zeros_like(w_end)
             Gr = np.zeros_like(w_end)
             for p in range(p1 - 1, p0 - 1, -1):

@@ -128,6 +128,7 @@ SIGNATURES = {
     "px_set_cheb_plan_law": (c_int, [c_void_p, c_int, POINTER(c_double), POINTER(c_double)]),
     "px_set_time_law": (c_int, [c_void_p, POINTER(c_double)]),
     "px_set_local_blocks": (c_int, [c_void_p, c_int]),
+    "px_set_local_block_sizes": (c_int, [c_void_p, c_int, POINTER(c_int)]),
     "px_set_variant": (c_int, [c_void_p, c_int, c_int]),
     "px_get_variant": (c_int, [c_void_p, c_int, POINTER(c_int)]),
     "px_set_adjoint_mode": (c_int, [c_void_p, c_int]),

@@ -377,6 +377,20 @@ int px_set_local_blocks(void* handle, int blocks) {
   return pxi::set_local_blocks(h, blocks);
 }
 
+int px_set_local_block_sizes(void* handle, int blocks, const int* sizes) {
+  Handle* h = bind(handle);
+  if (!h || !sizes) return fail(h, PX_ERR_ARG, "null argument");
+  if (blocks < 1 || blocks > PX_MAX_LOCAL_BLOCKS || blocks > h->Pl)
+    return fail(h, PX_ERR_ARG, "local blocks: 1 … 16 and at most the rank's slice count");
+  int sum = 0;
+  for (int g = 0; g < blocks; ++g) {
+    if (sizes[g] < 1) return fail(h, PX_ERR_ARG, "local blocks: every block needs a slice");
+    sum += sizes[g];
+  }
+  if (sum != h->Pl) return fail(h, PX_ERR_ARG, "local blocks: the sizes must add up to the rank's slices");
+  return pxi::set_local_blocks(h, blocks, sizes);
+}
+
 int px_set_inputs(void* handle, const double* u0, const double* u_target, const double* ctrl, int mem,
                   void* stream) {
   Handle* h = bind(handle);

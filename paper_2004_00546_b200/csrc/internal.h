@@ -116,7 +116,8 @@ struct Handle {
     double* S = nullptr;   // block's Σ of carry inputs (2D Chebyshev adjoint)
     cudaStream_t st = nullptr;
     cudaEvent_t ev = nullptr;
-    int q0 = 0, q1 = 0;
+    int q0 = 0, q1 = 0;  // direct sweep: local slices [q0, q1)
+    int a0 = 0, a1 = 0;  // adjoint sweep: the mirrored partition (equal long-span lengths)
   };
   int lb = 1;
   std::vector<Block> blocks;
@@ -225,7 +226,7 @@ int adjoint_linear(Handle* h, cudaStream_t s);
 int finish_direct_impl(Handle* h, cudaStream_t s);
 int finish_adjoint_impl(Handle* h, cudaStream_t s);
 void free_blocks(Handle* h);
-int set_local_blocks(Handle* h, int blocks);
+int set_local_blocks(Handle* h, int blocks, const int* sizes = nullptr);
 
 // ---- burgers.cu -----------------------------------------------------------------------
 int burgers_direct(Handle* h, cudaStream_t s);

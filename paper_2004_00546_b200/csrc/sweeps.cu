@@ -114,21 +114,21 @@ int adjoint_blocks(Handle* h, const double* wend, double* out, double* gacc, cud
     PX_CUDA(h, cudaStreamWaitEvent(b.st, h->ev_fork, 0));
     ScratchSwap sw(h, b);
     PX_CUDA(h, cudaMemsetAsync(b.Gp, 0, sizeof(double) * h->B * h->n, b.st));
-    const double* C = wend + (size_t)(b.q1 - 1) * h->n;
+    const double* C = wend + (size_t)(b.a1 - 1) * h->n;
     long long C_bs = lane_bs;
-    const bool ss = use_ssum(h) && b.q1 - b.q0 > 1;
+    const bool ss = use_ssum(h) && b.a1 - b.a0 > 1;
     if (ss) PX_TRY(axpby(h, b.S, nb, C, C_bs, 1.0, nullptr, 0, 0.0, b.st));
-    for (int q = b.q1 - 2; q >= b.q0; --q) {
+    for (int q = b.a1 - 2; q >= b.a0; --q) {
       double* res = nullptr;
       PX_TRY(exp_action(h, PX_PLAN_SLICE, h->AT, C, C_bs, wend + (size_t)q * h->n, lane_bs, ss ? nullptr : b.Gp, &res,
-                        b.st, ss && q > b.q0 ? b.S : nullptr, top_time(h, q + 1)));
+                        b.st, ss && q > b.a0 ? b.S : nullptr, top_time(h, q + 1)));
       C = res;
       C_bs = nb;
     }
     if (g > 0) {
       double* res = nullptr;
       PX_TRY(exp_action(h, PX_PLAN_BLOCK_LONG + g - 1, h->AT, C, C_bs, nullptr, 0, b.Gp, &res, b.st, nullptr,
-                        top_time(h, b.q0)));
+                        top_time(h, b.a0)));
       C = res;
       C_bs = nb;
     }
@@ -164,19 +164,32 @@ void free_blocks(Handle* h) {
   h->lb = 1;
 }
 
-int set_local_blocks(Handle* h, int blocks) {
-  if (blocks == h->lb) return PX_OK;
+// Direct blocks take `sizes` (slice order; equal blocks when null); the adjoint uses the mirrored
+// partition, so adjoint block g's long span (the blocks before it) has the length of direct block
+// G−1−g's (the blocks after it): one set of long-span plans serves both sweeps. Unequal sizes
+// balance each block's carries against its long span (the first direct / last adjoint block
+// spans the most).
+int set_local_blocks(Handle* h, int blocks, const int* sizes) {
+  std::vector<int> sz(blocks, blocks > 0 ? h->Pl / blocks : 0);
+  if (sizes) sz.assign(sizes, sizes + blocks);
+  bool same = blocks == h->lb;
+  for (int g = 0; same && g < blocks && blocks > 1; ++g) same = h->blocks[g].q1 - h->blocks[g].q0 == sz[g];
+  if (same) return PX_OK;
   free_blocks(h);
   h->graph_valid = false;
   if (blocks == 1) return PX_OK;
   if (!h->ev_fork) PX_CUDA(h, cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
   const size_t Bn = (size_t)h->B * h->n;
-  const int per = h->Pl / blocks;
   h->blocks.resize(blocks);
+  int q = 0, qa = 0;
   for (int g = 0; g < blocks; ++g) {
     Handle::Block& b = h->blocks[g];
-    b.q0 = g * per;
-    b.q1 = (g + 1) * per;
+    b.q0 = q;
+    b.q1 = q + sz[g];
+    q = b.q1;
+    b.a0 = qa;
+    b.a1 = qa + sz[blocks - 1 - g];
+    qa = b.a1;
     for (auto& p : b.Wk) PX_CUDA(h, cudaMalloc(&p, sizeof(double) * Bn));
     for (auto& p : b.ACC) PX_CUDA(h, cudaMalloc(&p, sizeof(double) * Bn));
     PX_CUDA(h, cudaMalloc(&b.D, sizeof(double) * Bn));

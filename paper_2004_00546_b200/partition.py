@@ -116,3 +116,45 @@ def rank_block(P: int, rank: int, world: int) -> tuple[int, int]:
     p0 = rank * base + min(rank, extra)
     p1 = p0 + base + (1 if rank < extra else 0)
     return p0, p1
+
+
+def balanced_blocks(P: int, G: int, rho: float) -> list[int]:
+    """Sizes of G contiguous slice blocks whose block-scan critical paths are balanced: block g
+    runs s_g carries and then one long span over the later blocks costing ρ carries per slice
+    spanned, so s_g + ρ·Σ_{k>g} s_k is (as nearly as integers allow) the same for every block
+    (`px_set_local_block_sizes`; the adjoint sweep uses the mirrored partition)."""
+    if G < 1 or G > P:
+        raise ValueError("need 1 ≤ G ≤ P blocks")
+    if G == 1:
+        return [P]
+
+    def sizes_for(C):
+        out = [0.0] * G
+        acc = 0.0
+        for g in range(G - 1, -1, -1):
+            out[g] = max(C - rho * acc, 1.0)
+            acc += out[g]
+        return out
+
+    lo, hi = 1.0, float(P)
+    for _ in range(100):
+        mid = 0.5 * (lo + hi)
+        if sum(sizes_for(mid)) < P:
+            lo = mid
+        else:
+            hi = mid
+    real = sizes_for(hi)
+    ints = [max(1, int(math.floor(x))) for x in real]
+    # distribute the remainder to the blocks with the largest fractional parts (later blocks first)
+    rem = P - sum(ints)
+    order = sorted(range(G), key=lambda g: (-(real[g] - math.floor(real[g])), -g))
+    i = 0
+    while rem > 0:
+        ints[order[i % G]] += 1
+        rem -= 1
+        i += 1
+    while rem < 0:
+        g = max(range(G), key=lambda k: ints[k])
+        ints[g] -= 1
+        rem += 1
+    return ints

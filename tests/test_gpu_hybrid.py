@@ -176,3 +176,25 @@ def test_reference_binding_on_the_gpu(cuda_ok):
     assert r.grad.shape == (6 * nx,)
     assert rel_l2(r.grad[: 3 * nx].reshape(3, nx), gd["grad_rows"]) <= 1e-5
     assert np.all(r.grad[3 * nx:] == 0.0)
+
+
+def test_hybrid_fallbacks_and_limits(cuda_ok):
+    """More slice CTAs than SMs: the overlap is declined (a waiting CTA must never block the
+    sweep) and the slices run after it, with the same numbers; a grid that fits neither the
+    cluster nor the run layout is refused."""
+    from paper_2004_00546_b200 import (
+        ChebyshevConfig, Grid, ProblemSpec, TimeLaw, build_system, make_hybrid_plan, solve_hybrid_tracking,
+        synthesize_trajectory)
+    from paper_2004_00546_b200.problems import BURGERS
+    sysm, u0, f, f_true, rk, cfg, law = _case(nx=96, P=64, B=3)
+    target = synthesize_trajectory(sysm, f_true, rk, law)[:, 0, :]
+    plan = make_hybrid_plan(sysm.spec.T, 64, 4.0)
+    r = solve_hybrid_tracking(sysm, u0, f, target, plan, rk=rk, expaction=cfg, law=law, overlap=True)
+    assert not r.timing["overlapped"]   # 3·64 slice CTAs + 3 sweep CTAs > 148 SMs
+    o = _oracle(sysm, u0, f, target, r.offsets, law, cfg)
+    assert np.max(np.abs(r.J - o.J) / np.abs(o.J)) <= 1e-10
+    assert rel_l2(r.grad, o.grad) <= 1e-8 and rel_l2(r.qdag0, o.qdag0) <= 1e-10
+    bad = build_system(Grid(3000), ProblemSpec(BURGERS, (0.0, 0.0), 0.01, 0.1), 2)
+    with pytest.raises(ValueError):
+        solve_hybrid_tracking(bad, np.zeros(3000), np.zeros(3000), np.zeros((101, 3000)), None, N=2,
+                              rk=rk, law=TimeLaw.constant())

@@ -33,14 +33,14 @@ def _plans(c):
     return slice_plan, long_plan
 
 
-def _oracle_linear(c, world=1, want_boundary=False):
+def _oracle_linear(c, world=1, want_boundary=False, block_sizes=None):
     from oracle.config_mode import linear_gradient
     sysm = c.system
     u0, ut, ctrl = c.inputs()
     sp, lp = _plans(c)
     return linear_gradient(c.grid.nx, c.grid.ny, sysm.A.as_tuple(), sysm.basis, c.spec.T, c.P, c.nsteps,
                            u0, ut, ctrl, sp, lp, lp, formulation="scan" if world == 1 else "blockscan",
-                           world=world, want_boundary=want_boundary)
+                           world=world, want_boundary=want_boundary, block_sizes=block_sizes)
 
 
 def _gpu_linear(c, boundary=False):
@@ -146,6 +146,9 @@ def _fullsize_check(index):
     c = baseline(index)
     u0, ut, ctrl = c.inputs()
     eng = get_engine(c.system, c.P, RK4Config(c.dt), c.expaction, c.batch)
+    # the fixture is the single-rank scan (config 5) or the equal 4-block block-scan (config 4); the
+    # GPU's local blocks are balanced (unequal, engine._block_sizes) — equal to the fixture's
+    # decomposition far below the bars (G-invariance, §7 of DESIGN.md)
     want = str(ref["formulation"])
     assert want == ("scan" if eng.local_blocks == 1 else f"blockscan({eng.local_blocks})")
     loop = direct_adjoint_loop(c.system, ctrl, ut, "linear", N=c.P, rk=RK4Config(c.dt), expaction=c.expaction,
@@ -200,17 +203,33 @@ def test_config4_krylov_scaled(ortho):
     c = scaled(baseline(4), nx=96, P=12, steps_per_slice=5, K=16)
     eng = ParaexpEngine(EngineSpec(c.system, c.P, c.dt, c.expaction, c.batch, variants=(("krylov_ortho", ortho),)))
     assert eng.variant("krylov_ortho") == ortho and eng.local_blocks == 4
+    assert eng.block_sizes == [3, 3, 3, 3]
     u0, ut, ctrl = c.inputs()
     eng.set_inputs(u0, ut, ctrl)
     eng.gradient()
     r = eng.results()
-    ref = _oracle_linear(c, world=4)
+    ref = _oracle_linear(c, world=4, block_sizes=eng.block_sizes)
     assert rel_l2(r["uT"], ref.uT) <= 1e-10 and rel_l2(r["qdag0"], ref.qdag0) <= 1e-10
     assert rel_l2(r["G"], ref.G) <= 1e-10 and rel_l2(r["grad"], ref.grad) <= 1e-8
     assert np.max(np.abs(r["J"] - ref.J) / np.abs(ref.J)) <= 1e-10
     eng.close()
     if ortho == 1:
         _check(_gpu_linear(c), ref)   # the public API runs the default
+        # balanced (unequal, mirrored for the adjoint) blocks against the oracle's same partition
+        import os
+        os.environ["PX_BALANCED_BLOCKS"] = "1"
+        try:
+            e2 = ParaexpEngine(EngineSpec(c.system, c.P, c.dt, c.expaction, c.batch))
+            assert sum(e2.block_sizes) == c.P and len(set(e2.block_sizes)) > 1
+            e2.set_inputs(u0, ut, ctrl)
+            e2.gradient()
+            r2 = e2.results()
+            ref2 = _oracle_linear(c, world=4, block_sizes=e2.block_sizes)
+            assert rel_l2(r2["grad"], ref2.grad) <= 1e-8 and rel_l2(r2["uT"], ref2.uT) <= 1e-10
+            assert rel_l2(r2["qdag0"], ref2.qdag0) <= 1e-10 and rel_l2(r2["G"], ref2.G) <= 1e-10
+            e2.close()
+        finally:
+            del os.environ["PX_BALANCED_BLOCKS"]
 
 
 @pytest.mark.parametrize("blocks", [1, 3])
@@ -220,8 +239,13 @@ def test_local_blocks_chebyshev(blocks, monkeypatch):
     from paper_2004_00546_b200 import baseline, release_engines, scaled
     release_engines()
     monkeypatch.setenv("PX_LOCAL_BLOCKS", str(blocks))
+    from paper_2004_00546_b200 import RK4Config
+    from paper_2004_00546_b200.optimization import get_engine
     c = scaled(baseline(5), nx=96, P=12, steps_per_slice=8, K=16)
-    _check(_gpu_linear(c), _oracle_linear(c, world=blocks))
+    loop = _gpu_linear(c)
+    sizes = get_engine(c.system, c.P, RK4Config(c.dt), c.expaction, c.batch).block_sizes
+    assert sum(sizes) == c.P and len(sizes) == blocks
+    _check(loop, _oracle_linear(c, world=blocks, block_sizes=sizes if blocks > 1 else None))
     release_engines()
 
 
