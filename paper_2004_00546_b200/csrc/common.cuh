@@ -116,6 +116,7 @@ struct KrylovWork {
   // delayed reorthogonalization (one reduction and two basis passes per step)
   double* u = nullptr;        // 2 × B × n  the candidate vector (ping-pong)
   double* kc = nullptr;       // B × KC_STRIDE  per-step coefficients (g, a/β, 1/β, κ)
+  int* cnt = nullptr;         // B  ticket counters of the fused per-step finalisation
 };
 constexpr int KC_STRIDE = 2 * (KRYLOV_MAX_M + 1) + 4;
 

@@ -47,13 +47,17 @@ inline int krylov_alloc(KrylovWork& kw, int m, size_t n, int B, std::string* err
       !al(&kw.part, (size_t)B * (2 * (KRYLOV_MAX_M + 1) + 1) * std::max<size_t>((size_t)kw.nblk, 148 * 4)) || !al(&kw.beta, B) ||
       !al(&kw.coef, (size_t)B * 2 * m) || !al(&kw.u, 2 * (size_t)B * n) || !al(&kw.kc, (size_t)B * KC_STRIDE))
     return PX_ERR_NOMEM;
+  if (cudaMalloc(&kw.cnt, sizeof(int) * B) != cudaSuccess || cudaMemset(kw.cnt, 0, sizeof(int) * B) != cudaSuccess) {
+    if (err) *err = "krylov cudaMalloc: ticket counters";
+    return PX_ERR_NOMEM;
+  }
 
   return PX_OK;
 }
 
 inline void krylov_free(KrylovWork& kw) {
   cudaFree(kw.V); cudaFree(kw.w); cudaFree(kw.H); cudaFree(kw.hcol);
-  cudaFree(kw.part); cudaFree(kw.beta); cudaFree(kw.coef); cudaFree(kw.u); cudaFree(kw.kc);
+  cudaFree(kw.part); cudaFree(kw.beta); cudaFree(kw.coef); cudaFree(kw.u); cudaFree(kw.kc); cudaFree(kw.cnt);
   kw = KrylovWork{};
 }
 
@@ -412,82 +416,11 @@ __global__ void k_kr_combine(double* out, const double* V, const double* coef, i
 // to rounding; tests/test_gpu_parity.py compares both with the oracle).
 // ---------------------------------------------------------------------------
 
-// w = M·u (u from `u`, batch stride ubs); part slots: [0, j) Q_qᵀu, [j, 2j) Q_qᵀw, 2j γ, 2j+1 δ.
-// spmv = false: no w (the final reorthogonalization of u_m): slots [0, j) and 2j only.
-template <int DIM>
-__global__ void __launch_bounds__(256) k_kr_ddots(double* w, const double* u, long long ubs, const double* V, int j,
-                                                  Stencil5 st, double* part, int nblk, int B, int nx, int ny,
-                                                  int spmv) {
-  const size_t n = (size_t)nx * ny;
-  const int b = blockIdx.y;
-  const double* ub = u + b * ubs;
-  __shared__ double us[KR_BLK], wsh[KR_BLK];
-  __shared__ double red[8][2];
-  double gam = 0.0, dlt = 0.0;
-#pragma unroll
-  for (int k = 0; k < KR_PPT; ++k) {
-    const size_t i = (size_t)blockIdx.x * KR_BLK + threadIdx.x + 256 * k;
-    double uv = 0.0, wv = 0.0;
-    if (i < n) {
-      uv = ub[i];
-      if (spmv) {
-        const int y = (int)(i / nx), x = (int)(i - (size_t)y * nx);
-        wv = stencil_at<DIM>(ub, st, x, y, nx, ny);
-        w[(size_t)b * n + i] = wv;
-      }
-    }
-    us[threadIdx.x + 256 * k] = uv;
-    wsh[threadIdx.x + 256 * k] = wv;
-    gam = fma(uv, uv, gam);
-    dlt = fma(uv, wv, dlt);
-  }
-  // γ, δ: block sums in fixed order
-  for (int o = 16; o > 0; o >>= 1) {
-    gam += __shfl_down_sync(0xffffffffu, gam, o);
-    dlt += __shfl_down_sync(0xffffffffu, dlt, o);
-  }
-  const int wid = threadIdx.x >> 5, ln = threadIdx.x & 31;
-  if (ln == 0) {
-    red[wid][0] = gam;
-    red[wid][1] = dlt;
-  }
-  __syncthreads();
-  double* pb = part + (size_t)b * (2 * (KRYLOV_MAX_M + 1) + 1) * nblk;
-  if (threadIdx.x < 2 && (spmv || threadIdx.x == 0)) {
-    double s2 = 0.0;
-    for (int k = 0; k < 8; ++k) s2 += red[k][threadIdx.x];
-    pb[(size_t)(2 * j + threadIdx.x) * nblk + blockIdx.x] = s2;
-  }
-  // Q_qᵀu and Q_qᵀw: one warp per column, the column chunk read once
-  const size_t i0 = (size_t)blockIdx.x * KR_BLK;
-  const int cnt = (int)min((size_t)KR_BLK, n - i0);
-  for (int q = wid; q < j; q += 8) {
-    const double* __restrict__ Vq = V + ((size_t)q * B + b) * n + i0;
-    double au = 0.0, aw = 0.0;
-#pragma unroll 8
-    for (int t = ln; t < KR_BLK; t += 32)
-      if (t < cnt) {
-        const double v = Vq[t];
-        au = fma(v, us[t], au);
-        aw = fma(v, wsh[t], aw);
-      }
-    for (int o = 16; o > 0; o >>= 1) {
-      au += __shfl_down_sync(0xffffffffu, au, o);
-      aw += __shfl_down_sync(0xffffffffu, aw, o);
-    }
-    if (ln == 0) {
-      pb[(size_t)q * nblk + blockIdx.x] = au;
-      if (spmv) pb[(size_t)(j + q) * nblk + blockIdx.x] = aw;
-    }
-  }
-}
-
 // One CTA per member: reduce the partials (one warp per slot, fixed order), then the step's small
 // algebra in parallel over the rows (j ≤ 40). j = 0: β is ‖src‖ (kw.beta). final: only the last
 // column's delayed correction H[:, m−1] += a and its subdiagonal.
-__global__ void __launch_bounds__(256) k_kr_dfinal(double* H, double* kc, double* beta0, const double* part, int nblk,
-                                                   int m, int j, int final_step) {
-  const int b = blockIdx.x;
+__device__ __forceinline__ void kr_dfinal_body(int b, double* H, double* kc, double* beta0, const double* part,
+                                               int nblk, int m, int j, int final_step) {
   const int t = threadIdx.x, wid = t >> 5, ln = t & 31;
   __shared__ double r[2 * (KRYLOV_MAX_M + 1) + 2];
   __shared__ double sh[4];  // β, 1/β, κ, a_{j−1}+c_v … (see below)
@@ -569,6 +502,101 @@ __global__ void __launch_bounds__(256) k_kr_dfinal(double* H, double* kc, double
   }
 }
 
+__global__ void __launch_bounds__(256) k_kr_dfinal(double* H, double* kc, double* beta0, const double* part, int nblk,
+                                                   int m, int j, int final_step) {
+  kr_dfinal_body(blockIdx.x, H, kc, beta0, part, nblk, m, j, final_step);
+}
+
+// w = M·u (u from `u`, batch stride ubs); part slots: [0, j) Q_qᵀu, [j, 2j) Q_qᵀw, 2j γ, 2j+1 δ.
+// spmv = false: no w (the final reorthogonalization of u_m): slots [0, j) and 2j only.
+// fin != null: the last CTA of each member (atomic ticket after a fence, threadFenceReduction
+// pattern) runs the step's finalisation (kr_dfinal_body) — no separate launch.
+struct KrFin {
+  double *H, *kc, *beta0;
+  int* cnt;
+  int m, final_step;
+};
+
+template <int DIM>
+__global__ void __launch_bounds__(256) k_kr_ddots(double* w, const double* u, long long ubs, const double* V, int j,
+                                                  Stencil5 st, double* part, int nblk, int B, int nx, int ny,
+                                                  int spmv, KrFin fin) {
+  const size_t n = (size_t)nx * ny;
+  const int b = blockIdx.y;
+  const double* ub = u + b * ubs;
+  __shared__ double us[KR_BLK], wsh[KR_BLK];
+  __shared__ double red[8][2];
+  double gam = 0.0, dlt = 0.0;
+#pragma unroll
+  for (int k = 0; k < KR_PPT; ++k) {
+    const size_t i = (size_t)blockIdx.x * KR_BLK + threadIdx.x + 256 * k;
+    double uv = 0.0, wv = 0.0;
+    if (i < n) {
+      uv = ub[i];
+      if (spmv) {
+        const int y = (int)(i / nx), x = (int)(i - (size_t)y * nx);
+        wv = stencil_at<DIM>(ub, st, x, y, nx, ny);
+        w[(size_t)b * n + i] = wv;
+      }
+    }
+    us[threadIdx.x + 256 * k] = uv;
+    wsh[threadIdx.x + 256 * k] = wv;
+    gam = fma(uv, uv, gam);
+    dlt = fma(uv, wv, dlt);
+  }
+  // γ, δ: block sums in fixed order
+  for (int o = 16; o > 0; o >>= 1) {
+    gam += __shfl_down_sync(0xffffffffu, gam, o);
+    dlt += __shfl_down_sync(0xffffffffu, dlt, o);
+  }
+  const int wid = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  if (ln == 0) {
+    red[wid][0] = gam;
+    red[wid][1] = dlt;
+  }
+  __syncthreads();
+  double* pb = part + (size_t)b * (2 * (KRYLOV_MAX_M + 1) + 1) * nblk;
+  if (threadIdx.x < 2 && (spmv || threadIdx.x == 0)) {
+    double s2 = 0.0;
+    for (int k = 0; k < 8; ++k) s2 += red[k][threadIdx.x];
+    pb[(size_t)(2 * j + threadIdx.x) * nblk + blockIdx.x] = s2;
+  }
+  // Q_qᵀu and Q_qᵀw: one warp per column, the column chunk read once
+  const size_t i0 = (size_t)blockIdx.x * KR_BLK;
+  const int cnt = (int)min((size_t)KR_BLK, n - i0);
+  for (int q = wid; q < j; q += 8) {
+    const double* __restrict__ Vq = V + ((size_t)q * B + b) * n + i0;
+    double au = 0.0, aw = 0.0;
+#pragma unroll 8
+    for (int t = ln; t < KR_BLK; t += 32)
+      if (t < cnt) {
+        const double v = Vq[t];
+        au = fma(v, us[t], au);
+        aw = fma(v, wsh[t], aw);
+      }
+    for (int o = 16; o > 0; o >>= 1) {
+      au += __shfl_down_sync(0xffffffffu, au, o);
+      aw += __shfl_down_sync(0xffffffffu, aw, o);
+    }
+    if (ln == 0) {
+      pb[(size_t)q * nblk + blockIdx.x] = au;
+      if (spmv) pb[(size_t)(j + q) * nblk + blockIdx.x] = aw;
+    }
+  }
+  if (fin.cnt) {
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(fin.cnt + b, 1) == (int)gridDim.x - 1);
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      kr_dfinal_body(b, fin.H, fin.kc, fin.beta0, part, nblk, fin.m, j, fin.final_step);
+      if (threadIdx.x == 0) fin.cnt[b] = 0;
+    }
+  }
+}
+
 // v_j = u·(1/β) − Σ_q (a_q/β)·Q_q;  u_next = w·(1/β) − κ·u − Σ_q g_q·Q_q  (Q read once)
 __global__ void __launch_bounds__(256) k_kr_dupdate(double* Vj, double* unext, const double* u, long long ubs,
                                                     const double* w, const double* V, const double* kc, int j, int B,
@@ -631,31 +659,31 @@ inline int krylov_action(KrylovWork& kw, double tau, int substeps, int m, const 
       cudaMemsetAsync(kw.H, 0, sizeof(double) * B * (m + 1) * m, s);
       const double* u = src;
       long long ubs = src_bs;
+      const KrFin fin{kw.H, kw.kc, kw.beta, kw.cnt, m, 0};
       for (int j = 0; j < m; ++j) {
         if (dim == 2)
-          k_kr_ddots<2><<<g, 256, 0, s>>>(kw.w, u, ubs, kw.V, j, st, kw.part, kw.nblk, B, nx, ny, 1);
+          k_kr_ddots<2><<<g, 256, 0, s>>>(kw.w, u, ubs, kw.V, j, st, kw.part, kw.nblk, B, nx, ny, 1, fin);
         else
-          k_kr_ddots<1><<<g, 256, 0, s>>>(kw.w, u, ubs, kw.V, j, st, kw.part, kw.nblk, B, nx, ny, 1);
-        k_kr_dfinal<<<B, 256, 0, s>>>(kw.H, kw.kc, kw.beta, kw.part, kw.nblk, m, j, 0);
+          k_kr_ddots<1><<<g, 256, 0, s>>>(kw.w, u, ubs, kw.V, j, st, kw.part, kw.nblk, B, nx, ny, 1, fin);
         double* un = kw.u + (size_t)(j & 1) * B * n;
         k_kr_dupdate<<<g, 256, 0, s>>>(kw.V + (size_t)j * B * n, un, u, ubs, kw.w, kw.V, kw.kc, j, B, n);
         u = un;
         ubs = nb;
-        launches += 3;
+        launches += 2;
       }
       // the delayed second projection of the last candidate completes H's last column
+      const KrFin fin_last{kw.H, kw.kc, kw.beta, kw.cnt, m, 1};
       if (dim == 2)
-        k_kr_ddots<2><<<g, 256, 0, s>>>(kw.w, u, ubs, kw.V, m, st, kw.part, kw.nblk, B, nx, ny, 0);
+        k_kr_ddots<2><<<g, 256, 0, s>>>(kw.w, u, ubs, kw.V, m, st, kw.part, kw.nblk, B, nx, ny, 0, fin_last);
       else
-        k_kr_ddots<1><<<g, 256, 0, s>>>(kw.w, u, ubs, kw.V, m, st, kw.part, kw.nblk, B, nx, ny, 0);
-      k_kr_dfinal<<<B, 256, 0, s>>>(kw.H, kw.kc, kw.beta, kw.part, kw.nblk, m, m, 1);
+        k_kr_ddots<1><<<g, 256, 0, s>>>(kw.w, u, ubs, kw.V, m, st, kw.part, kw.nblk, B, nx, ny, 0, fin_last);
       const int N = m + 1;
       const size_t smem = KR_EXPM_MATS * (size_t)N * N * sizeof(double);
       cudaFuncSetAttribute(k_kr_expm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       k_kr_expm<<<B, 256, smem, s>>>(kw.coef, kw.H, kw.beta, m, tau);
       k_kr_combine<<<dim3((unsigned)((n + 255) / 256), B), 256, 0, s>>>(
           out, kw.V, kw.coef, m, B, n, sub == substeps - 1 ? addend : nullptr, add_bs, pacc);
-      launches += 4;
+      launches += 3;
       src = out;
       src_bs = nb;
       continue;
