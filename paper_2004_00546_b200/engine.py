@@ -345,6 +345,7 @@ class ParaexpEngine:
 
     def set_inputs(self, u0, u_target, ctrl, stream: int | None = None) -> None:
         """numpy arrays (host) or CUDA torch tensors (device)."""
+        self._detach_snapshots()
         s = current_stream_handle() if stream is None else stream
         torch = _torch()
         if torch is not None and isinstance(u0, torch.Tensor) and u0.is_cuda:
@@ -429,6 +430,7 @@ class ParaexpEngine:
     # reduction). ``distributed_gradient`` chains them with an NCCL allreduce.
 
     def direct_partial(self, stream: int | None = None) -> None:
+        self._detach_snapshots()
         s = current_stream_handle() if stream is None else stream
         if self.spec.direct == "iterative":
             self.direct_iterative(s)
@@ -439,6 +441,7 @@ class ParaexpEngine:
         """Algorithm 2 (`nonlinear.py:149-194`): Jacobian-augmented sweeps until the
         max-over-slices relative change < eps (and ≥ min_iter sweeps); the J(ū_p)
         actions are planned on the host from each iterate's slice means."""
+        self._detach_snapshots()
         s = current_stream_handle() if stream is None else stream
         spec = self.spec
         cfg = spec.expaction
@@ -483,6 +486,7 @@ class ParaexpEngine:
         self._adjoint_mode = mode
 
     def adjoint_partial(self, stream: int | None = None) -> None:
+        self._detach_snapshots()
         s = current_stream_handle() if stream is None else stream
         span = self._adjoint_mode == "frozen_span"
         if not self.spec.system.is_linear and (self.p1 - self.p0 > 1 or self.p0 > 0 or span):
@@ -516,6 +520,7 @@ class ParaexpEngine:
 
 
     def set_adjoint_terminal(self, qdag_T, stream: int | None = None) -> None:
+        self._detach_snapshots()
         s = current_stream_handle() if stream is None else stream
         a = np.ascontiguousarray(qdag_T, dtype=np.float64).reshape(-1)
         if a.size != self.B * self.n:
@@ -525,6 +530,7 @@ class ParaexpEngine:
 
     def gradient(self, stream: int | None = None, group=None, want_fields: bool = True) -> None:
         """One full direct-adjoint gradient evaluation, enqueued on ``stream``."""
+        self._detach_snapshots()
         s = current_stream_handle() if stream is None else stream
         if self.spec.world == 1 and self.spec.system.is_linear:
             N.check(self.lib, self.lib.px_gradient(self.h, s), self.h)
@@ -549,15 +555,30 @@ class ParaexpEngine:
         return out
 
     def snapshot(self, field: int, shape):
-        """A device-side copy of a result field, read to the host on first use
-        (`optimization.DeviceField`); a host array when torch/CUDA is unavailable."""
+        """A result field read to the host on first use (`optimization.DeviceField`): it views
+        the native buffer and is copied on the device only if this engine is about to overwrite
+        it while the field is still referenced (copy-on-write, `_detach_snapshots`); a host
+        array when torch/CUDA is unavailable."""
+        import weakref
+
         from .optimization import DeviceField
         torch = _torch()
         if torch is None or not torch.cuda.is_available():
             return self.get(field).reshape(shape)
-        return DeviceField(self.device_view(field).clone(), shape)
+        f = DeviceField(self.device_view(field), shape, live=True)
+        self._snapshots = [r for r in getattr(self, "_snapshots", []) if r() is not None]
+        self._snapshots.append(weakref.ref(f))
+        return f
+
+    def _detach_snapshots(self) -> None:
+        for r in getattr(self, "_snapshots", []):
+            f = r()
+            if f is not None:
+                f.detach()
+        self._snapshots = []
 
     def close(self) -> None:
+        self._detach_snapshots()
         if getattr(self, "h", None):
             self.lib.px_destroy(self.h)
             self.h = None

@@ -48,15 +48,23 @@ class DeviceField:
     scalar outputs (J, ∂J/∂c) are read eagerly; the n-sized fields only when asked
     for, like the reference's lazily evaluated `PiecewiseSolution`s."""
 
-    def __init__(self, tensor, shape):
-        self._t = tensor
+    def __init__(self, tensor, shape, live: bool = False):
+        self._t = tensor        # a view of the engine's buffer while `live`, else a private copy
         self._shape = shape
         self._host = None
+        self._live = live
+
+    def detach(self) -> None:
+        """Copy-on-write: the engine calls this before new work overwrites the buffer."""
+        if self._live and self._t is not None:
+            self._t = self._t.clone()
+        self._live = False
 
     def numpy(self) -> np.ndarray:
         if self._host is None:
             self._host = self._t.cpu().numpy().reshape(self._shape)
             self._t = None
+            self._live = False
         return self._host
 
 

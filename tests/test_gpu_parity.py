@@ -970,3 +970,21 @@ def test_raw_c_abi_gradient_matches_python_api():
                                u0=u0)
     assert J[0] == float(np.ravel(loop.J)[0])
     assert np.array_equal(grad, np.ravel(loop.grad))
+
+
+def test_result_fields_survive_later_gradients():
+    """The loop's n-sized results view the engine's buffers and are copied on the device only
+    when a later gradient on the same engine is about to overwrite them (copy-on-write)."""
+    from paper_2004_00546_b200 import RK4Config, baseline, direct_adjoint_loop, scaled
+    c = scaled(baseline(5), nx=64, P=8, steps_per_slice=6, K=16)
+    u0, ut, ctrl = c.inputs()
+    run = lambda cc: direct_adjoint_loop(c.system, cc, ut, "linear", N=c.P, rk=RK4Config(c.dt),
+                                         expaction=c.expaction, u0=u0)
+    first = run(ctrl)
+    second = run(2.0 * ctrl)              # same cached engine: overwrites the native buffers
+    ref1 = _oracle_linear(c)
+    assert rel_l2(first.direct.final_state, ref1.uT) <= 1e-10
+    assert rel_l2(first.adjoint.integral, ref1.G) <= 1e-10
+    assert not np.allclose(second.direct.final_state, first.direct.final_state)
+    third = run(ctrl)                      # fields read right away (no copy needed)
+    assert np.array_equal(third.direct.final_state, first.direct.final_state)
