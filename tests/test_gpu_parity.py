@@ -988,3 +988,25 @@ def test_result_fields_survive_later_gradients():
     assert not np.allclose(second.direct.final_state, first.direct.final_state)
     third = run(ctrl)                      # fields read right away (no copy needed)
     assert np.array_equal(third.direct.final_state, first.direct.final_state)
+
+
+@pytest.mark.parametrize("ortho", [1, 0])
+def test_krylov_happy_breakdown(ortho):
+    """A 6×6 grid (n = 36) with m = 40 Arnoldi vectors: the Krylov space is exhausted before m
+    (happy breakdown, h_{j+1,j} ≈ 0) — both orthogonalisations truncate like the oracle's CGS2."""
+    from paper_2004_00546_b200 import KrylovConfig, baseline, scaled
+    from dataclasses import replace
+    from paper_2004_00546_b200.engine import EngineSpec, ParaexpEngine
+    c = scaled(baseline(4), nx=6, P=4, steps_per_slice=3, K=4)
+    c = replace(c, expaction=KrylovConfig(m=40, tol=1e-10, horizon=c.spec.T))
+    eng = ParaexpEngine(EngineSpec(c.system, c.P, c.dt, c.expaction, c.batch, local_blocks=1,
+                                   variants=(("krylov_ortho", ortho),)))
+    u0, ut, ctrl = c.inputs()
+    eng.set_inputs(u0, ut, ctrl)
+    eng.gradient()
+    r = eng.results()
+    ref = _oracle_linear(c)
+    assert np.all(np.isfinite(r["grad"]))
+    assert rel_l2(r["uT"], ref.uT) <= 1e-10 and rel_l2(r["qdag0"], ref.qdag0) <= 1e-10
+    assert rel_l2(r["grad"], ref.grad) <= 1e-8
+    eng.close()
