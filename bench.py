@@ -151,7 +151,7 @@ def cpu_reference(index: int, workers: int) -> dict:
         rate, wall, units, frac = sampled_rate(c, workers)
         w = max(1, min(workers, c.P))
         sample = (f"bounded sample: each of {w} concurrent worker processes (slice block of a {w}-way "
-                  f"block-scan) times 2 direct and 2 adjoint RK4 steps, one slice action with and one "
+                  f"block-scan) times 1 direct and 1 adjoint RK4 step (after a warm-up step), one slice action with and one "
                   f"without the φ₁ accumulator on the full {c.grid.nx}x{c.grid.ny} field; one gradient = "
                   f"the slowest worker's unit counts × unit times ({frac:.4f} of a gradient per step)")
         return {"value": rate, "seconds": wall, "cores": w, "sample": sample, "gradient_fraction": frac,

@@ -202,7 +202,7 @@ def predict_gradient_seconds(case, world: int, u: dict) -> float:
     return worst
 
 
-def sampled_rate(case, workers: int, reps: int = 3):
+def sampled_rate(case, workers: int, reps: int = 1):
     """One bounded sample: W concurrent workers time their units; returns (evals/s predicted,
     sample wall seconds, per-unit costs (slowest worker), fraction of a gradient the sample is)."""
     workers = max(1, min(workers, case.P))
