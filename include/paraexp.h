@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define PX_ABI_VERSION 3
+#define PX_ABI_VERSION 4
 
 enum {
   PX_OK = 0,
@@ -72,7 +72,7 @@ enum {
   PX_FIELD_FROZEN_BOUNDS = 6, /* (3)          Burgers: re_lo, re_hi, im of the frozen-operator FOV union */
   PX_FIELD_VEND = 7,        /* (B, P_local, n) per-slice inhomogeneous end states v_p(T_{p+1}) */
   PX_FIELD_WEND = 8,        /* (B, P_local, n) per-slice adjoint inhomogeneous end states */
-  PX_FIELD_TRAJ = 9,        /* (S+1, B, n)    Burgers direct trajectory (S = P·nsteps) */
+  PX_FIELD_TRAJ = 9,        /* (S+1, B, n)    Burgers / tracking direct trajectory (S = P·nsteps) */
   PX_FIELD_COUNT = 10
 };
 
@@ -173,6 +173,18 @@ int px_set_cheb_plan_law(void* handle, int slot, const double* coef_gc, const do
  * (Krylov plans: PX_ERR_ARG); lanes run one RK4 step per launch and the adjoint keeps a per-lane
  * θ-weighted ∫ accumulator. */
 int px_set_time_law(void* handle, const double* law4);
+
+/* Tracking objective of the linear testbed — the reference's linear loop with its own objective
+ * (optimization.py:84-112,154-231, algorithm "linear"): J = (1/T)∫‖u − u_t‖² dt (trapezoid on the
+ * RK4 nodes), adjoint source 2(u − u_t) with zero terminal data (solve_adjoint_linear with
+ * adj_forcing, paraexp.py:298-326), ∂L/∂f = (1/T)∫θ·q† dt. After the Paraexp direct every slice
+ * re-marches from its edge state u(T_p) to record the trajectory (PX_FIELD_TRAJ, (S+1, B, n)), and
+ * the adjoint lanes read it at their stage times; the carries are the terminal objective's.
+ * target: (S+1) × n (per_member 0) or (S+1) × B × n (per_member 1), S = P·nsteps, on the host or the
+ * device (mem). nullptr restores the terminal objective ½‖u(T) − u_target‖². One rank (p_begin = 0,
+ * p_end = P); local blocks are not used; PX_FIELD_UBND holds the edge states. Replaces: the
+ * objective/adjoint-source closures of direct_adjoint_loop for the linear system. */
+int px_set_tracking_target(void* handle, const double* target, int per_member, int mem, void* stream);
 
 /* Kernel-variant selection (PX_VAR_*), per handle; invalidates the captured gradient graph. */
 int px_set_variant(void* handle, int key, int value);

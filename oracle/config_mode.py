@@ -915,3 +915,105 @@ def linear_gradient_law(grid_nx, grid_ny, A, basis, T, P, nsteps, u0, u_target, 
     qdag0 = qT + C
     grad = basis.project(G)
     return OracleResult(J=J, grad=grad, uT=uT, qdag0=qdag0, G=G)
+
+
+# ---------------------------------------------------------------------------
+# The reference's linear loop with its own objective (`optimization.py:154-231`, algorithm
+# "linear"): Paraexp direct with the forcing f·θ(t), tracking cost, adjoint with the source
+# 2(q − q_true) and zero terminal data, ∂L/∂f = (1/T)∫θ·q† dt
+# ---------------------------------------------------------------------------
+
+
+def rk4_full_law(apply, y0, f, law, t0: float, h: float, nsteps: int):
+    """Classical RK4 of y' = M y + θ(t)·f from y0, every node kept: (nsteps+1, B, n)."""
+    out = np.empty((nsteps + 1,) + y0.shape)
+    y = y0.copy()
+    out[0] = y
+    for k in range(nsteps):
+        t = t0 + k * h
+        th1, th2, th4 = law_value(law, t), law_value(law, t + 0.5 * h), law_value(law, t + h)
+        k1 = apply(y) + th1 * f
+        k2 = apply(y + (0.5 * h) * k1) + th2 * f
+        k3 = apply(y + (0.5 * h) * k2) + th2 * f
+        k4 = apply(y + h * k3) + th4 * f
+        y = y + (h / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+        out[k + 1] = y
+    return out
+
+
+def linear_tracking_gradient(grid_nx, grid_ny, A, basis, T, P, nsteps, u0, ctrl, law, target, plan_slice):
+    """Config-mode restatement of the reference's linear loop (single-rank scan):
+
+    * direct: the Paraexp direct of `linear_gradient_law` gives the slice-edge states u(T_p)
+      (absorbed u0, every slice's own RK4 lane, summed-chain carries); the solution inside slice p
+      is the RK4 sweep of u' = A u + θ(t) f from u(T_p) over the slice's steps (by linearity the
+      lane plus the homogeneous propagation of the incoming state, `paraexp.py:202-218`);
+    * cost J = (1/T)∫‖u − u_t‖² dt, trapezoid on the RK4 nodes;
+    * adjoint (`solve_adjoint_linear` with adj_forcing = 2(q − q_true), zero terminal data,
+      `paraexp.py:298-326`): per slice a' = Aᵀa + 2(u − u_t) from a = 0 at T_{p+1} in reflected time
+      (trajectory and target linearly interpolated at the half steps), the θ-weighted
+      RK4-consistent ∫; the slice ends carried through exp(ΔAᵀ) with the law series;
+    * ∂L/∂f = (1/T)(Σ z_p + Σ carry integrals) (`gradient_wrt_forcing`), on the basis (field or modes).
+    Returns an OracleResult (grad projected on the basis; G the field gradient)."""
+    nx, ny = grid_nx, grid_ny
+    n = nx * ny
+    ctrl = np.atleast_2d(np.asarray(ctrl, dtype=np.float64))
+    B = ctrl.shape[0]
+    u0 = np.broadcast_to(_as_batch(u0, n), (B, n)).copy()
+    AT = tuple(np.asarray(A)[[0, 2, 1, 4, 3]])
+    applyA = lambda u: stencil_apply(A, u, nx, ny)
+    applyAT = lambda u: stencil_apply(AT, u, nx, ny)
+    delta = T / P
+    h = delta / nsteps
+    S = P * nsteps
+    f = basis.field(ctrl)
+    g0 = applyA(u0)
+    # slice-edge states by the Paraexp direct (the same operation sequence as linear_gradient_law)
+    edges = [u0.copy()]
+    D = None
+    for p in range(P):
+        v = rk4_linear_law(applyA, g0, f, law, p * delta, h, nsteps)
+        D = v if p == 0 else exp_action(applyA, plan_slice, D) + v
+        edges.append(u0 + D)
+    # the trajectory inside every slice from its edge state
+    traj = np.empty((S + 1, B, n))
+    traj[0] = u0
+    for p in range(P):
+        seg = rk4_full_law(applyA, edges[p], f, law, p * delta, h, nsteps)
+        traj[p * nsteps + 1:(p + 1) * nsteps + 1] = seg[1:]
+    tg = np.asarray(target, dtype=np.float64)
+    tg = tg[:, None, :] if tg.ndim == 2 else tg
+    J = tracking_cost(traj, tg, T, h)
+    a_end = np.empty((P, B, n))
+    zsum = np.zeros((B, n))
+    for p in range(P):
+        a = np.zeros((B, n))
+        z = np.zeros((B, n))
+        for i in range(nsteps):
+            top = (p + 1) * nsteps - i
+            ua, ub = traj[top], traj[top - 1]
+            ta, tb = tg[top], tg[top - 1]
+            sa, sb = 2.0 * (ua - ta), 2.0 * (ub - tb)
+            sm = 2.0 * ((0.5 * ua + 0.5 * ub) - (0.5 * ta + 0.5 * tb))
+            t_a = top * h
+            th_a, th_m, th_b = law_value(law, t_a), law_value(law, t_a - 0.5 * h), law_value(law, t_a - h)
+            k1 = applyAT(a) + sa
+            Y2 = a + (0.5 * h) * k1
+            k2 = applyAT(Y2) + sm
+            Y3 = a + (0.5 * h) * k2
+            k3 = applyAT(Y3) + sm
+            Y4 = a + h * k3
+            k4 = applyAT(Y4) + sb
+            z = z + (h / 6.0) * (th_a * a + 2.0 * th_m * (Y2 + Y3) + th_b * Y4)
+            a = a + (h / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+        a_end[p] = a
+        zsum += z
+    C = a_end[P - 1].copy()
+    Gh = np.zeros((B, n))
+    for p in range(P - 2, -1, -1):
+        C = cheb_law_action(applyAT, plan_slice, C, Gh, law, (p + 1) * delta) + a_end[p]
+    G = (zsum + Gh) / T
+    # u(T) is the Paraexp direct's (the last edge state), as the reference's direct.eval(T); the
+    # recorded node S differs from it by the RK4 error of the homogeneous propagation over slice P−1
+    return OracleResult(J=J, grad=basis.project(G), uT=edges[-1], qdag0=C, G=G,
+                        extras={"traj": traj, "edges": np.stack(edges), "a_end": a_end})

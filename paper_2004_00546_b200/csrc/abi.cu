@@ -276,10 +276,23 @@ int px_set_time_law(void* handle, const double* law) {
   if (!constant && !h->fctl) PX_TRY(pxi::dalloc_t(h, &h->fctl, (size_t)h->B * h->n));
   for (int k = 0; k < 4; ++k) h->law[k] = law[k];
   h->has_law = !constant;
+  if (h->tracking) PX_TRY(pxi::tracking_theta(h));
   // the closed-form adjoint ∫ holds for the time-constant weight only
   h->z_closed = !h->has_law && h->dim == 2 && !(h->d.flags & PX_FLAG_Z_ACCUM);
   if (h->has_law && h->dim == 2 && !h->Z) PX_TRY(pxi::dalloc_t(h, &h->Z, (size_t)h->L * h->n));
   h->graph_valid = false;
+  return PX_OK;
+}
+
+int px_set_tracking_target(void* handle, const double* target, int per_member, int mem, void* stream) {
+  Handle* h = bind(handle);
+  if (!h) return fail(h, PX_ERR_ARG, "null handle");
+  if (h->d.kind != PX_KIND_ADVDIFF)
+    return fail(h, PX_ERR_ARG, "tracking objective: the linear testbed (Burgers: the px_hybrid handle)");
+  if (h->d.p_begin != 0 || h->d.p_end != h->d.P) return fail(h, PX_ERR_ARG, "tracking objective: one rank");
+  if (per_member != 0 && per_member != 1) return fail(h, PX_ERR_ARG, "per_member must be 0 or 1");
+  PX_TRY(pxi::tracking_set(h, target, per_member, mem, static_cast<cudaStream_t>(stream)));
+  h->stage = 0;
   return PX_OK;
 }
 

@@ -256,7 +256,8 @@ int cheb_action(Handle* h, const Plan& pl, const px::Stencil5& st, const double*
 // 1D linear sweeps: the whole carry recursion in one CTA (or one 8-CTA cluster) per member
 bool use_scan1d(const Handle* h) {
   const Plan& sl = h->plans[PX_PLAN_SLICE];
-  return h->dim == 1 && h->n <= 4096 && (!sl.set || !sl.krylov) && !(h->d.flags & PX_FLAG_BOUNDARY_STATES);
+  return h->dim == 1 && h->n <= 4096 && (!sl.set || !sl.krylov) && !(h->d.flags & PX_FLAG_BOUNDARY_STATES) &&
+         !h->tracking;
 }
 
 int scan1d(Handle* h, bool adjoint, const double* lanes, double* out, double* pacc, int long_slot, cudaStream_t s) {

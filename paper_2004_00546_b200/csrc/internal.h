@@ -12,6 +12,8 @@
 //   krylov.cu   krylov.cuh: batched Arnoldi exp-actions
 //   burgers.cu  burgers.cuh, burgers_iter.cuh: Burgers serial sweep, adjoint, Algorithm 2
 //   ops.cu      kernels.cuh: axpby, projections, reductions, control sources, closed-form ∫
+//   tracking.cu tracking.cuh: the linear testbed's tracking objective (recording sweep, cost,
+//               adjoint lanes with the source 2(u − u_t))
 //   hybrid.cu   C ABI of the reference's hybrid with its tracking objective (px_hybrid_*); its
 //               kernels (hybrid.cuh) are instantiated in burgers.cu
 #pragma once
@@ -84,6 +86,13 @@ struct Handle {
   bool has_law = false;
   double law[4] = {1.0, 0.0, 0.0, 0.0};
   double* fctl = nullptr;
+  // tracking objective (px_set_tracking_target, the reference's linear loop): node target
+  // (S+1) × n or (S+1) × B × n, θ at the half steps, recording/adjoint lane buffers (tracking.cu)
+  bool tracking = false;
+  int trk_per_member = 0;
+  double *trk_target = nullptr, *trk_theta = nullptr;
+  double *trk_y = nullptr, *trk_acc = nullptr, *trk_z = nullptr;
+  double* trk_x[2] = {nullptr, nullptr};
   cufftHandle fft = 0;
   double2* fbuf = nullptr;  // B × n complex
   double* bsum = nullptr;   // B: Σ_i b[b][i]
@@ -194,6 +203,8 @@ int project(Handle* h, double* grad, const double* F, long long Fbs, double alph
 int apply_plus_control(Handle* h, double* out, const double* x, long long xbs, const px::Stencil5& st,
                        bool with_control, cudaStream_t s);
 int objective(Handle* h, cudaStream_t s);  // J = ½‖QT‖² per member (non-finite flag)
+// out[b] = scale·Σ_j partial[b·m + j] (fixed order; non-finite flag)
+int finalize_sum(Handle* h, double* out, const double* partial, int m, double scale, cudaStream_t s);
 int z_closed_form(Handle* h, const double* wend, cudaStream_t s);
 
 // ---- lanes.cu -------------------------------------------------------------------------
@@ -227,6 +238,12 @@ int finish_direct_impl(Handle* h, cudaStream_t s);
 int finish_adjoint_impl(Handle* h, cudaStream_t s);
 void free_blocks(Handle* h);
 int set_local_blocks(Handle* h, int blocks, const int* sizes = nullptr);
+
+// ---- tracking.cu ----------------------------------------------------------------------
+int tracking_set(Handle* h, const double* target, int per_member, int mem, cudaStream_t s);
+int tracking_theta(Handle* h);  // θ(j·h/2) table from the handle's law
+int track_direct(Handle* h, cudaStream_t s);
+int track_adjoint_lanes(Handle* h, const double** wend, cudaStream_t s);
 
 // ---- burgers.cu -----------------------------------------------------------------------
 int burgers_direct(Handle* h, cudaStream_t s);

@@ -49,6 +49,12 @@ int apply_plus_control(Handle* h, double* out, const double* x, long long xbs, c
 }
 
 // J[b] = ½‖QT[b]‖² (fixed-order two-level reduction); raises the non-finite flag
+int finalize_sum(Handle* h, double* out, const double* partial, int m, double scale, cudaStream_t s) {
+  px::k_finalize_sum<<<h->B, 256, 0, s>>>(out, partial, m, scale, h->nonfinite);
+  PX_CHECK_LAUNCH(h);
+  return PX_OK;
+}
+
 int objective(Handle* h, cudaStream_t s) {
   px::k_sumsq_partial<<<dim3(h->red_blocks, h->B), 256, 0, s>>>(h->partial, h->QT, h->n);
   PX_CHECK_LAUNCH(h);

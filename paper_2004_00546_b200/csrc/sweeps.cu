@@ -51,7 +51,9 @@ struct ScratchSwap {
   }
 };
 
-bool use_blocks(const Handle* h) { return h->lb > 1 && h->dim == 2 && !(h->d.flags & PX_FLAG_BOUNDARY_STATES); }
+bool use_blocks(const Handle* h) {
+  return h->lb > 1 && h->dim == 2 && !(h->d.flags & PX_FLAG_BOUNDARY_STATES) && !h->tracking;
+}
 
 // The adjoint's φ₁ integral of the slice carries, Σ_q Δ·φ₁(ΔAᵀ)·C_q, is linear in the carry
 // inputs and every carry applies the same operator: it equals ONE φ₁ action on S = Σ_q C_q.
@@ -230,7 +232,7 @@ int direct_linear(Handle* h, cudaStream_t s) {
     tend(h, tm, s);
     return PX_OK;
   }
-  const bool bnd = (h->d.flags & PX_FLAG_BOUNDARY_STATES) && h->UBND;
+  const bool bnd = ((h->d.flags & PX_FLAG_BOUNDARY_STATES) || h->tracking) && h->UBND;
   const long long ubs = (long long)(h->d.P + 1) * nb;
   if (bnd) PX_TRY(axpby(h, h->UBND, ubs, h->u0, 0, 1.0, nullptr, 0, 0.0, s));
   if (use_blocks(h)) {
@@ -262,6 +264,7 @@ int direct_linear(Handle* h, cudaStream_t s) {
   }
   PX_TRY(axpby(h, h->UT, nb, D, D_bs, 1.0, nullptr, 0, 0.0, s));
   tend(h, tm, s);
+  if (h->tracking) PX_TRY(track_direct(h, s));
   return PX_OK;
 }
 
@@ -269,15 +272,24 @@ int adjoint_linear(Handle* h, cudaStream_t s) {
   const long long nb = (long long)h->n;
   const long long lane_bs = (long long)h->Pl * nb;
   const double* wend = nullptr;
-  int tm = tbegin(h, PX_PHASE_RK4_ADJOINT, s);
-  PX_TRY(rk4_sweep(h, true, &wend, s));
-  tend(h, tm, s);
-  h->wend = wend;
-  tm = tbegin(h, PX_PHASE_EXP_ADJOINT, s);
+  int tm;
+  if (h->tracking) {  // lanes with the tracking source from zero data; G <- Σ_p z_p
+    PX_TRY(track_adjoint_lanes(h, &wend, s));
+    h->wend = wend;
+    tm = tbegin(h, PX_PHASE_EXP_ADJOINT, s);
+  } else {
+    tm = tbegin(h, PX_PHASE_RK4_ADJOINT, s);
+    PX_TRY(rk4_sweep(h, true, &wend, s));
+    tend(h, tm, s);
+    h->wend = wend;
+    tm = tbegin(h, PX_PHASE_EXP_ADJOINT, s);
+  }
   // G partial <- Σ_p z_p  (z_p = Σ_steps h·w3 + nsteps·c; with a time law the θ-weighted lane
-  // integrals and the summed source part in cz, lanes.cu)
-  if (h->z_closed) PX_TRY(z_closed_form(h, wend, s));
-  else PX_TRY(lane_sum_plus(h, h->G, h->Z, h->cz, h->has_law ? 1.0 : (double)h->Pl * h->d.nsteps, h->z_valid, s));
+  // integrals and the summed source part in cz, lanes.cu; tracking: summed with its lanes)
+  if (!h->tracking) {
+    if (h->z_closed) PX_TRY(z_closed_form(h, wend, s));
+    else PX_TRY(lane_sum_plus(h, h->G, h->Z, h->cz, h->has_law ? 1.0 : (double)h->Pl * h->d.nsteps, h->z_valid, s));
+  }
   if (use_scan1d(h) && !h->has_law) {
     PX_TRY(scan1d(h, true, wend, h->QDAG0, h->G, h->d.p_begin > 0 ? PX_PLAN_LONG_ADJOINT : -1, s));
   } else if (use_blocks(h)) {
@@ -314,6 +326,9 @@ int adjoint_linear(Handle* h, cudaStream_t s) {
   }
   tend(h, tm, s);
   tm = tbegin(h, PX_PHASE_OTHER, s);
+  // tracking: ∂L/∂f = (1/T)∫θ·q† dt (optimization.py:103-112); the terminal objective adds its
+  // absorbed final-condition part in finish_adjoint_impl
+  if (h->tracking) PX_TRY(axpby(h, h->G, nb, h->G, nb, 1.0 / h->d.T, nullptr, 0, 0.0, s));
   PX_TRY(project(h, h->GRAD, h->G, nb, 1.0, 0.0, s));
   tend(h, tm, s);
   return PX_OK;
@@ -325,6 +340,10 @@ int finish_direct_impl(Handle* h, cudaStream_t s) {
   // u(T) = u0 + Σ carries (the Burgers sweep writes u(T) itself)
   if (h->d.kind == PX_KIND_ADVDIFF) PX_TRY(axpby(h, h->UT, nb, h->UT, nb, 1.0, h->u0, 0, 1.0, s));
   PX_TRY(axpby(h, h->QT, nb, h->UT, nb, 1.0, h->ut, 0, -1.0, s));
+  if (h->tracking) {  // J came with the recording sweep; the adjoint has zero terminal data
+    tend(h, tm, s);
+    return PX_OK;
+  }
   PX_TRY(objective(h, s));
   if (h->d.kind == PX_KIND_ADVDIFF) PX_TRY(apply_plus_control(h, h->gadj, h->QT, nb, h->AT, false, s));
   tend(h, tm, s);
@@ -334,6 +353,7 @@ int finish_direct_impl(Handle* h, cudaStream_t s) {
 int finish_adjoint_impl(Handle* h, cudaStream_t s) {
   const long long nb = (long long)h->n;
   if (h->adjoint_mode == PX_ADJOINT_FROZEN_SPAN) return PX_OK;  // q†_T is not absorbed: nothing to add
+  if (h->tracking) return PX_OK;                                  // q†(T) = 0: nothing to add
   const int tm = tbegin(h, PX_PHASE_OTHER, s);
   // absorbed final condition: q† = q†_T + the solved part (paraexp.py:268-270)
   PX_TRY(axpby(h, h->QDAG0, nb, h->QDAG0, nb, 1.0, h->QT, nb, 1.0, s));

@@ -188,6 +188,7 @@ class ParaexpEngine:
 
     def __init__(self, spec: EngineSpec):
         self.spec = spec
+        self.tracking = False  # px_set_tracking_target: the reference's linear loop objective
         self.lib = N.load()
         sysm = spec.system
         grid = sysm.grid
@@ -367,6 +368,37 @@ class ParaexpEngine:
                                         N.PX_MEM_HOST, s)
             self._keep = [a, b, c]
         N.check(self.lib, rc, self.h)
+
+    def set_tracking_target(self, target, stream: int | None = None) -> None:
+        """The tracking objective (`px_set_tracking_target`, the reference's linear loop): the
+        target trajectory on the RK4 nodes, (S+1, n) shared or (S+1, B, n) per member, numpy or a
+        contiguous float64 CUDA tensor; None restores the terminal objective."""
+        self._detach_snapshots()
+        s = current_stream_handle() if stream is None else stream
+        if target is None:
+            N.check(self.lib, self.lib.px_set_tracking_target(self.h, None, 0, N.PX_MEM_HOST, s), self.h)
+            self.tracking = False
+            return
+        S = self.spec.P * self.spec.nsteps
+        torch = _torch()
+        dev = torch is not None and isinstance(target, torch.Tensor) and target.is_cuda
+        if dev:
+            if target.dtype != torch.float64 or not target.is_contiguous():
+                raise ValueError("a device target must be a contiguous float64 tensor")
+            t, cnt, mem = target, target.numel(), N.PX_MEM_DEVICE
+        else:
+            t = np.ascontiguousarray(target, dtype=np.float64)
+            cnt, mem = t.size, N.PX_MEM_HOST
+        if cnt == (S + 1) * self.n:
+            per = 0
+        elif cnt == (S + 1) * self.B * self.n:
+            per = 1
+        else:
+            raise ValueError(f"tracking target: (S+1, n) or (S+1, B, n) values with S = {S}")
+        ptr = t.data_ptr() if dev else t.ctypes.data
+        N.check(self.lib, self.lib.px_set_tracking_target(self.h, ptr, per, mem, s), self.h)
+        self._keep.append(t)
+        self.tracking = True
 
     def field_count(self, field: int) -> int:
         p = ctypes.c_void_p()

@@ -12,9 +12,12 @@ reference's own layouts:
 
 * `system_from_reference(ref_system)` → (System, f, TimeLaw, embedding);
 * `direct_adjoint_loop(ref_system, f, q_true, algorithm, N, rk, leja, plan=…, dt=…)` — the
-  reference's loop signature; Burgers with "hybrid" or "serial" runs the tracking loop on the
-  GPU (`tracking.py`): the reference's 1D-embedded Burgers (y-invariant U on an nx×ny grid,
-  V ≡ 0) maps onto the 1D path, J and ∂L/∂f are returned on the embedded grid;
+  reference's loop signature with its tracking objective; advection–diffusion with "linear" or
+  "serial" runs the Paraexp linear loop (`px_set_tracking_target`: the trajectory recorded from
+  the slice edge states, the adjoint with the source 2(q − q_true)); Burgers with "hybrid" or
+  "serial" runs the hybrid tracking loop on the GPU (`tracking.py`): the reference's 1D-embedded
+  Burgers (y-invariant U on an nx×ny grid, V ≡ 0) maps onto the 1D path, J and ∂L/∂f are
+  returned on the embedded grid;
 * `solve_direct_linear` / `solve_adjoint_linear` (`paraexp.py:221-326`) for the linear
   testbed with the reference's forcing f·sin(ωt) and a terminal adjoint condition.
 
@@ -110,14 +113,16 @@ def direct_adjoint_loop(ref_system, f, q_true, algorithm: str, N: int = 1, rk=No
     forced = ref_system.with_forcing_field(np.asarray(f, dtype=np.float64)) \
         if hasattr(ref_system, "with_forcing_field") else ref_system
     sysm, f1, law, emb = system_from_reference(forced)
-    if sysm.is_linear:
-        raise ConfigError("the reference's linear loop tracks a trajectory ((1/T)∫‖q − q_true‖²), which this "
-                          "path does not evaluate on the Paraexp direct; use solve_direct_linear / "
-                          "solve_adjoint_linear (terminal data) or the Burgers hybrid loop")
     T = sysm.spec.T
-    S = max(1, int(math.ceil(T / dt - 1e-9)))
+    if sysm.is_linear:
+        # the linear loop (Paraexp direct and adjoint on N equal slices): whole steps per slice
+        steps = max(1, int(math.ceil(T / (N * dt) - 1e-9)))
+        S = N * steps
+        gplan = None
+    else:
+        S = max(1, int(math.ceil(T / dt - 1e-9)))
+        gplan = make_hybrid_plan(T, plan.N, float(plan.k)) if plan is not None else None
     target = _node_trajectory(q_true, emb, T, S)
-    gplan = make_hybrid_plan(T, plan.N, float(plan.k)) if plan is not None else None
     r = loop(sysm, f1, target, algorithm, N=N, rk=RK4Config(T / S), expaction=expaction, u0=np.zeros(sysm.n),
              objective="tracking", plan=gplan, time_law=law, overlap=overlap)
     rows = emb.ny if emb.kind == "burgers1d" else 1

@@ -145,8 +145,9 @@ def _default_expaction(system: System):
 
 def get_engine(system: System, N: int, rk: RK4Config, expaction, batch: int, rank: int = 0, world: int = 1,
                boundary_states: bool = False, direct: str = "serial", eps: float = 1e-3, max_iter: int = 25,
-               min_iter: int = 2, law: tuple = (1.0, 0.0, 0.0, 0.0)) -> ParaexpEngine:
-    """Cached engine per (problem, partition, numerics, rank): handles own HBM scratch."""
+               min_iter: int = 2, law: tuple = (1.0, 0.0, 0.0, 0.0), tracking: bool = False) -> ParaexpEngine:
+    """Cached engine per (problem, partition, numerics, rank): handles own HBM scratch. A cached
+    engine left in the tracking objective is switched back unless ``tracking``."""
     key = (system.grid, system.spec, type(system.basis).__name__, system.basis.K, N, rk.dt, expaction, batch, rank,
            world, boundary_states, direct, eps, max_iter, min_iter, tuple(law))
     eng = _ENGINES.get(key)
@@ -154,6 +155,8 @@ def get_engine(system: System, N: int, rk: RK4Config, expaction, batch: int, ran
         eng = ParaexpEngine(EngineSpec(system, N, rk.dt, expaction, batch, rank, world, boundary_states,
                                        direct, eps, max_iter, min_iter, law=tuple(law)))
         _ENGINES[key] = eng
+    if eng.tracking and not tracking:
+        eng.set_tracking_target(None)
     return eng
 
 
@@ -293,7 +296,7 @@ def _tracking_loop(system, f, q_true, algorithm, N, rk, expaction, u0, backend, 
     if backend not in BACKENDS:
         raise ValueError(f"unknown backend {backend!r}; the B200 path provides {BACKENDS}")
     if system.is_linear:
-        raise ValueError("the tracking objective runs on the Burgers testbed (the hybrid's serial direct sweep)")
+        return _linear_tracking_loop(system, f, q_true, algorithm, N, rk, expaction, u0, plan, time_law)
     if algorithm not in (HYBRID, SERIAL):
         raise ValueError("the tracking objective runs with algorithm 'hybrid' or 'serial'")
     if rk is None:
@@ -319,6 +322,59 @@ def _tracking_loop(system, f, q_true, algorithm, N, rk, expaction, u0, backend, 
         DirectSolution(r.partition, r.final_state[0] if single else r.final_state),
         AdjointSolution(r.partition, r.qdag0[0] if single else r.qdag0, r.grad[0] if single else r.grad),
         iterations=1, seconds=time.perf_counter() - tick, stats={"timing": r.timing, "offsets": r.offsets})
+
+
+def _linear_tracking_loop(system, f, q_true, algorithm, N, rk, expaction, u0, plan, time_law):
+    """The reference's linear loop with its own objective (`optimization.py:154-231`, algorithm
+    "linear"): the Paraexp direct with the forcing f·θ(t), the trajectory recorded from the slice
+    edge states, J = (1/T)∫‖u − u_t‖² dt, the adjoint with the source 2(u − u_t) and zero terminal
+    data, ∂L/∂f = (1/T)∫θ·q† dt (`px_set_tracking_target`). One rank."""
+    if algorithm not in (LINEAR, SERIAL):
+        raise ValueError("the linear testbed's tracking loop runs with algorithm 'linear' or 'serial'")
+    if plan is not None:
+        raise ConfigError("plan: the geometric partition belongs to the Burgers hybrid")
+    if rk is None:
+        raise ConfigError("rk: an RK4Config(dt) is required (fixed-step RK4)")
+    if algorithm == SERIAL:
+        N = 1
+    law = tuple(float(v) for v in time_law.as_tuple()) if time_law is not None else (1.0, 0.0, 0.0, 0.0)
+    ctrl = np.atleast_2d(np.asarray(f, dtype=np.float64))
+    B = ctrl.shape[0]
+    if ctrl.shape[1] != system.basis.K:
+        raise ValueError("f: K control values per member (a field system takes the forcing field)")
+    u0 = np.zeros(system.n) if u0 is None else np.asarray(u0, dtype=np.float64)
+    eng = get_engine(system, N, rk, expaction or _default_expaction(system), B, 0, 1, False, "serial", law=law,
+                     tracking=True)
+    S = N * eng.spec.nsteps
+    torch = _torch_or_none()
+    tgt = q_true if torch is not None and isinstance(q_true, torch.Tensor) else np.asarray(q_true, dtype=np.float64)
+    if tuple(tgt.shape[:1]) != (S + 1,):
+        raise ValueError(f"q_true: the target trajectory on the {S + 1} RK4 nodes ((S+1, n) or (S+1, B, n))")
+    from . import _native as _N
+    tick = time.perf_counter()
+    eng.set_inputs(u0, np.zeros(system.n), ctrl)
+    eng.set_tracking_target(tgt)  # get_engine restores the terminal objective for the other loops
+    eng.gradient()
+    res = eng.results(fields=False)
+    fields = {k: eng.snapshot(fld, (B, system.n))
+              for k, fld in (("uT", _N.PX_FIELD_UT), ("qdag0", _N.PX_FIELD_QDAG0), ("G", _N.PX_FIELD_G))}
+    fields["traj"] = eng.snapshot(_N.PX_FIELD_TRAJ, (S + 1, B, system.n))
+    bnd = eng.get(_N.PX_FIELD_UBND).reshape(B, N + 1, system.n)
+    single = np.ndim(f) == 1
+    part = partition_equidistant(system.spec.T, N)
+    return LoopResult(
+        float(res["J"][0]) if single else res["J"], res["grad"][0] if single else res["grad"],
+        DirectSolution(part, fields["uT"], bnd),
+        AdjointSolution(part, fields["qdag0"], fields["G"]),
+        iterations=1, seconds=time.perf_counter() - tick, stats={**eng.stats(), "trajectory": fields["traj"]})
+
+
+def _torch_or_none():
+    try:
+        import torch
+        return torch
+    except ImportError:  # pragma: no cover
+        return None
 
 
 def descend(

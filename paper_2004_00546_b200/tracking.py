@@ -258,10 +258,18 @@ def solve_hybrid_tracking(system: System, u0, f, target, plan: HybridPlan | None
 
 def synthesize_trajectory(system: System, f_true, rk: RK4Config, law: TimeLaw | None = None, u0=None) -> np.ndarray:
     """The tracking target: the serial sweep's node trajectory (S+1, B, n) of the system under
-    ``f_true``·θ(t) (`optimization.py:66-80`, on the GPU)."""
+    ``f_true``·θ(t) (`optimization.py:66-80`, on the GPU). The linear testbed records it with the
+    one-slice tracking loop (``f_true``: K values per member; a field system takes the field)."""
     law = law or TimeLaw.constant()
     f = np.atleast_2d(np.asarray(f_true, dtype=np.float64))
     B, n = f.shape[0], system.n
+    if system.is_linear:
+        from .optimization import SERIAL, direct_adjoint_loop
+        from .partition import slice_steps
+        S = slice_steps(system.spec.T, rk.dt)
+        r = direct_adjoint_loop(system, f, np.zeros((S + 1, n)), SERIAL, rk=rk, u0=u0, objective="tracking",
+                                time_law=law)
+        return r.stats["trajectory"].numpy()
     offs, _ = _offsets_for(system, None, 1, rk)
     S = int(offs[-1])
     u0 = np.zeros(n) if u0 is None else u0

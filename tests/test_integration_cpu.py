@@ -119,5 +119,31 @@ def test_binding_refuses_what_the_path_cannot_express(R):
     bad = R.build_system(grid, R.ProblemSpec("burgers", 0.0, 0.05, 1.0, 0.5, f))
     with pytest.raises(ConfigError):
         system_from_reference(bad)
-    with pytest.raises(ConfigError):   # the linear loop's tracking objective
-        direct_adjoint_loop(_advdiff(R), np.zeros(120), None, "linear", dt=1e-3)
+    with pytest.raises(ValueError):    # the binding is the cuda backend
+        direct_adjoint_loop(_advdiff(R), np.zeros(120), None, "linear", backend="thread", dt=1e-3)
+
+
+def test_linear_loop_conversion_vs_the_reference_loop(R):
+    """The reference's own linear loop (tracking objective, f·sin ωt, Paraexp direct and adjoint,
+    `optimization.py:154-231`) against the binding's conversion (field system, law, q_true on the
+    nodes) solved by the oracle restatement (oracle.config_mode.linear_tracking_gradient)."""
+    from oracle.config_mode import linear_tracking_gradient
+    from paper_2004_00546_b200.expaction import ChebyshevConfig, plan_chebyshev
+    from paper_2004_00546_b200.integration import _node_trajectory, system_from_reference
+    ref = _advdiff(R, omega=4.0)
+    rng = np.random.default_rng(9)
+    f, f_true = 0.5 * rng.standard_normal(ref.n), 0.5 * rng.standard_normal(ref.n)
+    leja = R.LejaConfig(tol=1e-13)
+    q_true = R.synthesize_truth(ref, f_true, R.RKConfig(rtol=1e-11, atol=1e-14, h_max=2.5e-4), leja=leja)
+    res = R.direct_adjoint_loop(ref, f, q_true, "linear", N=2, rk=R.RKConfig(rtol=1e-11, atol=1e-14), leja=leja,
+                                probe_nodes=4001)
+    sysm, f1, law, e = system_from_reference(ref.with_forcing_field(f))
+    assert np.array_equal(f1, f) and e.kind == "field"
+    T, N, steps = ref.spec.T, 2, 200
+    target = _node_trajectory(q_true, e, T, N * steps)
+    pl = plan_chebyshev(sysm.region(), T / N, ChebyshevConfig(tol=1e-13), omega=law.omega)
+    o = linear_tracking_gradient(12, 10, sysm.A.as_tuple(), sysm.basis, T, N, steps, np.zeros(ref.n), f,
+                                 law.as_tuple(), target, pl)
+    assert abs(o.J[0] - res.J) <= 2e-5 * abs(res.J)
+    assert rel_l2(o.grad[0], res.grad) <= 1e-5
+    assert rel_l2(o.qdag0[0], res.adjoint.eval(0.0)) <= 1e-5
