@@ -84,10 +84,16 @@ __global__ void __launch_bounds__(256) k_cheb_term(ChebTermArgs a) {
 }
 
 
-constexpr int CM_NT = 160;  // 5 warps, pairs of columns: computed width ≤ 320 (192 measured slower)
+#ifndef PX_CM_NT
+#define PX_CM_NT 160
+#endif
+#ifndef PX_CM_MINB
+#define PX_CM_MINB 2
+#endif
+constexpr int CM_NT = PX_CM_NT;  // 5 warps, pairs of columns: computed width ≤ 320 (192 measured slower)
 constexpr int CM_MAXT = 7;  // terms per pass (template M ≤ CM_MAXT)
 constexpr int CM_DEPTH = 5; // cp.async ring depth (rows)
-constexpr int CM_MINB = 2;  // resident CTAs per SM (3 measured slower: spills + smaller bands)
+constexpr int CM_MINB = PX_CM_MINB;  // resident CTAs per SM (3 measured slower: spills + smaller bands)
 
 struct ChebMarchArgs {
   const double* u_prev; long long prev_bs;  // U_{k−1} (unused on the first pass)
