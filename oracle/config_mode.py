@@ -78,6 +78,63 @@ def burgers_adjoint_apply(u, y, D, h):
     return dx_central(u * y, h) - dx_central(u, h) * y + D * lap
 
 
+def _split2(q, nx, ny):
+    """(…, 2n) state → U, V as (…, ny, nx) grids (x fastest; `problems.py:170-174`)."""
+    n = nx * ny
+    shp = q.shape[:-1]
+    return q[..., :n].reshape(shp + (ny, nx)), q[..., n:].reshape(shp + (ny, nx))
+
+
+def _d2(W, hx, hy):
+    """Periodic central Dx, Dy and the 5-point Laplacian of a (…, ny, nx) grid (`problems.py:98-134`)."""
+    e, w = np.roll(W, -1, axis=-1), np.roll(W, 1, axis=-1)
+    n_, s_ = np.roll(W, -1, axis=-2), np.roll(W, 1, axis=-2)
+    return (e - w) / (2.0 * hx), (n_ - s_) / (2.0 * hy), (e - 2.0 * W + w) / (hx * hx) + (n_ - 2.0 * W + s_) / (hy * hy)
+
+
+def burgers2d_rhs(q, f, D, hx, hy, nx, ny):
+    """Two-field viscous Burgers rhs (`problems.py:177-186`): −U∂xU − V∂yU + D∇²U + f_U and the
+    same for V; ``q`` and ``f`` are (…, 2n) with the U block first."""
+    U, V = _split2(q, nx, ny)
+    dUx, dUy, lU = _d2(U, hx, hy)
+    dVx, dVy, lV = _d2(V, hx, hy)
+    ru = -U * dUx - V * dUy + D * lU
+    rv = -U * dVx - V * dVy + D * lV
+    shp = q.shape[:-1]
+    return np.concatenate([ru.reshape(shp + (-1,)), rv.reshape(shp + (-1,))], axis=-1) + f
+
+
+def burgers2d_adjoint_apply(q, y, D, hx, hy, nx, ny):
+    """J(q)ᵀy of the two-field system (`problems.py:316-343`):
+    out_a = ∂x(U a) + ∂y(V a) − (∂xU) a − (∂xV) b + D∇²a,
+    out_b = ∂x(U b) + ∂y(V b) − (∂yU) a − (∂yV) b + D∇²b."""
+    U, V = _split2(q, nx, ny)
+    a, b = _split2(y, nx, ny)
+    dUx, dUy, _ = _d2(U, hx, hy)
+    dVx, dVy, _ = _d2(V, hx, hy)
+    dxUa, _, la = _d2(U * a, hx, hy)
+    _, dyVa, _ = _d2(V * a, hx, hy)
+    dxUb, _, _ = _d2(U * b, hx, hy)
+    _, dyVb, _ = _d2(V * b, hx, hy)
+    _, _, la = _d2(a, hx, hy)
+    _, _, lb = _d2(b, hx, hy)
+    oa = dxUa + dyVa - dUx * a - dVx * b + D * la
+    ob = dxUb + dyVb - dUy * a - dVy * b + D * lb
+    shp = np.broadcast_shapes(q.shape[:-1], y.shape[:-1])
+    return np.concatenate([oa.reshape(shp + (-1,)), ob.reshape(shp + (-1,))], axis=-1)
+
+
+def burgers_ops(nx, D, ny=None, hy=None):
+    """(rhs(u, f), adj(u, y), n) of the Burgers testbed: 1D one-field (ny None) or the
+    reference's 2D two-field system (state length 2·nx·ny)."""
+    hx = 2.0 * np.pi / nx
+    if ny is None:
+        return (lambda u, f: burgers_rhs(u, f, D, hx)), (lambda u, y: burgers_adjoint_apply(u, y, D, hx)), nx
+    hy = 2.0 * np.pi / ny if hy is None else hy
+    return ((lambda u, f: burgers2d_rhs(u, f, D, hx, hy, nx, ny)),
+            (lambda u, y: burgers2d_adjoint_apply(u, y, D, hx, hy, nx, ny)), 2 * nx * ny)
+
+
 # ---------------------------------------------------------------------------
 # Steppers and exponential actions
 # ---------------------------------------------------------------------------
@@ -712,8 +769,13 @@ def cheb_law_action(apply, plan: ChebPlan, v, G, law, t_top: float):
     return y
 
 
-def burgers_direct_law(u0, f, law, D, h_grid, h, S):
-    """Serial classical RK4 of u' = −u∘Dx u + D·L u + θ(t)·f keeping every node."""
+def burgers_direct_law(u0, f, law, D, h_grid, h, S, rhs=None):
+    """Serial classical RK4 of u' = −u∘Dx u + D·L u + θ(t)·f keeping every node (``rhs(u, f)``:
+    another right-hand side, e.g. the 2D two-field one of `burgers_ops`)."""
+    if rhs is not None:
+        burgers_rhs = lambda u, ff, D_, h_: rhs(u, ff)  # noqa: E731 (shadows the 1D rhs below)
+    else:
+        burgers_rhs = globals()["burgers_rhs"]
     traj = np.empty((S + 1,) + u0.shape)
     u = u0.copy()
     traj[0] = u
@@ -751,7 +813,7 @@ def tracking_cost(traj, target, T, h):
     return (h / T) * np.tensordot(w, e, axes=(0, 0))
 
 
-def burgers_tracking_hybrid(nx, D, T, offsets, u0, f, law, target, plans_for, qdag_T=None):
+def burgers_tracking_hybrid(nx, D, T, offsets, u0, f, law, target, plans_for, qdag_T=None, ny=None):
     """The reference's hybrid loop with the configs' numerics.
 
     * direct: serial RK4 with forcing θ(t)·f (`hybrid.py:185-191`, `problems.py:155-162`);
@@ -767,8 +829,10 @@ def burgers_tracking_hybrid(nx, D, T, offsets, u0, f, law, target, plans_for, qd
 
     ``offsets``: the slices' node offsets (P+1 ints, 0 … S), h = T/S. ``plans_for(ubar)`` returns
     the per-slice plans (slice p of span (offsets[p+1]−offsets[p])·h). Returns an OracleResult
-    whose ``grad`` is the field gradient (B, n)."""
-    n = nx
+    whose ``grad`` is the field gradient (B, n). ``ny``: the reference's 2D two-field Burgers on
+    an nx×ny grid (states, forcing, target and gradient of length 2·nx·ny, U block first)."""
+    rhs2, adj2, n = burgers_ops(nx, D, ny)
+    burgers_adjoint_apply = lambda u, y, D_, h_: adj2(u, y)  # noqa: E731 (1D or 2D operator)
     hg = 2.0 * np.pi / nx
     f = np.atleast_2d(np.asarray(f, dtype=np.float64))
     B = f.shape[0]
@@ -779,7 +843,7 @@ def burgers_tracking_hybrid(nx, D, T, offsets, u0, f, law, target, plans_for, qd
     h = T / S
     target = np.asarray(target, dtype=np.float64)
     tg = target[:, None, :] if target.ndim == 2 else target
-    traj = burgers_direct_law(u0, f, law, D, hg, h, S)
+    traj = burgers_direct_law(u0, f, law, D, hg, h, S, rhs=rhs2)
     J = tracking_cost(traj, tg, T, h)
     ubar = slice_means_var(traj, offsets)
     plans = plans_for(ubar)

@@ -336,6 +336,36 @@ def frozen_bounds(ubar: np.ndarray, grid: Grid, D: float) -> tuple[float, float,
     return float(np.min(diag - rad)), float(np.max(diag + rad)), float(np.max(im))
 
 
+def frozen_bounds_2d(qbar: np.ndarray, grid: Grid, D: float) -> tuple[float, float, float]:
+    """Raw field-of-values box (re_lo, re_hi, im) of B̄ = J(q̄)ᵀ for the two-field Burgers system
+    (`problems.py:316-343`), union over the rows of ``qbar`` (…, 2n; U block first).
+
+    B̄(a, b) = (Dx(Ūa) + Dy(V̄a) − (DxŪ)a − (DxV̄)b + D∇²a,  Dx(Ūb) + Dy(V̄b) − (DyŪ)a − (DyV̄)b + D∇²b).
+    Real parts of W(B̄) lie in the Gershgorin interval of the symmetric part (advective entries
+    (Ū_e − Ū_c)/(4hx) …, the diagonal −DxŪ resp. −DyV̄, the block coupling −½(DxV̄ + DyŪ), D∇²);
+    imaginary parts within the row sums of the skew part ((Ū_e + Ū_c)/(4hx) …, ½|DyŪ − DxV̄|)."""
+    q = np.asarray(qbar, dtype=np.float64).reshape(-1, 2 * grid.npoints)
+    n, nx, ny = grid.npoints, grid.nx, grid.ny
+    hx, hy = grid.hx, grid.hy
+    U = q[:, :n].reshape(-1, ny, nx)
+    V = q[:, n:].reshape(-1, ny, nx)
+    Ue, Uw = np.roll(U, -1, axis=2), np.roll(U, 1, axis=2)
+    Un, Us = np.roll(U, -1, axis=1), np.roll(U, 1, axis=1)
+    Ve, Vw = np.roll(V, -1, axis=2), np.roll(V, 1, axis=2)
+    Vn, Vs = np.roll(V, -1, axis=1), np.roll(V, 1, axis=1)
+    dUx, dUy = (Ue - Uw) / (2.0 * hx), (Un - Us) / (2.0 * hy)
+    dVx, dVy = (Ve - Vw) / (2.0 * hx), (Vn - Vs) / (2.0 * hy)
+    dd = 2.0 * D / (hx * hx) + 2.0 * D / (hy * hy)
+    rad = ((np.abs(Ue - U) + np.abs(U - Uw)) / (4.0 * hx) + (np.abs(Vn - V) + np.abs(V - Vs)) / (4.0 * hy)
+           + dd + 0.5 * np.abs(dVx + dUy))
+    im = ((np.abs(Ue + U) + np.abs(U + Uw)) / (4.0 * hx) + (np.abs(Vn + V) + np.abs(V + Vs)) / (4.0 * hy)
+          + 0.5 * np.abs(dUy - dVx))
+    da, db = -dUx - dd, -dVy - dd
+    lo = min(float(np.min(da - rad)), float(np.min(db - rad)))
+    hi = max(float(np.max(da + rad)), float(np.max(db + rad)))
+    return lo, hi, float(np.max(im))
+
+
 def frozen_region_from_bounds(re_lo: float, re_hi: float, im: float) -> SpectralRegion:
     """Quantised FOV box → region (Crouzeix–Palencia factor 1+√2).
 
