@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define PX_ABI_VERSION 4
+#define PX_ABI_VERSION 5
 
 enum {
   PX_OK = 0,
@@ -311,6 +311,11 @@ typedef struct px_hybrid_desc {
   const int* offsets;  /* P+1 node offsets 0 = o_0 < … < o_P = S (host); h = T/S */
   double law[4];       /* θ(t) */
   int target_batched;  /* 0: target (S+1)×n shared by the members; 1: (S+1)×B×n */
+  /* ny > 1: the reference's own 2D two-field Burgers testbed on an nx×ny grid (problems.py:177-186,
+   * 316-343): states, forcing, target and gradient are (U, V) pairs of length n = 2·nx·ny, the U
+   * block first, x fastest; hy the y spacing. ny ≤ 1: 1D (V ≡ 0), hy unused. */
+  int ny;
+  double hy;
 } px_hybrid_desc;
 enum {
   PX_HFIELD_J = 0,     /* (B)          tracking cost */

@@ -61,7 +61,7 @@ from .problems import (
     mode_basis,
 )
 from .solvers import solve_adjoint_linear, solve_direct_linear, solve_hybrid, synthesize_truth
-from .systems import System, build_field_system, build_system
+from .systems import System, build_burgers2d_system, build_field_system, build_system
 from .tracking import (
     HybridTrackingEngine,
     HybridTrackingResult,

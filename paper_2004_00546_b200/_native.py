@@ -27,7 +27,7 @@ PX_MAX_LOCAL_BLOCKS = 16
 (PX_FIELD_J, PX_FIELD_GRAD, PX_FIELD_UT, PX_FIELD_QDAG0, PX_FIELD_G, PX_FIELD_UBND,
  PX_FIELD_FROZEN_BOUNDS, PX_FIELD_VEND, PX_FIELD_WEND, PX_FIELD_TRAJ) = range(10)
 PX_FLAG_BOUNDARY_STATES, PX_FLAG_Z_ACCUM, PX_FLAG_FIELD_CONTROL = 1, 2, 4
-ABI_VERSION = 4
+ABI_VERSION = 5
 # kernel-variant keys (px_set_variant)
 VARIANTS = {"march2": 0, "march_cols": 1, "march_band": 2, "cheb_terms": 3, "cheb_strip": 4, "cheb_band": 5,
             "scan1d_cluster": 6, "burgers_cluster": 7, "cheb_terms_phi": 8, "krylov_ortho": 9}
@@ -81,6 +81,8 @@ class HybridDesc(ctypes.Structure):
         ("offsets", POINTER(c_int)),
         ("law", c_double * 4),
         ("target_batched", c_int),
+        ("ny", c_int),
+        ("hy", c_double),
     ]
 
 

@@ -10,12 +10,12 @@
 #include <cmath>
 #include <vector>
 
+#include "hybrid2d.h"
 #include "internal.h"
 
 namespace pxi {
 
-struct Hybrid {
-  Handle base;  // device, error text, allocations
+struct Hybrid : HybridHead {  // dim = 1 (hybrid2d.h: the common head)
   int nx = 0, B = 1, P = 1, S = 1, ppt = 1, target_b = 1;
   double D = 0.0, hx = 0.0, T = 1.0, h = 1.0;
   double law[4] = {1.0, 0.0, 0.0, 0.0};
@@ -49,6 +49,10 @@ struct Hybrid {
 namespace {
 
 Hybrid* H(void* p) { return static_cast<Hybrid*>(p); }
+// the 2D two-field handle (desc.ny > 1, hybrid2d.cu), or null for the 1D one
+Hybrid2D* H2(void* p) {
+  return p && static_cast<HybridHead*>(p)->dim == 2 ? static_cast<Hybrid2D*>(static_cast<HybridHead*>(p)) : nullptr;
+}
 
 int cuda_fail(Hybrid* hy, cudaError_t e, const char* what) {
   return fail(&hy->base, e == cudaErrorMemoryAllocation ? PX_ERR_NOMEM : PX_ERR_CUDA,
@@ -91,7 +95,7 @@ int px_hybrid_create(const px_hybrid_desc* d, void** out) {
   using namespace pxi;
   if (!d || !out) return fail(nullptr, PX_ERR_ARG, "px_hybrid_create: null argument");
   *out = nullptr;
-  if (d->nx < 3 || d->nx > 8192) return fail(nullptr, PX_ERR_ARG, "hybrid: nx must be in [3, 8192]");
+  if (d->nx < 3 || (d->ny <= 1 && d->nx > 8192)) return fail(nullptr, PX_ERR_ARG, "hybrid: nx must be in [3, 8192]");
   if (d->batch < 1 || d->nslices < 1 || !d->offsets) return fail(nullptr, PX_ERR_ARG, "hybrid: batch/nslices/offsets");
   if (!(d->T > 0) || !(d->D > 0) || !(d->hx > 0)) return fail(nullptr, PX_ERR_ARG, "hybrid: T, D, hx must be positive");
   if (!(d->law[3] >= 0.0)) return fail(nullptr, PX_ERR_ARG, "hybrid: law ω must be non-negative");
@@ -99,6 +103,7 @@ int px_hybrid_create(const px_hybrid_desc* d, void** out) {
   if (d->offsets[0] != 0) return fail(nullptr, PX_ERR_ARG, "hybrid: offsets must start at 0");
   for (int p = 0; p < P; ++p)
     if (d->offsets[p + 1] <= d->offsets[p]) return fail(nullptr, PX_ERR_ARG, "hybrid: offsets must increase");
+  if (d->ny > 1) return h2_create(d, out);  // the reference's 2D two-field testbed (hybrid2d.cu)
   // runs of PPT points per thread, PPT a power of two dividing n, n/PPT ≤ HYB_NT
   int ppt = 0;
   for (int c = 1; c <= 32; c *= 2)
@@ -152,6 +157,7 @@ int px_hybrid_create(const px_hybrid_desc* d, void** out) {
 
 void px_hybrid_destroy(void* p) {
   if (!p) return;
+  if (pxi::Hybrid2D* h2 = pxi::H2(p)) return pxi::h2_destroy(h2);
   Hybrid* hy = pxi::H(p);
   cudaSetDevice(hy->base.device);
   if (hy->side) cudaStreamSynchronize(hy->side);
@@ -165,13 +171,14 @@ void px_hybrid_destroy(void* p) {
 }
 
 const char* px_hybrid_last_error(const void* p) {
-  return p ? static_cast<const Hybrid*>(p)->base.err.c_str() : pxi::g_last_error.c_str();
+  return p ? static_cast<const pxi::HybridHead*>(p)->base.err.c_str() : pxi::g_last_error.c_str();
 }
 
 int px_hybrid_set_inputs(void* p, const double* u0, const double* f, const double* target, const double* qdag_T,
                          int mem, void* stream) {
   using namespace pxi;
   if (!p || !u0 || !f || !target) return fail(p ? &H(p)->base : nullptr, PX_ERR_ARG, "hybrid inputs: null pointer");
+  if (Hybrid2D* h2 = H2(p)) return h2_set_inputs(h2, u0, f, target, qdag_T, mem, (cudaStream_t)stream);
   Hybrid* hy = H(p);
   cudaSetDevice(hy->base.device);
   cudaStream_t s = (cudaStream_t)stream;
@@ -189,6 +196,7 @@ int px_hybrid_set_inputs(void* p, const double* u0, const double* f, const doubl
 int px_hybrid_direct(void* p, int overlap, void* stream) {
   using namespace pxi;
   if (!p) return fail(nullptr, PX_ERR_ARG, "null handle");
+  if (Hybrid2D* h2 = H2(p)) return h2_direct(h2, overlap, (cudaStream_t)stream);
   Hybrid* hy = H(p);
   if (!hy->inputs) return fail(&hy->base, PX_ERR_STATE, "hybrid: inputs not set");
   cudaSetDevice(hy->base.device);
@@ -240,6 +248,7 @@ int px_hybrid_direct(void* p, int overlap, void* stream) {
 int px_hybrid_bounds(void* p, double* out3, void* stream) {
   using namespace pxi;
   if (!p || !out3) return fail(p ? &H(p)->base : nullptr, PX_ERR_ARG, "null argument");
+  if (Hybrid2D* h2 = H2(p)) return h2_bounds(h2, out3, (cudaStream_t)stream);
   Hybrid* hy = H(p);
   if (!hy->direct_done) return fail(&hy->base, PX_ERR_STATE, "hybrid: run px_hybrid_direct first");
   cudaSetDevice(hy->base.device);
@@ -258,6 +267,7 @@ int px_hybrid_set_slice_plan(void* p, int sl, const px_cheb_plan* plan, const do
   using namespace pxi;
   if (!p || !plan || !plan->coef_exp || !plan->coef_phi)
     return fail(p ? &H(p)->base : nullptr, PX_ERR_ARG, "hybrid plan: null argument");
+  if (Hybrid2D* h2 = H2(p)) return h2_set_slice_plan(h2, sl, plan, gc, gs);
   Hybrid* hy = H(p);
   if (sl < 0 || sl >= hy->P) return fail(&hy->base, PX_ERR_ARG, "hybrid plan: slice out of range");
   if (plan->substeps < 1 || plan->degree < 1 || !(plan->scale > 0) || (plan->sigma != 1 && plan->sigma != -1))
@@ -285,6 +295,7 @@ int px_hybrid_set_slice_plan(void* p, int sl, const px_cheb_plan* plan, const do
 int px_hybrid_adjoint(void* p, void* stream) {
   using namespace pxi;
   if (!p) return fail(nullptr, PX_ERR_ARG, "null handle");
+  if (Hybrid2D* h2 = H2(p)) return h2_adjoint(h2, (cudaStream_t)stream);
   Hybrid* hy = H(p);
   if (!hy->direct_done) return fail(&hy->base, PX_ERR_STATE, "hybrid: run px_hybrid_direct first");
   cudaSetDevice(hy->base.device);
@@ -332,6 +343,7 @@ int px_hybrid_adjoint(void* p, void* stream) {
 int px_hybrid_get(void* p, int field, double* dst, size_t count, int mem, void* stream) {
   using namespace pxi;
   if (!p || !dst) return fail(p ? &H(p)->base : nullptr, PX_ERR_ARG, "null argument");
+  if (Hybrid2D* h2 = H2(p)) return h2_get(h2, field, dst, count, mem, (cudaStream_t)stream);
   Hybrid* hy = H(p);
   cudaSetDevice(hy->base.device);
   const size_t n = hy->nx, B = hy->B, P = hy->P, S = hy->S;
@@ -362,6 +374,7 @@ int px_hybrid_get(void* p, int field, double* dst, size_t count, int mem, void* 
 int px_hybrid_get_timing(void* p, double* ms) {
   using namespace pxi;
   if (!p || !ms) return fail(p ? &H(p)->base : nullptr, PX_ERR_ARG, "null argument");
+  if (Hybrid2D* h2 = H2(p)) return h2_get_timing(h2, ms);
   Hybrid* hy = H(p);
   if (!hy->direct_done) return fail(&hy->base, PX_ERR_STATE, "hybrid: no direct sweep timed");
   cudaSetDevice(hy->base.device);

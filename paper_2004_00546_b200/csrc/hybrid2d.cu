@@ -1,0 +1,723 @@
+// hybrid2d.cu — the reference's hybrid loop on its own 2D two-field Burgers testbed
+// (px_hybrid_* with desc.ny > 1): problems.py:177-186 (rhs), :316-343 (J(q)ᵀ), :346-366 (slice
+// means), hybrid.py:185-237 (serial direct sweep, per-slice adjoint solves, frozen spans),
+// optimization.py:84-112 (tracking cost, adjoint source, ∂L/∂f).
+//
+// State q = (U, V), 2n doubles per member, x fastest, the U block first (problems.py:170-174).
+// Everything lives in HBM and every RK4 stage / Chebyshev term is one launch over (points,
+// members or lanes): the fields are far larger than one CTA's registers for the grids this path
+// is for, and the launches of the serial sweep are dependent anyway. The overlap pipeline is
+// stream-level: when the serial sweep has stored the last node of slice p an event releases
+// that slice's adjoint solve (its 4·n_p stage launches) on a side stream while the sweep goes on.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "hybrid2d.h"
+
+namespace px {
+
+struct B2Geom {
+  int nx, ny;
+  double i2hx, i2hy;  // 1/(2hx), 1/(2hy)
+  double dx2, dy2;    // D/hx², D/hy²
+};
+
+__device__ __forceinline__ void b2_nbrs(int i, const B2Geom& g, int& e, int& w, int& n, int& s) {
+  const int y = i / g.nx, x = i - y * g.nx;
+  e = (x + 1 == g.nx) ? i + 1 - g.nx : i + 1;
+  w = (x == 0) ? i + g.nx - 1 : i - 1;
+  n = (y + 1 == g.ny) ? x : i + g.nx;
+  s = (y == 0) ? i + (g.ny - 1) * g.nx : i - g.nx;
+}
+
+// ---- serial direct sweep: one RK4 stage ------------------------------------------------------
+struct B2DirectArgs {
+  const double* win; long long win_bs;      // stage input W (neighbours read)
+  const double* base; long long base_bs;    // u_i
+  const double* accin; long long accin_bs;  // running u_i + Σ weights·k
+  double* wout;                             // next stage input u_i + cw·k (B × 2n; null at stage 4)
+  double* accout; long long accout_bs;
+  const double* f;                          // B × 2n forcing field
+  double cw, ca, theta;
+  B2Geom g;
+};
+
+__global__ void __launch_bounds__(256) k_b2_direct_stage(B2DirectArgs a) {
+  const int n = a.g.nx * a.g.ny;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const size_t b = blockIdx.y;
+  const double* U = a.win + b * a.win_bs;
+  const double* V = U + n;
+  int e, w, nn, s;
+  b2_nbrs(i, a.g, e, w, nn, s);
+  const double uc = U[i], ue = U[e], uw = U[w], un = U[nn], us = U[s];
+  const double vc = V[i], ve = V[e], vw = V[w], vn = V[nn], vs = V[s];
+  const double dUx = (ue - uw) * a.g.i2hx, dUy = (un - us) * a.g.i2hy;
+  const double dVx = (ve - vw) * a.g.i2hx, dVy = (vn - vs) * a.g.i2hy;
+  const double lU = a.g.dx2 * (ue - 2.0 * uc + uw) + a.g.dy2 * (un - 2.0 * uc + us);
+  const double lV = a.g.dx2 * (ve - 2.0 * vc + vw) + a.g.dy2 * (vn - 2.0 * vc + vs);
+  const double* f = a.f + b * 2 * n;
+  const double ku = -uc * dUx - vc * dUy + lU + a.theta * f[i];
+  const double kv = -uc * dVx - vc * dVy + lV + a.theta * f[n + i];
+  const double* bs = a.base + b * a.base_bs;
+  if (a.wout) {
+    double* wo = a.wout + b * 2 * n;
+    wo[i] = bs[i] + a.cw * ku;
+    wo[n + i] = bs[n + i] + a.cw * kv;
+  }
+  const double* ai = a.accin + b * a.accin_bs;
+  double* ao = a.accout + b * a.accout_bs;
+  ao[i] = ai[i] + a.ca * ku;
+  ao[n + i] = ai[n + i] + a.ca * kv;
+}
+
+// ---- tracking cost: per-member partial sums of w_j·‖traj_j − target_j‖² (fixed order) --------
+__global__ void __launch_bounds__(256) k_b2_cost_partial(double* partial, const double* traj, const double* target,
+                                                         int target_b, size_t n2, int S, int B) {
+  __shared__ double red[8];
+  const size_t b = blockIdx.y;
+  const size_t total = (size_t)(S + 1) * n2;
+  double acc = 0.0;
+  for (size_t m = (size_t)blockIdx.x * blockDim.x + threadIdx.x; m < total; m += (size_t)gridDim.x * blockDim.x) {
+    const size_t j = m / n2, i = m - j * n2;
+    const double d = traj[(j * B + b) * n2 + i] - target[(target_b > 1 ? j * B + b : j) * n2 + i];
+    acc += (j == 0 || j == (size_t)S ? 0.5 : 1.0) * d * d;
+  }
+  const double r = block_sum<256>(acc, red);
+  if (threadIdx.x == 0) partial[b * gridDim.x + blockIdx.x] = r;
+}
+
+__global__ void k_b2_cost_final(double* J, const double* partial, int m, double scale, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double s = 0.0;
+  for (int k = 0; k < m; ++k) s += partial[(size_t)b * m + k];
+  J[b] = scale * s;
+}
+
+// ---- slice means (trapezoid on the slice's nodes, problems.py:346-366) -----------------------
+__global__ void __launch_bounds__(256) k_b2_means(double* ubar, const double* traj, const int* offs, int B, size_t n2) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n2) return;
+  const size_t b = blockIdx.y, p = blockIdx.z;
+  const int lo = offs[p], hi = offs[p + 1];
+  double acc = 0.5 * traj[((size_t)lo * B + b) * n2 + i];
+  for (int j = lo + 1; j < hi; ++j) acc += traj[((size_t)j * B + b) * n2 + i];
+  acc += 0.5 * traj[((size_t)hi * B + b) * n2 + i];
+  ubar[(p * B + b) * n2 + i] = acc / (double)(hi - lo);
+}
+
+// ---- FOV box of the frozen operators J(q̄_p)ᵀ (problems.frozen_bounds_2d), per-block partials --
+__global__ void __launch_bounds__(256) k_b2_bounds(double* part, const double* ubar, int rows, B2Geom g, double D) {
+  __shared__ double red[3][8];
+  const int n = g.nx * g.ny;
+  double lo = INFINITY, hi = -INFINITY, im = 0.0;
+  bool bad = false;
+  const size_t total = (size_t)rows * n;
+  const double dd = 2.0 * g.dx2 + 2.0 * g.dy2;
+  for (size_t m = (size_t)blockIdx.x * blockDim.x + threadIdx.x; m < total; m += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = m / n;
+    const int i = (int)(m - r * n);
+    const double* U = ubar + r * 2 * n;
+    const double* V = U + n;
+    int e, w, nn, s;
+    b2_nbrs(i, g, e, w, nn, s);
+    const double uc = U[i], ue = U[e], uw = U[w], un = U[nn], us = U[s];
+    const double vc = V[i], ve = V[e], vw = V[w], vn = V[nn], vs = V[s];
+    const double dUx = (ue - uw) * g.i2hx, dUy = (un - us) * g.i2hy;
+    const double dVx = (ve - vw) * g.i2hx, dVy = (vn - vs) * g.i2hy;
+    const double rad = (fabs(ue - uc) + fabs(uc - uw)) * (0.5 * g.i2hx) + (fabs(vn - vc) + fabs(vc - vs)) * (0.5 * g.i2hy) +
+                       dd + 0.5 * fabs(dVx + dUy);
+    const double imv = (fabs(ue + uc) + fabs(uc + uw)) * (0.5 * g.i2hx) + (fabs(vn + vc) + fabs(vc + vs)) * (0.5 * g.i2hy) +
+                       0.5 * fabs(dUy - dVx);
+    const double da = -dUx - dd, db = -dVy - dd;
+    if (!(isfinite(rad) && isfinite(imv) && isfinite(da) && isfinite(db))) bad = true;
+    lo = fmin(lo, fmin(da, db) - rad);
+    hi = fmax(hi, fmax(da, db) + rad);
+    im = fmax(im, imv);
+  }
+  if (bad) lo = hi = im = NAN;  // fmin/fmax drop NaN: carry it explicitly
+  // block reduction (NaN-propagating)
+  auto comb = [](double x, double y, int op) {
+    if (x != x || y != y) return (double)NAN;
+    return op == 0 ? fmin(x, y) : fmax(x, y);
+  };
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = comb(lo, __shfl_down_sync(0xffffffffu, lo, o), 0);
+    hi = comb(hi, __shfl_down_sync(0xffffffffu, hi, o), 1);
+    im = comb(im, __shfl_down_sync(0xffffffffu, im, o), 1);
+  }
+  const int wp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  if (ln == 0) { red[0][wp] = lo; red[1][wp] = hi; red[2][wp] = im; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < 8; ++k) {
+      lo = comb(lo, red[0][k], 0);
+      hi = comb(hi, red[1][k], 1);
+      im = comb(im, red[2][k], 1);
+    }
+    part[3 * blockIdx.x + 0] = lo;
+    part[3 * blockIdx.x + 1] = hi;
+    part[3 * blockIdx.x + 2] = im;
+  }
+}
+
+// J(q)ᵀ(a, b) at point i (problems.py:316-343): out_a = ∂x(Ua) + ∂y(Va) − (∂xU)a − (∂xV)b + D∇²a,
+// out_b = ∂x(Ub) + ∂y(Vb) − (∂yU)a − (∂yV)b + D∇²b
+struct B2Pt {
+  double ue, uw, un, us, ve, vw, vn, vs;
+};
+__device__ __forceinline__ void b2_adj_apply(const B2Geom& g, const B2Pt& q, const double* A, const double* Bf, int i,
+                                             int e, int w, int nn, int s, double& oa, double& ob) {
+  const double ac = A[i], ae = A[e], aw = A[w], an = A[nn], as = A[s];
+  const double bc = Bf[i], be = Bf[e], bw = Bf[w], bn = Bf[nn], bs = Bf[s];
+  const double dUx = (q.ue - q.uw) * g.i2hx, dUy = (q.un - q.us) * g.i2hy;
+  const double dVx = (q.ve - q.vw) * g.i2hx, dVy = (q.vn - q.vs) * g.i2hy;
+  oa = (q.ue * ae - q.uw * aw) * g.i2hx + (q.vn * an - q.vs * as) * g.i2hy - dUx * ac - dVx * bc +
+       g.dx2 * (ae - 2.0 * ac + aw) + g.dy2 * (an - 2.0 * ac + as);
+  ob = (q.ue * be - q.uw * bw) * g.i2hx + (q.vn * bn - q.vs * bs) * g.i2hy - dUy * ac - dVy * bc +
+       g.dx2 * (be - 2.0 * bc + bw) + g.dy2 * (bn - 2.0 * bc + bs);
+}
+
+// ---- slice adjoint solves (hybrid.py:194-203): one RK4 stage of every active lane ------------
+struct B2AdjArgs {
+  const double* yin;    // L × 2n stage input (neighbours read)
+  double* a;            // L × 2n: a_i (base); stage 4 writes a_{i+1} here
+  const double* accin;  // L × 2n (stage 1: a)
+  double* accout;       // L × 2n (stage 4: a)
+  double* yout;         // L × 2n next stage input (null at stage 4)
+  double* z;            // L × 2n: ∫θ·a dt (RK4-consistent)
+  const double* traj;   // (S+1) × B × 2n
+  const double* target; // (S+1) × (B | 1) × 2n
+  const int* offs;
+  const double* theta;  // θ(k·h/2)
+  double wa, wb;        // stage state = wa·node[top] + wb·node[top − 1]
+  double cw, ca, cz;
+  int tsel;             // θ at node top (0), top − ½ (1), top − 1 (2)
+  int step, p0, pcount, P, B, target_b;
+  B2Geom g;
+};
+
+__global__ void __launch_bounds__(256) k_b2_adj_stage(B2AdjArgs a) {
+  const int n = a.g.nx * a.g.ny;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int b = blockIdx.y / a.pcount;
+  const int p = a.p0 + blockIdx.y % a.pcount;
+  const int np = a.offs[p + 1] - a.offs[p];
+  if (a.step >= np) return;
+  const int top = a.offs[p + 1] - a.step;
+  const size_t n2 = 2 * (size_t)n;
+  const size_t lane = (size_t)b * a.P + p;
+  const double* qa = a.traj + ((size_t)top * a.B + b) * n2;
+  const double* qb = a.traj + ((size_t)(top - 1) * a.B + b) * n2;
+  const double* ta = a.target + ((size_t)top * a.target_b + (a.target_b > 1 ? b : 0)) * n2;
+  const double* tb = a.target + ((size_t)(top - 1) * a.target_b + (a.target_b > 1 ? b : 0)) * n2;
+  int e, w, nn, s;
+  b2_nbrs(i, a.g, e, w, nn, s);
+  auto st = [&](size_t k) { return a.wa * qa[k] + a.wb * qb[k]; };
+  B2Pt q;
+  q.ue = st(e); q.uw = st(w); q.un = st(nn); q.us = st(s);
+  q.ve = st(n + e); q.vw = st(n + w); q.vn = st(n + nn); q.vs = st(n + s);
+  const double su = 2.0 * (st(i) - (a.wa * ta[i] + a.wb * tb[i]));
+  const double sv = 2.0 * (st(n + i) - (a.wa * ta[n + i] + a.wb * tb[n + i]));
+  const double* Y = a.yin + lane * n2;
+  double ka, kb;
+  b2_adj_apply(a.g, q, Y, Y + n, i, e, w, nn, s, ka, kb);
+  ka += su;
+  kb += sv;
+  const double th = a.theta[2 * top - a.tsel];
+  double* z = a.z + lane * n2;
+  z[i] += a.cz * th * Y[i];
+  z[n + i] += a.cz * th * Y[n + i];
+  const double* base = a.a + lane * n2;
+  const double* ai = a.accin + lane * n2;
+  const double ra = ai[i] + a.ca * ka, rb = ai[n + i] + a.ca * kb;
+  if (a.yout) {
+    double* yo = a.yout + lane * n2;
+    yo[i] = base[i] + a.cw * ka;
+    yo[n + i] = base[n + i] + a.cw * kb;
+  }
+  double* ao = a.accout + lane * n2;
+  ao[i] = ra;
+  ao[n + i] = rb;
+}
+
+// ---- frozen-operator carry: one Chebyshev term of exp(τ·J(q̄_p)ᵀ) with the law series ----------
+struct B2ChebArgs {
+  const double* x;     // B × 2n: U_k (neighbours read)
+  const double* prev;  // B × 2n: U_{k−1} (unused on the first term)
+  double* out;         // B × 2n: U_{k+1}
+  double* acc;         // B × 2n: Σ be_k U_k
+  double* G;           // B × 2n: += Σ bl_k U_k (the θ-weighted integral)
+  const double* qbar;  // B × 2n: the slice mean q̄_p
+  double alpha, c0, sg, be0, bek, bl0, blk;
+  int first;
+  B2Geom g;
+};
+
+__global__ void __launch_bounds__(256) k_b2_cheb_term(B2ChebArgs a) {
+  const int n = a.g.nx * a.g.ny;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const size_t off = (size_t)blockIdx.y * 2 * n;
+  const double* U = a.qbar + off;
+  const double* V = U + n;
+  int e, w, nn, s;
+  b2_nbrs(i, a.g, e, w, nn, s);
+  B2Pt q{U[e], U[w], U[nn], U[s], V[e], V[w], V[nn], V[s]};
+  const double* X = a.x + off;
+  double oa, ob;
+  b2_adj_apply(a.g, q, X, X + n, i, e, w, nn, s, oa, ob);
+  const double xa = X[i], xb = X[n + i];
+  double ua = a.alpha * (oa - a.c0 * xa), ub = a.alpha * (ob - a.c0 * xb);
+  double* acc = a.acc + off;
+  double* G = a.G + off;
+  if (a.first) {
+    acc[i] = a.be0 * xa + a.bek * ua;
+    acc[n + i] = a.be0 * xb + a.bek * ub;
+    G[i] += a.bl0 * xa + a.blk * ua;
+    G[n + i] += a.bl0 * xb + a.blk * ub;
+  } else {
+    const double* P = a.prev + off;
+    ua += a.sg * P[i];
+    ub += a.sg * P[n + i];
+    acc[i] += a.bek * ua;
+    acc[n + i] += a.bek * ub;
+    G[i] += a.blk * ua;
+    G[n + i] += a.blk * ub;
+  }
+  double* o = a.out + off;
+  o[i] = ua;
+  o[n + i] = ub;
+}
+
+// C[b] = (add ? C[b] : 0) + lanes[b·P + p]
+__global__ void k_b2_take_lane(double* C, const double* lanes, int P, int p, int add, size_t n2) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n2) return;
+  const size_t b = blockIdx.y;
+  const double v = lanes[(b * P + p) * n2 + i];
+  C[b * n2 + i] = add ? C[b * n2 + i] + v : v;
+}
+
+// grad[b] = (Σ_p zl[b·P + p] + G[b]) / T
+__global__ void k_b2_grad(double* grad, const double* zl, const double* G, int P, double invT, size_t n2) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n2) return;
+  const size_t b = blockIdx.y;
+  double s = 0.0;
+  for (int p = 0; p < P; ++p) s += zl[(b * P + p) * n2 + i];
+  grad[b * n2 + i] = (s + G[b * n2 + i]) * invT;
+}
+
+}  // namespace px
+
+namespace pxi {
+
+namespace {
+
+int cuda_fail2(Hybrid2D* hy, cudaError_t e, const char* what) {
+  return fail(&hy->base, e == cudaErrorMemoryAllocation ? PX_ERR_NOMEM : PX_ERR_CUDA,
+              std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define H2_CUDA(hy, call)                                      \
+  do {                                                         \
+    cudaError_t _e = (call);                                   \
+    if (_e != cudaSuccess) return cuda_fail2((hy), _e, #call); \
+  } while (0)
+
+#define H2_LAUNCHED(hy)                                                                       \
+  do {                                                                                        \
+    cudaError_t _e = cudaGetLastError();                                                      \
+    if (_e != cudaSuccess) return cuda_fail2((hy), _e, "kernel launch");                      \
+    (hy)->base.stats.kernel_launches++;                                                       \
+  } while (0)
+
+px::B2Geom geom(const Hybrid2D* hy) {
+  px::B2Geom g;
+  g.nx = hy->nx; g.ny = hy->ny;
+  g.i2hx = 1.0 / (2.0 * hy->hx); g.i2hy = 1.0 / (2.0 * hy->hy);
+  g.dx2 = hy->D / (hy->hx * hy->hx); g.dy2 = hy->D / (hy->hy * hy->hy);
+  return g;
+}
+
+int copy_in2(Hybrid2D* hy, double* dst, const double* src, size_t count, int mem, cudaStream_t s) {
+  H2_CUDA(hy, cudaMemcpyAsync(dst, src, count * sizeof(double),
+                              mem == PX_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  return PX_OK;
+}
+
+// the four RK4 stages of local step `step` of slices [p0, p0 + pcount) (all members)
+int adjoint_step(Hybrid2D* hy, int step, int p0, int pcount, cudaStream_t s) {
+  const int n = hy->nx * hy->ny;
+  px::B2AdjArgs a{};
+  a.a = hy->la; a.z = hy->lz; a.traj = hy->traj; a.target = hy->target; a.offs = hy->d_offs; a.theta = hy->theta;
+  a.step = step; a.p0 = p0; a.pcount = pcount; a.P = hy->P; a.B = hy->B; a.target_b = hy->target_b;
+  a.g = geom(hy);
+  const double h = hy->h;
+  const dim3 grid((unsigned)((n + 255) / 256), (unsigned)(hy->B * pcount));
+  // stage 1 at node top
+  a.yin = hy->la; a.accin = hy->la; a.accout = hy->lacc; a.yout = hy->ly[0];
+  a.wa = 1.0; a.wb = 0.0; a.tsel = 0; a.cw = 0.5 * h; a.ca = h / 6.0; a.cz = h / 6.0;
+  px::k_b2_adj_stage<<<grid, 256, 0, s>>>(a);
+  H2_LAUNCHED(hy);
+  // stages 2 and 3 at the half step (trajectory and target linearly interpolated, timestepping.py:64-75)
+  a.yin = hy->ly[0]; a.accin = hy->lacc; a.yout = hy->ly[1];
+  a.wa = 0.5; a.wb = 0.5; a.tsel = 1; a.ca = h / 3.0; a.cz = h / 3.0;
+  px::k_b2_adj_stage<<<grid, 256, 0, s>>>(a);
+  H2_LAUNCHED(hy);
+  a.yin = hy->ly[1]; a.yout = hy->ly[0]; a.cw = h;
+  px::k_b2_adj_stage<<<grid, 256, 0, s>>>(a);
+  H2_LAUNCHED(hy);
+  // stage 4 at node top − 1
+  a.yin = hy->ly[0]; a.accout = hy->la; a.yout = nullptr;
+  a.wa = 0.0; a.wb = 1.0; a.tsel = 2; a.ca = h / 6.0; a.cz = h / 6.0;
+  px::k_b2_adj_stage<<<grid, 256, 0, s>>>(a);
+  H2_LAUNCHED(hy);
+  return PX_OK;
+}
+
+}  // namespace
+
+int h2_create(const px_hybrid_desc* d, void** out) {
+  if (d->nx < 3 || d->ny < 3) return fail(nullptr, PX_ERR_ARG, "hybrid 2D: nx, ny must be ≥ 3");
+  if ((long long)d->nx * d->ny > (1LL << 28)) return fail(nullptr, PX_ERR_ARG, "hybrid 2D: grid too large");
+  if (!(d->hy > 0)) return fail(nullptr, PX_ERR_ARG, "hybrid 2D: hy must be positive");
+  const int P = d->nslices;
+  auto* hy = new Hybrid2D();
+  Handle* hb = &hy->base;
+  cudaGetDevice(&hb->device);
+  hy->nx = d->nx; hy->ny = d->ny; hy->B = d->batch; hy->P = P; hy->S = d->offsets[P];
+  hy->D = d->D; hy->hx = d->hx; hy->hy = d->hy; hy->T = d->T; hy->h = d->T / hy->S;
+  for (int k = 0; k < 4; ++k) hy->law[k] = d->law[k];
+  hy->target_b = d->target_batched ? hy->B : 1;
+  hy->offs.assign(d->offsets, d->offsets + P + 1);
+  hy->plans.resize(P);
+  hy->max_np = 0;
+  for (int p = 0; p < P; ++p) hy->max_np = std::max(hy->max_np, hy->offs[p + 1] - hy->offs[p]);
+  const size_t n2 = 2 * (size_t)hy->nx * hy->ny, B = hy->B, S = hy->S, L = B * P;
+  hy->cost_blocks = (int)std::min<size_t>(148 * 4, ((S + 1) * n2 + 255) / 256);
+  hy->bounds_blocks = (int)std::min<size_t>(148 * 2, ((size_t)P * B * (n2 / 2) + 255) / 256);
+  int rc = PX_OK;
+  auto al = [&](double** p, size_t cnt) { if (rc == PX_OK) rc = dalloc_t(hb, p, cnt); };
+  al(&hy->u0, B * n2); al(&hy->f, B * n2); al(&hy->target, (S + 1) * hy->target_b * n2); al(&hy->qT, B * n2);
+  al(&hy->traj, (S + 1) * B * n2); al(&hy->J, B); al(&hy->ubar, (size_t)P * B * n2);
+  al(&hy->qdag0, B * n2); al(&hy->grad, B * n2); al(&hy->G, B * n2);
+  al(&hy->w[0], B * n2); al(&hy->w[1], B * n2); al(&hy->w[2], B * n2); al(&hy->w[3], B * n2);
+  al(&hy->la, L * n2); al(&hy->lz, L * n2); al(&hy->lacc, L * n2); al(&hy->ly[0], L * n2); al(&hy->ly[1], L * n2);
+  al(&hy->cpart, B * (size_t)hy->cost_blocks); al(&hy->bpart, 3 * (size_t)hy->bounds_blocks);
+  if (rc == PX_OK) rc = dalloc_t(hb, &hy->d_offs, (size_t)P + 1);
+  if (rc == PX_OK && cudaMemcpy(hy->d_offs, d->offsets, sizeof(int) * (P + 1), cudaMemcpyHostToDevice) != cudaSuccess)
+    rc = fail(hb, PX_ERR_CUDA, "hybrid 2D: offsets upload");
+  if (rc == PX_OK) rc = dalloc_t(hb, &hy->theta, 2 * S + 1);
+  if (rc == PX_OK) {
+    hy->theta_host.resize(2 * S + 1);
+    for (size_t k = 0; k <= 2 * S; ++k) {
+      const double t = (double)k * (0.5 * hy->h);
+      hy->theta_host[k] = hy->law[0] + hy->law[1] * std::sin(hy->law[3] * t) + hy->law[2] * std::cos(hy->law[3] * t);
+    }
+    if (cudaMemcpy(hy->theta, hy->theta_host.data(), sizeof(double) * hy->theta_host.size(), cudaMemcpyHostToDevice) !=
+        cudaSuccess)
+      rc = fail(hb, PX_ERR_CUDA, "hybrid 2D: law table upload");
+  }
+  for (int k = 0; k < Hybrid2D::NSIDE && rc == PX_OK; ++k)
+    if (cudaStreamCreateWithFlags(&hy->side[k], cudaStreamNonBlocking) != cudaSuccess)
+      rc = fail(hb, PX_ERR_CUDA, "hybrid 2D: stream creation");
+  hy->ev_slice.assign(P, nullptr);
+  for (int p = 0; p < P && rc == PX_OK; ++p)
+    if (cudaEventCreateWithFlags(&hy->ev_slice[p], cudaEventDisableTiming) != cudaSuccess)
+      rc = fail(hb, PX_ERR_CUDA, "hybrid 2D: event creation");
+  for (int k = 0; k < Hybrid2D::NSIDE && rc == PX_OK; ++k)
+    if (cudaEventCreateWithFlags(&hy->ev_join[k], cudaEventDisableTiming) != cudaSuccess)
+      rc = fail(hb, PX_ERR_CUDA, "hybrid 2D: event creation");
+  for (int k = 0; k < 4 && rc == PX_OK; ++k)
+    if (cudaEventCreate(&hy->ev[k]) != cudaSuccess) rc = fail(hb, PX_ERR_CUDA, "hybrid 2D: event creation");
+  if (rc != PX_OK) {
+    h2_destroy(hy);
+    return rc;
+  }
+  *out = hy;
+  return PX_OK;
+}
+
+void h2_destroy(Hybrid2D* hy) {
+  cudaSetDevice(hy->base.device);
+  for (auto st : hy->side)
+    if (st) cudaStreamSynchronize(st);
+  for (void* a : hy->base.allocs) cudaFree(a);
+  for (auto st : hy->side)
+    if (st) cudaStreamDestroy(st);
+  for (auto e : hy->ev_slice)
+    if (e) cudaEventDestroy(e);
+  for (auto e : hy->ev_join)
+    if (e) cudaEventDestroy(e);
+  for (auto e : hy->ev)
+    if (e) cudaEventDestroy(e);
+  delete hy;
+}
+
+int h2_set_inputs(Hybrid2D* hy, const double* u0, const double* f, const double* target, const double* qdag_T, int mem,
+                  cudaStream_t s) {
+  cudaSetDevice(hy->base.device);
+  const size_t n2 = 2 * (size_t)hy->nx * hy->ny, B = hy->B;
+  PX_TRY(copy_in2(hy, hy->u0, u0, B * n2, mem, s));
+  PX_TRY(copy_in2(hy, hy->f, f, B * n2, mem, s));
+  PX_TRY(copy_in2(hy, hy->target, target, (size_t)(hy->S + 1) * hy->target_b * n2, mem, s));
+  hy->has_qT = qdag_T != nullptr;
+  if (qdag_T) PX_TRY(copy_in2(hy, hy->qT, qdag_T, B * n2, mem, s));
+  hy->inputs = true;
+  hy->direct_done = hy->adjoint_done = hy->means_done = false;
+  return PX_OK;
+}
+
+int h2_direct(Hybrid2D* hy, int overlap, cudaStream_t s) {
+  if (!hy->inputs) return fail(&hy->base, PX_ERR_STATE, "hybrid: inputs not set");
+  cudaSetDevice(hy->base.device);
+  const int n = hy->nx * hy->ny;
+  const size_t n2 = 2 * (size_t)n, B = hy->B, L = B * hy->P;
+  const double h = hy->h;
+  const bool ov = overlap && hy->P > 1;
+  H2_CUDA(hy, cudaMemsetAsync(hy->la, 0, L * n2 * sizeof(double), s));
+  H2_CUDA(hy, cudaMemsetAsync(hy->lz, 0, L * n2 * sizeof(double), s));
+  H2_CUDA(hy, cudaMemcpyAsync(hy->traj, hy->u0, B * n2 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  H2_CUDA(hy, cudaEventRecord(hy->ev[0], s));
+  if (ov) {  // the side streams start after the lane buffers are cleared
+    for (int k = 0; k < Hybrid2D::NSIDE; ++k) H2_CUDA(hy, cudaStreamWaitEvent(hy->side[k], hy->ev[0], 0));
+  }
+  px::B2DirectArgs a{};
+  a.f = hy->f;
+  a.g = geom(hy);
+  const dim3 grid((unsigned)((n + 255) / 256), (unsigned)B);
+  const long long bs = (long long)n2;
+  bool slices_marked = false;
+  int p = 0;
+  for (int i = 0; i < hy->S; ++i) {
+    const double* ui = hy->traj + (size_t)i * B * n2;
+    double* un = hy->traj + (size_t)(i + 1) * B * n2;
+    a.base = ui; a.base_bs = bs;
+    a.win = ui; a.win_bs = bs; a.accin = ui; a.accin_bs = bs; a.wout = hy->w[0]; a.accout = hy->w[2]; a.accout_bs = bs;
+    a.cw = 0.5 * h; a.ca = h / 6.0; a.theta = hy->theta_host[2 * i];
+    px::k_b2_direct_stage<<<grid, 256, 0, s>>>(a);
+    H2_LAUNCHED(hy);
+    a.win = hy->w[0]; a.accin = hy->w[2]; a.wout = hy->w[1]; a.ca = h / 3.0; a.theta = hy->theta_host[2 * i + 1];
+    px::k_b2_direct_stage<<<grid, 256, 0, s>>>(a);
+    H2_LAUNCHED(hy);
+    a.win = hy->w[1]; a.wout = hy->w[0]; a.cw = h;
+    px::k_b2_direct_stage<<<grid, 256, 0, s>>>(a);
+    H2_LAUNCHED(hy);
+    a.win = hy->w[0]; a.wout = nullptr; a.accout = un; a.ca = h / 6.0; a.theta = hy->theta_host[2 * i + 2];
+    px::k_b2_direct_stage<<<grid, 256, 0, s>>>(a);
+    H2_LAUNCHED(hy);
+    if (ov && i + 1 == hy->offs[p + 1]) {  // slice p is stored: release its adjoint solve on a side stream
+      cudaStream_t sd = hy->side[p % Hybrid2D::NSIDE];
+      H2_CUDA(hy, cudaEventRecord(hy->ev_slice[p], s));
+      H2_CUDA(hy, cudaStreamWaitEvent(sd, hy->ev_slice[p], 0));
+      if (!slices_marked) {
+        H2_CUDA(hy, cudaEventRecord(hy->ev[2], sd));
+        slices_marked = true;
+      }
+      const int np = hy->offs[p + 1] - hy->offs[p];
+      for (int k = 0; k < np; ++k) PX_TRY(adjoint_step(hy, k, p, 1, sd));
+      ++p;
+    }
+  }
+  H2_CUDA(hy, cudaEventRecord(hy->ev[1], s));
+  if (ov) {
+    // join: the last slice's stream carries the end-of-slices mark after every other side stream
+    cudaStream_t last = hy->side[(hy->P - 1) % Hybrid2D::NSIDE];
+    for (int k = 0; k < Hybrid2D::NSIDE; ++k) {
+      if (hy->side[k] == last) continue;
+      H2_CUDA(hy, cudaEventRecord(hy->ev_join[k], hy->side[k]));
+      H2_CUDA(hy, cudaStreamWaitEvent(last, hy->ev_join[k], 0));
+    }
+    H2_CUDA(hy, cudaEventRecord(hy->ev[3], last));
+    H2_CUDA(hy, cudaStreamWaitEvent(s, hy->ev[3], 0));
+  } else {
+    H2_CUDA(hy, cudaEventRecord(hy->ev[2], s));
+    for (int k = 0; k < hy->max_np; ++k) PX_TRY(adjoint_step(hy, k, 0, hy->P, s));
+    H2_CUDA(hy, cudaEventRecord(hy->ev[3], s));
+  }
+  // tracking cost
+  px::k_b2_cost_partial<<<dim3((unsigned)hy->cost_blocks, (unsigned)B), 256, 0, s>>>(hy->cpart, hy->traj, hy->target,
+                                                                                   hy->target_b, n2, hy->S, hy->B);
+  H2_LAUNCHED(hy);
+  px::k_b2_cost_final<<<(hy->B + 63) / 64, 64, 0, s>>>(hy->J, hy->cpart, hy->cost_blocks, h / hy->T, hy->B);
+  H2_LAUNCHED(hy);
+  hy->base.stats.rk4_lane_steps += (uint64_t)hy->B * hy->S * 2;
+  hy->overlapped = ov ? 1 : 0;
+  hy->direct_done = true;
+  hy->adjoint_done = hy->means_done = false;
+  return PX_OK;
+}
+
+int h2_bounds(Hybrid2D* hy, double* out3, cudaStream_t s) {
+  if (!hy->direct_done) return fail(&hy->base, PX_ERR_STATE, "hybrid: run px_hybrid_direct first");
+  cudaSetDevice(hy->base.device);
+  const int n = hy->nx * hy->ny;
+  const size_t n2 = 2 * (size_t)n;
+  px::k_b2_means<<<dim3((unsigned)((n2 + 255) / 256), (unsigned)hy->B, (unsigned)hy->P), 256, 0, s>>>(
+      hy->ubar, hy->traj, hy->d_offs, hy->B, n2);
+  H2_LAUNCHED(hy);
+  px::k_b2_bounds<<<hy->bounds_blocks, 256, 0, s>>>(hy->bpart, hy->ubar, hy->P * hy->B, geom(hy), hy->D);
+  H2_LAUNCHED(hy);
+  std::vector<double> part(3 * (size_t)hy->bounds_blocks);
+  H2_CUDA(hy, cudaMemcpyAsync(part.data(), hy->bpart, part.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  H2_CUDA(hy, cudaStreamSynchronize(s));
+  double lo = INFINITY, hi = -INFINITY, im = 0.0;
+  bool bad = false;
+  for (int k = 0; k < hy->bounds_blocks; ++k) {
+    const double a = part[3 * k], b = part[3 * k + 1], c = part[3 * k + 2];
+    if (a != a || b != b || c != c) bad = true;
+    lo = std::min(lo, a); hi = std::max(hi, b); im = std::max(im, c);
+  }
+  if (bad || !std::isfinite(lo) || !std::isfinite(hi) || !std::isfinite(im))
+    return fail(&hy->base, PX_ERR_NONFINITE, "hybrid: non-finite direct trajectory");
+  out3[0] = lo; out3[1] = hi; out3[2] = im;
+  hy->means_done = true;
+  return PX_OK;
+}
+
+int h2_set_slice_plan(Hybrid2D* hy, int sl, const px_cheb_plan* plan, const double* gc, const double* gs) {
+  if (sl < 0 || sl >= hy->P) return fail(&hy->base, PX_ERR_ARG, "hybrid plan: slice out of range");
+  if (plan->substeps < 1 || plan->degree < 1 || !(plan->scale > 0) || (plan->sigma != 1 && plan->sigma != -1))
+    return fail(&hy->base, PX_ERR_ARG, "hybrid plan: bad substeps/degree/scale/sigma");
+  if (hy->law[3] != 0.0 && (!gc || !gs))
+    return fail(&hy->base, PX_ERR_ARG, "hybrid plan: a sine/cosine time law needs the coef_gc / coef_gs series");
+  const double span = (hy->offs[sl + 1] - hy->offs[sl]) * hy->h;
+  if (std::fabs(plan->span - span) > 1e-12 * std::max(1.0, span))
+    return fail(&hy->base, PX_ERR_ARG, "hybrid plan: span does not match the slice width");
+  Hybrid2D::SlicePlan& sp = hy->plans[sl];
+  const int K = plan->degree;
+  sp.set = true;
+  sp.substeps = plan->substeps; sp.degree = K; sp.sigma = plan->sigma;
+  sp.c0 = plan->center; sp.d = plan->scale; sp.span = plan->span;
+  sp.be.assign(plan->coef_exp, plan->coef_exp + K + 1);
+  sp.law.assign((size_t)sp.substeps * (K + 1), 0.0);
+  const double tau = plan->span / plan->substeps;
+  const double t_top = hy->offs[sl + 1] * hy->h;
+  const double la = hy->law[0], lb = hy->law[1], lc = hy->law[2], lw = hy->law[3];
+  for (int j = 0; j < sp.substeps; ++j) {
+    double* out = sp.law.data() + (size_t)j * (K + 1);
+    const double tt = t_top - j * tau;
+    if (lw == 0.0) {
+      for (int k = 0; k <= K; ++k) out[k] = (la + lc) * plan->coef_phi[k];
+    } else {
+      const double A = lb * std::sin(lw * tt) + lc * std::cos(lw * tt);
+      const double Bc = -lb * std::cos(lw * tt) + lc * std::sin(lw * tt);
+      for (int k = 0; k <= K; ++k) out[k] = la * plan->coef_phi[k] + A * gc[k] + Bc * gs[k];
+    }
+  }
+  return PX_OK;
+}
+
+int h2_adjoint(Hybrid2D* hy, cudaStream_t s) {
+  if (!hy->direct_done) return fail(&hy->base, PX_ERR_STATE, "hybrid: run px_hybrid_direct first");
+  if (!hy->means_done) return fail(&hy->base, PX_ERR_STATE, "hybrid: run px_hybrid_bounds first (slice means)");
+  cudaSetDevice(hy->base.device);
+  const int top = hy->has_qT ? hy->P - 1 : hy->P - 2;
+  for (int q = 0; q <= top; ++q)
+    if (!hy->plans[q].set) return fail(&hy->base, PX_ERR_STATE, "hybrid: slice plan " + std::to_string(q) + " not set");
+  const int n = hy->nx * hy->ny;
+  const size_t n2 = 2 * (size_t)n, B = hy->B;
+  const dim3 gridn((unsigned)((n + 255) / 256), (unsigned)B);
+  const dim3 grid2((unsigned)((n2 + 255) / 256), (unsigned)B);
+  H2_CUDA(hy, cudaMemsetAsync(hy->G, 0, B * n2 * sizeof(double), s));
+  // the carry C lives in w[c]; the other three buffers hold the recurrence and the accumulator
+  int c = 0;
+  if (hy->has_qT) {
+    H2_CUDA(hy, cudaMemcpyAsync(hy->w[c], hy->qT, B * n2 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  } else {
+    px::k_b2_take_lane<<<grid2, 256, 0, s>>>(hy->w[c], hy->la, hy->P, hy->P - 1, 0, n2);
+    H2_LAUNCHED(hy);
+  }
+  px::B2ChebArgs a{};
+  a.G = hy->G;
+  a.g = geom(hy);
+  uint64_t terms = 0;
+  for (int p = top; p >= 0; --p) {
+    const Hybrid2D::SlicePlan& sp = hy->plans[p];
+    const int K = sp.degree;
+    a.qbar = hy->ubar + (size_t)p * B * n2;
+    a.c0 = sp.c0;
+    for (int j = 0; j < sp.substeps; ++j) {
+      const double* bl = sp.law.data() + (size_t)j * (K + 1);
+      int f1 = (c + 1) & 3, f2 = (c + 2) & 3, f3 = (c + 3) & 3;
+      // term 1: U_1 = (M − c0)U_0/d, acc = be0 U_0 + be1 U_1
+      a.x = hy->w[c]; a.prev = nullptr; a.out = hy->w[f1]; a.acc = hy->w[f2];
+      a.alpha = 1.0 / sp.d; a.sg = 0.0; a.first = 1;
+      a.be0 = sp.be[0]; a.bek = sp.be[1]; a.bl0 = bl[0]; a.blk = bl[1];
+      px::k_b2_cheb_term<<<gridn, 256, 0, s>>>(a);
+      H2_LAUNCHED(hy);
+      int prev = c, cur = f1, nxt = f3;
+      a.alpha = 2.0 / sp.d; a.sg = (double)sp.sigma; a.first = 0;
+      for (int k = 2; k <= K; ++k) {
+        a.x = hy->w[cur]; a.prev = hy->w[prev]; a.out = hy->w[nxt];
+        a.bek = sp.be[k]; a.blk = bl[k];
+        px::k_b2_cheb_term<<<gridn, 256, 0, s>>>(a);
+        H2_LAUNCHED(hy);
+        const int t = prev;
+        prev = cur; cur = nxt; nxt = t;
+      }
+      c = f2;  // the substep's result
+      terms += (uint64_t)K;
+    }
+    px::k_b2_take_lane<<<grid2, 256, 0, s>>>(hy->w[c], hy->la, hy->P, p, 1, n2);  // + a_p(T_p)
+    H2_LAUNCHED(hy);
+  }
+  H2_CUDA(hy, cudaMemcpyAsync(hy->qdag0, hy->w[c], B * n2 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  px::k_b2_grad<<<grid2, 256, 0, s>>>(hy->grad, hy->lz, hy->G, hy->P, 1.0 / hy->T, n2);
+  H2_LAUNCHED(hy);
+  hy->base.stats.exp_terms += terms * hy->B;
+  hy->adjoint_done = true;
+  return PX_OK;
+}
+
+int h2_get(Hybrid2D* hy, int field, double* dst, size_t count, int mem, cudaStream_t s) {
+  cudaSetDevice(hy->base.device);
+  const size_t n2 = 2 * (size_t)hy->nx * hy->ny, B = hy->B, P = hy->P, S = hy->S;
+  const double* src = nullptr;
+  size_t have = 0;
+  switch (field) {
+    case PX_HFIELD_J: src = hy->J; have = B; break;
+    case PX_HFIELD_GRAD: src = hy->grad; have = B * n2; break;
+    case PX_HFIELD_UT: src = hy->traj + S * B * n2; have = B * n2; break;
+    case PX_HFIELD_QDAG0: src = hy->qdag0; have = B * n2; break;
+    case PX_HFIELD_TRAJ: src = hy->traj; have = (S + 1) * B * n2; break;
+    case PX_HFIELD_AEND: src = hy->la; have = B * P * n2; break;
+    case PX_HFIELD_ZL: src = hy->lz; have = B * P * n2; break;
+    case PX_HFIELD_UBAR: src = hy->ubar; have = P * B * n2; break;
+    default: return fail(&hy->base, PX_ERR_ARG, "hybrid: unknown field");
+  }
+  const bool needs_adj = field == PX_HFIELD_GRAD || field == PX_HFIELD_QDAG0;
+  if ((needs_adj && !hy->adjoint_done) || (!needs_adj && !hy->direct_done) || (field == PX_HFIELD_UBAR && !hy->means_done))
+    return fail(&hy->base, PX_ERR_STATE, "hybrid: field not computed yet");
+  if (count != have) return fail(&hy->base, PX_ERR_ARG, "hybrid: count mismatch (" + std::to_string(have) + ")");
+  H2_CUDA(hy, cudaMemcpyAsync(dst, src, count * sizeof(double),
+                              mem == PX_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  if (mem != PX_MEM_DEVICE) H2_CUDA(hy, cudaStreamSynchronize(s));
+  return PX_OK;
+}
+
+int h2_get_timing(Hybrid2D* hy, double* ms) {
+  if (!hy->direct_done) return fail(&hy->base, PX_ERR_STATE, "hybrid: no direct sweep timed");
+  cudaSetDevice(hy->base.device);
+  H2_CUDA(hy, cudaEventSynchronize(hy->ev[3]));
+  H2_CUDA(hy, cudaEventSynchronize(hy->ev[1]));
+  float a = 0, b = 0, c = 0, e = 0;
+  H2_CUDA(hy, cudaEventElapsedTime(&a, hy->ev[0], hy->ev[1]));
+  H2_CUDA(hy, cudaEventElapsedTime(&b, hy->ev[2], hy->ev[3]));
+  H2_CUDA(hy, cudaEventElapsedTime(&c, hy->ev[0], hy->ev[3]));
+  H2_CUDA(hy, cudaEventElapsedTime(&e, hy->ev[1], hy->ev[3]));
+  ms[0] = a;
+  ms[1] = b;
+  ms[2] = std::max(a, c);
+  ms[3] = std::max(0.0f, e);
+  ms[4] = hy->overlapped;
+  return PX_OK;
+}
+
+}  // namespace pxi

@@ -17,7 +17,8 @@ reference's own layouts:
   the slice edge states, the adjoint with the source 2(q − q_true)); Burgers with "hybrid" or
   "serial" runs the hybrid tracking loop on the GPU (`tracking.py`): the reference's 1D-embedded
   Burgers (y-invariant U on an nx×ny grid, V ≡ 0) maps onto the 1D path, J and ∂L/∂f are
-  returned on the embedded grid;
+  returned on the embedded grid; a genuinely two-dimensional forcing (U and V) runs the
+  two-field 2D path (`csrc/hybrid2d.cu`) in the reference's own state layout;
 * `solve_direct_linear` / `solve_adjoint_linear` (`paraexp.py:221-326`) for the linear
   testbed with the reference's forcing f·sin(ωt) and a terminal adjoint condition.
 
@@ -39,7 +40,7 @@ from .expaction import ChebyshevConfig
 from .hybrid import TimeLaw, make_hybrid_plan
 from .partition import RK4Config
 from .problems import ADVECTION_DIFFUSION, BURGERS, Grid, ProblemSpec
-from .systems import System, build_field_system, build_system
+from .systems import System, build_burgers2d_system, build_field_system, build_system
 
 
 @dataclass(frozen=True)
@@ -73,8 +74,9 @@ def system_from_reference(ref_system):
         n = nx * ny
         U, V = f[:n].reshape(ny, nx), f[n:]
         if np.any(V != 0.0) or np.any(U != U[0]):
-            raise ConfigError("Burgers on the GPU path is 1D: a y-invariant U forcing and V ≡ 0 "
-                              "(the reference's 2D system embedding a 1D problem)")
+            # genuinely two-dimensional: the two-field path (hybrid2d.cu), the reference's own layout
+            sysm = build_burgers2d_system(Grid(nx, ny), ProblemSpec(BURGERS, (0.0, 0.0), float(spec.D), float(spec.T)))
+            return sysm, f.copy(), law, Embedding("field", nx, ny)
         sysm = build_system(Grid(nx), ProblemSpec(BURGERS, (0.0, 0.0), float(spec.D), float(spec.T)), 2)
         return sysm, U[0].copy(), law, Embedding("burgers1d", nx, ny)
     raise ConfigError(f"unknown problem kind {spec.kind!r}")

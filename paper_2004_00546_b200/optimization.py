@@ -223,6 +223,9 @@ def direct_adjoint_loop(
     """
     if objective not in ("terminal", "tracking"):
         raise ValueError(f"objective must be 'terminal' or 'tracking', not {objective!r}")
+    if getattr(system, "is_burgers2d", False) and objective != "tracking":
+        raise ConfigError("the two-field 2D Burgers testbed runs the reference's own loop: objective='tracking' "
+                          "with algorithm 'hybrid' or 'serial'")
     if objective == "tracking":
         return _tracking_loop(system, f, q_true, algorithm, N, rk, expaction, u0, backend, plan, time_law, overlap)
     if plan is not None:

@@ -34,7 +34,13 @@ class System:
 
     @property
     def n(self) -> int:
-        return self.grid.npoints
+        """State length: the grid's points, twice that for the two-field 2D Burgers system
+        (U block first, `problems.py:170-174`)."""
+        return self.grid.npoints * (2 if self.is_burgers2d else 1)
+
+    @property
+    def is_burgers2d(self) -> bool:
+        return self.spec.kind == BURGERS and self.grid.dim == 2
 
     @property
     def is_linear(self) -> bool:
@@ -57,8 +63,19 @@ class System:
 def build_system(grid: Grid, spec: ProblemSpec, K: int) -> System:
     """(`systems.py:106-117`) with a K-mode Fourier control instead of f·sin(ωt)."""
     if spec.kind == BURGERS and grid.dim != 1:
-        raise ValueError("the Burgers path is 1D (the reference's 2D system with V ≡ 0)")
+        raise ValueError("mode-basis Burgers is 1D (the reference's 2D system with V ≡ 0); the two-field 2D "
+                         "testbed takes field controls: build_burgers2d_system")
     return System(grid, spec, mode_basis(grid, K))
+
+
+def build_burgers2d_system(grid: Grid, spec: ProblemSpec) -> System:
+    """The reference's own Burgers testbed: two fields (U, V) on a 2D grid with a forcing field on
+    both components (`problems.py:177-186`, `systems.py:106-117`). It runs the hybrid / serial loop
+    with the tracking objective (`tracking.solve_hybrid_tracking`); the control and the gradient
+    are fields of length 2·nx·ny."""
+    if spec.kind != BURGERS or grid.dim != 2:
+        raise ValueError("build_burgers2d_system: a Burgers spec on a 2D grid")
+    return System(grid, spec, FieldBasis(2 * grid.npoints))
 
 
 def build_field_system(grid: Grid, spec: ProblemSpec) -> System:

@@ -60,6 +60,8 @@ class HybridTrackingEngine:
         self.step = system.spec.T / self.S
         d = N.HybridDesc()
         d.nx = system.grid.nx
+        d.ny = system.grid.ny if system.is_burgers2d else 0  # ny > 1: the two-field 2D testbed (hybrid2d.cu)
+        d.hy = system.grid.hy
         d.D = system.spec.D
         d.hx = system.grid.hx
         d.T = system.spec.T
@@ -290,8 +292,11 @@ def pilot_times(system: System, steps: int, rk: RK4Config, repeats: int, law: Ti
     offs = np.array([0, steps], dtype=np.int32)
     eng = HybridTrackingEngine(sysp, offs, law, 1, False)
     try:
-        x = system.grid.x1()
-        u0 = 0.5 * np.sin(x)
+        if system.is_burgers2d:
+            X, Y = system.grid.coordinates()
+            u0 = np.concatenate([0.5 * np.sin(X), 0.5 * np.sin(Y)])
+        else:
+            u0 = 0.5 * np.sin(system.grid.x1())
         f = np.zeros(system.n)
         tgt = np.zeros((steps + 1, system.n))
         dirs, adjs = [], []

@@ -46,7 +46,7 @@ def test_bindings_cover_the_header(lib):
 
 def test_abi_version_and_build_info(lib):
     from paper_2004_00546_b200 import _native as N
-    assert lib.px_abi_version() == N.ABI_VERSION == 4
+    assert lib.px_abi_version() == N.ABI_VERSION == 5
     assert b"sm_100a" in lib.px_build_info()
 
 

@@ -115,10 +115,13 @@ def test_binding_refuses_what_the_path_cannot_express(R):
     from paper_2004_00546_b200.errors import ConfigError
     from paper_2004_00546_b200.integration import direct_adjoint_loop, system_from_reference
     grid = R.Grid2D(8, 3)
-    f = np.concatenate([np.arange(24) * 0.1, np.zeros(24)])      # not y-invariant
-    bad = R.build_system(grid, R.ProblemSpec("burgers", 0.0, 0.05, 1.0, 0.5, f))
-    with pytest.raises(ConfigError):
-        system_from_reference(bad)
+    f = np.concatenate([np.arange(24) * 0.1, np.zeros(24)])      # not y-invariant: the two-field 2D path
+    two = R.build_system(grid, R.ProblemSpec("burgers", 0.0, 0.05, 1.0, 0.5, f))
+    sysm, f2, law, emb = system_from_reference(two)
+    assert sysm.is_burgers2d and sysm.n == 48 and np.array_equal(f2, f) and emb.kind == "field" and law.omega == 1.0
+    from paper_2004_00546_b200 import direct_adjoint_loop as loop
+    with pytest.raises(ConfigError):   # the two-field testbed runs the reference's own (tracking) loop only
+        loop(sysm, f2, np.zeros(48), "hybrid", N=2)
     with pytest.raises(ValueError):    # the binding is the cuda backend
         direct_adjoint_loop(_advdiff(R), np.zeros(120), None, "linear", backend="thread", dt=1e-3)
 
