@@ -16,6 +16,7 @@
 //               adjoint lanes with the source 2(u − u_t))
 //   hybrid.cu   C ABI of the reference's hybrid with its tracking objective (px_hybrid_*); its
 //               kernels (hybrid.cuh) are instantiated in burgers.cu
+//   hybrid2d.cu the same entry points on the reference's 2D two-field Burgers testbed (desc.ny > 1)
 #pragma once
 #include <cuda_runtime.h>
 #include <cufft.h>

@@ -1,0 +1,74 @@
+"""Device timing of the hybrid tracking path on the reference's own 2D two-field Burgers testbed
+(csrc/hybrid2d.cu): the reference's `configs/burgers_hybrid.json` shape (32×32, D = 1, ω = 1,
+T = 1) and larger grids; sequential vs stream-overlapped slice solves; whole-gradient time with
+events around the public solve; for the 32×32 case the CPU oracle's time for the same gradient.
+Prints one JSON line per variant."""
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def run(nx, ny, D, T, dt, P, k, with_oracle):
+    import torch
+
+    from paper_2004_00546_b200 import (
+        ChebyshevConfig, Grid, ProblemSpec, RK4Config, TimeLaw, build_burgers2d_system, make_hybrid_plan,
+        solve_hybrid_tracking, synthesize_trajectory)
+    from paper_2004_00546_b200.problems import BURGERS
+    sysm = build_burgers2d_system(Grid(nx, ny), ProblemSpec(BURGERS, (0.0, 0.0), D, T))
+    X, Y = sysm.grid.coordinates()
+    rk, cfg, law = RK4Config(dt), ChebyshevConfig(tol=1e-12), TimeLaw.sine(1.0)
+    f_true = np.concatenate([np.sin(X) * np.sin(Y)] * 2)
+    f = np.ones(sysm.n)
+    u0 = np.zeros(sysm.n)
+    target_host = synthesize_trajectory(sysm, f_true, rk, law)[:, 0, :]
+    target = torch.as_tensor(target_host, device="cuda")
+    plan = make_hybrid_plan(T, P, k)
+    for ov in (False, True):
+        for _ in range(2):
+            solve_hybrid_tracking(sysm, u0, f, target, plan, rk=rk, expaction=cfg, law=law, overlap=ov)
+        reps = []
+        for _ in range(4):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            a.record()
+            r = solve_hybrid_tracking(sysm, u0, f, target, plan, rk=rk, expaction=cfg, law=law, overlap=ov)
+            b.record()
+            torch.cuda.synchronize()
+            reps.append((a.elapsed_time(b), (time.perf_counter() - t0) * 1e3, r.timing))
+        best = min(reps, key=lambda z: z[0])
+        S = int(r.offsets[-1])
+        terms = sum(p.substeps * p.degree for p in r.plans[:-1])
+        print(json.dumps({"grid": [nx, ny], "steps": S, "slices": P, "k": k, "overlap": ov,
+                          "gradient_ms_events": best[0], "gradient_ms_wall": best[1], **best[2],
+                          "frozen_terms": terms, "J": float(r.J[0])}), flush=True)
+    if with_oracle:
+        from oracle.config_mode import burgers_tracking_hybrid
+        from paper_2004_00546_b200.expaction import plan_family
+        from paper_2004_00546_b200.problems import frozen_bounds_2d, frozen_region_from_bounds
+        offs = r.offsets
+        h = T / offs[-1]
+
+        def pf(ub):
+            reg = frozen_region_from_bounds(*frozen_bounds_2d(ub, sysm.grid, D))
+            return plan_family(reg, [(offs[p + 1] - offs[p]) * h for p in range(P)], cfg, omega=law.omega)
+
+        t0 = time.perf_counter()
+        o = burgers_tracking_hybrid(nx, D, T, offs, u0, f[None, :], law.as_tuple(), target_host, pf, ny=ny)
+        sec = time.perf_counter() - t0
+        print(json.dumps({"grid": [nx, ny], "cpu_oracle_s": sec, "cores": 1,
+                          "J_rel": abs(o.J[0] - r.J[0]) / abs(o.J[0]),
+                          "grad_rel": float(np.linalg.norm(o.grad - r.grad) / np.linalg.norm(o.grad))}), flush=True)
+
+
+if __name__ == "__main__":
+    run(32, 32, 1.0, 1.0, 1e-3, 16, 3.0, True)       # the reference's burgers_hybrid.json shape
+    run(128, 128, 0.05, 0.5, 1e-3, 16, 3.0, False)
+    run(512, 512, 0.01, 0.2, 1e-3, 8, 3.0, False)
