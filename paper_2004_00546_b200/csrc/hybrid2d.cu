@@ -11,6 +11,7 @@
 // that slice's adjoint solve (its 4·n_p stage launches) on a side stream while the sweep goes on.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "hybrid2d.h"
@@ -313,6 +314,379 @@ __global__ void k_b2_grad(double* grad, const double* zl, const double* G, int P
   grad[b * n2 + i] = (s + G[b * n2 + i]) * invT;
 }
 
+
+// =============================================================================================
+// On-chip variants for small grids (nx·ny ≤ B2S_MAX_N — the reference's 32×32 configs): the
+// whole state of a member (or of a slice lane) stays in shared memory and registers, so the
+// serial sweep is ONE kernel (one CTA per member, a CTA barrier per RK4 stage) instead of 4·S
+// dependent launches, every slice's adjoint solve is one CTA of a second kernel that waits on a
+// per-slice progress flag while the sweep is still running (as the 1D path, hybrid.cuh), and the
+// frozen-operator carry is one kernel per gradient.
+// =============================================================================================
+constexpr int B2S_NT = 512;
+constexpr int B2S_MAX_N = 2048;  // points per field: 4 state arrays of 2n doubles = 128 KB in the lane kernel
+
+// the two-field rhs at point i from a shared-memory state W = (U | V)
+__device__ __forceinline__ void b2s_rhs(const B2Geom& g, const double* W, int n, int i, int e, int w, int nn, int s,
+                                        double& ku, double& kv) {
+  const double* V = W + n;
+  const double uc = W[i], ue = W[e], uw = W[w], un = W[nn], us = W[s];
+  const double vc = V[i], ve = V[e], vw = V[w], vn = V[nn], vs = V[s];
+  const double dUx = (ue - uw) * g.i2hx, dUy = (un - us) * g.i2hy;
+  const double dVx = (ve - vw) * g.i2hx, dVy = (vn - vs) * g.i2hy;
+  ku = -uc * dUx - vc * dUy + g.dx2 * (ue - 2.0 * uc + uw) + g.dy2 * (un - 2.0 * uc + us);
+  kv = -uc * dVx - vc * dVy + g.dx2 * (ve - 2.0 * vc + vw) + g.dy2 * (vn - 2.0 * vc + vs);
+}
+
+struct B2sDirectArgs {
+  const double* u0;     // B × 2n
+  const double* f;      // B × 2n
+  double* traj;         // (S+1) × B × 2n
+  const double* theta;  // θ(k·h/2)
+  int* flags;           // B × P progress flags
+  const int* offs;      // P+1
+  int P, B, S;
+  double h;
+  B2Geom g;
+};
+
+template <int PPT>
+__global__ void __launch_bounds__(B2S_NT) k_b2s_direct(B2sDirectArgs a) {
+  extern __shared__ double b2s_sm[];
+  const int n = a.g.nx * a.g.ny, n2 = 2 * n;
+  const int t = threadIdx.x;
+  const size_t b = blockIdx.x;
+  double* W0 = b2s_sm;
+  double* W1 = b2s_sm + n2;
+  double u[PPT][2], acc[PPT][2], fr[PPT][2];
+  int ie[PPT], iw[PPT], in[PPT], is[PPT];
+  const double* u0 = a.u0 + b * n2;
+  const double* f = a.f + b * n2;
+  double* tr = a.traj + b * n2;
+  const size_t ns = (size_t)a.B * n2;
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int i = t + q * B2S_NT;
+    if (i < n) {
+      b2_nbrs(i, a.g, ie[q], iw[q], in[q], is[q]);
+      u[q][0] = u0[i]; u[q][1] = u0[n + i];
+      fr[q][0] = f[i]; fr[q][1] = f[n + i];
+      W0[i] = u[q][0]; W0[n + i] = u[q][1];
+      tr[i] = u[q][0]; tr[n + i] = u[q][1];
+    }
+  }
+  __syncthreads();
+  auto stage = [&](const double* Wi, double* Wo, double cw, double ca, double th, bool first) {
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const int i = t + q * B2S_NT;
+      if (i < n) {
+        double ku, kv;
+        b2s_rhs(a.g, Wi, n, i, ie[q], iw[q], in[q], is[q], ku, kv);
+        ku += th * fr[q][0];
+        kv += th * fr[q][1];
+        acc[q][0] = (first ? u[q][0] : acc[q][0]) + ca * ku;
+        acc[q][1] = (first ? u[q][1] : acc[q][1]) + ca * kv;
+        Wo[i] = u[q][0] + cw * ku;
+        Wo[n + i] = u[q][1] + cw * kv;
+      }
+    }
+  };
+  const double h = a.h;
+  int p = 0, next = a.offs[1];
+  for (int s = 0; s < a.S; ++s) {
+    const double th1 = a.theta[2 * s], th2 = a.theta[2 * s + 1], th4 = a.theta[2 * s + 2];
+    stage(W0, W1, 0.5 * h, h / 6.0, th1, true);
+    __syncthreads();
+    stage(W1, W0, 0.5 * h, h / 3.0, th2, false);
+    __syncthreads();
+    stage(W0, W1, h, h / 3.0, th2, false);
+    __syncthreads();
+    double* node = tr + (size_t)(s + 1) * ns;
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const int i = t + q * B2S_NT;
+      if (i < n) {
+        double ku, kv;
+        b2s_rhs(a.g, W1, n, i, ie[q], iw[q], in[q], is[q], ku, kv);
+        u[q][0] = acc[q][0] + (h / 6.0) * (ku + th4 * fr[q][0]);
+        u[q][1] = acc[q][1] + (h / 6.0) * (kv + th4 * fr[q][1]);
+        W0[i] = u[q][0]; W0[n + i] = u[q][1];
+        node[i] = u[q][0]; node[n + i] = u[q][1];
+      }
+    }
+    if (s + 1 == next) {  // slice p's nodes are stored: every writer fences, then one flag
+      __threadfence();
+      __syncthreads();
+      if (t == 0) atomicExch(a.flags + b * a.P + p, 1);
+      ++p;
+      next = (p < a.P) ? a.offs[p + 1] : -1;
+    } else {
+      __syncthreads();
+    }
+  }
+}
+
+struct B2sLaneArgs {
+  const double* traj;    // (S+1) × B × 2n
+  const double* target;  // (S+1) × tb × 2n
+  const int* offs;
+  const double* theta;
+  int* flags;
+  double* aend;          // (B·P) × 2n
+  double* zl;            // (B·P) × 2n
+  int P, B, target_b, wait;
+  double h;
+  B2Geom g;
+};
+
+// J(q)ᵀy at point i with the stage state q = wa·Qa + wb·Qb (MODE 0: Qa, 1: the node mean, 2: Qb)
+template <int MODE>
+__device__ __forceinline__ double b2s_state(const double* Qa, const double* Qb, int k) {
+  if constexpr (MODE == 0) return Qa[k];
+  else if constexpr (MODE == 2) return Qb[k];
+  else return 0.5 * Qa[k] + 0.5 * Qb[k];
+}
+
+template <int PPT>
+__global__ void __launch_bounds__(B2S_NT) k_b2s_lanes(B2sLaneArgs a) {
+  extern __shared__ double b2s_sm[];
+  const int n = a.g.nx * a.g.ny, n2 = 2 * n;
+  const int t = threadIdx.x;
+  const int lane = blockIdx.x, b = lane / a.P, p = lane % a.P;
+  const int o0 = a.offs[p], o1 = a.offs[p + 1];
+  if (a.wait) {
+    if (t == 0) {
+      volatile int* fl = a.flags + lane;
+      while (*fl == 0) __nanosleep(200);
+      __threadfence();
+    }
+    __syncthreads();
+  }
+  double* Y0 = b2s_sm;
+  double* Y1 = Y0 + n2;
+  double* Qa = Y1 + n2;
+  double* Qb = Qa + n2;
+  const size_t ns = (size_t)a.B * n2, ts = (size_t)a.target_b * n2;
+  const double* nb = a.traj + (size_t)b * n2;
+  const double* tg = a.target + (a.target_b > 1 ? (size_t)b * n2 : 0);
+  double av[PPT][2], acc[PPT][2], z[PPT][2], ta[PPT][2], tb[PPT][2];
+  int ie[PPT], iw[PPT], in[PPT], is[PPT];
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int i = t + q * B2S_NT;
+    if (i < n) {
+      b2_nbrs(i, a.g, ie[q], iw[q], in[q], is[q]);
+      av[q][0] = av[q][1] = z[q][0] = z[q][1] = 0.0;
+      Y0[i] = 0.0; Y0[n + i] = 0.0;
+      Qa[i] = __ldcg(nb + (size_t)o1 * ns + i);
+      Qa[n + i] = __ldcg(nb + (size_t)o1 * ns + n + i);
+      ta[q][0] = tg[(size_t)o1 * ts + i];
+      ta[q][1] = tg[(size_t)o1 * ts + n + i];
+    }
+  }
+  const double h = a.h;
+  auto stage = [&](auto mode, const double* Yi, double* Yo, double cw, double ca, double cz, double th, bool first,
+                   bool last) {
+    constexpr int MODE = decltype(mode)::value;
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const int i = t + q * B2S_NT;
+      if (i < n) {
+        B2Pt s;
+        s.ue = b2s_state<MODE>(Qa, Qb, ie[q]); s.uw = b2s_state<MODE>(Qa, Qb, iw[q]);
+        s.un = b2s_state<MODE>(Qa, Qb, in[q]); s.us = b2s_state<MODE>(Qa, Qb, is[q]);
+        s.ve = b2s_state<MODE>(Qa, Qb, n + ie[q]); s.vw = b2s_state<MODE>(Qa, Qb, n + iw[q]);
+        s.vn = b2s_state<MODE>(Qa, Qb, n + in[q]); s.vs = b2s_state<MODE>(Qa, Qb, n + is[q]);
+        double ka, kb;
+        b2_adj_apply(a.g, s, Yi, Yi + n, i, ie[q], iw[q], in[q], is[q], ka, kb);
+        double tu, tv;
+        if constexpr (MODE == 0) { tu = ta[q][0]; tv = ta[q][1]; }
+        else if constexpr (MODE == 2) { tu = tb[q][0]; tv = tb[q][1]; }
+        else { tu = 0.5 * ta[q][0] + 0.5 * tb[q][0]; tv = 0.5 * ta[q][1] + 0.5 * tb[q][1]; }
+        ka += 2.0 * (b2s_state<MODE>(Qa, Qb, i) - tu);
+        kb += 2.0 * (b2s_state<MODE>(Qa, Qb, n + i) - tv);
+        z[q][0] += cz * th * Yi[i];
+        z[q][1] += cz * th * Yi[n + i];
+        const double ra = (first ? av[q][0] : acc[q][0]) + ca * ka;
+        const double rb = (first ? av[q][1] : acc[q][1]) + ca * kb;
+        if (last) {
+          av[q][0] = ra; av[q][1] = rb;
+          Yo[i] = ra; Yo[n + i] = rb;
+        } else {
+          acc[q][0] = ra; acc[q][1] = rb;
+          Yo[i] = av[q][0] + cw * ka;
+          Yo[n + i] = av[q][1] + cw * kb;
+        }
+      }
+    }
+  };
+  for (int top = o1; top > o0; --top) {
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const int i = t + q * B2S_NT;
+      if (i < n) {
+        Qb[i] = __ldcg(nb + (size_t)(top - 1) * ns + i);
+        Qb[n + i] = __ldcg(nb + (size_t)(top - 1) * ns + n + i);
+        tb[q][0] = tg[(size_t)(top - 1) * ts + i];
+        tb[q][1] = tg[(size_t)(top - 1) * ts + n + i];
+      }
+    }
+    __syncthreads();
+    const double th0 = a.theta[2 * top], th1 = a.theta[2 * top - 1], th2 = a.theta[2 * top - 2];
+    stage(IC<0>{}, Y0, Y1, 0.5 * h, h / 6.0, h / 6.0, th0, true, false);
+    __syncthreads();
+    stage(IC<1>{}, Y1, Y0, 0.5 * h, h / 3.0, h / 3.0, th1, false, false);
+    __syncthreads();
+    stage(IC<1>{}, Y0, Y1, h, h / 3.0, h / 3.0, th1, false, false);
+    __syncthreads();
+    stage(IC<2>{}, Y1, Y0, 0.0, h / 6.0, h / 6.0, th2, false, true);
+    __syncthreads();
+    double* sw = Qa; Qa = Qb; Qb = sw;
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) { ta[q][0] = tb[q][0]; ta[q][1] = tb[q][1]; }
+  }
+  double* ae = a.aend + (size_t)lane * n2;
+  double* zo = a.zl + (size_t)lane * n2;
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int i = t + q * B2S_NT;
+    if (i < n) {
+      ae[i] = av[q][0]; ae[n + i] = av[q][1];
+      zo[i] = z[q][0]; zo[n + i] = z[q][1];
+    }
+  }
+}
+
+struct B2sScanArgs {
+  const double* ubar;         // P × B × 2n
+  const double* aend;         // (B·P) × 2n
+  const double* zl;           // (B·P) × 2n
+  const double* qT;           // B × 2n or null
+  const HybSlicePlan* plans;  // P
+  const double* coef;         // pool: exp series per slice, law series per (slice, substep)
+  double* qdag0;              // B × 2n
+  double* grad;               // B × 2n
+  int P, B;
+  double invT;
+  B2Geom g;
+};
+
+template <int PPT>
+__global__ void __launch_bounds__(B2S_NT) k_b2s_scan(B2sScanArgs a) {
+  extern __shared__ double b2s_sm[];
+  const int n = a.g.nx * a.g.ny, n2 = 2 * n;
+  const int t = threadIdx.x;
+  const size_t b = blockIdx.x;
+  double* X[3] = {b2s_sm, b2s_sm + n2, b2s_sm + 2 * n2};
+  double* Qm = b2s_sm + 3 * n2;
+  double acc[PPT][2], G[PPT][2];
+  int ie[PPT], iw[PPT], in[PPT], is[PPT];
+  const int top = a.qT ? a.P - 1 : a.P - 2;
+  const double* c0src = a.qT ? a.qT + b * n2 : a.aend + (b * a.P + (a.P - 1)) * n2;
+  int c = 0;
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int i = t + q * B2S_NT;
+    if (i < n) {
+      b2_nbrs(i, a.g, ie[q], iw[q], in[q], is[q]);
+      G[q][0] = G[q][1] = 0.0;
+      X[0][i] = c0src[i]; X[0][n + i] = c0src[n + i];
+    }
+  }
+  for (int p = top; p >= 0; --p) {
+    const double* qb = a.ubar + ((size_t)p * a.B + b) * n2;
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const int i = t + q * B2S_NT;
+      if (i < n) { Qm[i] = qb[i]; Qm[n + i] = qb[n + i]; }
+    }
+    __syncthreads();
+    const HybSlicePlan pl = a.plans[p];
+    const double* be = a.coef + pl.exp_off;
+    const int K = pl.degree;
+    for (int j = 0; j < pl.substeps; ++j) {
+      const double* bl = a.coef + pl.law_off + (size_t)j * (K + 1);
+      int prv = c, cur = (c + 1) % 3, nxt = (c + 2) % 3;
+      // term 1
+      {
+        const double inv = 1.0 / pl.d;
+        const double* Xc = X[c];
+        double* Xo = X[cur];
+#pragma unroll
+        for (int q = 0; q < PPT; ++q) {
+          const int i = t + q * B2S_NT;
+          if (i < n) {
+            B2Pt s{Qm[ie[q]], Qm[iw[q]], Qm[in[q]], Qm[is[q]], Qm[n + ie[q]], Qm[n + iw[q]], Qm[n + in[q]], Qm[n + is[q]]};
+            double oa, ob;
+            b2_adj_apply(a.g, s, Xc, Xc + n, i, ie[q], iw[q], in[q], is[q], oa, ob);
+            const double xa = Xc[i], xb = Xc[n + i];
+            const double ua = inv * (oa - pl.c0 * xa), ub = inv * (ob - pl.c0 * xb);
+            acc[q][0] = be[0] * xa + be[1] * ua;
+            acc[q][1] = be[0] * xb + be[1] * ub;
+            G[q][0] += bl[0] * xa + bl[1] * ua;
+            G[q][1] += bl[0] * xb + bl[1] * ub;
+            Xo[i] = ua; Xo[n + i] = ub;
+          }
+        }
+        __syncthreads();
+      }
+      const double two = 2.0 / pl.d, sg = (double)pl.sigma;
+      for (int k = 2; k <= K; ++k) {
+        const double* Xc = X[cur];
+        const double* Xp = X[prv];
+        double* Xo = X[nxt];
+        const double bek = be[k], blk = bl[k];
+#pragma unroll
+        for (int q = 0; q < PPT; ++q) {
+          const int i = t + q * B2S_NT;
+          if (i < n) {
+            B2Pt s{Qm[ie[q]], Qm[iw[q]], Qm[in[q]], Qm[is[q]], Qm[n + ie[q]], Qm[n + iw[q]], Qm[n + in[q]], Qm[n + is[q]]};
+            double oa, ob;
+            b2_adj_apply(a.g, s, Xc, Xc + n, i, ie[q], iw[q], in[q], is[q], oa, ob);
+            const double ua = two * (oa - pl.c0 * Xc[i]) + sg * Xp[i];
+            const double ub = two * (ob - pl.c0 * Xc[n + i]) + sg * Xp[n + i];
+            acc[q][0] += bek * ua; acc[q][1] += bek * ub;
+            G[q][0] += blk * ua; G[q][1] += blk * ub;
+            Xo[i] = ua; Xo[n + i] = ub;   // Xo ≠ Xc, Xp: safe without a barrier before the write
+          }
+        }
+        __syncthreads();
+        const int tmp = prv; prv = cur; cur = nxt; nxt = tmp;
+      }
+      // the substep's result becomes the next input (nxt is free: its last readers passed the barrier)
+      const bool slice_end = j + 1 == pl.substeps;
+      const double* ae = a.aend + (b * a.P + p) * n2;
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) {
+        const int i = t + q * B2S_NT;
+        if (i < n) {
+          X[nxt][i] = acc[q][0] + (slice_end ? ae[i] : 0.0);       // + a_p(T_p) after slice p's action
+          X[nxt][n + i] = acc[q][1] + (slice_end ? ae[n + i] : 0.0);
+        }
+      }
+      c = nxt;
+      __syncthreads();
+    }
+  }
+  double* qo = a.qdag0 + b * n2;
+  double* go = a.grad + b * n2;
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int i = t + q * B2S_NT;
+    if (i < n) {
+      qo[i] = X[c][i]; qo[n + i] = X[c][n + i];
+      double su = 0.0, sv = 0.0;
+      for (int p = 0; p < a.P; ++p) {
+        su += a.zl[(b * a.P + p) * n2 + i];
+        sv += a.zl[(b * a.P + p) * n2 + n + i];
+      }
+      go[i] = (su + G[q][0]) * a.invT;
+      go[n + i] = (sv + G[q][1]) * a.invT;
+    }
+  }
+}
+
 }  // namespace px
 
 namespace pxi {
@@ -381,6 +755,118 @@ int adjoint_step(Hybrid2D* hy, int step, int p0, int pcount, cudaStream_t s) {
   return PX_OK;
 }
 
+
+template <typename F>
+cudaError_t b2s_dispatch(int ppt, F&& f) {
+  switch (ppt) {
+    case 1: return f(px::IC<1>{});
+    case 2: return f(px::IC<2>{});
+    default: return f(px::IC<4>{});
+  }
+}
+
+cudaError_t b2s_launch_direct(const px::B2sDirectArgs& a, int ppt, size_t smem, cudaStream_t s) {
+  return b2s_dispatch(ppt, [&](auto pc) {
+    constexpr int PPT = decltype(pc)::value;
+    cudaError_t e = cudaFuncSetAttribute(px::k_b2s_direct<PPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    px::k_b2s_direct<PPT><<<a.B, px::B2S_NT, smem, s>>>(a);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t b2s_launch_lanes(const px::B2sLaneArgs& a, int ppt, size_t smem, cudaStream_t s) {
+  return b2s_dispatch(ppt, [&](auto pc) {
+    constexpr int PPT = decltype(pc)::value;
+    cudaError_t e = cudaFuncSetAttribute(px::k_b2s_lanes<PPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    px::k_b2s_lanes<PPT><<<a.B * a.P, px::B2S_NT, smem, s>>>(a);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t b2s_launch_scan(const px::B2sScanArgs& a, int ppt, size_t smem, cudaStream_t s) {
+  return b2s_dispatch(ppt, [&](auto pc) {
+    constexpr int PPT = decltype(pc)::value;
+    cudaError_t e = cudaFuncSetAttribute(px::k_b2s_scan<PPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    px::k_b2s_scan<PPT><<<a.B, px::B2S_NT, smem, s>>>(a);
+    return cudaGetLastError();
+  });
+}
+
+// the on-chip sweep: one kernel for the serial direct (one CTA per member), one for every slice's
+// adjoint solve (one CTA per lane), overlapped through the progress flags when all CTAs fit
+int direct_small(Hybrid2D* hy, int overlap, cudaStream_t s) {
+  const size_t n2 = 2 * (size_t)hy->nx * hy->ny;
+  int sms = 0;
+  H2_CUDA(hy, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, hy->base.device));
+  const bool ov = overlap && hy->P > 1 && (long long)hy->B * hy->P + hy->B <= sms;
+  px::B2sDirectArgs d{};
+  d.u0 = hy->u0; d.f = hy->f; d.traj = hy->traj; d.theta = hy->theta; d.flags = hy->flags; d.offs = hy->d_offs;
+  d.P = hy->P; d.B = hy->B; d.S = hy->S; d.h = hy->h; d.g = geom(hy);
+  px::B2sLaneArgs l{};
+  l.traj = hy->traj; l.target = hy->target; l.offs = hy->d_offs; l.theta = hy->theta; l.flags = hy->flags;
+  l.aend = hy->la; l.zl = hy->lz; l.P = hy->P; l.B = hy->B; l.target_b = hy->target_b; l.wait = ov ? 1 : 0;
+  l.h = hy->h; l.g = geom(hy);
+  H2_CUDA(hy, cudaMemsetAsync(hy->flags, 0, sizeof(int) * hy->B * hy->P, s));
+  H2_CUDA(hy, cudaEventRecord(hy->ev[0], s));
+  if (ov) {
+    cudaStream_t sd = hy->side[0];
+    H2_CUDA(hy, cudaStreamWaitEvent(sd, hy->ev[0], 0));
+    H2_CUDA(hy, b2s_launch_direct(d, hy->ppt, 2 * n2 * sizeof(double), s));
+    H2_CUDA(hy, cudaEventRecord(hy->ev[1], s));
+    H2_CUDA(hy, cudaEventRecord(hy->ev[2], sd));
+    H2_CUDA(hy, b2s_launch_lanes(l, hy->ppt, 4 * n2 * sizeof(double), sd));
+    H2_CUDA(hy, cudaEventRecord(hy->ev[3], sd));
+    H2_CUDA(hy, cudaStreamWaitEvent(s, hy->ev[3], 0));
+  } else {
+    H2_CUDA(hy, b2s_launch_direct(d, hy->ppt, 2 * n2 * sizeof(double), s));
+    H2_CUDA(hy, cudaEventRecord(hy->ev[1], s));
+    H2_CUDA(hy, cudaEventRecord(hy->ev[2], s));
+    H2_CUDA(hy, b2s_launch_lanes(l, hy->ppt, 4 * n2 * sizeof(double), s));
+    H2_CUDA(hy, cudaEventRecord(hy->ev[3], s));
+  }
+  hy->base.stats.kernel_launches += 2;
+  hy->overlapped = ov ? 1 : 0;
+  return PX_OK;
+}
+
+int adjoint_small(Hybrid2D* hy, cudaStream_t s) {
+  const size_t n2 = 2 * (size_t)hy->nx * hy->ny;
+  if (hy->plans_dirty) {
+    std::vector<double> pool;
+    std::vector<px::HybSlicePlan> table(hy->P);
+    for (int q = 0; q < hy->P; ++q) {
+      const Hybrid2D::SlicePlan& sp = hy->plans[q];
+      px::HybSlicePlan& t = table[q];
+      t.substeps = sp.set ? sp.substeps : 0;
+      t.degree = sp.degree; t.sigma = sp.sigma; t.c0 = sp.c0; t.d = sp.set ? sp.d : 1.0;
+      t.exp_off = (int)pool.size();
+      pool.insert(pool.end(), sp.be.begin(), sp.be.end());
+      t.law_off = (int)pool.size();
+      pool.insert(pool.end(), sp.law.begin(), sp.law.end());
+    }
+    if (pool.empty()) pool.push_back(0.0);
+    if (pool.size() > hy->coef_cap) {
+      if (hy->d_coef) cudaFree(hy->d_coef);
+      hy->d_coef = nullptr;
+      H2_CUDA(hy, cudaMalloc(&hy->d_coef, pool.size() * sizeof(double)));
+      hy->coef_cap = pool.size();
+    }
+    H2_CUDA(hy, cudaMemcpy(hy->d_coef, pool.data(), pool.size() * sizeof(double), cudaMemcpyHostToDevice));
+    H2_CUDA(hy, cudaMemcpy(hy->d_plans, table.data(), sizeof(px::HybSlicePlan) * hy->P, cudaMemcpyHostToDevice));
+    hy->plans_dirty = false;
+  }
+  px::B2sScanArgs a{};
+  a.ubar = hy->ubar; a.aend = hy->la; a.zl = hy->lz; a.qT = hy->has_qT ? hy->qT : nullptr;
+  a.plans = hy->d_plans; a.coef = hy->d_coef; a.qdag0 = hy->qdag0; a.grad = hy->grad;
+  a.P = hy->P; a.B = hy->B; a.invT = 1.0 / hy->T; a.g = geom(hy);
+  H2_CUDA(hy, b2s_launch_scan(a, hy->ppt, 4 * n2 * sizeof(double), s));
+  hy->base.stats.kernel_launches += 1;
+  return PX_OK;
+}
+
 }  // namespace
 
 int h2_create(const px_hybrid_desc* d, void** out) {
@@ -400,6 +886,9 @@ int h2_create(const px_hybrid_desc* d, void** out) {
   hy->max_np = 0;
   for (int p = 0; p < P; ++p) hy->max_np = std::max(hy->max_np, hy->offs[p + 1] - hy->offs[p]);
   const size_t n2 = 2 * (size_t)hy->nx * hy->ny, B = hy->B, S = hy->S, L = B * P;
+  const char* onchip = std::getenv("PX_HYB2D_ONCHIP");
+  hy->small = n2 / 2 <= (size_t)px::B2S_MAX_N && !(onchip && onchip[0] == '0');
+  hy->ppt = n2 / 2 <= (size_t)px::B2S_NT ? 1 : (n2 / 2 <= 2 * (size_t)px::B2S_NT ? 2 : 4);
   hy->cost_blocks = (int)std::min<size_t>(148 * 4, ((S + 1) * n2 + 255) / 256);
   hy->bounds_blocks = (int)std::min<size_t>(148 * 2, ((size_t)P * B * (n2 / 2) + 255) / 256);
   int rc = PX_OK;
@@ -411,6 +900,8 @@ int h2_create(const px_hybrid_desc* d, void** out) {
   al(&hy->la, L * n2); al(&hy->lz, L * n2); al(&hy->lacc, L * n2); al(&hy->ly[0], L * n2); al(&hy->ly[1], L * n2);
   al(&hy->cpart, B * (size_t)hy->cost_blocks); al(&hy->bpart, 3 * (size_t)hy->bounds_blocks);
   if (rc == PX_OK) rc = dalloc_t(hb, &hy->d_offs, (size_t)P + 1);
+  if (rc == PX_OK) rc = dalloc_t(hb, &hy->flags, B * P);
+  if (rc == PX_OK) rc = dalloc_t(hb, &hy->d_plans, (size_t)P);
   if (rc == PX_OK && cudaMemcpy(hy->d_offs, d->offsets, sizeof(int) * (P + 1), cudaMemcpyHostToDevice) != cudaSuccess)
     rc = fail(hb, PX_ERR_CUDA, "hybrid 2D: offsets upload");
   if (rc == PX_OK) rc = dalloc_t(hb, &hy->theta, 2 * S + 1);
@@ -449,6 +940,7 @@ void h2_destroy(Hybrid2D* hy) {
   for (auto st : hy->side)
     if (st) cudaStreamSynchronize(st);
   for (void* a : hy->base.allocs) cudaFree(a);
+  if (hy->d_coef) cudaFree(hy->d_coef);
   for (auto st : hy->side)
     if (st) cudaStreamDestroy(st);
   for (auto e : hy->ev_slice)
@@ -480,6 +972,18 @@ int h2_direct(Hybrid2D* hy, int overlap, cudaStream_t s) {
   const int n = hy->nx * hy->ny;
   const size_t n2 = 2 * (size_t)n, B = hy->B, L = B * hy->P;
   const double h = hy->h;
+  if (hy->small) {
+    PX_TRY(direct_small(hy, overlap, s));
+    px::k_b2_cost_partial<<<dim3((unsigned)hy->cost_blocks, (unsigned)B), 256, 0, s>>>(hy->cpart, hy->traj, hy->target,
+                                                                                     hy->target_b, n2, hy->S, hy->B);
+    H2_LAUNCHED(hy);
+    px::k_b2_cost_final<<<(hy->B + 63) / 64, 64, 0, s>>>(hy->J, hy->cpart, hy->cost_blocks, h / hy->T, hy->B);
+    H2_LAUNCHED(hy);
+    hy->base.stats.rk4_lane_steps += (uint64_t)hy->B * hy->S * 2;
+    hy->direct_done = true;
+    hy->adjoint_done = hy->means_done = false;
+    return PX_OK;
+  }
   const bool ov = overlap && hy->P > 1;
   H2_CUDA(hy, cudaMemsetAsync(hy->la, 0, L * n2 * sizeof(double), s));
   H2_CUDA(hy, cudaMemsetAsync(hy->lz, 0, L * n2 * sizeof(double), s));
@@ -593,6 +1097,7 @@ int h2_set_slice_plan(Hybrid2D* hy, int sl, const px_cheb_plan* plan, const doub
   Hybrid2D::SlicePlan& sp = hy->plans[sl];
   const int K = plan->degree;
   sp.set = true;
+  hy->plans_dirty = true;
   sp.substeps = plan->substeps; sp.degree = K; sp.sigma = plan->sigma;
   sp.c0 = plan->center; sp.d = plan->scale; sp.span = plan->span;
   sp.be.assign(plan->coef_exp, plan->coef_exp + K + 1);
@@ -621,6 +1126,14 @@ int h2_adjoint(Hybrid2D* hy, cudaStream_t s) {
   const int top = hy->has_qT ? hy->P - 1 : hy->P - 2;
   for (int q = 0; q <= top; ++q)
     if (!hy->plans[q].set) return fail(&hy->base, PX_ERR_STATE, "hybrid: slice plan " + std::to_string(q) + " not set");
+  if (hy->small) {
+    PX_TRY(adjoint_small(hy, s));
+    uint64_t tm = 0;
+    for (int q = 0; q <= top; ++q) tm += (uint64_t)hy->plans[q].substeps * hy->plans[q].degree;
+    hy->base.stats.exp_terms += tm * hy->B;
+    hy->adjoint_done = true;
+    return PX_OK;
+  }
   const int n = hy->nx * hy->ny;
   const size_t n2 = 2 * (size_t)n, B = hy->B;
   const dim3 gridn((unsigned)((n + 255) / 256), (unsigned)B);

@@ -39,6 +39,16 @@ struct Hybrid2D : HybridHead {
     std::vector<double> be, law;  // exp series; law series per substep (substeps × (degree+1))
   };
   std::vector<SlicePlan> plans;
+  // on-chip variants for small grids (nx·ny ≤ 2048: the whole sweep / every slice solve / the frozen
+  // carry as one kernel each, slices released by progress flags); PX_HYB2D_ONCHIP=0 at create forces
+  // the per-stage launches
+  bool small = false;
+  int ppt = 1;
+  int* flags = nullptr;
+  px::HybSlicePlan* d_plans = nullptr;
+  double* d_coef = nullptr;
+  size_t coef_cap = 0;
+  bool plans_dirty = true;
   cudaStream_t side[NSIDE] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> ev_slice;
   cudaEvent_t ev_join[NSIDE] = {nullptr, nullptr, nullptr, nullptr};

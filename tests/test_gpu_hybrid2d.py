@@ -42,14 +42,25 @@ def _oracle(sysm, u0, f, target, offs, law, cfg, qdag_T=None):
                                    qdag_T=qdag_T, ny=sysm.grid.ny)
 
 
+@pytest.fixture
+def per_stage_launches(monkeypatch):
+    """Force the per-stage-launch kernels on a small grid (handles read PX_HYB2D_ONCHIP at create)."""
+    from paper_2004_00546_b200.tracking import release_tracking_engines
+    release_tracking_engines()
+    monkeypatch.setenv("PX_HYB2D_ONCHIP", "0")
+    yield
+    release_tracking_engines()
+
+
 @pytest.mark.parametrize("overlap", [True, False])
-def test_hybrid2d_tracking_vs_oracle(cuda_ok, overlap):
+@pytest.mark.parametrize("grid", [(48, 40), (64, 48)])   # on-chip kernels (≤ 2048 points) / per-stage launches
+def test_hybrid2d_tracking_vs_oracle(cuda_ok, overlap, grid):
     """Geometric partition (6 slices), sine law, two members, both fields active: J, ∂L/∂f,
     q†(0), u(T), the slice means and the slice adjoint ends against the oracle."""
     from paper_2004_00546_b200 import make_hybrid_plan, solve_hybrid_tracking, synthesize_trajectory
     from paper_2004_00546_b200 import _native as N
     from paper_2004_00546_b200.tracking import get_tracking_engine
-    sysm, u0, f, f_true, rk, cfg, law = _case()
+    sysm, u0, f, f_true, rk, cfg, law = _case(nx=grid[0], ny=grid[1])
     target = synthesize_trajectory(sysm, f_true, rk, law)[:, 0, :]
     plan = make_hybrid_plan(sysm.spec.T, 6, 1.5)
     r = solve_hybrid_tracking(sysm, u0, f, target, plan, rk=rk, expaction=cfg, law=law, overlap=overlap)
@@ -178,3 +189,21 @@ def test_hybrid2d_reference_config_size_and_overlap(cuda_ok):
     bad[7] = np.nan
     with pytest.raises((IntegrationFailure, FloatingPointError, ValueError)):
         solve_hybrid_tracking(sysm, np.zeros(sysm.n), bad, target, plan, rk=rk, expaction=cfg, law=law)
+
+
+def test_hybrid2d_on_chip_equals_per_stage_launches(cuda_ok, per_stage_launches):
+    """The same small case through the per-stage-launch kernels (PX_HYB2D_ONCHIP=0) against the
+    oracle, with terminal data and a mixed law (the on-chip run of it is the test above)."""
+    from paper_2004_00546_b200 import TimeLaw, make_hybrid_plan, solve_hybrid_tracking, synthesize_trajectory
+    law = TimeLaw(0.4, 0.7, -0.3, 3.0)
+    sysm, u0, f, f_true, rk, cfg, _ = _case(nx=33, ny=21, law=law)
+    tg = synthesize_trajectory(sysm, f_true, rk, law)[:, 0, :]
+    X, Y = sysm.grid.coordinates()
+    qT = 0.1 * np.concatenate([np.sin(X), np.cos(Y)])
+    for ov in (False, True):
+        r = solve_hybrid_tracking(sysm, u0, f, tg, make_hybrid_plan(sysm.spec.T, 5, 2.0), rk=rk, expaction=cfg, law=law,
+                                  qdag_T=qT, overlap=ov)
+        assert r.timing["overlapped"] == ov
+        o = _oracle(sysm, u0, f, tg, r.offsets, law, cfg, qdag_T=qT)
+        assert np.max(np.abs(r.J - o.J) / np.abs(o.J)) <= 1e-10
+        assert rel_l2(r.grad, o.grad) <= 1e-8 and rel_l2(r.qdag0, o.qdag0) <= 1e-10
