@@ -4,6 +4,7 @@ for the BASELINE configs with ``backend="cuda"``).
     python -m paper_2004_00546_b200 run --config 5 --repeats 3 --output results/c5
     python -m paper_2004_00546_b200 run --config 3 --checkpoints 3
     python -m paper_2004_00546_b200 predict --config 5 --gpus 1 2 4 8
+    python -m paper_2004_00546_b200 run --config burgers_hybrid.json      # a reference run file (runfile.py)
 
 ``run`` times `direct_adjoint_loop` (or config 2's 20-step `descend`) on this
 GPU and writes ``results.csv`` and ``summary.json`` (timing columns separate,
@@ -29,9 +30,22 @@ def _case(index: int):
     return baseline(index)
 
 
+def _run_file(args) -> int:
+    """`run --config file.json`: a run file in the reference's own layout (`config.py:28-175`)."""
+    from .runfile import load_run_file, run_file
+    rf = load_run_file(args.config)
+    out = args.output if args.output != "results" else rf.output
+    summary = run_file(rf, out, dt=args.dt, repeats=args.repeats if args.repeats != 3 else None)
+    print(json.dumps(summary))
+    return 0
+
+
 def cmd_run(args) -> int:
     from .optimization import descend, direct_adjoint_loop
     from .partition import RK4Config
+    if not str(args.config).isdigit():
+        return _run_file(args)
+    args.config = int(args.config)
     c = _case(args.config)
     u0, ut, ctrl = c.inputs()
     algo = "linear" if c.system.is_linear else ("nonlinear" if args.nonlinear else "hybrid")
@@ -139,7 +153,9 @@ def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="python -m paper_2004_00546_b200")
     sub = ap.add_subparsers(dest="cmd", required=True)
     r = sub.add_parser("run", help="time the direct-adjoint loop of a BASELINE config on this GPU")
-    r.add_argument("--config", type=int, default=5)
+    r.add_argument("--config", default="5",
+                   help="a BASELINE config number, or a run file in the reference's JSON layout (configs/*.json)")
+    r.add_argument("--dt", type=float, default=None, help="run files: the fixed RK4 step (default min(T/200, 1/λ))")
     r.add_argument("--repeats", type=int, default=3)
     r.add_argument("--output", default="results")
     r.add_argument("--single", action="store_true", help="one gradient even for descent configs")

@@ -392,15 +392,17 @@ def descend(
     expaction=None,
     u0: np.ndarray | None = None,
     backend: str = "cuda",
+    **loop_options,
 ) -> DescentResult:
-    """Fixed-step gradient descent on the control coefficients (`optimization.py:242-281`)."""
+    """Fixed-step gradient descent on the control coefficients (`optimization.py:242-281`).
+    ``loop_options`` go to `direct_adjoint_loop` (objective, time_law, plan, overlap, …)."""
     if lr <= 0:
         raise ValueError("learning rate must be positive")
     f = np.array(f_init, dtype=np.float64)
     J_history, grad_norms, step_seconds = [], [], []
     for _ in range(steps):
         loop = direct_adjoint_loop(system, f, q_true, algorithm, N=N, rk=rk, expaction=expaction, u0=u0,
-                                   backend=backend)
+                                   backend=backend, **loop_options)
         if not np.all(np.isfinite(loop.J)):
             raise FloatingPointError("cost became non-finite during descent")
         J_history.append(loop.J)
