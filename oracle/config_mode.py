@@ -124,6 +124,37 @@ def burgers2d_adjoint_apply(q, y, D, hx, hy, nx, ny):
     return np.concatenate([oa.reshape(shp + (-1,)), ob.reshape(shp + (-1,))], axis=-1)
 
 
+def burgers2d_advection(q, hx, hy, nx, ny):
+    """N(q) = (−U∂xU − V∂yU, −U∂xV − V∂yV) (`problems.py:189-195`)."""
+    U, V = _split2(q, nx, ny)
+    dUx, dUy, _ = _d2(U, hx, hy)
+    dVx, dVy, _ = _d2(V, hx, hy)
+    shp = q.shape[:-1]
+    return np.concatenate([(-U * dUx - V * dUy).reshape(shp + (-1,)), (-U * dVx - V * dVy).reshape(shp + (-1,))],
+                          axis=-1)
+
+
+def burgers2d_advection_jacobian_apply(qbar, y, hx, hy, nx, ny):
+    """(∂N/∂q at q̄)·y (`problems.py:213-287`): (−Ū∂x a − V̄∂y a − (∂xŪ)a − (∂yŪ)b,
+    −Ū∂x b − V̄∂y b − (∂xV̄)a − (∂yV̄)b)."""
+    U, V = _split2(qbar, nx, ny)
+    a, b = _split2(y, nx, ny)
+    dUx, dUy, _ = _d2(U, hx, hy)
+    dVx, dVy, _ = _d2(V, hx, hy)
+    dax, day, _ = _d2(a, hx, hy)
+    dbx, dby, _ = _d2(b, hx, hy)
+    oa = -U * dax - V * day - dUx * a - dUy * b
+    ob = -U * dbx - V * dby - dVx * a - dVy * b
+    shp = np.broadcast_shapes(qbar.shape[:-1], y.shape[:-1])
+    return np.concatenate([oa.reshape(shp + (-1,)), ob.reshape(shp + (-1,))], axis=-1)
+
+
+def laplacian2d(q, D, hx, hy, nx, ny):
+    U, V = _split2(q, nx, ny)
+    shp = q.shape[:-1]
+    return D * np.concatenate([_d2(U, hx, hy)[2].reshape(shp + (-1,)), _d2(V, hx, hy)[2].reshape(shp + (-1,))], axis=-1)
+
+
 def burgers_ops(nx, D, ny=None, hy=None):
     """(rhs(u, f), adj(u, y), n) of the Burgers testbed: 1D one-field (ny None) or the
     reference's 2D two-field system (state length 2·nx·ny)."""
@@ -692,6 +723,97 @@ def burgers_iterative_direct(nx, D, basis, T, P, nsteps, u0, ctrl, plan_for_regi
     raise RuntimeError(f"no convergence after {max_iter} sweeps: {history}")
 
 
+def burgers2d_iterative_direct(nx, ny, D, T, P, nsteps, u0, f, law, plans_for, eps, max_iter=25, min_iter=2):
+    """`solve_direct_nonlinear` (`nonlinear.py:69-194`) on the reference's two-field 2D Burgers
+    system with the forcing f·θ(t) and the configs' numerics — the 2D form of
+    `burgers_iterative_direct`: iterate Q on all RK4 nodes (constant u0 initially); per sweep the
+    slice means q̄_p, per slice y' = (D∇² + J̄_p)y + s(t), s = D∇²u0 + θ(t)f + N(Q) − J̄_p(Q − u0)
+    (J̄_p = ∂N/∂q at q̄_p, `nonlinear.py:113-116`), y(T_p) = 0, classical RK4 with Q linearly
+    interpolated at the stages; summed-chain carry D_{p+1} = exp(Δ(D∇² + J̄_p))D_p + y_p(end); the
+    new iterate u0 + y_p(kh) + exp(kh(D∇² + J̄_p))D_p on every node; stop when the largest per-slice
+    relative L2 change is below eps after at least min_iter sweeps. ``plans_for(qbar)`` returns
+    (slice-width plan, step-width plan). Returns (Q, sweeps, history)."""
+    hx, hy = 2.0 * np.pi / nx, 2.0 * np.pi / ny
+    n2 = 2 * nx * ny
+    f = np.atleast_2d(np.asarray(f, dtype=np.float64))
+    B = f.shape[0]
+    u0 = np.broadcast_to(_as_batch(u0, n2), (B, n2)).copy()
+    delta = T / P
+    h = delta / nsteps
+    S = P * nsteps
+    Q = np.broadcast_to(u0, (S + 1, B, n2)).copy()
+    lapu0 = laplacian2d(u0, D, hx, hy, nx, ny)
+    jadv = lambda qb, y: burgers2d_advection_jacobian_apply(qb, y, hx, hy, nx, ny)
+    jfull = lambda qb, y: jadv(qb, y) + laplacian2d(y, D, hx, hy, nx, ny)
+    history = []
+    for it in range(1, max_iter + 1):
+        qbar = slice_means(Q, P, nsteps)
+        plan_s, plan_h = plans_for(qbar)
+        Qn = np.empty_like(Q)
+        y_end = np.empty((P, B, n2))
+        for p in range(P):
+            qb_ = qbar[p]
+
+            def src(qt, t):
+                return (lapu0 + law_value(law, t) * f + burgers2d_advection(qt, hx, hy, nx, ny) - jadv(qb_, qt - u0))
+
+            y = np.zeros((B, n2))
+            for k in range(nsteps):
+                node = p * nsteps + k
+                t = node * h
+                qa, qc = Q[node], Q[node + 1]
+                qm = 0.5 * qa + 0.5 * qc
+                k1 = jfull(qb_, y) + src(qa, t)
+                k2 = jfull(qb_, y + (0.5 * h) * k1) + src(qm, t + 0.5 * h)
+                k3 = jfull(qb_, y + (0.5 * h) * k2) + src(qm, t + 0.5 * h)
+                k4 = jfull(qb_, y + h * k3) + src(qc, t + h)
+                y = y + (h / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+                if k + 1 < nsteps:
+                    Qn[node + 1] = u0 + y
+            y_end[p] = y
+        Dc = np.zeros((P + 1, B, n2))
+        for p in range(P):
+            op = lambda v, qb_=qbar[p]: jfull(qb_, v)
+            Dc[p + 1] = (y_end[p].copy() if p == 0 else exp_action(op, plan_s, Dc[p]) + y_end[p])
+        for p in range(P):
+            op = lambda v, qb_=qbar[p]: jfull(qb_, v)
+            Qn[p * nsteps] = u0 + Dc[p]
+            H = Dc[p]
+            for k in range(1, nsteps):
+                H = exp_action(op, plan_h, H)
+                Qn[p * nsteps + k] += H
+        Qn[S] = u0 + Dc[P]
+        err = 0.0
+        for p in range(P):
+            a = Qn[p * nsteps:(p + 1) * nsteps + 1]
+            b = Q[p * nsteps:(p + 1) * nsteps + 1]
+            for m in range(B):
+                num = float(np.sqrt(np.sum((a[:, m] - b[:, m]) ** 2)))
+                den = float(np.sqrt(np.sum(b[:, m] ** 2)))
+                err = max(err, num / den if den > 0 else num)
+        history.append(err)
+        Q = Qn
+        if err < eps and it >= min_iter:
+            return Q, it, history
+    raise RuntimeError(f"no convergence after {max_iter} sweeps: {history}")
+
+
+def burgers2d_nonlinear_tracking(nx, ny, D, T, P, nsteps, u0, f, law, target, plans_nl, plans_adj, eps,
+                                 max_iter=25, min_iter=2):
+    """The reference's loop with algorithm "nonlinear" (`optimization.py:206-231`): the iterative
+    direct (Algorithm 2) for the trajectory, then `solve_adjoint_varying` with zero terminal data
+    and the source 2(q − q_t) on the same equidistant partition — with q†_T = 0 the absorbed form
+    is the hybrid's (zero-terminal slice solves + frozen spans), so the adjoint, cost and gradient
+    are `burgers_tracking_hybrid`'s on the iterated trajectory."""
+    Q, sweeps, history = burgers2d_iterative_direct(nx, ny, D, T, P, nsteps, u0, f, law, plans_nl, eps, max_iter,
+                                                    min_iter)
+    offs = np.arange(P + 1) * nsteps
+    r = burgers_tracking_hybrid(nx, D, T, offs, u0, f, law, target, plans_adj, ny=ny, traj=Q)
+    r.extras["sweeps"] = sweeps
+    r.extras["history"] = history
+    return r
+
+
 # ---------------------------------------------------------------------------
 # Equispaced checkpointing (`checkpointing.py:119-267`) over the config-mode pieces
 # ---------------------------------------------------------------------------
@@ -813,7 +935,7 @@ def tracking_cost(traj, target, T, h):
     return (h / T) * np.tensordot(w, e, axes=(0, 0))
 
 
-def burgers_tracking_hybrid(nx, D, T, offsets, u0, f, law, target, plans_for, qdag_T=None, ny=None):
+def burgers_tracking_hybrid(nx, D, T, offsets, u0, f, law, target, plans_for, qdag_T=None, ny=None, traj=None):
     """The reference's hybrid loop with the configs' numerics.
 
     * direct: serial RK4 with forcing θ(t)·f (`hybrid.py:185-191`, `problems.py:155-162`);
@@ -843,7 +965,8 @@ def burgers_tracking_hybrid(nx, D, T, offsets, u0, f, law, target, plans_for, qd
     h = T / S
     target = np.asarray(target, dtype=np.float64)
     tg = target[:, None, :] if target.ndim == 2 else target
-    traj = burgers_direct_law(u0, f, law, D, hg, h, S, rhs=rhs2)
+    if traj is None:   # (a given direct trajectory: the nonlinear loop's, `optimization.py:206-225`)
+        traj = burgers_direct_law(u0, f, law, D, hg, h, S, rhs=rhs2)
     J = tracking_cost(traj, tg, T, h)
     ubar = slice_means_var(traj, offsets)
     plans = plans_for(ubar)

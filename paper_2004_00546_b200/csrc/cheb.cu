@@ -75,7 +75,7 @@ int cheb_action_march(Handle* h, const Plan& pl, const px::Stencil5& st, const d
   if (h->var.cheb_band > 0) {
     br = h->var.cheb_band;
   } else {
-    // about one full wave of 2 CTAs per SM, bands of ≥ 32 rows
+    // about one full wave of CM_MINB CTAs per SM
     const size_t per_band_ctas = (size_t)a.nstrips * B;
     const size_t target = (size_t)px::CM_MINB * 148;
     size_t nb_bands = std::max<size_t>(1, target / per_band_ctas);

@@ -84,16 +84,19 @@ __global__ void __launch_bounds__(256) k_cheb_term(ChebTermArgs a) {
 }
 
 
+// CTA size / resident CTAs per SM (compile-time experiment knobs). Measured on config 5 (both scans
+// per gradient): 160 × 2 → 106.4 ms, 128 × 3 → 99.0 ms, 96 × 4 → 101.4 ms, 64 × 6 → 102.1 ms, 192 × 2 slower:
+// four warps per CTA spread evenly over the SM's four schedulers, 12 resident warps, 168 registers.
 #ifndef PX_CM_NT
-#define PX_CM_NT 160
+#define PX_CM_NT 128
 #endif
 #ifndef PX_CM_MINB
-#define PX_CM_MINB 2
+#define PX_CM_MINB 3
 #endif
-constexpr int CM_NT = PX_CM_NT;  // 5 warps, pairs of columns: computed width ≤ 320 (192 measured slower)
+constexpr int CM_NT = PX_CM_NT;  // pairs of columns per thread: computed width ≤ 2·CM_NT
 constexpr int CM_MAXT = 7;  // terms per pass (template M ≤ CM_MAXT)
 constexpr int CM_DEPTH = 5; // cp.async ring depth (rows)
-constexpr int CM_MINB = PX_CM_MINB;  // resident CTAs per SM (3 measured slower: spills + smaller bands)
+constexpr int CM_MINB = PX_CM_MINB;  // resident CTAs per SM
 
 struct ChebMarchArgs {
   const double* u_prev; long long prev_bs;  // U_{k−1} (unused on the first pass)

@@ -99,3 +99,41 @@ def test_oracle_2d_gradient_vs_finite_differences():
     fd = (run(f + eps * d).J[0] - run(f - eps * d).J[0]) / (2 * eps)
     # the gradient w.r.t. a field on the grid: L's derivative in direction d is ⟨grad, d⟩
     assert abs(fd - float(r.grad[0] @ d)) <= 2e-4 * abs(fd)
+
+
+def _nl_plans(grid, D, delta, h, w, tol=1e-12):
+    from paper_2004_00546_b200.expaction import plan_chebyshev
+    cfg = ChebyshevConfig(tol=tol)
+
+    def plans_nl(qbar):
+        reg = frozen_region_from_bounds(*frozen_bounds_2d(qbar, grid, D))
+        return plan_chebyshev(reg, delta, cfg), plan_chebyshev(reg, h, cfg)
+
+    return plans_nl
+
+
+def test_oracle_2d_nonlinear_loop_pinned_to_the_reference_loop():
+    """The reference's loop with algorithm "nonlinear" (Algorithm 2 + `solve_adjoint_varying`,
+    eps = 1e-9, DOPRI5 at rtol 1e-10, Leja) against the restatement (RK4 with the iterate linearly
+    interpolated, Chebyshev actions, node trapezoid): agreement at the discretisations' level, and
+    the iterated trajectory converges to the serial sweep's (Algorithm 2's fixed point)."""
+    from oracle.config_mode import burgers2d_nonlinear_tracking, burgers_direct_law, burgers_ops
+    gd = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_nonlinear2d_tracking.npz"))
+    nx, ny, T, D, w, P = int(gd["nx"]), int(gd["ny"]), float(gd["T"]), float(gd["D"]), float(gd["omega"]), int(gd["N"])
+    law = TimeLaw.sine(w).as_tuple()
+    grid = Grid(nx, ny)
+    nsteps = 125
+    S = P * nsteps
+    h = T / S
+    offs = np.arange(P + 1) * nsteps
+    rhs, _, n2 = burgers_ops(nx, D, ny)
+    tgt = burgers_direct_law(np.zeros((1, n2)), gd["f_true"][None, :], law, D, grid.hx, h, S, rhs=rhs)[:, 0, :]
+    r = burgers2d_nonlinear_tracking(nx, ny, D, T, P, nsteps, np.zeros(n2), gd["f"], law, tgt,
+                                     _nl_plans(grid, D, T / P, h, w), _plans_for(grid, D, offs, h, w), eps=1e-10)
+    assert abs(r.J[0] - gd["J"]) <= 2e-6 * abs(gd["J"])
+    assert rel_l2(r.grad[0], gd["grad"]) <= 1e-5
+    assert rel_l2(r.qdag0[0], gd["qdag0"]) <= 1e-5
+    assert rel_l2(r.uT[0], gd["uT"]) <= 1e-6
+    assert 2 <= r.extras["sweeps"] <= 12 and r.extras["history"][-1] < 1e-10
+    serial = burgers_direct_law(np.zeros((1, n2)), gd["f"][None, :], law, D, grid.hx, h, S, rhs=rhs)
+    assert rel_l2(r.extras["traj"][-1], serial[-1]) <= 1e-6   # second order in h (interpolated iterate)
