@@ -345,6 +345,19 @@ int px_hybrid_set_slice_plan(void* handle, int p, const px_cheb_plan* plan, cons
                              const double* coef_gs);
 /* The frozen-operator carry and the gradient (needs every slice plan). */
 int px_hybrid_adjoint(void* handle, void* stream);
+/* The reference's loop with algorithm "nonlinear" on the 2D two-field handle (desc.ny > 1, equal
+ * slices, nx·ny ≤ 2048): the iterative nonlinear direct, Algorithm 2 (nonlinear.py:69-194;
+ * optimization.py:206-231). px_hybrid_nl_init: the constant initial guess u0 on every node; then per
+ * sweep px_hybrid_bounds (slice means and FOV box of the iterate) → px_hybrid_nl_set_plans (the
+ * actions exp(Δ(D∇² + J̄_p)) of slice width and of step width, exp series only) →
+ * px_hybrid_nl_sweep (err = max over slices of the relative L2 change, nonlinear.py:44-66; syncs)
+ * until err < eps; px_hybrid_nl_finish makes the iterate the direct trajectory (tracking cost, every
+ * slice's adjoint solve), after which px_hybrid_bounds / set_slice_plan / adjoint run as for the
+ * hybrid (with q†_T = 0 `solve_adjoint_varying`'s absorbed form is the hybrid's). */
+int px_hybrid_nl_init(void* handle, void* stream);
+int px_hybrid_nl_set_plans(void* handle, const px_cheb_plan* slice, const px_cheb_plan* step);
+int px_hybrid_nl_sweep(void* handle, double* err, void* stream);
+int px_hybrid_nl_finish(void* handle, void* stream);
 int px_hybrid_get(void* handle, int field, double* dst, size_t count, int mem, void* stream);
 /* Device ms of the last px_hybrid_direct: ms[0] the serial direct kernel, ms[1] the slice-solve
  * kernel (from its launch, waiting included), ms[2] both (first start to last end), ms[3] the

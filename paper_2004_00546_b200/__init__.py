@@ -67,6 +67,7 @@ from .tracking import (
     HybridTrackingResult,
     release_tracking_engines,
     solve_hybrid_tracking,
+    solve_nonlinear_tracking,
     synthesize_trajectory,
 )
 

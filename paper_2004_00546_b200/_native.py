@@ -163,6 +163,10 @@ SIGNATURES = {
     "px_hybrid_bounds": (c_int, [c_void_p, POINTER(c_double), c_void_p]),
     "px_hybrid_set_slice_plan": (c_int, [c_void_p, c_int, POINTER(ChebPlanC), POINTER(c_double), POINTER(c_double)]),
     "px_hybrid_adjoint": (c_int, [c_void_p, c_void_p]),
+    "px_hybrid_nl_init": (c_int, [c_void_p, c_void_p]),
+    "px_hybrid_nl_set_plans": (c_int, [c_void_p, POINTER(ChebPlanC), POINTER(ChebPlanC)]),
+    "px_hybrid_nl_sweep": (c_int, [c_void_p, POINTER(c_double), c_void_p]),
+    "px_hybrid_nl_finish": (c_int, [c_void_p, c_void_p]),
     "px_hybrid_get": (c_int, [c_void_p, c_int, c_void_p, c_size_t, c_int, c_void_p]),
     "px_hybrid_get_timing": (c_int, [c_void_p, POINTER(c_double)]),
 }

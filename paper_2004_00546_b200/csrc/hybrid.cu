@@ -340,6 +340,35 @@ int px_hybrid_adjoint(void* p, void* stream) {
   return PX_OK;
 }
 
+/* Algorithm 2 on the 2D two-field testbed (hybrid2d.cu); the 1D Algorithm 2 is px_nl_*. */
+int px_hybrid_nl_init(void* p, void* stream) {
+  using namespace pxi;
+  if (!p) return fail(nullptr, PX_ERR_ARG, "null handle");
+  if (Hybrid2D* h2 = H2(p)) return h2_nl_init(h2, (cudaStream_t)stream);
+  return fail(&H(p)->base, PX_ERR_ARG, "px_hybrid_nl_*: the 2D two-field handle (1D: px_nl_init / px_nl_sweep)");
+}
+
+int px_hybrid_nl_set_plans(void* p, const px_cheb_plan* slice, const px_cheb_plan* step) {
+  using namespace pxi;
+  if (!p || !slice || !step) return fail(p ? &H(p)->base : nullptr, PX_ERR_ARG, "null argument");
+  if (Hybrid2D* h2 = H2(p)) return h2_nl_set_plans(h2, slice, step);
+  return fail(&H(p)->base, PX_ERR_ARG, "px_hybrid_nl_*: the 2D two-field handle");
+}
+
+int px_hybrid_nl_sweep(void* p, double* err, void* stream) {
+  using namespace pxi;
+  if (!p || !err) return fail(p ? &H(p)->base : nullptr, PX_ERR_ARG, "null argument");
+  if (Hybrid2D* h2 = H2(p)) return h2_nl_sweep(h2, err, (cudaStream_t)stream);
+  return fail(&H(p)->base, PX_ERR_ARG, "px_hybrid_nl_*: the 2D two-field handle");
+}
+
+int px_hybrid_nl_finish(void* p, void* stream) {
+  using namespace pxi;
+  if (!p) return fail(nullptr, PX_ERR_ARG, "null handle");
+  if (Hybrid2D* h2 = H2(p)) return h2_nl_finish(h2, (cudaStream_t)stream);
+  return fail(&H(p)->base, PX_ERR_ARG, "px_hybrid_nl_*: the 2D two-field handle");
+}
+
 int px_hybrid_get(void* p, int field, double* dst, size_t count, int mem, void* stream) {
   using namespace pxi;
   if (!p || !dst) return fail(p ? &H(p)->base : nullptr, PX_ERR_ARG, "null argument");

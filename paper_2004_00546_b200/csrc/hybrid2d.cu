@@ -687,6 +687,345 @@ __global__ void __launch_bounds__(B2S_NT) k_b2s_scan(B2sScanArgs a) {
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Algorithm 2 on the two-field testbed (nonlinear.py:69-194), on chip (small grids): one sweep =
+// k_b2s_nl_lanes (per slice the Jacobian-augmented linear problem from zero data, RK4 with the
+// previous iterate linearly interpolated at the stages), k_b2s_nl_carry (the summed chain through
+// exp(Δ(D∇² + J̄_p))), k_b2s_nl_hom (the homogeneous part on every node, step-width actions) and
+// k_b2s_nl_err (per-slice relative change).
+// ---------------------------------------------------------------------------------------------
+
+// forward operator (D∇² + ∂N/∂q at q̄)·x at point i; q̄ and x in shared memory
+__device__ __forceinline__ void b2s_jfull(const B2Geom& g, const double* Qm, const double* X, int n, int i, int e, int w,
+                                          int nn, int s, double& oa, double& ob) {
+  const double* Vm = Qm + n;
+  const double* Xb = X + n;
+  const double Ub = Qm[i], Vb = Vm[i];
+  const double dUx = (Qm[e] - Qm[w]) * g.i2hx, dUy = (Qm[nn] - Qm[s]) * g.i2hy;
+  const double dVx = (Vm[e] - Vm[w]) * g.i2hx, dVy = (Vm[nn] - Vm[s]) * g.i2hy;
+  const double ac = X[i], ae = X[e], aw = X[w], an = X[nn], as = X[s];
+  const double bc = Xb[i], be = Xb[e], bw = Xb[w], bn = Xb[nn], bs = Xb[s];
+  oa = -Ub * (ae - aw) * g.i2hx - Vb * (an - as) * g.i2hy - dUx * ac - dUy * bc +
+       g.dx2 * (ae - 2.0 * ac + aw) + g.dy2 * (an - 2.0 * ac + as);
+  ob = -Ub * (be - bw) * g.i2hx - Vb * (bn - bs) * g.i2hy - dVx * ac - dVy * bc +
+       g.dx2 * (be - 2.0 * bc + bw) + g.dy2 * (bn - 2.0 * bc + bs);
+}
+
+struct B2sNlArgs {
+  const double* Q;      // (S+1) × B × 2n: the current iterate
+  double* Qn;           // (S+1) × B × 2n: the next iterate
+  const double* ubar;   // P × B × 2n slice means of Q
+  const double* u0;     // B × 2n
+  const double* f;      // B × 2n
+  const double* theta;  // θ(k·h/2)
+  double* yend;         // (B·P) × 2n
+  double* Dc;           // (P+1) × B × 2n carried homogeneous parts at the slice starts
+  double* err;          // B·P
+  const double* coef;   // be_slice[0..Ks], be_step[0..Kh]
+  int P, B, nsteps, S;
+  int Ks, subs_s, sig_s, Kh, subs_h, sig_h;
+  double c0_s, d_s, c0_h, d_h;
+  double h;
+  B2Geom g;
+};
+
+template <int PPT>
+__global__ void __launch_bounds__(B2S_NT) k_b2s_nl_lanes(B2sNlArgs a) {
+  extern __shared__ double b2s_sm[];
+  const int n = a.g.nx * a.g.ny, n2 = 2 * n;
+  const int t = threadIdx.x;
+  const int lane = blockIdx.x, b = lane / a.P, p = lane % a.P;
+  double* Y0 = b2s_sm;
+  double* Y1 = Y0 + n2;
+  double* Qm = Y1 + n2;
+  double* Qa = Qm + n2;
+  double* Qb = Qa + n2;
+  const size_t ns = (size_t)a.B * n2;
+  const double* Qg = a.Q + (size_t)b * n2;
+  double* Qo = a.Qn + (size_t)b * n2;
+  const double* u0 = a.u0 + (size_t)b * n2;
+  const double* f = a.f + (size_t)b * n2;
+  const double* qb = a.ubar + ((size_t)p * a.B + b) * n2;
+  double y[PPT][2], acc[PPT][2], cst[PPT][2];
+  int ie[PPT], iw[PPT], in[PPT], is[PPT];
+  const int node0 = p * a.nsteps;
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int i = t + q * B2S_NT;
+    if (i < n) {
+      b2_nbrs(i, a.g, ie[q], iw[q], in[q], is[q]);
+      Qm[i] = qb[i]; Qm[n + i] = qb[n + i];
+      Qb[i] = u0[i]; Qb[n + i] = u0[n + i];   // u0 with neighbours, for the constant part of the source
+      Qa[i] = Qg[(size_t)node0 * ns + i]; Qa[n + i] = Qg[(size_t)node0 * ns + n + i];
+      Y0[i] = 0.0; Y0[n + i] = 0.0;
+      y[q][0] = y[q][1] = 0.0;
+    }
+  }
+  __syncthreads();
+  // cst = D∇²u0 + J̄_adv·u0 (so that s(t) = cst + θ f + N(Q) − J̄_adv·Q): the full operator on u0
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int i = t + q * B2S_NT;
+    if (i < n) b2s_jfull(a.g, Qm, Qb, n, i, ie[q], iw[q], in[q], is[q], cst[q][0], cst[q][1]);
+  }
+  __syncthreads();
+  const double h = a.h;
+  auto stage = [&](auto mode, const double* Yi, double* Yo, double cw, double ca, double th, bool first, bool last) {
+    constexpr int MODE = decltype(mode)::value;
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const int i = t + q * B2S_NT;
+      if (i < n) {
+        const int e = ie[q], w = iw[q], nn = in[q], s = is[q];
+        // stage state qs (the previous iterate at the stage time) with neighbours
+        const double uc = b2s_state<MODE>(Qa, Qb, i), ue = b2s_state<MODE>(Qa, Qb, e), uw = b2s_state<MODE>(Qa, Qb, w);
+        const double un = b2s_state<MODE>(Qa, Qb, nn), us = b2s_state<MODE>(Qa, Qb, s);
+        const double vc = b2s_state<MODE>(Qa, Qb, n + i), ve = b2s_state<MODE>(Qa, Qb, n + e);
+        const double vw = b2s_state<MODE>(Qa, Qb, n + w), vn = b2s_state<MODE>(Qa, Qb, n + nn);
+        const double vs = b2s_state<MODE>(Qa, Qb, n + s);
+        // N(qs)
+        const double Nu = -uc * (ue - uw) * a.g.i2hx - vc * (un - us) * a.g.i2hy;
+        const double Nv = -uc * (ve - vw) * a.g.i2hx - vc * (vn - vs) * a.g.i2hy;
+        // J̄_adv·qs
+        const double* Vm = Qm + n;
+        const double Ub = Qm[i], Vb = Vm[i];
+        const double dUx = (Qm[e] - Qm[w]) * a.g.i2hx, dUy = (Qm[nn] - Qm[s]) * a.g.i2hy;
+        const double dVx = (Vm[e] - Vm[w]) * a.g.i2hx, dVy = (Vm[nn] - Vm[s]) * a.g.i2hy;
+        const double Ja = -Ub * (ue - uw) * a.g.i2hx - Vb * (un - us) * a.g.i2hy - dUx * uc - dUy * vc;
+        const double Jb = -Ub * (ve - vw) * a.g.i2hx - Vb * (vn - vs) * a.g.i2hy - dVx * uc - dVy * vc;
+        double ka, kb;
+        b2s_jfull(a.g, Qm, Yi, n, i, e, w, nn, s, ka, kb);
+        ka += cst[q][0] + th * f[i] + Nu - Ja;
+        kb += cst[q][1] + th * f[n + i] + Nv - Jb;
+        const double ra = (first ? y[q][0] : acc[q][0]) + ca * ka;
+        const double rb = (first ? y[q][1] : acc[q][1]) + ca * kb;
+        if (last) {
+          y[q][0] = ra; y[q][1] = rb;
+          Yo[i] = ra; Yo[n + i] = rb;
+        } else {
+          acc[q][0] = ra; acc[q][1] = rb;
+          Yo[i] = y[q][0] + cw * ka;
+          Yo[n + i] = y[q][1] + cw * kb;
+        }
+      }
+    }
+  };
+  for (int k = 0; k < a.nsteps; ++k) {
+    const int node = node0 + k;
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const int i = t + q * B2S_NT;
+      if (i < n) {
+        Qb[i] = Qg[(size_t)(node + 1) * ns + i];
+        Qb[n + i] = Qg[(size_t)(node + 1) * ns + n + i];
+      }
+    }
+    __syncthreads();
+    const double th0 = a.theta[2 * node], th1 = a.theta[2 * node + 1], th2 = a.theta[2 * node + 2];
+    stage(IC<0>{}, Y0, Y1, 0.5 * h, h / 6.0, th0, true, false);
+    __syncthreads();
+    stage(IC<1>{}, Y1, Y0, 0.5 * h, h / 3.0, th1, false, false);
+    __syncthreads();
+    stage(IC<1>{}, Y0, Y1, h, h / 3.0, th1, false, false);
+    __syncthreads();
+    stage(IC<2>{}, Y1, Y0, 0.0, h / 6.0, th2, false, true);
+    if (k + 1 < a.nsteps) {
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) {
+        const int i = t + q * B2S_NT;
+        if (i < n) {
+          Qo[(size_t)(node + 1) * ns + i] = u0[i] + y[q][0];
+          Qo[(size_t)(node + 1) * ns + n + i] = u0[n + i] + y[q][1];
+        }
+      }
+    }
+    __syncthreads();
+    double* sw = Qa; Qa = Qb; Qb = sw;
+  }
+  double* ye = a.yend + (size_t)lane * n2;
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int i = t + q * B2S_NT;
+    if (i < n) { ye[i] = y[q][0]; ye[n + i] = y[q][1]; }
+  }
+}
+
+// One planned action exp(span·(D∇² + J̄))·X[c] on chip: `subs` substeps of a degree-K Chebyshev
+// series (coefficients be); X: three rotating vectors in shared memory; returns the buffer index
+// of the result. Every thread holds the accumulator of its own points.
+template <int PPT>
+__device__ __forceinline__ int b2s_fwd_action(const B2Geom& g, double* const* X, const double* Qm, int n, int c,
+                                              const double* be, int K, int subs, double c0, double d, int sigma,
+                                              const int* ie, const int* iw, const int* in, const int* is) {
+  const int t = threadIdx.x;
+  double acc[PPT][2];
+  for (int j = 0; j < subs; ++j) {
+    int prv = c, cur = (c + 1) % 3, nxt = (c + 2) % 3;
+    {
+      const double inv = 1.0 / d;
+      const double* Xc = X[c];
+      double* Xo = X[cur];
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) {
+        const int i = t + q * B2S_NT;
+        if (i < n) {
+          double oa, ob;
+          b2s_jfull(g, Qm, Xc, n, i, ie[q], iw[q], in[q], is[q], oa, ob);
+          const double xa = Xc[i], xb = Xc[n + i];
+          const double ua = inv * (oa - c0 * xa), ub = inv * (ob - c0 * xb);
+          acc[q][0] = be[0] * xa + be[1] * ua;
+          acc[q][1] = be[0] * xb + be[1] * ub;
+          Xo[i] = ua; Xo[n + i] = ub;
+        }
+      }
+      __syncthreads();
+    }
+    const double two = 2.0 / d, sg = (double)sigma;
+    for (int k = 2; k <= K; ++k) {
+      const double* Xc = X[cur];
+      const double* Xp = X[prv];
+      double* Xo = X[nxt];
+      const double bek = be[k];
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) {
+        const int i = t + q * B2S_NT;
+        if (i < n) {
+          double oa, ob;
+          b2s_jfull(g, Qm, Xc, n, i, ie[q], iw[q], in[q], is[q], oa, ob);
+          const double ua = two * (oa - c0 * Xc[i]) + sg * Xp[i];
+          const double ub = two * (ob - c0 * Xc[n + i]) + sg * Xp[n + i];
+          acc[q][0] += bek * ua; acc[q][1] += bek * ub;
+          Xo[i] = ua; Xo[n + i] = ub;
+        }
+      }
+      __syncthreads();
+      const int tmp = prv; prv = cur; cur = nxt; nxt = tmp;
+    }
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const int i = t + q * B2S_NT;
+      if (i < n) { X[nxt][i] = acc[q][0]; X[nxt][n + i] = acc[q][1]; }
+    }
+    c = nxt;
+    __syncthreads();
+  }
+  return c;
+}
+
+template <int PPT>
+__global__ void __launch_bounds__(B2S_NT) k_b2s_nl_carry(B2sNlArgs a) {
+  extern __shared__ double b2s_sm[];
+  const int n = a.g.nx * a.g.ny, n2 = 2 * n;
+  const int t = threadIdx.x;
+  const size_t b = blockIdx.x;
+  double* X[3] = {b2s_sm, b2s_sm + n2, b2s_sm + 2 * n2};
+  double* Qm = b2s_sm + 3 * n2;
+  int ie[PPT], iw[PPT], in[PPT], is[PPT];
+  const size_t ns = (size_t)a.B * n2;
+  int c = 0;
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int i = t + q * B2S_NT;
+    if (i < n) {
+      b2_nbrs(i, a.g, ie[q], iw[q], in[q], is[q]);
+      a.Dc[b * n2 + i] = 0.0; a.Dc[b * n2 + n + i] = 0.0;   // D_0 = 0
+    }
+  }
+  for (int p = 0; p < a.P; ++p) {
+    const double* ye = a.yend + (b * a.P + p) * n2;
+    if (p > 0) {
+      const double* qb = a.ubar + ((size_t)p * a.B + b) * n2;
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) {
+        const int i = t + q * B2S_NT;
+        if (i < n) { Qm[i] = qb[i]; Qm[n + i] = qb[n + i]; }
+      }
+      __syncthreads();
+      c = b2s_fwd_action<PPT>(a.g, X, Qm, n, c, a.coef, a.Ks, a.subs_s, a.c0_s, a.d_s, a.sig_s, ie, iw, in, is);
+    }
+    double* Dn = a.Dc + (size_t)(p + 1) * ns + b * n2;
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const int i = t + q * B2S_NT;
+      if (i < n) {
+        const double va = (p > 0 ? X[c][i] : 0.0) + ye[i], vb = (p > 0 ? X[c][n + i] : 0.0) + ye[n + i];
+        X[c][i] = va; X[c][n + i] = vb;
+        Dn[i] = va; Dn[n + i] = vb;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int PPT>
+__global__ void __launch_bounds__(B2S_NT) k_b2s_nl_hom(B2sNlArgs a) {
+  extern __shared__ double b2s_sm[];
+  const int n = a.g.nx * a.g.ny, n2 = 2 * n;
+  const int t = threadIdx.x;
+  const int lane = blockIdx.x, b = lane / a.P, p = lane % a.P;
+  double* X[3] = {b2s_sm, b2s_sm + n2, b2s_sm + 2 * n2};
+  double* Qm = b2s_sm + 3 * n2;
+  int ie[PPT], iw[PPT], in[PPT], is[PPT];
+  const size_t ns = (size_t)a.B * n2;
+  const double* u0 = a.u0 + (size_t)b * n2;
+  const double* Dp = a.Dc + (size_t)p * ns + (size_t)b * n2;
+  const double* qb = a.ubar + ((size_t)p * a.B + b) * n2;
+  double* Qo = a.Qn + (size_t)b * n2;
+  const int node0 = p * a.nsteps;
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int i = t + q * B2S_NT;
+    if (i < n) {
+      b2_nbrs(i, a.g, ie[q], iw[q], in[q], is[q]);
+      Qm[i] = qb[i]; Qm[n + i] = qb[n + i];
+      X[0][i] = Dp[i]; X[0][n + i] = Dp[n + i];
+      Qo[(size_t)node0 * ns + i] = u0[i] + Dp[i];
+      Qo[(size_t)node0 * ns + n + i] = u0[n + i] + Dp[n + i];
+      if (p == a.P - 1) {   // the last node: u0 + D_P
+        const double* DP = a.Dc + (size_t)a.P * ns + (size_t)b * n2;
+        Qo[(size_t)a.S * ns + i] = u0[i] + DP[i];
+        Qo[(size_t)a.S * ns + n + i] = u0[n + i] + DP[n + i];
+      }
+    }
+  }
+  __syncthreads();
+  if (p == 0) return;   // D_0 = 0: nothing to propagate
+  int c = 0;
+  const double* be = a.coef + (a.Ks + 1);
+  for (int k = 1; k < a.nsteps; ++k) {
+    c = b2s_fwd_action<PPT>(a.g, X, Qm, n, c, be, a.Kh, a.subs_h, a.c0_h, a.d_h, a.sig_h, ie, iw, in, is);
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const int i = t + q * B2S_NT;
+      if (i < n) {
+        Qo[(size_t)(node0 + k) * ns + i] += X[c][i];
+        Qo[(size_t)(node0 + k) * ns + n + i] += X[c][n + i];
+      }
+    }
+  }
+}
+
+// per (member, slice): ‖Qn − Q‖ / ‖Q‖ over the slice's nodes (both ends included), nonlinear.py:44-66
+__global__ void __launch_bounds__(256) k_b2s_nl_err(B2sNlArgs a) {
+  __shared__ double red[8];
+  const int n2 = 2 * a.g.nx * a.g.ny;
+  const int lane = blockIdx.x, b = lane / a.P, p = lane % a.P;
+  const size_t ns = (size_t)a.B * n2;
+  const size_t total = (size_t)(a.nsteps + 1) * n2;
+  double num = 0.0, den = 0.0;
+  for (size_t m = threadIdx.x; m < total; m += blockDim.x) {
+    const size_t j = m / n2, i = m - j * n2;
+    const size_t off = (size_t)(p * a.nsteps + j) * ns + (size_t)b * n2 + i;
+    const double qo = a.Q[off], d = a.Qn[off] - qo;
+    num += d * d;
+    den += qo * qo;
+  }
+  const double rn = block_sum<256>(num, red);
+  const double rd = block_sum<256>(den, red);
+  if (threadIdx.x == 0) a.err[lane] = rd > 0.0 ? sqrt(rn) / sqrt(rd) : sqrt(rn);
+}
+
 }  // namespace px
 
 namespace pxi {
@@ -1186,6 +1525,124 @@ int h2_adjoint(Hybrid2D* hy, cudaStream_t s) {
   H2_LAUNCHED(hy);
   hy->base.stats.exp_terms += terms * hy->B;
   hy->adjoint_done = true;
+  return PX_OK;
+}
+
+// ---- Algorithm 2 (iterative nonlinear direct) on the two-field testbed --------------------------
+int h2_nl_init(Hybrid2D* hy, cudaStream_t s) {
+  if (!hy->inputs) return fail(&hy->base, PX_ERR_STATE, "hybrid: inputs not set");
+  if (!hy->small) return fail(&hy->base, PX_ERR_ARG, "Algorithm 2 on the 2D testbed runs on chip: nx·ny ≤ 2048");
+  const int ns = hy->offs[1];
+  for (int p = 0; p <= hy->P; ++p)
+    if (hy->offs[p] != p * ns) return fail(&hy->base, PX_ERR_ARG, "Algorithm 2 needs equal slices (nonlinear.py: equidistant)");
+  cudaSetDevice(hy->base.device);
+  const size_t n2 = 2 * (size_t)hy->nx * hy->ny, B = hy->B, S = hy->S, P = hy->P;
+  if (!hy->Qn) {
+    int rc = dalloc_t(&hy->base, &hy->Qn, (S + 1) * B * n2);
+    if (rc == PX_OK) rc = dalloc_t(&hy->base, &hy->Dc, (P + 1) * B * n2);
+    if (rc == PX_OK) rc = dalloc_t(&hy->base, &hy->nl_err, B * P);
+    if (rc == PX_OK) rc = dalloc_t(&hy->base, &hy->nl_coef, 2 * (size_t)(PX_MAX_CHEB_DEGREE + 1));
+    if (rc != PX_OK) return rc;
+  }
+  // constant-in-time initial guess (nonlinear.py:98-100)
+  for (size_t j = 0; j <= S; ++j)
+    H2_CUDA(hy, cudaMemcpyAsync(hy->traj + j * B * n2, hy->u0, B * n2 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  hy->nl_active = true;
+  hy->nl_plans = false;
+  hy->direct_done = true;   // the iterate is a trajectory: px_hybrid_bounds gives its slice means and FOV box
+  hy->adjoint_done = hy->means_done = false;
+  return PX_OK;
+}
+
+int h2_nl_set_plans(Hybrid2D* hy, const px_cheb_plan* ps, const px_cheb_plan* ph) {
+  if (!hy->nl_active) return fail(&hy->base, PX_ERR_STATE, "hybrid: run px_hybrid_nl_init first");
+  const px_cheb_plan* pl[2] = {ps, ph};
+  const double spans[2] = {hy->offs[1] * hy->h, hy->h};
+  for (int k = 0; k < 2; ++k) {
+    if (pl[k]->substeps < 1 || pl[k]->degree < 1 || pl[k]->degree > PX_MAX_CHEB_DEGREE || !(pl[k]->scale > 0) ||
+        (pl[k]->sigma != 1 && pl[k]->sigma != -1) || !pl[k]->coef_exp)
+      return fail(&hy->base, PX_ERR_ARG, "hybrid nl plan: bad substeps/degree/scale/sigma");
+    if (std::fabs(pl[k]->span - spans[k]) > 1e-12 * std::max(1.0, spans[k]))
+      return fail(&hy->base, PX_ERR_ARG, "hybrid nl plan: span does not match the slice / step width");
+  }
+  cudaSetDevice(hy->base.device);
+  std::vector<double> pool(ps->coef_exp, ps->coef_exp + ps->degree + 1);
+  pool.insert(pool.end(), ph->coef_exp, ph->coef_exp + ph->degree + 1);
+  H2_CUDA(hy, cudaMemcpy(hy->nl_coef, pool.data(), pool.size() * sizeof(double), cudaMemcpyHostToDevice));
+  hy->nl_s = {ps->degree, ps->substeps, ps->sigma, ps->center, ps->scale};
+  hy->nl_h = {ph->degree, ph->substeps, ph->sigma, ph->center, ph->scale};
+  hy->nl_plans = true;
+  return PX_OK;
+}
+
+int h2_nl_sweep(Hybrid2D* hy, double* err_out, cudaStream_t s) {
+  if (!hy->nl_active || !hy->nl_plans) return fail(&hy->base, PX_ERR_STATE, "hybrid: nl_init / nl_set_plans first");
+  if (!hy->means_done) return fail(&hy->base, PX_ERR_STATE, "hybrid: run px_hybrid_bounds on the iterate first");
+  cudaSetDevice(hy->base.device);
+  const size_t n2 = 2 * (size_t)hy->nx * hy->ny;
+  px::B2sNlArgs a{};
+  a.Q = hy->traj; a.Qn = hy->Qn; a.ubar = hy->ubar; a.u0 = hy->u0; a.f = hy->f; a.theta = hy->theta;
+  a.yend = hy->lacc; a.Dc = hy->Dc; a.err = hy->nl_err; a.coef = hy->nl_coef;
+  a.P = hy->P; a.B = hy->B; a.nsteps = hy->offs[1]; a.S = hy->S;
+  a.Ks = hy->nl_s.K; a.subs_s = hy->nl_s.subs; a.sig_s = hy->nl_s.sigma; a.c0_s = hy->nl_s.c0; a.d_s = hy->nl_s.d;
+  a.Kh = hy->nl_h.K; a.subs_h = hy->nl_h.subs; a.sig_h = hy->nl_h.sigma; a.c0_h = hy->nl_h.c0; a.d_h = hy->nl_h.d;
+  a.h = hy->h; a.g = geom(hy);
+  const int lanes = hy->B * hy->P;
+  H2_CUDA(hy, b2s_dispatch(hy->ppt, [&](auto pc) {
+    constexpr int PPT = decltype(pc)::value;
+    const size_t sm5 = 5 * n2 * sizeof(double), sm4 = 4 * n2 * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(px::k_b2s_nl_lanes<PPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm5);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(px::k_b2s_nl_carry<PPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(px::k_b2s_nl_hom<PPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
+    if (e != cudaSuccess) return e;
+    px::k_b2s_nl_lanes<PPT><<<lanes, px::B2S_NT, sm5, s>>>(a);
+    px::k_b2s_nl_carry<PPT><<<hy->B, px::B2S_NT, sm4, s>>>(a);
+    px::k_b2s_nl_hom<PPT><<<lanes, px::B2S_NT, sm4, s>>>(a);
+    return cudaGetLastError();
+  }));
+  px::k_b2s_nl_err<<<lanes, 256, 0, s>>>(a);
+  H2_LAUNCHED(hy);
+  hy->base.stats.kernel_launches += 3;
+  std::vector<double> e(lanes);
+  H2_CUDA(hy, cudaMemcpyAsync(e.data(), hy->nl_err, lanes * sizeof(double), cudaMemcpyDeviceToHost, s));
+  H2_CUDA(hy, cudaStreamSynchronize(s));
+  double mx = 0.0;
+  for (double v : e) {
+    if (v != v) mx = NAN;
+    else if (mx == mx) mx = std::max(mx, v);
+  }
+  std::swap(hy->traj, hy->Qn);
+  hy->means_done = false;
+  hy->base.stats.rk4_lane_steps += (uint64_t)hy->B * hy->S;
+  if (!std::isfinite(mx)) return fail(&hy->base, PX_ERR_NONFINITE, "hybrid: non-finite iterate in the nonlinear sweep");
+  *err_out = mx;
+  return PX_OK;
+}
+
+// the converged iterate is the direct trajectory: tracking cost and every slice's adjoint solve
+int h2_nl_finish(Hybrid2D* hy, cudaStream_t s) {
+  if (!hy->nl_active) return fail(&hy->base, PX_ERR_STATE, "hybrid: run px_hybrid_nl_init first");
+  cudaSetDevice(hy->base.device);
+  const size_t n2 = 2 * (size_t)hy->nx * hy->ny;
+  px::B2sLaneArgs l{};
+  l.traj = hy->traj; l.target = hy->target; l.offs = hy->d_offs; l.theta = hy->theta; l.flags = hy->flags;
+  l.aend = hy->la; l.zl = hy->lz; l.P = hy->P; l.B = hy->B; l.target_b = hy->target_b; l.wait = 0;
+  l.h = hy->h; l.g = geom(hy);
+  H2_CUDA(hy, cudaEventRecord(hy->ev[0], s));
+  H2_CUDA(hy, cudaEventRecord(hy->ev[1], s));
+  H2_CUDA(hy, cudaEventRecord(hy->ev[2], s));
+  H2_CUDA(hy, b2s_launch_lanes(l, hy->ppt, 4 * n2 * sizeof(double), s));
+  H2_CUDA(hy, cudaEventRecord(hy->ev[3], s));
+  px::k_b2_cost_partial<<<dim3((unsigned)hy->cost_blocks, (unsigned)hy->B), 256, 0, s>>>(
+      hy->cpart, hy->traj, hy->target, hy->target_b, n2, hy->S, hy->B);
+  H2_LAUNCHED(hy);
+  px::k_b2_cost_final<<<(hy->B + 63) / 64, 64, 0, s>>>(hy->J, hy->cpart, hy->cost_blocks, hy->h / hy->T, hy->B);
+  H2_LAUNCHED(hy);
+  hy->base.stats.kernel_launches += 1;
+  hy->overlapped = 0;
+  hy->nl_active = false;
+  hy->direct_done = true;
+  hy->adjoint_done = hy->means_done = false;
   return PX_OK;
 }
 

@@ -8,6 +8,8 @@
 
 namespace pxi {
 
+constexpr int PX_MAX_CHEB_DEGREE = 2048;  // Algorithm 2's two plans (device coefficient pool)
+
 // Both hybrid handles (1D: hybrid.cu, 2D two-field: hybrid2d.cu) start with this head.
 struct HybridHead {
   Handle base;  // device, error text, allocations, stats
@@ -49,6 +51,12 @@ struct Hybrid2D : HybridHead {
   double* d_coef = nullptr;
   size_t coef_cap = 0;
   bool plans_dirty = true;
+  // Algorithm 2 (px_hybrid_nl_*): the next iterate, the carried homogeneous parts, per-slice errors,
+  // the two plans' exp series (slice width, step width)
+  double *Qn = nullptr, *Dc = nullptr, *nl_err = nullptr, *nl_coef = nullptr;
+  struct NlPlan { int K = 0, subs = 0, sigma = -1; double c0 = 0.0, d = 1.0; };
+  NlPlan nl_s, nl_h;
+  bool nl_active = false, nl_plans = false;
   cudaStream_t side[NSIDE] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> ev_slice;
   cudaEvent_t ev_join[NSIDE] = {nullptr, nullptr, nullptr, nullptr};
@@ -65,6 +73,10 @@ int h2_direct(Hybrid2D* hy, int overlap, cudaStream_t s);
 int h2_bounds(Hybrid2D* hy, double* out3, cudaStream_t s);
 int h2_set_slice_plan(Hybrid2D* hy, int sl, const px_cheb_plan* plan, const double* gc, const double* gs);
 int h2_adjoint(Hybrid2D* hy, cudaStream_t s);
+int h2_nl_init(Hybrid2D* hy, cudaStream_t s);
+int h2_nl_set_plans(Hybrid2D* hy, const px_cheb_plan* slice, const px_cheb_plan* step);
+int h2_nl_sweep(Hybrid2D* hy, double* err, cudaStream_t s);
+int h2_nl_finish(Hybrid2D* hy, cudaStream_t s);
 int h2_get(Hybrid2D* hy, int field, double* dst, size_t count, int mem, cudaStream_t s);
 int h2_get_timing(Hybrid2D* hy, double* ms5);
 

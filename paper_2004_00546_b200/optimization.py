@@ -227,7 +227,8 @@ def direct_adjoint_loop(
         raise ConfigError("the two-field 2D Burgers testbed runs the reference's own loop: objective='tracking' "
                           "with algorithm 'hybrid' or 'serial'")
     if objective == "tracking":
-        return _tracking_loop(system, f, q_true, algorithm, N, rk, expaction, u0, backend, plan, time_law, overlap)
+        return _tracking_loop(system, f, q_true, algorithm, N, rk, expaction, u0, backend, plan, time_law, overlap,
+                              eps, max_iter, min_iter)
     if plan is not None:
         raise ConfigError("plan: the geometric partition belongs to the hybrid tracking loop (objective='tracking')")
     law = tuple(float(v) for v in time_law.as_tuple()) if time_law is not None else (1.0, 0.0, 0.0, 0.0)
@@ -293,15 +294,39 @@ def direct_adjoint_loop(
     )
 
 
-def _tracking_loop(system, f, q_true, algorithm, N, rk, expaction, u0, backend, plan, time_law, overlap):
+def _nonlinear_tracking_loop(system, f, q_true, N, rk, expaction, u0, time_law, eps, max_iter, min_iter):
+    """The reference's loop with algorithm "nonlinear" on the two-field 2D Burgers testbed
+    (`optimization.py:206-231`): Algorithm 2 direct + the zero-terminal adjoint with the tracking source."""
+    from .hybrid import TimeLaw
+    from .tracking import solve_nonlinear_tracking
+    fa = np.asarray(f, dtype=np.float64)
+    tick = time.perf_counter()
+    r = solve_nonlinear_tracking(system, np.zeros(system.n) if u0 is None else u0, np.atleast_2d(fa), q_true, N, rk,
+                                 expaction or ChebyshevConfig(tol=1e-12), time_law or TimeLaw.constant(), eps,
+                                 max_iter, min_iter)
+    single = fa.ndim == 1
+    hist = list(r.timing.get("history", []))
+    return LoopResult(
+        float(r.J[0]) if single else r.J, r.grad[0] if single else r.grad,
+        DirectSolution(r.partition, r.final_state[0] if single else r.final_state),
+        AdjointSolution(r.partition, r.qdag0[0] if single else r.qdag0, r.grad[0] if single else r.grad),
+        iterations=len(hist), seconds=time.perf_counter() - tick, error_history=hist,
+        stats={"timing": r.timing, "offsets": r.offsets})
+
+
+def _tracking_loop(system, f, q_true, algorithm, N, rk, expaction, u0, backend, plan, time_law, overlap,
+                   eps=1e-3, max_iter=25, min_iter=2):
     from .hybrid import HybridPlan, TimeLaw
     from .tracking import solve_hybrid_tracking
     if backend not in BACKENDS:
         raise ValueError(f"unknown backend {backend!r}; the B200 path provides {BACKENDS}")
     if system.is_linear:
         return _linear_tracking_loop(system, f, q_true, algorithm, N, rk, expaction, u0, plan, time_law)
+    if algorithm == NONLINEAR and getattr(system, "is_burgers2d", False):
+        return _nonlinear_tracking_loop(system, f, q_true, N, rk, expaction, u0, time_law, eps, max_iter, min_iter)
     if algorithm not in (HYBRID, SERIAL):
-        raise ValueError("the tracking objective runs with algorithm 'hybrid' or 'serial'")
+        raise ValueError("the tracking objective runs with algorithm 'hybrid' or 'serial' "
+                         "(and 'nonlinear' on the two-field 2D testbed)")
     if rk is None:
         raise ConfigError("rk: an RK4Config(dt) is required (fixed-step RK4)")
     if algorithm == SERIAL:

@@ -11,7 +11,7 @@ f·sin(ωt), and ``results.csv`` / ``summary.json`` (and ``descent.csv``) are wr
 The reference's adaptive tolerances (``rtol``, ``leja_tol``) have no fixed-step counterpart: the
 RK4 step is ``dt`` (default: min(T/200, 1/λ) with λ the diffusion part's spectral radius) and the
 exponential actions are planned to 1e-12. ``checkpoints`` and the Gantt / PNG outputs are not
-part of this path. Field shapes: "sin_product", "ones", "zeros" or a flat list."""
+part of this path; `algorithm: "nonlinear"` (Algorithm 2) runs for nx·ny ≤ 2048. Field shapes: "sin_product", "ones", "zeros" or a flat list."""
 
 from __future__ import annotations
 
@@ -49,6 +49,7 @@ class RunFile:
     output: str = "results"
     descent_steps: int = 0
     descent_lr: float = 0.5
+    eps: float = 1e-3
 
 
 def _take(obj: dict, where: str, key: str, types, default=_MISSING):
@@ -126,8 +127,11 @@ def parse_run_file(data: dict) -> RunFile:
     lr = float(_take(descent, "descent", "lr", num, 0.5))
     if steps < 0 or (steps and lr <= 0):
         raise ConfigError("descent: steps cannot be negative and lr must be positive")
+    eps = float(_take(data, "", "eps", num, 1e-3))
+    if eps <= 0:
+        raise ConfigError("eps: must be positive")
     return RunFile(kind, nx, ny, a, D, omega, T, f_true, f_init, algorithm, tuple(workers), checkpoints, repeats,
-                   pilot, _take(data, "", "output", str, "results"), steps, lr)
+                   pilot, _take(data, "", "output", str, "results"), steps, lr, eps)
 
 
 def load_run_file(path: str) -> RunFile:
@@ -156,8 +160,10 @@ def run_file(rf: RunFile, output: str | None = None, dt: float | None = None, re
     from .tracking import synthesize_trajectory
     if rf.checkpoints:
         raise ConfigError("checkpoints: run files run without checkpointing here (run_checkpointed_loop takes BASELINE configs)")
-    if rf.algorithm == "nonlinear":
-        raise ConfigError("algorithm: the iterative nonlinear direct (Algorithm 2) runs on the 1D Burgers testbed here")
+    if rf.algorithm == "nonlinear" and rf.nx * rf.ny > 2048:
+        raise ConfigError("algorithm: the iterative nonlinear direct (Algorithm 2) runs on chip here: nx·ny ≤ 2048")
+    if rf.algorithm in ("hybrid", "nonlinear") and rf.kind != BURGERS:
+        raise ConfigError(f"algorithm: the {rf.algorithm} algorithm is for the Burgers testbed")
     out = output or rf.output
     reps = repeats or rf.repeats
     grid = Grid(rf.nx, rf.ny)
@@ -177,13 +183,15 @@ def run_file(rf: RunFile, output: str | None = None, dt: float | None = None, re
         return targets[S]
 
     def steps_for(N: int) -> int:
-        if linear:   # whole steps per (equal) slice
+        if linear or rf.algorithm == "nonlinear":   # whole steps per (equal) slice
             return N * max(1, int(np.ceil(rf.T / (N * dt0) - 1e-9)))
         return max(1, int(np.ceil(rf.T / dt0 - 1e-9)))
 
     def timed(algorithm, N, plan=None):
         S = steps_for(N)
         kw = dict(N=N, rk=RK4Config(rf.T / S), expaction=cfg, objective="tracking", time_law=law)
+        if algorithm == "nonlinear":
+            kw["eps"] = rf.eps
         if plan is not None:
             kw["plan"] = plan
         tgt = target_for(S)

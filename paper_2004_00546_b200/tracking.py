@@ -186,6 +186,54 @@ class HybridTrackingEngine:
         s = current_stream_handle() if stream is None else stream
         self._chk(self.lib.px_hybrid_adjoint(self.h, ctypes.c_void_p(s)))
 
+    # ---- Algorithm 2 on the 2D two-field testbed (px_hybrid_nl_*) ------------------------------
+    @staticmethod
+    def _plan_c(pl):
+        c = N.ChebPlanC()
+        c.span, c.substeps, c.degree, c.center, c.scale, c.sigma = (pl.span, pl.substeps, pl.degree, pl.center,
+                                                                     pl.scale, pl.sigma)
+        be, ka = N.dptr(pl.coef_exp)
+        bp, kb = N.dptr(pl.coef_phi)
+        c.coef_exp, c.coef_phi = be, bp
+        return c, (ka, kb)
+
+    def iterate_direct(self, expaction: ChebyshevConfig, eps: float, max_iter: int = 25, min_iter: int = 2,
+                       stream: int | None = None) -> list:
+        """`solve_direct_nonlinear` (`nonlinear.py:69-194`): sweeps until the largest per-slice relative
+        change is below ``eps`` (at least ``min_iter`` sweeps); the iterate becomes the direct trajectory.
+        Returns the error history; raises `IterationDivergence` after ``max_iter`` sweeps."""
+        from .errors import IterationDivergence
+        from .expaction import plan_chebyshev
+        s = current_stream_handle() if stream is None else stream
+        self._chk(self.lib.px_hybrid_nl_init(self.h, ctypes.c_void_p(s)))
+        delta = float(self.offsets[1]) * self.step
+        history = []
+        for it in range(1, max_iter + 1):
+            region = frozen_region_from_bounds(*self.bounds(s))
+            cs, k1 = self._plan_c(plan_chebyshev(region, delta, expaction))
+            ch, k2 = self._plan_c(plan_chebyshev(region, self.step, expaction))
+            self._chk(self.lib.px_hybrid_nl_set_plans(self.h, ctypes.byref(cs), ctypes.byref(ch)))
+            del k1, k2
+            err = ctypes.c_double()
+            self._chk(self.lib.px_hybrid_nl_sweep(self.h, ctypes.byref(err), ctypes.c_void_p(s)))
+            history.append(float(err.value))
+            if err.value < eps and it >= min_iter:
+                self._chk(self.lib.px_hybrid_nl_finish(self.h, ctypes.c_void_p(s)))
+                return history
+        raise IterationDivergence(history)
+
+    def run_nonlinear(self, u0, f, target, expaction: ChebyshevConfig, eps: float, max_iter: int = 25,
+                      min_iter: int = 2) -> dict:
+        self.set_inputs(u0, f, target, None)
+        history = self.iterate_direct(expaction, eps, max_iter, min_iter)
+        b = self.bounds()
+        plans = self.plan(expaction, b, False) if self.P > 1 else []
+        self.adjoint()
+        B, n = self.B, self.n
+        return {"J": self.get(N.PX_HFIELD_J, (B,)), "grad": self.get(N.PX_HFIELD_GRAD, (B, n)),
+                "uT": self.get(N.PX_HFIELD_UT, (B, n)), "qdag0": self.get(N.PX_HFIELD_QDAG0, (B, n)),
+                "timing": self.timing(), "plans": plans, "bounds": b, "history": history}
+
     def run(self, u0, f, target, expaction: ChebyshevConfig, qdag_T=None, overlap: bool = True) -> dict:
         self.set_inputs(u0, f, target, qdag_T)
         self.direct(overlap)
@@ -256,6 +304,47 @@ def solve_hybrid_tracking(system: System, u0, f, target, plan: HybridPlan | None
     r = eng.run(u0, f, target, expaction, qdag_T, overlap)
     return HybridTrackingResult(J=r["J"], grad=r["grad"], final_state=r["uT"], qdag0=r["qdag0"], partition=part,
                                 offsets=offs, timing=r["timing"], plans=r["plans"])
+
+
+def solve_nonlinear_tracking(system: System, u0, f, target, N: int = 1, rk: RK4Config | None = None,
+                             expaction: ChebyshevConfig | None = None, law: TimeLaw | None = None,
+                             eps: float = 1e-3, max_iter: int = 25, min_iter: int = 2) -> HybridTrackingResult:
+    """The reference's loop with algorithm "nonlinear" on its 2D two-field Burgers testbed
+    (`optimization.py:206-231`): the iterative nonlinear direct (Algorithm 2, `nonlinear.py:69-194`)
+    on ``N`` equal slices, then `solve_adjoint_varying` with the source 2(q − q_t) and zero terminal
+    data (the hybrid's adjoint form), the tracking cost and ∂L/∂f. ``timing["history"]`` holds the
+    sweeps' errors. Small grids (nx·ny ≤ 2048), whole RK4 steps per slice."""
+    if rk is None:
+        raise ConfigError("rk: an RK4Config(dt) is required (fixed-step RK4)")
+    if not getattr(system, "is_burgers2d", False):
+        raise ConfigError("solve_nonlinear_tracking: the two-field 2D Burgers testbed (1D: algorithm='nonlinear' "
+                          "with the terminal objective)")
+    if eps <= 0:
+        raise ValueError("eps must be positive")
+    law = law or TimeLaw.constant()
+    expaction = expaction or ChebyshevConfig(tol=1e-12)
+    f = np.atleast_2d(np.asarray(f, dtype=np.float64))
+    if f.shape[-1] != system.n:
+        raise ValueError("f must be a forcing field of n points (or B fields)")
+    B = f.shape[0]
+    steps = max(1, int(np.ceil(system.spec.T / (N * rk.dt) - 1e-9)))
+    offs = (np.arange(N + 1) * steps).astype(np.int32)
+    S = int(offs[-1])
+    if abs(system.spec.T / S - rk.dt) > 1e-12 * rk.dt:
+        raise ConfigError(f"rk.dt must divide the slice width T/N into whole steps (nearest: {system.spec.T / S!r})")
+    target = np.asarray(target, dtype=np.float64)
+    if tuple(target.shape) == (S + 1, system.n):
+        batched = False
+    elif tuple(target.shape) == (S + 1, B, system.n):
+        batched = True
+    else:
+        raise ValueError(f"target must be given on the {S + 1} nodes of the sweep: (S+1, n) or (S+1, B, n)")
+    eng = get_tracking_engine(system, offs, law, B, batched)
+    r = eng.run_nonlinear(u0, f, target, expaction, eps, max_iter, min_iter)
+    timing = dict(r["timing"], history=r["history"])
+    return HybridTrackingResult(J=r["J"], grad=r["grad"], final_state=r["uT"], qdag0=r["qdag0"],
+                                partition=partition_equidistant(system.spec.T, N), offsets=offs, timing=timing,
+                                plans=r["plans"])
 
 
 def synthesize_trajectory(system: System, f_true, rk: RK4Config, law: TimeLaw | None = None, u0=None) -> np.ndarray:

@@ -207,3 +207,69 @@ def test_hybrid2d_on_chip_equals_per_stage_launches(cuda_ok, per_stage_launches)
         o = _oracle(sysm, u0, f, tg, r.offsets, law, cfg, qdag_T=qT)
         assert np.max(np.abs(r.J - o.J) / np.abs(o.J)) <= 1e-10
         assert rel_l2(r.grad, o.grad) <= 1e-8 and rel_l2(r.qdag0, o.qdag0) <= 1e-10
+
+
+def _nl_oracle(sysm, u0, f, target, P, nsteps, law, cfg, eps):
+    from oracle.config_mode import burgers2d_nonlinear_tracking
+    from paper_2004_00546_b200.expaction import plan_chebyshev, plan_family
+    from paper_2004_00546_b200.problems import frozen_bounds_2d, frozen_region_from_bounds
+    T, D, g = sysm.spec.T, sysm.spec.D, sysm.grid
+    h = T / (P * nsteps)
+
+    def plans_nl(qbar):
+        reg = frozen_region_from_bounds(*frozen_bounds_2d(qbar, g, D))
+        return plan_chebyshev(reg, T / P, cfg), plan_chebyshev(reg, h, cfg)
+
+    def plans_adj(ubar):
+        reg = frozen_region_from_bounds(*frozen_bounds_2d(ubar, g, D))
+        return plan_family(reg, [T / P] * P, cfg, omega=law.omega)
+
+    return burgers2d_nonlinear_tracking(g.nx, g.ny, D, T, P, nsteps, u0, f, law.as_tuple(), target, plans_nl, plans_adj,
+                                        eps)
+
+
+def test_nonlinear2d_loop_vs_oracle(cuda_ok):
+    """Algorithm 2 on the two-field testbed (px_hybrid_nl_*) + the zero-terminal adjoint: sweeps, error
+    history, J, ∂L/∂f, q†(0), u(T) against the oracle; two members; through the loop API."""
+    from paper_2004_00546_b200 import direct_adjoint_loop, solve_nonlinear_tracking, synthesize_trajectory
+    sysm, u0, f, f_true, rk, cfg, law = _case(nx=24, ny=20, T=0.3, dt=1.5e-3)
+    P, nsteps = 4, 50
+    target = synthesize_trajectory(sysm, f_true, rk, law)[:, 0, :]
+    r = solve_nonlinear_tracking(sysm, u0, f, target, N=P, rk=rk, expaction=cfg, law=law, eps=1e-10)
+    o = _nl_oracle(sysm, u0, f, target, P, nsteps, law, cfg, 1e-10)
+    hist = r.timing["history"]
+    assert len(hist) == o.extras["sweeps"]
+    for a, b in zip(hist[:-1], o.extras["history"][:-1]):
+        assert abs(a - b) <= 1e-6 * abs(b)
+    assert np.max(np.abs(r.J - o.J) / np.abs(o.J)) <= 1e-10
+    assert rel_l2(r.final_state, o.uT) <= 1e-10
+    assert rel_l2(r.grad, o.grad) <= 1e-8 and rel_l2(r.qdag0, o.qdag0) <= 1e-10
+    loop = direct_adjoint_loop(sysm, f[0], target, "nonlinear", N=P, rk=rk, expaction=cfg, u0=u0,
+                               objective="tracking", time_law=law, eps=1e-10)
+    assert loop.iterations == len(hist) and loop.J == pytest.approx(float(r.J[0]), rel=1e-13)
+    assert rel_l2(loop.grad, r.grad[0]) <= 1e-12 and len(loop.error_history) == loop.iterations
+
+
+def test_nonlinear2d_against_the_reference_golden_and_limits(cuda_ok):
+    """The reference's own nonlinear-loop case (tests/golden/reference_nonlinear2d_tracking.npz) on the
+    GPU; a loose eps stops early; too few sweeps allowed raises IterationDivergence."""
+    from paper_2004_00546_b200 import (
+        ChebyshevConfig, Grid, ProblemSpec, RK4Config, TimeLaw, build_burgers2d_system, solve_nonlinear_tracking,
+        synthesize_trajectory)
+    from paper_2004_00546_b200.errors import IterationDivergence
+    from paper_2004_00546_b200.problems import BURGERS
+    gd = np.load(os.path.join(ROOT, "tests", "golden", "reference_nonlinear2d_tracking.npz"))
+    nx, ny, T, D, w, P = int(gd["nx"]), int(gd["ny"]), float(gd["T"]), float(gd["D"]), float(gd["omega"]), int(gd["N"])
+    sysm = build_burgers2d_system(Grid(nx, ny), ProblemSpec(BURGERS, (0.0, 0.0), D, T))
+    law, rk, cfg = TimeLaw.sine(w), RK4Config(T / (P * 125)), ChebyshevConfig(tol=1e-12)
+    target = synthesize_trajectory(sysm, gd["f_true"], rk, law)[:, 0, :]
+    r = solve_nonlinear_tracking(sysm, np.zeros(sysm.n), gd["f"], target, N=P, rk=rk, expaction=cfg, law=law, eps=1e-10)
+    assert abs(r.J[0] - gd["J"]) <= 2e-6 * abs(gd["J"])
+    assert rel_l2(r.grad[0], gd["grad"]) <= 1e-5
+    assert rel_l2(r.qdag0[0], gd["qdag0"]) <= 1e-5
+    assert len(r.timing["history"]) == int(gd["iterations"])   # the reference needed the same number of sweeps
+    loose = solve_nonlinear_tracking(sysm, np.zeros(sysm.n), gd["f"], target, N=P, rk=rk, expaction=cfg, law=law, eps=1e-2)
+    assert len(loose.timing["history"]) < len(r.timing["history"])
+    with pytest.raises(IterationDivergence):
+        solve_nonlinear_tracking(sysm, np.zeros(sysm.n), gd["f"], target, N=P, rk=rk, expaction=cfg, law=law,
+                                 eps=1e-12, max_iter=2)

@@ -51,6 +51,22 @@ def test_linear_run_file_and_errors(cuda_ok, tmp_path):
     g = [float(r["grad_norm"]) for r in rows]
     # Paraexp is exact for the linear problem: J and the gradient do not depend on N beyond the step size
     assert max(J) - min(J) <= 1e-6 * abs(J[0]) and max(g) - min(g) <= 1e-6 * g[0]
-    bad = dict(doc, algorithm="nonlinear")
+    bad = dict(doc, algorithm="hybrid")   # the hybrid needs the nonlinear testbed
     assert main(["run", "--config", _write(tmp_path, bad), "--output", str(out)]) == 1
     assert main(["run", "--config", str(tmp_path / "missing.json")]) == 1
+
+
+def test_burgers_iterative_run_file(cuda_ok, tmp_path):
+    """The reference's `configs/burgers_iterative.json` shape: algorithm "nonlinear" (Algorithm 2), eps 1e-3."""
+    from paper_2004_00546_b200.__main__ import main
+    doc = {"problem": {"kind": "burgers", "nx": 32, "ny": 32, "D": 1.0, "omega": 1.0, "T": 1.0,
+                       "f_true": "sin_product", "f_init": "ones"},
+           "algorithm": "nonlinear", "workers": [2, 4, 8], "rtol": 1e-3, "eps": 1e-3, "repeats": 2, "seed": 0}
+    out = tmp_path / "it"
+    assert main(["run", "--config", _write(tmp_path, doc), "--output", str(out)]) == 0
+    rows = list(csv.DictReader(open(out / "results.csv")))
+    assert [int(r["N"]) for r in rows] == [2, 4, 8] and all(int(r["K"]) >= 2 for r in rows)
+    summary = json.load(open(out / "summary.json"))
+    J = [float(r["J"]) for r in rows]
+    # the converged iterate is the serial trajectory up to eps and the step size
+    assert all(abs(j - summary["J_serial"]) <= 1e-3 * abs(summary["J_serial"]) for j in J)
