@@ -410,6 +410,18 @@ def main():
                "d2h_bytes_per_step": (c.batch + c.batch * c.K) * 8,
                "api": "direct_adjoint_loop(numpy host arrays); J and dJ/dc read to the host each step, "
                       "u(T) / q†(0) / ∫q† kept as device snapshots copied on first access"}
+        # the same with every n-sized result field read to the host each step (u(T), q†(0), ∫q† dt)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            lp = direct_adjoint_loop(c.system, ctrl, ut, algo, N=c.P, rk=rk, expaction=c.expaction, u0=u0)
+            fields = (lp.direct.final_state, lp.adjoint.initial_state, lp.adjoint.integral)
+        torch.cuda.synchronize()
+        el2 = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(el2, op=dist.ReduceOp.MAX)
+        e2e["with_result_fields"] = {"value": args.e2e_steps * c.batch / float(el2.item()), "unit": UNIT,
+                                     "d2h_bytes_per_step": (c.batch + c.batch * c.K) * 8 + sum(int(f.nbytes) for f in fields)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
