@@ -293,7 +293,8 @@ int px_get_kernel_timing(void* handle, int kclass, double* ms, uint64_t* launche
 
 /* ---- The reference's hybrid algorithm with its own objective (hybrid.py:1-290,
  * optimization.py:84-112,172-189) — a separate handle ----------------
- * 1D Burgers (V ≡ 0) with the forcing field f(x)·θ(t), θ(t) = law[0] + law[1]·sin(law[3]·t) +
+ * 1D Burgers (V ≡ 0), or with desc.ny > 1 the reference's own two-field system (U, V) on an nx×ny
+ * grid (problems.py:177-186, 316-343), with the forcing field f(x)·θ(t), θ(t) = law[0] + law[1]·sin(law[3]·t) +
  * law[2]·cos(law[3]·t) (the reference's f·sin(ωt): {0, 1, 0, ω}); tracking objective
  * J = (1/T)∫‖u − u_t‖² dt (trapezoid on the RK4 nodes) against a target given on the nodes;
  * slices of any widths on the serial sweep's uniform node grid (the geometric partition,
@@ -304,7 +305,7 @@ int px_get_kernel_timing(void* handle, int kclass, double* ms, uint64_t* launche
  * the slice (a progress flag per slice in HBM), i.e. during the serial sweep — the reference's
  * overlapped worker pipeline (hybrid.py:185-204). */
 typedef struct px_hybrid_desc {
-  int nx;              /* periodic 1D grid, n = nx */
+  int nx;              /* periodic grid; 1D: n = nx points per state */
   double D, hx, T;     /* diffusion, spacing, horizon */
   int batch;           /* B members, one forcing field each */
   int nslices;         /* P */
