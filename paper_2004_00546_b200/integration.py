@@ -18,7 +18,8 @@ reference's own layouts:
   "serial" runs the hybrid tracking loop on the GPU (`tracking.py`): the reference's 1D-embedded
   Burgers (y-invariant U on an nx×ny grid, V ≡ 0) maps onto the 1D path, J and ∂L/∂f are
   returned on the embedded grid; a genuinely two-dimensional forcing (U and V) runs the
-  two-field 2D path (`csrc/hybrid2d.cu`) in the reference's own state layout;
+  two-field 2D path (`csrc/hybrid2d.cu`) in the reference's own state layout, with "hybrid",
+  "serial" or "nonlinear" (Algorithm 2, ``eps`` / ``min_iter`` / ``max_iter`` as the reference's);
 * `solve_direct_linear` / `solve_adjoint_linear` (`paraexp.py:221-326`) for the linear
   testbed with the reference's forcing f·sin(ωt) and a terminal adjoint condition.
 
@@ -102,7 +103,8 @@ class ReferenceLoopResult:
     cuda: object = field(repr=False, default=None)
 
 
-def direct_adjoint_loop(ref_system, f, q_true, algorithm: str, N: int = 1, rk=None, leja=None, plan=None,
+def direct_adjoint_loop(ref_system, f, q_true, algorithm: str, N: int = 1, rk=None, leja=None, eps: float = 1e-3,
+                        min_iter: int = 2, max_iter: int = 25, plan=None,
                         backend: str = "cuda", probe_nodes: int | None = None, *, dt: float,
                         expaction: ChebyshevConfig | None = None, overlap: bool = True) -> ReferenceLoopResult:
     """`paradjoint.direct_adjoint_loop` with backend="cuda" (`optimization.py:154-231`).
@@ -116,8 +118,8 @@ def direct_adjoint_loop(ref_system, f, q_true, algorithm: str, N: int = 1, rk=No
         if hasattr(ref_system, "with_forcing_field") else ref_system
     sysm, f1, law, emb = system_from_reference(forced)
     T = sysm.spec.T
-    if sysm.is_linear:
-        # the linear loop (Paraexp direct and adjoint on N equal slices): whole steps per slice
+    if sysm.is_linear or algorithm == "nonlinear":
+        # equal slices (the linear loop; the iterative nonlinear direct): whole steps per slice
         steps = max(1, int(math.ceil(T / (N * dt) - 1e-9)))
         S = N * steps
         gplan = None
@@ -126,7 +128,8 @@ def direct_adjoint_loop(ref_system, f, q_true, algorithm: str, N: int = 1, rk=No
         gplan = make_hybrid_plan(T, plan.N, float(plan.k)) if plan is not None else None
     target = _node_trajectory(q_true, emb, T, S)
     r = loop(sysm, f1, target, algorithm, N=N, rk=RK4Config(T / S), expaction=expaction, u0=np.zeros(sysm.n),
-             objective="tracking", plan=gplan, time_law=law, overlap=overlap)
+             objective="tracking", plan=gplan, time_law=law, overlap=overlap, eps=eps, min_iter=min_iter,
+             max_iter=max_iter)
     rows = emb.ny if emb.kind == "burgers1d" else 1
     return ReferenceLoopResult(J=float(r.J) * rows, grad=emb.to_reference(np.asarray(r.grad)), seconds=r.seconds,
                                cuda=r)

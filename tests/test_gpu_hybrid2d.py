@@ -157,6 +157,11 @@ def test_hybrid2d_against_the_reference_golden_and_binding(cuda_ok):
     rb = direct_adjoint_loop(ref_system(np.zeros(sysm.n)), gd["f"], q_true, "hybrid", N=3, plan=plan, dt=1e-3)
     assert abs(rb.J - gd["J"]) <= 1e-6 * abs(gd["J"]) and rb.grad.shape == (sysm.n,)
     assert rel_l2(rb.grad, gd["grad"]) <= 1e-5
+    # the same binding with the reference's algorithm "nonlinear" (its golden numbers: the nonlinear loop's)
+    gn = np.load(os.path.join(ROOT, "tests", "golden", "reference_nonlinear2d_tracking.npz"))
+    rn = direct_adjoint_loop(ref_system(np.zeros(sysm.n)), gn["f"], q_true, "nonlinear", N=int(gn["N"]), eps=1e-9, dt=1e-3)
+    assert abs(rn.J - gn["J"]) <= 2e-6 * abs(gn["J"]) and rel_l2(rn.grad, gn["grad"]) <= 1e-5
+    assert rn.cuda.iterations == int(gn["iterations"])
 
 
 def test_hybrid2d_reference_config_size_and_overlap(cuda_ok):
