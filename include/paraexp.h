@@ -347,7 +347,7 @@ int px_hybrid_set_slice_plan(void* handle, int p, const px_cheb_plan* plan, cons
 /* The frozen-operator carry and the gradient (needs every slice plan). */
 int px_hybrid_adjoint(void* handle, void* stream);
 /* The reference's loop with algorithm "nonlinear" on the 2D two-field handle (desc.ny > 1, equal
- * slices, nx·ny ≤ 2048): the iterative nonlinear direct, Algorithm 2 (nonlinear.py:69-194;
+ * slices): the iterative nonlinear direct, Algorithm 2 (nonlinear.py:69-194;
  * optimization.py:206-231). px_hybrid_nl_init: the constant initial guess u0 on every node; then per
  * sweep px_hybrid_bounds (slice means and FOV box of the iterate) → px_hybrid_nl_set_plans (the
  * actions exp(Δ(D∇² + J̄_p)) of slice width and of step width, exp series only) →

@@ -1026,6 +1026,178 @@ __global__ void __launch_bounds__(256) k_b2s_nl_err(B2sNlArgs a) {
   if (threadIdx.x == 0) a.err[lane] = rd > 0.0 ? sqrt(rn) / sqrt(rd) : sqrt(rn);
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Algorithm 2 with the fields in HBM (grids above B2S_MAX_N points): one launch per RK4 stage /
+// Chebyshev term over (points, lanes), the same operation sequence as the on-chip kernels.
+// ---------------------------------------------------------------------------------------------
+
+// forward operator (D∇² + ∂N/∂q at q̄)·x at point i, q̄ and x in global memory
+__device__ __forceinline__ void b2_jfull(const B2Geom& g, const double* Qm, const double* X, int n, int i, int e, int w,
+                                         int nn, int s, double& oa, double& ob) {
+  b2s_jfull(g, Qm, X, n, i, e, w, nn, s, oa, ob);  // plain pointer arithmetic: any address space
+}
+
+struct B2NlStageArgs {
+  const double* yin;    // L × 2n stage input (neighbours read)
+  double* y;            // L × 2n: y_k (base); stage 4 writes y_{k+1}
+  const double* accin;  // L × 2n (stage 1: y)
+  double* accout;       // L × 2n (stage 4: y)
+  double* yout;         // L × 2n or null
+  const double* cst;    // L × 2n: (D∇² + J̄_p)·u0
+  const double* Q;      // (S+1) × B × 2n iterate
+  double* Qn;           // next iterate (stage 4: node + 1 ← u0 + y_{k+1} when write_node)
+  const double* ubar;   // P × B × 2n
+  const double* u0;     // B × 2n
+  const double* f;      // B × 2n
+  const double* theta;
+  double wa, wb, cw, ca;
+  int tsel;             // θ at node (0), node + ½ (1), node + 1 (2)
+  int k, nsteps, P, B, write_node;
+  B2Geom g;
+};
+
+__global__ void __launch_bounds__(256) k_b2_nl_stage(B2NlStageArgs a) {
+  const int n = a.g.nx * a.g.ny;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int lane = blockIdx.y, b = lane / a.P, p = lane % a.P;
+  const size_t n2 = 2 * (size_t)n, ns = (size_t)a.B * n2;
+  const int node = p * a.nsteps + a.k;
+  const double* qa = a.Q + (size_t)node * ns + (size_t)b * n2;
+  const double* qc = a.Q + (size_t)(node + 1) * ns + (size_t)b * n2;
+  const double* Qm = a.ubar + ((size_t)p * a.B + b) * n2;
+  int e, w, nn, s;
+  b2_nbrs(i, a.g, e, w, nn, s);
+  auto st = [&](size_t k) { return a.wa * qa[k] + a.wb * qc[k]; };
+  const double uc = st(i), ue = st(e), uw = st(w), un = st(nn), us = st(s);
+  const double vc = st(n + i), ve = st(n + e), vw = st(n + w), vn = st(n + nn), vs = st(n + s);
+  const double Nu = -uc * (ue - uw) * a.g.i2hx - vc * (un - us) * a.g.i2hy;
+  const double Nv = -uc * (ve - vw) * a.g.i2hx - vc * (vn - vs) * a.g.i2hy;
+  const double* Vm = Qm + n;
+  const double Ub = Qm[i], Vb = Vm[i];
+  const double dUx = (Qm[e] - Qm[w]) * a.g.i2hx, dUy = (Qm[nn] - Qm[s]) * a.g.i2hy;
+  const double dVx = (Vm[e] - Vm[w]) * a.g.i2hx, dVy = (Vm[nn] - Vm[s]) * a.g.i2hy;
+  const double Ja = -Ub * (ue - uw) * a.g.i2hx - Vb * (un - us) * a.g.i2hy - dUx * uc - dUy * vc;
+  const double Jb = -Ub * (ve - vw) * a.g.i2hx - Vb * (vn - vs) * a.g.i2hy - dVx * uc - dVy * vc;
+  const double* Y = a.yin + (size_t)lane * n2;
+  double ka, kb;
+  b2_jfull(a.g, Qm, Y, n, i, e, w, nn, s, ka, kb);
+  const double th = a.theta[2 * node + a.tsel];
+  const double* cs = a.cst + (size_t)lane * n2;
+  const double* f = a.f + (size_t)b * n2;
+  ka += cs[i] + th * f[i] + Nu - Ja;
+  kb += cs[n + i] + th * f[n + i] + Nv - Jb;
+  const double* base = a.y + (size_t)lane * n2;
+  const double* ai = a.accin + (size_t)lane * n2;
+  const double ra = ai[i] + a.ca * ka, rb = ai[n + i] + a.ca * kb;
+  if (a.yout) {
+    double* yo = a.yout + (size_t)lane * n2;
+    yo[i] = base[i] + a.cw * ka;
+    yo[n + i] = base[n + i] + a.cw * kb;
+  }
+  double* ao = a.accout + (size_t)lane * n2;
+  ao[i] = ra;
+  ao[n + i] = rb;
+  if (a.write_node) {
+    const double* u0 = a.u0 + (size_t)b * n2;
+    double* qo = a.Qn + (size_t)(node + 1) * ns + (size_t)b * n2;
+    qo[i] = u0[i] + ra;
+    qo[n + i] = u0[n + i] + rb;
+  }
+}
+
+// cst[lane] = (D∇² + J̄_p)·u0, y[lane] = 0
+__global__ void __launch_bounds__(256) k_b2_nl_prepare(double* cst, double* y, const double* ubar, const double* u0,
+                                                       int P, int B, B2Geom g) {
+  const int n = g.nx * g.ny;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int lane = blockIdx.y, b = lane / P, p = lane % P;
+  const size_t n2 = 2 * (size_t)n;
+  int e, w, nn, s;
+  b2_nbrs(i, g, e, w, nn, s);
+  double oa, ob;
+  b2_jfull(g, ubar + ((size_t)p * B + b) * n2, u0 + (size_t)b * n2, n, i, e, w, nn, s, oa, ob);
+  cst[(size_t)lane * n2 + i] = oa;
+  cst[(size_t)lane * n2 + n + i] = ob;
+  y[(size_t)lane * n2 + i] = 0.0;
+  y[(size_t)lane * n2 + n + i] = 0.0;
+}
+
+// one Chebyshev term of exp(τ(D∇² + J̄))·x over `rows` vectors; row r uses q̄ of slice
+// (pfix ≥ 0 ? pfix : r mod P) and member (pfix ≥ 0 ? r : r / P); rows with skip0 and slice 0 idle
+struct B2FwdTermArgs {
+  const double* x; const double* prev; double* out; double* acc;
+  const double* ubar;
+  double alpha, c0, sg, be0, bek;
+  int first, P, B, pfix, skip0;
+  B2Geom g;
+};
+
+__global__ void __launch_bounds__(256) k_b2_fwd_term(B2FwdTermArgs a) {
+  const int n = a.g.nx * a.g.ny;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int r = blockIdx.y;
+  const int p = a.pfix >= 0 ? a.pfix : r % a.P, b = a.pfix >= 0 ? r : r / a.P;
+  if (a.skip0 && p == 0) return;
+  const size_t n2 = 2 * (size_t)n, off = (size_t)r * n2;
+  int e, w, nn, s;
+  b2_nbrs(i, a.g, e, w, nn, s);
+  const double* X = a.x + off;
+  double oa, ob;
+  b2_jfull(a.g, a.ubar + ((size_t)p * a.B + b) * n2, X, n, i, e, w, nn, s, oa, ob);
+  const double xa = X[i], xb = X[n + i];
+  double ua = a.alpha * (oa - a.c0 * xa), ub = a.alpha * (ob - a.c0 * xb);
+  double* acc = a.acc + off;
+  if (a.first) {
+    acc[i] = a.be0 * xa + a.bek * ua;
+    acc[n + i] = a.be0 * xb + a.bek * ub;
+  } else {
+    const double* P_ = a.prev + off;
+    ua += a.sg * P_[i];
+    ub += a.sg * P_[n + i];
+    acc[i] += a.bek * ua;
+    acc[n + i] += a.bek * ub;
+  }
+  double* o = a.out + off;
+  o[i] = ua;
+  o[n + i] = ub;
+}
+
+// D_{p+1}[b] = (p > 0 ? C[b] : 0) + yend[b·P + p]; C ← D_{p+1}
+__global__ void k_b2_nl_carry_add(double* C, double* Dnext, const double* yend, int P, int p, size_t n2) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n2) return;
+  const size_t b = blockIdx.y;
+  const double v = (p > 0 ? C[b * n2 + i] : 0.0) + yend[(b * P + p) * n2 + i];
+  C[b * n2 + i] = v;
+  Dnext[b * n2 + i] = v;
+}
+
+// H[lane] = D_p[b]; Qn[p·ns][b] = u0 + D_p; lane P−1 also Qn[S][b] = u0 + D_P
+__global__ void k_b2_nl_hom_init(double* H, double* Qn, const double* Dc, const double* u0, int P, int B, int nsteps,
+                                 int S, size_t n2) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n2) return;
+  const int lane = blockIdx.y, b = lane / P, p = lane % P;
+  const size_t ns = (size_t)B * n2;
+  const double d = Dc[(size_t)p * ns + (size_t)b * n2 + i], u = u0[(size_t)b * n2 + i];
+  H[(size_t)lane * n2 + i] = d;
+  Qn[(size_t)(p * nsteps) * ns + (size_t)b * n2 + i] = u + d;
+  if (p == P - 1) Qn[(size_t)S * ns + (size_t)b * n2 + i] = u + Dc[(size_t)P * ns + (size_t)b * n2 + i];
+}
+
+// Qn[p·ns + k][b] += H[lane] (lanes of slice 0 idle: D_0 = 0)
+__global__ void k_b2_nl_hom_add(double* Qn, const double* H, int P, int B, int nsteps, int k, size_t n2) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n2) return;
+  const int lane = blockIdx.y, b = lane / P, p = lane % P;
+  if (p == 0) return;
+  Qn[(size_t)(p * nsteps + k) * (size_t)B * n2 + (size_t)b * n2 + i] += H[(size_t)lane * n2 + i];
+}
+
 }  // namespace px
 
 namespace pxi {
@@ -1528,10 +1700,92 @@ int h2_adjoint(Hybrid2D* hy, cudaStream_t s) {
   return PX_OK;
 }
 
+// One planned forward action on `rows` vectors held in four rotating buffers buf[0..3] (each
+// rows × 2n); the input is buf[*c], the result's index is returned in *c.
+int fwd_action_launches(Hybrid2D* hy, double* const* buf, int* c, int rows, int pfix, int skip0,
+                        const Hybrid2D::NlPlan& pl, const std::vector<double>& be, cudaStream_t s) {
+  const int n = hy->nx * hy->ny;
+  const dim3 grid((unsigned)((n + 255) / 256), (unsigned)rows);
+  px::B2FwdTermArgs a{};
+  a.ubar = hy->ubar; a.c0 = pl.c0; a.P = hy->P; a.B = hy->B; a.pfix = pfix; a.skip0 = skip0; a.g = geom(hy);
+  for (int j = 0; j < pl.subs; ++j) {
+    const int f1 = (*c + 1) & 3, f2 = (*c + 2) & 3, f3 = (*c + 3) & 3;
+    a.x = buf[*c]; a.prev = nullptr; a.out = buf[f1]; a.acc = buf[f2];
+    a.alpha = 1.0 / pl.d; a.sg = 0.0; a.first = 1; a.be0 = be[0]; a.bek = be[1];
+    px::k_b2_fwd_term<<<grid, 256, 0, s>>>(a);
+    H2_LAUNCHED(hy);
+    int prev = *c, cur = f1, nxt = f3;
+    a.alpha = 2.0 / pl.d; a.sg = (double)pl.sigma; a.first = 0;
+    for (int k = 2; k <= pl.K; ++k) {
+      a.x = buf[cur]; a.prev = buf[prev]; a.out = buf[nxt]; a.bek = be[k];
+      px::k_b2_fwd_term<<<grid, 256, 0, s>>>(a);
+      H2_LAUNCHED(hy);
+      const int t = prev;
+      prev = cur; cur = nxt; nxt = t;
+    }
+    *c = f2;
+  }
+  return PX_OK;
+}
+
+// Algorithm 2's sweep with one launch per stage / term (any grid size)
+int nl_sweep_launches(Hybrid2D* hy, cudaStream_t s) {
+  const int n = hy->nx * hy->ny;
+  const size_t n2 = 2 * (size_t)n, B = hy->B;
+  const int P = hy->P, L = hy->B * P, ns = hy->offs[1];
+  const double h = hy->h;
+  const dim3 gl((unsigned)((n + 255) / 256), (unsigned)L), gl2((unsigned)((n2 + 255) / 256), (unsigned)L);
+  const dim3 gb2((unsigned)((n2 + 255) / 256), (unsigned)B);
+  // slice lanes: y = la, cst = lz, acc = lacc, stage inputs ly[0/1]
+  px::k_b2_nl_prepare<<<gl, 256, 0, s>>>(hy->lz, hy->la, hy->ubar, hy->u0, P, hy->B, geom(hy));
+  H2_LAUNCHED(hy);
+  px::B2NlStageArgs a{};
+  a.y = hy->la; a.cst = hy->lz; a.Q = hy->traj; a.Qn = hy->Qn; a.ubar = hy->ubar; a.u0 = hy->u0; a.f = hy->f;
+  a.theta = hy->theta; a.nsteps = ns; a.P = P; a.B = hy->B; a.g = geom(hy);
+  for (int k = 0; k < ns; ++k) {
+    a.k = k; a.write_node = 0;
+    a.yin = hy->la; a.accin = hy->la; a.accout = hy->lacc; a.yout = hy->ly[0];
+    a.wa = 1.0; a.wb = 0.0; a.tsel = 0; a.cw = 0.5 * h; a.ca = h / 6.0;
+    px::k_b2_nl_stage<<<gl, 256, 0, s>>>(a);
+    H2_LAUNCHED(hy);
+    a.yin = hy->ly[0]; a.accin = hy->lacc; a.yout = hy->ly[1];
+    a.wa = 0.5; a.wb = 0.5; a.tsel = 1; a.ca = h / 3.0;
+    px::k_b2_nl_stage<<<gl, 256, 0, s>>>(a);
+    H2_LAUNCHED(hy);
+    a.yin = hy->ly[1]; a.yout = hy->ly[0]; a.cw = h;
+    px::k_b2_nl_stage<<<gl, 256, 0, s>>>(a);
+    H2_LAUNCHED(hy);
+    a.yin = hy->ly[0]; a.accout = hy->la; a.yout = nullptr;
+    a.wa = 0.0; a.wb = 1.0; a.tsel = 2; a.ca = h / 6.0; a.write_node = (k + 1 < ns) ? 1 : 0;
+    px::k_b2_nl_stage<<<gl, 256, 0, s>>>(a);
+    H2_LAUNCHED(hy);
+  }
+  // summed-chain carry (member vectors in w[0..3]); yend = la
+  int c = 0;
+  H2_CUDA(hy, cudaMemsetAsync(hy->Dc, 0, B * n2 * sizeof(double), s));
+  for (int p = 0; p < P; ++p) {
+    if (p > 0) PX_TRY(fwd_action_launches(hy, hy->w, &c, hy->B, p, 0, hy->nl_s, hy->nl_be_s, s));
+    px::k_b2_nl_carry_add<<<gb2, 256, 0, s>>>(hy->w[c], hy->Dc + (size_t)(p + 1) * B * n2, hy->la, P, p, n2);
+    H2_LAUNCHED(hy);
+  }
+  // homogeneous parts on every node: lane vectors rotate through ly[0], ly[1], lacc, lz
+  double* hb[4] = {hy->ly[0], hy->ly[1], hy->lacc, hy->lz};
+  int hc = 0;
+  px::k_b2_nl_hom_init<<<gl2, 256, 0, s>>>(hb[0], hy->Qn, hy->Dc, hy->u0, P, hy->B, ns, hy->S, n2);
+  H2_LAUNCHED(hy);
+  if (P > 1) {
+    for (int k = 1; k < ns; ++k) {
+      PX_TRY(fwd_action_launches(hy, hb, &hc, L, -1, 1, hy->nl_h, hy->nl_be_h, s));
+      px::k_b2_nl_hom_add<<<gl2, 256, 0, s>>>(hy->Qn, hb[hc], P, hy->B, ns, k, n2);
+      H2_LAUNCHED(hy);
+    }
+  }
+  return PX_OK;
+}
+
 // ---- Algorithm 2 (iterative nonlinear direct) on the two-field testbed --------------------------
 int h2_nl_init(Hybrid2D* hy, cudaStream_t s) {
   if (!hy->inputs) return fail(&hy->base, PX_ERR_STATE, "hybrid: inputs not set");
-  if (!hy->small) return fail(&hy->base, PX_ERR_ARG, "Algorithm 2 on the 2D testbed runs on chip: nx·ny ≤ 2048");
   const int ns = hy->offs[1];
   for (int p = 0; p <= hy->P; ++p)
     if (hy->offs[p] != p * ns) return fail(&hy->base, PX_ERR_ARG, "Algorithm 2 needs equal slices (nonlinear.py: equidistant)");
@@ -1569,6 +1823,8 @@ int h2_nl_set_plans(Hybrid2D* hy, const px_cheb_plan* ps, const px_cheb_plan* ph
   std::vector<double> pool(ps->coef_exp, ps->coef_exp + ps->degree + 1);
   pool.insert(pool.end(), ph->coef_exp, ph->coef_exp + ph->degree + 1);
   H2_CUDA(hy, cudaMemcpy(hy->nl_coef, pool.data(), pool.size() * sizeof(double), cudaMemcpyHostToDevice));
+  hy->nl_be_s.assign(ps->coef_exp, ps->coef_exp + ps->degree + 1);
+  hy->nl_be_h.assign(ph->coef_exp, ph->coef_exp + ph->degree + 1);
   hy->nl_s = {ps->degree, ps->substeps, ps->sigma, ps->center, ps->scale};
   hy->nl_h = {ph->degree, ph->substeps, ph->sigma, ph->center, ph->scale};
   hy->nl_plans = true;
@@ -1588,6 +1844,9 @@ int h2_nl_sweep(Hybrid2D* hy, double* err_out, cudaStream_t s) {
   a.Kh = hy->nl_h.K; a.subs_h = hy->nl_h.subs; a.sig_h = hy->nl_h.sigma; a.c0_h = hy->nl_h.c0; a.d_h = hy->nl_h.d;
   a.h = hy->h; a.g = geom(hy);
   const int lanes = hy->B * hy->P;
+  if (!hy->small) {
+    PX_TRY(nl_sweep_launches(hy, s));
+  } else
   H2_CUDA(hy, b2s_dispatch(hy->ppt, [&](auto pc) {
     constexpr int PPT = decltype(pc)::value;
     const size_t sm5 = 5 * n2 * sizeof(double), sm4 = 4 * n2 * sizeof(double);
@@ -1631,7 +1890,14 @@ int h2_nl_finish(Hybrid2D* hy, cudaStream_t s) {
   H2_CUDA(hy, cudaEventRecord(hy->ev[0], s));
   H2_CUDA(hy, cudaEventRecord(hy->ev[1], s));
   H2_CUDA(hy, cudaEventRecord(hy->ev[2], s));
-  H2_CUDA(hy, b2s_launch_lanes(l, hy->ppt, 4 * n2 * sizeof(double), s));
+  if (hy->small) {
+    H2_CUDA(hy, b2s_launch_lanes(l, hy->ppt, 4 * n2 * sizeof(double), s));
+  } else {
+    const size_t L = (size_t)hy->B * hy->P;
+    H2_CUDA(hy, cudaMemsetAsync(hy->la, 0, L * n2 * sizeof(double), s));
+    H2_CUDA(hy, cudaMemsetAsync(hy->lz, 0, L * n2 * sizeof(double), s));
+    for (int k = 0; k < hy->max_np; ++k) PX_TRY(adjoint_step(hy, k, 0, hy->P, s));
+  }
   H2_CUDA(hy, cudaEventRecord(hy->ev[3], s));
   px::k_b2_cost_partial<<<dim3((unsigned)hy->cost_blocks, (unsigned)hy->B), 256, 0, s>>>(
       hy->cpart, hy->traj, hy->target, hy->target_b, n2, hy->S, hy->B);

@@ -56,6 +56,7 @@ struct Hybrid2D : HybridHead {
   double *Qn = nullptr, *Dc = nullptr, *nl_err = nullptr, *nl_coef = nullptr;
   struct NlPlan { int K = 0, subs = 0, sigma = -1; double c0 = 0.0, d = 1.0; };
   NlPlan nl_s, nl_h;
+  std::vector<double> nl_be_s, nl_be_h;  // host copies of the two exp series (per-term launches)
   bool nl_active = false, nl_plans = false;
   cudaStream_t side[NSIDE] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> ev_slice;

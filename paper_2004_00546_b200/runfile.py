@@ -11,7 +11,7 @@ f·sin(ωt), and ``results.csv`` / ``summary.json`` (and ``descent.csv``) are wr
 The reference's adaptive tolerances (``rtol``, ``leja_tol``) have no fixed-step counterpart: the
 RK4 step is ``dt`` (default: min(T/200, 1/λ) with λ the diffusion part's spectral radius) and the
 exponential actions are planned to 1e-12. ``checkpoints`` and the Gantt / PNG outputs are not
-part of this path; `algorithm: "nonlinear"` (Algorithm 2) runs for nx·ny ≤ 2048. Field shapes: "sin_product", "ones", "zeros" or a flat list."""
+part of this path. Field shapes: "sin_product", "ones", "zeros" or a flat list."""
 
 from __future__ import annotations
 
@@ -160,8 +160,6 @@ def run_file(rf: RunFile, output: str | None = None, dt: float | None = None, re
     from .tracking import synthesize_trajectory
     if rf.checkpoints:
         raise ConfigError("checkpoints: run files run without checkpointing here (run_checkpointed_loop takes BASELINE configs)")
-    if rf.algorithm == "nonlinear" and rf.nx * rf.ny > 2048:
-        raise ConfigError("algorithm: the iterative nonlinear direct (Algorithm 2) runs on chip here: nx·ny ≤ 2048")
     if rf.algorithm in ("hybrid", "nonlinear") and rf.kind != BURGERS:
         raise ConfigError(f"algorithm: the {rf.algorithm} algorithm is for the Burgers testbed")
     out = output or rf.output

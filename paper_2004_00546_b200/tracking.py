@@ -313,7 +313,7 @@ def solve_nonlinear_tracking(system: System, u0, f, target, N: int = 1, rk: RK4C
     (`optimization.py:206-231`): the iterative nonlinear direct (Algorithm 2, `nonlinear.py:69-194`)
     on ``N`` equal slices, then `solve_adjoint_varying` with the source 2(q − q_t) and zero terminal
     data (the hybrid's adjoint form), the tracking cost and ∂L/∂f. ``timing["history"]`` holds the
-    sweeps' errors. Small grids (nx·ny ≤ 2048), whole RK4 steps per slice."""
+    sweeps' errors. Whole RK4 steps per slice (on chip for nx·ny ≤ 2048, per-stage launches above)."""
     if rk is None:
         raise ConfigError("rk: an RK4Config(dt) is required (fixed-step RK4)")
     if not getattr(system, "is_burgers2d", False):

@@ -278,3 +278,19 @@ def test_nonlinear2d_against_the_reference_golden_and_limits(cuda_ok):
     with pytest.raises(IterationDivergence):
         solve_nonlinear_tracking(sysm, np.zeros(sysm.n), gd["f"], target, N=P, rk=rk, expaction=cfg, law=law,
                                  eps=1e-12, max_iter=2)
+
+
+@pytest.mark.parametrize("grid", [(24, 20), (64, 48)])
+def test_nonlinear2d_per_stage_launches_vs_oracle(cuda_ok, per_stage_launches, grid):
+    """Algorithm 2 through the per-stage-launch kernels (forced on a small grid, and a grid above the
+    on-chip limit): the same sweeps and numbers as the oracle."""
+    from paper_2004_00546_b200 import solve_nonlinear_tracking, synthesize_trajectory
+    sysm, u0, f, f_true, rk, cfg, law = _case(nx=grid[0], ny=grid[1], T=0.24, dt=1.5e-3, B=2 if grid[0] < 32 else 1)
+    P, nsteps = 4, 40
+    target = synthesize_trajectory(sysm, f_true, rk, law)[:, 0, :]
+    r = solve_nonlinear_tracking(sysm, u0, f, target, N=P, rk=rk, expaction=cfg, law=law, eps=1e-10)
+    o = _nl_oracle(sysm, u0, f, target, P, nsteps, law, cfg, 1e-10)
+    assert len(r.timing["history"]) == o.extras["sweeps"]
+    assert np.max(np.abs(r.J - o.J) / np.abs(o.J)) <= 1e-10
+    assert rel_l2(r.final_state, o.uT) <= 1e-10
+    assert rel_l2(r.grad, o.grad) <= 1e-8 and rel_l2(r.qdag0, o.qdag0) <= 1e-10

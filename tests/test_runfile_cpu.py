@@ -55,9 +55,9 @@ def test_invalid_run_files_name_the_field(doc, text):
 
 def test_unsupported_parts_are_refused_before_any_gpu_work():
     from paper_2004_00546_b200.runfile import run_file
-    big = _doc(algorithm="nonlinear")
-    big["problem"] = dict(big["problem"], nx=64, ny=64)
-    with pytest.raises(ConfigError, match="Algorithm 2"):
-        run_file(parse_run_file(big))
+    lin = _doc(algorithm="hybrid")
+    lin["problem"] = dict(lin["problem"], kind="advection_diffusion")
+    with pytest.raises(ConfigError, match="Burgers"):
+        run_file(parse_run_file(lin))
     with pytest.raises(ConfigError, match="checkpoints"):
         run_file(parse_run_file(_doc(checkpoints=2)))
