@@ -16,7 +16,8 @@
 //               adjoint lanes with the source 2(u − u_t))
 //   hybrid.cu   C ABI of the reference's hybrid with its tracking objective (px_hybrid_*); its
 //               kernels (hybrid.cuh) are instantiated in burgers.cu
-//   hybrid2d.cu the same entry points on the reference's 2D two-field Burgers testbed (desc.ny > 1)
+//   hybrid2d.cu hybrid2d.cuh: the same entry points on the reference's 2D two-field Burgers testbed
+//               (desc.ny > 1), Algorithm 2 on it (px_hybrid_nl_*)
 #pragma once
 #include <cuda_runtime.h>
 #include <cufft.h>
