@@ -70,3 +70,19 @@ def test_burgers_iterative_run_file(cuda_ok, tmp_path):
     J = [float(r["J"]) for r in rows]
     # the converged iterate is the serial trajectory up to eps and the step size
     assert all(abs(j - summary["J_serial"]) <= 1e-3 * abs(summary["J_serial"]) for j in J)
+
+
+def test_numbered_baseline_configs_through_the_cli(cuda_ok, tmp_path, capsys):
+    """`run --config K` (BASELINE configs), the checkpointed run and `predict` still answer."""
+    from paper_2004_00546_b200.__main__ import main
+    out = tmp_path / "c1"
+    assert main(["run", "--config", "1", "--repeats", "1", "--output", str(out)]) == 0
+    s = json.load(open(out / "summary.json"))
+    assert s["backend"] == "cuda" and s["timing"]["gradient_evals_per_s"] > 0
+    assert main(["run", "--config", "3", "--repeats", "1", "--checkpoints", "3", "--output", str(tmp_path / "c3")]) == 0
+    assert json.load(open(tmp_path / "c3" / "summary.json"))["checkpoints"] == 3
+    capsys.readouterr()
+    assert main(["predict", "--config", "2", "--repeats", "1", "--gpus", "1", "2"]) == 0
+    pred = json.loads(capsys.readouterr().out)
+    assert [p["gpus"] for p in pred["prediction"]] == [1, 2]
+    assert main(["run", "--config", "9"]) == 1   # unknown config number
