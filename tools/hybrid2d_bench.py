@@ -1,8 +1,8 @@
 """Device timing of the hybrid tracking path on the reference's own 2D two-field Burgers testbed
 (csrc/hybrid2d.cu): the reference's `configs/burgers_hybrid.json` shape (32×32, D = 1, ω = 1,
 T = 1) and larger grids; sequential vs stream-overlapped slice solves; whole-gradient time with
-events around the public solve; for the 32×32 case the CPU oracle's time for the same gradient.
-Prints one JSON line per variant."""
+events around the public solve. Prints one JSON line per variant. (The CPU oracle's time for the
+same gradients: tests/time_hybrid2d_vs_oracle.py — only tests/ may run the oracle.)"""
 
 import json
 import os
@@ -14,7 +14,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
-def run(nx, ny, D, T, dt, P, k, with_oracle):
+def run(nx, ny, D, T, dt, P, k, with_oracle=False):
     import torch
 
     from paper_2004_00546_b200 import (
@@ -49,26 +49,10 @@ def run(nx, ny, D, T, dt, P, k, with_oracle):
         print(json.dumps({"grid": [nx, ny], "steps": S, "slices": P, "k": k, "overlap": ov,
                           "gradient_ms_events": best[0], "gradient_ms_wall": best[1], **best[2],
                           "frozen_terms": terms, "J": float(r.J[0])}), flush=True)
-    if with_oracle:
-        from oracle.config_mode import burgers_tracking_hybrid
-        from paper_2004_00546_b200.expaction import plan_family
-        from paper_2004_00546_b200.problems import frozen_bounds_2d, frozen_region_from_bounds
-        offs = r.offsets
-        h = T / offs[-1]
-
-        def pf(ub):
-            reg = frozen_region_from_bounds(*frozen_bounds_2d(ub, sysm.grid, D))
-            return plan_family(reg, [(offs[p + 1] - offs[p]) * h for p in range(P)], cfg, omega=law.omega)
-
-        t0 = time.perf_counter()
-        o = burgers_tracking_hybrid(nx, D, T, offs, u0, f[None, :], law.as_tuple(), target_host, pf, ny=ny)
-        sec = time.perf_counter() - t0
-        print(json.dumps({"grid": [nx, ny], "cpu_oracle_s": sec, "cores": 1,
-                          "J_rel": abs(o.J[0] - r.J[0]) / abs(o.J[0]),
-                          "grad_rel": float(np.linalg.norm(o.grad - r.grad) / np.linalg.norm(o.grad))}), flush=True)
+    return sysm, u0, f, law, cfg, target_host, r
 
 
-def run_nonlinear(nx, ny, D, T, dt, P, eps, with_oracle):
+def run_nonlinear(nx, ny, D, T, dt, P, eps, with_oracle=False):
     """The reference's `configs/burgers_iterative.json` shape: Algorithm 2 + the zero-terminal adjoint."""
     import torch
 
@@ -94,28 +78,14 @@ def run_nonlinear(nx, ny, D, T, dt, P, eps, with_oracle):
         reps.append((time.perf_counter() - t0) * 1e3)
     print(json.dumps({"grid": [nx, ny], "algorithm": "nonlinear", "slices": P, "steps": int(r.offsets[-1]), "eps": eps,
                       "sweeps": len(r.timing["history"]), "gradient_ms_wall": min(reps), "J": float(r.J[0])}), flush=True)
-    if with_oracle:
-        from oracle.config_mode import burgers2d_nonlinear_tracking
-        from paper_2004_00546_b200.expaction import plan_chebyshev, plan_family
-        from paper_2004_00546_b200.problems import frozen_bounds_2d, frozen_region_from_bounds
-        nsteps = int(r.offsets[1])
-        h = T / (P * nsteps)
-        reg = lambda q: frozen_region_from_bounds(*frozen_bounds_2d(q, sysm.grid, D))
-        t0 = time.perf_counter()
-        o = burgers2d_nonlinear_tracking(nx, ny, D, T, P, nsteps, u0, f[None, :], law.as_tuple(), target,
-                                         lambda q: (plan_chebyshev(reg(q), T / P, cfg), plan_chebyshev(reg(q), h, cfg)),
-                                         lambda q: plan_family(reg(q), [T / P] * P, cfg, omega=law.omega), eps)
-        sec = time.perf_counter() - t0
-        print(json.dumps({"grid": [nx, ny], "algorithm": "nonlinear", "cpu_oracle_s": sec, "cores": 1,
-                          "sweeps": o.extras["sweeps"], "J_rel": abs(o.J[0] - r.J[0]) / abs(o.J[0]),
-                          "grad_rel": float(np.linalg.norm(o.grad - r.grad) / np.linalg.norm(o.grad))}), flush=True)
+    return sysm, u0, f, law, cfg, target, r
 
 
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "small":   # the 32×32 hybrid case only (ncu captures)
         run(32, 32, 1.0, 1.0, 1e-3, 16, 3.0, False)
         sys.exit(0)
-    run_nonlinear(32, 32, 1.0, 1.0, 1e-3, 8, 1e-3, True)   # the reference's burgers_iterative.json shape
-    run(32, 32, 1.0, 1.0, 1e-3, 16, 3.0, True)       # the reference's burgers_hybrid.json shape
+    run_nonlinear(32, 32, 1.0, 1.0, 1e-3, 8, 1e-3)   # the reference's burgers_iterative.json shape
+    run(32, 32, 1.0, 1.0, 1e-3, 16, 3.0)      # the reference's burgers_hybrid.json shape
     run(128, 128, 0.05, 0.5, 1e-3, 16, 3.0, False)
     run(512, 512, 0.01, 0.2, 1e-3, 8, 3.0, False)
