@@ -7,7 +7,8 @@ sweeps as hand-written sm_100a fp64 kernels behind the C ABI in
 ``include/paraexp.h`` (``libparaexp.so``). There is no CPU fallback.
 """
 
-from .checkpointing import CheckpointRun, CheckpointSchedule, MemoryCounter, run_checkpointed_loop
+from .checkpointing import (CheckpointRun, CheckpointSchedule, CheckpointTrackingRun, MemoryCounter,
+                            run_checkpointed_loop, run_checkpointed_tracking)
 from .configs import BaselineCase, baseline, scaled
 from .engine import EngineSpec, ParaexpEngine
 from .errors import (

@@ -213,3 +213,86 @@ def run_checkpointed_loop(
         segment_bounds=bounds, checkpoint_states=states, adjoint_checkpoint_states=adj_states[::-1],
         memory=memory, segment_grads=seg_grads[::-1],
     )
+
+
+@dataclass
+class CheckpointTrackingRun:
+    """Result of `run_checkpointed_tracking` (the reference's `CheckpointRun`, `checkpointing.py:79-91`)."""
+
+    gradient: np.ndarray            # (n,) ∂L/∂f
+    qdag0: np.ndarray               # (n,) q†(0)
+    cost: float                     # J = (1/T)∫‖q − q_t‖² dt
+    final_state: np.ndarray         # (n,) q(T)
+    segment_bounds: list[tuple[float, float]]
+    checkpoint_states: list[np.ndarray]
+    adjoint_checkpoint_states: list[np.ndarray]
+    memory: MemoryCounter
+
+
+def run_checkpointed_tracking(system: System, f, target, sched: CheckpointSchedule, N: int = 1,
+                              rk: RK4Config | None = None, expaction=None, law=None, k_ratio: float | None = None,
+                              u0=None, overlap: bool = True) -> CheckpointTrackingRun:
+    """The reference's checkpointed loop with its own objective on the Burgers testbed, algorithm
+    "hybrid" (`checkpointing.py:119-267`): phase one sweeps the segments forward keeping only the
+    checkpoint states; phase two walks them backward — each segment is one hybrid solve
+    (`tracking.solve_hybrid_tracking`) from its checkpoint with the forcing law and the target in
+    the segment's local time, seeded with the carried adjoint state as terminal data (the final
+    span, `hybrid.py:232-233`), its cost and gradient shares (T_seg/T of the segment's own
+    (1/T_seg)∫) accumulated. ``N`` slices per segment: geometric with ``k_ratio``, else equal.
+    ``target`` on the RK4 nodes of the whole horizon, (S+1, n); S a multiple of the segment count.
+    With equal slices the result equals the plain hybrid loop on (M+1)·N slices up to the
+    exp-action truncation (the same frozen operators and carries)."""
+    from .hybrid import TimeLaw, make_hybrid_plan
+    from .tracking import get_tracking_engine, solve_hybrid_tracking, _offsets_for
+    if rk is None:
+        raise ConfigError("rk: an RK4Config(dt) is required (fixed-step RK4)")
+    if system.is_linear:
+        raise ConfigError("run_checkpointed_tracking: the Burgers testbed (hybrid algorithm)")
+    if abs(sched.T - system.spec.T) > 1e-12 * system.spec.T:
+        raise ValueError("schedule horizon differs from the system's T")
+    law = law or TimeLaw.constant()
+    n = system.n
+    f = np.asarray(f, dtype=np.float64).reshape(n)
+    target = np.asarray(target, dtype=np.float64)
+    M1 = sched.segment_count
+    S = target.shape[0] - 1
+    if target.shape != (S + 1, n) or S % M1:
+        raise ValueError(f"target: (S+1, n) on the RK4 nodes with S a multiple of the {M1} segments")
+    if abs(system.spec.T / S - rk.dt) > 1e-12 * rk.dt:
+        raise ConfigError("rk.dt must be the node spacing T/S of the target")
+    S_seg = S // M1
+    T_seg = sched.T / M1
+    seg = segment_system(system, T_seg)
+    plan = make_hybrid_plan(T_seg, N, k_ratio) if k_ratio is not None else None
+    u0 = np.zeros(n) if u0 is None else np.asarray(u0, dtype=np.float64).reshape(n)
+    memory = MemoryCounter()
+    offs, _ = _offsets_for(seg, plan, N, rk)
+    # ---- phase 1: rough sweep, checkpoint states only ----------------------
+    states = [u0.copy()]
+    zeros = np.zeros((S_seg + 1, n))
+    for m in range(M1 - 1):
+        eng = get_tracking_engine(seg, offs, law.shifted(m * T_seg), 1, False)
+        eng.set_inputs(states[-1], f, zeros)
+        eng.direct(overlap=False)
+        states.append(eng.get(NV.PX_HFIELD_UT, (1, n))[0])
+    # ---- phase 2: backward sweep with recompute ----------------------------
+    grad = np.zeros(n)
+    cost = 0.0
+    qdag = None
+    uT = None
+    adj_states = []
+    share = T_seg / sched.T
+    for m in range(M1 - 1, -1, -1):
+        memory.acquire(S_seg + 1)
+        r = solve_hybrid_tracking(seg, states[m], f, target[m * S_seg:(m + 1) * S_seg + 1], plan, N, rk, expaction,
+                                  law.shifted(m * T_seg), qdag, overlap)
+        if uT is None:
+            uT = r.final_state[0]
+        cost += float(r.J[0]) * share
+        grad += r.grad[0] * share
+        qdag = r.qdag0[0]
+        adj_states.append(qdag.copy())
+        memory.release(S_seg + 1)
+    return CheckpointTrackingRun(gradient=grad, qdag0=qdag, cost=cost, final_state=uT,
+                                 segment_bounds=sched.segment_bounds, checkpoint_states=states,
+                                 adjoint_checkpoint_states=adj_states[::-1], memory=memory)

@@ -66,6 +66,12 @@ class TimeLaw:
     def __call__(self, t):
         return self.alpha + self.beta * np.sin(self.omega * t) + self.gamma * np.cos(self.omega * t)
 
+    def shifted(self, t0: float) -> "TimeLaw":
+        """The law in local time τ = t − t0: θ(t0 + τ) as α + β′ sin ωτ + γ′ cos ωτ (a segment of a
+        checkpointed run, the reference's `_shifted_system`, `checkpointing.py:94-101`)."""
+        c, s = math.cos(self.omega * t0), math.sin(self.omega * t0)
+        return TimeLaw(self.alpha, self.beta * c - self.gamma * s, self.beta * s + self.gamma * c, self.omega)
+
 
 def partition_geometric(T: float, N: int, k: float) -> TimePartition:
     """Boundaries T_n = T·(1 − rⁿ)/(1 − r^N), r = k/(k+1) (`hybrid.py:35-55`): later slices

@@ -10,8 +10,8 @@ f·sin(ωt), and ``results.csv`` / ``summary.json`` (and ``descent.csv``) are wr
 
 The reference's adaptive tolerances (``rtol``, ``leja_tol``) have no fixed-step counterpart: the
 RK4 step is ``dt`` (default: min(T/200, 1/λ) with λ the diffusion part's spectral radius) and the
-exponential actions are planned to 1e-12. ``checkpoints`` and the Gantt / PNG outputs are not
-part of this path. Field shapes: "sin_product", "ones", "zeros" or a flat list."""
+exponential actions are planned to 1e-12. ``checkpoints`` run with the hybrid algorithm
+(`checkpointing.run_checkpointed_tracking`); the Gantt / PNG outputs are not part of this path. Field shapes: "sin_product", "ones", "zeros" or a flat list."""
 
 from __future__ import annotations
 
@@ -158,8 +158,8 @@ def run_file(rf: RunFile, output: str | None = None, dt: float | None = None, re
     from .partition import RK4Config
     from .systems import build_burgers2d_system, build_field_system
     from .tracking import synthesize_trajectory
-    if rf.checkpoints:
-        raise ConfigError("checkpoints: run files run without checkpointing here (run_checkpointed_loop takes BASELINE configs)")
+    if rf.checkpoints and rf.algorithm != "hybrid":
+        raise ConfigError("checkpoints: checkpointed run files run the hybrid algorithm here (run_checkpointed_tracking)")
     if rf.algorithm in ("hybrid", "nonlinear") and rf.kind != BURGERS:
         raise ConfigError(f"algorithm: the {rf.algorithm} algorithm is for the Burgers testbed")
     out = output or rf.output
@@ -185,6 +185,20 @@ def run_file(rf: RunFile, output: str | None = None, dt: float | None = None, re
             return N * max(1, int(np.ceil(rf.T / (N * dt0) - 1e-9)))
         return max(1, int(np.ceil(rf.T / dt0 - 1e-9)))
 
+    def timed_checkpointed(N, k):
+        """`checkpoints` > 0 (`cli.py:155-162`): the hybrid loop segment by segment."""
+        from .checkpointing import CheckpointSchedule, run_checkpointed_tracking
+        M1 = rf.checkpoints + 1
+        S = M1 * max(1, int(np.ceil(rf.T / (M1 * dt0) - 1e-9)))
+        kw = dict(N=N, rk=RK4Config(rf.T / S), expaction=cfg, law=law, k_ratio=k)
+        sched = CheckpointSchedule(rf.T, rf.checkpoints)
+        tgt = target_for(S)
+        run = run_checkpointed_tracking(system, rf.f_init, tgt, sched, **kw)
+        tick = time.perf_counter()
+        for _ in range(reps):
+            run = run_checkpointed_tracking(system, rf.f_init, tgt, sched, **kw)
+        return (time.perf_counter() - tick) / reps, run
+
     def timed(algorithm, N, plan=None):
         S = steps_for(N)
         kw = dict(N=N, rk=RK4Config(rf.T / S), expaction=cfg, objective="tracking", time_law=law)
@@ -206,6 +220,11 @@ def run_file(rf: RunFile, output: str | None = None, dt: float | None = None, re
     rows = []
     last = None
     for N in rf.workers:
+        if rf.checkpoints:
+            t_par, run = timed_checkpointed(N, k)
+            rows.append([rf.algorithm, N, rf.D, reps, 1, f"{t_serial:.6f}", f"{t_par:.6f}", f"{t_serial / t_par:.6f}",
+                         f"{run.cost:.12e}", f"{np.linalg.norm(run.gradient):.12e}"])
+            continue
         plan = make_hybrid_plan(rf.T, N, k) if rf.algorithm == "hybrid" else None
         t_par, loop, kw, tgt = timed(rf.algorithm, N, plan)
         last = (N, kw, tgt)
@@ -216,11 +235,11 @@ def run_file(rf: RunFile, output: str | None = None, dt: float | None = None, re
         w = csv.writer(fh)
         w.writerow(["algorithm", "N", "D", "repeats", "K", "t_serial_s", "t_parallel_s", "s_measured", "J", "grad_norm"])
         w.writerows(rows)
-    summary = {"algorithm": rf.algorithm, "workers": list(rf.workers), "checkpoints": 0, "D": rf.D, "T": rf.T,
+    summary = {"algorithm": rf.algorithm, "workers": list(rf.workers), "checkpoints": rf.checkpoints, "D": rf.D, "T": rf.T,
                "grid": [rf.nx, rf.ny], "backend": "cuda", "dt": rf.T / steps_for(1), "k": k,
                "t_serial_s": t_serial, "J_serial": float(serial.J),
                "J": {str(r[1]): float(r[8]) for r in rows}}
-    if rf.descent_steps > 0:
+    if rf.descent_steps > 0 and last is not None:
         N, kw, tgt = last
         res = descend(system, rf.f_init, tgt, rf.descent_steps, rf.descent_lr, algorithm=rf.algorithm, **kw)
         with open(os.path.join(out, "descent.csv"), "w", newline="") as fh:

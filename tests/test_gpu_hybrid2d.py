@@ -294,3 +294,38 @@ def test_nonlinear2d_per_stage_launches_vs_oracle(cuda_ok, per_stage_launches, g
     assert np.max(np.abs(r.J - o.J) / np.abs(o.J)) <= 1e-10
     assert rel_l2(r.final_state, o.uT) <= 1e-10
     assert rel_l2(r.grad, o.grad) <= 1e-8 and rel_l2(r.qdag0, o.qdag0) <= 1e-10
+
+
+@pytest.mark.parametrize("two_d", [False, True])
+def test_checkpointed_hybrid_tracking_equals_the_plain_loop(cuda_ok, two_d):
+    """`run_checkpointed_tracking` (the reference's checkpointed loop, hybrid algorithm): M = 0 is the
+    plain loop; M = 1 with N equal slices per segment equals the plain hybrid loop on 2N equal slices
+    (same serial sweep from the checkpoint, same frozen operators and carries; the terminal data of the
+    first segment is the second's q†) up to the exp-action truncation; memory peaks at one segment."""
+    from paper_2004_00546_b200 import (
+        CheckpointSchedule, ChebyshevConfig, Grid, ProblemSpec, RK4Config, TimeLaw, build_burgers2d_system,
+        build_system, run_checkpointed_tracking, solve_hybrid_tracking, synthesize_trajectory)
+    from paper_2004_00546_b200.problems import BURGERS
+    T, D, S, N = 0.4, 0.02, 400, 3
+    law, rk, cfg = TimeLaw(0.2, 0.8, -0.3, 4.0), RK4Config(T / S), ChebyshevConfig(tol=1e-13)
+    spec = ProblemSpec(BURGERS, (0.0, 0.0), D, T)
+    if two_d:
+        sysm = build_burgers2d_system(Grid(20, 18), spec)
+        X, Y = sysm.grid.coordinates()
+        f = np.concatenate([0.3 * np.cos(X) * np.sin(Y), 0.2 * np.sin(X + Y)])
+        ft = np.concatenate([0.5 * np.sin(X) * np.sin(Y), 0.1 * np.cos(Y)])
+        u0 = np.concatenate([0.2 * np.sin(X), 0.1 * np.cos(X - Y)])
+    else:
+        sysm = build_system(Grid(128), spec, 2)
+        x = sysm.grid.x1()
+        f, ft, u0 = 0.3 * np.cos(2 * x) + 0.2 * np.sin(x), 0.4 * np.sin(x) + 0.1 * np.cos(3 * x), 0.5 * np.sin(x)
+    target = synthesize_trajectory(sysm, ft, rk, law, u0=u0)[:, 0, :]
+    plain = solve_hybrid_tracking(sysm, u0, f, target, None, N=2 * N, rk=rk, expaction=cfg, law=law)
+    c0 = run_checkpointed_tracking(sysm, f, target, CheckpointSchedule(T, 0), N=2 * N, rk=rk, expaction=cfg, law=law, u0=u0)
+    assert c0.cost == pytest.approx(float(plain.J[0]), rel=1e-13) and rel_l2(c0.gradient, plain.grad[0]) <= 1e-13
+    c1 = run_checkpointed_tracking(sysm, f, target, CheckpointSchedule(T, 1), N=N, rk=rk, expaction=cfg, law=law, u0=u0)
+    assert c1.cost == pytest.approx(float(plain.J[0]), rel=1e-12)
+    assert rel_l2(c1.final_state, plain.final_state[0]) <= 1e-13
+    assert rel_l2(c1.gradient, plain.grad[0]) <= 1e-9 and rel_l2(c1.qdag0, plain.qdag0[0]) <= 1e-9
+    assert c1.memory.peak == S // 2 + 1 and len(c1.checkpoint_states) == 2
+    assert rel_l2(c1.checkpoint_states[1], target[0] * 0 + synthesize_trajectory(sysm, f, rk, law, u0=u0)[S // 2, 0]) <= 1e-13

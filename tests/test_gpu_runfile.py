@@ -86,3 +86,18 @@ def test_numbered_baseline_configs_through_the_cli(cuda_ok, tmp_path, capsys):
     pred = json.loads(capsys.readouterr().out)
     assert [p["gpus"] for p in pred["prediction"]] == [1, 2]
     assert main(["run", "--config", "9"]) == 1   # unknown config number
+
+
+def test_checkpointed_hybrid_run_file(cuda_ok, tmp_path):
+    """`checkpoints` in a run file (`cli.py:155-162`): the hybrid loop segment by segment; the direct
+    sweep, hence J, is the serial one whatever the segmentation."""
+    from paper_2004_00546_b200.__main__ import main
+    doc = {"problem": {"kind": "burgers", "nx": 16, "ny": 16, "D": 0.5, "omega": 2.0, "T": 0.5,
+                       "f_true": "sin_product", "f_init": "ones"},
+           "algorithm": "hybrid", "workers": [2, 4], "checkpoints": 1, "repeats": 1}
+    out = tmp_path / "ck"
+    assert main(["run", "--config", _write(tmp_path, doc), "--output", str(out), "--dt", "2.5e-3"]) == 0
+    rows = list(csv.DictReader(open(out / "results.csv")))
+    summary = json.load(open(out / "summary.json"))
+    assert summary["checkpoints"] == 1 and [int(r["N"]) for r in rows] == [2, 4]
+    assert all(abs(float(r["J"]) - summary["J_serial"]) <= 1e-11 * abs(summary["J_serial"]) for r in rows)

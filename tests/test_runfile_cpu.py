@@ -60,4 +60,4 @@ def test_unsupported_parts_are_refused_before_any_gpu_work():
     with pytest.raises(ConfigError, match="Burgers"):
         run_file(parse_run_file(lin))
     with pytest.raises(ConfigError, match="checkpoints"):
-        run_file(parse_run_file(_doc(checkpoints=2)))
+        run_file(parse_run_file(_doc(checkpoints=2, algorithm="nonlinear")))
