@@ -329,3 +329,18 @@ def test_checkpointed_hybrid_tracking_equals_the_plain_loop(cuda_ok, two_d):
     assert rel_l2(c1.gradient, plain.grad[0]) <= 1e-9 and rel_l2(c1.qdag0, plain.qdag0[0]) <= 1e-9
     assert c1.memory.peak == S // 2 + 1 and len(c1.checkpoint_states) == 2
     assert rel_l2(c1.checkpoint_states[1], target[0] * 0 + synthesize_trajectory(sysm, f, rk, law, u0=u0)[S // 2, 0]) <= 1e-13
+
+
+def test_serial2d_gradient_vs_finite_differences_on_the_device(cuda_ok):
+    """Independent of the oracle: the serial (one-slice) loop's ∂L/∂f on the 2D testbed against central
+    differences of the device's own J in a random direction of both components (second order in h)."""
+    from paper_2004_00546_b200 import direct_adjoint_loop, synthesize_trajectory
+    sysm, u0, f, f_true, rk, cfg, law = _case(nx=32, ny=32, T=0.3, dt=1e-3, B=1)
+    target = synthesize_trajectory(sysm, f_true, rk, law, u0=u0)[:, 0, :]
+    run = lambda ff: direct_adjoint_loop(sysm, ff, target, "serial", rk=rk, expaction=cfg, u0=u0, objective="tracking",
+                                         time_law=law)
+    r = run(f[0])
+    d = np.random.default_rng(11).standard_normal(sysm.n)
+    eps = 1e-5
+    fd = (run(f[0] + eps * d).J - run(f[0] - eps * d).J) / (2 * eps)
+    assert abs(fd - float(r.grad @ d)) <= 2e-4 * abs(fd)
