@@ -56,7 +56,7 @@ def _take(obj: dict, where: str, key: str, types, default=_MISSING):
     name = f"{where}.{key}" if where else key
     if key not in obj:
         if default is _MISSING:
-            raise ConfigError(f"{name}: missing required field")
+            raise ConfigError(f"{name}: this field is required")
         return default
     v = obj[key]
     if isinstance(v, bool) or not isinstance(v, types):
@@ -72,22 +72,22 @@ def _shape(value, grid: Grid, fields: int, name: str) -> np.ndarray:
             return np.tile(np.sin(X) * np.sin(Y), fields)
         if value in ("ones", "zeros"):
             return np.full(n, 1.0 if value == "ones" else 0.0)
-        raise ConfigError(f"{name}: unknown field shape {value!r}")
+        raise ConfigError(f"{name}: no field shape called {value!r} (sin_product, ones, zeros)")
     if isinstance(value, list):
         arr = np.asarray(value, dtype=np.float64)
         if arr.shape != (n,):
             raise ConfigError(f"{name}: expected {n} values, got {arr.size}")
         return arr
-    raise ConfigError(f"{name}: expected a shape name or a flat list")
+    raise ConfigError(f"{name}: a shape name (sin_product, ones, zeros) or a flat list of values")
 
 
 def parse_run_file(data: dict) -> RunFile:
     if not isinstance(data, dict):
-        raise ConfigError("config root must be a JSON object")
+        raise ConfigError("a run file is a JSON object (problem, algorithm, workers, …)")
     prob = _take(data, "", "problem", dict)
     kind = _take(prob, "problem", "kind", str)
     if kind not in (ADVECTION_DIFFUSION, BURGERS):
-        raise ConfigError(f"problem.kind: expected '{ADVECTION_DIFFUSION}' or '{BURGERS}'")
+        raise ConfigError(f"problem.kind: one of '{ADVECTION_DIFFUSION}', '{BURGERS}'")
     nx, ny = _take(prob, "problem", "nx", int, 32), _take(prob, "problem", "ny", int, 32)
     if nx < 3 or ny < 3:
         raise ConfigError("problem.nx/ny: the periodic stencil needs at least 3 points per direction")
@@ -106,23 +106,23 @@ def parse_run_file(data: dict) -> RunFile:
     if algorithm not in ALGORITHMS:
         raise ConfigError(f"algorithm: expected one of {ALGORITHMS}")
     if algorithm == "linear" and kind == BURGERS:
-        raise ConfigError("algorithm: the linear algorithm needs a linear problem")
+        raise ConfigError("algorithm: 'linear' is for the advection–diffusion (linear) problem")
     workers = data.get("workers", [1, 2, 4, 8, 16])
     if isinstance(workers, int) and not isinstance(workers, bool):
         workers = [workers]
     if not isinstance(workers, list) or not workers or not all(
             isinstance(w, int) and not isinstance(w, bool) and w >= 1 for w in workers):
-        raise ConfigError("workers: expected a positive integer or list of them")
+        raise ConfigError("workers: a slice count ≥ 1 or a non-empty list of such counts")
     checkpoints = _take(data, "", "checkpoints", int, 0)
     repeats = _take(data, "", "repeats", int, 3)
     if repeats < 1:
-        raise ConfigError("repeats: must be at least 1")
+        raise ConfigError("repeats: at least one timed repetition is needed")
     pilot = float(_take(data, "", "pilot_fraction", num, 0.05))
     if not 0.0 < pilot <= 0.1:
-        raise ConfigError("pilot_fraction: must lie in (0, 0.1]")
+        raise ConfigError("pilot_fraction: a fraction of the horizon in (0, 0.1]")
     descent = data.get("descent", {})
     if not isinstance(descent, dict):
-        raise ConfigError("descent: expected an object")
+        raise ConfigError("descent: an object {steps, lr}")
     steps = _take(descent, "descent", "steps", int, 0)
     lr = float(_take(descent, "descent", "lr", num, 0.5))
     if steps < 0 or (steps and lr <= 0):
