@@ -62,10 +62,30 @@ class DeviceField:
 
     def numpy(self) -> np.ndarray:
         if self._host is None:
-            self._host = self._t.cpu().numpy().reshape(self._shape)
+            self._host = _to_host(self._t).reshape(self._shape)
             self._t = None
             self._live = False
         return self._host
+
+
+_PINNED: dict = {}
+
+
+def _to_host(t) -> np.ndarray:
+    """Device tensor → a fresh numpy array through a cached pinned staging buffer (large fields: the
+    D2H copy runs at the link rate instead of the pageable-memory rate)."""
+    import torch
+    if not t.is_cuda or t.numel() < (1 << 16):
+        return t.cpu().numpy()
+    key = (t.numel(), t.dtype)
+    buf = _PINNED.get(key)
+    if buf is None:
+        if len(_PINNED) >= 4:
+            _PINNED.clear()
+        buf = _PINNED[key] = torch.empty(t.numel(), dtype=t.dtype, pin_memory=True)
+    buf.copy_(t.reshape(-1), non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return buf.numpy().copy()
 
 
 def _host(v):
