@@ -76,7 +76,7 @@ int px_create(const px_problem_desc* desc, void** out_handle) {
   if (d.p_begin < 0 || d.p_end > d.P || d.p_begin >= d.p_end) return fail(nullptr, PX_ERR_ARG, "bad slice block");
   if (!(d.T > 0)) return fail(nullptr, PX_ERR_ARG, "T must be positive");
   if (d.kind != PX_KIND_ADVDIFF && d.kind != PX_KIND_BURGERS) return fail(nullptr, PX_ERR_ARG, "bad kind");
-  if (d.kind == PX_KIND_BURGERS && d.ny != 1) return fail(nullptr, PX_ERR_ARG, "Burgers path is 1D");
+  if (d.kind == PX_KIND_BURGERS && d.ny != 1) return fail(nullptr, PX_ERR_ARG, "px_create: Burgers is 1D on this handle (terminal objective); the two-field 2D testbed runs through px_hybrid_* (desc.ny > 1: solve_hybrid_tracking / solve_nonlinear_tracking)");
   if (d.expaction == PX_EXP_KRYLOV && (d.krylov_m < 2 || d.krylov_m > px::KRYLOV_MAX_M))
     return fail(nullptr, PX_ERR_ARG, "krylov_m out of range");
   if (d.basis_rows_x < 1 || d.basis_rows_x > 64 || d.basis_rows_y < 1)
