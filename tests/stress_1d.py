@@ -16,14 +16,13 @@ def rel(a, b):
     return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
 
 
-def main():
+def run(count: int, seed: int) -> dict:
     from oracle.config_mode import burgers_gradient
     from paper_2004_00546_b200 import RK4Config, baseline, direct_adjoint_loop, release_engines, scaled
     from paper_2004_00546_b200.expaction import plan_chebyshev
     from paper_2004_00546_b200.problems import burgers_frozen_region
     from tests.test_gpu_parity import _gpu_linear, _oracle_linear
-    count = int(sys.argv[1]) if len(sys.argv) > 1 else 12
-    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 5)
+    rng = np.random.default_rng(seed)
     worst = {}
     for case in range(count):
         burgers = rng.random() < 0.45
@@ -56,9 +55,10 @@ def main():
               " ".join(f"{k}={v:.1e}" for k, v in e.items()) + ("" if ok else "  <-- FAIL"), flush=True)
         release_engines()
         if not ok:
-            sys.exit(1)
+            raise AssertionError(f"case {case} exceeds the parity bounds: {e}")
     print("worst", worst)
+    return worst
 
 
 if __name__ == "__main__":
-    main()
+    run(int(sys.argv[1]) if len(sys.argv) > 1 else 12, int(sys.argv[2]) if len(sys.argv) > 2 else 7)

@@ -15,7 +15,7 @@ def rel(a, b):
     return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
 
 
-def main():
+def run(count: int, seed: int) -> dict:
     from paper_2004_00546_b200 import (
         ChebyshevConfig, Grid, ProblemSpec, RK4Config, TimeLaw, build_system, make_hybrid_plan,
         solve_hybrid_tracking, synthesize_trajectory)
@@ -23,8 +23,7 @@ def main():
     from paper_2004_00546_b200.problems import BURGERS
     from paper_2004_00546_b200.tracking import release_tracking_engines
     from tests.test_gpu_hybrid import _oracle
-    count = int(sys.argv[1]) if len(sys.argv) > 1 else 12
-    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 9)
+    rng = np.random.default_rng(seed)
     worst = {}
     for case in range(count):
         nx = int(rng.choice([48, 64, 96, 128, 192, 256, 320, 512, 1024, 2048, 4096]))
@@ -63,9 +62,10 @@ def main():
               f"/{r.timing['overlapped']}: " + " ".join(f"{k}={v:.1e}" for k, v in e.items()) + ("" if ok else "  <-- FAIL"), flush=True)
         release_tracking_engines()
         if not ok:
-            sys.exit(1)
+            raise AssertionError(f"case {case} exceeds the parity bounds: {e}")
     print("worst", worst)
+    return worst
 
 
 if __name__ == "__main__":
-    main()
+    run(int(sys.argv[1]) if len(sys.argv) > 1 else 12, int(sys.argv[2]) if len(sys.argv) > 2 else 7)

@@ -15,7 +15,7 @@ def rel(a, b):
     return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
 
 
-def main():
+def run(count: int, seed: int) -> dict:
     from oracle.config_mode import burgers2d_nonlinear_tracking, burgers_tracking_hybrid
     from paper_2004_00546_b200 import (
         ChebyshevConfig, Grid, ProblemSpec, RK4Config, TimeLaw, build_burgers2d_system, make_hybrid_plan,
@@ -23,8 +23,7 @@ def main():
     from paper_2004_00546_b200.expaction import plan_chebyshev, plan_family
     from paper_2004_00546_b200.problems import BURGERS, frozen_bounds_2d, frozen_region_from_bounds
     from paper_2004_00546_b200.tracking import release_tracking_engines
-    count = int(sys.argv[1]) if len(sys.argv) > 1 else 12
-    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 7)
+    rng = np.random.default_rng(seed)
     worst = {"J": 0.0, "grad": 0.0, "qdag0": 0.0, "uT": 0.0}
     for case in range(count):
         big = rng.random() < 0.3
@@ -70,9 +69,10 @@ def main():
               ("" if ok else "  <-- FAIL"), flush=True)
         release_tracking_engines()
         if not ok:
-            sys.exit(1)
+            raise AssertionError(f"case {case} exceeds the parity bounds: {e}")
     print("worst", worst)
+    return worst
 
 
 if __name__ == "__main__":
-    main()
+    run(int(sys.argv[1]) if len(sys.argv) > 1 else 12, int(sys.argv[2]) if len(sys.argv) > 2 else 7)

@@ -17,12 +17,11 @@ def rel(a, b):
     return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
 
 
-def main():
+def run(count: int, seed: int) -> dict:
     from paper_2004_00546_b200 import Grid, RK4Config, baseline, release_engines, scaled
     from paper_2004_00546_b200.optimization import get_engine
     from tests.test_gpu_parity import _gpu_linear, _oracle_linear
-    count = int(sys.argv[1]) if len(sys.argv) > 1 else 12
-    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 11)
+    rng = np.random.default_rng(seed)
     worst = {}
     for case in range(count):
         krylov = rng.random() < 0.25
@@ -52,9 +51,10 @@ def main():
               " ".join(f"{k}={v:.1e}" for k, v in e.items()) + ("" if ok else "  <-- FAIL"), flush=True)
         release_engines()
         if not ok:
-            sys.exit(1)
+            raise AssertionError(f"case {case} exceeds the parity bounds: {e}")
     print("worst", worst)
+    return worst
 
 
 if __name__ == "__main__":
-    main()
+    run(int(sys.argv[1]) if len(sys.argv) > 1 else 12, int(sys.argv[2]) if len(sys.argv) > 2 else 7)

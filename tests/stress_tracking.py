@@ -17,13 +17,12 @@ def rel(a, b):
     return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
 
 
-def main():
+def run(count: int, seed: int) -> dict:
     from paper_2004_00546_b200 import (
         ChebyshevConfig, Grid, RK4Config, TimeLaw, baseline, direct_adjoint_loop, release_engines, scaled)
     from paper_2004_00546_b200.systems import build_field_system
     from tests.test_gpu_tracking import _oracle, _target
-    count = int(sys.argv[1]) if len(sys.argv) > 1 else 12
-    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 3)
+    rng = np.random.default_rng(seed)
     worst = {}
     for case in range(count):
         two_d = rng.random() < 0.6
@@ -63,9 +62,10 @@ def main():
               f"own_target={own}: " + " ".join(f"{k}={v:.1e}" for k, v in e.items()) + ("" if ok else "  <-- FAIL"), flush=True)
         release_engines()
         if not ok:
-            sys.exit(1)
+            raise AssertionError(f"case {case} exceeds the parity bounds: {e}")
     print("worst", worst)
+    return worst
 
 
 if __name__ == "__main__":
-    main()
+    run(int(sys.argv[1]) if len(sys.argv) > 1 else 12, int(sys.argv[2]) if len(sys.argv) > 2 else 7)
